@@ -1,0 +1,130 @@
+/* cgmimo_b200.h -- C ABI of the B200 (sm_100a) CG detection / precoding path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and int status codes,
+ * no CUDA or C++ types in any signature.  Each entry point replaces a
+ * reference interface of /root/reference/proj (cited per function); the C++
+ * drop-in headers in include/cgmimo/ (same signatures as the reference's
+ * cgmimo::detect / cgmimo::precode) are implemented on top of it, and
+ * INTEGRATION.md shows the ctypes / C++ bindings.
+ *
+ * Layouts (complex64 = interleaved float re,im; all arrays dense, row-major):
+ *   H  uplink   [n_sc][B][U]   element (b,u) at b*U+u   (reference linalg.hpp:28)
+ *   Hd downlink [n_sc][U][B]   element (u,b) at u*B+b   (precode.hpp:31, H_d is U x B)
+ *   Y  [n_sc][S][B]            the S received vectors that share channel sc
+ *   T  [n_sc][S][U]            the S transmit-symbol vectors t of channel sc
+ *   xhat [n_sc][S][U] complex64, mu / rho [n_sc][S][U] float,
+ *   llr  [n_sc][S][U][qam_bits] float (I-axis bits MSB first, then Q-axis bits),
+ *   q / s [n_sc][S][B] complex64, gain [n_sc][S] float,
+ *   status [n_sc][S] uint8: bit0 = solver breakdown (outputs zeroed; the
+ *   reference throws solvers::SolverBreakdown, solvers.cpp:55-57),
+ *   bit1 = zero_input (precode, precode.cpp:25-31).
+ * Any output pointer may be NULL to skip that output.
+ *
+ * Memory spaces: without CGM_DEVICE_POINTERS every array is a HOST pointer
+ * and the call is synchronous (host->device copies, kernels and device->host
+ * copies are pipelined in chunks inside the call).  With CGM_DEVICE_POINTERS
+ * every array is a device pointer on the context's device and the call only
+ * enqueues work on the context stream (cgm_ctx_set_stream).
+ *
+ * Numerics: complex64 / FP32 arithmetic (the reference is FP64); see
+ * DESIGN.md for the tolerance contract.  The reference's 1e-9
+ * imaginary-part check on p^H A p (solvers.cpp:29-35) is not applied: A is
+ * Hermitian by construction.
+ */
+#ifndef CGMIMO_B200_H
+#define CGMIMO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define CGM_OK 0
+#define CGM_EINVAL 1     /* std::invalid_argument in the reference (detect.cpp:186-188) */
+#define CGM_EBREAKDOWN 2 /* solvers::SolverBreakdown (solvers.cpp:55-57), per-call API only */
+#define CGM_ECUDA 3
+#define CGM_ENCCL 4
+#define CGM_ENOMEM 5
+
+/* SinrTracker (detect.hpp:38): same enumerator order as the reference */
+#define CGM_TRACKER_EXACT 0
+#define CGM_TRACKER_APPROX 1
+
+/* flags */
+#define CGM_DEVICE_POINTERS 0x1u  /* arrays are device pointers; asynchronous */
+#define CGM_HD_UPLINK_LAYOUT 0x2u /* precode: matrix given as H_u [B][U], H_d = H_u^H */
+
+typedef struct cgm_ctx cgm_ctx;
+
+/* One context per host thread (or stream): owns the stream, device
+ * workspaces and the last-error string.  device = CUDA ordinal. */
+int cgm_ctx_create(int device, cgm_ctx** out);
+int cgm_ctx_destroy(cgm_ctx* ctx);
+/* stream = cudaStream_t (0 = legacy default stream) */
+int cgm_ctx_set_stream(cgm_ctx* ctx, void* stream);
+int cgm_synchronize(cgm_ctx* ctx);
+const char* cgm_last_error(const cgm_ctx* ctx);
+/* kernels this context has launched since creation (the bench's gpu_launches) */
+long cgm_kernel_launches(const cgm_ctx* ctx);
+/* library version string, e.g. "cgmimo_b200 0.1 sm_100a" */
+const char* cgm_version(void);
+
+/* Batched detect::detect_cg (detect.hpp:58-61, detect.cpp:182-237):
+ * Gram + matched filter, K CG iterations with the exact (Eq. 10) or
+ * approximate (Eq. 11) SINR tracker, max-log LLRs (detect.cpp:68-86).
+ * rho_u is the regulariser argument (A = H^H H + rho_u^-1 I), n0 / es the
+ * noise and symbol energies; qam_bits in {2, 4, 6}. 1 <= U <= 64, K <= 16. */
+int cgm_detect_cg(cgm_ctx* ctx, int B, int U, long n_sc, int S, const float* H,
+                  const float* Y, double rho_u, double n0, double es, int qam_bits, int K,
+                  int tracker, float* xhat, float* mu, float* rho, float* llr,
+                  uint8_t* status, unsigned flags);
+
+/* Batched precode::precode_cg (precode.hpp:31-33, precode.cpp:56-71):
+ * A_d = H_d H_d^H + rho_d^-1 I, K CG iterations on t, q = H_d^H v_K,
+ * gain = ||q||, s = q / gain (precode.cpp:22-36). */
+int cgm_precode_cg(cgm_ctx* ctx, int B, int U, long n_sc, int S, const float* Hd,
+                   const float* T, double rho_d, int K, float* q, float* s, float* gain,
+                   uint8_t* status, unsigned flags);
+
+/* Uplink detection and downlink precoding on the SAME channels (TDD
+ * reciprocity, H_d = H_u^H) in one pass: the Gram matrix is formed once per
+ * subcarrier and shared by the S uplink and St downlink systems.  Equivalent
+ * to cgm_detect_cg(...) followed by cgm_precode_cg(..., CGM_HD_UPLINK_LAYOUT). */
+int cgm_detect_precode_cg(cgm_ctx* ctx, int B, int U, long n_sc, int S, const float* H,
+                          const float* Y, double rho_u, double n0, double es, int qam_bits,
+                          int K, int tracker, float* xhat, float* mu, float* rho, float* llr,
+                          uint8_t* status, int St, const float* T, double rho_d, int Kt,
+                          float* q, float* s, float* gain, uint8_t* pstatus, unsigned flags);
+
+/* Seeded synthetic inputs on the device (always device pointers, async),
+ * following the reference's stream conventions (sim.cpp:151-179,
+ * channel.cpp:10-30, rng.cpp): with root = Rng(seed),
+ *   H(sc)       = rayleigh_channel(B, U, root.fork(2).fork(sc))   (row-major draws)
+ *   labels(i)   : root.fork(1).fork(i), qam_bits draws of next_u64() & 1 per user
+ *   noise(i)    : root.fork(3).fork(i), transmit() component std sqrt(N0/2)
+ *   t labels(i) : root.fork(4).fork(i)
+ * with instance index i = sc*S + s, so results do not depend on sharding.
+ * sc0 offsets the subcarrier index (shard start).  labels may be NULL. */
+int cgm_generate_uplink(cgm_ctx* ctx, int B, int U, long sc0, long n_sc, int S, uint64_t seed,
+                        int qam_bits, double n0, float* H, float* Y, uint8_t* labels);
+/* Downlink: Hd(sc) = U x B rayleigh draws from root.fork(2).fork(sc); T from
+ * labels root.fork(4).fork(i). */
+int cgm_generate_downlink(cgm_ctx* ctx, int B, int U, long sc0, long n_sc, int S,
+                          uint64_t seed, int qam_bits, float* Hd, float* T, uint8_t* labels);
+/* Downlink symbol vectors only (T [n_sc][S][U]) from root.fork(4). */
+int cgm_generate_symbols(cgm_ctx* ctx, int U, long sc0, long n_sc, int S, uint64_t seed,
+                         int qam_bits, float* T, uint8_t* labels);
+/* BS-side correlated channel: H_u = (H_w R^{1/2})^H per subcarrier where
+ * H_w (U x B) is drawn like cgm_generate_downlink's Hd and rsqrt is the
+ * B x B real symmetric square root of R (row-major float).  Then Y is drawn
+ * as in cgm_generate_uplink from the correlated channel. */
+int cgm_generate_uplink_correlated(cgm_ctx* ctx, int B, int U, long sc0, long n_sc, int S,
+                                   uint64_t seed, int qam_bits, double n0, const float* rsqrt,
+                                   float* H, float* Y, uint8_t* labels);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CGMIMO_B200_H */

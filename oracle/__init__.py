@@ -1,0 +1,204 @@
+"""oracle -- TEST INFRASTRUCTURE ONLY (the checker, never the product).
+
+Two FP64 CPU implementations of the reference hot path behind one numpy API:
+
+* ``kind="ref"``  -- the UNMODIFIED reference library (``/root/reference/proj/src``)
+  compiled by ``oracle/Makefile`` into ``oracle/_ref/libcgmimo_ref.so`` and driven
+  through ``oracle/ref_shim.cpp`` (calls ``detect::detect_cg`` detect.cpp:182,
+  ``precode::precode_cg`` precode.cpp:56, ... per instance).
+* ``kind="port"`` -- ``oracle/cg_oracle.c``, the plain-C restatement (each function
+  cites the reference file:line it follows), pinned against ``ref`` and the
+  committed fixtures in ``tests/golden/``.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+REF_LIB = os.path.join(_HERE, "_ref", "libcgmimo_ref.so")
+PORT_LIB = os.path.join(_HERE, "_build", "libcgoracle.so")
+REF_SRC = "/root/reference/proj"
+
+_dp = C.POINTER(C.c_double)
+_u8p = C.POINTER(C.c_uint8)
+_u64p = C.POINTER(C.c_uint64)
+
+
+def build(quiet: bool = True) -> None:
+    """Compile the C restatement and, when the reference tree exists, oracle/_ref."""
+    targets = ["port"]
+    if os.path.isdir(REF_SRC):
+        targets.append("ref")
+    out = subprocess.run(["make", "-C", _HERE, "-j8", *targets], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
+    if not quiet:
+        print(out.stdout)
+
+
+def available(kind: str) -> bool:
+    return os.path.exists(REF_LIB if kind == "ref" else PORT_LIB)
+
+
+def _ptr(a, t=_dp):
+    return a.ctypes.data_as(t)
+
+
+def _c128(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.complex128)
+
+
+class Oracle:
+    """numpy front-end over one of the two oracle libraries."""
+
+    def __init__(self, kind: str = "ref"):
+        if kind not in ("ref", "port"):
+            raise ValueError(kind)
+        self.kind = kind
+        path = REF_LIB if kind == "ref" else PORT_LIB
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"oracle library missing: {path} (run `make -C oracle`)")
+        self.lib = C.CDLL(path)
+        self.pfx = "ref_" if kind == "ref" else "orc_"
+        self._threaded = kind == "ref"
+
+    def _fn(self, name):
+        return getattr(self.lib, self.pfx + name)
+
+    # ------------------------------------------------------------ detection
+    def detect(self, H, Y, rho_u, n0, es, qam_bits, K=1, tracker="approx", method="cg",
+               threads=1):
+        """H: (n_sc, B, U) complex; Y: (n_sc, S, B) complex. Returns dict of arrays
+        shaped (n_sc, S, U[, bits])."""
+        H = _c128(H)
+        Y = _c128(Y)
+        n_sc, B, U = H.shape
+        S = Y.shape[1]
+        assert Y.shape == (n_sc, S, B), (Y.shape, H.shape)
+        xhat = np.zeros((n_sc, S, U), np.complex128)
+        mu = np.zeros((n_sc, S, U))
+        rho = np.zeros((n_sc, S, U))
+        llr = np.zeros((n_sc, S, U, qam_bits))
+        status = np.zeros((n_sc, S), np.uint8)
+        trk = 0 if tracker == "exact" else 1
+        common_out = (_ptr(xhat), _ptr(mu), _ptr(rho), _ptr(llr), _ptr(status, _u8p))
+        if method == "cg":
+            f = self._fn("detect_cg")
+            args = [C.c_int(B), C.c_int(U), C.c_long(n_sc), C.c_int(S), _ptr(H), _ptr(Y),
+                    C.c_double(rho_u), C.c_double(n0), C.c_double(es), C.c_int(qam_bits),
+                    C.c_int(K), C.c_int(trk), *common_out]
+        elif method in ("explicit", "cholesky"):
+            f = self._fn("detect_explicit" if method == "explicit" or self.kind == "port"
+                         else "detect_cholesky")
+            args = [C.c_int(B), C.c_int(U), C.c_long(n_sc), C.c_int(S), _ptr(H), _ptr(Y),
+                    C.c_double(rho_u), C.c_double(n0), C.c_double(es), C.c_int(qam_bits),
+                    *common_out]
+        else:
+            raise ValueError(method)
+        if self._threaded:
+            args.append(C.c_int(threads))
+        rc = f(*args)
+        if rc != 0:
+            raise ValueError(f"oracle detect rejected arguments (rc={rc})")
+        return dict(xhat=xhat, mu=mu, rho=rho, llr=llr, status=status)
+
+    # ------------------------------------------------------------ precoding
+    def precode(self, Hd, T, rho_d, K=1, method="cg", threads=1):
+        """Hd: (n_sc, U, B) complex; T: (n_sc, S, U) complex."""
+        Hd = _c128(Hd)
+        T = _c128(T)
+        n_sc, U, B = Hd.shape
+        S = T.shape[1]
+        assert T.shape == (n_sc, S, U)
+        q = np.zeros((n_sc, S, B), np.complex128)
+        s = np.zeros((n_sc, S, B), np.complex128)
+        gain = np.zeros((n_sc, S))
+        status = np.zeros((n_sc, S), np.uint8)
+        outs = (_ptr(q), _ptr(s), _ptr(gain), _ptr(status, _u8p))
+        if method == "cg":
+            args = [C.c_int(B), C.c_int(U), C.c_long(n_sc), C.c_int(S), _ptr(Hd), _ptr(T),
+                    C.c_double(rho_d), C.c_int(K), *outs]
+            f = self._fn("precode_cg")
+        elif method == "explicit":
+            args = [C.c_int(B), C.c_int(U), C.c_long(n_sc), C.c_int(S), _ptr(Hd), _ptr(T),
+                    C.c_double(rho_d), *outs]
+            f = self._fn("precode_explicit")
+        else:
+            raise ValueError(method)
+        if self._threaded:
+            args.append(C.c_int(threads))
+        f(*args)
+        return dict(q=q, s=s, gain=gain, status=status)
+
+    # ------------------------------------------------------------ helpers
+    def compute_llrs(self, xhat: complex, mu: float, rho: float, qam_bits: int) -> np.ndarray:
+        out = np.zeros(qam_bits)
+        rc = self._fn("compute_llrs")(C.c_double(xhat.real), C.c_double(xhat.imag),
+                                      C.c_double(mu), C.c_double(rho), C.c_int(qam_bits),
+                                      _ptr(out))
+        if rc:
+            raise ValueError("bad qam_bits")
+        return out
+
+    def constellation(self, qam_bits: int):
+        pts = np.zeros(1 << qam_bits, np.complex128)
+        half = qam_bits // 2
+        per = (1 << half) // 2
+        a0 = np.zeros((half, per))
+        a1 = np.zeros((half, per))
+        self._fn("constellation")(C.c_int(qam_bits), _ptr(pts), _ptr(a0), _ptr(a1))
+        return pts, a0, a1
+
+    def rng_u64(self, key: int, forks, n: int) -> np.ndarray:
+        fk = np.ascontiguousarray(forks, dtype=np.uint64)
+        out = np.zeros(n, np.uint64)
+        self._fn("rng_u64")(C.c_uint64(key), _ptr(fk, _u64p), C.c_int(len(fk)), C.c_long(n),
+                            _ptr(out, _u64p))
+        return out
+
+    def rng_cgaussian(self, key: int, forks, variance: float, n: int) -> np.ndarray:
+        fk = np.ascontiguousarray(forks, dtype=np.uint64)
+        out = np.zeros(n, np.complex128)
+        self._fn("rng_cgaussian")(C.c_uint64(key), _ptr(fk, _u64p), C.c_int(len(fk)),
+                                  C.c_double(variance), C.c_long(n), _ptr(out))
+        return out
+
+    def rayleigh(self, key: int, forks, B: int, U: int) -> np.ndarray:
+        fk = np.ascontiguousarray(forks, dtype=np.uint64)
+        out = np.zeros((B, U), np.complex128)
+        self._fn("rayleigh")(C.c_uint64(key), _ptr(fk, _u64p), C.c_int(len(fk)), C.c_int(B),
+                             C.c_int(U), _ptr(out))
+        return out
+
+    # reference-only probes ------------------------------------------------
+    def count_detect_stages(self, method: int, B: int, U: int, K: int) -> np.ndarray:
+        out = np.zeros(16, np.uint64)
+        n = self.lib.ref_count_detect_stages(C.c_int(method), C.c_int(B), C.c_int(U),
+                                             C.c_int(K), _ptr(out, _u64p))
+        return out[:n]
+
+    def tally_detect_cg(self, B: int, U: int, K: int, tracker: str, seed: int) -> np.ndarray:
+        out = np.zeros(16, np.uint64)
+        n = self.lib.ref_tally_detect_cg(C.c_int(B), C.c_int(U), C.c_int(K),
+                                         C.c_int(0 if tracker == "exact" else 1),
+                                         C.c_uint64(seed), _ptr(out, _u64p))
+        return out[:n]
+
+    def exact_filters(self, H, y, rho_u: float, K: int):
+        H = _c128(H)
+        y = _c128(y)
+        B, U = H.shape
+        filt = np.zeros((K, U, U), np.complex128)
+        its = np.zeros((K, U), np.complex128)
+        rc = self.lib.ref_exact_filters(C.c_int(B), C.c_int(U), _ptr(H), _ptr(y),
+                                        C.c_double(rho_u), C.c_int(K), _ptr(filt), _ptr(its))
+        if rc:
+            raise RuntimeError(f"exact_filters rc={rc}")
+        return filt, its

@@ -1,0 +1,38 @@
+/* oracle/cg_oracle.h -- TEST INFRASTRUCTURE: plain-C FP64 restatement of the
+ * reference hot path, used only by tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline leg as the CHECKER.  Never linked into the product.
+ *
+ * Same batch layout and status bits as oracle/ref_shim.cpp (see there).
+ * Pinned against oracle/_ref (the reference itself) and tests/golden/.
+ */
+#ifndef CG_ORACLE_H
+#define CG_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+int orc_constellation(int qam_bits, double* points, double* axis0, double* axis1);
+int orc_compute_llrs(double xr, double xi, double mu, double rho, int qam_bits, double* out);
+
+int orc_detect_cg(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                  double rho_u, double n0, double es, int qam_bits, int K, int tracker,
+                  double* xhat, double* mu, double* rho, double* llr, uint8_t* status);
+int orc_detect_explicit(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                        double rho_u, double n0, double es, int qam_bits, double* xhat,
+                        double* mu, double* rho, double* llr, uint8_t* status);
+int orc_precode_cg(int B, int U, long n_sc, int S, const double* Hd, const double* T,
+                   double rho_d, int K, double* q, double* s, double* gain, uint8_t* status);
+int orc_precode_explicit(int B, int U, long n_sc, int S, const double* Hd, const double* T,
+                         double rho_d, double* q, double* s, double* gain, uint8_t* status);
+
+void orc_rng_u64(uint64_t key, const uint64_t* forks, int n_forks, long n, uint64_t* out);
+void orc_rng_cgaussian(uint64_t key, const uint64_t* forks, int n_forks, double variance,
+                       long n, double* out);
+void orc_rayleigh(uint64_t key, const uint64_t* forks, int n_forks, int B, int U, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

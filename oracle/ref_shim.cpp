@@ -1,0 +1,359 @@
+// oracle/ref_shim.cpp -- TEST INFRASTRUCTURE, never part of the product path.
+//
+// A flat extern "C" surface over the UNMODIFIED reference library
+// (/root/reference/proj/src/*.cpp, compiled by oracle/Makefile into
+// oracle/_ref/libcgmimo_ref.so).  It loops the reference's own per-call API
+// over a batch so Python tests and bench.py's reference arm can drive it:
+//
+//   detect::detect_cg        (detect.hpp:58-61, detect.cpp:182-237)
+//   detect::detect_explicit  (detect.hpp:44-49, detect.cpp:94-126)
+//   precode::precode_cg      (precode.hpp:31-33, precode.cpp:56-71)
+//   precode::precode_explicit(precode.hpp:26-27, precode.cpp:45-54)
+//   detect::compute_llrs     (detect.cpp:68-86)
+//   phy::make_constellation  (constellation.cpp:37-86)
+//   phy::Rng                 (rng.cpp:12-52)
+//   opcount::count_detect_stages (opcount.cpp:69-138)
+//
+// Batch layout (shared with the CUDA path and oracle/cg_oracle.c):
+//   H  uplink   [n_sc][B][U]  element (b,u) at b*U+u   (linalg.hpp:28)
+//   Hd downlink [n_sc][U][B]  element (u,b) at u*B+b
+//   Y  [n_sc][S][B]; T [n_sc][S][U]
+//   outputs per instance (sc,s): xhat[U] mu[U] rho[U] llr[U][bits]; q[B] s[B] gain
+// Complex values are interleaved (re,im) doubles.  Status per instance:
+//   bit0 = SolverBreakdown (outputs zeroed), bit1 = zero_input (precode),
+//   bit2 = std::invalid_argument / other exception.
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "cgmimo/channel.hpp"
+#include "cgmimo/constellation.hpp"
+#include "cgmimo/detect.hpp"
+#include "cgmimo/linalg.hpp"
+#include "cgmimo/opcount.hpp"
+#include "cgmimo/precode.hpp"
+#include "cgmimo/rng.hpp"
+#include "cgmimo/solvers.hpp"
+
+using namespace cgmimo;
+
+namespace {
+
+phy::Modulation modulation_of(int bits) {
+  switch (bits) {
+    case 2: return phy::Modulation::kQpsk;
+    case 4: return phy::Modulation::kQam16;
+    case 6: return phy::Modulation::kQam64;
+  }
+  throw std::invalid_argument("qam_bits must be 2, 4 or 6");
+}
+
+template <class F>
+void parallel_for(long n, int threads, F&& body) {
+  if (threads <= 1 || n <= 1) {
+    for (long i = 0; i < n; ++i) body(i);
+    return;
+  }
+  std::atomic<long> next{0};
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&] {
+      for (long i = next.fetch_add(1); i < n; i = next.fetch_add(1)) body(i);
+    });
+  for (auto& th : pool) th.join();
+}
+
+ComplexMatrix load_matrix(const double* p, std::size_t rows, std::size_t cols) {
+  ComplexMatrix m(rows, cols);
+  for (std::size_t i = 0; i < rows; ++i)
+    for (std::size_t j = 0; j < cols; ++j) {
+      const double* e = p + 2 * (i * cols + j);
+      m(i, j) = cplx(e[0], e[1]);
+    }
+  return m;
+}
+
+ComplexVector load_vector(const double* p, std::size_t n) {
+  ComplexVector v(n);
+  for (std::size_t i = 0; i < n; ++i) v[i] = cplx(p[2 * i], p[2 * i + 1]);
+  return v;
+}
+
+void store_vector(const ComplexVector& v, double* p) {
+  for (std::size_t i = 0; i < v.size(); ++i) {
+    p[2 * i] = v[i].real();
+    p[2 * i + 1] = v[i].imag();
+  }
+}
+
+void store_soft(const detect::SoftOutput& o, std::size_t users, int bits, double* xhat,
+                double* mu, double* rho, double* llr) {
+  store_vector(o.xhat, xhat);
+  for (std::size_t u = 0; u < users; ++u) {
+    mu[u] = o.mu[u];
+    rho[u] = o.rho[u];
+    for (int b = 0; b < bits; ++b) llr[u * bits + b] = o.llrs[u][b];
+  }
+}
+
+// mode 0 = detect_cg, 1 = detect_explicit, 2 = detect_cholesky
+int detect_batch(int mode, int B, int U, long n_sc, int S, const double* H, const double* Y,
+                 double rho_u, double n0, double es, int qam_bits, int K, int tracker,
+                 double* xhat, double* mu, double* rho, double* llr, uint8_t* status,
+                 int threads) {
+  phy::Constellation c;
+  try {
+    c = phy::make_constellation(modulation_of(qam_bits));
+  } catch (const std::exception&) {
+    return 2;
+  }
+  const std::size_t users = U, bs = B;
+  const auto trk = tracker == 0 ? detect::SinrTracker::kExact : detect::SinrTracker::kApprox;
+  parallel_for(n_sc, threads, [&](long sc) {
+    const ComplexMatrix h = load_matrix(H + 2 * sc * bs * users, bs, users);
+    for (int s = 0; s < S; ++s) {
+      const long inst = sc * S + s;
+      const ComplexVector y = load_vector(Y + 2 * inst * bs, bs);
+      double* xo = xhat + 2 * inst * users;
+      double* mo = mu + inst * users;
+      double* ro = rho + inst * users;
+      double* lo = llr + inst * users * qam_bits;
+      uint8_t st = 0;
+      try {
+        detect::SoftOutput o;
+        if (mode == 0)
+          o = detect::detect_cg(h, y, rho_u, n0, es, c, static_cast<std::size_t>(K), trk);
+        else if (mode == 1)
+          o = detect::detect_explicit(h, y, rho_u, n0, es, c);
+        else
+          o = detect::detect_cholesky(h, y, rho_u, n0, es, c);
+        store_soft(o, users, qam_bits, xo, mo, ro, lo);
+      } catch (const solvers::SolverBreakdown&) {
+        st = 1;
+      } catch (const std::exception&) {
+        st = 4;
+      }
+      if (st) {
+        std::memset(xo, 0, sizeof(double) * 2 * users);
+        std::memset(mo, 0, sizeof(double) * users);
+        std::memset(ro, 0, sizeof(double) * users);
+        std::memset(lo, 0, sizeof(double) * users * qam_bits);
+      }
+      status[inst] = st;
+    }
+  });
+  return 0;
+}
+
+int precode_batch(int mode, int B, int U, long n_sc, int S, const double* Hd, const double* T,
+                  double rho_d, int K, double* q, double* s_out, double* gain, uint8_t* status,
+                  int threads) {
+  const std::size_t users = U, bs = B;
+  parallel_for(n_sc, threads, [&](long sc) {
+    const ComplexMatrix hd = load_matrix(Hd + 2 * sc * users * bs, users, bs);
+    for (int s = 0; s < S; ++s) {
+      const long inst = sc * S + s;
+      const ComplexVector t = load_vector(T + 2 * inst * users, users);
+      double* qo = q + 2 * inst * bs;
+      double* so = s_out ? s_out + 2 * inst * bs : nullptr;
+      uint8_t st = 0;
+      try {
+        const precode::PrecodeResult r =
+            mode == 0 ? precode::precode_cg(hd, t, rho_d, static_cast<std::size_t>(K))
+                      : precode::precode_explicit(hd, t, rho_d);
+        store_vector(r.precoded, qo);
+        if (so) store_vector(r.transmit, so);
+        gain[inst] = r.gain;
+        if (r.zero_input) st |= 2;
+      } catch (const solvers::SolverBreakdown&) {
+        st = 1;
+      } catch (const std::exception&) {
+        st = 4;
+      }
+      if (st & 5) {
+        std::memset(qo, 0, sizeof(double) * 2 * bs);
+        if (so) std::memset(so, 0, sizeof(double) * 2 * bs);
+        gain[inst] = 0.0;
+      }
+      status[inst] = st;
+    }
+  });
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_detect_cg(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                  double rho_u, double n0, double es, int qam_bits, int K, int tracker,
+                  double* xhat, double* mu, double* rho, double* llr, uint8_t* status,
+                  int threads) {
+  return detect_batch(0, B, U, n_sc, S, H, Y, rho_u, n0, es, qam_bits, K, tracker, xhat, mu,
+                      rho, llr, status, threads);
+}
+
+int ref_detect_explicit(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                        double rho_u, double n0, double es, int qam_bits, double* xhat,
+                        double* mu, double* rho, double* llr, uint8_t* status, int threads) {
+  return detect_batch(1, B, U, n_sc, S, H, Y, rho_u, n0, es, qam_bits, 1, 0, xhat, mu, rho,
+                      llr, status, threads);
+}
+
+int ref_detect_cholesky(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                        double rho_u, double n0, double es, int qam_bits, double* xhat,
+                        double* mu, double* rho, double* llr, uint8_t* status, int threads) {
+  return detect_batch(2, B, U, n_sc, S, H, Y, rho_u, n0, es, qam_bits, 1, 0, xhat, mu, rho,
+                      llr, status, threads);
+}
+
+int ref_precode_cg(int B, int U, long n_sc, int S, const double* Hd, const double* T,
+                   double rho_d, int K, double* q, double* s, double* gain, uint8_t* status,
+                   int threads) {
+  return precode_batch(0, B, U, n_sc, S, Hd, T, rho_d, K, q, s, gain, status, threads);
+}
+
+int ref_precode_explicit(int B, int U, long n_sc, int S, const double* Hd, const double* T,
+                         double rho_d, double* q, double* s, double* gain, uint8_t* status,
+                         int threads) {
+  return precode_batch(1, B, U, n_sc, S, Hd, T, rho_d, 1, q, s, gain, status, threads);
+}
+
+// Max-log LLRs of one user (detect.cpp:68-86); out has qam_bits entries.
+int ref_compute_llrs(double xr, double xi, double mu, double rho, int qam_bits, double* out) {
+  try {
+    const auto c = phy::make_constellation(modulation_of(qam_bits));
+    const auto l = detect::compute_llrs(cplx(xr, xi), mu, rho, c);
+    for (int b = 0; b < qam_bits; ++b) out[b] = l[b];
+    return 0;
+  } catch (const std::exception&) {
+    return 2;
+  }
+}
+
+// Constellation tables (constellation.cpp:37-86): points[2^bits] complex,
+// axis amplitudes axis0/axis1 [axis_bits][levels/2].
+int ref_constellation(int qam_bits, double* points, double* axis0, double* axis1) {
+  try {
+    const auto c = phy::make_constellation(modulation_of(qam_bits));
+    store_vector(c.points, points);
+    const int half = c.axis_bits, per = (1 << half) / 2;
+    for (int p = 0; p < half; ++p)
+      for (int k = 0; k < per; ++k) {
+        axis0[p * per + k] = c.axis_bit0[p][k];
+        axis1[p * per + k] = c.axis_bit1[p][k];
+      }
+    return 0;
+  } catch (const std::exception&) {
+    return 2;
+  }
+}
+
+// Rng stream: Rng(key).fork(f0).fork(f1)... then n draws of next_u64.
+void ref_rng_u64(uint64_t key, const uint64_t* forks, int n_forks, long n, uint64_t* out) {
+  phy::Rng r(key);
+  for (int i = 0; i < n_forks; ++i) r = r.fork(forks[i]);
+  for (long i = 0; i < n; ++i) out[i] = r.next_u64();
+}
+
+// n complex Gaussians of the given variance from the same stream construction.
+void ref_rng_cgaussian(uint64_t key, const uint64_t* forks, int n_forks, double variance,
+                       long n, double* out) {
+  phy::Rng r(key);
+  for (int i = 0; i < n_forks; ++i) r = r.fork(forks[i]);
+  for (long i = 0; i < n; ++i) {
+    const auto z = r.next_cgaussian(variance);
+    out[2 * i] = z.real();
+    out[2 * i + 1] = z.imag();
+  }
+}
+
+// rayleigh_channel (channel.cpp:10-17) from Rng(key).fork(...).
+void ref_rayleigh(uint64_t key, const uint64_t* forks, int n_forks, int B, int U, double* out) {
+  phy::Rng r(key);
+  for (int i = 0; i < n_forks; ++i) r = r.fork(forks[i]);
+  const auto h = phy::rayleigh_channel(B, U, r);
+  for (int b = 0; b < B; ++b)
+    for (int u = 0; u < U; ++u) {
+      out[2 * (b * U + u)] = h(b, u).real();
+      out[2 * (b * U + u) + 1] = h(b, u).imag();
+    }
+}
+
+double ref_uplink_noise_variance(double snr_db, int users) {
+  return phy::uplink_noise_variance(snr_db, users);
+}
+double ref_downlink_noise_variance(double snr_db) {
+  return phy::downlink_noise_variance(snr_db);
+}
+
+// Closed-form stage counts (opcount.cpp:69-138); method 0..3 = Cholesky, CG,
+// CGLS, Neumann. out has opcount::kStageCount entries.
+int ref_count_detect_stages(int method, int B, int U, int K, uint64_t* out) {
+  const auto m = static_cast<opcount::DetectMethod>(method);
+  const auto c = opcount::count_detect_stages(m, B, U, K);
+  for (int s = 0; s < opcount::kStageCount; ++s) out[s] = c.by_stage[s];
+  return opcount::kStageCount;
+}
+
+// Instrumented tally of one detect_cg call (approx tracker), per stage.
+int ref_tally_detect_cg(int B, int U, int K, int tracker, uint64_t seed, uint64_t* out) {
+  phy::Rng rng(seed);
+  ComplexMatrix h(B, U);
+  for (int b = 0; b < B; ++b)
+    for (int u = 0; u < U; ++u) h(b, u) = rng.next_cgaussian(1.0);
+  ComplexVector y(B);
+  for (auto& v : y) v = rng.next_cgaussian(1.0);
+  const auto c = phy::make_constellation(phy::Modulation::kQam16);
+  opcount::Tally tally;
+  {
+    opcount::ScopedTally scope(tally);
+    (void)detect::detect_cg(h, y, 10.0, 0.1, 1.0, c, K,
+                            tracker == 0 ? detect::SinrTracker::kExact
+                                         : detect::SinrTracker::kApprox);
+  }
+  for (int s = 0; s < opcount::kStageCount; ++s)
+    out[s] = tally.get(static_cast<opcount::Stage>(s));
+  return opcount::kStageCount;
+}
+
+// Exact-tracker filters L_1..L_K of one (H, y) pair (detect.cpp:336-368),
+// driven by cg_solve exactly as detect_cg drives it; filters [K][U][U] c128,
+// iterates [K][U] c128. Used to pin the kernel's polynomial-basis tracker.
+int ref_exact_filters(int B, int U, const double* H, const double* Y, double rho_u, int K,
+                      double* filters, double* iterates) {
+  try {
+    const ComplexMatrix h = load_matrix(H, B, U);
+    const ComplexVector y = load_vector(Y, B);
+    const auto a = gram_regularized(h, 1.0 / rho_u, GramSide::kUplink);
+    const auto a_full = a.full();
+    const auto b = matvec_adjoint(h, y);
+    detect::ExactSinrTracker tr(U);
+    solvers::IterOptions opts;
+    opts.keep_trace = true;
+    int k = 0;
+    opts.on_iteration = [&](std::size_t, double alpha, double beta) {
+      tr.step(a_full, alpha, beta);
+      const auto& f = tr.filter();
+      for (int i = 0; i < U; ++i)
+        for (int j = 0; j < U; ++j) {
+          filters[2 * ((k * U + i) * U + j)] = f(i, j).real();
+          filters[2 * ((k * U + i) * U + j) + 1] = f(i, j).imag();
+        }
+      ++k;
+    };
+    const auto res = solvers::cg_solve(a, b, K, opts);
+    for (int kk = 0; kk < K; ++kk) store_vector(res.trace[kk], iterates + 2 * kk * U);
+    return 0;
+  } catch (const solvers::SolverBreakdown&) {
+    return 1;
+  } catch (const std::exception&) {
+    return 2;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+"""ctypes binding of libcgmimo_b200.so (the C ABI in include/cgmimo_b200.h).
+
+There is no fallback: if the library is missing or no sm_100 device is
+present, the calls raise.  ``symbols()`` lists every exported entry point the
+header declares (checked by tests/test_abi.py without a GPU).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcgmimo_b200.so")
+
+CGM_OK, CGM_EINVAL, CGM_EBREAKDOWN, CGM_ECUDA, CGM_ENCCL, CGM_ENOMEM = range(6)
+CGM_TRACKER_EXACT, CGM_TRACKER_APPROX = 0, 1
+CGM_DEVICE_POINTERS = 0x1
+CGM_HD_UPLINK_LAYOUT = 0x2
+
+_vp = C.c_void_p
+_int = C.c_int
+_long = C.c_long
+_dbl = C.c_double
+_u64 = C.c_uint64
+
+# name -> (restype, argtypes); mirrors include/cgmimo_b200.h
+SIGNATURES = {
+    "cgm_ctx_create": (_int, [_int, C.POINTER(_vp)]),
+    "cgm_ctx_destroy": (_int, [_vp]),
+    "cgm_ctx_set_stream": (_int, [_vp, _vp]),
+    "cgm_synchronize": (_int, [_vp]),
+    "cgm_last_error": (C.c_char_p, [_vp]),
+    "cgm_kernel_launches": (_long, [_vp]),
+    "cgm_version": (C.c_char_p, []),
+    "cgm_detect_cg": (_int, [_vp, _int, _int, _long, _int, _vp, _vp, _dbl, _dbl, _dbl, _int, _int,
+                             _int, _vp, _vp, _vp, _vp, _vp, C.c_uint]),
+    "cgm_precode_cg": (_int, [_vp, _int, _int, _long, _int, _vp, _vp, _dbl, _int, _vp, _vp, _vp,
+                              _vp, C.c_uint]),
+    "cgm_detect_precode_cg": (_int, [_vp, _int, _int, _long, _int, _vp, _vp, _dbl, _dbl, _dbl,
+                                     _int, _int, _int, _vp, _vp, _vp, _vp, _vp, _int, _vp, _dbl,
+                                     _int, _vp, _vp, _vp, _vp, C.c_uint]),
+    "cgm_generate_uplink": (_int, [_vp, _int, _int, _long, _long, _int, _u64, _int, _dbl, _vp,
+                                   _vp, _vp]),
+    "cgm_generate_downlink": (_int, [_vp, _int, _int, _long, _long, _int, _u64, _int, _vp, _vp,
+                                     _vp]),
+    "cgm_generate_symbols": (_int, [_vp, _int, _long, _long, _int, _u64, _int, _vp, _vp]),
+    "cgm_generate_uplink_correlated": (_int, [_vp, _int, _int, _long, _long, _int, _u64, _int,
+                                              _dbl, _vp, _vp, _vp, _vp]),
+}
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load the in-tree library (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def symbols() -> list[str]:
+    return sorted(SIGNATURES)

@@ -1,0 +1,82 @@
+"""The BASELINE.json workloads as data.
+
+SNR conventions follow the reference: uplink N0 = U Es / SNR
+(channel.cpp:44-47) and rho_u = Es / N0 (sim.cpp:376-377); downlink
+N0 = 1 / SNR (channel.cpp:49-51) with the BASELINE regulariser alpha = U N0 / Es,
+passed to precode_cg as rho_d = 1 / alpha (the reference harness uses
+alpha = N0, sim.cpp:397-398 -- only the argument differs).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    kind: str              # "uplink" | "downlink" | "both"
+    B: int
+    U: int
+    S: int                 # vectors per subcarrier sharing H
+    n_sc: int
+    K: int
+    tracker: str = "exact"
+    qam_bits: int = 6
+    snr_db: float = 15.0
+    seed: int = 1
+    corr: float = 0.0      # BS-side exponential correlation R_ij = corr^|i-j|
+    es: float = 1.0
+
+    @property
+    def n0(self) -> float:
+        snr = 10.0 ** (self.snr_db / 10.0)
+        return self.U * self.es / snr if self.kind != "downlink" else 1.0 / snr
+
+    @property
+    def rho_u(self) -> float:
+        return self.es / self.n0
+
+    @property
+    def rho_d(self) -> float:
+        snr = 10.0 ** (self.snr_db / 10.0)
+        alpha = self.U * (1.0 / snr) / self.es
+        return 1.0 / alpha
+
+    @property
+    def vectors(self) -> int:
+        return self.n_sc * self.S
+
+    def scaled(self, n_sc: int) -> "Config":
+        return replace(self, n_sc=n_sc)
+
+    def rsqrt(self) -> np.ndarray | None:
+        """R^{1/2} of R_ij = corr^|i-j| (B x B), FP64 symmetric eigendecomposition."""
+        if not self.corr:
+            return None
+        idx = np.arange(self.B)
+        R = self.corr ** np.abs(idx[:, None] - idx[None, :])
+        w, V = np.linalg.eigh(R)
+        return (V * np.sqrt(np.clip(w, 0.0, None))) @ V.T
+
+
+CONFIGS = {
+    "cfg1": Config("cfg1", "uplink", B=128, U=8, S=1, n_sc=1024, K=3, tracker="exact",
+                   qam_bits=4, snr_db=10.0, seed=1),
+    "cfg2": Config("cfg2", "uplink", B=128, U=32, S=14, n_sc=1200, K=4, tracker="approx",
+                   qam_bits=6, snr_db=15.0, seed=2),
+    "cfg3": Config("cfg3", "downlink", B=128, U=16, S=1, n_sc=16384, K=3, qam_bits=4,
+                   snr_db=10.0, seed=3),
+    "cfg5": Config("cfg5", "both", B=256, U=32, S=16, n_sc=65536, K=4, tracker="exact",
+                   qam_bits=6, snr_db=15.0, seed=5, corr=0.5),
+}
+for _K in (2, 4, 8):
+    CONFIGS[f"cfg4a_K{_K}"] = Config(f"cfg4a_K{_K}", "uplink", B=64, U=32, S=1, n_sc=65536,
+                                     K=_K, tracker="exact", qam_bits=6, snr_db=20.0, seed=4)
+    CONFIGS[f"cfg4b_K{_K}"] = Config(f"cfg4b_K{_K}", "uplink", B=128, U=64, S=1, n_sc=65536,
+                                     K=_K, tracker="exact", qam_bits=6, snr_db=20.0, seed=4)
+
+
+def get_config(name: str) -> Config:
+    return CONFIGS[name]

@@ -1,0 +1,454 @@
+// cgm_capi.cu -- host runtime behind include/cgmimo_b200.h: contexts and
+// streams, argument validation with the reference's error semantics,
+// template dispatch of the fused subcarrier kernel, the chunked host-buffer
+// pipeline (H2D / kernel / D2H overlapped on two streams) and the seeded
+// device input generators.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cgmimo_b200.h"
+#include "cgm_kernels.cuh"
+
+struct cgm_ctx {
+  int device = 0;
+  int sms = 0;
+  int max_smem = 0;
+  cudaStream_t user_stream = nullptr;
+  cudaStream_t pipe[2] = {nullptr, nullptr};
+  // host-mode device workspaces, one set per pipeline stream
+  void* ws[2] = {nullptr, nullptr};
+  size_t ws_bytes[2] = {0, 0};
+  float* tscratch = nullptr;
+  size_t tscratch_bytes = 0;
+  long launches = 0;
+  std::string err;
+};
+
+namespace {
+
+int fail(cgm_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return code;
+}
+
+#define CGM_CUDA(ctx, call)                                                        \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(ctx, CGM_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                             \
+  } while (0)
+
+unsigned gray_decode(unsigned g) {
+  unsigned m = g;
+  for (unsigned s = g >> 1; s != 0; s >>= 1) m ^= s;
+  return m;
+}
+
+// Axis amplitude subsets of Gray square QAM, constellation.cpp:75-84.
+cgm::AxisTables make_axis_tables() {
+  cgm::AxisTables t;
+  std::memset(&t, 0, sizeof t);
+  for (int q = 0; q < 3; ++q) {
+    const int half = q + 1;
+    const unsigned levels = 1u << half;
+    const double scale = 1.0 / std::sqrt(2.0 * ((double)levels * levels - 1.0) / 3.0);
+    int n0[3] = {0, 0, 0}, n1[3] = {0, 0, 0};
+    for (unsigned g = 0; g < levels; ++g) {
+      const double amp = (2.0 * gray_decode(g) - (levels - 1.0)) * scale;
+      for (int p = 0; p < half; ++p) {
+        if ((g >> (half - 1 - p)) & 1u) t.a1[q][p][n1[p]++] = static_cast<float>(amp);
+        else t.a0[q][p][n0[p]++] = static_cast<float>(amp);
+      }
+    }
+  }
+  return t;
+}
+
+int up_of(int U) { return U <= 8 ? 8 : U <= 16 ? 16 : U <= 32 ? 32 : 64; }
+
+struct Launch {
+  int smem = 0;
+  int grid = 0;
+  int t_in_smem = 1;
+};
+
+template <int UP, int NT>
+int plan_and_launch(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
+  cgm::GramPlan<UP, NT> gp;
+  gp.plan(p.B, p.S);
+  cgm::ChebPlan<UP, NT> cp;
+  cp.plan();
+  const int red = std::max(gp.red_floats(), cp.red_floats());
+  const int Kmax = std::max(p.K, p.Kt);
+  cgm::Smem<UP> L;
+  p.t_in_smem = 1;
+  L.plan(p.B, p.S, p.St, Kmax, p.exact, 1, red, NT / 32);
+  if (L.total > ctx->max_smem) {
+    p.t_in_smem = 0;
+    L.plan(p.B, p.S, p.St, Kmax, p.exact, 0, red, NT / 32);
+  }
+  if (L.total > ctx->max_smem)
+    return fail(ctx, CGM_EINVAL,
+                "per-subcarrier working set %d B exceeds shared memory (%d B): reduce B or S",
+                L.total, ctx->max_smem);
+  auto kern = cgm::subcarrier_kernel<UP, NT>;
+  CGM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total));
+  int occ = 0;
+  CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, L.total));
+  if (occ < 1) return fail(ctx, CGM_EINVAL, "kernel does not fit on an SM (smem %d)", L.total);
+  long grid = std::min<long>(p.n_sc, static_cast<long>(occ) * ctx->sms);
+  if (grid < 1) grid = 1;
+  if (p.exact && !p.t_in_smem) {
+    const size_t need = static_cast<size_t>(grid) * Kmax * UP * UP * sizeof(float2);
+    if (need > ctx->tscratch_bytes) {
+      if (ctx->tscratch) cudaFree(ctx->tscratch);
+      ctx->tscratch = nullptr;
+      ctx->tscratch_bytes = 0;
+      CGM_CUDA(ctx, cudaMalloc(&ctx->tscratch, need));
+      ctx->tscratch_bytes = need;
+    }
+    p.tscratch = ctx->tscratch;
+  }
+  kern<<<static_cast<unsigned>(grid), NT, L.total, st>>>(p);
+  CGM_CUDA(ctx, cudaGetLastError());
+  ctx->launches += 1;
+  return CGM_OK;
+}
+
+int launch(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
+  if (p.n_sc <= 0) return CGM_OK;
+  const int UP = up_of(p.U);
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
+  p.use_tma = (!p.hd_layout && p.U == UP && (p.B % 2) == 0 && (a & 15u) == 0) ? 1 : 0;
+  switch (UP) {
+    case 8: return plan_and_launch<8, 128>(ctx, p, st);
+    case 16: return plan_and_launch<16, 128>(ctx, p, st);
+    case 32: return plan_and_launch<32, 256>(ctx, p, st);
+    default: return plan_and_launch<64, 256>(ctx, p, st);
+  }
+}
+
+// ------------------------------------------------------------ validation
+struct Job {
+  int B = 0, U = 0, S = 0, St = 0, K = 0, Kt = 0, bits = 0, tracker = 0;
+  long n_sc = 0;
+  double rho_u = 1, n0 = 1, es = 1, rho_d = 1;
+  bool hd_layout = false;
+  const float *H = nullptr, *Y = nullptr, *T = nullptr;
+  float *xhat = nullptr, *mu = nullptr, *rho = nullptr, *llr = nullptr;
+  uint8_t* status = nullptr;
+  float *q = nullptr, *s = nullptr, *gain = nullptr;
+  uint8_t* pstatus = nullptr;
+};
+
+int validate(cgm_ctx* ctx, const Job& j) {
+  if (!ctx) return CGM_EINVAL;
+  if (j.n_sc < 0) return fail(ctx, CGM_EINVAL, "n_sc must be >= 0");
+  if (j.B < 1 || j.U < 1) return fail(ctx, CGM_EINVAL, "B and U must be >= 1");
+  if (j.U > 64) return fail(ctx, CGM_EINVAL, "U = %d > 64 is not supported", j.U);
+  if (j.S < 0 || j.St < 0 || j.S + j.St > cgm::kMaxSys)
+    return fail(ctx, CGM_EINVAL, "vectors per subcarrier must be in [0, %d]", cgm::kMaxSys);
+  if (j.S > 0) {
+    // detect.cpp:186-188
+    if (!(j.rho_u > 0.0 && j.n0 > 0.0 && j.es > 0.0))
+      return fail(ctx, CGM_EINVAL, "detect_cg: bad parameters (rho_u, N0, Es must be > 0)");
+    if (j.K < 1) return fail(ctx, CGM_EINVAL, "detect_cg: need at least one iteration");
+    if (j.K > cgm::kMaxK) return fail(ctx, CGM_EINVAL, "K = %d > %d", j.K, cgm::kMaxK);
+    if (j.bits != 2 && j.bits != 4 && j.bits != 6)
+      return fail(ctx, CGM_EINVAL, "qam_bits must be 2, 4 or 6");
+    if (j.tracker != CGM_TRACKER_EXACT && j.tracker != CGM_TRACKER_APPROX)
+      return fail(ctx, CGM_EINVAL, "unknown tracker %d", j.tracker);
+    if (!j.H || !j.Y) return fail(ctx, CGM_EINVAL, "H and Y are required");
+  }
+  if (j.St > 0) {
+    // precode.cpp:59-60, solvers.cpp:39-40
+    if (!(j.rho_d > 0.0)) return fail(ctx, CGM_EINVAL, "precode_cg: rho_d must be positive");
+    if (j.Kt < 1) return fail(ctx, CGM_EINVAL, "cg_solve: need at least one iteration");
+    if (j.Kt > cgm::kMaxK) return fail(ctx, CGM_EINVAL, "K = %d > %d", j.Kt, cgm::kMaxK);
+    if (!j.H || !j.T) return fail(ctx, CGM_EINVAL, "H and T are required");
+  }
+  return CGM_OK;
+}
+
+cgm::KernelParams params_of(const Job& j, long n_sc) {
+  cgm::KernelParams p;
+  std::memset(&p, 0, sizeof p);
+  p.H = reinterpret_cast<const float2*>(j.H);
+  p.Y = reinterpret_cast<const float2*>(j.Y);
+  p.T = reinterpret_cast<const float2*>(j.T);
+  p.xhat = reinterpret_cast<float2*>(j.xhat);
+  p.mu = j.mu;
+  p.rho = j.rho;
+  p.llr = j.llr;
+  p.status = j.status;
+  p.q = reinterpret_cast<float2*>(j.q);
+  p.s_out = reinterpret_cast<float2*>(j.s);
+  p.gain = j.gain;
+  p.pstatus = j.pstatus;
+  p.n_sc = n_sc;
+  p.B = j.B;
+  p.U = j.U;
+  p.S = j.S;
+  p.St = j.St;
+  p.K = j.S > 0 ? j.K : 0;
+  p.Kt = j.St > 0 ? j.Kt : 0;
+  p.bits = j.bits > 0 ? j.bits : 2;
+  p.hd_layout = j.hd_layout ? 1 : 0;
+  p.exact = (j.S > 0 && j.tracker == CGM_TRACKER_EXACT) ? 1 : 0;
+  p.rho_inv_u = j.S > 0 ? static_cast<float>(1.0 / j.rho_u) : 0.f;
+  p.rho_inv_d = j.St > 0 ? static_cast<float>(1.0 / j.rho_d) : 0.f;
+  p.n0 = static_cast<float>(j.n0);
+  p.es = static_cast<float>(j.es);
+  return p;
+}
+
+// Per-subcarrier byte counts of each array (host pipeline).
+struct Sizes {
+  size_t h, y, t, xhat, mu, rho, llr, st, q, s, gain, pst;
+  size_t in() const { return h + y + t; }
+  size_t total() const { return h + y + t + xhat + mu + rho + llr + st + q + s + gain + pst; }
+};
+
+Sizes sizes_of(const Job& j) {
+  Sizes z;
+  z.h = static_cast<size_t>(j.B) * j.U * 8;
+  z.y = static_cast<size_t>(j.S) * j.B * 8;
+  z.t = static_cast<size_t>(j.St) * j.U * 8;
+  z.xhat = j.xhat ? static_cast<size_t>(j.S) * j.U * 8 : 0;
+  z.mu = j.mu ? static_cast<size_t>(j.S) * j.U * 4 : 0;
+  z.rho = j.rho ? static_cast<size_t>(j.S) * j.U * 4 : 0;
+  z.llr = j.llr ? static_cast<size_t>(j.S) * j.U * j.bits * 4 : 0;
+  z.st = j.status ? static_cast<size_t>(j.S) : 0;
+  z.q = j.q ? static_cast<size_t>(j.St) * j.B * 8 : 0;
+  z.s = j.s ? static_cast<size_t>(j.St) * j.B * 8 : 0;
+  z.gain = j.gain ? static_cast<size_t>(j.St) * 4 : 0;
+  z.pst = j.pstatus ? static_cast<size_t>(j.St) : 0;
+  return z;
+}
+
+size_t round_up(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+int run_job(cgm_ctx* ctx, const Job& j, unsigned flags) {
+  int rc = validate(ctx, j);
+  if (rc) return rc;
+  CGM_CUDA(ctx, cudaSetDevice(ctx->device));
+  if (j.n_sc == 0) return CGM_OK;
+  if (flags & CGM_DEVICE_POINTERS) {
+    cgm::KernelParams p = params_of(j, j.n_sc);
+    return launch(ctx, p, ctx->user_stream);
+  }
+  // ---------------- host buffers: chunked, double-buffered pipeline
+  const Sizes z = sizes_of(j);
+  const size_t per_sc = z.total() + 16 * 12;
+  const size_t budget = 192ull << 20;  // per buffer set
+  long chunk = static_cast<long>(std::max<size_t>(1, budget / std::max<size_t>(per_sc, 1)));
+  chunk = std::min(chunk, j.n_sc);
+  // aim for >= 4 chunks on large jobs so copies overlap compute
+  if (j.n_sc >= 4 * 148) chunk = std::min(chunk, (j.n_sc + 3) / 4);
+  for (int b = 0; b < 2; ++b) {
+    size_t need = 0;
+    const size_t parts[12] = {z.h, z.y, z.t, z.xhat, z.mu, z.rho, z.llr, z.st, z.q, z.s, z.gain, z.pst};
+    for (size_t x : parts) need += round_up(x * chunk);
+    if (need > ctx->ws_bytes[b]) {
+      if (ctx->ws[b]) cudaFree(ctx->ws[b]);
+      ctx->ws[b] = nullptr;
+      ctx->ws_bytes[b] = 0;
+      CGM_CUDA(ctx, cudaMalloc(&ctx->ws[b], need));
+      ctx->ws_bytes[b] = need;
+    }
+  }
+  auto H8 = reinterpret_cast<const char*>(j.H);
+  auto Y8 = reinterpret_cast<const char*>(j.Y);
+  auto T8 = reinterpret_cast<const char*>(j.T);
+  int ci = 0;
+  for (long c0 = 0; c0 < j.n_sc; c0 += chunk, ++ci) {
+    const long n = std::min(chunk, j.n_sc - c0);
+    const int b = ci & 1;
+    cudaStream_t st = ctx->pipe[b];
+    char* base = static_cast<char*>(ctx->ws[b]);
+    size_t off = 0;
+    auto carve = [&](size_t per) -> char* {
+      char* p = per ? base + off : nullptr;
+      off += round_up(per * chunk);
+      return p;
+    };
+    char* dH = carve(z.h);
+    char* dY = carve(z.y);
+    char* dT = carve(z.t);
+    char* dX = carve(z.xhat);
+    char* dMu = carve(z.mu);
+    char* dRho = carve(z.rho);
+    char* dL = carve(z.llr);
+    char* dSt = carve(z.st);
+    char* dQ = carve(z.q);
+    char* dS = carve(z.s);
+    char* dG = carve(z.gain);
+    char* dPs = carve(z.pst);
+    if (z.h) CGM_CUDA(ctx, cudaMemcpyAsync(dH, H8 + z.h * c0, z.h * n, cudaMemcpyHostToDevice, st));
+    if (z.y) CGM_CUDA(ctx, cudaMemcpyAsync(dY, Y8 + z.y * c0, z.y * n, cudaMemcpyHostToDevice, st));
+    if (z.t) CGM_CUDA(ctx, cudaMemcpyAsync(dT, T8 + z.t * c0, z.t * n, cudaMemcpyHostToDevice, st));
+    Job jd = j;
+    jd.H = reinterpret_cast<float*>(dH);
+    jd.Y = reinterpret_cast<float*>(dY);
+    jd.T = reinterpret_cast<float*>(dT);
+    jd.xhat = reinterpret_cast<float*>(dX);
+    jd.mu = reinterpret_cast<float*>(dMu);
+    jd.rho = reinterpret_cast<float*>(dRho);
+    jd.llr = reinterpret_cast<float*>(dL);
+    jd.status = reinterpret_cast<uint8_t*>(dSt);
+    jd.q = reinterpret_cast<float*>(dQ);
+    jd.s = reinterpret_cast<float*>(dS);
+    jd.gain = reinterpret_cast<float*>(dG);
+    jd.pstatus = reinterpret_cast<uint8_t*>(dPs);
+    cgm::KernelParams p = params_of(jd, n);
+    rc = launch(ctx, p, st);
+    if (rc) return rc;
+    auto d2h = [&](void* host, const char* dev, size_t per) -> cudaError_t {
+      if (!per) return cudaSuccess;
+      return cudaMemcpyAsync(static_cast<char*>(host) + per * c0, dev, per * n,
+                             cudaMemcpyDeviceToHost, st);
+    };
+    CGM_CUDA(ctx, d2h(j.xhat, dX, z.xhat));
+    CGM_CUDA(ctx, d2h(j.mu, dMu, z.mu));
+    CGM_CUDA(ctx, d2h(j.rho, dRho, z.rho));
+    CGM_CUDA(ctx, d2h(j.llr, dL, z.llr));
+    CGM_CUDA(ctx, d2h(j.status, dSt, z.st));
+    CGM_CUDA(ctx, d2h(j.q, dQ, z.q));
+    CGM_CUDA(ctx, d2h(j.s, dS, z.s));
+    CGM_CUDA(ctx, d2h(j.gain, dG, z.gain));
+    CGM_CUDA(ctx, d2h(j.pstatus, dPs, z.pst));
+  }
+  CGM_CUDA(ctx, cudaStreamSynchronize(ctx->pipe[0]));
+  CGM_CUDA(ctx, cudaStreamSynchronize(ctx->pipe[1]));
+  return CGM_OK;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+const char* cgm_version(void) { return "cgmimo_b200 0.1 sm_100a"; }
+
+// hooks for cgm_generate.cu (same library, not part of the public header)
+int cgm_internal_fail(cgm_ctx* ctx, int code, const char* msg) { return fail(ctx, code, "%s", msg); }
+int cgm_internal_device(cgm_ctx* ctx, void** stream, int* sms, long** launches) {
+  if (!ctx) return CGM_EINVAL;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, CGM_ECUDA, "cudaSetDevice");
+  *stream = ctx->user_stream;
+  *sms = ctx->sms;
+  *launches = &ctx->launches;
+  return CGM_OK;
+}
+
+int cgm_ctx_create(int device, cgm_ctx** out) {
+  if (!out) return CGM_EINVAL;
+  *out = nullptr;
+  cgm_ctx* ctx = new cgm_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess)
+    e = cudaDeviceGetAttribute(&ctx->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  int major = 0, minor = 0;
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+  if (e == cudaSuccess && major != 10) {
+    delete ctx;
+    return CGM_ECUDA;  // built for sm_100a only
+  }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pipe[0], cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pipe[1], cudaStreamNonBlocking);
+  if (e == cudaSuccess) {
+    const cgm::AxisTables t = make_axis_tables();
+    e = cudaMemcpyToSymbol(cgm::c_axis, &t, sizeof t);
+  }
+  if (e != cudaSuccess) {
+    delete ctx;
+    return CGM_ECUDA;
+  }
+  *out = ctx;
+  return CGM_OK;
+}
+
+int cgm_ctx_destroy(cgm_ctx* ctx) {
+  if (!ctx) return CGM_OK;
+  cudaSetDevice(ctx->device);
+  for (int b = 0; b < 2; ++b) {
+    if (ctx->ws[b]) cudaFree(ctx->ws[b]);
+    if (ctx->pipe[b]) cudaStreamDestroy(ctx->pipe[b]);
+  }
+  if (ctx->tscratch) cudaFree(ctx->tscratch);
+  delete ctx;
+  return CGM_OK;
+}
+
+int cgm_ctx_set_stream(cgm_ctx* ctx, void* stream) {
+  if (!ctx) return CGM_EINVAL;
+  ctx->user_stream = static_cast<cudaStream_t>(stream);
+  return CGM_OK;
+}
+
+int cgm_synchronize(cgm_ctx* ctx) {
+  if (!ctx) return CGM_EINVAL;
+  CGM_CUDA(ctx, cudaSetDevice(ctx->device));
+  CGM_CUDA(ctx, cudaStreamSynchronize(ctx->user_stream));
+  return CGM_OK;
+}
+
+const char* cgm_last_error(const cgm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+long cgm_kernel_launches(const cgm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int cgm_detect_cg(cgm_ctx* ctx, int B, int U, long n_sc, int S, const float* H, const float* Y,
+                  double rho_u, double n0, double es, int qam_bits, int K, int tracker,
+                  float* xhat, float* mu, float* rho, float* llr, uint8_t* status,
+                  unsigned flags) {
+  Job j;
+  j.B = B; j.U = U; j.n_sc = n_sc; j.S = S; j.H = H; j.Y = Y;
+  j.rho_u = rho_u; j.n0 = n0; j.es = es; j.bits = qam_bits; j.K = K; j.tracker = tracker;
+  j.xhat = xhat; j.mu = mu; j.rho = rho; j.llr = llr; j.status = status;
+  if (S < 1) return fail(ctx, CGM_EINVAL, "detect_cg: S must be >= 1");
+  return run_job(ctx, j, flags);
+}
+
+int cgm_precode_cg(cgm_ctx* ctx, int B, int U, long n_sc, int S, const float* Hd,
+                   const float* T, double rho_d, int K, float* q, float* s, float* gain,
+                   uint8_t* status, unsigned flags) {
+  Job j;
+  j.B = B; j.U = U; j.n_sc = n_sc; j.St = S; j.H = Hd; j.T = T; j.rho_d = rho_d; j.Kt = K;
+  j.hd_layout = !(flags & CGM_HD_UPLINK_LAYOUT);
+  j.q = q; j.s = s; j.gain = gain; j.pstatus = status;
+  if (S < 1) return fail(ctx, CGM_EINVAL, "precode_cg: S must be >= 1");
+  return run_job(ctx, j, flags);
+}
+
+int cgm_detect_precode_cg(cgm_ctx* ctx, int B, int U, long n_sc, int S, const float* H,
+                          const float* Y, double rho_u, double n0, double es, int qam_bits,
+                          int K, int tracker, float* xhat, float* mu, float* rho, float* llr,
+                          uint8_t* status, int St, const float* T, double rho_d, int Kt,
+                          float* q, float* s, float* gain, uint8_t* pstatus, unsigned flags) {
+  Job j;
+  j.B = B; j.U = U; j.n_sc = n_sc; j.S = S; j.H = H; j.Y = Y;
+  j.rho_u = rho_u; j.n0 = n0; j.es = es; j.bits = qam_bits; j.K = K; j.tracker = tracker;
+  j.xhat = xhat; j.mu = mu; j.rho = rho; j.llr = llr; j.status = status;
+  j.St = St; j.T = T; j.rho_d = rho_d; j.Kt = Kt;
+  j.q = q; j.s = s; j.gain = gain; j.pstatus = pstatus;
+  if (S < 1 || St < 1) return fail(ctx, CGM_EINVAL, "detect_precode_cg: S and St must be >= 1");
+  return run_job(ctx, j, flags);
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+// cgm_device.cuh -- device helpers shared by the sm_100a kernels:
+// complex64 arithmetic on float2, warp reductions, the TMA bulk-copy
+// (cp.async.bulk + mbarrier complete_tx) used to stage each subcarrier's
+// contiguous H / Y block into shared memory, and the 4x4 register-tiled
+// "conj(X)^T Y" contraction that the Gram, matched filter and Chebyshev
+// basis products are all built from.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cgm {
+
+// ------------------------------------------------------------ complex64
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cscale(float s, float2 a) { return make_float2(s * a.x, s * a.y); }
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+// acc += a * b
+__device__ __forceinline__ void cfma(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, acc.x);
+  acc.x = fmaf(-a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y);
+  acc.y = fmaf(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+__device__ __forceinline__ void cfma_conj(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, acc.x);
+  acc.x = fmaf(a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y);
+  acc.y = fmaf(-a.y, b.x, acc.y);
+}
+__device__ __forceinline__ float cnorm(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }
+
+// ------------------------------------------------------------ reductions
+// Sum over aligned groups of G lanes (G a power of two <= 32).
+template <int G>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------ TMA bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+// One bulk global->shared copy (bytes % 16 == 0, both addresses 16B aligned)
+// completing on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Order prior generic-proxy smem accesses before later async-proxy writes
+// into the same buffer (buffer reuse across subcarriers).
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ------------------------------------------------------------ 4x4 tile
+// acc[r][c] += sum_{k in [k0,k1)} conj(X[k*ldx + i0 + r]) * Y(k, j0 + c)
+// where Y(k, j) = Ys[k*yk + j*yj].  X rows are read as two float4 (i0 % 2 == 0
+// and the row 16B aligned); columns of Y with j >= jmax read column jmax-1
+// (results discarded by the caller).
+template <bool Y_ROW_CONTIG>
+__device__ __forceinline__ void tile4x4(float2 (&acc)[4][4], const float2* __restrict__ X, int ldx,
+                                        int i0, const float2* __restrict__ Ys, int yk, int yj,
+                                        int j0, int jmax, int k0, int k1) {
+  int jc[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) jc[c] = min(j0 + c, jmax - 1);
+#pragma unroll 2
+  for (int k = k0; k < k1; ++k) {
+    const float4* xr = reinterpret_cast<const float4*>(X + k * ldx + i0);
+    const float4 xa = xr[0], xb = xr[1];
+    const float2 x[4] = {make_float2(xa.x, xa.y), make_float2(xa.z, xa.w),
+                         make_float2(xb.x, xb.y), make_float2(xb.z, xb.w)};
+    float2 y[4];
+    if (Y_ROW_CONTIG) {
+      const float4* yr = reinterpret_cast<const float4*>(Ys + k * yk + j0);
+      const float4 ya = yr[0], yb = yr[1];
+      y[0] = make_float2(ya.x, ya.y);
+      y[1] = make_float2(ya.z, ya.w);
+      y[2] = make_float2(yb.x, yb.y);
+      y[3] = make_float2(yb.z, yb.w);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) y[c] = Ys[k * yk + jc[c] * yj];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cfma_conj(acc[r][c], x[r], y[c]);
+  }
+}
+
+}  // namespace cgm
