@@ -1,0 +1,397 @@
+"""bench.py -- throughput of the B200 CG detection path on BASELINE's headline
+workload (configs[1] = cfg2: uplink 128x32, approximate SINR, K=4, 64-QAM,
+1200 subcarriers x 14 OFDM symbols = 16,800 vectors per step).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2]
+
+* a step = one pass of the fused kernel over one batch (16,800 vectors) with
+  inputs resident in HBM; steps rotate over R distinct frames whose inputs
+  total more than the 126 MB L2 (no L2 reuse between steps);
+* value = whole-job vectors/s (max device time over ranks, CUDA events on the
+  launching stream); e2e = the same metric through the public host-buffer
+  API (pinned host H/Y in, LLR/xhat/mu/rho/status out, copies in the timed
+  region);
+* N > 1 (torchrun): every rank processes its own shard of subcarriers (weak
+  scaling, no data-path collective); the NCCL gather of LLRs to rank 0 is
+  timed separately and reported under "gather";
+* --impl reference: the unmodified reference (oracle/_ref, FP64 per-call
+  detect_cg over all host threads) on the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "detected subcarrier-vectors/s"
+UNIT = "vectors/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = {"hbm_gbs": 6449.1, "sm_max_mhz": 1965.0, "source": "fallback"}
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        peaks.update({k: d[k] for k in ("hbm_gbs", "sm_max_mhz") if k in d})
+        peaks["source"] = "MEASURED_PEAKS.json"
+    return peaks
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons while the timed region runs."""
+
+    def __init__(self, device: int, period_s: float = 0.002):
+        self.device = device
+        self.period = period_s
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self._t = None
+        self.max_mhz = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            names = {
+                "hw_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+                "hw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": getattr(pynvml, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+                "hw_power_brake_slowdown": getattr(pynvml, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80),
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                        for n, bit in names.items():
+                            if r & bit:
+                                self.reasons.add(n)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception as e:  # NVML unavailable: record why
+            self.reasons.add(f"nvml-unavailable:{type(e).__name__}")
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=1)
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "reasons": sorted(self.reasons)}
+
+
+def read_traffic(cfg_name: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f).get(cfg_name)
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    import oracle.cpu_bench as cb
+    from paper_1404_0424_b200.configs import get_config
+
+    cfg = get_config(args.config)
+    threads = os.cpu_count() or 1
+    r = cb.spawn(args.config, cfg.n_sc, threads, passes=max(1, args.steps),
+                 warmup=max(0, args.warmup), timeout=3600)
+    v = r["value"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["seconds_per_pass"] * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "complex128",
+        "data": "synthetic", "config": workload_config(cfg),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+                         "sample": r["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "llr_gbit_s": v * cfg.U * cfg.qam_bits / 1e9,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, frames=None):
+    d = {"workload": f"{cfg.name}: {cfg.kind} B={cfg.B} U={cfg.U} {cfg.tracker} K={cfg.K} "
+                     f"{1 << cfg.qam_bits}-QAM SNR={cfg.snr_db}dB, {cfg.n_sc} subcarriers x "
+                     f"{cfg.S} vectors sharing H",
+         "B": cfg.B, "U": cfg.U, "S": cfg.S, "n_sc_per_gpu": cfg.n_sc, "K": cfg.K,
+         "tracker": cfg.tracker, "qam_bits": cfg.qam_bits, "snr_db": cfg.snr_db,
+         "vectors_per_step_per_gpu": cfg.vectors, "parallelism": "subcarrier shards"}
+    if frames is not None:
+        d["l2"] = (f"inputs larger than L2: steps rotate over {frames['n']} frames, "
+                   f"{frames['bytes'] / 1e6:.0f} MB of H+Y in total (> 126 MB L2)")
+    return d
+
+
+def ours_arm(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1404_0424_b200 import Context, get_config
+
+    cfg = get_config(args.config)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ctx = Context(local_rank)
+    stream = torch.cuda.current_stream(dev)
+    # ---------------------------------------------------------------- frames
+    frame_bytes = cfg.n_sc * (cfg.B * cfg.U + cfg.S * cfg.B) * 8
+    n_frames = max(3, int(np.ceil(3 * 126e6 / frame_bytes)))
+    frames = []
+    rs = cfg.rsqrt()
+    rs = None if rs is None else torch.tensor(rs)
+    for f in range(n_frames):
+        sc0 = (rank * n_frames + f) * cfg.n_sc
+        if cfg.kind == "downlink":
+            Hd, T = ctx.generate_downlink(cfg.B, cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits, sc0=sc0)
+            frames.append((Hd, T))
+        else:
+            H, Y = ctx.generate_uplink(cfg.B, cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits, cfg.n0,
+                                       sc0=sc0, rsqrt=rs)
+            T = (ctx.generate_symbols(cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits, sc0=sc0)
+                 if cfg.kind == "both" else None)
+            frames.append((H, Y, T))
+    torch.cuda.synchronize()
+    out = {}
+
+    def step(i):
+        fr = frames[i % n_frames]
+        if cfg.kind == "downlink":
+            ctx.precode_cg(fr[0], fr[1], cfg.rho_d, cfg.K, out=out)
+        elif cfg.kind == "both":
+            ctx.detect_precode_cg(fr[0], fr[1], cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                                  cfg.tracker, fr[2], cfg.rho_d, cfg.K, out=out)
+        else:
+            ctx.detect_cg(fr[0], fr[1], cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                          cfg.tracker, out=out)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # --------------------------------------------------------- device timing
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    l0 = ctx.kernel_launches
+    with ClockSampler(local_rank) as clk:
+        evs[0].record(stream)
+        for i in range(args.steps):
+            step(args.warmup + i)
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches = ctx.kernel_launches - l0
+    per_step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    total_ms = max_over_ranks(evs[0].elapsed_time(evs[-1]))
+    value = world * cfg.vectors * args.steps / (total_ms / 1e3)
+    kernel_ms = sum(per_step_ms) / len(per_step_ms)  # one fused kernel launch per step
+
+    # ------------------------------------------------------------ e2e (host)
+    def pinned(shape, dtype):
+        return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
+
+    h_frames = []
+    for fr in frames[: min(2, n_frames)]:
+        hf = []
+        for t in fr:
+            if t is None:
+                hf.append(None)
+                continue
+            a = pinned(tuple(t.shape), torch.complex64)
+            a[...] = t.cpu().numpy()
+            hf.append(a)
+        h_frames.append(hf)
+    S, U, B, bits = cfg.S, cfg.U, cfg.B, cfg.qam_bits
+    if cfg.kind == "downlink":
+        h_out = {"q": pinned((cfg.n_sc, S, B), torch.complex64),
+                 "s": pinned((cfg.n_sc, S, B), torch.complex64),
+                 "gain": pinned((cfg.n_sc, S), torch.float32),
+                 "status": pinned((cfg.n_sc, S), torch.uint8)}
+    else:
+        h_out = {"xhat": pinned((cfg.n_sc, S, U), torch.complex64),
+                 "mu": pinned((cfg.n_sc, S, U), torch.float32),
+                 "rho": pinned((cfg.n_sc, S, U), torch.float32),
+                 "llr": pinned((cfg.n_sc, S, U, bits), torch.float32),
+                 "status": pinned((cfg.n_sc, S), torch.uint8)}
+        if cfg.kind == "both":
+            h_out.update({"q": pinned((cfg.n_sc, S, B), torch.complex64),
+                          "s": pinned((cfg.n_sc, S, B), torch.complex64),
+                          "gain": pinned((cfg.n_sc, S), torch.float32),
+                          "pstatus": pinned((cfg.n_sc, S), torch.uint8)})
+    h2d = sum(a.nbytes for a in h_frames[0] if a is not None)
+    d2h = sum(a.nbytes for a in h_out.values())
+
+    def e2e_step(i):
+        fr = h_frames[i % len(h_frames)]
+        if cfg.kind == "downlink":
+            ctx.precode_cg(fr[0], fr[1], cfg.rho_d, cfg.K, out=h_out)
+        elif cfg.kind == "both":
+            ctx.detect_precode_cg(fr[0], fr[1], cfg.rho_u, cfg.n0, cfg.es, bits, cfg.K,
+                                  cfg.tracker, fr[2], cfg.rho_d, cfg.K, out=h_out)
+        else:
+            ctx.detect_cg(fr[0], fr[1], cfg.rho_u, cfg.n0, cfg.es, bits, cfg.K, cfg.tracker,
+                          out=h_out)
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        e2e_step(i)
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    barrier()
+    e2e_value = world * cfg.vectors * args.steps / e2e_s
+
+    # ---------------------------------------------------- gather (N > 1 only)
+    gather = None
+    if world > 1 and "llr" in out:
+        from paper_1404_0424_b200.parallel import gather_to_root
+
+        llr = out["llr"].reshape(-1)
+        gather_to_root(llr, world, rank)  # warm
+        torch.cuda.synchronize()
+        barrier()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        reps = 5
+        for _ in range(reps):
+            gather_to_root(llr, world, rank)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = max_over_ranks(g0.elapsed_time(g1) / reps)
+        gather = {"what": "LLRs of every rank's step to rank 0 (NCCL)", "ms": gms,
+                  "bytes_to_root": llr.numel() * 4 * (world - 1)}
+
+    # -------------------------------------------------------------- roofline
+    peaks = load_peaks()
+    fp32_peak = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12  # TFLOP/s
+    flops_launch = cfg.flops_per_vector() * cfg.vectors
+    bytes_launch = cfg.bytes_per_vector() * cfg.vectors
+    t_fp32 = flops_launch / (fp32_peak * 1e12)
+    t_hbm = bytes_launch / (peaks["hbm_gbs"] * 1e9)
+    k_s = kernel_ms / 1e3
+    traffic = read_traffic(cfg.name)
+    if t_fp32 >= t_hbm:
+        roof = {"bound": "fp32", "achieved": flops_launch / k_s / 1e12, "peak": fp32_peak,
+                "unit": "TFLOP/s",
+                "peak_source": f"derived: 148 SMs x 128 FP32 lanes x 2 x {peaks['sm_max_mhz']:.0f} MHz "
+                               f"(sm_max_mhz from {peaks['source']}; no measured FP32 figure exists)"}
+    else:
+        roof = {"bound": "hbm", "achieved": bytes_launch / k_s / 1e9, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "peak_source": f"hbm_gbs of {peaks['source']}"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = traffic
+    roof["algorithmic_per_launch"] = {"flops": flops_launch, "bytes": bytes_launch,
+                                      "flops_per_vector": cfg.flops_per_vector(),
+                                      "bytes_per_vector": cfg.bytes_per_vector()}
+    roof["hbm_achieved_gbs"] = bytes_launch / k_s / 1e9
+    roof["kernel"] = "cgm::subcarrier_kernel (fused Gram+MF+CG+SINR+LLR)"
+    roof["kernel_ms"] = kernel_ms
+
+    # ----------------------------------------------------------- CPU baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            import oracle.cpu_bench as cb
+
+            r = cb.spawn(cfg.name, cfg.n_sc if cfg.vectors <= 20000 else max(1, 20000 // cfg.S),
+                         os.cpu_count() or 1, passes=3, warmup=2)
+            cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+                   "sample": r["sample"]}
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {e}"[:300]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "complex64", "data": "synthetic",
+            "config": workload_config(cfg, {"n": n_frames, "bytes": n_frames * frame_bytes}),
+            "llr_gbit_s": value * cfg.U * cfg.qam_bits / 1e9 if cfg.kind != "downlink" else None,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        if gather:
+            line["gather"] = gather
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        if args.impl == "reference":
+            reference_arm(args, rank, world)
+        else:
+            ours_arm(args, rank, world, local_rank)
+    finally:
+        if world > 1 and args.impl == "ours":
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -48,6 +48,37 @@ class Config:
     def vectors(self) -> int:
         return self.n_sc * self.S
 
+    # ---- algorithmic counts of SURVEY.md section 8(d) (complex MAC = 8 flops,
+    # Hermitian products on one triangle, each input read once / output
+    # written once; intermediates not credited)
+    def flops_per_vector(self) -> float:
+        B, U, K, S = self.B, self.U, self.K, self.S
+        M = 1 << self.qam_bits
+        f = 0.0
+        if self.kind in ("uplink", "both"):
+            f += 4 * B * U * (U + 1) / S                    # Gram, shared by S vectors
+            f += 8 * B * U                                  # matched filter
+            f += K * (8 * U * U + 20 * U) + 4 * U           # CG
+            if self.tracker == "exact":
+                f += (K - 1) * 4 * U * (U + 1) * (U + 2) + 4 * U * U * (U + 1) + 8 * U * U
+            else:
+                f += (K - 1) * 6 * U + 2 * U
+            f += U * (4 + self.qam_bits * (3 * np.sqrt(M) + 3))  # LLR
+        if self.kind == "downlink":
+            f += 4 * B * U * (U + 1) / S
+        if self.kind in ("downlink", "both"):
+            f += K * (8 * U * U + 20 * U) + 4 * U + 8 * B * U + 4 * B
+        return f
+
+    def bytes_per_vector(self) -> float:
+        B, U, S = self.B, self.U, self.S
+        b = 8 * B * U / S                                   # channel, shared by S vectors
+        if self.kind in ("uplink", "both"):
+            b += 8 * B + 8 * U + 4 * U + 4 * U + 4 * U * self.qam_bits
+        if self.kind in ("downlink", "both"):
+            b += 8 * U + 8 * B + 4
+        return b
+
     def scaled(self, n_sc: int) -> "Config":
         return replace(self, n_sc=n_sc)
 
