@@ -10,7 +10,8 @@
  * Layouts (complex64 = interleaved float re,im; all arrays dense, row-major):
  *   H  uplink   [n_sc][B][U]   element (b,u) at b*U+u   (reference linalg.hpp:28)
  *   Hd downlink [n_sc][U][B]   element (u,b) at u*B+b   (precode.hpp:31, H_d is U x B)
- *   Y  [n_sc][S][B]            the S received vectors that share channel sc
+ *   Y  [n_sc][B][S]            antenna-major: column s of the B x S matrix is the
+ *                              s-th received vector sharing channel sc
  *   T  [n_sc][S][U]            the S transmit-symbol vectors t of channel sc
  *   xhat [n_sc][S][U] complex64, mu / rho [n_sc][S][U] float,
  *   llr  [n_sc][S][U][qam_bits] float (I-axis bits MSB first, then Q-axis bits),
@@ -65,6 +66,10 @@ int cgm_ctx_destroy(cgm_ctx* ctx);
 /* stream = cudaStream_t (0 = legacy default stream) */
 int cgm_ctx_set_stream(cgm_ctx* ctx, void* stream);
 int cgm_synchronize(cgm_ctx* ctx);
+/* 0 (default): the split path (channel kernel + solve kernel per L2-sized
+ * chunk of subcarriers); 1: the single fused per-subcarrier kernel (A/B
+ * testing).  Both are parity-tested. */
+int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy);
 const char* cgm_last_error(const cgm_ctx* ctx);
 /* kernels this context has launched since creation (the bench's gpu_launches) */
 long cgm_kernel_launches(const cgm_ctx* ctx);

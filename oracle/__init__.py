@@ -75,13 +75,14 @@ class Oracle:
     # ------------------------------------------------------------ detection
     def detect(self, H, Y, rho_u, n0, es, qam_bits, K=1, tracker="approx", method="cg",
                threads=1):
-        """H: (n_sc, B, U) complex; Y: (n_sc, S, B) complex. Returns dict of arrays
-        shaped (n_sc, S, U[, bits])."""
+        """H: (n_sc, B, U) complex; Y: (n_sc, B, S) complex (antenna-major, the
+        product's batch layout; the S columns are the received vectors).
+        Returns dict of arrays shaped (n_sc, S, U[, bits])."""
         H = _c128(H)
-        Y = _c128(Y)
         n_sc, B, U = H.shape
-        S = Y.shape[1]
-        assert Y.shape == (n_sc, S, B), (Y.shape, H.shape)
+        assert Y.shape[:2] == (n_sc, B), (Y.shape, H.shape)
+        S = Y.shape[2]
+        Y = _c128(np.transpose(Y, (0, 2, 1)))  # per-vector rows for the C entry points
         xhat = np.zeros((n_sc, S, U), np.complex128)
         mu = np.zeros((n_sc, S, U))
         rho = np.zeros((n_sc, S, U))

@@ -45,8 +45,8 @@ def synth(cfg, n_sc, seed=7):
         return dict(Hd=Hd, T=T)
     H = cn((n_sc, cfg.B, cfg.U)).astype(np.complex64)
     X = pts[rng.integers(0, 1 << cfg.qam_bits, (n_sc, cfg.S, cfg.U))]
-    Y = (np.einsum("nbu,nsu->nsb", H.astype(np.complex128), X)
-         + cn((n_sc, cfg.S, cfg.B), cfg.n0)).astype(np.complex64)
+    Y = (np.einsum("nbu,nsu->nbs", H.astype(np.complex128), X)
+         + cn((n_sc, cfg.B, cfg.S), cfg.n0)).astype(np.complex64)
     out = dict(H=H, Y=Y)
     if cfg.kind == "both":
         out["T"] = pts[rng.integers(0, 1 << cfg.qam_bits, (n_sc, cfg.S, cfg.U))].astype(np.complex64)

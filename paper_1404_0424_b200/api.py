@@ -4,8 +4,9 @@ Same names, argument meaning and error behaviour as the reference's
 ``cgmimo::detect::detect_cg`` (detect.hpp:58-61) and
 ``cgmimo::precode::precode_cg`` (precode.hpp:31-33), batched:
 
-* ``H`` uplink ``(n_sc, B, U)`` complex64, ``Y`` ``(n_sc, S, B)`` complex64
-  (S received vectors share channel ``sc``); downlink ``Hd`` ``(n_sc, U, B)``,
+* ``H`` uplink ``(n_sc, B, U)`` complex64, ``Y`` ``(n_sc, B, S)`` complex64
+  (antenna-major: column s is the s-th received vector sharing channel
+  ``sc``); downlink ``Hd`` ``(n_sc, U, B)``,
   ``T`` ``(n_sc, S, U)``.
 * numpy arrays are HOST buffers (synchronous call, copies pipelined inside the
   C ABI); torch CUDA tensors are DEVICE buffers (asynchronous on the current
@@ -88,6 +89,11 @@ class Context:
 
         self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
 
+    def set_kernel_policy(self, policy: str):
+        """"auto" (split channel + solve kernels, production) or "generic"
+        (single fused per-subcarrier kernel)."""
+        self._check(self.lib.cgm_ctx_set_kernel_policy(self.h, {"auto": 0, "generic": 1}[policy]))
+
     def synchronize(self):
         self._check(self.lib.cgm_synchronize(self.h))
 
@@ -101,9 +107,9 @@ class Context:
         """Batched detect_cg.  Returns dict with the requested outputs."""
         device = _is_torch(H)
         n_sc, B, U = H.shape
-        if Y.shape[0] != n_sc or Y.shape[2] != B:
+        if Y.ndim != 3 or Y.shape[0] != n_sc or Y.shape[1] != B:
             raise ValueError("detect_cg: dimension mismatch")
-        S = Y.shape[1]
+        S = Y.shape[2]
         if tracker not in TRACKERS:
             raise ValueError(f"unknown tracker {tracker!r}")
         out = dict(out or {})
@@ -162,7 +168,9 @@ class Context:
         """Uplink detection + downlink precoding on the same channels, one pass."""
         device = _is_torch(H)
         n_sc, B, U = H.shape
-        S, St = Y.shape[1], T.shape[1]
+        if Y.ndim != 3 or Y.shape[:2] != (n_sc, B) or T.shape[0] != n_sc or T.shape[2] != U:
+            raise ValueError("detect_precode_cg: dimension mismatch")
+        S, St = Y.shape[2], T.shape[1]
         out = dict(out or {})
         shapes = {"xhat": ((n_sc, S, U), "c64"), "mu": ((n_sc, S, U), "f32"),
                   "rho": ((n_sc, S, U), "f32"), "llr": ((n_sc, S, U, qam_bits), "f32"),
@@ -189,12 +197,12 @@ class Context:
     # ---------------------------------------------------------- generators
     def generate_uplink(self, B, U, n_sc, S, seed, qam_bits, n0, sc0=0, labels=False,
                         rsqrt=None):
-        """Seeded device inputs (torch CUDA tensors): H (n_sc,B,U), Y (n_sc,S,B)."""
+        """Seeded device inputs (torch CUDA tensors): H (n_sc,B,U), Y (n_sc,B,S)."""
         import torch
 
         dev = torch.device("cuda", self.device)
         H = torch.empty((n_sc, B, U), dtype=torch.complex64, device=dev)
-        Y = torch.empty((n_sc, S, B), dtype=torch.complex64, device=dev)
+        Y = torch.empty((n_sc, B, S), dtype=torch.complex64, device=dev)
         L = torch.empty((n_sc, S, U), dtype=torch.uint8, device=dev) if labels else None
         self._bind_torch_stream()
         if rsqrt is None:
@@ -287,7 +295,7 @@ def detect_cg_single(h, y, rho_u, n0, es, qam_bits, iters, tracker="exact"):
     if h.ndim != 2 or y.ndim != 1 or h.shape[0] != y.shape[0]:
         raise ValueError("detect_cg: dimension mismatch")
     H = np.ascontiguousarray(h, dtype=np.complex64)[None]
-    Yb = np.ascontiguousarray(y, dtype=np.complex64)[None, None]
+    Yb = np.ascontiguousarray(y, dtype=np.complex64)[None, :, None]
     o = detect_cg(H, Yb, rho_u, n0, es, qam_bits, iters, tracker)
     if o["status"][0, 0] & 1:
         raise SolverBreakdown("cg_solve: non-positive curvature p^H A p")

@@ -9,12 +9,13 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/cgmimo_b200.h"
-#include "cgm_kernels.cuh"
+#include "cgm_split.cuh"
 
 struct cgm_ctx {
   int device = 0;
@@ -28,6 +29,7 @@ struct cgm_ctx {
   float* tscratch = nullptr;
   size_t tscratch_bytes = 0;
   long launches = 0;
+  int policy = 0;  // 0 split K1+K2 path (production), 1 single fused kernel (A/B)
   std::string err;
 };
 
@@ -66,6 +68,8 @@ cgm::AxisTables make_axis_tables() {
     const unsigned levels = 1u << half;
     const double scale = 1.0 / std::sqrt(2.0 * ((double)levels * levels - 1.0) / 3.0);
     int n0[3] = {0, 0, 0}, n1[3] = {0, 0, 0};
+    for (unsigned k = 0; k < levels; ++k)
+      t.lv[q][k] = static_cast<float>((2.0 * k - (levels - 1.0)) * scale);
     for (unsigned g = 0; g < levels; ++g) {
       const double amp = (2.0 * gray_decode(g) - (levels - 1.0)) * scale;
       for (int p = 0; p < half; ++p) {
@@ -85,33 +89,28 @@ struct Launch {
   int t_in_smem = 1;
 };
 
-template <int UP, int NT>
+template <int UP, int NT, bool EXACT>
 int plan_and_launch(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
-  cgm::GramPlan<UP, NT> gp;
-  gp.plan(p.B, p.S);
-  cgm::ChebPlan<UP, NT> cp;
-  cp.plan();
-  const int red = std::max(gp.red_floats(), cp.red_floats());
   const int Kmax = std::max(p.K, p.Kt);
   cgm::Smem<UP> L;
   p.t_in_smem = 1;
-  L.plan(p.B, p.S, p.St, Kmax, p.exact, 1, red, NT / 32);
+  L.plan(p.B, p.S, p.St, Kmax, EXACT, 1);
   if (L.total > ctx->max_smem) {
     p.t_in_smem = 0;
-    L.plan(p.B, p.S, p.St, Kmax, p.exact, 0, red, NT / 32);
+    L.plan(p.B, p.S, p.St, Kmax, EXACT, 0);
   }
   if (L.total > ctx->max_smem)
     return fail(ctx, CGM_EINVAL,
                 "per-subcarrier working set %d B exceeds shared memory (%d B): reduce B or S",
                 L.total, ctx->max_smem);
-  auto kern = cgm::subcarrier_kernel<UP, NT>;
+  auto kern = cgm::subcarrier_kernel<UP, NT, EXACT>;
   CGM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total));
   int occ = 0;
   CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, L.total));
   if (occ < 1) return fail(ctx, CGM_EINVAL, "kernel does not fit on an SM (smem %d)", L.total);
   long grid = std::min<long>(p.n_sc, static_cast<long>(occ) * ctx->sms);
   if (grid < 1) grid = 1;
-  if (p.exact && !p.t_in_smem) {
+  if (EXACT && !p.t_in_smem) {
     const size_t need = static_cast<size_t>(grid) * Kmax * UP * UP * sizeof(float2);
     if (need > ctx->tscratch_bytes) {
       if (ctx->tscratch) cudaFree(ctx->tscratch);
@@ -128,16 +127,95 @@ int plan_and_launch(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
   return CGM_OK;
 }
 
-int launch(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
+// Split path (cgm_split.cuh): K1 channel kernel + K2 solve kernel per chunk
+// of subcarriers; the chunk is sized so the K1->K2 workspace (and the H that
+// the precoder re-reads) stays resident in the 126 MB L2.
+template <int UP, int NT1, bool EXACT>
+int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
+  const int Kmax = std::max(p.K, p.Kt);
+  cgm::K1Smem<UP> L1;
+  L1.plan(p.B, p.S, EXACT);
+  cgm::K2Smem<UP> L2;
+  L2.plan(p.B, p.S, p.St, Kmax, EXACT);
+  if (L1.total > ctx->max_smem || L2.total > ctx->max_smem)
+    return fail(ctx, CGM_EINVAL,
+                "per-subcarrier working set (%d / %d B) exceeds shared memory (%d B)", L1.total,
+                L2.total, ctx->max_smem);
+  cgm::WsOffsets W;
+  W.plan(UP, p.S, p.K, EXACT);
+  auto k1 = cgm::channel_kernel<UP, NT1, EXACT>;
+  auto k2 = cgm::solve_kernel<UP, EXACT>;
+  CGM_CUDA(ctx, cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, L1.total));
+  CGM_CUDA(ctx, cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, L2.total));
+  int occ1 = 0;
+  CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k1, NT1, L1.total));
+  if (occ1 < 1) return fail(ctx, CGM_EINVAL, "channel kernel does not fit on an SM");
+  // K2 block: enough lane groups for every system at once (>= UP threads
+  // for the exact extraction), at most 8 warps
+  using GE = cgm::K2Geo<UP>;
+  const int nsys = p.S + p.St;
+  int nw2 = (nsys + GE::GPW * GE::NS - 1) / (GE::GPW * GE::NS);
+  if (EXACT) nw2 = std::max(nw2, std::max(4, UP / 32));
+  nw2 = std::max(1, std::min(8, nw2));
+  // chunk so that workspace + channel (+ Y) of a chunk fit comfortably in L2
+  const size_t per_sc = static_cast<size_t>(W.stride) * 8 + static_cast<size_t>(p.B) * p.U * 8 +
+                        static_cast<size_t>(p.B) * p.S * 8;
+  long chunk = static_cast<long>((80ull << 20) / std::max<size_t>(per_sc, 1));
+  chunk = std::max<long>(chunk, static_cast<long>(ctx->sms) * occ1);
+  chunk = std::min(chunk, p.n_sc);
+  const size_t ws_need = static_cast<size_t>(chunk) * W.stride * sizeof(float2);
+  if (ws_need > ctx->tscratch_bytes) {
+    if (ctx->tscratch) cudaFree(ctx->tscratch);
+    ctx->tscratch = nullptr;
+    ctx->tscratch_bytes = 0;
+    CGM_CUDA(ctx, cudaMalloc(&ctx->tscratch, ws_need));
+    ctx->tscratch_bytes = ws_need;
+  }
+  p.ws = reinterpret_cast<float2*>(ctx->tscratch);
+  const long total = p.n_sc;
+  for (long c0 = 0; c0 < total; c0 += chunk) {
+    const long n = std::min(chunk, total - c0);
+    p.sc_base = c0;
+    p.n_sc = n;
+    const long g1 = std::max<long>(1, std::min<long>(n, static_cast<long>(occ1) * ctx->sms));
+    k1<<<static_cast<unsigned>(g1), NT1, L1.total, st>>>(p);
+    CGM_CUDA(ctx, cudaGetLastError());
+    k2<<<static_cast<unsigned>(n), 32 * nw2, L2.total, st>>>(p);
+    CGM_CUDA(ctx, cudaGetLastError());
+    ctx->launches += 2;
+  }
+  return CGM_OK;
+}
+
+template <int UP, int NT1>
+int dispatch_split(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
+  return exact ? launch_split<UP, NT1, true>(ctx, p, st) : launch_split<UP, NT1, false>(ctx, p, st);
+}
+
+template <int UP, int NT>
+int dispatch_exact(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
+  return exact ? plan_and_launch<UP, NT, true>(ctx, p, st)
+               : plan_and_launch<UP, NT, false>(ctx, p, st);
+}
+
+int launch(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
   if (p.n_sc <= 0) return CGM_OK;
   const int UP = up_of(p.U);
   const uintptr_t a = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
   p.use_tma = (!p.hd_layout && p.U == UP && (p.B % 2) == 0 && (a & 15u) == 0) ? 1 : 0;
+  if (ctx->policy == 0) {
+    switch (UP) {
+      case 8: return dispatch_split<8, 128>(ctx, p, exact, st);
+      case 16: return dispatch_split<16, 128>(ctx, p, exact, st);
+      case 32: return dispatch_split<32, 288>(ctx, p, exact, st);
+      default: return dispatch_split<64, 320>(ctx, p, exact, st);
+    }
+  }
   switch (UP) {
-    case 8: return plan_and_launch<8, 128>(ctx, p, st);
-    case 16: return plan_and_launch<16, 128>(ctx, p, st);
-    case 32: return plan_and_launch<32, 256>(ctx, p, st);
-    default: return plan_and_launch<64, 256>(ctx, p, st);
+    case 8: return dispatch_exact<8, 128>(ctx, p, exact, st);
+    case 16: return dispatch_exact<16, 128>(ctx, p, exact, st);
+    case 32: return dispatch_exact<32, 288>(ctx, p, exact, st);
+    default: return dispatch_exact<64, 320>(ctx, p, exact, st);
   }
 }
 
@@ -207,18 +285,19 @@ cgm::KernelParams params_of(const Job& j, long n_sc) {
   p.Kt = j.St > 0 ? j.Kt : 0;
   p.bits = j.bits > 0 ? j.bits : 2;
   p.hd_layout = j.hd_layout ? 1 : 0;
-  p.exact = (j.S > 0 && j.tracker == CGM_TRACKER_EXACT) ? 1 : 0;
   p.rho_inv_u = j.S > 0 ? static_cast<float>(1.0 / j.rho_u) : 0.f;
   p.rho_inv_d = j.St > 0 ? static_cast<float>(1.0 / j.rho_d) : 0.f;
   p.n0 = static_cast<float>(j.n0);
+  if (const char* dbg = std::getenv("CGMIMO_DEBUG_WS")) p.debug = std::atoi(dbg);
   p.es = static_cast<float>(j.es);
   return p;
 }
 
+bool is_exact(const Job& j) { return j.S > 0 && j.tracker == CGM_TRACKER_EXACT; }
+
 // Per-subcarrier byte counts of each array (host pipeline).
 struct Sizes {
   size_t h, y, t, xhat, mu, rho, llr, st, q, s, gain, pst;
-  size_t in() const { return h + y + t; }
   size_t total() const { return h + y + t + xhat + mu + rho + llr + st + q + s + gain + pst; }
 };
 
@@ -248,7 +327,7 @@ int run_job(cgm_ctx* ctx, const Job& j, unsigned flags) {
   if (j.n_sc == 0) return CGM_OK;
   if (flags & CGM_DEVICE_POINTERS) {
     cgm::KernelParams p = params_of(j, j.n_sc);
-    return launch(ctx, p, ctx->user_stream);
+    return launch(ctx, p, is_exact(j), ctx->user_stream);
   }
   // ---------------- host buffers: chunked, double-buffered pipeline
   const Sizes z = sizes_of(j);
@@ -314,7 +393,7 @@ int run_job(cgm_ctx* ctx, const Job& j, unsigned flags) {
     jd.gain = reinterpret_cast<float*>(dG);
     jd.pstatus = reinterpret_cast<uint8_t*>(dPs);
     cgm::KernelParams p = params_of(jd, n);
-    rc = launch(ctx, p, st);
+    rc = launch(ctx, p, is_exact(j), st);
     if (rc) return rc;
     auto d2h = [&](void* host, const char* dev, size_t per) -> cudaError_t {
       if (!per) return cudaSuccess;
@@ -399,6 +478,12 @@ int cgm_ctx_destroy(cgm_ctx* ctx) {
 int cgm_ctx_set_stream(cgm_ctx* ctx, void* stream) {
   if (!ctx) return CGM_EINVAL;
   ctx->user_stream = static_cast<cudaStream_t>(stream);
+  return CGM_OK;
+}
+
+int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy) {
+  if (!ctx || policy < 0 || policy > 1) return CGM_EINVAL;
+  ctx->policy = policy;
   return CGM_OK;
 }
 

@@ -70,6 +70,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   } while (!done);
 }
 
+// Plain arrive (release at CTA scope): the consumer-side "slot free" /
+// "data ready" signal of the producer/consumer rings.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Named barrier over a subset of warps (ids 1..15; 0 is __syncthreads).
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // One bulk global->shared copy (bytes % 16 == 0, both addresses 16B aligned)
 // completing on `bar`.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -121,6 +132,34 @@ __device__ __forceinline__ void tile4x4(float2 (&acc)[4][4], const float2* __res
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) cfma_conj(acc[r][c], x[r], y[c]);
+  }
+}
+
+// acc[r][c] += sum_k conj(X[k*ldx + i0 + r]) * Z[k*ldz + j0 + c], r, c < 2.
+// X rows 16B aligned; Z rows 16B aligned when Z_VEC (else 2 scalar loads,
+// columns >= jmax clamped).  Neighbouring lanes share either the X or the Z
+// pair, so the loads are broadcasts or contiguous (no bank conflicts).
+template <bool Z_VEC>
+__device__ __forceinline__ void tile2x2(float2 (&acc)[2][2], const float2* __restrict__ X, int ldx,
+                                        int i0, const float2* __restrict__ Z, int ldz, int j0,
+                                        int jmax, int k0, int k1) {
+  const int j1 = min(j0 + 1, jmax - 1);
+#pragma unroll 4
+  for (int k = k0; k < k1; ++k) {
+    const float4 xa = *reinterpret_cast<const float4*>(X + k * ldx + i0);
+    float4 za;
+    if (Z_VEC) {
+      za = *reinterpret_cast<const float4*>(Z + k * ldz + j0);
+    } else {
+      const float2 z0 = Z[k * ldz + j0], z1 = Z[k * ldz + j1];
+      za = make_float4(z0.x, z0.y, z1.x, z1.y);
+    }
+    const float2 x0 = make_float2(xa.x, xa.y), x1 = make_float2(xa.z, xa.w);
+    const float2 y0 = make_float2(za.x, za.y), y1 = make_float2(za.z, za.w);
+    cfma_conj(acc[0][0], x0, y0);
+    cfma_conj(acc[0][1], x0, y1);
+    cfma_conj(acc[1][0], x1, y0);
+    cfma_conj(acc[1][1], x1, y1);
   }
 }
 

@@ -125,7 +125,9 @@ __global__ void gen_received(float2* Y, const float2* H, int B, int U, long sc0,
         im += static_cast<double>(hv.x) * xs[u].y + static_cast<double>(hv.y) * xs[u].x;
       }
       const double2 nz = gauss_pair(nk, static_cast<uint64_t>(b), sqrt(0.5 * n0));
-      Y[inst * B + b] = make_float2(static_cast<float>(re + nz.x), static_cast<float>(im + nz.y));
+      // antenna-major batch layout: Y[sc][b][s]
+      Y[(sc * B + b) * S + (inst - sc * S)] =
+          make_float2(static_cast<float>(re + nz.x), static_cast<float>(im + nz.y));
     }
     __syncthreads();
   }

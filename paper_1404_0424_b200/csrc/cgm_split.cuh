@@ -1,0 +1,706 @@
+// cgm_split.cuh -- the production path: two kernels per chunk of subcarriers.
+//
+//   K1 channel_kernel  (one CTA per subcarrier, persistent grid-stride)
+//      TMA-stage H and Y, form G = H^H H (lower 4x4 tiles + mirror) and the
+//      matched filter H^H Y in register tiles with shuffle-reduced split-K,
+//      and for the exact tracker the Chebyshev basis T_1..T_K of
+//      Ahat = (A - cI)/d (K-1 Hermitian products).  Writes them to a
+//      workspace sized to stay L2-resident for K2.
+//        replaces gram_regularized (linalg.cpp:59-101), matvec_adjoint
+//        (linalg.cpp:116-126) and the U^3 part of ExactSinrTracker::step
+//        (detect.cpp:336-368, see cgm_kernels.cuh for the basis argument)
+//   K2 solve_kernel    (one CTA per subcarrier, many CTAs per SM)
+//      one lane group per system (uplink vector or downlink t): K CG
+//      iterations on G + rho^-1 I (solvers.cpp:37-72) with the approximate
+//      tracker (detect.cpp:397-441) or the exact one's coefficient recursion
+//      + extraction from the basis (detect.cpp:330-395), max-log LLRs
+//      (detect.cpp:57-86), and the precoder's q = H_d^H v, gain, s
+//      (precode.cpp:22-71).
+//
+// The split keeps both kernels at high occupancy: K1 is FFMA/tile bound,
+// K2 is latency bound (short dependent CG chains) and needs many resident
+// warps -- fusing them into one CTA serialises the two regimes.
+#pragma once
+
+#include "cgm_kernels.cuh"
+
+namespace cgm {
+
+// workspace layout per subcarrier (float2 units)
+struct WsOffsets {
+  int g, mf, cd, t, stride;
+  __host__ __device__ void plan(int UP, int S, int K, bool exact) {
+    g = 0;
+    mf = UP * UP;
+    cd = mf + S * UP;
+    t = cd + 2;
+    stride = t + (exact ? K * UP * UP : 0);
+    stride = (stride + 1) & ~1;
+  }
+};
+
+template <int UP>
+struct K1Smem {
+  int bar, hs, ys, gs, tb, misc, total;
+  __host__ __device__ static int align(int x) { return (x + 127) & ~127; }
+  __host__ __device__ void plan(int B, int S, bool exact) {
+    int o = 0;
+    bar = o; o = align(o + 16);
+    hs = o; o = align(o + B * UP * 8);
+    ys = o; o = align(o + B * S * 8 + 64);
+    gs = o; o = align(o + UP * UP * 8);
+    tb = o; o = align(o + (exact ? 2 * UP * UP * 8 : 0));  // T_1 and T_m
+    misc = o; o = align(o + 16);
+    total = o;
+  }
+};
+
+template <int UP, int NT, bool EXACT>
+__global__ void __launch_bounds__(NT) channel_kernel(const KernelParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  K1Smem<UP> L;
+  L.plan(p.B, p.S, EXACT);
+  WsOffsets W;
+  W.plan(UP, p.S, p.K, EXACT);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  float2* Hs = reinterpret_cast<float2*>(smem + L.hs);
+  float2* Ys = reinterpret_cast<float2*>(smem + L.ys);
+  float2* Gs = reinterpret_cast<float2*>(smem + L.gs);
+  float2* T1 = reinterpret_cast<float2*>(smem + L.tb);
+  float2* Tm = T1 + UP * UP;
+  float* misc = reinterpret_cast<float*>(smem + L.misc);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int B = p.B, S = p.S, U = p.U;
+  const int nb = UP / 4, n_gram = nb * (nb + 1) / 2, nsb = (S + 3) / 4;
+
+  if (p.use_tma && tid == 0) mbar_init(bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  for (long lsc = blockIdx.x; lsc < p.n_sc; lsc += gridDim.x, phase ^= 1u) {
+    const long sc = p.sc_base + lsc;
+    float2* ws = p.ws + lsc * W.stride;
+    // ---------------------------------------------------------- stage H, Y
+    if (p.use_tma) {
+      if (tid == 0) {
+        const uint32_t hbytes = static_cast<uint32_t>(B) * UP * 8u;
+        const uint32_t ybytes = static_cast<uint32_t>(B) * S * 8u;
+        fence_proxy_async();
+        mbar_expect_tx(bar, hbytes + ybytes);
+        bulk_g2s(Hs, p.H + sc * static_cast<long>(B) * UP, hbytes, bar);
+        if (S > 0) bulk_g2s(Ys, p.Y + sc * static_cast<long>(B) * S, ybytes, bar);
+      }
+      mbar_wait(bar, phase);
+    } else {
+      if (p.hd_layout) {
+        // downlink H_d [U][B] -> Hs[b][u] = conj(H_d[u][b])  (= H_u = H_d^H)
+        const float2* src = p.H + sc * static_cast<long>(U) * B;
+        for (int e = tid; e < UP * B; e += NT) {
+          const int u = e / B, b = e - u * B;
+          Hs[b * UP + u] = u < U ? cconj(src[u * B + b]) : make_float2(0.f, 0.f);
+        }
+      } else {
+        const float2* src = p.H + sc * static_cast<long>(B) * U;
+        for (int e = tid; e < UP * B; e += NT) {
+          const int b = e / UP, u = e - b * UP;
+          Hs[e] = u < U ? src[b * U + u] : make_float2(0.f, 0.f);
+        }
+      }
+      for (int e = tid; e < S * B; e += NT) Ys[e] = p.Y[sc * static_cast<long>(B) * S + e];
+      __syncthreads();
+    }
+    // ------------------------------------------- Gram + matched filter tiles
+    float2* MFw = ws + W.mf;
+    if (UP >= 32) {
+      // 2x2 register tiles, one per thread, no split-K: lower-triangle Gram
+      // blocks (row-major: lanes share X) then MF blocks (lanes share Z)
+      constexpr int nb2 = UP / 2;
+      const int n_g2 = nb2 * (nb2 + 1) / 2, nsb2 = (S + 1) / 2;
+      const int n_t2 = n_g2 + nb2 * nsb2;
+      for (int t = tid; t < n_t2; t += NT) {
+        float2 acc[2][2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) acc[r][c] = make_float2(0.f, 0.f);
+        if (t < n_g2) {
+          int ib, jb;
+          tri_block(t, ib, jb);
+          tile2x2<true>(acc, Hs, UP, ib * 2, Hs, UP, jb * 2, 1 << 30, 0, B);
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int i = ib * 2 + r, j = jb * 2 + c;
+              if (j < i) {
+                Gs[i * UP + j] = acc[r][c];
+                Gs[j * UP + i] = cconj(acc[r][c]);
+              } else if (j == i) {
+                Gs[i * UP + i] = make_float2(acc[r][c].x, 0.f);
+              }
+            }
+        } else {
+          const int m = t - n_g2;
+          const int jb = m / nb2, ib = m - jb * nb2;
+          if ((S & 1) == 0)
+            tile2x2<true>(acc, Hs, UP, ib * 2, Ys, S, jb * 2, S, 0, B);
+          else
+            tile2x2<false>(acc, Hs, UP, ib * 2, Ys, S, jb * 2, S, 0, B);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int s = jb * 2 + c;
+            if (s < S)
+              *reinterpret_cast<float4*>(MFw + s * UP + ib * 2) =
+                  make_float4(acc[0][c].x, acc[0][c].y, acc[1][c].x, acc[1][c].y);
+          }
+        }
+      }
+    } else {
+      tile_pass<NT>(n_gram, nb * nsb, nsb, Hs, UP, Hs, UP, Ys, S, S, B,
+                    [&](int tile, int ib, int jb, float2 (&acc)[4][4]) {
+                      if (tile < n_gram) {
+#pragma unroll
+                        for (int r = 0; r < 4; ++r)
+#pragma unroll
+                          for (int c = 0; c < 4; ++c) {
+                            const int i = ib * 4 + r, j = jb * 4 + c;
+                            if (j < i) {
+                              Gs[i * UP + j] = acc[r][c];
+                              Gs[j * UP + i] = cconj(acc[r][c]);
+                            } else if (j == i) {
+                              Gs[i * UP + i] = make_float2(acc[r][c].x, 0.f);
+                            }
+                          }
+                      } else {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                          const int s = jb * 4 + c;
+                          if (s < S) {
+                            float4* dst = reinterpret_cast<float4*>(MFw + s * UP + ib * 4);
+                            dst[0] = make_float4(acc[0][c].x, acc[0][c].y, acc[1][c].x, acc[1][c].y);
+                            dst[1] = make_float4(acc[2][c].x, acc[2][c].y, acc[3][c].x, acc[3][c].y);
+                          }
+                        }
+                      }
+                    });
+    }
+    __syncthreads();
+    {  // G -> workspace (coalesced)
+      const float4* src = reinterpret_cast<const float4*>(Gs);
+      float4* dst = reinterpret_cast<float4*>(ws + W.g);
+      for (int e = tid; e < UP * UP / 2; e += NT) dst[e] = src[e];
+    }
+    if (EXACT && S > 0) {
+      const int K = p.K;
+      if (warp == 0) {
+        // centre c = tr(A)/U and half-width d = 2 ||A - cI||_F / sqrt(U)
+        // (any d > 0 is exact algebra; this choice keeps the basis well
+        // conditioned in FP32)
+        float tr = 0.f, fr = 0.f;
+        for (int i = lane; i < UP; i += 32) tr += Gs[i * UP + i].x + p.rho_inv_u;
+        tr = group_sum<32>(tr);
+        const float c = tr / UP;
+        for (int e = lane; e < UP * UP; e += 32) {
+          float2 a = Gs[e];
+          if (e / UP == e % UP) a.x += p.rho_inv_u - c;
+          fr += cnorm(a);
+        }
+        fr = group_sum<32>(fr);
+        float d = 2.f * sqrtf(fr / UP);
+        if (!(d > 1e-6f * fmaxf(fabsf(c), 1e-30f))) d = fmaxf(fabsf(c), 1.f);
+        if (lane == 0) {
+          misc[0] = c;
+          misc[1] = d;
+          ws[W.cd] = make_float2(c, d);
+        }
+      }
+      __syncthreads();
+      const float cc = misc[0], invd = 1.f / misc[1];
+      float2* Tw = ws + W.t;
+      for (int e = tid; e < UP * UP; e += NT) {  // T_1 = (A - cI)/d
+        float2 a = Gs[e];
+        if (e / UP == e % UP) a.x += p.rho_inv_u - cc;
+        a = cscale(invd, a);
+        T1[e] = a;
+        Tm[e] = a;
+        Tw[e] = a;
+      }
+      __syncthreads();
+      // T_{m+1} = 2 T_1 T_m - T_{m-1} (lower tiles + mirror; T_{m-1} from L2)
+      for (int m = 1; m < K; ++m) {
+        const float2* Tp = m >= 2 ? Tw + (m - 2) * UP * UP : nullptr;
+        float2* Tn = Tw + m * UP * UP;
+        tile_pass<NT>(n_gram, 0, 1, T1, UP, Tm, UP, T1, 1, 1, UP,
+                      [&](int, int ib, int jb, float2 (&acc)[4][4]) {
+#pragma unroll
+                        for (int r = 0; r < 4; ++r)
+#pragma unroll
+                          for (int c = 0; c < 4; ++c) {
+                            const int i = ib * 4 + r, j = jb * 4 + c;
+                            if (j > i) continue;
+                            const float2 prev =
+                                Tp ? Tp[i * UP + j] : make_float2(i == j ? 1.f : 0.f, 0.f);
+                            float2 val = make_float2(2.f * acc[r][c].x - prev.x,
+                                                     2.f * acc[r][c].y - prev.y);
+                            if (i == j) val.y = 0.f;
+                            Tn[i * UP + j] = val;
+                            if (i != j) Tn[j * UP + i] = cconj(val);
+                          }
+                      });
+        __syncthreads();
+        if (m + 1 < K) {  // T_m <- T_{m+1} for the next product
+          for (int e = tid; e < UP * UP; e += NT) Tm[e] = Tn[e];
+          __syncthreads();
+        }
+      }
+    }
+    __syncthreads();  // smem reuse by the next subcarrier (TMA overwrite)
+  }
+}
+
+// ------------------------------------------------------------------- K2
+template <int UP>
+struct K2Geo {
+  static constexpr int G = UP < 32 ? UP : 32;  // lanes per system
+  static constexpr int RU = UP / G;            // rows per lane
+  static constexpr int GPW = 32 / G;           // groups per warp
+  static constexpr int NS = UP == 32 ? 2 : 1;  // systems per group, interleaved
+};
+
+template <int UP>
+struct K2Smem {
+  int gs, ps, vs, qs, hist, sys_st, mu, rho, coef, gpart, total;
+  __host__ __device__ static int align(int x) { return (x + 127) & ~127; }
+  __host__ __device__ void plan(int B, int S, int St, int K, bool exact) {
+    const int nsys = S + St;
+    int o = 0;
+    gs = o; o = align(o + UP * UP * 8);
+    ps = o; o = align(o + nsys * UP * 8);
+    vs = o; o = align(o + nsys * UP * 8);
+    qs = o; o = align(o + St * B * 8);
+    hist = o; o = align(o + (exact ? S * K * 2 * 4 : 0));
+    sys_st = o; o = align(o + nsys);
+    mu = o; o = align(o + (exact ? S * UP * 4 : 0));
+    rho = o; o = align(o + (exact ? S * UP * 4 : 0));
+    coef = o; o = align(o + (exact ? S * 2 * (K + 2) * 4 : 0));
+    gpart = o; o = align(o + ((B + 31) / 32) * (St > 0 ? St : 1) * 4);
+    total = o;
+  }
+};
+
+template <int UP, bool EXACT>
+__global__ void __launch_bounds__(256, 3) solve_kernel(const KernelParams p) {
+  using GE = K2Geo<UP>;
+  constexpr int G = GE::G, RU = GE::RU, GPW = GE::GPW, NS = GE::NS;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int S = p.S, St = p.St, B = p.B, U = p.U;
+  const int nsys = S + St;
+  const int Kmax = p.K > p.Kt ? p.K : p.Kt;
+  K2Smem<UP> L;
+  L.plan(B, S, St, Kmax, EXACT);
+  WsOffsets W;
+  W.plan(UP, S, p.K, EXACT);
+  float2* Gs = reinterpret_cast<float2*>(smem + L.gs);
+  float2* Ps = reinterpret_cast<float2*>(smem + L.ps);
+  float2* Vs = reinterpret_cast<float2*>(smem + L.vs);
+  float2* Qs = reinterpret_cast<float2*>(smem + L.qs);
+  float* hist = reinterpret_cast<float*>(smem + L.hist);
+  uint8_t* sys_st = reinterpret_cast<uint8_t*>(smem + L.sys_st);
+  float* MUs = reinterpret_cast<float*>(smem + L.mu);
+  float* RHOs = reinterpret_cast<float*>(smem + L.rho);
+  float* coef = reinterpret_cast<float*>(smem + L.coef);
+  float* gpart = reinterpret_cast<float*>(smem + L.gpart);
+  const int nt = blockDim.x, nw = nt >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long lsc = blockIdx.x;
+  const long sc = p.sc_base + lsc;
+  const float2* ws = p.ws + lsc * W.stride;
+
+  {  // G <- workspace
+    const float4* src = reinterpret_cast<const float4*>(ws + W.g);
+    float4* dst = reinterpret_cast<float4*>(Gs);
+    for (int e = tid; e < UP * UP / 2; e += nt) dst[e] = src[e];
+  }
+  __syncthreads();
+
+  // ------------------------------------------------------------------ CG
+  {
+    const int grp = lane / G, gl = lane - grp * G;
+    const int n_slots = nw * GPW * NS;
+    float gdiag[RU];
+#pragma unroll
+    for (int m = 0; m < RU; ++m) gdiag[m] = Gs[(gl + m * G) * UP + gl + m * G].x;
+    // warp-uniform trip count (the shuffles below use the full mask)
+    for (int wbase = warp * GPW * NS; wbase < nsys; wbase += n_slots) {
+      const int base = wbase + grp * NS;
+      int sys[NS];
+      bool live[NS], down[NS];
+      float reg[NS];
+      int iters[NS];
+      float2 v[NS][RU], r[NS][RU], pp[NS][RU];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        sys[s] = base + s;
+        live[s] = sys[s] < nsys;
+        down[s] = sys[s] >= S;
+        reg[s] = down[s] ? p.rho_inv_d : p.rho_inv_u;
+        iters[s] = live[s] ? (down[s] ? p.Kt : p.K) : 0;
+#pragma unroll
+        for (int m = 0; m < RU; ++m) {
+          const int u = gl + m * G;
+          float2 b = make_float2(0.f, 0.f);
+          if (live[s] && u < U)
+            b = down[s] ? p.T[(sc * St + (sys[s] - S)) * static_cast<long>(U) + u]
+                        : ws[W.mf + sys[s] * UP + u];
+          v[s][m] = make_float2(0.f, 0.f);
+          r[s][m] = b;
+          pp[s][m] = b;
+          if (live[s]) Ps[sys[s] * UP + u] = b;
+        }
+      }
+      float rn[NS], rn0[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        rn[s] = 0.f;
+#pragma unroll
+        for (int m = 0; m < RU; ++m) rn[s] += cnorm(r[s][m]);
+      }
+      group_sum_n<G, NS>(rn);
+      bool broke[NS];
+      float f0[NS][RU], f1[NS][RU], f2[NS][RU];
+      float am1[NS], am2[NS], bm1[NS], bm2[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        rn0[s] = rn[s];
+        broke[s] = false;
+        am1[s] = am2[s] = 1.f;
+        bm1[s] = bm2[s] = 0.f;
+#pragma unroll
+        for (int m = 0; m < RU; ++m) f0[s][m] = f1[s][m] = f2[s][m] = 0.f;
+      }
+      __syncwarp();
+      for (int k = 1; k <= Kmax; ++k) {
+        // e = (G + reg I) p: G read as column (conflict-free), p broadcast;
+        // two partial sums per component shorten the FMA chains
+        float2 e[NS][RU], e2[NS][RU];
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+#pragma unroll
+          for (int m = 0; m < RU; ++m) e[s][m] = e2[s][m] = make_float2(0.f, 0.f);
+#pragma unroll 4
+        for (int j = 0; j < UP; j += 2) {
+          float2 g0[RU], g1[RU];
+#pragma unroll
+          for (int m = 0; m < RU; ++m) {
+            g0[m] = cconj(Gs[j * UP + gl + m * G]);
+            g1[m] = cconj(Gs[(j + 1) * UP + gl + m * G]);
+          }
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            const int row = live[s] ? sys[s] : 0;
+            const float4 pj = *reinterpret_cast<const float4*>(Ps + row * UP + j);
+#pragma unroll
+            for (int m = 0; m < RU; ++m) {
+              cfma(e[s][m], g0[m], make_float2(pj.x, pj.y));
+              cfma(e2[s][m], g1[m], make_float2(pj.z, pj.w));
+            }
+          }
+        }
+        float curv[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          curv[s] = 0.f;
+#pragma unroll
+          for (int m = 0; m < RU; ++m) {
+            e[s][m] = cadd(e[s][m], e2[s][m]);
+            e[s][m].x = fmaf(reg[s], pp[s][m].x, e[s][m].x);
+            e[s][m].y = fmaf(reg[s], pp[s][m].y, e[s][m].y);
+            curv[s] += pp[s][m].x * e[s][m].x + pp[s][m].y * e[s][m].y;  // Re p^H e
+          }
+        }
+        group_sum_n<G, NS>(curv);
+        float alpha[NS], beta[NS], rnx[NS];
+        bool upd[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          const bool step = k <= iters[s];
+          const bool frozen = !(rn[s] > 1e-28f * rn0[s]);  // solvers.cpp:21,25-27
+          const bool go = step && !frozen && !broke[s];
+          if (go && curv[s] < 1e-30f) broke[s] = true;    // solvers.cpp:55-57
+          upd[s] = go && !broke[s];
+          alpha[s] = upd[s] ? __fdividef(rn[s], curv[s]) : 1.f;
+          beta[s] = 0.f;
+          rnx[s] = 0.f;
+#pragma unroll
+          for (int m = 0; m < RU; ++m) {
+            if (upd[s]) {
+              v[s][m].x = fmaf(alpha[s], pp[s][m].x, v[s][m].x);
+              v[s][m].y = fmaf(alpha[s], pp[s][m].y, v[s][m].y);
+              r[s][m].x = fmaf(-alpha[s], e[s][m].x, r[s][m].x);
+              r[s][m].y = fmaf(-alpha[s], e[s][m].y, r[s][m].y);
+            }
+            rnx[s] += cnorm(r[s][m]);
+          }
+        }
+        group_sum_n<G, NS>(rnx);
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          if (upd[s]) {
+            beta[s] = __fdividef(rnx[s], rn[s]);
+            rn[s] = rnx[s];
+#pragma unroll
+            for (int m = 0; m < RU; ++m) {
+              pp[s][m].x = fmaf(beta[s], pp[s][m].x, r[s][m].x);
+              pp[s][m].y = fmaf(beta[s], pp[s][m].y, r[s][m].y);
+              Ps[sys[s] * UP + gl + m * G] = pp[s][m];
+            }
+          }
+          if (k <= iters[s]) {
+            if (!down[s]) {
+              if (EXACT) {
+                if (gl == 0) {
+                  hist[(sys[s] * Kmax + (k - 1)) * 2 + 0] = alpha[s];
+                  hist[(sys[s] * Kmax + (k - 1)) * 2 + 1] = beta[s];
+                }
+              } else {
+                // Eq. (11) on the diagonal (detect.cpp:409-427)
+#pragma unroll
+                for (int m = 0; m < RU; ++m) {
+                  float nf;
+                  if (k == 1) {
+                    nf = alpha[s];
+                  } else {
+                    const float c1 = __fdividef(alpha[s] * (1.f + bm1[s]), am1[s]);
+                    const float c2 = __fdividef(alpha[s] * bm2[s], am2[s]);
+                    nf = f0[s][m] + (c1 - alpha[s] * (gdiag[m] + reg[s])) * (f0[s][m] - f1[s][m]) -
+                         c2 * (f1[s][m] - f2[s][m]);
+                  }
+                  f2[s][m] = f1[s][m];
+                  f1[s][m] = f0[s][m];
+                  f0[s][m] = nf;
+                }
+              }
+            }
+            am2[s] = am1[s]; am1[s] = alpha[s];
+            bm2[s] = bm1[s]; bm1[s] = beta[s];
+          }
+        }
+        __syncwarp();
+      }
+      // ------------------------------------------------ per-system epilogue
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (!live[s]) continue;
+        if (gl == 0) sys_st[sys[s]] = broke[s] ? 1 : 0;
+        if (EXACT || down[s]) {
+#pragma unroll
+          for (int m = 0; m < RU; ++m) Vs[sys[s] * UP + gl + m * G] = v[s][m];
+          continue;
+        }
+        // approx uplink: mu = Ltilde G_ii, rho = G_ii / N0 (detect.cpp:435-441),
+        // LLRs and stores straight from the lane
+#pragma unroll
+        for (int m = 0; m < RU; ++m) {
+          const int u = gl + m * G;
+          if (u >= U) continue;
+          const long o = (sc * S + sys[s]) * static_cast<long>(U) + u;
+          const bool ok = !broke[s];
+          const float2 xh = ok ? v[s][m] : make_float2(0.f, 0.f);
+          const float mu_u = ok ? f0[s][m] * gdiag[m] : 0.f;
+          const float rho_u = ok ? gdiag[m] / p.n0 : 0.f;
+          if (p.xhat) p.xhat[o] = xh;
+          if (p.mu) p.mu[o] = mu_u;
+          if (p.rho) p.rho[o] = rho_u;
+          if (p.llr) store_llrs_fast(xh, mu_u, rho_u, p.bits, p.llr + o * p.bits);
+          if (p.status && gl == 0) p.status[sc * S + sys[s]] = ok ? 0 : 1;
+        }
+      }
+    }
+  }
+
+  // ------------------------------------------ exact tracker extraction
+  if (EXACT && S > 0) {
+    __syncthreads();
+    const int K = p.K;
+    const float2 cdv = ws[W.cd];
+    const double cc = cdv.x, dd = cdv.y;
+    for (int s = tid; s < S; s += nt) {
+      // three-term recursion (detect.cpp:336-368) on Chebyshev coefficients, FP64
+      double l0[kMaxK + 2], l1[kMaxK + 2], l2[kMaxK + 2], tmp[kMaxK + 2], d1[kMaxK + 2];
+      const int n = K + 2;
+      for (int m = 0; m < n; ++m) l0[m] = l1[m] = l2[m] = 0.0;
+      double a_m1 = 1.0, a_m2 = 1.0, b_m1 = 0.0, b_m2 = 0.0;
+      auto mulA = [&](const double* x, double* out) {
+        // A T_0 = c T_0 + d T_1;  A T_m = c T_m + d/2 (T_{m+1} + T_{m-1})
+        for (int m = 0; m < n; ++m) out[m] = cc * x[m];
+        for (int m = 0; m < n; ++m) {
+          const double h = dd * x[m];
+          if (m == 0) {
+            out[1] += h;
+          } else {
+            if (m + 1 < n) out[m + 1] += 0.5 * h;
+            out[m - 1] += 0.5 * h;
+          }
+        }
+      };
+      for (int k = 1; k <= K; ++k) {
+        const double a = hist[(s * Kmax + (k - 1)) * 2 + 0];
+        const double bb = hist[(s * Kmax + (k - 1)) * 2 + 1];
+        if (k == 1) {
+          for (int m = 0; m < n; ++m) { l2[m] = l1[m]; l1[m] = l0[m]; l0[m] = 0.0; }
+          l0[0] = a;  // L_1 = alpha_1 I
+        } else {
+          const double c1 = a * (1.0 + b_m1) / a_m1, c2 = a * b_m2 / a_m2;
+          for (int m = 0; m < n; ++m) d1[m] = l0[m] - l1[m];
+          mulA(d1, tmp);
+          for (int m = 0; m < n; ++m) {
+            const double nx = l0[m] + c1 * d1[m] - a * tmp[m] - c2 * (l1[m] - l2[m]);
+            l2[m] = l1[m];
+            l1[m] = l0[m];
+            l0[m] = nx;
+          }
+        }
+        a_m2 = a_m1; a_m1 = a; b_m2 = b_m1; b_m1 = bb;
+      }
+      // B = L (A - rho^-1 I)  (G = unregularised A, detect.cpp:215)
+      mulA(l0, tmp);
+      float* cl = coef + s * 2 * (K + 2);
+      float* cb = cl + (K + 2);
+      for (int m = 0; m < n; ++m) {
+        cl[m] = static_cast<float>(l0[m]);
+        cb[m] = static_cast<float>(tmp[m] - static_cast<double>(p.rho_inv_u) * l0[m]);
+      }
+    }
+    __syncthreads();
+    // extraction (detect.cpp:375-395): thread <-> (row i, pair of systems);
+    // each T_m(i, j) is read once (L1/L2) and used for both systems
+    const float2* Tw = ws + W.t;
+    const int ngrp = nt / UP;
+    const int i = tid % UP, g = tid / UP;
+    if (g < ngrp) {
+      for (int s0 = g; s0 < S; s0 += 2 * ngrp) {
+        const int s1 = s0 + ngrp;
+        const bool has1 = s1 < S;
+        const float* cl0 = coef + s0 * 2 * (K + 2);
+        const float* cb0 = cl0 + (K + 2);
+        const float* cl1 = coef + (has1 ? s1 : s0) * 2 * (K + 2);
+        const float* cb1 = cl1 + (K + 2);
+        float ib2[2] = {0.f, 0.f}, ibl[2] = {0.f, 0.f}, mu_i[2] = {0.f, 0.f};
+        for (int j = 0; j < UP; ++j) {
+          float2 B0 = make_float2(i == j ? cb0[0] : 0.f, 0.f);
+          float2 L0 = make_float2(i == j ? cl0[0] : 0.f, 0.f);
+          float2 B1 = make_float2(i == j ? cb1[0] : 0.f, 0.f);
+          float2 L1 = make_float2(i == j ? cl1[0] : 0.f, 0.f);
+          for (int m = 1; m <= K; ++m) {
+            const float2 t = cconj(__ldg(Tw + (m - 1) * UP * UP + j * UP + i));  // T_m[i][j]
+            B0.x = fmaf(cb0[m], t.x, B0.x); B0.y = fmaf(cb0[m], t.y, B0.y);
+            B1.x = fmaf(cb1[m], t.x, B1.x); B1.y = fmaf(cb1[m], t.y, B1.y);
+            if (m < K) {
+              L0.x = fmaf(cl0[m], t.x, L0.x); L0.y = fmaf(cl0[m], t.y, L0.y);
+              L1.x = fmaf(cl1[m], t.x, L1.x); L1.y = fmaf(cl1[m], t.y, L1.y);
+            }
+          }
+          if (j == i) { mu_i[0] = B0.x; mu_i[1] = B1.x; }
+          else { ib2[0] += cnorm(B0); ib2[1] += cnorm(B1); }
+          ibl[0] += B0.x * L0.x + B0.y * L0.y;  // Re(B_ij conj(L_ij))
+          ibl[1] += B1.x * L1.x + B1.y * L1.y;
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (t == 1 && !has1) break;
+          const int s = t ? s1 : s0;
+          const float nu2 = ib2[t] * p.es + ibl[t] * p.n0;
+          MUs[s * UP + i] = mu_i[t];
+          RHOs[s * UP + i] = nu2 <= 0.f ? 0.f : mu_i[t] * mu_i[t] / nu2;  // safe_rho
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < S * U; e += nt) {
+      const int s = e / U, u = e - s * U;
+      const long o = (sc * S + s) * static_cast<long>(U) + u;
+      const bool ok = sys_st[s] == 0;
+      const float2 xh = ok ? Vs[s * UP + u] : make_float2(0.f, 0.f);
+      const float m = ok ? MUs[s * UP + u] : 0.f;
+      const float rr = ok ? RHOs[s * UP + u] : 0.f;
+      if (p.xhat) p.xhat[o] = xh;
+      if (p.mu) p.mu[o] = m;
+      if (p.rho) p.rho[o] = rr;
+      if (p.llr) store_llrs_fast(xh, m, rr, p.bits, p.llr + o * p.bits);
+    }
+    if (p.status)
+      for (int s = tid; s < S; s += nt) p.status[sc * S + s] = sys_st[s];
+  }
+
+  // ------------------------------------------------ precode q = H_d^H v
+  // q_b = sum_u H_u[b][u] v_u = sum_u conj(H_d[u][b]) v_u (precode.cpp:69),
+  // then gain = ||q||, s = q / gain, zero_input when ||q|| vanishes (:22-36)
+  if (St > 0) {
+    __syncthreads();
+    const int nrb = (B + 31) / 32;
+    for (int rb = warp; rb < nrb; rb += nw) {
+      const int bidx = rb * 32 + lane;
+      const bool okb = bidx < B;
+      const int bb = okb ? bidx : 0;
+      for (int ts0 = 0; ts0 < St; ts0 += 8) {
+        float2 acc[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[t] = make_float2(0.f, 0.f);
+        if (p.hd_layout) {
+          const float2* hd = p.H + sc * static_cast<long>(U) * B;  // [U][B], coalesced in b
+          for (int u = 0; u < U; ++u) {
+            const float2 h = cconj(__ldg(hd + u * B + bb));
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+              if (ts0 + t < St) cfma(acc[t], h, Vs[(S + ts0 + t) * UP + u]);
+          }
+        } else {
+          const float2* hu = p.H + sc * static_cast<long>(B) * UP + bb * UP;  // row b of H_u
+#pragma unroll 4
+          for (int u = 0; u < UP; u += 2) {
+            const float4 h = __ldg(reinterpret_cast<const float4*>(hu + u));
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              if (ts0 + t < St) {
+                const float4 vv = *reinterpret_cast<const float4*>(Vs + (S + ts0 + t) * UP + u);
+                cfma(acc[t], make_float2(h.x, h.y), make_float2(vv.x, vv.y));
+                cfma(acc[t], make_float2(h.z, h.w), make_float2(vv.z, vv.w));
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (ts0 + t < St) {
+            if (okb) Qs[(ts0 + t) * B + bidx] = acc[t];
+            float nrm = okb ? cnorm(acc[t]) : 0.f;
+            nrm = group_sum<32>(nrm);
+            if (lane == 0) gpart[rb * St + ts0 + t] = nrm;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (int ts = warp; ts < St; ts += nw) {
+      const int sysi = S + ts;
+      const bool ok = sys_st[sysi] == 0;
+      float nrm = 0.f;
+      for (int rb = 0; rb < nrb; ++rb) nrm += gpart[rb * St + ts];  // fixed order
+      const float g = sqrtf(nrm);
+      const bool zero = ok && !(g > 0.f);
+      const float inv = (ok && !zero) ? 1.f / g : 0.f;
+      const long ob = (sc * St + ts) * static_cast<long>(B);
+      for (int b = lane; b < B; b += 32) {
+        const float2 q = Qs[ts * B + b];
+        if (p.q) p.q[ob + b] = ok ? q : make_float2(0.f, 0.f);
+        if (p.s_out) p.s_out[ob + b] = cscale(inv, q);
+      }
+      if (lane == 0) {
+        if (p.gain) p.gain[sc * St + ts] = (ok && !zero) ? g : 0.f;
+        if (p.pstatus) p.pstatus[sc * St + ts] = ok ? (zero ? 2 : 0) : 1;
+      }
+    }
+  }
+}
+
+}  // namespace cgm

@@ -34,8 +34,18 @@ def run_uplink(ctx, cfg, H, Y):
     return {k: to_np(v) for k, v in out.items()}
 
 
+@pytest.fixture(params=["auto", "generic"])
+def policy_ctx(gpu_ctx, request):
+    """Both kernels: the warp-specialised pipeline (auto, U = 32 shapes) and
+    the generic fused kernel."""
+    gpu_ctx.set_kernel_policy(request.param)
+    yield gpu_ctx
+    gpu_ctx.set_kernel_policy("auto")
+
+
 @pytest.mark.parametrize("name,n_sc", UPLINK)
-def test_uplink_parity(gpu_ctx, checker, name, n_sc):
+def test_uplink_parity(policy_ctx, checker, name, n_sc):
+    gpu_ctx = policy_ctx
     cfg = get_config(name).scaled(n_sc)
     H, Y = gen_uplink(gpu_ctx, cfg)
     got = run_uplink(gpu_ctx, cfg, H, Y)
@@ -44,7 +54,8 @@ def test_uplink_parity(gpu_ctx, checker, name, n_sc):
     check_detect(got, want, name)
 
 
-def test_downlink_parity_cfg3(gpu_ctx, checker):
+def test_downlink_parity_cfg3(policy_ctx, checker):
+    gpu_ctx = policy_ctx
     cfg = get_config("cfg3").scaled(1024)
     Hd, T = gpu_ctx.generate_downlink(cfg.B, cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits)
     out = gpu_ctx.precode_cg(Hd, T, cfg.rho_d, cfg.K)
@@ -54,7 +65,8 @@ def test_downlink_parity_cfg3(gpu_ctx, checker):
     check_precode(got, want, "cfg3")
 
 
-def test_fused_parity_cfg5(gpu_ctx, checker):
+def test_fused_parity_cfg5(policy_ctx, checker):
+    gpu_ctx = policy_ctx
     cfg = get_config("cfg5").scaled(24)
     H, Y = gen_uplink(gpu_ctx, cfg)
     T = gpu_ctx.generate_symbols(cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits)
