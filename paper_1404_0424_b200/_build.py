@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU = ["cgm_capi.cu", "cgm_generate.cu"]
 CPP = ["cgm_dropin.cpp"]
-HDRS = ["cgm_device.cuh", "cgm_kernels.cuh"]
+HDRS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 
 
 def _newer(out: str, deps) -> bool:

@@ -130,11 +130,22 @@ int plan_and_launch(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
 // Split path (cgm_split.cuh): K1 channel kernel + K2 solve kernel per chunk
 // of subcarriers; the chunk is sized so the K1->K2 workspace (and the H that
 // the precoder re-reads) stays resident in the 126 MB L2.
-template <int UP, int NT1, bool EXACT>
+template <int UP, bool EXACT>
 int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   const int Kmax = std::max(p.K, p.Kt);
+  // K1: persistent, two TMA stages (prefetch one subcarrier ahead)
+  cgm::K1Split sp;
+  sp.plan(UP, p.B, p.S);
   cgm::K1Smem<UP> L1;
-  L1.plan(p.B, p.S, EXACT);
+  L1.plan(p.B, p.S, EXACT, 2);
+  if (L1.total > ctx->max_smem) {  // very large B: single stage
+    sp.nstage = 1;
+    L1.plan(p.B, p.S, EXACT, 1);
+  }
+  p.k1_pair = sp.nstage;
+  p.k1_spl = sp.spl;
+  p.k1_wpp = sp.wpp;
+  const int nt1 = 32 * sp.wpp;
   cgm::K2Smem<UP> L2;
   L2.plan(p.B, p.S, p.St, Kmax, EXACT);
   if (L1.total > ctx->max_smem || L2.total > ctx->max_smem)
@@ -143,12 +154,12 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
                 L2.total, ctx->max_smem);
   cgm::WsOffsets W;
   W.plan(UP, p.S, p.K, EXACT);
-  auto k1 = cgm::channel_kernel<UP, NT1, EXACT>;
+  auto k1 = cgm::channel_kernel<UP, EXACT>;
   auto k2 = cgm::solve_kernel<UP, EXACT>;
   CGM_CUDA(ctx, cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, L1.total));
   CGM_CUDA(ctx, cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, L2.total));
   int occ1 = 0;
-  CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k1, NT1, L1.total));
+  CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k1, nt1, L1.total));
   if (occ1 < 1) return fail(ctx, CGM_EINVAL, "channel kernel does not fit on an SM");
   // K2 block: enough lane groups for every system at once (>= UP threads
   // for the exact extraction), at most 8 warps
@@ -178,7 +189,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
     p.sc_base = c0;
     p.n_sc = n;
     const long g1 = std::max<long>(1, std::min<long>(n, static_cast<long>(occ1) * ctx->sms));
-    k1<<<static_cast<unsigned>(g1), NT1, L1.total, st>>>(p);
+    k1<<<static_cast<unsigned>(g1), nt1, L1.total, st>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
     k2<<<static_cast<unsigned>(n), 32 * nw2, L2.total, st>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
@@ -187,9 +198,9 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   return CGM_OK;
 }
 
-template <int UP, int NT1>
+template <int UP>
 int dispatch_split(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
-  return exact ? launch_split<UP, NT1, true>(ctx, p, st) : launch_split<UP, NT1, false>(ctx, p, st);
+  return exact ? launch_split<UP, true>(ctx, p, st) : launch_split<UP, false>(ctx, p, st);
 }
 
 template <int UP, int NT>
@@ -202,13 +213,14 @@ int launch(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
   if (p.n_sc <= 0) return CGM_OK;
   const int UP = up_of(p.U);
   const uintptr_t a = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
-  p.use_tma = (!p.hd_layout && p.U == UP && (p.B % 2) == 0 && (a & 15u) == 0) ? 1 : 0;
+  p.use_tma = (!p.hd_layout && p.U == UP && (p.B % 2) == 0 && (p.S % 2) == 0 && (a & 15u) == 0)
+                  ? 1 : 0;
   if (ctx->policy == 0) {
     switch (UP) {
-      case 8: return dispatch_split<8, 128>(ctx, p, exact, st);
-      case 16: return dispatch_split<16, 128>(ctx, p, exact, st);
-      case 32: return dispatch_split<32, 288>(ctx, p, exact, st);
-      default: return dispatch_split<64, 320>(ctx, p, exact, st);
+      case 8: return dispatch_split<8>(ctx, p, exact, st);
+      case 16: return dispatch_split<16>(ctx, p, exact, st);
+      case 32: return dispatch_split<32>(ctx, p, exact, st);
+      default: return dispatch_split<64>(ctx, p, exact, st);
     }
   }
   switch (UP) {

@@ -135,6 +135,39 @@ __device__ __forceinline__ void tile4x4(float2 (&acc)[4][4], const float2* __res
   }
 }
 
+// Software-pipelined 4x4 tile: the operands of row k+1 are loaded before the
+// 64 FFMAs of row k, so each warp keeps one LDS round trip in flight.
+// acc[r][c] += sum_k conj(X[k*ldx + i0 + r]) * Z[k*ldz + j0 + c]; X and Z rows
+// 16B aligned (Z columns past the valid range are read and discarded).
+__device__ __forceinline__ void tile4x4_pipe(float2 (&acc)[4][4], const float2* __restrict__ X,
+                                             int ldx, int i0, const float2* __restrict__ Z,
+                                             int ldz, int j0, int k0, int k1) {
+  const float4* xp = reinterpret_cast<const float4*>(X + k0 * ldx + i0);
+  const float4* zp = reinterpret_cast<const float4*>(Z + k0 * ldz + j0);
+  const int xs = ldx / 2, zs = ldz / 2;  // float4 strides
+  auto fma_row = [&](const float4& xa, const float4& xb, const float4& za, const float4& zb) {
+    const float2 x[4] = {make_float2(xa.x, xa.y), make_float2(xa.z, xa.w),
+                         make_float2(xb.x, xb.y), make_float2(xb.z, xb.w)};
+    const float2 y[4] = {make_float2(za.x, za.y), make_float2(za.z, za.w),
+                         make_float2(zb.x, zb.y), make_float2(zb.z, zb.w)};
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) cfma_conj(acc[r][c], x[r], y[c]);
+  };
+  int k = k0;
+  // two rows per trip: both rows' operands are in flight before the FMAs
+  for (; k + 2 <= k1; k += 2) {
+    const float4 xa0 = xp[0], xb0 = xp[1], za0 = zp[0], zb0 = zp[1];
+    const float4 xa1 = xp[xs], xb1 = xp[xs + 1], za1 = zp[zs], zb1 = zp[zs + 1];
+    xp += 2 * xs;
+    zp += 2 * zs;
+    fma_row(xa0, xb0, za0, zb0);
+    fma_row(xa1, xb1, za1, zb1);
+  }
+  if (k < k1) fma_row(xp[0], xp[1], zp[0], zp[1]);
+}
+
 // acc[r][c] += sum_k conj(X[k*ldx + i0 + r]) * Z[k*ldz + j0 + c], r, c < 2.
 // X rows 16B aligned; Z rows 16B aligned when Z_VEC (else 2 scalar loads,
 // columns >= jmax clamped).  Neighbouring lanes share either the X or the Z

@@ -58,6 +58,7 @@ struct KernelParams {
   int debug;      // profiling knobs (0 in production)
   float2* ws;     // split path: per-subcarrier workspace (G, MF, basis)
   long sc_base;   // split path: first subcarrier of this chunk
+  int k1_pair, k1_spl, k1_wpp;  // channel kernel: subcarriers per CTA, k-parts, warps per part
 };
 
 // Per-axis Gray amplitude subsets (constellation.cpp:75-84), [qam][p][k],
@@ -123,8 +124,8 @@ __device__ __forceinline__ void tri_block(int t, int& ib, int& jb) {
 // lanes of one warp share a tile and split k; their partial sums are
 // combined with butterflies, no CTA barrier.  Epilogue fn(tile, ib, jb, acc)
 // runs on the split-0 lane.
-template <int SPL, int NT, class Epi>
-__device__ __forceinline__ void tile_pass_spl(int n_lower, int n_other, int nsb,
+template <int SPL, class Epi>
+__device__ __forceinline__ void tile_pass_spl(int nwarps, int n_lower, int n_other, int nsb,
                                              const float2* __restrict__ X, int ldx,
                                              const float2* __restrict__ Yl, int ldyl,
                                              const float2* __restrict__ Zs, int ldz, int zcols,
@@ -135,7 +136,7 @@ __device__ __forceinline__ void tile_pass_spl(int n_lower, int n_other, int nsb,
   const int part = lane % SPL;
   const int kchunk = (klen + SPL - 1) / SPL;
   const int k0 = part * kchunk, k1 = min(klen, k0 + kchunk);
-  for (int base = warp * TPW; base < n_tiles; base += (NT / 32) * TPW) {
+  for (int base = warp * TPW; base < n_tiles; base += nwarps * TPW) {
     const int tile = base + lane / SPL;
     const bool active = tile < n_tiles;
     float2 acc[4][4];
@@ -172,23 +173,30 @@ __device__ __forceinline__ void tile_pass_spl(int n_lower, int n_other, int nsb,
   }
 }
 
+template <class Epi>
+__device__ __forceinline__ void tile_pass_nw(int NW, int n_lower, int n_other, int nsb,
+                                             const float2* X, int ldx, const float2* Yl, int ldyl,
+                                             const float2* Zs, int ldz, int zcols, int klen,
+                                             Epi&& fn) {
+  const int n_tiles = n_lower + n_other;
+  // widest split whose tiles fit in one pass over the warps
+  if (n_tiles <= NW * 2 && klen >= 64)
+    tile_pass_spl<16>(NW, n_lower, n_other, nsb, X, ldx, Yl, ldyl, Zs, ldz, zcols, klen, fn);
+  else if (n_tiles <= NW * 4 && klen >= 32)
+    tile_pass_spl<8>(NW, n_lower, n_other, nsb, X, ldx, Yl, ldyl, Zs, ldz, zcols, klen, fn);
+  else if (n_tiles <= NW * 8 && klen >= 16)
+    tile_pass_spl<4>(NW, n_lower, n_other, nsb, X, ldx, Yl, ldyl, Zs, ldz, zcols, klen, fn);
+  else if (n_tiles <= NW * 16 && klen >= 8)
+    tile_pass_spl<2>(NW, n_lower, n_other, nsb, X, ldx, Yl, ldyl, Zs, ldz, zcols, klen, fn);
+  else
+    tile_pass_spl<1>(NW, n_lower, n_other, nsb, X, ldx, Yl, ldyl, Zs, ldz, zcols, klen, fn);
+}
+
 template <int NT, class Epi>
 __device__ __forceinline__ void tile_pass(int n_lower, int n_other, int nsb, const float2* X,
                                           int ldx, const float2* Yl, int ldyl, const float2* Zs,
                                           int ldz, int zcols, int klen, Epi&& fn) {
-  constexpr int NW = NT / 32;
-  const int n_tiles = n_lower + n_other;
-  // widest split whose tiles fit in one pass over the warps
-  if (n_tiles <= NW * 2 && klen >= 64)
-    tile_pass_spl<16, NT>(n_lower, n_other, nsb, X, ldx, Yl, ldyl, Zs, ldz, zcols, klen, fn);
-  else if (n_tiles <= NW * 4 && klen >= 32)
-    tile_pass_spl<8, NT>(n_lower, n_other, nsb, X, ldx, Yl, ldyl, Zs, ldz, zcols, klen, fn);
-  else if (n_tiles <= NW * 8 && klen >= 16)
-    tile_pass_spl<4, NT>(n_lower, n_other, nsb, X, ldx, Yl, ldyl, Zs, ldz, zcols, klen, fn);
-  else if (n_tiles <= NW * 16 && klen >= 8)
-    tile_pass_spl<2, NT>(n_lower, n_other, nsb, X, ldx, Yl, ldyl, Zs, ldz, zcols, klen, fn);
-  else
-    tile_pass_spl<1, NT>(n_lower, n_other, nsb, X, ldx, Yl, ldyl, Zs, ldz, zcols, klen, fn);
+  tile_pass_nw(NT / 32, n_lower, n_other, nsb, X, ldx, Yl, ldyl, Zs, ldz, zcols, klen, fn);
 }
 
 // ------------------------------------------------------------------ LLR

@@ -39,155 +39,198 @@ struct WsOffsets {
   }
 };
 
+// K1 shared memory: two TMA stages of {H [B][UP], Y [B][S]} (the next
+// subcarrier is prefetched while the current one is contracted), the Gram
+// matrix, and (exact) T_1 / T_m of the basis product chain.
 template <int UP>
 struct K1Smem {
-  int bar, hs, ys, gs, tb, misc, total;
+  int bar, slot, hs, ys, gs, tb, misc, total;
   __host__ __device__ static int align(int x) { return (x + 127) & ~127; }
-  __host__ __device__ void plan(int B, int S, bool exact) {
+  __host__ __device__ void plan(int B, int S, bool exact, int nstage) {
+    const int Sp = (S + 1) & ~1;  // Y rows padded to an even length (16B aligned)
     int o = 0;
-    bar = o; o = align(o + 16);
-    hs = o; o = align(o + B * UP * 8);
-    ys = o; o = align(o + B * S * 8 + 64);
+    bar = o; o = align(o + 32);
+    hs = o;
+    ys = align(B * UP * 8);
+    slot = align(ys + B * Sp * 8 + 64);  // +64: last-row 4-wide tile reads
+    o = align(o + nstage * slot);
     gs = o; o = align(o + UP * UP * 8);
-    tb = o; o = align(o + (exact ? 2 * UP * UP * 8 : 0));  // T_1 and T_m
+    tb = o; o = align(o + (exact ? 2 * UP * UP * 8 : 0));
     misc = o; o = align(o + 16);
     total = o;
   }
 };
 
-template <int UP, int NT, bool EXACT>
-__global__ void __launch_bounds__(NT) channel_kernel(const KernelParams p) {
+// Host/device-consistent work split of K1: 4x4 tiles x `spl` k-parts as
+// thread-granular work items (item = part * n_tiles + tile); all parts'
+// partial tiles are parked in the consumed TMA stage and summed by every
+// thread in a fixed order.
+struct K1Split {
+  int nstage, spl, wpp, n_tiles;
+  __host__ __device__ void plan(int UP, int B, int S) {
+    const int nb = UP / 4;
+    n_tiles = nb * (nb + 1) / 2 + nb * ((S + 3) / 4);
+    const int Sp = (S + 1) & ~1;
+    const int stage_bytes = B * UP * 8 + B * Sp * 8;
+    int s = 320 / n_tiles;                                  // <= 10 warps per CTA
+    const int cap_k = B / 16 > 0 ? B / 16 : 1;              // >= 16 rows per part
+    const int cap_m = stage_bytes / (n_tiles * 128);        // partials fit in the stage
+    s = s > cap_k ? cap_k : s;
+    s = s > cap_m ? cap_m : s;
+    spl = s < 1 ? 1 : s;
+    wpp = (spl * n_tiles + 31) / 32;  // total warps (name kept for the params field)
+    nstage = 2;
+  }
+};
+
+__device__ __forceinline__ void k1_issue(const KernelParams& p, float2* Hs, float2* Ys,
+                                         uint64_t* bar, long sc, int UP) {
+  const uint32_t hbytes = static_cast<uint32_t>(p.B) * UP * 8u;
+  const uint32_t ybytes = static_cast<uint32_t>(p.B) * p.S * 8u;
+  fence_proxy_async();
+  mbar_expect_tx(bar, hbytes + ybytes);
+  bulk_g2s(Hs, p.H + sc * static_cast<long>(p.B) * UP, hbytes, bar);
+  if (p.S > 0) bulk_g2s(Ys, p.Y + sc * static_cast<long>(p.B) * p.S, ybytes, bar);
+}
+
+template <int UP, bool EXACT>
+__global__ void __launch_bounds__(320, 2) channel_kernel(const KernelParams p) {  // NOLINT
   extern __shared__ __align__(128) unsigned char smem[];
+  const int spl = p.k1_spl, nstage = p.k1_pair;
   K1Smem<UP> L;
-  L.plan(p.B, p.S, EXACT);
+  L.plan(p.B, p.S, EXACT, nstage);
   WsOffsets W;
   W.plan(UP, p.S, p.K, EXACT);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
-  float2* Hs = reinterpret_cast<float2*>(smem + L.hs);
-  float2* Ys = reinterpret_cast<float2*>(smem + L.ys);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar);
   float2* Gs = reinterpret_cast<float2*>(smem + L.gs);
   float2* T1 = reinterpret_cast<float2*>(smem + L.tb);
   float2* Tm = T1 + UP * UP;
   float* misc = reinterpret_cast<float*>(smem + L.misc);
+  const int nt = blockDim.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int B = p.B, S = p.S, U = p.U;
   const int nb = UP / 4, n_gram = nb * (nb + 1) / 2, nsb = (S + 3) / 4;
+  const int n_tiles = n_gram + nb * nsb;
+  auto Hs_of = [&](int st) { return reinterpret_cast<float2*>(smem + L.hs + st * L.slot); };
+  auto Ys_of = [&](int st) {
+    return reinterpret_cast<float2*>(smem + L.hs + st * L.slot + L.ys);
+  };
 
-  if (p.use_tma && tid == 0) mbar_init(bar, 1);
+  const int n_items = spl * n_tiles;
+  const int part = tid / n_tiles;
+  const int tile = tid - part * n_tiles;
+  const bool active = tid < n_items;
+  const bool is_gram = tile < n_gram;
+  int ib = 0, jb = 0;
+  if (is_gram) {
+    tri_block(tile, ib, jb);  // row-major: neighbouring lanes share X
+  } else {
+    const int m = tile - n_gram;  // neighbouring lanes share the Y block
+    jb = m / nb;
+    ib = m - jb * nb;
+  }
+  const int kchunk = (B + spl - 1) / spl;
+  const int k0 = part * kchunk, k1 = min(B, k0 + kchunk);
+  const long n_local = p.n_sc > blockIdx.x ? (p.n_sc - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto sc_of = [&](long i) { return p.sc_base + blockIdx.x + i * gridDim.x; };
+
+  if (tid == 0 && p.use_tma) {
+    for (int st = 0; st < nstage; ++st) mbar_init(bars + st, 1);
+  }
   __syncthreads();
-  uint32_t phase = 0;
-  for (long lsc = blockIdx.x; lsc < p.n_sc; lsc += gridDim.x, phase ^= 1u) {
+  if (tid == 0 && p.use_tma)
+    for (int st = 0; st < nstage && st < n_local; ++st) k1_issue(p, Hs_of(st), Ys_of(st), bars + st, sc_of(st), UP);
+
+  for (long i = 0; i < n_local; ++i) {
+    const int st = static_cast<int>(i % nstage);
+    const uint32_t ph = static_cast<uint32_t>((i / nstage) & 1);
+    const long lsc = blockIdx.x + i * gridDim.x;  // within the chunk
     const long sc = p.sc_base + lsc;
+    float2* Hs = Hs_of(st);
+    float2* Ys = Ys_of(st);
     float2* ws = p.ws + lsc * W.stride;
-    // ---------------------------------------------------------- stage H, Y
+    // ------------------------------------------------------ stage H, Y
+    const int Sp = (S + 1) & ~1;
     if (p.use_tma) {
-      if (tid == 0) {
-        const uint32_t hbytes = static_cast<uint32_t>(B) * UP * 8u;
-        const uint32_t ybytes = static_cast<uint32_t>(B) * S * 8u;
-        fence_proxy_async();
-        mbar_expect_tx(bar, hbytes + ybytes);
-        bulk_g2s(Hs, p.H + sc * static_cast<long>(B) * UP, hbytes, bar);
-        if (S > 0) bulk_g2s(Ys, p.Y + sc * static_cast<long>(B) * S, ybytes, bar);
-      }
-      mbar_wait(bar, phase);
+      mbar_wait(bars + st, ph);
     } else {
       if (p.hd_layout) {
         // downlink H_d [U][B] -> Hs[b][u] = conj(H_d[u][b])  (= H_u = H_d^H)
         const float2* src = p.H + sc * static_cast<long>(U) * B;
-        for (int e = tid; e < UP * B; e += NT) {
+        for (int e = tid; e < UP * B; e += nt) {
           const int u = e / B, b = e - u * B;
           Hs[b * UP + u] = u < U ? cconj(src[u * B + b]) : make_float2(0.f, 0.f);
         }
       } else {
         const float2* src = p.H + sc * static_cast<long>(B) * U;
-        for (int e = tid; e < UP * B; e += NT) {
+        for (int e = tid; e < UP * B; e += nt) {
           const int b = e / UP, u = e - b * UP;
           Hs[e] = u < U ? src[b * U + u] : make_float2(0.f, 0.f);
         }
       }
-      for (int e = tid; e < S * B; e += NT) Ys[e] = p.Y[sc * static_cast<long>(B) * S + e];
+      for (int e = tid; e < Sp * B; e += nt) {
+        const int b = e / Sp, s = e - b * Sp;
+        Ys[e] = s < S ? p.Y[(sc * B + b) * static_cast<long>(S) + s] : make_float2(0.f, 0.f);
+      }
       __syncthreads();
     }
-    // ------------------------------------------- Gram + matched filter tiles
-    float2* MFw = ws + W.mf;
-    if (UP >= 32) {
-      // 2x2 register tiles, one per thread, no split-K: lower-triangle Gram
-      // blocks (row-major: lanes share X) then MF blocks (lanes share Z)
-      constexpr int nb2 = UP / 2;
-      const int n_g2 = nb2 * (nb2 + 1) / 2, nsb2 = (S + 1) / 2;
-      const int n_t2 = n_g2 + nb2 * nsb2;
-      for (int t = tid; t < n_t2; t += NT) {
-        float2 acc[2][2];
+    // --------------------------------------- Gram + matched-filter tiles
+    // one branch-free loop for both tile kinds (a warp may hold both): the
+    // second operand is H itself (Gram) or the Y block (matched filter)
+    float2 acc[4][4];
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
+    for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < 2; ++c) acc[r][c] = make_float2(0.f, 0.f);
-        if (t < n_g2) {
-          int ib, jb;
-          tri_block(t, ib, jb);
-          tile2x2<true>(acc, Hs, UP, ib * 2, Hs, UP, jb * 2, 1 << 30, 0, B);
+      for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(0.f, 0.f);
+    if (active) {
+      const float2* Z = is_gram ? Hs : Ys;
+      const int ldz = is_gram ? UP : Sp;
+      tile4x4_pipe(acc, Hs, UP, ib * 4, Z, ldz, jb * 4, k0, k1);
+    }
+    __syncthreads();  // (A) every k loop done: the stage may hold partials
+    {
+      // partials parked entry-major / tile-minor ([part][16][n_tiles]) so a
+      // warp's stores and the reduction's loads are contiguous (no conflicts)
+      float2* pb = Hs;
+      if (active) {
+        float2* dst = pb + part * 16 * n_tiles + tile;
 #pragma unroll
-          for (int r = 0; r < 2; ++r)
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const int i = ib * 2 + r, j = jb * 2 + c;
-              if (j < i) {
-                Gs[i * UP + j] = acc[r][c];
-                Gs[j * UP + i] = cconj(acc[r][c]);
-              } else if (j == i) {
-                Gs[i * UP + i] = make_float2(acc[r][c].x, 0.f);
-              }
-            }
-        } else {
-          const int m = t - n_g2;
-          const int jb = m / nb2, ib = m - jb * nb2;
-          if ((S & 1) == 0)
-            tile2x2<true>(acc, Hs, UP, ib * 2, Ys, S, jb * 2, S, 0, B);
-          else
-            tile2x2<false>(acc, Hs, UP, ib * 2, Ys, S, jb * 2, S, 0, B);
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int s = jb * 2 + c;
-            if (s < S)
-              *reinterpret_cast<float4*>(MFw + s * UP + ib * 2) =
-                  make_float4(acc[0][c].x, acc[0][c].y, acc[1][c].x, acc[1][c].y);
+          for (int c = 0; c < 4; ++c) dst[(r * 4 + c) * n_tiles] = acc[r][c];
+      }
+      __syncthreads();  // (B)
+      // every thread finishes entries: fixed-order sum over the k-parts, then
+      // G (one triangle + conjugate mirror, G == G^H exactly) or the MF
+      float2* MFw = ws + W.mf;
+      for (int e = tid; e < n_tiles * 16; e += nt) {
+        const int rc = e / n_tiles, t = e - rc * n_tiles, r = rc >> 2, c = rc & 3;
+        float2 v = pb[e];
+        for (int sp = 1; sp < spl; ++sp) v = cadd(v, pb[sp * n_tiles * 16 + e]);
+        if (t < n_gram) {
+          int tib, tjb;
+          tri_block(t, tib, tjb);
+          const int ii = tib * 4 + r, j = tjb * 4 + c;
+          if (j < ii) {
+            Gs[ii * UP + j] = v;
+            Gs[j * UP + ii] = cconj(v);
+          } else if (j == ii) {
+            Gs[ii * UP + ii] = make_float2(v.x, 0.f);
           }
+        } else {
+          const int m = t - n_gram, tjb = m / nb, tib = m - tjb * nb;
+          const int s_ = tjb * 4 + c;
+          if (s_ < S) MFw[s_ * UP + tib * 4 + r] = v;
         }
       }
-    } else {
-      tile_pass<NT>(n_gram, nb * nsb, nsb, Hs, UP, Hs, UP, Ys, S, S, B,
-                    [&](int tile, int ib, int jb, float2 (&acc)[4][4]) {
-                      if (tile < n_gram) {
-#pragma unroll
-                        for (int r = 0; r < 4; ++r)
-#pragma unroll
-                          for (int c = 0; c < 4; ++c) {
-                            const int i = ib * 4 + r, j = jb * 4 + c;
-                            if (j < i) {
-                              Gs[i * UP + j] = acc[r][c];
-                              Gs[j * UP + i] = cconj(acc[r][c]);
-                            } else if (j == i) {
-                              Gs[i * UP + i] = make_float2(acc[r][c].x, 0.f);
-                            }
-                          }
-                      } else {
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                          const int s = jb * 4 + c;
-                          if (s < S) {
-                            float4* dst = reinterpret_cast<float4*>(MFw + s * UP + ib * 4);
-                            dst[0] = make_float4(acc[0][c].x, acc[0][c].y, acc[1][c].x, acc[1][c].y);
-                            dst[1] = make_float4(acc[2][c].x, acc[2][c].y, acc[3][c].x, acc[3][c].y);
-                          }
-                        }
-                      }
-                    });
     }
-    __syncthreads();
+    __syncthreads();  // (C) stage consumed, G complete
+    if (tid == 0 && p.use_tma && i + nstage < n_local)
+      k1_issue(p, Hs, Ys, bars + st, sc_of(i + nstage), UP);  // prefetch into the freed stage
     {  // G -> workspace (coalesced)
       const float4* src = reinterpret_cast<const float4*>(Gs);
       float4* dst = reinterpret_cast<float4*>(ws + W.g);
-      for (int e = tid; e < UP * UP / 2; e += NT) dst[e] = src[e];
+      for (int e = tid; e < UP * UP / 2; e += nt) dst[e] = src[e];
     }
     if (EXACT && S > 0) {
       const int K = p.K;
@@ -196,7 +239,7 @@ __global__ void __launch_bounds__(NT) channel_kernel(const KernelParams p) {
         // (any d > 0 is exact algebra; this choice keeps the basis well
         // conditioned in FP32)
         float tr = 0.f, fr = 0.f;
-        for (int i = lane; i < UP; i += 32) tr += Gs[i * UP + i].x + p.rho_inv_u;
+        for (int ii = lane; ii < UP; ii += 32) tr += Gs[ii * UP + ii].x + p.rho_inv_u;
         tr = group_sum<32>(tr);
         const float c = tr / UP;
         for (int e = lane; e < UP * UP; e += 32) {
@@ -216,7 +259,7 @@ __global__ void __launch_bounds__(NT) channel_kernel(const KernelParams p) {
       __syncthreads();
       const float cc = misc[0], invd = 1.f / misc[1];
       float2* Tw = ws + W.t;
-      for (int e = tid; e < UP * UP; e += NT) {  // T_1 = (A - cI)/d
+      for (int e = tid; e < UP * UP; e += nt) {  // T_1 = (A - cI)/d
         float2 a = Gs[e];
         if (e / UP == e % UP) a.x += p.rho_inv_u - cc;
         a = cscale(invd, a);
@@ -225,35 +268,35 @@ __global__ void __launch_bounds__(NT) channel_kernel(const KernelParams p) {
         Tw[e] = a;
       }
       __syncthreads();
-      // T_{m+1} = 2 T_1 T_m - T_{m-1} (lower tiles + mirror; T_{m-1} from L2)
+      // T_{m+1} = 2 T_1 T_m - T_{m-1} (lower tiles + mirror; T_{m-1} via L2)
       for (int m = 1; m < K; ++m) {
         const float2* Tp = m >= 2 ? Tw + (m - 2) * UP * UP : nullptr;
         float2* Tn = Tw + m * UP * UP;
-        tile_pass<NT>(n_gram, 0, 1, T1, UP, Tm, UP, T1, 1, 1, UP,
-                      [&](int, int ib, int jb, float2 (&acc)[4][4]) {
+        tile_pass_nw(nt / 32, n_gram, 0, 1, T1, UP, Tm, UP, T1, 1, 1, UP,
+                     [&](int, int tib, int tjb, float2 (&a4)[4][4]) {
 #pragma unroll
-                        for (int r = 0; r < 4; ++r)
+                       for (int r = 0; r < 4; ++r)
 #pragma unroll
-                          for (int c = 0; c < 4; ++c) {
-                            const int i = ib * 4 + r, j = jb * 4 + c;
-                            if (j > i) continue;
-                            const float2 prev =
-                                Tp ? Tp[i * UP + j] : make_float2(i == j ? 1.f : 0.f, 0.f);
-                            float2 val = make_float2(2.f * acc[r][c].x - prev.x,
-                                                     2.f * acc[r][c].y - prev.y);
-                            if (i == j) val.y = 0.f;
-                            Tn[i * UP + j] = val;
-                            if (i != j) Tn[j * UP + i] = cconj(val);
-                          }
-                      });
+                         for (int c = 0; c < 4; ++c) {
+                           const int ii = tib * 4 + r, j = tjb * 4 + c;
+                           if (j > ii) continue;
+                           const float2 prev =
+                               Tp ? Tp[ii * UP + j] : make_float2(ii == j ? 1.f : 0.f, 0.f);
+                           float2 val = make_float2(2.f * a4[r][c].x - prev.x,
+                                                    2.f * a4[r][c].y - prev.y);
+                           if (ii == j) val.y = 0.f;
+                           Tn[ii * UP + j] = val;
+                           if (ii != j) Tn[j * UP + ii] = cconj(val);
+                         }
+                     });
         __syncthreads();
         if (m + 1 < K) {  // T_m <- T_{m+1} for the next product
-          for (int e = tid; e < UP * UP; e += NT) Tm[e] = Tn[e];
+          for (int e = tid; e < UP * UP; e += nt) Tm[e] = Tn[e];
           __syncthreads();
         }
       }
     }
-    __syncthreads();  // smem reuse by the next subcarrier (TMA overwrite)
+    __syncthreads();  // Gs is rewritten by the next subcarrier
   }
 }
 
