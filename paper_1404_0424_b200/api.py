@@ -106,10 +106,7 @@ class Context:
                   want=("xhat", "mu", "rho", "llr", "status")):
         """Batched detect_cg.  Returns dict with the requested outputs."""
         device = _is_torch(H)
-        n_sc, B, U = H.shape
-        if Y.ndim != 3 or Y.shape[0] != n_sc or Y.shape[1] != B:
-            raise ValueError("detect_cg: dimension mismatch")
-        S = Y.shape[2]
+        n_sc, B, U, S = detect_dims(H, Y)
         if tracker not in TRACKERS:
             raise ValueError(f"unknown tracker {tracker!r}")
         out = dict(out or {})
@@ -138,13 +135,7 @@ class Context:
         """Batched precode_cg.  Hd (n_sc, U, B); with uplink_layout=True the
         matrix is H_u (n_sc, B, U) and H_d = H_u^H (TDD reciprocity)."""
         device = _is_torch(Hd)
-        if uplink_layout:
-            n_sc, B, U = Hd.shape
-        else:
-            n_sc, U, B = Hd.shape
-        if T.shape[0] != n_sc or T.shape[2] != U:
-            raise ValueError("precode_cg: dimension mismatch")
-        S = T.shape[1]
+        n_sc, B, U, S = precode_dims(Hd, T, uplink_layout)
         out = dict(out or {})
         shapes = {"q": ((n_sc, S, B), "c64"), "s": ((n_sc, S, B), "c64"),
                   "gain": ((n_sc, S), "f32"), "status": ((n_sc, S), "u8")}
@@ -237,6 +228,30 @@ class Context:
         self._check(self.lib.cgm_generate_symbols(self.h, U, sc0, n_sc, S, seed, qam_bits,
                                                   _ptr(T), None))
         return T
+
+
+def detect_dims(H, Y):
+    """(n_sc, B, U, S) of a batched detect call; raises ValueError like the
+    reference's std::invalid_argument (detect.cpp:186)."""
+    if len(H.shape) != 3 or len(Y.shape) != 3:
+        raise ValueError("detect_cg: H must be (n_sc, B, U) and Y (n_sc, B, S)")
+    n_sc, B, U = H.shape
+    if Y.shape[0] != n_sc or Y.shape[1] != B:
+        raise ValueError("detect_cg: dimension mismatch")
+    return n_sc, B, U, Y.shape[2]
+
+
+def precode_dims(Hd, T, uplink_layout=False):
+    """(n_sc, B, U, S) of a batched precode call (precode.cpp:60)."""
+    if len(Hd.shape) != 3 or len(T.shape) != 3:
+        raise ValueError("precode_cg: Hd must be (n_sc, U, B) and T (n_sc, S, U)")
+    if uplink_layout:
+        n_sc, B, U = Hd.shape
+    else:
+        n_sc, U, B = Hd.shape
+    if T.shape[0] != n_sc or T.shape[2] != U:
+        raise ValueError("precode_cg: dimension mismatch")
+    return n_sc, B, U, T.shape[1]
 
 
 def _alloc(spec, device, like):

@@ -204,7 +204,7 @@ __device__ __forceinline__ float axis_min_sq(float z, const float* amps, int n) 
   float best = INFINITY;
   for (int k = 0; k < n; ++k) {
     const float d = z - amps[k];
-    best = fminf(best, d * d);
+    best = fminf(best, __fmul_rn(d, d));
   }
   return best;
 }
@@ -259,7 +259,7 @@ __device__ __forceinline__ void llr_axis(float z, float rho, float* o) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const float t = z - c_axis.lv[q][k];
-      d[k] = t * t;
+      d[k] = __fmul_rn(t, t);  // rounded alone (no FMA contraction): exact ties stay 0
     }
     const float b0 = fminf(fminf(d[0], d[1]), fminf(d[2], d[3])) -
                      fminf(fminf(d[4], d[5]), fminf(d[6], d[7]));
@@ -275,13 +275,13 @@ __device__ __forceinline__ void llr_axis(float z, float rho, float* o) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const float t = z - c_axis.lv[q][k];
-      d[k] = t * t;
+      d[k] = __fmul_rn(t, t);
     }
     o[0] = fminf(64.f, fmaxf(-64.f, rho * (fminf(d[0], d[1]) - fminf(d[2], d[3]))));
     o[1] = fminf(64.f, fmaxf(-64.f, rho * (fminf(d[0], d[3]) - fminf(d[1], d[2]))));
   } else {
     const float t0 = z - c_axis.lv[q][0], t1 = z - c_axis.lv[q][1];
-    o[0] = fminf(64.f, fmaxf(-64.f, rho * (t0 * t0 - t1 * t1)));
+    o[0] = fminf(64.f, fmaxf(-64.f, rho * (__fmul_rn(t0, t0) - __fmul_rn(t1, t1))));
   }
 }
 

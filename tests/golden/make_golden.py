@@ -1,0 +1,110 @@
+"""Generate tests/golden/*.npz from the UNMODIFIED reference library.
+
+Runs the reference (oracle/_ref/libcgmimo_ref.so, built by `make -C oracle`
+from /root/reference/proj/src) on small seeded complex64 inputs of every
+BASELINE shape family plus the known-answer cases of the reference's own
+tests, and stores inputs and FP64 outputs.  The fixtures travel with the repo
+(the GPU box has no /root/reference) and pin both the C restatement
+(tests/test_oracle.py) and the CUDA path (tests/test_gpu_golden.py).
+
+    python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+
+
+def cn(rng, shape, var=1.0):
+    return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) * np.sqrt(var / 2)
+
+
+# (name, B, U, S, K, tracker, qam_bits, snr_db, n_sc)
+DETECT_CASES = [
+    ("cfg1_like", 128, 8, 1, 3, "exact", 4, 10.0, 6),
+    ("cfg2_like", 128, 32, 14, 4, "approx", 6, 15.0, 2),
+    ("cfg4a_like_K8", 64, 32, 1, 8, "exact", 6, 20.0, 4),
+    ("cfg4b_like_K4", 128, 64, 1, 4, "exact", 6, 20.0, 2),
+    ("cfg5_like_ul", 256, 32, 4, 4, "exact", 6, 15.0, 2),
+    ("small_qpsk", 16, 4, 3, 2, "approx", 2, 5.0, 3),
+    ("ragged_U5", 12, 5, 2, 5, "exact", 4, 8.0, 3),
+]
+# (name, B, U, S, K, snr_db, n_sc)
+PRECODE_CASES = [
+    ("cfg3_like", 128, 16, 1, 3, 10.0, 6),
+    ("cfg5_like_dl", 256, 32, 4, 4, 15.0, 2),
+    ("small_dl", 16, 4, 2, 2, 5.0, 3),
+]
+
+
+def main():
+    ref = oracle.Oracle("ref")
+    rng = np.random.default_rng(20260419)
+    out = {}
+    for name, B, U, S, K, trk, bits, snr, n_sc in DETECT_CASES:
+        n0 = U / 10 ** (snr / 10)
+        rho_u = 1.0 / n0
+        H = cn(rng, (n_sc, B, U)).astype(np.complex64)
+        pts, _, _ = ref.constellation(bits)
+        X = pts[rng.integers(0, 1 << bits, (n_sc, S, U))]
+        Y = (np.einsum("nbu,nsu->nbs", H.astype(np.complex128), X)
+             + cn(rng, (n_sc, B, S), n0)).astype(np.complex64)
+        r = ref.detect(H, Y, rho_u, n0, 1.0, bits, K, trk)
+        out[f"det_{name}"] = dict(H=H, Y=Y, meta=np.array([B, U, S, K, bits, trk == "exact"]),
+                                  params=np.array([rho_u, n0, 1.0]), **r)
+    for name, B, U, S, K, snr, n_sc in PRECODE_CASES:
+        n0 = 1.0 / 10 ** (snr / 10)
+        rho_d = 1.0 / (U * n0)
+        Hd = cn(rng, (n_sc, U, B)).astype(np.complex64)
+        pts, _, _ = ref.constellation(4)
+        T = pts[rng.integers(0, 16, (n_sc, S, U))].astype(np.complex64)
+        r = ref.precode(Hd, T, rho_d, K)
+        out[f"pre_{name}"] = dict(Hd=Hd, T=T, meta=np.array([B, U, S, K]),
+                                  params=np.array([rho_d]), **r)
+    # known answers from the reference's tests (test_detect.cpp:71-89, :347-370,
+    # :393-422; test_precode.cpp:42-53): identity channels, zero observation
+    kat = {}
+    I4 = np.eye(4, dtype=np.complex64)[None]
+    bits = np.array([0, 1, 1, 0, 1, 1, 0, 0, 0, 0, 1, 1, 1, 0, 1, 0], np.uint8)
+    pts16, _, _ = ref.constellation(4)
+    labels = bits.reshape(4, 4) @ np.array([8, 4, 2, 1])
+    x = pts16[labels].astype(np.complex64)
+    r = ref.detect(I4, x[None, :, None], 1e12, 1e-12, 1.0, 4, 4, "exact")
+    kat["noiseless_identity"] = dict(H=I4, Y=x[None, :, None], bits=bits, **r)
+    y = cn(np.random.default_rng(61), 4).astype(np.complex64)
+    r = ref.detect(I4, y[None, :, None], 5.0, 0.2, 1.0, 4, 1, "approx")
+    kat["identity_k1"] = dict(H=I4, Y=y[None, :, None], **r)
+    z = np.zeros((1, 4, 1), np.complex64)
+    kat["zero_obs_qpsk"] = dict(H=I4, Y=z, **ref.detect(I4, z, 4.0, 0.25, 1.0, 2, 3, "approx"))
+    kat["zero_obs_16qam"] = dict(H=I4, Y=z, **ref.detect(I4, z, 4.0, 0.25, 1.0, 4, 3, "approx"))
+    tz = np.zeros((1, 1, 4), np.complex64)
+    kat["zero_transmit"] = dict(Hd=I4, T=tz, **ref.precode(I4, tz, 2.0, 2))
+    for k, v in kat.items():
+        out[f"kat_{k}"] = v
+    # LLR known answers (detect.cpp:68-86 via compute_llrs)
+    llr_cases = [(0.9 + 0.9j, 1.0, 2.0, 4), (0.0 + 0.5j, 1.0, 2.0, 4), (0.9 + 0.9j, 1e-14, 10.0, 4),
+                 (0.3 - 1.1j, 0.8, 40.0, 6), (-0.2 + 0.05j, 1.2, -3.0, 6), (1.0 + 0.0j, 1.0, 1.5, 2)]
+    arr = np.array([[c.real, c.imag, m, r_, b] for c, m, r_, b in llr_cases])
+    vals = np.zeros((len(llr_cases), 6))
+    for i, (c, m, r_, b) in enumerate(llr_cases):
+        vals[i, :b] = ref.compute_llrs(c, m, r_, b)
+    out["llr_cases"] = dict(inputs=arr, llrs=vals)
+    # RNG streams (rng.cpp): u64 draws and Rayleigh channel of a fork path
+    out["rng"] = dict(u64=ref.rng_u64(12345, [2, 7], 16),
+                      gauss=ref.rng_cgaussian(99, [3, 11], 0.5, 8),
+                      rayleigh=ref.rayleigh(5, [2, 3], 8, 4))
+    for name, d in out.items():
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
+    print(f"wrote {len(out)} fixtures to {HERE}")
+
+
+if __name__ == "__main__":
+    main()

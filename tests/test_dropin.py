@@ -1,0 +1,113 @@
+"""The C++ drop-in: a program written against the reference's API compiles
+against include/cgmimo/ and links libcgmimo_b200.so (CPU); on a GPU its
+per-call detect_cg / precode_cg results and opcount tallies match the
+reference (gpu)."""
+import os
+import struct
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import cplx_randn
+from parity import assert_close, assert_hard_bits
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tests", "dropin", "dropin_main.cpp")
+PKG = os.path.join(ROOT, "paper_1404_0424_b200")
+
+
+@pytest.fixture(scope="module")
+def dropin_exe(tmp_path_factory):
+    exe = str(tmp_path_factory.mktemp("dropin") / "dropin_main")
+    r = subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-I" + os.path.join(ROOT, "include"),
+                        SRC, "-L" + PKG, "-lcgmimo_b200", "-Wl,-rpath," + PKG, "-o", exe],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_dropin_host_behaviour(dropin_exe, oracle_port):
+    r = subprocess.run([dropin_exe, "host"], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stderr)
+    lines = r.stdout.splitlines()
+    assert lines[-1] == "host ok"
+    for line in lines:
+        if line.startswith("constellation"):
+            f = line.split()
+            bits = int(f[1])
+            vals = np.array([float(x) for x in f[2:]])
+            pts = vals[0::2] + 1j * vals[1::2]
+            want, _, _ = oracle_port.constellation(bits)
+            assert np.array_equal(pts, want)
+    llrs = [np.array([float(x) for x in line.split()[1:]]) for line in lines if line.startswith("llr")]
+    cases = [(0.9 + 0.9j, 1.0, 2.0, 4), (0.0 + 0.5j, 1.0, 2.0, 4), (0.9 + 0.9j, 1e-14, 10.0, 4),
+             (0.3 - 1.1j, 0.8, 40.0, 6), (-0.2 + 0.05j, 1.2, -3.0, 6), (1.0 + 0.0j, 1.0, 1.5, 2)]
+    for got, (x, mu, rho, bits) in zip(llrs, cases):
+        np.testing.assert_allclose(got, oracle_port.compute_llrs(x, mu, rho, bits), atol=1e-14)
+
+
+@pytest.mark.gpu
+def test_dropin_per_call_on_gpu(dropin_exe, checker, tmp_path):
+    rng = np.random.default_rng(5)
+    B, U, K, bits, n = 32, 8, 3, 6, 5
+    n0 = 0.1
+    H = [cplx_randn(rng, (B, U)).astype(np.complex64).astype(np.complex128) for _ in range(n)]
+    y = [cplx_randn(rng, B, 3.0).astype(np.complex64).astype(np.complex128) for _ in range(n)]
+    Bd, Ud, Kd, nd = 48, 8, 4, 3
+    Hd = [cplx_randn(rng, (Ud, Bd)).astype(np.complex64).astype(np.complex128) for _ in range(nd)]
+    t = [cplx_randn(rng, Ud).astype(np.complex64).astype(np.complex128) for _ in range(nd)]
+    t[1][:] = 0
+    rho_d = 2.0
+    with open(tmp_path / "in.bin", "wb") as f:
+        f.write(struct.pack("6i", B, U, K, bits, 0, n))
+        for h, v in zip(H, y):
+            f.write(h.tobytes())
+            f.write(v.tobytes())
+        f.write(struct.pack("4i", Bd, Ud, Kd, nd))
+        for h, v in zip(Hd, t):
+            f.write(h.tobytes())
+            f.write(v.tobytes())
+        f.write(struct.pack("3d", 1 / n0, n0, rho_d))
+    r = subprocess.run([dropin_exe, "gpu", str(tmp_path / "in.bin"), str(tmp_path / "out.bin")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    data = open(tmp_path / "out.bin", "rb").read()
+    off = 0
+
+    def take(count, dt):
+        nonlocal off
+        a = np.frombuffer(data, dt, count, off)
+        off += a.nbytes
+        return a
+
+    want = checker.detect(np.stack(H), np.stack(y)[:, :, None], 1 / n0, n0, 1.0, bits, K, "exact")
+    tallies = []
+    for i in range(n):
+        xh = take(U, np.complex128)
+        mu = take(U, np.float64)
+        rho = take(U, np.float64)
+        llr = take(U * bits, np.float64).reshape(U, bits)
+        tallies.append(take(9, np.uint64))
+        assert_close(xh, want["xhat"][i, 0], "dropin xhat")
+        assert_close(mu, want["mu"][i, 0], "dropin mu")
+        assert_close(rho, want["rho"][i, 0], "dropin rho")
+        assert_close(llr, want["llr"][i, 0], "dropin llr")
+        assert_hard_bits(llr, want["llr"][i, 0])
+    if hasattr(checker, "tally_detect_cg") and checker.kind == "ref":
+        # opcount parity: the drop-in records what the reference's
+        # instrumented path records (test_opcount.cpp:74-98)
+        ref_t = checker.tally_detect_cg(B, U, K, "exact", 1)
+        assert np.array_equal(tallies[0], ref_t)
+    wantp = checker.precode(np.stack(Hd), np.stack(t)[:, None, :], rho_d, Kd)
+    for i in range(nd):
+        q = take(Bd, np.complex128)
+        s = take(Bd, np.complex128)
+        gain, zero = take(2, np.float64)
+        trace = take(Kd * Bd, np.complex128).reshape(Kd, Bd)
+        assert_close(q, wantp["q"][i, 0], "dropin q")
+        assert_close(s, wantp["s"][i, 0], "dropin s")
+        assert bool(zero) == bool(wantp["status"][i, 0] & 2)
+        assert_close(trace[-1], wantp["q"][i, 0], "dropin q_trace[K-1]")
+    broke = take(1, np.int32)[0]
+    assert broke == 1

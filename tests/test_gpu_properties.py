@@ -1,0 +1,136 @@
+"""GPU: full-size BASELINE configs, checked through size-independent
+properties (the oracle is too slow at these sizes): completion, value
+ranges, run-to-run determinism, shard invariance (results do not depend on
+how subcarriers are split across launches / GPUs), exact power-of-two
+linearity, host-buffer == device-buffer results, and a random subsample of
+full-size instances against the oracle."""
+import numpy as np
+import pytest
+import torch
+
+from paper_1404_0424_b200 import get_config
+from parity import check_detect, check_precode
+
+pytestmark = pytest.mark.gpu
+
+
+def gen(ctx, cfg, sc0=0, n_sc=None):
+    n = cfg.n_sc if n_sc is None else n_sc
+    rs = cfg.rsqrt()
+    rs = None if rs is None else torch.tensor(rs)
+    H, Y = ctx.generate_uplink(cfg.B, cfg.U, n, cfg.S, cfg.seed, cfg.qam_bits, cfg.n0, sc0=sc0,
+                               rsqrt=rs)
+    return H, Y
+
+
+def run(ctx, cfg, H, Y):
+    out = ctx.detect_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K, cfg.tracker)
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg4a_K8", "cfg4b_K2"])
+def test_full_size_uplink_properties(gpu_ctx, checker, name):
+    cfg = get_config(name)
+    if cfg.n_sc > 16384:
+        cfg = cfg.scaled(16384)
+    H, Y = gen(gpu_ctx, cfg)
+    a = run(gpu_ctx, cfg, H, Y)
+    b = run(gpu_ctx, cfg, H, Y)
+    assert int(a["status"].sum()) == 0
+    for k in a:  # bitwise deterministic
+        assert torch.equal(a[k], b[k]), k
+    llr = a["llr"]
+    assert torch.isfinite(llr).all() and float(llr.abs().max()) <= 64.0
+    assert torch.isfinite(a["rho"]).all() and float(a["mu"].min()) > 0
+    # shard invariance: regenerate + detect a middle slice on its own
+    s0, n = cfg.n_sc // 3, cfg.n_sc // 4
+    Hs, Ys = gen(gpu_ctx, cfg, sc0=s0, n_sc=n)
+    assert torch.equal(Hs, H[s0:s0 + n]) and torch.equal(Ys, Y[s0:s0 + n])
+    c = run(gpu_ctx, cfg, Hs, Ys)
+    for k in a:
+        assert torch.equal(c[k], a[k][s0:s0 + n]), k
+    # random subsample of full-size instances against the oracle
+    idx = np.random.default_rng(0).choice(cfg.n_sc, size=16, replace=False)
+    Hn, Yn = H[idx].cpu().numpy(), Y[idx].cpu().numpy()
+    want = checker.detect(Hn, Yn, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K, cfg.tracker,
+                          threads=8)
+    check_detect({k: v[idx].cpu().numpy() for k, v in a.items()}, want, name + " subsample")
+
+
+def test_linearity_power_of_two(gpu_ctx):
+    """Scaling the received vectors by 2 is exact in binary FP: CG scalars
+    are unchanged, x-hat doubles bitwise, mu is unchanged bitwise."""
+    cfg = get_config("cfg2").scaled(256)
+    H, Y = gen(gpu_ctx, cfg)
+    a = run(gpu_ctx, cfg, H, Y)
+    b = run(gpu_ctx, cfg, H, Y * 2)
+    assert torch.equal(b["xhat"], a["xhat"] * 2)
+    assert torch.equal(b["mu"], a["mu"]) and torch.equal(b["rho"], a["rho"])
+
+
+def test_host_and_device_buffers_agree_bitwise(gpu_ctx):
+    cfg = get_config("cfg2").scaled(700)
+    H, Y = gen(gpu_ctx, cfg)
+    dev = run(gpu_ctx, cfg, H, Y)
+    host = gpu_ctx.detect_cg(H.cpu().numpy(), Y.cpu().numpy(), cfg.rho_u, cfg.n0, cfg.es,
+                             cfg.qam_bits, cfg.K, cfg.tracker)
+    for k in host:
+        assert np.array_equal(host[k], dev[k].cpu().numpy()), k
+
+
+def test_cfg5_full_size_fused(gpu_ctx, checker):
+    cfg = get_config("cfg5").scaled(8192)
+    H, Y = gen(gpu_ctx, cfg)
+    T = gpu_ctx.generate_symbols(cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits)
+    a = gpu_ctx.detect_precode_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                                  cfg.tracker, T, cfg.rho_d, cfg.K)
+    b = gpu_ctx.detect_precode_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                                  cfg.tracker, T * 2, cfg.rho_d, cfg.K)
+    torch.cuda.synchronize()
+    assert int(a["status"].sum()) == 0 and int(a["pstatus"].sum()) == 0
+    assert torch.equal(b["q"], a["q"] * 2) and torch.equal(b["s"], a["s"])  # linearity
+    nrm = torch.linalg.vector_norm(a["s"], dim=-1)
+    assert float((nrm - 1).abs().max()) < 1e-5  # ||s|| = 1 (test_precode.cpp:104-120)
+    idx = np.random.default_rng(1).choice(cfg.n_sc, size=8, replace=False)
+    Hn, Yn, Tn = H[idx].cpu().numpy(), Y[idx].cpu().numpy(), T[idx].cpu().numpy()
+    want = checker.detect(Hn, Yn, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K, cfg.tracker,
+                          threads=8)
+    check_detect({k: a[k][idx].cpu().numpy() for k in ("xhat", "mu", "rho", "llr", "status")},
+                 want, "cfg5 subsample uplink")
+    Hd = np.ascontiguousarray(np.conj(np.transpose(Hn, (0, 2, 1))))
+    wantd = checker.precode(Hd, Tn, cfg.rho_d, cfg.K, threads=8)
+    check_precode({"q": a["q"][idx].cpu().numpy(), "s": a["s"][idx].cpu().numpy(),
+                   "gain": a["gain"][idx].cpu().numpy(), "status": a["pstatus"][idx].cpu().numpy()},
+                  wantd, "cfg5 subsample downlink")
+
+
+def test_generator_matches_reference_streams(gpu_ctx, oracle_port):
+    """GPU seeded generator vs the reference Rng streams (rng.cpp): channel
+    entries agree to the last complex64 ulp, labels exactly."""
+    H, Y, L = gpu_ctx.generate_uplink(16, 4, 3, 2, 77, 4, 0.1, sc0=5, labels=True)
+    torch.cuda.synchronize()
+    Hn = H.cpu().numpy()
+    for i in range(3):
+        want = oracle_port.rayleigh(77, [2, 5 + i], 16, 4).astype(np.complex64)
+        np.testing.assert_array_max_ulp(Hn[i].view(np.float32), want.view(np.float32), maxulp=1)
+    # labels: bits drawn as next_u64() & 1 from root.fork(1).fork(instance)
+    Ln = L.cpu().numpy()
+    for i in range(3):
+        for s in range(2):
+            draws = oracle_port.rng_u64(77, [1, (5 + i) * 2 + s], 4 * 4)
+            for u in range(4):
+                lab = 0
+                for b in range(4):
+                    lab = (lab << 1) | int(draws[u * 4 + b] & 1)
+                assert Ln[i, s, u] == lab
+
+
+def test_kernel_launch_accounting(gpu_ctx):
+    before = gpu_ctx.kernel_launches
+    cfg = get_config("cfg2").scaled(64)
+    H, Y = gen(gpu_ctx, cfg)
+    mid = gpu_ctx.kernel_launches
+    run(gpu_ctx, cfg, H, Y)
+    assert mid > before  # generator kernels
+    assert gpu_ctx.kernel_launches - mid >= 1  # the hot path ran native kernels

@@ -1,0 +1,68 @@
+"""CPU: host-side logic -- workload configs, algorithmic counts, argument
+validation of the Python mirror, sharding arithmetic."""
+import numpy as np
+import pytest
+
+from paper_1404_0424_b200 import CONFIGS, api, get_config
+from paper_1404_0424_b200.parallel import shard_range
+
+
+def test_configs_follow_reference_snr_conventions():
+    c1 = get_config("cfg1")
+    assert c1.n0 == pytest.approx(0.8) and c1.rho_u == pytest.approx(1.25)  # channel.cpp:44-47
+    c3 = get_config("cfg3")
+    assert c3.n0 == pytest.approx(0.1) and c3.rho_d == pytest.approx(0.625)  # channel.cpp:49-51
+    c5 = get_config("cfg5")
+    assert c5.rho_d == pytest.approx(c5.rho_u)  # A_dl == A_ul: the Gram is shared
+    assert c5.rsqrt().shape == (256, 256)
+    R = 0.5 ** np.abs(np.subtract.outer(np.arange(256), np.arange(256)))
+    np.testing.assert_allclose(c5.rsqrt() @ c5.rsqrt(), R, atol=1e-10)
+
+
+def test_algorithmic_counts_match_survey_table():
+    # flop / byte per vector
+    want = {"cfg1": (56192, 9472), "cfg2": (112795, 4645), "cfg3": (163328, 17540),
+            "cfg5": (850112, 9732), "cfg4a_K2": (596800, 18176), "cfg4b_K8": (11264128, 69120)}
+    for name, (f, b) in want.items():
+        c = CONFIGS[name]
+        assert round(c.flops_per_vector()) == f, name
+        assert round(c.bytes_per_vector()) == b, name
+
+
+def test_argument_validation_mirrors_reference():
+    H = np.zeros((2, 8, 4), np.complex64)
+    assert api.detect_dims(H, np.zeros((2, 8, 3), np.complex64)) == (2, 8, 4, 3)
+    with pytest.raises(ValueError):
+        api.detect_dims(H, np.zeros((2, 7, 3), np.complex64))
+    with pytest.raises(ValueError):
+        api.detect_dims(H[0], np.zeros((8, 3), np.complex64))
+    Hd = np.zeros((2, 4, 16), np.complex64)
+    assert api.precode_dims(Hd, np.zeros((2, 5, 4), np.complex64)) == (2, 16, 4, 5)
+    assert api.precode_dims(H, np.zeros((2, 1, 4), np.complex64), uplink_layout=True) == (2, 8, 4, 1)
+    with pytest.raises(ValueError):
+        api.precode_dims(Hd, np.zeros((2, 5, 3), np.complex64))
+    with pytest.raises(ValueError):
+        api._check_inputs(False, np.zeros((2, 3), np.complex128))
+    with pytest.raises(ValueError):
+        api.detect_cg_single(np.zeros((8, 4)), np.zeros(7), 1.0, 1.0, 1.0, 4, 2)
+
+
+@pytest.mark.parametrize("n,w", [(1200, 1), (1200, 2), (1200, 8), (65536, 8), (7, 4), (3, 8)])
+def test_shard_range_partitions_contiguously(n, w):
+    spans = [shard_range(n, r, w) for r in range(w)]
+    assert spans[0][0] == 0 and spans[-1][1] == n
+    for (a, b), (c, d) in zip(spans, spans[1:]):
+        assert b == c
+    sizes = [b - a for a, b in spans]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def test_seed_scheme_is_shard_invariant(oracle_port):
+    """Per-subcarrier streams (root.fork(2).fork(sc)) make any shard's inputs
+    identical to the same rows of the unsharded draw."""
+    full = [oracle_port.rayleigh(3, [2, sc], 16, 4) for sc in range(12)]
+    for w in (2, 3, 4):
+        for r in range(w):
+            a, b = shard_range(12, r, w)
+            part = [oracle_port.rayleigh(3, [2, sc], 16, 4) for sc in range(a, b)]
+            assert all(np.array_equal(x, y) for x, y in zip(part, full[a:b]))
