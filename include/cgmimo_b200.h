@@ -70,6 +70,12 @@ int cgm_synchronize(cgm_ctx* ctx);
  * chunk of subcarriers); 1: the single fused per-subcarrier kernel (A/B
  * testing).  Both are parity-tested. */
 int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy);
+/* Per-kernel device timing: while on, every channel/solve launch pair is
+ * bracketed by CUDA events on the launch stream; cgm_ctx_kernel_times
+ * synchronises and returns the summed milliseconds of each kernel and the
+ * number of channel-kernel launches since profiling was (re)enabled. */
+int cgm_ctx_set_profiling(cgm_ctx* ctx, int on);
+int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, long* launches);
 const char* cgm_last_error(const cgm_ctx* ctx);
 /* kernels this context has launched since creation (the bench's gpu_launches) */
 long cgm_kernel_launches(const cgm_ctx* ctx);

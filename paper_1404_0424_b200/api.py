@@ -94,6 +94,15 @@ class Context:
         (single fused per-subcarrier kernel)."""
         self._check(self.lib.cgm_ctx_set_kernel_policy(self.h, {"auto": 0, "generic": 1}[policy]))
 
+    def set_profiling(self, on: bool):
+        self._check(self.lib.cgm_ctx_set_profiling(self.h, 1 if on else 0))
+
+    def kernel_times(self):
+        """(channel_ms, solve_ms, launches) summed since profiling was enabled."""
+        a, b, n = C.c_double(), C.c_double(), C.c_long()
+        self._check(self.lib.cgm_ctx_kernel_times(self.h, C.byref(a), C.byref(b), C.byref(n)))
+        return a.value, b.value, n.value
+
     def synchronize(self):
         self._check(self.lib.cgm_synchronize(self.h))
 

@@ -30,10 +30,25 @@ struct cgm_ctx {
   size_t tscratch_bytes = 0;
   long launches = 0;
   int policy = 0;  // 0 split K1+K2 path (production), 1 single fused kernel (A/B)
+  // optional per-kernel event timing (bench roofline): pairs of events per launch
+  int profiling = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_log;  // kind, (start, stop)
+  size_t ev_next = 0;
   std::string err;
 };
 
 namespace {
+
+// Record a timing event pair around one kernel launch when profiling is on.
+cudaEvent_t prof_event(cgm_ctx* ctx) {
+  if (ctx->ev_next == ctx->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->ev_pool.push_back(e);
+  }
+  return ctx->ev_pool[ctx->ev_next++];
+}
 
 int fail(cgm_ctx* ctx, int code, const char* fmt, ...) {
   char buf[512];
@@ -189,10 +204,23 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
     p.sc_base = c0;
     p.n_sc = n;
     const long g1 = std::max<long>(1, std::min<long>(n, static_cast<long>(occ1) * ctx->sms));
+    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+    if (ctx->profiling) {
+      e0 = prof_event(ctx);
+      e1 = prof_event(ctx);
+      e2 = prof_event(ctx);
+      cudaEventRecord(e0, st);
+    }
     k1<<<static_cast<unsigned>(g1), nt1, L1.total, st>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
+    if (ctx->profiling) cudaEventRecord(e1, st);
     k2<<<static_cast<unsigned>(n), 32 * nw2, L2.total, st>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
+    if (ctx->profiling) {
+      cudaEventRecord(e2, st);
+      ctx->ev_log.push_back({1, {e0, e1}});
+      ctx->ev_log.push_back({2, {e1, e2}});
+    }
     ctx->launches += 2;
   }
   return CGM_OK;
@@ -483,6 +511,7 @@ int cgm_ctx_destroy(cgm_ctx* ctx) {
     if (ctx->pipe[b]) cudaStreamDestroy(ctx->pipe[b]);
   }
   if (ctx->tscratch) cudaFree(ctx->tscratch);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   delete ctx;
   return CGM_OK;
 }
@@ -490,6 +519,28 @@ int cgm_ctx_destroy(cgm_ctx* ctx) {
 int cgm_ctx_set_stream(cgm_ctx* ctx, void* stream) {
   if (!ctx) return CGM_EINVAL;
   ctx->user_stream = static_cast<cudaStream_t>(stream);
+  return CGM_OK;
+}
+
+int cgm_ctx_set_profiling(cgm_ctx* ctx, int on) {
+  if (!ctx) return CGM_EINVAL;
+  ctx->profiling = on ? 1 : 0;
+  ctx->ev_log.clear();
+  ctx->ev_next = 0;
+  return CGM_OK;
+}
+
+int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, long* launches) {
+  if (!ctx || !channel_ms || !solve_ms || !launches) return CGM_EINVAL;
+  *channel_ms = *solve_ms = 0.0;
+  *launches = 0;
+  for (auto& rec : ctx->ev_log) {
+    CGM_CUDA(ctx, cudaEventSynchronize(rec.second.second));
+    float ms = 0.f;
+    CGM_CUDA(ctx, cudaEventElapsedTime(&ms, rec.second.first, rec.second.second));
+    (rec.first == 1 ? *channel_ms : *solve_ms) += ms;
+    if (rec.first == 1) ++*launches;
+  }
   return CGM_OK;
 }
 
