@@ -32,6 +32,10 @@ struct cgm_ctx {
   int policy = 0;  // 0 split K1+K2 path (production), 1 single fused kernel (A/B)
   // optional per-kernel event timing (bench roofline): pairs of events per launch
   int profiling = 0;
+  // overlapped split path: channel kernel of chunk c+1 runs concurrently with
+  // the solve kernel of chunk c (two internal streams, two workspace halves)
+  cudaStream_t ov[2] = {nullptr, nullptr};
+  cudaEvent_t ov_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // start, done1[2], done2[2]
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_log;  // kind, (start, stop)
   size_t ev_next = 0;
@@ -189,7 +193,17 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   long chunk = static_cast<long>((80ull << 20) / std::max<size_t>(per_sc, 1));
   chunk = std::max<long>(chunk, static_cast<long>(ctx->sms) * occ1);
   chunk = std::min(chunk, p.n_sc);
-  const size_t ws_need = static_cast<size_t>(chunk) * W.stride * sizeof(float2);
+  // overlap K1(c+1) with K2(c): at least `ovl` chunks (CGMIMO_OVERLAP_CHUNKS,
+  // default 1 = off: measured slower on cfg2/cfg3/cfg5)
+  int ovl = 1;
+  if (const char* e = std::getenv("CGMIMO_OVERLAP_CHUNKS")) ovl = std::max(1, std::atoi(e));
+  const long min_chunk = static_cast<long>(ctx->sms) * occ1;
+  if (ovl > 1 && p.n_sc >= 2 * min_chunk)
+    chunk = std::min(chunk, std::max(min_chunk, (p.n_sc + ovl - 1) / ovl));
+  const long total = p.n_sc;
+  const bool overlap = chunk < total && ovl > 1;
+  const size_t ws_half = static_cast<size_t>(chunk) * W.stride * sizeof(float2);
+  const size_t ws_need = ws_half * (overlap ? 2 : 1);
   if (ws_need > ctx->tscratch_bytes) {
     if (ctx->tscratch) cudaFree(ctx->tscratch);
     ctx->tscratch = nullptr;
@@ -197,31 +211,59 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
     CGM_CUDA(ctx, cudaMalloc(&ctx->tscratch, ws_need));
     ctx->tscratch_bytes = ws_need;
   }
-  p.ws = reinterpret_cast<float2*>(ctx->tscratch);
-  const long total = p.n_sc;
-  for (long c0 = 0; c0 < total; c0 += chunk) {
+  cudaStream_t s1 = st, s2 = st;
+  if (overlap) {
+    if (!ctx->ov[0]) {
+      for (int i = 0; i < 2; ++i) CGM_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->ov[i], cudaStreamNonBlocking));
+      for (int i = 0; i < 5; ++i) CGM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ov_ev[i], cudaEventDisableTiming));
+    }
+    s1 = ctx->ov[0];
+    s2 = ctx->ov[1];
+    CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[0], st));  // order after prior work on st
+    CGM_CUDA(ctx, cudaStreamWaitEvent(s1, ctx->ov_ev[0], 0));
+    CGM_CUDA(ctx, cudaStreamWaitEvent(s2, ctx->ov_ev[0], 0));
+  }
+  long ci = 0;
+  for (long c0 = 0; c0 < total; c0 += chunk, ++ci) {
     const long n = std::min(chunk, total - c0);
+    const int half = overlap ? static_cast<int>(ci & 1) : 0;
+    p.ws = reinterpret_cast<float2*>(reinterpret_cast<char*>(ctx->tscratch) + half * ws_half);
     p.sc_base = c0;
     p.n_sc = n;
     const long g1 = std::max<long>(1, std::min<long>(n, static_cast<long>(occ1) * ctx->sms));
-    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+    if (overlap && ci >= 2)  // K2 of chunk ci-2 has released this workspace half
+      CGM_CUDA(ctx, cudaStreamWaitEvent(s1, ctx->ov_ev[3 + half], 0));
+    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
     if (ctx->profiling) {
       e0 = prof_event(ctx);
       e1 = prof_event(ctx);
       e2 = prof_event(ctx);
-      cudaEventRecord(e0, st);
+      e3 = prof_event(ctx);
+      cudaEventRecord(e0, s1);
     }
-    k1<<<static_cast<unsigned>(g1), nt1, L1.total, st>>>(p);
+    k1<<<static_cast<unsigned>(g1), nt1, L1.total, s1>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
-    if (ctx->profiling) cudaEventRecord(e1, st);
-    k2<<<static_cast<unsigned>(n), 32 * nw2, L2.total, st>>>(p);
+    if (ctx->profiling) cudaEventRecord(e1, s1);
+    if (overlap) {
+      CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[1 + half], s1));
+      CGM_CUDA(ctx, cudaStreamWaitEvent(s2, ctx->ov_ev[1 + half], 0));
+    }
+    if (ctx->profiling) cudaEventRecord(e2, s2);
+    k2<<<static_cast<unsigned>(n), 32 * nw2, L2.total, s2>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
     if (ctx->profiling) {
-      cudaEventRecord(e2, st);
+      cudaEventRecord(e3, s2);
       ctx->ev_log.push_back({1, {e0, e1}});
-      ctx->ev_log.push_back({2, {e1, e2}});
+      ctx->ev_log.push_back({2, {e2, e3}});
     }
+    if (overlap) CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[3 + half], s2));
     ctx->launches += 2;
+  }
+  if (overlap) {  // the caller's stream waits for both internal streams
+    CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[0], s1));
+    CGM_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ov_ev[0], 0));
+    CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[0], s2));
+    CGM_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ov_ev[0], 0));
   }
   return CGM_OK;
 }
@@ -512,6 +554,10 @@ int cgm_ctx_destroy(cgm_ctx* ctx) {
   }
   if (ctx->tscratch) cudaFree(ctx->tscratch);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i)
+    if (ctx->ov[i]) cudaStreamDestroy(ctx->ov[i]);
+  for (int i = 0; i < 5; ++i)
+    if (ctx->ov_ev[i]) cudaEventDestroy(ctx->ov_ev[i]);
   delete ctx;
   return CGM_OK;
 }

@@ -57,8 +57,10 @@ struct K1Smem {
     gs = o; o = align(o + UP * UP * 8);
     tb = o; o = align(o + (exact ? 2 * UP * UP * 8 : 0));
     misc = o; o = align(o + 16);
+    lut = o; o = align(o + 2 * 512);  // per-tile (ib, jb), <= 512 tiles
     total = o;
   }
+  int lut;
 };
 
 // Host/device-consistent work split of K1: 4x4 tiles x `spl` k-parts as
@@ -93,8 +95,10 @@ __device__ __forceinline__ void k1_issue(const KernelParams& p, float2* Hs, floa
   if (p.S > 0) bulk_g2s(Ys, p.Y + sc * static_cast<long>(p.B) * p.S, ybytes, bar);
 }
 
-template <int UP, bool EXACT>
-__global__ void __launch_bounds__(320, 2) channel_kernel(const KernelParams p) {  // NOLINT
+// MINB: CTAs per SM the register budget is sized for; PIPE: software-
+// pipelined tile loop (operands of row k+1 in flight) or the plain one.
+template <int UP, bool EXACT, int MINB = 2, bool PIPE = true>
+__global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int spl = p.k1_spl, nstage = p.k1_pair;
   K1Smem<UP> L;
@@ -116,6 +120,19 @@ __global__ void __launch_bounds__(320, 2) channel_kernel(const KernelParams p) {
     return reinterpret_cast<float2*>(smem + L.hs + st * L.slot + L.ys);
   };
 
+  uint8_t* tile_ib = reinterpret_cast<uint8_t*>(smem + L.lut);
+  uint8_t* tile_jb = tile_ib + 512;
+  for (int t = tid; t < n_tiles; t += nt) {
+    int a, b;
+    if (t < n_gram) {
+      tri_block(t, a, b);
+    } else {
+      b = (t - n_gram) / nb;
+      a = (t - n_gram) - b * nb;
+    }
+    tile_ib[t] = static_cast<uint8_t>(a);
+    tile_jb[t] = static_cast<uint8_t>(b);
+  }
   const int n_items = spl * n_tiles;
   const int part = tid / n_tiles;
   const int tile = tid - part * n_tiles;
@@ -182,13 +199,16 @@ __global__ void __launch_bounds__(320, 2) channel_kernel(const KernelParams p) {
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(0.f, 0.f);
-    if (active) {
+    if (active && !(p.debug & 4)) {
       const float2* Z = is_gram ? Hs : Ys;
       const int ldz = is_gram ? UP : Sp;
-      tile4x4_pipe(acc, Hs, UP, ib * 4, Z, ldz, jb * 4, k0, k1);
+      if (PIPE)
+        tile4x4_pipe(acc, Hs, UP, ib * 4, Z, ldz, jb * 4, k0, k1);
+      else
+        tile4x4<true>(acc, Hs, UP, ib * 4, Z, ldz, 1, jb * 4, 1 << 30, k0, k1);
     }
     __syncthreads();  // (A) every k loop done: the stage may hold partials
-    {
+    if (!(p.debug & 8)) {
       // partials parked entry-major / tile-minor ([part][16][n_tiles]) so a
       // warp's stores and the reduction's loads are contiguous (no conflicts)
       float2* pb = Hs;
@@ -200,27 +220,37 @@ __global__ void __launch_bounds__(320, 2) channel_kernel(const KernelParams p) {
           for (int c = 0; c < 4; ++c) dst[(r * 4 + c) * n_tiles] = acc[r][c];
       }
       __syncthreads();  // (B)
-      // every thread finishes entries: fixed-order sum over the k-parts, then
-      // G (one triangle + conjugate mirror, G == G^H exactly) or the MF
+      // thread <-> (tile, row r): fixed-order sum of the k-parts for the 4
+      // entries of the row, then G (one triangle + conjugate mirror, G == G^H
+      // exactly) or the matched filter.  Loads are tile-contiguous.
       float2* MFw = ws + W.mf;
-      for (int e = tid; e < n_tiles * 16; e += nt) {
-        const int rc = e / n_tiles, t = e - rc * n_tiles, r = rc >> 2, c = rc & 3;
-        float2 v = pb[e];
-        for (int sp = 1; sp < spl; ++sp) v = cadd(v, pb[sp * n_tiles * 16 + e]);
+      for (int e = tid; e < n_tiles * 4; e += nt) {
+        const int r = e / n_tiles, t = e - r * n_tiles;
+        const int tib = tile_ib[t], tjb = tile_jb[t];
+        float2 v[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          v[c] = pb[(r * 4 + c) * n_tiles + t];
+          for (int sp = 1; sp < spl; ++sp) v[c] = cadd(v[c], pb[(sp * 16 + r * 4 + c) * n_tiles + t]);
+        }
         if (t < n_gram) {
-          int tib, tjb;
-          tri_block(t, tib, tjb);
-          const int ii = tib * 4 + r, j = tjb * 4 + c;
-          if (j < ii) {
-            Gs[ii * UP + j] = v;
-            Gs[j * UP + ii] = cconj(v);
-          } else if (j == ii) {
-            Gs[ii * UP + ii] = make_float2(v.x, 0.f);
+          const int ii = tib * 4 + r;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int j = tjb * 4 + c;
+            if (j < ii) {
+              Gs[ii * UP + j] = v[c];
+              Gs[j * UP + ii] = cconj(v[c]);
+            } else if (j == ii) {
+              Gs[ii * UP + ii] = make_float2(v[c].x, 0.f);
+            }
           }
         } else {
-          const int m = t - n_gram, tjb = m / nb, tib = m - tjb * nb;
-          const int s_ = tjb * 4 + c;
-          if (s_ < S) MFw[s_ * UP + tib * 4 + r] = v;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int s_ = tjb * 4 + c;
+            if (s_ < S) MFw[s_ * UP + tib * 4 + r] = v[c];
+          }
         }
       }
     }
@@ -301,12 +331,12 @@ __global__ void __launch_bounds__(320, 2) channel_kernel(const KernelParams p) {
 }
 
 // ------------------------------------------------------------------- K2
-template <int UP>
+template <int UP, int NSO = 0>
 struct K2Geo {
   static constexpr int G = UP < 32 ? UP : 32;  // lanes per system
   static constexpr int RU = UP / G;            // rows per lane
   static constexpr int GPW = 32 / G;           // groups per warp
-  static constexpr int NS = UP == 32 ? 2 : 1;  // systems per group, interleaved
+  static constexpr int NS = NSO > 0 ? NSO : (UP == 32 ? 2 : 1);  // systems per group, interleaved
 };
 
 template <int UP>
@@ -330,9 +360,13 @@ struct K2Smem {
   }
 };
 
-template <int UP, bool EXACT>
-__global__ void __launch_bounds__(256, 3) solve_kernel(const KernelParams p) {
-  using GE = K2Geo<UP>;
+// GREG: row u of G held in registers for the whole subcarrier (U = 32, one
+// system per lane group at a time); p_j is read in 8-column chunks so the
+// loads of a chunk are in flight together, with 4 independent FMA chains.
+template <int UP, bool EXACT, int MINB = 3, int NSO = 0, bool GREG = false>
+__global__ void __launch_bounds__(256, MINB) solve_kernel(const KernelParams p) {
+  using GE = K2Geo<UP, NSO>;
+  static_assert(!GREG || (UP == 32 && GE::NS == 1), "GREG needs U = 32, one system per warp");
   constexpr int G = GE::G, RU = GE::RU, GPW = GE::GPW, NS = GE::NS;
   extern __shared__ __align__(128) unsigned char smem[];
   const int S = p.S, St = p.St, B = p.B, U = p.U;
@@ -372,8 +406,13 @@ __global__ void __launch_bounds__(256, 3) solve_kernel(const KernelParams p) {
     float gdiag[RU];
 #pragma unroll
     for (int m = 0; m < RU; ++m) gdiag[m] = Gs[(gl + m * G) * UP + gl + m * G].x;
+    float2 grow[GREG ? UP : 1];
+    if constexpr (GREG) {
+#pragma unroll
+      for (int j = 0; j < UP; ++j) grow[j] = cconj(Gs[j * UP + gl]);  // G[u][j]
+    }
     // warp-uniform trip count (the shuffles below use the full mask)
-    for (int wbase = warp * GPW * NS; wbase < nsys; wbase += n_slots) {
+    for (int wbase = warp * GPW * NS; wbase < ((p.debug & 16) ? 0 : nsys); wbase += n_slots) {
       const int base = wbase + grp * NS;
       int sys[NS];
       bool live[NS], down[NS];
@@ -421,7 +460,7 @@ __global__ void __launch_bounds__(256, 3) solve_kernel(const KernelParams p) {
         for (int m = 0; m < RU; ++m) f0[s][m] = f1[s][m] = f2[s][m] = 0.f;
       }
       __syncwarp();
-      for (int k = 1; k <= Kmax; ++k) {
+      for (int k = 1; k <= ((p.debug & 32) ? 0 : Kmax); ++k) {
         // e = (G + reg I) p: G read as column (conflict-free), p broadcast;
         // two partial sums per component shorten the FMA chains
         float2 e[NS][RU], e2[NS][RU];
@@ -429,6 +468,26 @@ __global__ void __launch_bounds__(256, 3) solve_kernel(const KernelParams p) {
         for (int s = 0; s < NS; ++s)
 #pragma unroll
           for (int m = 0; m < RU; ++m) e[s][m] = e2[s][m] = make_float2(0.f, 0.f);
+        if constexpr (GREG) {
+          const float4* prow = reinterpret_cast<const float4*>(Ps + (live[0] ? sys[0] : 0) * UP);
+          float2 e3 = make_float2(0.f, 0.f), e4 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int j0 = 0; j0 < UP; j0 += 8) {
+            float4 pj[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pj[q] = prow[j0 / 2 + q];
+            cfma(e[0][0], grow[j0 + 0], make_float2(pj[0].x, pj[0].y));
+            cfma(e2[0][0], grow[j0 + 1], make_float2(pj[0].z, pj[0].w));
+            cfma(e3, grow[j0 + 2], make_float2(pj[1].x, pj[1].y));
+            cfma(e4, grow[j0 + 3], make_float2(pj[1].z, pj[1].w));
+            cfma(e[0][0], grow[j0 + 4], make_float2(pj[2].x, pj[2].y));
+            cfma(e2[0][0], grow[j0 + 5], make_float2(pj[2].z, pj[2].w));
+            cfma(e3, grow[j0 + 6], make_float2(pj[3].x, pj[3].y));
+            cfma(e4, grow[j0 + 7], make_float2(pj[3].z, pj[3].w));
+          }
+          e[0][0] = cadd(e[0][0], e3);
+          e2[0][0] = cadd(e2[0][0], e4);
+        } else {
 #pragma unroll 4
         for (int j = 0; j < UP; j += 2) {
           float2 g0[RU], g1[RU];
@@ -447,6 +506,7 @@ __global__ void __launch_bounds__(256, 3) solve_kernel(const KernelParams p) {
               cfma(e2[s][m], g1[m], make_float2(pj.z, pj.w));
             }
           }
+        }
         }
         float curv[NS];
 #pragma unroll
@@ -554,7 +614,7 @@ __global__ void __launch_bounds__(256, 3) solve_kernel(const KernelParams p) {
           if (p.xhat) p.xhat[o] = xh;
           if (p.mu) p.mu[o] = mu_u;
           if (p.rho) p.rho[o] = rho_u;
-          if (p.llr) store_llrs_fast(xh, mu_u, rho_u, p.bits, p.llr + o * p.bits);
+          if (p.llr && !(p.debug & 64)) store_llrs_fast(xh, mu_u, rho_u, p.bits, p.llr + o * p.bits);
           if (p.status && gl == 0) p.status[sc * S + sys[s]] = ok ? 0 : 1;
         }
       }

@@ -134,3 +134,17 @@ def test_kernel_launch_accounting(gpu_ctx):
     run(gpu_ctx, cfg, H, Y)
     assert mid > before  # generator kernels
     assert gpu_ctx.kernel_launches - mid >= 1  # the hot path ran native kernels
+
+
+def test_overlapped_chunks_bitwise_equal(gpu_ctx, monkeypatch):
+    """The optional two-stream chunk overlap (CGMIMO_OVERLAP_CHUNKS) gives the
+    same bits as the default serial chunk loop."""
+    cfg = get_config("cfg2")
+    H, Y = gen(gpu_ctx, cfg)
+    a = run(gpu_ctx, cfg, H, Y)
+    monkeypatch.setenv("CGMIMO_OVERLAP_CHUNKS", "3")
+    b = run(gpu_ctx, cfg, H, Y)
+    monkeypatch.setenv("CGMIMO_OVERLAP_CHUNKS", "4")
+    c = run(gpu_ctx, cfg, H, Y)
+    for k in a:
+        assert torch.equal(a[k], b[k]) and torch.equal(a[k], c[k]), k
