@@ -15,7 +15,7 @@
 #include <vector>
 
 #include "../../include/cgmimo_b200.h"
-#include "cgm_split.cuh"
+#include "cgm_tc.cuh"
 
 struct cgm_ctx {
   int device = 0;
@@ -164,7 +164,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   p.k1_pair = sp.nstage;
   p.k1_spl = sp.spl;
   p.k1_wpp = sp.wpp;
-  const int nt1 = 32 * sp.wpp;
+  int nt1 = 32 * sp.wpp;
   cgm::K2Smem<UP> L2;
   L2.plan(p.B, p.S, p.St, Kmax, EXACT);
   if (L1.total > ctx->max_smem || L2.total > ctx->max_smem)
@@ -173,13 +173,47 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
                 L2.total, ctx->max_smem);
   cgm::WsOffsets W;
   W.plan(UP, p.S, p.K, EXACT);
-  auto k1 = cgm::channel_kernel<UP, EXACT>;
+  void (*k1)(cgm::KernelParams) = cgm::channel_kernel<UP, EXACT>;
   auto k2 = cgm::solve_kernel<UP, EXACT>;
-  CGM_CUDA(ctx, cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, L1.total));
+  int smem1 = L1.total;
+  // U = 32, natural layout, whole 64-antenna blocks: Gram + matched filter on
+  // the tensor cores (cgm_tc.cuh); CGMIMO_CHANNEL=ffma keeps the FFMA kernel
+  bool use_tc = false;
+  if constexpr (UP == 32) {
+    const char* force = std::getenv("CGMIMO_CHANNEL");
+    if (cgm::tc::supported(p.U, p.B, p.S, p.use_tma) && !(force && std::strcmp(force, "ffma") == 0)) {
+      cgm::tc::Smem T;
+      int nstg = 3;
+      T.plan(p.S, EXACT, nstg);
+      if (T.total > ctx->max_smem) T.plan(p.S, EXACT, nstg = 2);
+      if (T.total <= ctx->max_smem) {
+        use_tc = true;
+        p.k1_pair = nstg;
+        smem1 = T.total;
+        // epilogue / split warps (CGMIMO_TC_WARPS=EP,SP; SP = 0: the same
+        // warps do both).  Measured best (tools/microbench/tc_bench.cu):
+        // approx 8 + 8 specialised, exact 8 unified (the basis products
+        // then use all worker warps)
+        int nep = 8, nsp = EXACT ? 0 : 8;
+        if (const char* w = std::getenv("CGMIMO_TC_WARPS")) std::sscanf(w, "%d,%d", &nep, &nsp);
+        if (nep == 16 && nsp == 0)
+          k1 = cgm::channel_tc_kernel<EXACT, 16, 0>;
+        else if (nep == 4 && nsp == 8)
+          k1 = cgm::channel_tc_kernel<EXACT, 4, 8>;
+        else if (nep == 8 && nsp == 8)
+          k1 = cgm::channel_tc_kernel<EXACT, 8, 8>;
+        else
+          k1 = cgm::channel_tc_kernel<EXACT, 8, 0>, nep = 8, nsp = 0;
+        nt1 = 32 * (nep + nsp + 2);
+      }
+    }
+  }
+  CGM_CUDA(ctx, cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
   CGM_CUDA(ctx, cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, L2.total));
   int occ1 = 0;
-  CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k1, nt1, L1.total));
+  CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k1, nt1, smem1));
   if (occ1 < 1) return fail(ctx, CGM_EINVAL, "channel kernel does not fit on an SM");
+  if (use_tc) occ1 = 1;  // one CTA (and all 512 TMEM columns) per SM
   // K2 block: enough lane groups for every system at once (>= UP threads
   // for the exact extraction), at most 8 warps
   using GE = cgm::K2Geo<UP>;
@@ -241,7 +275,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       e3 = prof_event(ctx);
       cudaEventRecord(e0, s1);
     }
-    k1<<<static_cast<unsigned>(g1), nt1, L1.total, s1>>>(p);
+    k1<<<static_cast<unsigned>(g1), nt1, smem1, s1>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
     if (ctx->profiling) cudaEventRecord(e1, s1);
     if (overlap) {

@@ -59,6 +59,7 @@ struct KernelParams {
   float2* ws;     // split path: per-subcarrier workspace (G, MF, basis)
   long sc_base;   // split path: first subcarrier of this chunk
   int k1_pair, k1_spl, k1_wpp;  // channel kernel: subcarriers per CTA, k-parts, warps per part
+  unsigned long long* trace;    // microbenchmarks only: per-CTA event clocks (null in production)
 };
 
 // Per-axis Gray amplitude subsets (constellation.cpp:75-84), [qam][p][k],

@@ -95,6 +95,80 @@ __device__ __forceinline__ void k1_issue(const KernelParams& p, float2* Hs, floa
   if (p.S > 0) bulk_g2s(Ys, p.Y + sc * static_cast<long>(p.B) * p.S, ybytes, bar);
 }
 
+// Exact tracker, per subcarrier (detect.cpp:336-368 restated on a Chebyshev
+// basis): centre/half-width (c, d) of A = G + rho^-1 I and T_1..T_K of
+// Ahat = (A - cI)/d into the workspace, from G in shared memory.  Run by
+// threads [0, nt) (warps 0..nt/32-1); `sync` is a barrier over exactly those.
+template <int UP, class Sync>
+__device__ __forceinline__ void exact_basis(const KernelParams& p, const WsOffsets& W, float2* ws,
+                                            const float2* Gs, float2* T1, float2* Tm, float* misc,
+                                            int nt, Sync&& sync) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_gram = (UP / 4) * (UP / 4 + 1) / 2;
+  const int K = p.K;
+  if (warp == 0) {
+    // centre c = tr(A)/U and half-width d = 2 ||A - cI||_F / sqrt(U)
+    // (any d > 0 is exact algebra; this choice keeps the basis well
+    // conditioned in FP32)
+    float tr = 0.f, fr = 0.f;
+    for (int ii = lane; ii < UP; ii += 32) tr += Gs[ii * UP + ii].x + p.rho_inv_u;
+    tr = group_sum<32>(tr);
+    const float c = tr / UP;
+    for (int e = lane; e < UP * UP; e += 32) {
+      float2 a = Gs[e];
+      if (e / UP == e % UP) a.x += p.rho_inv_u - c;
+      fr += cnorm(a);
+    }
+    fr = group_sum<32>(fr);
+    float d = 2.f * sqrtf(fr / UP);
+    if (!(d > 1e-6f * fmaxf(fabsf(c), 1e-30f))) d = fmaxf(fabsf(c), 1.f);
+    if (lane == 0) {
+      misc[0] = c;
+      misc[1] = d;
+      ws[W.cd] = make_float2(c, d);
+    }
+  }
+  sync();
+  const float cc = misc[0], invd = 1.f / misc[1];
+  float2* Tw = ws + W.t;
+  for (int e = tid; e < UP * UP; e += nt) {  // T_1 = (A - cI)/d
+    float2 a = Gs[e];
+    if (e / UP == e % UP) a.x += p.rho_inv_u - cc;
+    a = cscale(invd, a);
+    T1[e] = a;
+    Tm[e] = a;
+    Tw[e] = a;
+  }
+  sync();
+  // T_{m+1} = 2 T_1 T_m - T_{m-1} (lower tiles + mirror; T_{m-1} via L2)
+  for (int m = 1; m < K; ++m) {
+    const float2* Tp = m >= 2 ? Tw + (m - 2) * UP * UP : nullptr;
+    float2* Tn = Tw + m * UP * UP;
+    tile_pass_nw(nt / 32, n_gram, 0, 1, T1, UP, Tm, UP, T1, 1, 1, UP,
+                 [&](int, int tib, int tjb, float2 (&a4)[4][4]) {
+#pragma unroll
+                   for (int r = 0; r < 4; ++r)
+#pragma unroll
+                     for (int c = 0; c < 4; ++c) {
+                       const int ii = tib * 4 + r, j = tjb * 4 + c;
+                       if (j > ii) continue;
+                       const float2 prev =
+                           Tp ? Tp[ii * UP + j] : make_float2(ii == j ? 1.f : 0.f, 0.f);
+                       float2 val = make_float2(2.f * a4[r][c].x - prev.x,
+                                                2.f * a4[r][c].y - prev.y);
+                       if (ii == j) val.y = 0.f;
+                       Tn[ii * UP + j] = val;
+                       if (ii != j) Tn[j * UP + ii] = cconj(val);
+                     }
+                 });
+    sync();
+    if (m + 1 < K) {  // T_m <- T_{m+1} for the next product
+      for (int e = tid; e < UP * UP; e += nt) Tm[e] = Tn[e];
+      sync();
+    }
+  }
+}
+
 // MINB: CTAs per SM the register budget is sized for; PIPE: software-
 // pipelined tile loop (operands of row k+1 in flight) or the plain one.
 template <int UP, bool EXACT, int MINB = 2, bool PIPE = true>
@@ -262,70 +336,7 @@ __global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p
       float4* dst = reinterpret_cast<float4*>(ws + W.g);
       for (int e = tid; e < UP * UP / 2; e += nt) dst[e] = src[e];
     }
-    if (EXACT && S > 0) {
-      const int K = p.K;
-      if (warp == 0) {
-        // centre c = tr(A)/U and half-width d = 2 ||A - cI||_F / sqrt(U)
-        // (any d > 0 is exact algebra; this choice keeps the basis well
-        // conditioned in FP32)
-        float tr = 0.f, fr = 0.f;
-        for (int ii = lane; ii < UP; ii += 32) tr += Gs[ii * UP + ii].x + p.rho_inv_u;
-        tr = group_sum<32>(tr);
-        const float c = tr / UP;
-        for (int e = lane; e < UP * UP; e += 32) {
-          float2 a = Gs[e];
-          if (e / UP == e % UP) a.x += p.rho_inv_u - c;
-          fr += cnorm(a);
-        }
-        fr = group_sum<32>(fr);
-        float d = 2.f * sqrtf(fr / UP);
-        if (!(d > 1e-6f * fmaxf(fabsf(c), 1e-30f))) d = fmaxf(fabsf(c), 1.f);
-        if (lane == 0) {
-          misc[0] = c;
-          misc[1] = d;
-          ws[W.cd] = make_float2(c, d);
-        }
-      }
-      __syncthreads();
-      const float cc = misc[0], invd = 1.f / misc[1];
-      float2* Tw = ws + W.t;
-      for (int e = tid; e < UP * UP; e += nt) {  // T_1 = (A - cI)/d
-        float2 a = Gs[e];
-        if (e / UP == e % UP) a.x += p.rho_inv_u - cc;
-        a = cscale(invd, a);
-        T1[e] = a;
-        Tm[e] = a;
-        Tw[e] = a;
-      }
-      __syncthreads();
-      // T_{m+1} = 2 T_1 T_m - T_{m-1} (lower tiles + mirror; T_{m-1} via L2)
-      for (int m = 1; m < K; ++m) {
-        const float2* Tp = m >= 2 ? Tw + (m - 2) * UP * UP : nullptr;
-        float2* Tn = Tw + m * UP * UP;
-        tile_pass_nw(nt / 32, n_gram, 0, 1, T1, UP, Tm, UP, T1, 1, 1, UP,
-                     [&](int, int tib, int tjb, float2 (&a4)[4][4]) {
-#pragma unroll
-                       for (int r = 0; r < 4; ++r)
-#pragma unroll
-                         for (int c = 0; c < 4; ++c) {
-                           const int ii = tib * 4 + r, j = tjb * 4 + c;
-                           if (j > ii) continue;
-                           const float2 prev =
-                               Tp ? Tp[ii * UP + j] : make_float2(ii == j ? 1.f : 0.f, 0.f);
-                           float2 val = make_float2(2.f * a4[r][c].x - prev.x,
-                                                    2.f * a4[r][c].y - prev.y);
-                           if (ii == j) val.y = 0.f;
-                           Tn[ii * UP + j] = val;
-                           if (ii != j) Tn[j * UP + ii] = cconj(val);
-                         }
-                     });
-        __syncthreads();
-        if (m + 1 < K) {  // T_m <- T_{m+1} for the next product
-          for (int e = tid; e < UP * UP; e += nt) Tm[e] = Tn[e];
-          __syncthreads();
-        }
-      }
-    }
+    if (EXACT && S > 0) exact_basis<UP>(p, W, ws, Gs, T1, Tm, misc, nt, [] { __syncthreads(); });
     __syncthreads();  // Gs is rewritten by the next subcarrier
   }
 }

@@ -148,3 +148,25 @@ def test_overlapped_chunks_bitwise_equal(gpu_ctx, monkeypatch):
     c = run(gpu_ctx, cfg, H, Y)
     for k in a:
         assert torch.equal(a[k], b[k]) and torch.equal(a[k], c[k]), k
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg4a_K8", "cfg5"])
+def test_tensor_core_channel_matches_ffma_channel(gpu_ctx, checker, monkeypatch, name):
+    """The tcgen05 channel kernel (bf16 x3 split, cgm_tc.cuh) and the FP32
+    FFMA channel kernel agree to FP32 rounding, and both match the oracle on
+    a subsample (U = 32, B a multiple of 64: the shapes the tensor-core path
+    takes)."""
+    cfg = get_config(name).scaled(600)
+    H, Y = gen(gpu_ctx, cfg)
+    tc = run(gpu_ctx, cfg, H, Y)
+    monkeypatch.setenv("CGMIMO_CHANNEL", "ffma")
+    ff = run(gpu_ctx, cfg, H, Y)
+    monkeypatch.delenv("CGMIMO_CHANNEL")
+    for k in ("xhat", "mu", "rho"):
+        a, b = tc[k].float(), ff[k].float()
+        assert float((a - b).abs().max()) <= 1e-4 + 1e-3 * float(b.abs().max()), k
+    assert int(tc["status"].sum()) == 0
+    idx = np.random.default_rng(2).choice(cfg.n_sc, size=8, replace=False)
+    want = checker.detect(H[idx].cpu().numpy(), Y[idx].cpu().numpy(), cfg.rho_u, cfg.n0, cfg.es,
+                          cfg.qam_bits, cfg.K, cfg.tracker, threads=8)
+    check_detect({k: v[idx].cpu().numpy() for k, v in tc.items()}, want, name + " tensor-core")
