@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/cgmimo_b200.h"
+#include "cgm_solve32.cuh"
 #include "cgm_tc.cuh"
 
 struct cgm_ctx {
@@ -174,7 +175,8 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   cgm::WsOffsets W;
   W.plan(UP, p.S, p.K, EXACT);
   void (*k1)(cgm::KernelParams) = cgm::channel_kernel<UP, EXACT>;
-  auto k2 = cgm::solve_kernel<UP, EXACT>;
+  void (*k2)(cgm::KernelParams) = cgm::solve_kernel<UP, EXACT>;
+  int smem2 = L2.total;
   int smem1 = L1.total;
   // U = 32, natural layout, whole 64-antenna blocks: Gram + matched filter on
   // the tensor cores (cgm_tc.cuh); CGMIMO_CHANNEL=ffma keeps the FFMA kernel
@@ -209,7 +211,24 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
     }
   }
   CGM_CUDA(ctx, cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
-  CGM_CUDA(ctx, cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, L2.total));
+  // K2: lane-per-row kernel by default; CGMIMO_SOLVE=tiles selects the
+  // block-tiled FFMA2 CG (cgm_solve32.cuh, U = 32, >= 8 systems), which
+  // issues ~25% fewer instructions but measured slower on cfg2 / cfg5 (lower
+  // occupancy: 50 vs 43 us on cfg2); CGMIMO_SOLVE_TS=2|4
+  bool use_s32 = false;
+  int ts2 = 2;
+  if constexpr (UP == 32) {
+    const char* force = std::getenv("CGMIMO_SOLVE");
+    if (const char* t = std::getenv("CGMIMO_SOLVE_TS")) ts2 = std::atoi(t) == 4 ? 4 : 2;
+    cgm::S32Smem T2;
+    T2.plan(p.B, p.S, p.St, Kmax, EXACT, ts2);
+    if (p.S + p.St >= 8 && T2.total <= ctx->max_smem && force && std::strcmp(force, "tiles") == 0) {
+      use_s32 = true;
+      k2 = ts2 == 4 ? cgm::solve32_kernel<EXACT, 4> : cgm::solve32_kernel<EXACT, 2>;
+      smem2 = T2.total;
+    }
+  }
+  CGM_CUDA(ctx, cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
   int occ1 = 0;
   CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k1, nt1, smem1));
   if (occ1 < 1) return fail(ctx, CGM_EINVAL, "channel kernel does not fit on an SM");
@@ -221,6 +240,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   int nw2 = (nsys + GE::GPW * GE::NS - 1) / (GE::GPW * GE::NS);
   if (EXACT) nw2 = std::max(nw2, std::max(4, UP / 32));
   nw2 = std::max(1, std::min(8, nw2));
+  if (use_s32) nw2 = ((nsys + ts2 - 1) / ts2 * 8 + 31) / 32;  // 8 threads per tile, whole warps
   // chunk so that workspace + channel (+ Y) of a chunk fit comfortably in L2
   const size_t per_sc = static_cast<size_t>(W.stride) * 8 + static_cast<size_t>(p.B) * p.U * 8 +
                         static_cast<size_t>(p.B) * p.S * 8;
@@ -283,7 +303,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       CGM_CUDA(ctx, cudaStreamWaitEvent(s2, ctx->ov_ev[1 + half], 0));
     }
     if (ctx->profiling) cudaEventRecord(e2, s2);
-    k2<<<static_cast<unsigned>(n), 32 * nw2, L2.total, s2>>>(p);
+    k2<<<static_cast<unsigned>(n), 32 * nw2, smem2, s2>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
     if (ctx->profiling) {
       cudaEventRecord(e3, s2);

@@ -16,19 +16,55 @@ __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cscale(float s, float2 a) { return make_float2(s * a.x, s * a.y); }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+// Packed FP32x2 (FFMA2) helpers.  One complex MAC is two fma.rn.f32x2,
+// (re, im) += (a.x, a.x) * (b.x, b.y) then (re, im) += (-a.y, a.y) * (b.y, b.x)
+// -- the same per-component FMA order as four scalar fmaf (bitwise equal
+// results) at half the instructions; the broadcast / swapped operands are
+// free SASS operand selectors.  As a drop-in inside float2 loops the
+// pack/unpack moves cost more than they save (measured), so cfma/cfma_conj
+// stay scalar unless CGM_FFMA2_CFMA is defined; the CG kernel
+// (cgm_solve32.cuh) keeps packed accumulators and uses ffma2 directly.
+__device__ __forceinline__ unsigned long long f2pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 f2unpack(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ void ffma2(unsigned long long& d, unsigned long long a,
+                                      unsigned long long b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
 // acc += a * b
 __device__ __forceinline__ void cfma(float2& acc, float2 a, float2 b) {
+#ifndef CGM_FFMA2_CFMA
   acc.x = fmaf(a.x, b.x, acc.x);
   acc.x = fmaf(-a.y, b.y, acc.x);
   acc.y = fmaf(a.x, b.y, acc.y);
   acc.y = fmaf(a.y, b.x, acc.y);
+#else
+  unsigned long long c = f2pack(acc.x, acc.y);
+  ffma2(c, f2pack(a.x, a.x), f2pack(b.x, b.y));
+  ffma2(c, f2pack(-a.y, a.y), f2pack(b.y, b.x));
+  acc = f2unpack(c);
+#endif
 }
 // acc += conj(a) * b
 __device__ __forceinline__ void cfma_conj(float2& acc, float2 a, float2 b) {
+#ifndef CGM_FFMA2_CFMA
   acc.x = fmaf(a.x, b.x, acc.x);
   acc.x = fmaf(a.y, b.y, acc.x);
   acc.y = fmaf(a.x, b.y, acc.y);
   acc.y = fmaf(-a.y, b.x, acc.y);
+#else
+  unsigned long long c = f2pack(acc.x, acc.y);
+  ffma2(c, f2pack(a.x, a.x), f2pack(b.x, b.y));
+  ffma2(c, f2pack(a.y, -a.y), f2pack(b.y, b.x));
+  acc = f2unpack(c);
+#endif
 }
 __device__ __forceinline__ float cnorm(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }
 

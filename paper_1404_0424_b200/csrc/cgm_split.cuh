@@ -371,6 +371,206 @@ struct K2Smem {
   }
 };
 
+// ---------------------------------------------------------- solve tails
+// Shared by solve_kernel and solve32_kernel, after the CG: Vs[sys][u] holds
+// v, sys_st the breakdown flags, hist the (alpha, beta) history.
+// Exact tracker (detect.cpp:330-395): FP64 coefficient recursion per system,
+// extraction of mu / nu^2 from the Chebyshev basis, then all outputs.
+template <int UP>
+__device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float2* ws,
+                                              const WsOffsets& W, long sc, int Kmax,
+                                              const float* hist, float* coef, float* MUs,
+                                              float* RHOs, const float2* Vs,
+                                              const uint8_t* sys_st) {
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const int S = p.S, U = p.U;
+    const int K = p.K;
+    const float2 cdv = ws[W.cd];
+    const double cc = cdv.x, dd = cdv.y;
+    for (int s = tid; s < S; s += nt) {
+      // three-term recursion (detect.cpp:336-368) on Chebyshev coefficients, FP64
+      double l0[kMaxK + 2], l1[kMaxK + 2], l2[kMaxK + 2], tmp[kMaxK + 2], d1[kMaxK + 2];
+      const int n = K + 2;
+      for (int m = 0; m < n; ++m) l0[m] = l1[m] = l2[m] = 0.0;
+      double a_m1 = 1.0, a_m2 = 1.0, b_m1 = 0.0, b_m2 = 0.0;
+      auto mulA = [&](const double* x, double* out) {
+        // A T_0 = c T_0 + d T_1;  A T_m = c T_m + d/2 (T_{m+1} + T_{m-1})
+        for (int m = 0; m < n; ++m) out[m] = cc * x[m];
+        for (int m = 0; m < n; ++m) {
+          const double h = dd * x[m];
+          if (m == 0) {
+            out[1] += h;
+          } else {
+            if (m + 1 < n) out[m + 1] += 0.5 * h;
+            out[m - 1] += 0.5 * h;
+          }
+        }
+      };
+      for (int k = 1; k <= K; ++k) {
+        const double a = hist[(s * Kmax + (k - 1)) * 2 + 0];
+        const double bb = hist[(s * Kmax + (k - 1)) * 2 + 1];
+        if (k == 1) {
+          for (int m = 0; m < n; ++m) { l2[m] = l1[m]; l1[m] = l0[m]; l0[m] = 0.0; }
+          l0[0] = a;  // L_1 = alpha_1 I
+        } else {
+          const double c1 = a * (1.0 + b_m1) / a_m1, c2 = a * b_m2 / a_m2;
+          for (int m = 0; m < n; ++m) d1[m] = l0[m] - l1[m];
+          mulA(d1, tmp);
+          for (int m = 0; m < n; ++m) {
+            const double nx = l0[m] + c1 * d1[m] - a * tmp[m] - c2 * (l1[m] - l2[m]);
+            l2[m] = l1[m];
+            l1[m] = l0[m];
+            l0[m] = nx;
+          }
+        }
+        a_m2 = a_m1; a_m1 = a; b_m2 = b_m1; b_m1 = bb;
+      }
+      // B = L (A - rho^-1 I)  (G = unregularised A, detect.cpp:215)
+      mulA(l0, tmp);
+      float* cl = coef + s * 2 * (K + 2);
+      float* cb = cl + (K + 2);
+      for (int m = 0; m < n; ++m) {
+        cl[m] = static_cast<float>(l0[m]);
+        cb[m] = static_cast<float>(tmp[m] - static_cast<double>(p.rho_inv_u) * l0[m]);
+      }
+    }
+    __syncthreads();
+    // extraction (detect.cpp:375-395): thread <-> (row i, pair of systems);
+    // each T_m(i, j) is read once (L1/L2) and used for both systems
+    const float2* Tw = ws + W.t;
+    const int ngrp = nt / UP;
+    const int i = tid % UP, g = tid / UP;
+    if (g < ngrp) {
+      for (int s0 = g; s0 < S; s0 += 2 * ngrp) {
+        const int s1 = s0 + ngrp;
+        const bool has1 = s1 < S;
+        const float* cl0 = coef + s0 * 2 * (K + 2);
+        const float* cb0 = cl0 + (K + 2);
+        const float* cl1 = coef + (has1 ? s1 : s0) * 2 * (K + 2);
+        const float* cb1 = cl1 + (K + 2);
+        float ib2[2] = {0.f, 0.f}, ibl[2] = {0.f, 0.f}, mu_i[2] = {0.f, 0.f};
+        for (int j = 0; j < UP; ++j) {
+          float2 B0 = make_float2(i == j ? cb0[0] : 0.f, 0.f);
+          float2 L0 = make_float2(i == j ? cl0[0] : 0.f, 0.f);
+          float2 B1 = make_float2(i == j ? cb1[0] : 0.f, 0.f);
+          float2 L1 = make_float2(i == j ? cl1[0] : 0.f, 0.f);
+          for (int m = 1; m <= K; ++m) {
+            const float2 t = cconj(__ldg(Tw + (m - 1) * UP * UP + j * UP + i));  // T_m[i][j]
+            B0.x = fmaf(cb0[m], t.x, B0.x); B0.y = fmaf(cb0[m], t.y, B0.y);
+            B1.x = fmaf(cb1[m], t.x, B1.x); B1.y = fmaf(cb1[m], t.y, B1.y);
+            if (m < K) {
+              L0.x = fmaf(cl0[m], t.x, L0.x); L0.y = fmaf(cl0[m], t.y, L0.y);
+              L1.x = fmaf(cl1[m], t.x, L1.x); L1.y = fmaf(cl1[m], t.y, L1.y);
+            }
+          }
+          if (j == i) { mu_i[0] = B0.x; mu_i[1] = B1.x; }
+          else { ib2[0] += cnorm(B0); ib2[1] += cnorm(B1); }
+          ibl[0] += B0.x * L0.x + B0.y * L0.y;  // Re(B_ij conj(L_ij))
+          ibl[1] += B1.x * L1.x + B1.y * L1.y;
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (t == 1 && !has1) break;
+          const int s = t ? s1 : s0;
+          const float nu2 = ib2[t] * p.es + ibl[t] * p.n0;
+          MUs[s * UP + i] = mu_i[t];
+          RHOs[s * UP + i] = nu2 <= 0.f ? 0.f : mu_i[t] * mu_i[t] / nu2;  // safe_rho
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < S * U; e += nt) {
+      const int s = e / U, u = e - s * U;
+      const long o = (sc * S + s) * static_cast<long>(U) + u;
+      const bool ok = sys_st[s] == 0;
+      const float2 xh = ok ? Vs[s * UP + u] : make_float2(0.f, 0.f);
+      const float m = ok ? MUs[s * UP + u] : 0.f;
+      const float rr = ok ? RHOs[s * UP + u] : 0.f;
+      if (p.xhat) p.xhat[o] = xh;
+      if (p.mu) p.mu[o] = m;
+      if (p.rho) p.rho[o] = rr;
+      if (p.llr) store_llrs_fast(xh, m, rr, p.bits, p.llr + o * p.bits);
+    }
+    if (p.status)
+      for (int s = tid; s < S; s += nt) p.status[sc * S + s] = sys_st[s];
+  }
+
+// Precoder (precode.cpp:22-71): q = H_d^H v, gain = ||q||, s = q / gain.
+template <int UP>
+__device__ __forceinline__ void k2_precode_tail(const KernelParams& p, long sc, const float2* Vs,
+                                                float2* Qs, float* gpart,
+                                                const uint8_t* sys_st) {
+  const int nt = blockDim.x, nw = nt >> 5, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int S = p.S, St = p.St, B = p.B, U = p.U;
+  (void)nt;
+  // ------------------------------------------------ precode q = H_d^H v
+  // q_b = sum_u H_u[b][u] v_u = sum_u conj(H_d[u][b]) v_u (precode.cpp:69),
+  // then gain = ||q||, s = q / gain, zero_input when ||q|| vanishes (:22-36)
+    const int nrb = (B + 31) / 32;
+    for (int rb = warp; rb < nrb; rb += nw) {
+      const int bidx = rb * 32 + lane;
+      const bool okb = bidx < B;
+      const int bb = okb ? bidx : 0;
+      for (int ts0 = 0; ts0 < St; ts0 += 8) {
+        float2 acc[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[t] = make_float2(0.f, 0.f);
+        if (p.hd_layout) {
+          const float2* hd = p.H + sc * static_cast<long>(U) * B;  // [U][B], coalesced in b
+          for (int u = 0; u < U; ++u) {
+            const float2 h = cconj(__ldg(hd + u * B + bb));
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+              if (ts0 + t < St) cfma(acc[t], h, Vs[(S + ts0 + t) * UP + u]);
+          }
+        } else {
+          const float2* hu = p.H + sc * static_cast<long>(B) * UP + bb * UP;  // row b of H_u
+#pragma unroll 4
+          for (int u = 0; u < UP; u += 2) {
+            const float4 h = __ldg(reinterpret_cast<const float4*>(hu + u));
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              if (ts0 + t < St) {
+                const float4 vv = *reinterpret_cast<const float4*>(Vs + (S + ts0 + t) * UP + u);
+                cfma(acc[t], make_float2(h.x, h.y), make_float2(vv.x, vv.y));
+                cfma(acc[t], make_float2(h.z, h.w), make_float2(vv.z, vv.w));
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (ts0 + t < St) {
+            if (okb) Qs[(ts0 + t) * B + bidx] = acc[t];
+            float nrm = okb ? cnorm(acc[t]) : 0.f;
+            nrm = group_sum<32>(nrm);
+            if (lane == 0) gpart[rb * St + ts0 + t] = nrm;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (int ts = warp; ts < St; ts += nw) {
+      const int sysi = S + ts;
+      const bool ok = sys_st[sysi] == 0;
+      float nrm = 0.f;
+      for (int rb = 0; rb < nrb; ++rb) nrm += gpart[rb * St + ts];  // fixed order
+      const float g = sqrtf(nrm);
+      const bool zero = ok && !(g > 0.f);
+      const float inv = (ok && !zero) ? 1.f / g : 0.f;
+      const long ob = (sc * St + ts) * static_cast<long>(B);
+      for (int b = lane; b < B; b += 32) {
+        const float2 q = Qs[ts * B + b];
+        if (p.q) p.q[ob + b] = ok ? q : make_float2(0.f, 0.f);
+        if (p.s_out) p.s_out[ob + b] = cscale(inv, q);
+      }
+      if (lane == 0) {
+        if (p.gain) p.gain[sc * St + ts] = (ok && !zero) ? g : 0.f;
+        if (p.pstatus) p.pstatus[sc * St + ts] = ok ? (zero ? 2 : 0) : 1;
+      }
+    }
+  }
+
 // GREG: row u of G held in registers for the whole subcarrier (U = 32, one
 // system per lane group at a time); p_j is read in 8-column chunks so the
 // loads of a chunk are in flight together, with 4 independent FMA chains.
@@ -635,185 +835,12 @@ __global__ void __launch_bounds__(256, MINB) solve_kernel(const KernelParams p) 
   // ------------------------------------------ exact tracker extraction
   if (EXACT && S > 0) {
     __syncthreads();
-    const int K = p.K;
-    const float2 cdv = ws[W.cd];
-    const double cc = cdv.x, dd = cdv.y;
-    for (int s = tid; s < S; s += nt) {
-      // three-term recursion (detect.cpp:336-368) on Chebyshev coefficients, FP64
-      double l0[kMaxK + 2], l1[kMaxK + 2], l2[kMaxK + 2], tmp[kMaxK + 2], d1[kMaxK + 2];
-      const int n = K + 2;
-      for (int m = 0; m < n; ++m) l0[m] = l1[m] = l2[m] = 0.0;
-      double a_m1 = 1.0, a_m2 = 1.0, b_m1 = 0.0, b_m2 = 0.0;
-      auto mulA = [&](const double* x, double* out) {
-        // A T_0 = c T_0 + d T_1;  A T_m = c T_m + d/2 (T_{m+1} + T_{m-1})
-        for (int m = 0; m < n; ++m) out[m] = cc * x[m];
-        for (int m = 0; m < n; ++m) {
-          const double h = dd * x[m];
-          if (m == 0) {
-            out[1] += h;
-          } else {
-            if (m + 1 < n) out[m + 1] += 0.5 * h;
-            out[m - 1] += 0.5 * h;
-          }
-        }
-      };
-      for (int k = 1; k <= K; ++k) {
-        const double a = hist[(s * Kmax + (k - 1)) * 2 + 0];
-        const double bb = hist[(s * Kmax + (k - 1)) * 2 + 1];
-        if (k == 1) {
-          for (int m = 0; m < n; ++m) { l2[m] = l1[m]; l1[m] = l0[m]; l0[m] = 0.0; }
-          l0[0] = a;  // L_1 = alpha_1 I
-        } else {
-          const double c1 = a * (1.0 + b_m1) / a_m1, c2 = a * b_m2 / a_m2;
-          for (int m = 0; m < n; ++m) d1[m] = l0[m] - l1[m];
-          mulA(d1, tmp);
-          for (int m = 0; m < n; ++m) {
-            const double nx = l0[m] + c1 * d1[m] - a * tmp[m] - c2 * (l1[m] - l2[m]);
-            l2[m] = l1[m];
-            l1[m] = l0[m];
-            l0[m] = nx;
-          }
-        }
-        a_m2 = a_m1; a_m1 = a; b_m2 = b_m1; b_m1 = bb;
-      }
-      // B = L (A - rho^-1 I)  (G = unregularised A, detect.cpp:215)
-      mulA(l0, tmp);
-      float* cl = coef + s * 2 * (K + 2);
-      float* cb = cl + (K + 2);
-      for (int m = 0; m < n; ++m) {
-        cl[m] = static_cast<float>(l0[m]);
-        cb[m] = static_cast<float>(tmp[m] - static_cast<double>(p.rho_inv_u) * l0[m]);
-      }
-    }
-    __syncthreads();
-    // extraction (detect.cpp:375-395): thread <-> (row i, pair of systems);
-    // each T_m(i, j) is read once (L1/L2) and used for both systems
-    const float2* Tw = ws + W.t;
-    const int ngrp = nt / UP;
-    const int i = tid % UP, g = tid / UP;
-    if (g < ngrp) {
-      for (int s0 = g; s0 < S; s0 += 2 * ngrp) {
-        const int s1 = s0 + ngrp;
-        const bool has1 = s1 < S;
-        const float* cl0 = coef + s0 * 2 * (K + 2);
-        const float* cb0 = cl0 + (K + 2);
-        const float* cl1 = coef + (has1 ? s1 : s0) * 2 * (K + 2);
-        const float* cb1 = cl1 + (K + 2);
-        float ib2[2] = {0.f, 0.f}, ibl[2] = {0.f, 0.f}, mu_i[2] = {0.f, 0.f};
-        for (int j = 0; j < UP; ++j) {
-          float2 B0 = make_float2(i == j ? cb0[0] : 0.f, 0.f);
-          float2 L0 = make_float2(i == j ? cl0[0] : 0.f, 0.f);
-          float2 B1 = make_float2(i == j ? cb1[0] : 0.f, 0.f);
-          float2 L1 = make_float2(i == j ? cl1[0] : 0.f, 0.f);
-          for (int m = 1; m <= K; ++m) {
-            const float2 t = cconj(__ldg(Tw + (m - 1) * UP * UP + j * UP + i));  // T_m[i][j]
-            B0.x = fmaf(cb0[m], t.x, B0.x); B0.y = fmaf(cb0[m], t.y, B0.y);
-            B1.x = fmaf(cb1[m], t.x, B1.x); B1.y = fmaf(cb1[m], t.y, B1.y);
-            if (m < K) {
-              L0.x = fmaf(cl0[m], t.x, L0.x); L0.y = fmaf(cl0[m], t.y, L0.y);
-              L1.x = fmaf(cl1[m], t.x, L1.x); L1.y = fmaf(cl1[m], t.y, L1.y);
-            }
-          }
-          if (j == i) { mu_i[0] = B0.x; mu_i[1] = B1.x; }
-          else { ib2[0] += cnorm(B0); ib2[1] += cnorm(B1); }
-          ibl[0] += B0.x * L0.x + B0.y * L0.y;  // Re(B_ij conj(L_ij))
-          ibl[1] += B1.x * L1.x + B1.y * L1.y;
-        }
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (t == 1 && !has1) break;
-          const int s = t ? s1 : s0;
-          const float nu2 = ib2[t] * p.es + ibl[t] * p.n0;
-          MUs[s * UP + i] = mu_i[t];
-          RHOs[s * UP + i] = nu2 <= 0.f ? 0.f : mu_i[t] * mu_i[t] / nu2;  // safe_rho
-        }
-      }
-    }
-    __syncthreads();
-    for (int e = tid; e < S * U; e += nt) {
-      const int s = e / U, u = e - s * U;
-      const long o = (sc * S + s) * static_cast<long>(U) + u;
-      const bool ok = sys_st[s] == 0;
-      const float2 xh = ok ? Vs[s * UP + u] : make_float2(0.f, 0.f);
-      const float m = ok ? MUs[s * UP + u] : 0.f;
-      const float rr = ok ? RHOs[s * UP + u] : 0.f;
-      if (p.xhat) p.xhat[o] = xh;
-      if (p.mu) p.mu[o] = m;
-      if (p.rho) p.rho[o] = rr;
-      if (p.llr) store_llrs_fast(xh, m, rr, p.bits, p.llr + o * p.bits);
-    }
-    if (p.status)
-      for (int s = tid; s < S; s += nt) p.status[sc * S + s] = sys_st[s];
+    k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st);
   }
-
   // ------------------------------------------------ precode q = H_d^H v
-  // q_b = sum_u H_u[b][u] v_u = sum_u conj(H_d[u][b]) v_u (precode.cpp:69),
-  // then gain = ||q||, s = q / gain, zero_input when ||q|| vanishes (:22-36)
   if (St > 0) {
     __syncthreads();
-    const int nrb = (B + 31) / 32;
-    for (int rb = warp; rb < nrb; rb += nw) {
-      const int bidx = rb * 32 + lane;
-      const bool okb = bidx < B;
-      const int bb = okb ? bidx : 0;
-      for (int ts0 = 0; ts0 < St; ts0 += 8) {
-        float2 acc[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) acc[t] = make_float2(0.f, 0.f);
-        if (p.hd_layout) {
-          const float2* hd = p.H + sc * static_cast<long>(U) * B;  // [U][B], coalesced in b
-          for (int u = 0; u < U; ++u) {
-            const float2 h = cconj(__ldg(hd + u * B + bb));
-#pragma unroll
-            for (int t = 0; t < 8; ++t)
-              if (ts0 + t < St) cfma(acc[t], h, Vs[(S + ts0 + t) * UP + u]);
-          }
-        } else {
-          const float2* hu = p.H + sc * static_cast<long>(B) * UP + bb * UP;  // row b of H_u
-#pragma unroll 4
-          for (int u = 0; u < UP; u += 2) {
-            const float4 h = __ldg(reinterpret_cast<const float4*>(hu + u));
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-              if (ts0 + t < St) {
-                const float4 vv = *reinterpret_cast<const float4*>(Vs + (S + ts0 + t) * UP + u);
-                cfma(acc[t], make_float2(h.x, h.y), make_float2(vv.x, vv.y));
-                cfma(acc[t], make_float2(h.z, h.w), make_float2(vv.z, vv.w));
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          if (ts0 + t < St) {
-            if (okb) Qs[(ts0 + t) * B + bidx] = acc[t];
-            float nrm = okb ? cnorm(acc[t]) : 0.f;
-            nrm = group_sum<32>(nrm);
-            if (lane == 0) gpart[rb * St + ts0 + t] = nrm;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    for (int ts = warp; ts < St; ts += nw) {
-      const int sysi = S + ts;
-      const bool ok = sys_st[sysi] == 0;
-      float nrm = 0.f;
-      for (int rb = 0; rb < nrb; ++rb) nrm += gpart[rb * St + ts];  // fixed order
-      const float g = sqrtf(nrm);
-      const bool zero = ok && !(g > 0.f);
-      const float inv = (ok && !zero) ? 1.f / g : 0.f;
-      const long ob = (sc * St + ts) * static_cast<long>(B);
-      for (int b = lane; b < B; b += 32) {
-        const float2 q = Qs[ts * B + b];
-        if (p.q) p.q[ob + b] = ok ? q : make_float2(0.f, 0.f);
-        if (p.s_out) p.s_out[ob + b] = cscale(inv, q);
-      }
-      if (lane == 0) {
-        if (p.gain) p.gain[sc * St + ts] = (ok && !zero) ? g : 0.f;
-        if (p.pstatus) p.pstatus[sc * St + ts] = ok ? (zero ? 2 : 0) : 1;
-      }
-    }
+    k2_precode_tail<UP>(p, sc, Vs, Qs, gpart, sys_st);
   }
 }
 

@@ -170,3 +170,32 @@ def test_tensor_core_channel_matches_ffma_channel(gpu_ctx, checker, monkeypatch,
     want = checker.detect(H[idx].cpu().numpy(), Y[idx].cpu().numpy(), cfg.rho_u, cfg.n0, cfg.es,
                           cfg.qam_bits, cfg.K, cfg.tracker, threads=8)
     check_detect({k: v[idx].cpu().numpy() for k, v in tc.items()}, want, name + " tensor-core")
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg5"])
+def test_tiled_cg_kernel_matches_default(gpu_ctx, monkeypatch, name):
+    """The optional block-tiled FFMA2 CG kernel (CGMIMO_SOLVE=tiles,
+    cgm_solve32.cuh) agrees with the default lane-per-row kernel to FP32
+    rounding, uplink and (cfg5) downlink."""
+    cfg = get_config(name).scaled(300)
+    H, Y = gen(gpu_ctx, cfg)
+    if cfg.kind == "both":
+        T = gpu_ctx.generate_symbols(cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits)
+        call = lambda: gpu_ctx.detect_precode_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits,
+                                                 cfg.K, cfg.tracker, T, cfg.rho_d, cfg.K)
+    else:
+        call = lambda: gpu_ctx.detect_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                                         cfg.tracker)
+    a = call()
+    torch.cuda.synchronize()
+    monkeypatch.setenv("CGMIMO_SOLVE", "tiles")
+    b = call()
+    torch.cuda.synchronize()
+    monkeypatch.delenv("CGMIMO_SOLVE")
+    for k in a:
+        if a[k].dtype == torch.uint8:
+            assert torch.equal(a[k], b[k]), k
+            continue
+        x, y = a[k].float(), b[k].float()
+        tol = 1e-4 + 1e-3 * float(x.abs().max()) if k != "llr" else 1e-3 * 64
+        assert float((x - y).abs().max()) <= tol, k
