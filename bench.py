@@ -104,12 +104,14 @@ class ClockSampler:
 
 
 def read_traffic(cfg_name: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    """dram bytes (read + write) per launch of each kernel, from the committed
+    ncu --set full capture: {"channel": B, "solve": B} or None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
-        return json.load(f).get(cfg_name)
+        v = json.load(f).get(cfg_name)
+    return v if isinstance(v, dict) else None
 
 
 def reference_arm(args, rank, world):
@@ -307,36 +309,45 @@ def ours_arm(args, rank, world, local_rank):
                   "bytes_to_root": llr.numel() * 4 * (world - 1)}
 
     # -------------------------------------------------------------- roofline
+    # per kernel, from the CUDA-event durations of each launch on its stream:
+    #   channel kernel: HBM-bound (Gram + matched filter at ~20 FLOP/B sits
+    #     far below the tensor-core ridge), algorithmic bytes = H + y
+    #   solve kernel: FP32-core-bound, algorithmic flops = CG + tracker + LLR
+    # "roofline" is the kernel with the larger share of the step.
     peaks = load_peaks()
     fp32_peak = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12  # TFLOP/s
+    fp32_src = (f"derived: 148 SMs x 128 FP32 lanes x 2 x {peaks['sm_max_mhz']:.0f} MHz "
+                f"(sm_max_mhz from {peaks['source']}; no measured FP32 figure exists)")
     flops_launch = cfg.flops_per_vector() * cfg.vectors
     bytes_launch = cfg.bytes_per_vector() * cfg.vectors
-    t_fp32 = flops_launch / (fp32_peak * 1e12)
-    t_hbm = bytes_launch / (peaks["hbm_gbs"] * 1e9)
-    k_s = kernel_ms / 1e3
-    traffic = read_traffic(cfg.name)
-    if t_fp32 >= t_hbm:
-        roof = {"bound": "fp32", "achieved": flops_launch / k_s / 1e12, "peak": fp32_peak,
-                "unit": "TFLOP/s",
-                "peak_source": f"derived: 148 SMs x 128 FP32 lanes x 2 x {peaks['sm_max_mhz']:.0f} MHz "
-                               f"(sm_max_mhz from {peaks['source']}; no measured FP32 figure exists)"}
-    else:
-        roof = {"bound": "hbm", "achieved": bytes_launch / k_s / 1e9, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "peak_source": f"hbm_gbs of {peaks['source']}"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = traffic
-    roof["algorithmic_per_launch"] = {"flops": flops_launch, "bytes": bytes_launch,
-                                      "flops_per_vector": cfg.flops_per_vector(),
-                                      "bytes_per_vector": cfg.bytes_per_vector()}
-    roof["hbm_achieved_gbs"] = bytes_launch / k_s / 1e9
-    roof["kernel"] = ("channel_kernel (Gram + matched filter [+ Chebyshev basis]) + solve_kernel "
-                      "(CG + SINR tracker + LLR [+ precoder]), one pair per L2 chunk; measured as "
-                      "the sum of their CUDA-event durations on the launch stream")
-    roof["kernel_ms"] = kernel_ms
-    roof["kernels"] = {"channel_ms_per_step": ch_ms / args.steps,
-                       "solve_ms_per_step": sv_ms / args.steps,
-                       "channel_share": ch_ms / max(ch_ms + sv_ms, 1e-12),
-                       "launch_pairs_per_step": n_pairs / args.steps}
+    ch_s = ch_ms / args.steps / 1e3
+    sv_s = sv_ms / args.steps / 1e3
+    traffic = read_traffic(cfg.name) or {}
+    k_ch = {"kernel": "channel (Gram + matched filter [+ Chebyshev basis]; tcgen05 for U = 32)",
+            "bound": "hbm", "unit": "GB/s", "peak": peaks["hbm_gbs"],
+            "peak_source": f"hbm_gbs of {peaks['source']}",
+            "algorithmic_bytes": cfg.channel_bytes_per_vector() * cfg.vectors,
+            "algorithmic_flops": cfg.channel_flops_per_vector() * cfg.vectors,
+            "ms": ch_s * 1e3, "traffic": traffic.get("channel")}
+    k_ch["achieved"] = k_ch["algorithmic_bytes"] / ch_s / 1e9 if ch_s > 0 else None
+    k_sv = {"kernel": "solve (CG + SINR tracker + LLR [+ precoder])", "bound": "fp32",
+            "unit": "TFLOP/s", "peak": fp32_peak, "peak_source": fp32_src,
+            "algorithmic_flops": cfg.solve_flops_per_vector() * cfg.vectors,
+            "algorithmic_bytes": cfg.solve_bytes_per_vector() * cfg.vectors,
+            "ms": sv_s * 1e3, "traffic": traffic.get("solve")}
+    k_sv["achieved"] = k_sv["algorithmic_flops"] / sv_s / 1e12 if sv_s > 0 else None
+    for k in (k_ch, k_sv):
+        k["frac"] = k["achieved"] / k["peak"] if k["achieved"] else None
+    dom = k_sv if sv_s >= ch_s else k_ch
+    roof = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
+            "unit": dom["unit"], "frac": dom["frac"], "traffic": dom["traffic"],
+            "peak_source": dom["peak_source"], "kernel": dom["kernel"],
+            "share_of_step": (sv_s if dom is k_sv else ch_s) / max(ch_s + sv_s, 1e-12),
+            "kernels": {"channel": k_ch, "solve": k_sv},
+            "pair": {"kernel_ms": kernel_ms, "launch_pairs_per_step": n_pairs / args.steps,
+                     "algorithmic_flops": flops_launch, "algorithmic_bytes": bytes_launch,
+                     "tflops": flops_launch / (kernel_ms / 1e3) / 1e12,
+                     "hbm_gbs": bytes_launch / (kernel_ms / 1e3) / 1e9}}
 
     # ----------------------------------------------------------- CPU baseline
     cpu = None

@@ -79,6 +79,29 @@ class Config:
             b += 8 * U + 8 * B + 4
         return b
 
+    # ---- the same counts split by kernel (bench.py's per-kernel rooflines)
+    def channel_flops_per_vector(self) -> float:
+        """Gram (+ matched filter) of the channel kernel."""
+        B, U, S = self.B, self.U, self.S
+        f = 4 * B * U * (U + 1) / S
+        if self.kind in ("uplink", "both"):
+            f += 8 * B * U
+        return f
+
+    def channel_bytes_per_vector(self) -> float:
+        """H (shared by S vectors) + y read by the channel kernel."""
+        b = 8 * self.B * self.U / self.S
+        if self.kind in ("uplink", "both"):
+            b += 8 * self.B
+        return b
+
+    def solve_flops_per_vector(self) -> float:
+        return self.flops_per_vector() - self.channel_flops_per_vector()
+
+    def solve_bytes_per_vector(self) -> float:
+        """Outputs written by the solve kernel (+ t read, H re-read by the precoder)."""
+        return self.bytes_per_vector() - self.channel_bytes_per_vector()
+
     def scaled(self, n_sc: int) -> "Config":
         return replace(self, n_sc=n_sc)
 
