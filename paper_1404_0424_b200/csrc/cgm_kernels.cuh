@@ -200,6 +200,64 @@ __device__ __forceinline__ void tile_pass(int n_lower, int n_other, int nsb, con
   tile_pass_nw(NT / 32, n_lower, n_other, nsb, X, ldx, Yl, ldyl, Zs, ldz, zcols, klen, fn);
 }
 
+// ------------------------------------------------ Chebyshev interval
+// Interval [lo, hi] containing the spectrum of A = G + reg I for the exact
+// tracker's basis T_m((A - cI)/d), c = (lo + hi)/2, d = (hi - lo)/2:
+// lo = reg (G >= 0), hi = 1.1 x a 6-step power-iteration estimate of
+// lambda_max.  A positive interval keeps the Chebyshev coefficients of
+// L_K ~ A^-1 small; the round-1 choice c = tr(A)/U, d = 2 ||A - cI||_F /
+// sqrt(U) reached below 0 at weak regularisation and lost up to 1.5e-3 in
+// rho at K = 16 (tools/fp32_tracker_study.py "weak": 1.5e-6 with this one).
+// One warp; G Hermitian in smem (read by columns); xs: UP float2 scratch.
+template <int UP>
+__device__ __forceinline__ float2 cheb_interval(const float2* Gs, float reg, float2* xs, int lane) {
+  constexpr int RU = UP < 32 ? 1 : UP / 32;
+  float2 xr[RU];
+#pragma unroll
+  for (int m = 0; m < RU; ++m) {
+    const int i = lane + 32 * m;
+    xr[m] = make_float2(i < UP ? 1.f : 0.f, 0.f);
+    if (i < UP) xs[i] = xr[m];
+  }
+  __syncwarp();
+  float lam = reg;
+  for (int it = 0; it <= 6; ++it) {
+    float2 y[RU];
+    float nrm = 0.f, ray = 0.f;
+#pragma unroll
+    for (int m = 0; m < RU; ++m) {
+      const int i = lane + 32 * m;
+      y[m] = make_float2(0.f, 0.f);
+      if (i < UP) {
+        // (A x)_i = sum_j conj(G[j][i]) x_j + reg x_i  (G Hermitian; column reads)
+        for (int j = 0; j < UP; ++j) cfma_conj(y[m], Gs[j * UP + i], xs[j]);
+        y[m].x = fmaf(reg, xr[m].x, y[m].x);
+        y[m].y = fmaf(reg, xr[m].y, y[m].y);
+      }
+      nrm += cnorm(y[m]);
+      ray += xr[m].x * y[m].x + xr[m].y * y[m].y;
+    }
+    nrm = group_sum<32>(nrm);
+    ray = group_sum<32>(ray);
+    if (it > 0) lam = ray;  // Rayleigh quotient x^H A x, ||x|| = 1
+    const float inv = nrm > 0.f ? rsqrtf(nrm) : 0.f;
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < RU; ++m) {
+      const int i = lane + 32 * m;
+      xr[m] = cscale(inv, y[m]);
+      if (i < UP) xs[i] = xr[m];
+    }
+    __syncwarp();
+  }
+  const float lo = reg;
+  const float hi = fmaxf(1.1f * lam, 1.0001f * lo);
+  const float c = 0.5f * (lo + hi);
+  float d = 0.5f * (hi - lo);
+  if (!(d > 1e-6f * fmaxf(fabsf(c), 1e-30f))) d = fmaxf(fabsf(c), 1.f);
+  return make_float2(c, d);
+}
+
 // ------------------------------------------------------------------ LLR
 __device__ __forceinline__ float axis_min_sq(float z, const float* amps, int n) {
   float best = INFINITY;
@@ -637,23 +695,8 @@ __global__ void __launch_bounds__(NT, 2) subcarrier_kernel(const KernelParams p)
       __syncthreads();
       const int K = p.K;
       if (warp == 0) {
-        // centre c = tr(A)/U and half-width d = 2 ||A - cI||_F / sqrt(U) of
-        // the basis (any d > 0 is exact algebra; this choice keeps the
-        // basis well conditioned)
-        float tr = 0.f, fr = 0.f;
-        for (int i = lane; i < UP; i += 32) tr += Gs[i * UP + i].x + p.rho_inv_u;
-        tr = group_sum<32>(tr);
-        const float c = tr / UP;
-        for (int e = lane; e < UP * UP; e += 32) {
-          const int i = e / UP, j = e - i * UP;
-          float2 a = Gs[e];
-          if (i == j) a.x += p.rho_inv_u - c;
-          fr += cnorm(a);
-        }
-        fr = group_sum<32>(fr);
-        float d = 2.f * sqrtf(fr / UP);
-        if (!(d > 1e-6f * fmaxf(fabsf(c), 1e-30f))) d = fmaxf(fabsf(c), 1.f);
-        if (lane == 0) { misc[0] = c; misc[1] = d; }
+        const float2 cd = cheb_interval<UP>(Gs, p.rho_inv_u, Tb, lane);  // Tb: scratch here
+        if (lane == 0) { misc[0] = cd.x; misc[1] = cd.y; }
       }
       __syncthreads();
       const float cc = misc[0], dd = misc[1];

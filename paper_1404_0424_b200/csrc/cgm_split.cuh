@@ -81,6 +81,7 @@ struct K1Split {
     s = s > cap_m ? cap_m : s;
     spl = s < 1 ? 1 : s;
     wpp = (spl * n_tiles + 31) / 32;  // total warps (name kept for the params field)
+    if (wpp > 10) wpp = 10;           // more tiles than threads: the kernel loops over tiles
     nstage = 2;
   }
 };
@@ -107,25 +108,11 @@ __device__ __forceinline__ void exact_basis(const KernelParams& p, const WsOffse
   const int n_gram = (UP / 4) * (UP / 4 + 1) / 2;
   const int K = p.K;
   if (warp == 0) {
-    // centre c = tr(A)/U and half-width d = 2 ||A - cI||_F / sqrt(U)
-    // (any d > 0 is exact algebra; this choice keeps the basis well
-    // conditioned in FP32)
-    float tr = 0.f, fr = 0.f;
-    for (int ii = lane; ii < UP; ii += 32) tr += Gs[ii * UP + ii].x + p.rho_inv_u;
-    tr = group_sum<32>(tr);
-    const float c = tr / UP;
-    for (int e = lane; e < UP * UP; e += 32) {
-      float2 a = Gs[e];
-      if (e / UP == e % UP) a.x += p.rho_inv_u - c;
-      fr += cnorm(a);
-    }
-    fr = group_sum<32>(fr);
-    float d = 2.f * sqrtf(fr / UP);
-    if (!(d > 1e-6f * fmaxf(fabsf(c), 1e-30f))) d = fmaxf(fabsf(c), 1.f);
+    const float2 cd = cheb_interval<UP>(Gs, p.rho_inv_u, Tm, lane);  // Tm: scratch here
     if (lane == 0) {
-      misc[0] = c;
-      misc[1] = d;
-      ws[W.cd] = make_float2(c, d);
+      misc[0] = cd.x;
+      misc[1] = cd.y;
+      ws[W.cd] = cd;
     }
   }
   sync();
@@ -266,65 +253,86 @@ __global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p
       __syncthreads();
     }
     // --------------------------------------- Gram + matched-filter tiles
-    // one branch-free loop for both tile kinds (a warp may hold both): the
-    // second operand is H itself (Gram) or the Y block (matched filter)
-    float2 acc[4][4];
+    float2* MFw = ws + W.mf;
+    // results of tile t, row r: G (one triangle + conjugate mirror, G == G^H
+    // exactly) or the matched filter
+    auto write_row = [&](int t, int r, const float2 (&v)[4]) {
+      const int tib = tile_ib[t], tjb = tile_jb[t];
+      if (t < n_gram) {
+        const int ii = tib * 4 + r;
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) {
+          const int j = tjb * 4 + c;
+          if (j < ii) {
+            Gs[ii * UP + j] = v[c];
+            Gs[j * UP + ii] = cconj(v[c]);
+          } else if (j == ii) {
+            Gs[ii * UP + ii] = make_float2(v[c].x, 0.f);
+          }
+        }
+      } else {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(0.f, 0.f);
-    if (active && !(p.debug & 4)) {
-      const float2* Z = is_gram ? Hs : Ys;
-      const int ldz = is_gram ? UP : Sp;
-      if (PIPE)
-        tile4x4_pipe(acc, Hs, UP, ib * 4, Z, ldz, jb * 4, k0, k1);
-      else
-        tile4x4<true>(acc, Hs, UP, ib * 4, Z, ldz, 1, jb * 4, 1 << 30, k0, k1);
-    }
-    __syncthreads();  // (A) every k loop done: the stage may hold partials
-    if (!(p.debug & 8)) {
-      // partials parked entry-major / tile-minor ([part][16][n_tiles]) so a
-      // warp's stores and the reduction's loads are contiguous (no conflicts)
-      float2* pb = Hs;
-      if (active) {
-        float2* dst = pb + part * 16 * n_tiles + tile;
+        for (int c = 0; c < 4; ++c) {
+          const int s_ = tjb * 4 + c;
+          if (s_ < S) MFw[s_ * UP + tib * 4 + r] = v[c];
+        }
+      }
+    };
+    if (n_items > nt) {
+      // more tiles than threads (U = 64 with many vectors; spl == 1): each
+      // thread loops over whole tiles and writes its results directly
+      for (int t = tid; t < n_tiles; t += nt) {
+        float2 acc[4][4];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) dst[(r * 4 + c) * n_tiles] = acc[r][c];
+          for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(0.f, 0.f);
+        const bool g = t < n_gram;
+        tile4x4_pipe(acc, Hs, UP, tile_ib[t] * 4, g ? Hs : Ys, g ? UP : Sp, tile_jb[t] * 4, 0, B);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) write_row(t, r, acc[r]);
       }
-      __syncthreads();  // (B)
-      // thread <-> (tile, row r): fixed-order sum of the k-parts for the 4
-      // entries of the row, then G (one triangle + conjugate mirror, G == G^H
-      // exactly) or the matched filter.  Loads are tile-contiguous.
-      float2* MFw = ws + W.mf;
-      for (int e = tid; e < n_tiles * 4; e += nt) {
-        const int r = e / n_tiles, t = e - r * n_tiles;
-        const int tib = tile_ib[t], tjb = tile_jb[t];
-        float2 v[4];
+    } else {
+      // one branch-free loop for both tile kinds (a warp may hold both): the
+      // second operand is H itself (Gram) or the Y block (matched filter)
+      float2 acc[4][4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          v[c] = pb[(r * 4 + c) * n_tiles + t];
-          for (int sp = 1; sp < spl; ++sp) v[c] = cadd(v[c], pb[(sp * 16 + r * 4 + c) * n_tiles + t]);
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(0.f, 0.f);
+      if (active && !(p.debug & 4)) {
+        const float2* Z = is_gram ? Hs : Ys;
+        const int ldz = is_gram ? UP : Sp;
+        if (PIPE)
+          tile4x4_pipe(acc, Hs, UP, ib * 4, Z, ldz, jb * 4, k0, k1);
+        else
+          tile4x4<true>(acc, Hs, UP, ib * 4, Z, ldz, 1, jb * 4, 1 << 30, k0, k1);
+      }
+      __syncthreads();  // (A) every k loop done: the stage may hold partials
+      if (!(p.debug & 8)) {
+        // partials parked entry-major / tile-minor ([part][16][n_tiles]) so a
+        // warp's stores and the reduction's loads are contiguous (no conflicts)
+        float2* pb = Hs;
+        if (active) {
+          float2* dst = pb + part * 16 * n_tiles + tile;
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) dst[(r * 4 + c) * n_tiles] = acc[r][c];
         }
-        if (t < n_gram) {
-          const int ii = tib * 4 + r;
+        __syncthreads();  // (B)
+        // thread <-> (tile, row r): fixed-order sum of the k-parts for the 4
+        // entries of the row, then G (one triangle + conjugate mirror, G == G^H
+        // exactly) or the matched filter.  Loads are tile-contiguous.
+        for (int e = tid; e < n_tiles * 4; e += nt) {
+          const int r = e / n_tiles, t = e - r * n_tiles;
+          float2 v[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const int j = tjb * 4 + c;
-            if (j < ii) {
-              Gs[ii * UP + j] = v[c];
-              Gs[j * UP + ii] = cconj(v[c]);
-            } else if (j == ii) {
-              Gs[ii * UP + ii] = make_float2(v[c].x, 0.f);
-            }
+            v[c] = pb[(r * 4 + c) * n_tiles + t];
+            for (int sp = 1; sp < spl; ++sp) v[c] = cadd(v[c], pb[(sp * 16 + r * 4 + c) * n_tiles + t]);
           }
-        } else {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int s_ = tjb * 4 + c;
-            if (s_ < S) MFw[s_ * UP + tib * 4 + r] = v[c];
-          }
+          write_row(t, r, v);
         }
       }
     }

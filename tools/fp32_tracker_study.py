@@ -5,6 +5,8 @@
 # basis; compared with the reference library (oracle/_ref) on random channels.
 import numpy as np, oracle, sys
 ref = oracle.Oracle('ref')
+import os
+PIT = int(os.environ.get('PIT', 12)); PMARGIN = float(os.environ.get('PMARGIN', 1.05))
 f32, c64 = np.float32, np.complex64
 
 def gen(B, U, n, S, n0, bits, rng, corr=False):
@@ -82,15 +84,28 @@ def run(B, U, S, K, snr_db, bits, nsc=40, mode='literal', seed=0):
             # half-width from Gershgorin-like radius or frobenius
             if mode == 'cheb':
                 d = f32(np.sqrt(np.sum(np.abs(dev)**2)/U)*2.5)
+            elif mode == 'chebk':  # the kernels' round-1 choice
+                d = f32(np.sqrt(np.sum(np.abs(dev)**2)/U)*2.0)
+            elif mode in ('chebpos', 'chebrow'):
+                # positive interval [rho^-1, lambda_max]: A = G + rho^-1 I >= rho^-1 I
+                lo = f32(1/rho_u)
+                if mode == 'chebpos':  # power-iteration estimate of lambda_max, margin
+                    x = np.ones(U, c64)
+                    for _ in range(PIT):
+                        x = (A @ x).astype(c64); x /= np.linalg.norm(x)
+                    hi = f32(np.vdot(x, A @ x).real * PMARGIN)
+                else:  # Gershgorin row-sum bound
+                    hi = f32(np.max(np.sum(np.abs(A), 1)))
+                c = f32((lo + hi) / 2); d = f32((hi - lo) / 2)
             else:
                 d = f32(1.0); c = f32(0.0)
             Ah = ((A - c*np.eye(U, dtype=c64))/d).astype(c64)
             T = [np.eye(U, dtype=c64), Ah]
             for m in range(2, K+2):
-                T.append((2*(Ah@T[-1]) - T[-2]).astype(c64) if mode == 'cheb' else (Ah@T[-1]).astype(c64))
+                T.append((2*(Ah@T[-1]) - T[-2]).astype(c64) if mode.startswith('cheb') else (Ah@T[-1]).astype(c64))
             def mulA(co):
                 out = c*co.copy()
-                if mode == 'cheb':
+                if mode.startswith('cheb'):
                     sh = np.zeros_like(co)
                     sh[1] += co[0]
                     for m in range(1, len(co)-1):
@@ -123,6 +138,11 @@ def run(B, U, S, K, snr_db, bits, nsc=40, mode='literal', seed=0):
             hard += np.sum(((llr > 0) != (rl > 0)) & (np.abs(rl) >= 1e-4))
     print(f"B={B} U={U} K={K} {mode:8s} x {np.max(errs['x']):.1e} mu {np.max(errs['mu']):.1e} rho {np.max(errs['rho']):.1e} llr_fail {llr_fail}/{llr_tot} hard {hard}")
 
+if sys.argv[1] == 'weak':  # U = 64 weakly regularised (rho_u ~ 10), K = 8 / 16
+    for mode in sys.argv[2:]:
+        run(128, 64, 2, 8, 28, 6, 6, mode)
+        run(128, 64, 2, 16, 28, 6, 6, mode)
+    sys.exit(0)
 for mode in sys.argv[1:]:
     run(128, 8, 1, 3, 10, 4, 60, mode)
     run(64, 32, 2, 2, 20, 6, 20, mode)
