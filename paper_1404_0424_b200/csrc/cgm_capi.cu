@@ -23,10 +23,13 @@ struct cgm_ctx {
   int sms = 0;
   int max_smem = 0;
   cudaStream_t user_stream = nullptr;
-  cudaStream_t pipe[2] = {nullptr, nullptr};
-  // host-mode device workspaces, one set per pipeline stream
-  void* ws[2] = {nullptr, nullptr};
-  size_t ws_bytes[2] = {0, 0};
+  // host-buffer pipeline: copy-in, compute and copy-out streams over a ring
+  // of kHostSets device buffer sets (events: in done, compute done, out done)
+  static constexpr int kHostSets = 3;
+  cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t hev[kHostSets][3] = {};
+  void* ws[kHostSets] = {nullptr, nullptr, nullptr};
+  size_t ws_bytes[kHostSets] = {0, 0, 0};
   float* tscratch = nullptr;
   size_t tscratch_bytes = 0;
   long launches = 0;
@@ -465,15 +468,24 @@ int run_job(cgm_ctx* ctx, const Job& j, unsigned flags) {
     cgm::KernelParams p = params_of(j, j.n_sc);
     return launch(ctx, p, is_exact(j), ctx->user_stream);
   }
-  // ---------------- host buffers: chunked, double-buffered pipeline
+  // ---------------- host buffers: chunked three-stream pipeline
+  // chunk i uses buffer set i % kHostSets: H2D on pipe[0] (after the set's
+  // previous D2H), kernels on pipe[1], D2H on pipe[2].  The host->device
+  // copies run back to back and overlap the device->host copies of earlier
+  // chunks (PCIe is full duplex); CGMIMO_HOST_CHUNKS sets the chunk count.
+  constexpr int NB = cgm_ctx::kHostSets;
   const Sizes z = sizes_of(j);
   const size_t per_sc = z.total() + 16 * 12;
   const size_t budget = 192ull << 20;  // per buffer set
   long chunk = static_cast<long>(std::max<size_t>(1, budget / std::max<size_t>(per_sc, 1)));
   chunk = std::min(chunk, j.n_sc);
-  // aim for >= 4 chunks on large jobs so copies overlap compute
-  if (j.n_sc >= 4 * 148) chunk = std::min(chunk, (j.n_sc + 3) / 4);
-  for (int b = 0; b < 2; ++b) {
+  int nch = 8;
+  if (const char* e = std::getenv("CGMIMO_HOST_CHUNKS")) nch = std::max(1, std::atoi(e));
+  const long min_chunk = std::max<long>(1, ctx->sms);  // keep each launch >= one wave
+  if (j.n_sc >= 2 * min_chunk)
+    chunk = std::min(chunk, std::max(min_chunk, (j.n_sc + nch - 1) / nch));
+  const int nsets = static_cast<int>(std::min<long>(NB, (j.n_sc + chunk - 1) / chunk));
+  for (int b = 0; b < nsets; ++b) {
     size_t need = 0;
     const size_t parts[12] = {z.h, z.y, z.t, z.xhat, z.mu, z.rho, z.llr, z.st, z.q, z.s, z.gain, z.pst};
     for (size_t x : parts) need += round_up(x * chunk);
@@ -484,15 +496,17 @@ int run_job(cgm_ctx* ctx, const Job& j, unsigned flags) {
       CGM_CUDA(ctx, cudaMalloc(&ctx->ws[b], need));
       ctx->ws_bytes[b] = need;
     }
+    for (int k = 0; k < 3; ++k)
+      if (!ctx->hev[b][k]) CGM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->hev[b][k], cudaEventDisableTiming));
   }
+  cudaStream_t s_in = ctx->pipe[0], s_comp = ctx->pipe[1], s_out = ctx->pipe[2];
   auto H8 = reinterpret_cast<const char*>(j.H);
   auto Y8 = reinterpret_cast<const char*>(j.Y);
   auto T8 = reinterpret_cast<const char*>(j.T);
   int ci = 0;
   for (long c0 = 0; c0 < j.n_sc; c0 += chunk, ++ci) {
     const long n = std::min(chunk, j.n_sc - c0);
-    const int b = ci & 1;
-    cudaStream_t st = ctx->pipe[b];
+    const int b = ci % nsets;
     char* base = static_cast<char*>(ctx->ws[b]);
     size_t off = 0;
     auto carve = [&](size_t per) -> char* {
@@ -512,9 +526,14 @@ int run_job(cgm_ctx* ctx, const Job& j, unsigned flags) {
     char* dS = carve(z.s);
     char* dG = carve(z.gain);
     char* dPs = carve(z.pst);
-    if (z.h) CGM_CUDA(ctx, cudaMemcpyAsync(dH, H8 + z.h * c0, z.h * n, cudaMemcpyHostToDevice, st));
-    if (z.y) CGM_CUDA(ctx, cudaMemcpyAsync(dY, Y8 + z.y * c0, z.y * n, cudaMemcpyHostToDevice, st));
-    if (z.t) CGM_CUDA(ctx, cudaMemcpyAsync(dT, T8 + z.t * c0, z.t * n, cudaMemcpyHostToDevice, st));
+    // ---- copy in (after this set's previous results left the device)
+    if (ci >= nsets) CGM_CUDA(ctx, cudaStreamWaitEvent(s_in, ctx->hev[b][2], 0));
+    if (z.h) CGM_CUDA(ctx, cudaMemcpyAsync(dH, H8 + z.h * c0, z.h * n, cudaMemcpyHostToDevice, s_in));
+    if (z.y) CGM_CUDA(ctx, cudaMemcpyAsync(dY, Y8 + z.y * c0, z.y * n, cudaMemcpyHostToDevice, s_in));
+    if (z.t) CGM_CUDA(ctx, cudaMemcpyAsync(dT, T8 + z.t * c0, z.t * n, cudaMemcpyHostToDevice, s_in));
+    CGM_CUDA(ctx, cudaEventRecord(ctx->hev[b][0], s_in));
+    // ---- compute
+    CGM_CUDA(ctx, cudaStreamWaitEvent(s_comp, ctx->hev[b][0], 0));
     Job jd = j;
     jd.H = reinterpret_cast<float*>(dH);
     jd.Y = reinterpret_cast<float*>(dY);
@@ -529,12 +548,15 @@ int run_job(cgm_ctx* ctx, const Job& j, unsigned flags) {
     jd.gain = reinterpret_cast<float*>(dG);
     jd.pstatus = reinterpret_cast<uint8_t*>(dPs);
     cgm::KernelParams p = params_of(jd, n);
-    rc = launch(ctx, p, is_exact(j), st);
+    rc = launch(ctx, p, is_exact(j), s_comp);
     if (rc) return rc;
+    CGM_CUDA(ctx, cudaEventRecord(ctx->hev[b][1], s_comp));
+    // ---- copy out
+    CGM_CUDA(ctx, cudaStreamWaitEvent(s_out, ctx->hev[b][1], 0));
     auto d2h = [&](void* host, const char* dev, size_t per) -> cudaError_t {
       if (!per) return cudaSuccess;
       return cudaMemcpyAsync(static_cast<char*>(host) + per * c0, dev, per * n,
-                             cudaMemcpyDeviceToHost, st);
+                             cudaMemcpyDeviceToHost, s_out);
     };
     CGM_CUDA(ctx, d2h(j.xhat, dX, z.xhat));
     CGM_CUDA(ctx, d2h(j.mu, dMu, z.mu));
@@ -545,9 +567,11 @@ int run_job(cgm_ctx* ctx, const Job& j, unsigned flags) {
     CGM_CUDA(ctx, d2h(j.s, dS, z.s));
     CGM_CUDA(ctx, d2h(j.gain, dG, z.gain));
     CGM_CUDA(ctx, d2h(j.pstatus, dPs, z.pst));
+    CGM_CUDA(ctx, cudaEventRecord(ctx->hev[b][2], s_out));
   }
-  CGM_CUDA(ctx, cudaStreamSynchronize(ctx->pipe[0]));
-  CGM_CUDA(ctx, cudaStreamSynchronize(ctx->pipe[1]));
+  CGM_CUDA(ctx, cudaStreamSynchronize(s_out));
+  CGM_CUDA(ctx, cudaStreamSynchronize(s_comp));
+  CGM_CUDA(ctx, cudaStreamSynchronize(s_in));
   return CGM_OK;
 }
 
@@ -585,8 +609,8 @@ int cgm_ctx_create(int device, cgm_ctx** out) {
     delete ctx;
     return CGM_ECUDA;  // built for sm_100a only
   }
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pipe[0], cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->pipe[1], cudaStreamNonBlocking);
+  for (int i = 0; i < 3 && e == cudaSuccess; ++i)
+    e = cudaStreamCreateWithFlags(&ctx->pipe[i], cudaStreamNonBlocking);
   if (e == cudaSuccess) {
     const cgm::AxisTables t = make_axis_tables();
     e = cudaMemcpyToSymbol(cgm::c_axis, &t, sizeof t);
@@ -602,10 +626,13 @@ int cgm_ctx_create(int device, cgm_ctx** out) {
 int cgm_ctx_destroy(cgm_ctx* ctx) {
   if (!ctx) return CGM_OK;
   cudaSetDevice(ctx->device);
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < cgm_ctx::kHostSets; ++b) {
     if (ctx->ws[b]) cudaFree(ctx->ws[b]);
-    if (ctx->pipe[b]) cudaStreamDestroy(ctx->pipe[b]);
+    for (int k = 0; k < 3; ++k)
+      if (ctx->hev[b][k]) cudaEventDestroy(ctx->hev[b][k]);
   }
+  for (int i = 0; i < 3; ++i)
+    if (ctx->pipe[i]) cudaStreamDestroy(ctx->pipe[i]);
   if (ctx->tscratch) cudaFree(ctx->tscratch);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i)
