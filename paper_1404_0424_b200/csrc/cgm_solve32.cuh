@@ -322,11 +322,12 @@ __global__ void __launch_bounds__(256, 2) solve32_kernel(const KernelParams p) {
   }
   if (EXACT && S > 0) {
     __syncthreads();
-    k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st);
+    k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st, nt,
+                      [] { __syncthreads(); });
   }
   if (St > 0) {
     __syncthreads();
-    k2_precode_tail<UP>(p, sc, Vs, Qs, gpart, sys_st);
+    k2_precode_tail<UP>(p, sc, Vs, Qs, gpart, sys_st, nt, [] { __syncthreads(); });
   }
 }
 

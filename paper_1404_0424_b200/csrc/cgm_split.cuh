@@ -384,13 +384,13 @@ struct K2Smem {
 // v, sys_st the breakdown flags, hist the (alpha, beta) history.
 // Exact tracker (detect.cpp:330-395): FP64 coefficient recursion per system,
 // extraction of mu / nu^2 from the Chebyshev basis, then all outputs.
-template <int UP>
+template <int UP, class Sync>
 __device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float2* ws,
                                               const WsOffsets& W, long sc, int Kmax,
                                               const float* hist, float* coef, float* MUs,
                                               float* RHOs, const float2* Vs,
-                                              const uint8_t* sys_st) {
-  const int nt = blockDim.x, tid = threadIdx.x;
+                                              const uint8_t* sys_st, int nt, Sync&& sync) {
+  const int tid = threadIdx.x;
   const int S = p.S, U = p.U;
     const int K = p.K;
     const float2 cdv = ws[W.cd];
@@ -442,7 +442,7 @@ __device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float
         cb[m] = static_cast<float>(tmp[m] - static_cast<double>(p.rho_inv_u) * l0[m]);
       }
     }
-    __syncthreads();
+    sync();
     // extraction (detect.cpp:375-395): thread <-> (row i, pair of systems);
     // each T_m(i, j) is read once (L1/L2) and used for both systems
     const float2* Tw = ws + W.t;
@@ -486,7 +486,7 @@ __device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float
         }
       }
     }
-    __syncthreads();
+    sync();
     for (int e = tid; e < S * U; e += nt) {
       const int s = e / U, u = e - s * U;
       const long o = (sc * S + s) * static_cast<long>(U) + u;
@@ -504,13 +504,12 @@ __device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float
   }
 
 // Precoder (precode.cpp:22-71): q = H_d^H v, gain = ||q||, s = q / gain.
-template <int UP>
+template <int UP, class Sync>
 __device__ __forceinline__ void k2_precode_tail(const KernelParams& p, long sc, const float2* Vs,
-                                                float2* Qs, float* gpart,
-                                                const uint8_t* sys_st) {
-  const int nt = blockDim.x, nw = nt >> 5, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+                                                float2* Qs, float* gpart, const uint8_t* sys_st,
+                                                int nt, Sync&& sync) {
+  const int nw = nt >> 5, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int S = p.S, St = p.St, B = p.B, U = p.U;
-  (void)nt;
   // ------------------------------------------------ precode q = H_d^H v
   // q_b = sum_u H_u[b][u] v_u = sum_u conj(H_d[u][b]) v_u (precode.cpp:69),
   // then gain = ||q||, s = q / gain, zero_input when ||q|| vanishes (:22-36)
@@ -557,7 +556,7 @@ __device__ __forceinline__ void k2_precode_tail(const KernelParams& p, long sc, 
         }
       }
     }
-    __syncthreads();
+    sync();
     for (int ts = warp; ts < St; ts += nw) {
       const int sysi = S + ts;
       const bool ok = sys_st[sysi] == 0;
@@ -582,12 +581,17 @@ __device__ __forceinline__ void k2_precode_tail(const KernelParams& p, long sc, 
 // GREG: row u of G held in registers for the whole subcarrier (U = 32, one
 // system per lane group at a time); p_j is read in 8-column chunks so the
 // loads of a chunk are in flight together, with 4 independent FMA chains.
-template <int UP, bool EXACT, int MINB = 3, int NSO = 0, bool GREG = false>
-__global__ void __launch_bounds__(256, MINB) solve_kernel(const KernelParams p) {
+// The whole per-subcarrier solve (CG, trackers, LLRs, precoder) for one
+// subcarrier `lsc` of the chunk, run by threads [0, nt) (warps 0..nt/32-1)
+// with `sync` a barrier over exactly those; smem holds the K2Smem plan.
+// Called by solve_kernel (one CTA per subcarrier) and, fused, by the
+// epilogue warps of channel_tc_kernel.
+template <int UP, bool EXACT, int NSO = 0, bool GREG = false, class Sync>
+__device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsigned char* smem,
+                                         int nt, Sync&& sync) {
   using GE = K2Geo<UP, NSO>;
   static_assert(!GREG || (UP == 32 && GE::NS == 1), "GREG needs U = 32, one system per warp");
   constexpr int G = GE::G, RU = GE::RU, GPW = GE::GPW, NS = GE::NS;
-  extern __shared__ __align__(128) unsigned char smem[];
   const int S = p.S, St = p.St, B = p.B, U = p.U;
   const int nsys = S + St;
   const int Kmax = p.K > p.Kt ? p.K : p.Kt;
@@ -605,9 +609,8 @@ __global__ void __launch_bounds__(256, MINB) solve_kernel(const KernelParams p) 
   float* RHOs = reinterpret_cast<float*>(smem + L.rho);
   float* coef = reinterpret_cast<float*>(smem + L.coef);
   float* gpart = reinterpret_cast<float*>(smem + L.gpart);
-  const int nt = blockDim.x, nw = nt >> 5;
+  const int nw = nt >> 5;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const long lsc = blockIdx.x;
   const long sc = p.sc_base + lsc;
   const float2* ws = p.ws + lsc * W.stride;
 
@@ -616,7 +619,7 @@ __global__ void __launch_bounds__(256, MINB) solve_kernel(const KernelParams p) 
     float4* dst = reinterpret_cast<float4*>(Gs);
     for (int e = tid; e < UP * UP / 2; e += nt) dst[e] = src[e];
   }
-  __syncthreads();
+  sync();
 
   // ------------------------------------------------------------------ CG
   {
@@ -842,14 +845,20 @@ __global__ void __launch_bounds__(256, MINB) solve_kernel(const KernelParams p) 
 
   // ------------------------------------------ exact tracker extraction
   if (EXACT && S > 0) {
-    __syncthreads();
-    k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st);
+    sync();
+    k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st, nt, sync);
   }
   // ------------------------------------------------ precode q = H_d^H v
   if (St > 0) {
-    __syncthreads();
-    k2_precode_tail<UP>(p, sc, Vs, Qs, gpart, sys_st);
+    sync();
+    k2_precode_tail<UP>(p, sc, Vs, Qs, gpart, sys_st, nt, sync);
   }
+}
+
+template <int UP, bool EXACT, int MINB = 3, int NSO = 0, bool GREG = false>
+__global__ void __launch_bounds__(256, MINB) solve_kernel(const KernelParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  solve_sc<UP, EXACT, NSO, GREG>(p, blockIdx.x, smem, blockDim.x, [] { __syncthreads(); });
 }
 
 }  // namespace cgm
