@@ -45,8 +45,8 @@ constexpr int KB = 64;             // antennas per k-block
 constexpr int ATOM = KB * 128;     // one SW128 column block: 64 rows x 64 bf16
 constexpr int PIECE = 2 * ATOM;    // H columns (atom 0) + Y columns (atom 1)
 constexpr int PSLOT = 3 * PIECE;   // the three bf16 pieces of one k-block
-constexpr int NPS = 2;             // piece slots
-constexpr int TMEM_COLS = 512;
+constexpr int NPS = 2;             // piece slots (max; RING of the kernel uses 1 or 2)
+constexpr int TMEM_COLS = 512;     // 2 subcarrier buffers (RING = 2); RING = 1 uses 256
 constexpr int GPS = UPT + 1;       // padded G row stride (float2) in smem
 constexpr int MAX_STG = 4;
 
@@ -178,10 +178,12 @@ __device__ __forceinline__ void split8(const float (&x)[8], uint4& o0, uint4& o1
 struct Smem {
   int pieces, stage, stage_bytes, nstg, gp, gs, tb, bar, total;
   __host__ __device__ static int align(int x, int a) { return (x + a - 1) / a * a; }
-  __host__ __device__ void plan(int S, bool exact, int nstage) {
+  // ring = piece slots and TMEM subcarrier buffers (2: one CTA per SM
+  // double-buffers; 1: half the shared memory, two CTAs per SM)
+  __host__ __device__ void plan(int S, bool exact, int nstage, int ring = NPS) {
     int o = 0;
     pieces = o;
-    o += NPS * PSLOT;
+    o += ring * PSLOT;
     stage_bytes = align(KB * UPT * 8 + KB * S * 8, 128);
     nstg = nstage;
     stage = o;
@@ -216,8 +218,8 @@ __device__ __forceinline__ void tc_trace(const KernelParams& p, long i, int ev) 
 // split.  NSP == 0 (unified): warps [0, NEP) split subcarrier i, then run
 // the epilogue of subcarrier i-1 while the tensor core works on i.  Then
 // the TMA producer warp and the MMA warp.  k1_pair carries the staging depth.
-template <bool EXACT, int NEP, int NSP>
-__global__ void __launch_bounds__(32 * (NEP + NSP + 2), 1) channel_tc_kernel(const KernelParams p) {
+template <bool EXACT, int NEP, int NSP, int RING = 2>
+__global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_kernel(const KernelParams p) {
   using namespace tc;
   constexpr int UP = UPT;
   constexpr bool UNIFIED = NSP == 0;
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 1) channel_tc_kernel(con
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   tc::Smem L;
-  L.plan(p.S, EXACT, p.k1_pair);
+  L.plan(p.S, EXACT, p.k1_pair, RING);
   WsOffsets W;
   W.plan(UP, p.S, p.K, EXACT);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -249,7 +251,8 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 1) channel_tc_kernel(con
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
   float* misc = reinterpret_cast<float*>(bars + 16) + 4;
 
-  if (warp == 0) tmem_alloc(tmem_slot, TMEM_COLS);
+  constexpr uint32_t TCOLS = RING == 2 ? TMEM_COLS : 256;
+  if (warp == 0) tmem_alloc(tmem_slot, TCOLS);
   if (tid == 0) {
     for (int s = 0; s < nstg; ++s) {
       mbar_init(stg_full + s, 1);
@@ -283,8 +286,8 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 1) channel_tc_kernel(con
     for (int kb = 0; kb < nkb; ++kb, ++pq) {
       if (!(p.debug & 1024)) mbar_wait(stg_full + stg_s, sph);
       if (st == 0) tc_trace(p, i, kb == 0 ? 2 : 4);
-      const int ps = static_cast<int>(pq & 1);
-      if (pq >= NPS) mbar_wait(pcs_empty + ps, static_cast<uint32_t>(((pq >> 1) - 1) & 1));
+      const int ps = static_cast<int>(pq % RING);
+      if (pq >= RING) mbar_wait(pcs_empty + ps, static_cast<uint32_t>(((pq / RING) - 1) & 1));
       if (st == 0) tc_trace(p, i, kb == 0 ? 13 : 14);
       const float* Hst = reinterpret_cast<const float*>(smem + L.stage + stg_s * L.stage_bytes);
       const float* Yst = Hst + KB * UP * 2;
@@ -385,8 +388,8 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 1) channel_tc_kernel(con
     const int u = m >> 1, odd = m & 1;            // user; re (even) / im (odd) row
     const int cbase = lane < 16 ? 0 : hoff;
     const int c_first = (warp >> 2) * 8, c_step = 8 * (NEP / 4);
-    const int ab = static_cast<int>(e & 1);
-    mbar_wait(acc_full + ab, static_cast<uint32_t>((e >> 1) & 1));
+    const int ab = static_cast<int>(e % RING);
+    mbar_wait(acc_full + ab, static_cast<uint32_t>((e / RING) & 1));
     tc_fence_after();
     if (tid == 0) tc_trace(p, e, 9);
     const long lsc = blockIdx.x + e * gridDim.x;
@@ -483,13 +486,13 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 1) channel_tc_kernel(con
     const uint64_t dbase = smem_desc(smem_u32(smem + L.pieces), ATOM, 1024);
     long mq = 0;
     for (long i = 0; i < n_local; ++i) {
-      const int ab = static_cast<int>(i & 1);
-      if (i >= 2) mbar_wait(acc_empty + ab, static_cast<uint32_t>(((i >> 1) - 1) & 1));
+      const int ab = static_cast<int>(i % RING);
+      if (i >= RING) mbar_wait(acc_empty + ab, static_cast<uint32_t>(((i / RING) - 1) & 1));
       tc_fence_after();
       const uint32_t d_big = tmem + ab * 256, d_small = d_big + 128;
       for (int kb = 0; kb < nkb; ++kb, ++mq) {
-        const int ps = static_cast<int>(mq & 1);
-        mbar_wait(pcs_full + ps, static_cast<uint32_t>((mq >> 1) & 1));
+        const int ps = static_cast<int>(mq % RING);
+        mbar_wait(pcs_full + ps, static_cast<uint32_t>((mq / RING) & 1));
         tc_fence_after();
         if (lane == 0) tc_trace(p, i, kb == 0 ? 6 : 7);
         // descriptor start addresses advance by (byte offset >> 4)
@@ -530,7 +533,7 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 1) channel_tc_kernel(con
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == 0) tmem_dealloc(tmem, TCOLS);
 }
 
 }  // namespace cgm

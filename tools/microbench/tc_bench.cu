@@ -12,16 +12,30 @@
 #include "../../paper_1404_0424_b200/csrc/cgm_tc.cuh"
 using namespace cgm;
 
-template <bool EXACT, int NEP, int NSP>
+template <bool EXACT, int NEP, int NSP, int RING = 2>
 void run(KernelParams p, int nstg, const char* tag) {
   tc::Smem L;
-  L.plan(p.S, EXACT, nstg);
+  L.plan(p.S, EXACT, nstg, RING);
   p.k1_pair = nstg;
-  auto k = channel_tc_kernel<EXACT, NEP, NSP>;
+  auto k = channel_tc_kernel<EXACT, NEP, NSP, RING>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int g = static_cast<int>(std::min<long>(p.n_sc, sms));
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 32 * (NEP + NSP + 2), L.total);
+  {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k);
+    printf("   attrs: regs=%d static_smem=%zu max_threads=%d local=%zu\n", fa.numRegs, fa.sharedSizeBytes,
+           fa.maxThreadsPerBlock, fa.localSizeBytes);
+    for (int sm : {20000, 60000, 100000, 110000}) {
+      int o = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, 32 * (NEP + NSP + 2), sm);
+      printf("   occ(smem=%d) = %d\n", sm, o);
+    }
+  }
+  const int g = static_cast<int>(std::min<long>(p.n_sc, (long)sms * (occ > 0 ? occ : 1)));
   const int nt = 32 * (NEP + NSP + 2);
   unsigned long long* tr = p.trace;
   p.trace = nullptr;
@@ -36,7 +50,7 @@ void run(KernelParams p, int nstg, const char* tag) {
   cudaEventSynchronize(b);
   float ms;
   cudaEventElapsedTime(&ms, a, b);
-  printf("%s NEP=%d NSP=%d nstg=%d smem=%d grid=%d: %.2f us  (%s)\n", tag, NEP, NSP, nstg, L.total, g,
+  printf("%s NEP=%d NSP=%d RING=%d nstg=%d smem=%d occ=%d grid=%d: %.2f us  (%s)\n", tag, NEP, NSP, RING, nstg, L.total, occ, g,
          1000 * ms / reps, cudaGetErrorString(cudaGetLastError()));
   {  // correctness of G and MF against FP64 on the host (first 4 subcarriers)
     cudaDeviceSynchronize();
@@ -77,6 +91,7 @@ void run(KernelParams p, int nstg, const char* tag) {
   }
   if (!tr) return;
   p.trace = tr;
+  if (g > 148) return;
   cudaMemset(tr, 0, sizeof(unsigned long long) * g * 512);
   k<<<g, nt, L.total>>>(p);
   cudaDeviceSynchronize();
@@ -136,6 +151,9 @@ int main(int argc, char** argv) {
   } else {
     run<false, 8, 8>(p, nstg, "approx");
     p.trace = nullptr;
+    run<false, 4, 4, 1>(p, 2, "approx 2cta");
+    run<false, 4, 4, 1>(p, 3, "approx 2cta");
+    run<false, 4, 2, 1>(p, 2, "approx 2cta");
     run<false, 4, 8>(p, nstg, "approx");
     run<false, 8, 0>(p, nstg, "approx unified");
     run<false, 16, 0>(p, nstg, "approx unified");
