@@ -35,6 +35,7 @@
 #ifndef CGMIMO_B200_H
 #define CGMIMO_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -134,6 +135,32 @@ int cgm_generate_symbols(cgm_ctx* ctx, int U, long sc0, long n_sc, int S, uint64
 int cgm_generate_uplink_correlated(cgm_ctx* ctx, int B, int U, long sc0, long n_sc, int S,
                                    uint64_t seed, int qam_bits, double n0, const float* rsqrt,
                                    float* H, float* Y, uint8_t* labels);
+
+/* ---- multi-GPU: one process per GPU, subcarriers
+ * sharded across ranks, the one collective is the gather of each rank's
+ * outputs to a root.  NCCL is loaded at run time (dlopen "libnccl.so.2"; the
+ * copy torch already loaded is reused); without it these return CGM_ENCCL.
+ *
+ *   rank 0: cgm_comm_unique_id(id); broadcast the 128 bytes to all ranks
+ *           (MPI, torch.distributed, a file, ...)
+ *   every rank: cgm_comm_create(ctx, nranks, rank, id, &comm)
+ *   every rank: cgm_gather(ctx, comm, send, counts, recv, root)
+ *
+ * cgm_gather: rank r contributes counts[r] bytes from the device buffer
+ * `send`; the root receives them concatenated in rank order into the device
+ * buffer `recv` (sum of counts bytes; ignored on other ranks).  counts[] is
+ * identical on every rank (ragged shards allowed).  Asynchronous on the
+ * context's stream (ncclSend / ncclRecv in one group); replaces the
+ * reference's host-side result collection (sim.cpp:286-305 joins worker
+ * threads) for the multi-GPU batch.  Reference interface: none (the
+ * reference is single-process); this is the §8(b) extra "cgm_gather". */
+typedef struct cgm_comm cgm_comm;
+int cgm_comm_unique_id(unsigned char id[128]);
+int cgm_comm_create(cgm_ctx* ctx, int nranks, int rank, const unsigned char id[128],
+                    cgm_comm** out);
+int cgm_comm_destroy(cgm_comm* comm);
+int cgm_gather(cgm_ctx* ctx, cgm_comm* comm, const void* send, const size_t* counts, void* recv,
+               int root);
 
 #ifdef __cplusplus
 }

@@ -59,7 +59,7 @@ def build(verbose: bool = False) -> str:
             log += _run(["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", *inc, "-c", s,
                          "-o", o])
     if _newer(LIB, objs):
-        log += _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs])
+        log += _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-ldl"])
     if verbose:
         print(log)
     return LIB

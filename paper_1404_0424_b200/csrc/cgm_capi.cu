@@ -4,6 +4,8 @@
 // pipeline (H2D / kernel / D2H overlapped on two streams) and the seeded
 // device input generators.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the entry points are resolved at run time
 
 #include <algorithm>
 #include <cmath>
@@ -724,6 +726,142 @@ int cgm_detect_precode_cg(cgm_ctx* ctx, int B, int U, long n_sc, int S, const fl
   j.q = q; j.s = s; j.gain = gain; j.pstatus = pstatus;
   if (S < 1 || St < 1) return fail(ctx, CGM_EINVAL, "detect_precode_cg: S and St must be >= 1");
   return run_job(ctx, j, flags);
+}
+
+
+// ---------------------------------------------------------------- multi-GPU
+struct cgm_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 0, rank = 0;
+};
+
+namespace {
+// NCCL through dlopen: the library loads (and single-GPU use works) where
+// NCCL is absent; in a torch process the already-loaded libnccl is reused.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GroupStart &&
+           a.GroupEnd && a.GetErrorString;
+    return a;
+  }();
+  return api;
+}
+}  // namespace
+
+#define CGM_NCCL(ctx, call)                                                                 \
+  do {                                                                                      \
+    const ncclResult_t r_ = (call);                                                         \
+    if (r_ != ncclSuccess)                                                                  \
+      return fail(ctx, CGM_ENCCL, "%s: %s", #call, nccl_api().GetErrorString(r_));           \
+  } while (0)
+
+int cgm_comm_unique_id(unsigned char id[128]) {
+  if (!id) return CGM_EINVAL;
+  NcclApi& n = nccl_api();
+  if (!n.ok) return CGM_ENCCL;
+  ncclUniqueId uid;
+  if (n.GetUniqueId(&uid) != ncclSuccess) return CGM_ENCCL;
+  static_assert(sizeof(uid) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id, &uid, sizeof uid);
+  return CGM_OK;
+}
+
+int cgm_comm_create(cgm_ctx* ctx, int nranks, int rank, const unsigned char id[128],
+                    cgm_comm** out) {
+  if (!ctx || !out || !id) return CGM_EINVAL;
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(ctx, CGM_EINVAL, "cgm_comm_create: rank %d of %d", rank, nranks);
+  NcclApi& n = nccl_api();
+  if (!n.ok) return fail(ctx, CGM_ENCCL, "libnccl.so.2 not available");
+  CGM_CUDA(ctx, cudaSetDevice(ctx->device));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  cgm_comm* c = new cgm_comm();
+  const ncclResult_t r = n.CommInitRank(&c->comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(ctx, CGM_ENCCL, "ncclCommInitRank: %s", n.GetErrorString(r));
+  }
+  c->nranks = nranks;
+  c->rank = rank;
+  *out = c;
+  return CGM_OK;
+}
+
+int cgm_comm_destroy(cgm_comm* comm) {
+  if (!comm) return CGM_OK;
+  if (comm->comm && nccl_api().ok) nccl_api().CommDestroy(comm->comm);
+  delete comm;
+  return CGM_OK;
+}
+
+int cgm_gather(cgm_ctx* ctx, cgm_comm* comm, const void* send, const size_t* counts, void* recv,
+               int root) {
+  if (!ctx || !comm || !counts) return CGM_EINVAL;
+  if (root < 0 || root >= comm->nranks)
+    return fail(ctx, CGM_EINVAL, "cgm_gather: root %d of %d ranks", root, comm->nranks);
+  NcclApi& n = nccl_api();
+  CGM_CUDA(ctx, cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->user_stream;
+  if (comm->rank == root) {
+    if (!recv) return fail(ctx, CGM_EINVAL, "cgm_gather: root needs a receive buffer");
+    size_t off = 0;
+    CGM_NCCL(ctx, n.GroupStart());
+    for (int r = 0; r < comm->nranks; ++r) {
+      char* dst = static_cast<char*>(recv) + off;
+      if (counts[r] > 0) {
+        if (r == root) {
+          const cudaError_t e = cudaMemcpyAsync(dst, send, counts[r], cudaMemcpyDeviceToDevice, st);
+          if (e != cudaSuccess) {
+            n.GroupEnd();
+            return fail(ctx, CGM_ECUDA, "cgm_gather: %s", cudaGetErrorString(e));
+          }
+        } else {
+          const ncclResult_t rr = n.Recv(dst, counts[r], ncclInt8, r, comm->comm, st);
+          if (rr != ncclSuccess) {
+            n.GroupEnd();
+            return fail(ctx, CGM_ENCCL, "ncclRecv: %s", n.GetErrorString(rr));
+          }
+        }
+      }
+      off += counts[r];
+    }
+    CGM_NCCL(ctx, n.GroupEnd());
+  } else if (counts[comm->rank] > 0) {
+    CGM_NCCL(ctx, n.GroupStart());
+    const ncclResult_t rs = n.Send(send, counts[comm->rank], ncclInt8, root, comm->comm, st);
+    if (rs != ncclSuccess) {
+      n.GroupEnd();
+      return fail(ctx, CGM_ENCCL, "ncclSend: %s", n.GetErrorString(rs));
+    }
+    CGM_NCCL(ctx, n.GroupEnd());
+  }
+  return CGM_OK;
 }
 
 }  // extern "C"

@@ -44,6 +44,52 @@ def gather_to_root(t, world: int, rank: int, sizes=None):
     return None
 
 
+class Comm:
+    """The C ABI's NCCL communicator (cgm_comm_create / cgm_gather): the same
+    gather as gather_to_root, callable from any FFI without torch.distributed.
+    Rank 0 makes the id with ``Comm.unique_id()`` and ships its 128 bytes to
+    the other ranks out of band."""
+
+    def __init__(self, ctx, nranks: int, rank: int, uid: bytes):
+        import ctypes as C
+
+        self.ctx, self.lib, self.rank, self.nranks = ctx, ctx.lib, rank, nranks
+        h = C.c_void_p()
+        ctx._check(self.lib.cgm_comm_create(ctx.h, nranks, rank, bytes(uid), C.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+        from . import _lib
+
+        buf = C.create_string_buffer(128)
+        rc = _lib.load().cgm_comm_unique_id(buf)
+        if rc != _lib.CGM_OK:
+            raise RuntimeError(f"cgm_comm_unique_id rc={rc} (NCCL not available?)")
+        return buf.raw
+
+    def gather(self, send, counts_bytes, recv=None, root: int = 0):
+        """Concatenate every rank's device buffer `send` (counts_bytes[r] bytes
+        on rank r) on `root` into the device tensor `recv`, rank order."""
+        import ctypes as C
+
+        self.ctx._bind_torch_stream()
+        cnt = (C.c_size_t * self.nranks)(*[int(c) for c in counts_bytes])
+        self.ctx._check(self.lib.cgm_gather(self.ctx.h, self.h, C.c_void_p(send.data_ptr()), cnt,
+                                            C.c_void_p(recv.data_ptr() if recv is not None else 0),
+                                            root))
+        return recv
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.cgm_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
 def sharded_detect(ctx, cfg, world: int, rank: int, gather: bool = True):
     """Generate this rank's shard of `cfg` on its GPU, detect it, and (optionally)
     gather LLRs to rank 0.  Returns (local outputs, gathered LLRs or None)."""

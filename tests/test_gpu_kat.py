@@ -202,3 +202,21 @@ def test_unsupported_sizes_fail_loudly(gpu_ctx):
     with pytest.raises(ValueError):
         gpu_ctx.detect_cg(np.zeros((1, 8, 4), np.complex64), np.zeros((1, 8, 65), np.complex64),
                           1.0, 1.0, 1.0, 4, 2, "approx")
+
+
+def test_c_abi_nccl_gather_single_rank(gpu_ctx):
+    """cgm_comm_create / cgm_gather (the C ABI's multi-GPU gather, NCCL via
+    dlopen) on a one-rank communicator: the root's own shard lands in recv.
+    Multi-rank behaviour is covered by tests/test_multiproc.py (gloo) and the
+    torchrun bench; one GPU here cannot host two NCCL ranks."""
+    import torch
+
+    from paper_1404_0424_b200.parallel import Comm
+
+    comm = Comm(gpu_ctx, 1, 0, Comm.unique_id())
+    send = torch.arange(1000, dtype=torch.float32, device="cuda")
+    recv = torch.zeros(1000, dtype=torch.float32, device="cuda")
+    comm.gather(send, [send.numel() * 4], recv, root=0)
+    torch.cuda.synchronize()
+    assert torch.equal(recv, send)
+    comm.close()
