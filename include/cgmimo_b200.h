@@ -136,6 +136,26 @@ int cgm_generate_uplink_correlated(cgm_ctx* ctx, int B, int U, long sc0, long n_
                                    uint64_t seed, int qam_bits, double n0, const float* rsqrt,
                                    float* H, float* Y, uint8_t* labels);
 
+/* ---- coded BLER harness: the reference's
+ * run_uplink_trial (sim.cpp:147-203) for a batch of trials -- frames
+ * (info bits, rate-5/6 convolutional code, interleaver), channel + noise from
+ * the trial's streams, ONE batched detect_cg over all (symbol, subcarrier)
+ * vectors, deinterleaving and a soft Viterbi decoder on the GPU.
+ * trial_keys[t] = cgm_sweep_trial_key(seed, 1, point, trial) reproduces
+ * run_uplink_sweep's trials (sim.cpp:378-380); snr_db per receive antenna
+ * (N0 = U / SNR, rho_u = 1 / N0).  Outputs per trial: user_errors (blocks
+ * of the U users decoded wrongly) and breakdown (1: a SolverBreakdown
+ * aborted the trial, no errors counted, as sim.cpp:183-188).  Host arrays. */
+int cgm_uplink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K, int tracker,
+                      double snr_db, long n_trials, const uint64_t* trial_keys,
+                      uint32_t* user_errors, uint8_t* breakdown);
+uint64_t cgm_sweep_trial_key(uint64_t seed, int direction, long point, long trial);
+/* Soft max-log Viterbi decoding of n_cw rate-5/6 codewords (coding.cpp:90-147):
+ * llrs [n_cw][coded_len] in coded-bit order (positive favours 1), coded_len a
+ * multiple of 6; info_out [n_cw][coded_len/6*5 - 6].  Host arrays. */
+int cgm_viterbi_decode(cgm_ctx* ctx, const double* llrs, long coded_len, long n_cw,
+                       uint8_t* info_out);
+
 /* ---- multi-GPU: one process per GPU, subcarriers
  * sharded across ranks, the one collective is the gather of each rank's
  * outputs to a root.  NCCL is loaded at run time (dlopen "libnccl.so.2"; the

@@ -68,6 +68,8 @@ class Oracle:
         self.lib = C.CDLL(path)
         self.pfx = "ref_" if kind == "ref" else "orc_"
         self._threaded = kind == "ref"
+        for nm in ("conv_encode", "viterbi_decode"):
+            self._fn(nm).restype = C.c_long
 
     def _fn(self, name):
         return getattr(self.lib, self.pfx + name)
@@ -156,6 +158,53 @@ class Oracle:
         a1 = np.zeros((half, per))
         self._fn("constellation")(C.c_int(qam_bits), _ptr(pts), _ptr(a0), _ptr(a1))
         return pts, a0, a1
+
+    # ------------------------------------------------- coded BLER harness
+    def _need_ref(self, what):
+        if self.kind != "ref":
+            raise NotImplementedError(f"{what}: reference library only (coding.cpp / sim.cpp)")
+
+    def conv_encode(self, info) -> np.ndarray:
+        """phy::conv_encode (coding.cpp): rate-5/6 punctured K=7 code."""
+        info = np.ascontiguousarray(info, dtype=np.uint8)
+        out = np.zeros(len(info) * 2 + 64, np.uint8)
+        n = self._fn("conv_encode")(info.ctypes.data_as(C.c_void_p), C.c_long(len(info)),
+                                     out.ctypes.data_as(C.c_void_p))
+        if n < 0:
+            raise ValueError("conv_encode: bad length")
+        return out[:n]
+
+    def viterbi_decode(self, llrs) -> np.ndarray:
+        """phy::viterbi_decode_soft (coding.cpp): max-log soft Viterbi, FP64."""
+        llrs = np.ascontiguousarray(llrs, dtype=np.float64)
+        out = np.zeros(len(llrs), np.uint8)
+        n = self._fn("viterbi_decode")(llrs.ctypes.data_as(C.c_void_p), C.c_long(len(llrs)),
+                                        out.ctypes.data_as(C.c_void_p))
+        if n < 0:
+            raise ValueError("viterbi_decode: bad length")
+        return out[:n]
+
+    def make_interleaver(self, key: int, forks, n: int) -> np.ndarray:
+        """phy::make_interleaver (coding.cpp) on Rng(key).fork(forks...)."""
+        fk = np.ascontiguousarray(forks, dtype=np.uint64)
+        perm = np.zeros(n, np.int64)
+        self._fn("make_interleaver")(C.c_uint64(key), _ptr(fk, _u64p), C.c_int(len(fk)),
+                                      C.c_long(n), perm.ctypes.data_as(C.c_void_p))
+        return perm
+
+    def uplink_sweep_point(self, B, U, qam_bits, K, tracker, snr_db, trials, n_sc, seed,
+                           threads=0) -> dict:
+        """sim::run_uplink_sweep (sim.cpp:365-384) at one SNR, CG detector:
+        frames (user blocks), block_errors, breakdowns, trials_run."""
+        self._need_ref("uplink_sweep_point")
+        out = np.zeros(4, np.int64)
+        rc = self.lib.ref_uplink_sweep_point(
+            C.c_int(B), C.c_int(U), C.c_int(qam_bits), C.c_int(K),
+            C.c_int(0 if tracker == "exact" else 1), C.c_double(snr_db), C.c_long(trials),
+            C.c_long(n_sc), C.c_uint64(seed), C.c_int(threads), out.ctypes.data_as(C.c_void_p))
+        if rc != 0:
+            raise RuntimeError("run_uplink_sweep raised")
+        return dict(zip(("frames", "block_errors", "breakdowns", "trials_run"), map(int, out)))
 
     def rng_u64(self, key: int, forks, n: int) -> np.ndarray:
         fk = np.ascontiguousarray(forks, dtype=np.uint64)

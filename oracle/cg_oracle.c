@@ -614,3 +614,98 @@ int orc_precode_explicit(int B, int U, long n_sc, int S, const double* Hd, const
                          double rho_d, double* q, double* s, double* gain, uint8_t* status) {
   return precode_common(1, B, U, n_sc, S, Hd, T, rho_d, 1, q, s, gain, status);
 }
+
+/* --------------------------------------------------------------- coding */
+/* K = 7 (133, 171)_8 mother code, puncture period 5 to rate 5/6, 6-bit tail
+ * (coding.cpp:14-58).  State = last 6 inputs, newest in bit 5; the encoder
+ * register word is (u << 6) | state. */
+enum { kMemory = 6, kNStates = 64, kPeriod = 5 };
+static const int kPunctA[kPeriod] = {1, 1, 0, 1, 0};
+static const int kPunctB[kPeriod] = {1, 0, 1, 0, 1};
+
+static unsigned par(unsigned w) {
+  w ^= w >> 16; w ^= w >> 8; w ^= w >> 4; w ^= w >> 2; w ^= w >> 1;
+  return w & 1u;
+}
+static void branch(unsigned s, unsigned u, unsigned* a, unsigned* b, unsigned* next) {
+  const unsigned word = (u << kMemory) | s;
+  *a = par(word & 0133u);
+  *b = par(word & 0171u);
+  *next = (u << (kMemory - 1)) | (s >> 1);
+}
+
+/* coding.cpp:65-84 */
+long orc_conv_encode(const uint8_t* info, long n, uint8_t* out) {
+  const long total = n + kMemory;
+  if (n < 0 || total % kPeriod != 0) return -1;
+  long pos = 0;
+  unsigned s = 0;
+  for (long t = 0; t < total; ++t) {
+    unsigned a, b, nx;
+    branch(s, t < n ? (info[t] & 1u) : 0u, &a, &b, &nx);
+    if (kPunctA[t % kPeriod]) out[pos++] = (uint8_t)a;
+    if (kPunctB[t % kPeriod]) out[pos++] = (uint8_t)b;
+    s = nx;
+  }
+  return pos;
+}
+
+/* coding.cpp:86-147: depuncture, max-log ACS in FP64 visiting states and
+ * inputs in ascending order with a strict '>' (ties keep the first), tail
+ * forces u = 0, traceback from state 0 */
+long orc_viterbi_decode(const double* llrs, long n, uint8_t* out) {
+  if (n % 6 != 0 || n / 6 * kPeriod <= kMemory) return -1;
+  const long total = n / 6 * kPeriod, info_len = total - kMemory;
+  double* la = xcalloc((size_t)total, sizeof(double));
+  double* lb = xcalloc((size_t)total, sizeof(double));
+  uint8_t* dec = xcalloc((size_t)total * kNStates, 1);
+  long pos = 0;
+  for (long t = 0; t < total; ++t) {
+    if (kPunctA[t % kPeriod]) la[t] = llrs[pos++];
+    if (kPunctB[t % kPeriod]) lb[t] = llrs[pos++];
+  }
+  double m[kNStates], nm[kNStates];
+  for (int s = 0; s < kNStates; ++s) m[s] = -INFINITY;
+  m[0] = 0.0;
+  for (long t = 0; t < total; ++t) {
+    const double bm[4] = {-la[t] - lb[t], -la[t] + lb[t], la[t] - lb[t], la[t] + lb[t]};
+    for (int s = 0; s < kNStates; ++s) nm[s] = -INFINITY;
+    const unsigned umax = t < info_len ? 2u : 1u;
+    for (unsigned s = 0; s < kNStates; ++s) {
+      if (m[s] == -INFINITY) continue;
+      for (unsigned u = 0; u < umax; ++u) {
+        unsigned a, b, nx;
+        branch(s, u, &a, &b, &nx);
+        const double v = m[s] + bm[(a << 1) | b];
+        if (v > nm[nx]) {
+          nm[nx] = v;
+          dec[t * kNStates + nx] = (uint8_t)((u << 6) | s);
+        }
+      }
+    }
+    memcpy(m, nm, sizeof m);
+  }
+  unsigned s = 0;
+  for (long t = total; t-- > 0;) {
+    const uint8_t d = dec[t * kNStates + s];
+    if (t < info_len) out[t] = (uint8_t)(d >> 6);
+    s = d & (kNStates - 1);
+  }
+  free(la);
+  free(lb);
+  free(dec);
+  return info_len;
+}
+
+/* coding.cpp:149-157: Fisher-Yates from the top with next_unit */
+void orc_make_interleaver(uint64_t key, const uint64_t* forks, int n_forks, long n, int64_t* perm) {
+  rng_t r = rng_path(key, forks, n_forks);
+  for (long i = 0; i < n; ++i) perm[i] = i;
+  for (long i = n; i-- > 1;) {
+    long j = (long)(rng_unit(&r) * (double)(i + 1));
+    if (j > i) j = i;
+    const int64_t x = perm[i];
+    perm[i] = perm[j];
+    perm[j] = x;
+  }
+}

@@ -32,6 +32,12 @@ void orc_rng_cgaussian(uint64_t key, const uint64_t* forks, int n_forks, double 
                        long n, double* out);
 void orc_rayleigh(uint64_t key, const uint64_t* forks, int n_forks, int B, int U, double* out);
 
+/* coded BLER harness (coding.cpp): same contracts as the ref_ entry points in
+ * ref_shim.cpp -- lengths returned, -1 on a length the reference rejects */
+long orc_conv_encode(const uint8_t* info, long n, uint8_t* out);
+long orc_viterbi_decode(const double* llrs, long n, uint8_t* out);
+void orc_make_interleaver(uint64_t key, const uint64_t* forks, int n_forks, long n, int64_t* perm);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,6 +13,8 @@
 //   phy::make_constellation  (constellation.cpp:37-86)
 //   phy::Rng                 (rng.cpp:12-52)
 //   opcount::count_detect_stages (opcount.cpp:69-138)
+//   phy::conv_encode / viterbi_decode_soft / make_interleaver (coding.cpp)
+//   sim::run_uplink_sweep    (sim.cpp:365-384, trials of run_uplink_trial)
 //
 // Batch layout (shared with the CUDA path and oracle/cg_oracle.c):
 //   H  uplink   [n_sc][B][U]  element (b,u) at b*U+u   (linalg.hpp:28)
@@ -31,7 +33,9 @@
 #include <vector>
 
 #include "cgmimo/channel.hpp"
+#include "cgmimo/coding.hpp"
 #include "cgmimo/constellation.hpp"
+#include "cgmimo/sim.hpp"
 #include "cgmimo/detect.hpp"
 #include "cgmimo/linalg.hpp"
 #include "cgmimo/opcount.hpp"
@@ -353,6 +357,67 @@ int ref_exact_filters(int B, int U, const double* H, const double* Y, double rho
     return 1;
   } catch (const std::exception&) {
     return 2;
+  }
+}
+
+// ---- coded BLER harness (sim.cpp / coding.cpp)
+long ref_conv_encode(const uint8_t* info, long n, uint8_t* out) {
+  try {
+    const auto coded = phy::conv_encode(std::vector<uint8_t>(info, info + n));
+    std::memcpy(out, coded.data(), coded.size());
+    return static_cast<long>(coded.size());
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+long ref_viterbi_decode(const double* llrs, long n, uint8_t* out) {
+  try {
+    const auto info = phy::viterbi_decode_soft(std::vector<double>(llrs, llrs + n));
+    std::memcpy(out, info.data(), info.size());
+    return static_cast<long>(info.size());
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+void ref_make_interleaver(uint64_t key, const uint64_t* forks, int n_forks, long n, int64_t* perm) {
+  phy::Rng rng(key);
+  for (int i = 0; i < n_forks; ++i) rng = rng.fork(forks[i]);
+  const auto p = phy::make_interleaver(static_cast<std::size_t>(n), rng);
+  for (long i = 0; i < n; ++i) perm[i] = static_cast<int64_t>(p[i]);
+}
+
+// One SNR point of the reference's uplink BLER sweep (CG detector):
+// out = {frames, block_errors, breakdowns, trials_run}; returns 0, or -1 on
+// an exception (e.g. BreakdownBudgetExceeded is disabled by fraction 1.0).
+int ref_uplink_sweep_point(int B, int U, int qam_bits, int K, int tracker, double snr_db,
+                           long trials, long n_sc, uint64_t seed, int threads, long* out) {
+  try {
+    sim::SweepConfig cfg;
+    cfg.bs_antennas = static_cast<std::size_t>(B);
+    cfg.users = static_cast<std::size_t>(U);
+    cfg.modulation = qam_bits == 2 ? phy::Modulation::kQpsk
+                                   : (qam_bits == 4 ? phy::Modulation::kQam16 : phy::Modulation::kQam64);
+    cfg.method = sim::Method::kCg;
+    cfg.iterations = static_cast<std::size_t>(K);
+    cfg.tracker = tracker == 0 ? detect::SinrTracker::kExact : detect::SinrTracker::kApprox;
+    cfg.snr_start_db = cfg.snr_stop_db = snr_db;
+    cfg.snr_step_db = 1.0;
+    cfg.trials = static_cast<std::size_t>(trials);
+    cfg.subcarriers = static_cast<std::size_t>(n_sc);
+    cfg.seed = seed;
+    cfg.threads = static_cast<std::size_t>(threads);
+    cfg.max_breakdown_fraction = 1.0;
+    const auto r = sim::run_uplink_sweep(cfg);
+    const auto& pt = r.points.at(0);
+    out[0] = static_cast<long>(pt.frames);
+    out[1] = static_cast<long>(pt.block_errors);
+    out[2] = static_cast<long>(pt.breakdowns);
+    out[3] = static_cast<long>(pt.trials_run);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
   }
 }
 

@@ -9,6 +9,7 @@ from ._lib import LIB_PATH, load as load_library, symbols
 from .api import (Context, CudaError, SolverBreakdown, default_context, detect_cg,
                   detect_cg_single, precode_cg, precode_cg_single)
 from .configs import CONFIGS, Config, get_config
+from . import sim  # noqa: E402  (coded BLER sweeps)
 
 __all__ = [
     "LIB_PATH", "load_library", "symbols", "Context", "CudaError", "SolverBreakdown",

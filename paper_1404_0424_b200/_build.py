@@ -17,7 +17,7 @@ LIB = os.path.join(PKG, "libcgmimo_b200.so")
 OBJ = os.path.join(PKG, "_obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU = ["cgm_capi.cu", "cgm_generate.cu"]
+CU = ["cgm_capi.cu", "cgm_generate.cu", "cgm_harness.cu"]
 CPP = ["cgm_dropin.cpp"]
 HDRS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 
@@ -59,7 +59,8 @@ def build(verbose: bool = False) -> str:
             log += _run(["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", *inc, "-c", s,
                          "-o", o])
     if _newer(LIB, objs):
-        log += _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-ldl"])
+        log += _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-ldl",
+                     "-lpthread"])
     if verbose:
         print(log)
     return LIB

@@ -110,6 +110,34 @@ class Context:
     def kernel_launches(self) -> int:
         return int(self.lib.cgm_kernel_launches(self.h))
 
+    # ------------------------------------------------- coded BLER harness
+    def uplink_trials(self, B, U, n_sc, qam_bits, K, tracker, snr_db, trial_keys):
+        """cgm_uplink_trials: block errors and breakdown flags of a batch of
+        the reference's coded uplink trials (sim.cpp:147-203)."""
+        import numpy as np
+
+        keys = np.ascontiguousarray(trial_keys, dtype=np.uint64)
+        n = len(keys)
+        errs = np.zeros(n, np.uint32)
+        brk = np.zeros(n, np.uint8)
+        trk = {"exact": _lib.CGM_TRACKER_EXACT, "approx": _lib.CGM_TRACKER_APPROX}[tracker]
+        self._check(self.lib.cgm_uplink_trials(self.h, B, U, n_sc, qam_bits, K, trk, float(snr_db), n,
+                                               keys.ctypes.data_as(C.c_void_p),
+                                               errs.ctypes.data_as(C.c_void_p),
+                                               brk.ctypes.data_as(C.c_void_p)))
+        return errs, brk
+
+    def viterbi_decode(self, llrs):
+        """cgm_viterbi_decode: (n_cw, coded_len) float64 LLRs -> (n_cw, info_len) bits."""
+        import numpy as np
+
+        llrs = np.ascontiguousarray(np.atleast_2d(llrs), dtype=np.float64)
+        n_cw, coded = llrs.shape
+        out = np.zeros((n_cw, coded // 6 * 5 - 6), np.uint8)
+        self._check(self.lib.cgm_viterbi_decode(self.h, llrs.ctypes.data_as(C.c_void_p), coded, n_cw,
+                                                out.ctypes.data_as(C.c_void_p)))
+        return out
+
     # ------------------------------------------------------------- detect
     def detect_cg(self, H, Y, rho_u, n0, es, qam_bits, iters, tracker="exact", out=None,
                   want=("xhat", "mu", "rho", "llr", "status")):

@@ -45,8 +45,46 @@ PRECODE_CASES = [
 ]
 
 
+# run_uplink_sweep points (sim.cpp:365-384) pinned for tests/test_gpu_harness.py:
+# (B, U, qam_bits, K, tracker, snr_db, n_sc, trials), seed 7
+SWEEP_CASES = [
+    (32, 8, 6, 4, "approx", 14.0, 128, 48),   # reference SweepConfig defaults (sim.hpp)
+    (32, 8, 6, 3, "exact", 12.0, 128, 32),
+    (64, 16, 4, 3, "approx", 6.0, 60, 32),    # 16-QAM, 2 OFDM symbols per frame
+    (16, 4, 2, 2, "exact", 2.0, 90, 32),      # QPSK
+]
+
+
+def coding_fixtures(ref):
+    """coding.cpp: encoder outputs, soft-Viterbi decisions (incl. tie-heavy
+    integer LLRs and an all-zero input) and interleavers; plus sweep points."""
+    rng = np.random.default_rng(20261019)
+    d = {}
+    for i, n in enumerate([94, 634, 994]):  # + 6 tail = 20 / 128 / 200 periods
+        info = rng.integers(0, 2, n).astype(np.uint8)
+        coded = ref.conv_encode(info)
+        d[f"info{i}"], d[f"coded{i}"] = info, coded
+        noisy = (2.0 * coded - 1.0) * 2.0 + rng.standard_normal(len(coded)) * 2.0
+        ties = rng.integers(-2, 3, len(coded)).astype(np.float64)
+        d[f"llr_noisy{i}"], d[f"dec_noisy{i}"] = noisy, ref.viterbi_decode(noisy)
+        d[f"llr_ties{i}"], d[f"dec_ties{i}"] = ties, ref.viterbi_decode(ties)
+        d[f"dec_zero{i}"] = ref.viterbi_decode(np.zeros(len(coded)))
+    d["perm_768"] = ref.make_interleaver(99, [4, 3], 768)
+    d["perm_7200"] = ref.make_interleaver(12345, [1, 0, 5, 4, 31], 7200)
+    sweep = np.zeros((len(SWEEP_CASES), 4), np.int64)
+    for i, (B, U, bits, K, trk, snr, n_sc, trials) in enumerate(SWEEP_CASES):
+        r = ref.uplink_sweep_point(B, U, bits, K, trk, snr, trials, n_sc, 7, threads=8)
+        sweep[i] = [r["frames"], r["block_errors"], r["breakdowns"], r["trials_run"]]
+    d["sweep"] = sweep
+    return d
+
+
 def main():
     ref = oracle.Oracle("ref")
+    if "--only-coding" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "coding.npz"), **coding_fixtures(ref))
+        print("wrote coding.npz")
+        return
     rng = np.random.default_rng(20260419)
     out = {}
     for name, B, U, S, K, trk, bits, snr, n_sc in DETECT_CASES:
@@ -101,6 +139,7 @@ def main():
     out["rng"] = dict(u64=ref.rng_u64(12345, [2, 7], 16),
                       gauss=ref.rng_cgaussian(99, [3, 11], 0.5, 8),
                       rayleigh=ref.rayleigh(5, [2, 3], 8, 4))
+    out["coding"] = coding_fixtures(ref)
     for name, d in out.items():
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
     print(f"wrote {len(out)} fixtures to {HERE}")

@@ -186,3 +186,40 @@ def test_splitmix_restatement_in_python(oracle_port):
     k = fork(fork(777, 4), 9)
     want = [mix((k + G * c) & M) for c in range(1, 6)]
     assert list(oracle_port.rng_u64(777, [4, 9], 5)) == want
+
+
+# ------------------------------------------------------- coding (coding.cpp)
+def test_port_coding_matches_reference_fixture(oracle_port):
+    d = load("coding")
+    for i in range(3):
+        assert np.array_equal(oracle_port.conv_encode(d[f"info{i}"]), d[f"coded{i}"])
+        for kind in ("noisy", "ties"):
+            got = oracle_port.viterbi_decode(d[f"llr_{kind}{i}"])
+            assert np.array_equal(got, d[f"dec_{kind}{i}"]), (i, kind)
+        assert np.array_equal(oracle_port.viterbi_decode(np.zeros(len(d[f"coded{i}"]))),
+                              d[f"dec_zero{i}"])
+    assert np.array_equal(oracle_port.make_interleaver(99, [4, 3], 768), d["perm_768"])
+    assert np.array_equal(oracle_port.make_interleaver(12345, [1, 0, 5, 4, 31], 7200),
+                          d["perm_7200"])
+
+
+def test_port_coding_equals_reference_random(oracle_ref, oracle_port):
+    rng = np.random.default_rng(5)
+    for n in (4, 34, 289):  # + 6 = multiples of the puncture period 5
+        info = rng.integers(0, 2, n).astype(np.uint8)
+        coded = oracle_ref.conv_encode(info)
+        assert np.array_equal(oracle_port.conv_encode(info), coded)
+        llr = np.round(rng.standard_normal(len(coded)) * 3) / 2  # many ties
+        assert np.array_equal(oracle_port.viterbi_decode(llr), oracle_ref.viterbi_decode(llr))
+    perm = oracle_port.make_interleaver(3, [9], 1000)
+    assert np.array_equal(np.sort(perm), np.arange(1000))
+    assert np.array_equal(perm, oracle_ref.make_interleaver(3, [9], 1000))
+
+
+def test_port_coding_rejects_reference_bad_lengths(oracle_port):
+    with pytest.raises(ValueError):
+        oracle_port.conv_encode(np.zeros(5, np.uint8))  # 11 not a multiple of 5
+    with pytest.raises(ValueError):
+        oracle_port.viterbi_decode(np.zeros(7))  # not whole periods
+    with pytest.raises(ValueError):
+        oracle_port.viterbi_decode(np.zeros(6))  # 5 steps < tail 6
