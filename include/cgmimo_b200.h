@@ -149,6 +149,16 @@ int cgm_generate_uplink_correlated(cgm_ctx* ctx, int B, int U, long sc0, long n_
 int cgm_uplink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K, int tracker,
                       double snr_db, long n_trials, const uint64_t* trial_keys,
                       uint32_t* user_errors, uint8_t* breakdown);
+/* run_downlink_trial (sim.cpp:205-275) for a batch of trials: same frames
+ * and streams, H_d = H^H of the trial's Rayleigh draws, ONE batched
+ * precode_cg over all (symbol, subcarrier) transmit vectors, z = H_d s plus
+ * noise per user, the genie demapper (gain z_u / t_u, LLRs of y_u / gain at
+ * rho = |gain|^2 / N0), deinterleaving and soft Viterbi.  snr_db per user
+ * (N0 = 1 / SNR, rho_d = 1 / N0); trial_keys[t] = cgm_sweep_trial_key(seed,
+ * 2, point, trial) (sim.cpp:397-399). */
+int cgm_downlink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K,
+                        double snr_db, long n_trials, const uint64_t* trial_keys,
+                        uint32_t* user_errors, uint8_t* breakdown);
 uint64_t cgm_sweep_trial_key(uint64_t seed, int direction, long point, long trial);
 /* Soft max-log Viterbi decoding of n_cw rate-5/6 codewords (coding.cpp:90-147):
  * llrs [n_cw][coded_len] in coded-bit order (positive favours 1), coded_len a

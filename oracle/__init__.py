@@ -206,6 +206,19 @@ class Oracle:
             raise RuntimeError("run_uplink_sweep raised")
         return dict(zip(("frames", "block_errors", "breakdowns", "trials_run"), map(int, out)))
 
+    def downlink_sweep_point(self, B, U, qam_bits, K, snr_db, trials, n_sc, seed,
+                             threads=0) -> dict:
+        """sim::run_downlink_sweep (sim.cpp:386-405) at one SNR, CG precoder."""
+        self._need_ref("downlink_sweep_point")
+        out = np.zeros(4, np.int64)
+        rc = self.lib.ref_downlink_sweep_point(
+            C.c_int(B), C.c_int(U), C.c_int(qam_bits), C.c_int(K), C.c_double(snr_db),
+            C.c_long(trials), C.c_long(n_sc), C.c_uint64(seed), C.c_int(threads),
+            out.ctypes.data_as(C.c_void_p))
+        if rc != 0:
+            raise RuntimeError("run_downlink_sweep raised")
+        return dict(zip(("frames", "block_errors", "breakdowns", "trials_run"), map(int, out)))
+
     def rng_u64(self, key: int, forks, n: int) -> np.ndarray:
         fk = np.ascontiguousarray(forks, dtype=np.uint64)
         out = np.zeros(n, np.uint64)

@@ -388,11 +388,12 @@ void ref_make_interleaver(uint64_t key, const uint64_t* forks, int n_forks, long
   for (long i = 0; i < n; ++i) perm[i] = static_cast<int64_t>(p[i]);
 }
 
-// One SNR point of the reference's uplink BLER sweep (CG detector):
+// One SNR point of the reference's uplink or downlink BLER sweep (CG solver):
 // out = {frames, block_errors, breakdowns, trials_run}; returns 0, or -1 on
 // an exception (e.g. BreakdownBudgetExceeded is disabled by fraction 1.0).
-int ref_uplink_sweep_point(int B, int U, int qam_bits, int K, int tracker, double snr_db,
-                           long trials, long n_sc, uint64_t seed, int threads, long* out) {
+static int sweep_point(bool downlink, int B, int U, int qam_bits, int K, int tracker,
+                       double snr_db, long trials, long n_sc, uint64_t seed, int threads,
+                       long* out) {
   try {
     sim::SweepConfig cfg;
     cfg.bs_antennas = static_cast<std::size_t>(B);
@@ -409,7 +410,7 @@ int ref_uplink_sweep_point(int B, int U, int qam_bits, int K, int tracker, doubl
     cfg.seed = seed;
     cfg.threads = static_cast<std::size_t>(threads);
     cfg.max_breakdown_fraction = 1.0;
-    const auto r = sim::run_uplink_sweep(cfg);
+    const auto r = downlink ? sim::run_downlink_sweep(cfg) : sim::run_uplink_sweep(cfg);
     const auto& pt = r.points.at(0);
     out[0] = static_cast<long>(pt.frames);
     out[1] = static_cast<long>(pt.block_errors);
@@ -419,6 +420,17 @@ int ref_uplink_sweep_point(int B, int U, int qam_bits, int K, int tracker, doubl
   } catch (const std::exception&) {
     return -1;
   }
+}
+
+int ref_uplink_sweep_point(int B, int U, int qam_bits, int K, int tracker, double snr_db,
+                           long trials, long n_sc, uint64_t seed, int threads, long* out) {
+  return sweep_point(false, B, U, qam_bits, K, tracker, snr_db, trials, n_sc, seed, threads, out);
+}
+
+// run_downlink_sweep (sim.cpp:386-405) at one SNR, CG precoder; same outputs
+int ref_downlink_sweep_point(int B, int U, int qam_bits, int K, double snr_db, long trials,
+                             long n_sc, uint64_t seed, int threads, long* out) {
+  return sweep_point(true, B, U, qam_bits, K, 1, snr_db, trials, n_sc, seed, threads, out);
 }
 
 }  // extern "C"

@@ -51,6 +51,8 @@ SIGNATURES = {
                                               _dbl, _vp, _vp, _vp, _vp]),
     "cgm_uplink_trials": (_int, [_vp, _int, _int, _int, _int, _int, _int, _dbl, _long, _vp, _vp,
                                  _vp]),
+    "cgm_downlink_trials": (_int, [_vp, _int, _int, _int, _int, _int, _dbl, _long, _vp, _vp,
+                                   _vp]),
     "cgm_sweep_trial_key": (_u64, [_u64, _int, _long, _long]),
     "cgm_viterbi_decode": (_int, [_vp, _vp, _long, _long, _vp]),
     "cgm_comm_unique_id": (_int, [C.c_char_p]),

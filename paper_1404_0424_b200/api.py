@@ -127,6 +127,21 @@ class Context:
                                                brk.ctypes.data_as(C.c_void_p)))
         return errs, brk
 
+    def downlink_trials(self, B, U, n_sc, qam_bits, K, snr_db, trial_keys):
+        """cgm_downlink_trials: block errors and breakdown flags of a batch of
+        the reference's coded downlink trials (sim.cpp:205-275)."""
+        import numpy as np
+
+        keys = np.ascontiguousarray(trial_keys, dtype=np.uint64)
+        n = len(keys)
+        errs = np.zeros(n, np.uint32)
+        brk = np.zeros(n, np.uint8)
+        self._check(self.lib.cgm_downlink_trials(self.h, B, U, n_sc, qam_bits, K, float(snr_db), n,
+                                                 keys.ctypes.data_as(C.c_void_p),
+                                                 errs.ctypes.data_as(C.c_void_p),
+                                                 brk.ctypes.data_as(C.c_void_p)))
+        return errs, brk
+
     def viterbi_decode(self, llrs):
         """cgm_viterbi_decode: (n_cw, coded_len) float64 LLRs -> (n_cw, info_len) bits."""
         import numpy as np

@@ -28,6 +28,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "../../include/cgmimo_b200.h"
@@ -114,6 +115,90 @@ __global__ void gen_received_trials(float2* Y, const float2* H, const uint8_t* l
       }
       const double2 nz = gauss_pair(nk, static_cast<uint64_t>(b), sqrt(0.5 * n0));
       Y[(g * B + b) * S + sym] = make_float2(static_cast<float>(re + nz.x), static_cast<float>(im + nz.y));
+    }
+    __syncthreads();
+  }
+}
+
+// Downlink transmit vectors t of every (trial, subcarrier, symbol): the
+// frames' constellation points (sim.cpp:233-236), T layout [g][sym][u]
+__global__ void gen_transmit_trials(float2* T, const uint8_t* labels, int bits, long n) {
+  for (long idx = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; idx < n;
+       idx += static_cast<long>(gridDim.x) * blockDim.x) {
+    const double2 x = qam_point(labels[idx], bits);
+    T[idx] = make_float2(static_cast<float>(x.x), static_cast<float>(x.y));
+  }
+}
+
+// detect::compute_llrs (detect.cpp:57-86) in FP64 for the downlink genie
+// demapper: z = xhat / mu, I-axis bits then Q-axis bits, per axis bit p the
+// nearest amplitude with bit p = 0 vs 1, rho * (d0 - d1), clip +-64
+__device__ void llrs_fp64(double zr, double zi, double rho, int bits, float* out) {
+  const int half = bits / 2;
+  const unsigned levels = 1u << half;
+  const double scale = 1.0 / sqrt(2.0 * ((double)levels * levels - 1.0) / 3.0);
+  if (rho < 0.0) rho = 0.0;
+  for (int axis = 0; axis < 2; ++axis) {
+    const double z = axis == 0 ? zr : zi;
+    for (int p = 0; p < half; ++p) {
+      double d0 = INFINITY, d1 = INFINITY;
+      for (unsigned g = 0; g < levels; ++g) {
+        const double amp = (2.0 * gray_decode(g) - (levels - 1.0)) * scale;
+        const double d = (z - amp) * (z - amp);
+        if ((g >> (half - 1 - p)) & 1u) d1 = d < d1 ? d : d1;
+        else d0 = d < d0 ? d : d0;
+      }
+      double v = rho * (d0 - d1);
+      v = v < -64.0 ? -64.0 : (v > 64.0 ? 64.0 : v);
+      out[axis * half + p] = static_cast<float>(v);
+    }
+  }
+}
+
+// Downlink receive side of run_downlink_trial (sim.cpp:248-266): z = H_d s
+// with H_d = H^H, y_u = z_u + n_u (n_u = next_gaussian pair u of
+// Rng(key_t).fork(3).fork(sym * n_sc + sc)), genie gain z_u / t_u, LLRs of
+// y_u / gain at rho = |gain|^2 / N0, zeros below |gain|^2 < 1e-24.
+__global__ void downlink_receive(float* llr, const float2* H, const float2* Sx,
+                                 const uint8_t* labels, int B, int U, int n_sc, int S, int bits,
+                                 double n0, long n_tot, const uint64_t* keys) {
+  extern __shared__ double2 sv[];
+  const double sd = sqrt(0.5 * n0);
+  for (long inst = blockIdx.x; inst < n_tot * S; inst += gridDim.x) {
+    const long g = inst / S;
+    const int sym = static_cast<int>(inst - g * S);
+    const long t = g / n_sc, sc = g - t * n_sc;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+      const float2 v = Sx[inst * B + b];
+      sv[b] = make_double2(v.x, v.y);
+    }
+    __syncthreads();
+    const uint64_t nk =
+        fork_key(fork_key(keys[t], 3), static_cast<uint64_t>(sym) * n_sc + static_cast<uint64_t>(sc));
+    const float2* h = H + g * static_cast<long>(B) * U;
+    for (int u = threadIdx.x; u < U; u += blockDim.x) {
+      double zr = 0.0, zi = 0.0;  // sum_b conj(H[b][u]) s_b
+      for (int b = 0; b < B; ++b) {
+        const float2 hv = h[b * U + u];
+        zr += static_cast<double>(hv.x) * sv[b].x + static_cast<double>(hv.y) * sv[b].y;
+        zi += static_cast<double>(hv.x) * sv[b].y - static_cast<double>(hv.y) * sv[b].x;
+      }
+      // cplx(sd * g(), sd * g()) at sim.cpp:252: the two draws are unsequenced
+      // constructor arguments; g++ (the reference's compiler) evaluates them
+      // right to left, so the real part gets the pair's SECOND variate
+      const double2 nz = gauss_pair(nk, static_cast<uint64_t>(u), sd);
+      const double yr = zr + nz.y, yi = zi + nz.x;
+      const double2 x = qam_point(labels[inst * U + u], bits);
+      const double xn = x.x * x.x + x.y * x.y;  // gain = z / t
+      const double gr = (zr * x.x + zi * x.y) / xn, gi = (zi * x.x - zr * x.y) / xn;
+      const double g2 = gr * gr + gi * gi;
+      float* o = llr + inst * static_cast<long>(U) * bits + u * bits;
+      if (g2 < 1e-24) {
+        for (int b = 0; b < bits; ++b) o[b] = 0.f;
+      } else {  // y / gain
+        const double qr = (yr * gr + yi * gi) / g2, qi = (yi * gr - yr * gi) / g2;
+        llrs_fp64(qr, qi, g2 / n0, bits, o);
+      }
     }
     __syncthreads();
   }
@@ -360,9 +445,15 @@ __global__ void __launch_bounds__(32 * kVitWarps) viterbi_decode(
 
 extern "C" {
 
-int cgm_uplink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K, int tracker,
-                      double snr_db, long n_trials, const uint64_t* trial_keys,
-                      uint32_t* user_errors, uint8_t* breakdown) {
+}  // extern "C"
+
+namespace {
+
+// run_uplink_trial / run_downlink_trial (sim.cpp:147-275) for a batch of trials
+int run_trials(cgm_ctx* ctx, bool downlink, int B, int U, int n_sc, int qam_bits, int K,
+               int tracker, double snr_db, long n_trials, const uint64_t* trial_keys,
+               uint32_t* user_errors, uint8_t* breakdown) {
+  const char* who = downlink ? "cgm_downlink_trials" : "cgm_uplink_trials";
   void* stv = nullptr;
   int sms = 0;
   long* launches = nullptr;
@@ -370,7 +461,7 @@ int cgm_uplink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K,
   cudaStream_t st = static_cast<cudaStream_t>(stv);
   if (B < 1 || U < 1 || U > B || n_sc < 1 || n_trials < 0 || !trial_keys || !user_errors ||
       (qam_bits != 2 && qam_bits != 4 && qam_bits != 6))
-    return cgm_internal_fail(ctx, CGM_EINVAL, "cgm_uplink_trials: bad arguments");
+    return cgm_internal_fail(ctx, CGM_EINVAL, (std::string(who) + ": bad arguments").c_str());
   if (n_trials == 0) return CGM_OK;
   // CGMIMO_HARNESS_TIMING=1: phase timings on stderr (pipeline study)
   const bool timing = std::getenv("CGMIMO_HARNESS_TIMING") != nullptr;
@@ -386,17 +477,18 @@ int cgm_uplink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K,
   };
   Plan pl;
   if (!plan_frame(n_sc, qam_bits, pl))
-    return cgm_internal_fail(ctx, CGM_EINVAL, "cgm_uplink_trials: frame does not fit the code");
+    return cgm_internal_fail(ctx, CGM_EINVAL, (std::string(who) + ": frame does not fit the code").c_str());
   const int S = pl.n_sym, bps = pl.bps;
-  const double n0 = static_cast<double>(U) / std::pow(10.0, snr_db / 10.0);  // channel.cpp:44-47
+  // channel.cpp:44-52: N0 = U / SNR uplink (per receive antenna), 1 / SNR downlink
+  const double n0 = (downlink ? 1.0 : static_cast<double>(U)) / std::pow(10.0, snr_db / 10.0);
   const long n_tot = n_trials * n_sc, n_cw = n_trials * U;
   // ---- device buffers (stream-ordered: the pool keeps them across calls)
   const long total_steps = pl.info + kTail;
   void *dH = nullptr, *dY = nullptr, *dLab = nullptr, *dLlr = nullptr, *dSt = nullptr,
        *dKeys = nullptr, *dInfo = nullptr, *dPerm = nullptr, *dCoded = nullptr, *dDec = nullptr,
-       *dErr = nullptr;
+       *dErr = nullptr, *dT = nullptr;
   auto cleanup = [&] {
-    for (void* q : {dH, dY, dLab, dLlr, dSt, dKeys, dInfo, dPerm, dCoded, dDec, dErr})
+    for (void* q : {dH, dY, dLab, dLlr, dSt, dKeys, dInfo, dPerm, dCoded, dDec, dErr, dT})
       if (q) cudaFreeAsync(q, st);
   };
   cudaError_t e = cudaSuccess;
@@ -423,9 +515,10 @@ int cgm_uplink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K,
   A(&dCoded, static_cast<size_t>(n_cw) * pl.coded * 8);
   A(&dDec, static_cast<size_t>(n_cw) * total_steps * 8);
   A(&dErr, static_cast<size_t>(n_cw));
+  if (downlink) A(&dT, static_cast<size_t>(n_tot) * S * U * 8);
   if (e != cudaSuccess) {
     cleanup();
-    return cgm_internal_fail(ctx, CGM_ENOMEM, "cgm_uplink_trials: device allocation");
+    return cgm_internal_fail(ctx, CGM_ENOMEM, (std::string(who) + ": device allocation").c_str());
   }
   cudaMemcpyAsync(dKeys, trial_keys, static_cast<size_t>(n_trials) * 8, cudaMemcpyHostToDevice, st);
   mark("alloc+keys");
@@ -457,19 +550,41 @@ int cgm_uplink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K,
   mark("frames");
   gen_channel_trials<<<grid(n_tot * B * U), 256, 0, st>>>(static_cast<float2*>(dH), B, U, n_sc,
                                                          n_tot, static_cast<uint64_t*>(dKeys));
-  gen_received_trials<<<static_cast<unsigned>(std::min<long>(n_tot * S, 32L * sms)), 128,
-                        U * sizeof(double2), st>>>(
-      static_cast<float2*>(dY), static_cast<float2*>(dH), static_cast<uint8_t*>(dLab), B, U, n_sc,
-      S, bps, n0, n_tot, static_cast<uint64_t*>(dKeys));
-  *launches += 2;
-  e = cudaGetLastError();
-  mark("channel+y");
   int rc = CGM_OK;
-  if (e == cudaSuccess) {
+  if (!downlink) {
+    gen_received_trials<<<static_cast<unsigned>(std::min<long>(n_tot * S, 32L * sms)), 128,
+                          U * sizeof(double2), st>>>(
+        static_cast<float2*>(dY), static_cast<float2*>(dH), static_cast<uint8_t*>(dLab), B, U, n_sc,
+        S, bps, n0, n_tot, static_cast<uint64_t*>(dKeys));
+    *launches += 2;
+    e = cudaGetLastError();
+    mark("channel+y");
     // ---- ONE batched detection over every subcarrier of every trial
-    rc = cgm_detect_cg(ctx, B, U, n_tot, S, static_cast<float*>(dH), static_cast<float*>(dY),
-                       1.0 / n0, n0, 1.0, qam_bits, K, tracker, nullptr, nullptr, nullptr,
-                       static_cast<float*>(dLlr), static_cast<uint8_t*>(dSt), CGM_DEVICE_POINTERS);
+    if (e == cudaSuccess)
+      rc = cgm_detect_cg(ctx, B, U, n_tot, S, static_cast<float*>(dH), static_cast<float*>(dY),
+                         1.0 / n0, n0, 1.0, qam_bits, K, tracker, nullptr, nullptr, nullptr,
+                         static_cast<float*>(dLlr), static_cast<uint8_t*>(dSt), CGM_DEVICE_POINTERS);
+  } else {
+    gen_transmit_trials<<<grid(n_tot * S * U), 256, 0, st>>>(
+        static_cast<float2*>(dT), static_cast<uint8_t*>(dLab), bps, n_tot * S * U);
+    *launches += 2;
+    e = cudaGetLastError();
+    mark("channel+t");
+    // ---- ONE batched precode over every (symbol, subcarrier) of every
+    // trial; H_d = H^H from the uplink-layout draws (sim.cpp:223); the
+    // transmit vectors s land in dY (same size)
+    if (e == cudaSuccess)
+      rc = cgm_precode_cg(ctx, B, U, n_tot, S, static_cast<float*>(dH), static_cast<float*>(dT),
+                          1.0 / n0, K, nullptr, static_cast<float*>(dY), nullptr,
+                          static_cast<uint8_t*>(dSt), CGM_DEVICE_POINTERS | CGM_HD_UPLINK_LAYOUT);
+    if (rc == CGM_OK) {
+      downlink_receive<<<static_cast<unsigned>(std::min<long>(n_tot * S, 32L * sms)), 64,
+                         B * sizeof(double2), st>>>(
+          static_cast<float*>(dLlr), static_cast<float2*>(dH), static_cast<float2*>(dY),
+          static_cast<uint8_t*>(dLab), B, U, n_sc, S, bps, n0, n_tot, static_cast<uint64_t*>(dKeys));
+      ++*launches;
+      e = cudaGetLastError();
+    }
   }
   mark("detect");
   if (e == cudaSuccess && rc == CGM_OK) {
@@ -495,13 +610,31 @@ int cgm_uplink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K,
   if (e != cudaSuccess) return cgm_internal_fail(ctx, CGM_ECUDA, cudaGetErrorString(e));
   for (long t = 0; t < n_trials; ++t) {
     bool broke = false;
-    for (long i = t * n_sc * S; i < (t + 1) * n_sc * S; ++i) broke |= stat[i] != 0;
+    for (long i = t * n_sc * S; i < (t + 1) * n_sc * S; ++i) broke |= (stat[i] & 1u) != 0;
     uint32_t ue = 0;
     for (int u = 0; u < U; ++u) ue += errs[t * U + u];
     user_errors[t] = broke ? 0u : ue;
     if (breakdown) breakdown[t] = broke ? 1 : 0;
   }
   return CGM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cgm_uplink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K, int tracker,
+                      double snr_db, long n_trials, const uint64_t* trial_keys,
+                      uint32_t* user_errors, uint8_t* breakdown) {
+  return run_trials(ctx, false, B, U, n_sc, qam_bits, K, tracker, snr_db, n_trials, trial_keys,
+                    user_errors, breakdown);
+}
+
+int cgm_downlink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K,
+                        double snr_db, long n_trials, const uint64_t* trial_keys,
+                        uint32_t* user_errors, uint8_t* breakdown) {
+  return run_trials(ctx, true, B, U, n_sc, qam_bits, K, CGM_TRACKER_APPROX, snr_db, n_trials,
+                    trial_keys, user_errors, breakdown);
 }
 
 int cgm_viterbi_decode(cgm_ctx* ctx, const double* llrs, long coded_len, long n_cw,

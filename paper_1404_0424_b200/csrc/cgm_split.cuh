@@ -530,6 +530,14 @@ __device__ __forceinline__ void k2_precode_tail(const KernelParams& p, long sc, 
             for (int t = 0; t < 8; ++t)
               if (ts0 + t < St) cfma(acc[t], h, Vs[(S + ts0 + t) * UP + u]);
           }
+        } else if (U != UP) {
+          const float2* hu = p.H + (sc * static_cast<long>(B) + bb) * U;  // row b of H_u
+          for (int u = 0; u < U; ++u) {
+            const float2 h = __ldg(hu + u);
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+              if (ts0 + t < St) cfma(acc[t], h, Vs[(S + ts0 + t) * UP + u]);
+          }
         } else {
           const float2* hu = p.H + sc * static_cast<long>(B) * UP + bb * UP;  // row b of H_u
 #pragma unroll 4

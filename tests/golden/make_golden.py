@@ -54,6 +54,14 @@ SWEEP_CASES = [
     (16, 4, 2, 2, "exact", 2.0, 90, 32),      # QPSK
 ]
 
+# run_downlink_sweep points (sim.cpp:386-405): (B, U, qam_bits, K, snr_db, n_sc, trials), seed 7
+DL_SWEEP_CASES = [
+    (32, 8, 6, 4, 13.0, 128, 48),
+    (64, 16, 4, 3, 7.0, 60, 32),
+    (16, 4, 2, 2, 0.0, 90, 32),
+    (32, 8, 6, 1, 12.0, 128, 32),   # K = 1: matched-filter direction
+]
+
 
 def coding_fixtures(ref):
     """coding.cpp: encoder outputs, soft-Viterbi decisions (incl. tie-heavy
@@ -76,6 +84,11 @@ def coding_fixtures(ref):
         r = ref.uplink_sweep_point(B, U, bits, K, trk, snr, trials, n_sc, 7, threads=8)
         sweep[i] = [r["frames"], r["block_errors"], r["breakdowns"], r["trials_run"]]
     d["sweep"] = sweep
+    dl = np.zeros((len(DL_SWEEP_CASES), 4), np.int64)
+    for i, (B, U, bits, K, snr, n_sc, trials) in enumerate(DL_SWEEP_CASES):
+        r = ref.downlink_sweep_point(B, U, bits, K, snr, trials, n_sc, 7, threads=8)
+        dl[i] = [r["frames"], r["block_errors"], r["breakdowns"], r["trials_run"]]
+    d["sweep_dl"] = dl
     return d
 
 

@@ -13,7 +13,7 @@ from paper_1404_0424_b200 import sim
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLDEN = os.path.join(HERE, "golden", "coding.npz")
 sys.path.insert(0, os.path.join(HERE, "golden"))
-from make_golden import SWEEP_CASES  # noqa: E402
+from make_golden import DL_SWEEP_CASES, SWEEP_CASES  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -69,6 +69,18 @@ def test_uplink_trials_match_reference_sweep(gpu_ctx, case):
     assert got["block_errors"] == want["block_errors"], (got["block_errors"], want["block_errors"])
     # the operating points are chosen to decode some blocks and lose others
     assert 0 < want["block_errors"] < want["frames"] or tracker == "exact"
+
+
+@pytest.mark.parametrize("case", range(len(DL_SWEEP_CASES)))
+def test_downlink_trials_match_reference_sweep(gpu_ctx, case):
+    """run_downlink_sweep's counts: CG precoding of every (symbol,
+    subcarrier) in one batch, the genie demapper, Viterbi (sim.cpp:205-275)."""
+    B, U, bits, K, snr, n_sc, trials = DL_SWEEP_CASES[case]
+    f = np.load(GOLDEN)["sweep_dl"][case]
+    got = sim.downlink_sweep_point(gpu_ctx, B, U, bits, K, snr, trials, n_sc, 7)
+    assert got["frames"] == int(f[0])
+    assert got["breakdowns"] == int(f[2])
+    assert got["block_errors"] == int(f[1]), (got["block_errors"], int(f[1]))
 
 
 def test_trial_keys_follow_reference_forks(oracle_port):

@@ -203,3 +203,21 @@ def test_tiled_cg_kernel_matches_default(gpu_ctx, monkeypatch, name):
             x, y = torch.view_as_real(x), torch.view_as_real(y)
         tol = 1e-4 + 1e-3 * float(x.abs().max()) if k != "llr" else 1e-3 * 64
         assert float((x - y).abs().max()) <= tol, k
+
+
+@pytest.mark.parametrize("U,B,K", [(4, 16, 2), (8, 32, 4), (16, 64, 3), (32, 128, 4)])
+def test_precode_uplink_layout_equals_downlink_layout(gpu_ctx, U, B, K):
+    """precode_cg given H_u with CGM_HD_UPLINK_LAYOUT == precode_cg given
+    H_d = H_u^H explicitly (sim.cpp:223 builds H_d exactly so)."""
+    g = torch.Generator().manual_seed(U)
+    n_sc, S = 37, 3
+    H = torch.complex(torch.randn(n_sc, B, U, generator=g), torch.randn(n_sc, B, U, generator=g))
+    T = torch.complex(torch.randn(n_sc, S, U, generator=g), torch.randn(n_sc, S, U, generator=g))
+    H, T = (H / 2 ** 0.5).cuda(), (T / 2 ** 0.5).cuda()
+    Hd = H.conj().transpose(1, 2).contiguous()
+    a = gpu_ctx.precode_cg(H, T, 3.0, K, uplink_layout=True)
+    b = gpu_ctx.precode_cg(Hd, T, 3.0, K)
+    torch.cuda.synchronize()
+    for k in ("q", "s"):
+        d = float((a[k] - b[k]).abs().max() / b[k].abs().max())
+        assert d < 1e-5, (k, d)
