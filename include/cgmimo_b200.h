@@ -110,6 +110,26 @@ int cgm_detect_precode_cg(cgm_ctx* ctx, int B, int U, long n_sc, int S, const fl
                           uint8_t* status, int St, const float* T, double rho_d, int Kt,
                           float* q, float* s, float* gain, uint8_t* pstatus, unsigned flags);
 
+/* ---- the other solvers of the reference's trade-off study (SURVEY.md
+ * section 8(f) row 4), same layouts, flags and status bytes as above, plus
+ * status bit2 = not positive definite / zero diagonal (the reference throws
+ * solvers::NotPositiveDefinite / std::domain_error, solvers.cpp:246-247,
+ * :332-333).  method follows sim::Method (sim.hpp:34). */
+#define CGM_METHOD_CHOLESKY 0 /* detect_cholesky (detect.cpp:122-181) / precode_explicit (precode.cpp:45-54) */
+#define CGM_METHOD_CG 1       /* detect_cg / precode_cg: same as the _cg entry points */
+#define CGM_METHOD_CGLS 2     /* detect_cgls (detect.cpp:238-272) / precode_cgls (precode.cpp:73-82) */
+#define CGM_METHOD_NEUMANN 3  /* detect_neumann (detect.cpp:274-326) / precode_neumann (precode.cpp:84-93) */
+/* iters = CG/CGLS iterations or Neumann series terms (ignored by Cholesky);
+ * tracker is used by CG only (CGLS always runs the approximate tracker,
+ * detect.cpp:258-263). */
+int cgm_detect(cgm_ctx* ctx, int method, int B, int U, long n_sc, int S, const float* H,
+               const float* Y, double rho_u, double n0, double es, int qam_bits, int iters,
+               int tracker, float* xhat, float* mu, float* rho, float* llr, uint8_t* status,
+               unsigned flags);
+int cgm_precode(cgm_ctx* ctx, int method, int B, int U, long n_sc, int S, const float* Hd,
+                const float* T, double rho_d, int iters, float* q, float* s, float* gain,
+                uint8_t* status, unsigned flags);
+
 /* Seeded synthetic inputs on the device (always device pointers, async),
  * following the reference's stream conventions (sim.cpp:151-179,
  * channel.cpp:10-30, rng.cpp): with root = Rng(seed),

@@ -92,17 +92,20 @@ class Oracle:
         status = np.zeros((n_sc, S), np.uint8)
         trk = 0 if tracker == "exact" else 1
         common_out = (_ptr(xhat), _ptr(mu), _ptr(rho), _ptr(llr), _ptr(status, _u8p))
+        base = [C.c_int(B), C.c_int(U), C.c_long(n_sc), C.c_int(S), _ptr(H), _ptr(Y),
+                C.c_double(rho_u), C.c_double(n0), C.c_double(es), C.c_int(qam_bits)]
         if method == "cg":
             f = self._fn("detect_cg")
-            args = [C.c_int(B), C.c_int(U), C.c_long(n_sc), C.c_int(S), _ptr(H), _ptr(Y),
-                    C.c_double(rho_u), C.c_double(n0), C.c_double(es), C.c_int(qam_bits),
-                    C.c_int(K), C.c_int(trk), *common_out]
-        elif method in ("explicit", "cholesky"):
-            f = self._fn("detect_explicit" if method == "explicit" or self.kind == "port"
-                         else "detect_cholesky")
-            args = [C.c_int(B), C.c_int(U), C.c_long(n_sc), C.c_int(S), _ptr(H), _ptr(Y),
-                    C.c_double(rho_u), C.c_double(n0), C.c_double(es), C.c_int(qam_bits),
-                    *common_out]
+            args = [*base, C.c_int(K), C.c_int(trk), *common_out]
+        elif method == "explicit":
+            f = self._fn("detect_explicit")
+            args = [*base, *common_out]
+        elif method in ("cholesky", "chol"):
+            f = self._fn("detect_cholesky")
+            args = [*base, *common_out]
+        elif method in ("cgls", "neumann"):
+            f = self._fn("detect_" + method)
+            args = [*base, C.c_int(K), *common_out]
         else:
             raise ValueError(method)
         if self._threaded:
@@ -125,13 +128,13 @@ class Oracle:
         gain = np.zeros((n_sc, S))
         status = np.zeros((n_sc, S), np.uint8)
         outs = (_ptr(q), _ptr(s), _ptr(gain), _ptr(status, _u8p))
-        if method == "cg":
-            args = [C.c_int(B), C.c_int(U), C.c_long(n_sc), C.c_int(S), _ptr(Hd), _ptr(T),
-                    C.c_double(rho_d), C.c_int(K), *outs]
-            f = self._fn("precode_cg")
-        elif method == "explicit":
-            args = [C.c_int(B), C.c_int(U), C.c_long(n_sc), C.c_int(S), _ptr(Hd), _ptr(T),
-                    C.c_double(rho_d), *outs]
+        base = [C.c_int(B), C.c_int(U), C.c_long(n_sc), C.c_int(S), _ptr(Hd), _ptr(T),
+                C.c_double(rho_d)]
+        if method in ("cg", "cgls", "neumann"):
+            args = [*base, C.c_int(K), *outs]
+            f = self._fn("precode_" + method)
+        elif method in ("explicit", "cholesky", "chol"):
+            args = [*base, *outs]
             f = self._fn("precode_explicit")
         else:
             raise ValueError(method)

@@ -535,6 +535,224 @@ int orc_detect_explicit(int B, int U, long n_sc, int S, const double* H, const d
   return 0;
 }
 
+/* solvers.cpp:323-359: Sum = D^-1 + T D^-1 + T^2 D^-1 + ..., T = -D^-1 E;
+ * from the third term on, one triangle (j >= i) and its mirror.  Returns 1
+ * on a zero diagonal entry (std::domain_error). */
+static int neumann_inverse(const cx* a, int n, int terms, cx* sum, cx* t, cx* term, cx* next,
+                           double* inv_d) {
+  for (int i = 0; i < n; ++i) {
+    const double d = creal(a[(long)i * n + i]);
+    if (fabs(d) < 1e-300) return 1;
+    inv_d[i] = 1.0 / d;
+  }
+  memset(sum, 0, sizeof(cx) * n * n);
+  for (int i = 0; i < n; ++i) sum[(long)i * n + i] = inv_d[i];
+  if (terms == 1) return 0;
+  memset(t, 0, sizeof(cx) * n * n);
+  memset(term, 0, sizeof(cx) * n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      if (i == j) continue;
+      t[(long)i * n + j] = -inv_d[i] * a[(long)i * n + j];
+      term[(long)i * n + j] = t[(long)i * n + j] * inv_d[j];
+    }
+  for (long e = 0; e < (long)n * n; ++e) sum[e] += term[e];
+  for (int extra = 2; extra < terms; ++extra) {
+    for (int i = 0; i < n; ++i)
+      for (int j = i; j < n; ++j) {
+        cx acc = 0.0;
+        for (int k = 0; k < n; ++k) acc += t[(long)i * n + k] * term[(long)k * n + j];
+        next[(long)i * n + j] = acc;
+        if (j != i) next[(long)j * n + i] = conj(acc);
+      }
+    for (long e = 0; e < (long)n * n; ++e) sum[e] += next[e];
+    memcpy(term, next, sizeof(cx) * n * n);
+  }
+  return 0;
+}
+
+/* detect_cholesky (detect.cpp:122-181, method 0), detect_cgls (:238-272,
+ * method 2: cgls_solve_regularized solvers.cpp:141-194 over cgls_core
+ * :87-139 with the approximate tracker), detect_neumann (:274-326, method 3) */
+static int detect_alt(int method, int B, int U, long n_sc, int S, const double* H,
+                      const double* Y, double rho_u, double n0, double es, int qam_bits, int K,
+                      double* xhat, double* mu, double* rho, double* llr, uint8_t* status) {
+  constel_t c;
+  if (constel_make(qam_bits, &c)) return 2;
+  const int bad = !(rho_u > 0.0 && n0 > 0.0 && es > 0.0) || (method != 0 && K < 1);
+  const double rho_inv = 1.0 / rho_u;
+  const int UU = U * U;
+  cx* h = xcalloc((size_t)B * U, sizeof(cx));
+  cx* y = xcalloc((size_t)B + U, sizeof(cx));
+  cx *a = xcalloc(UU, sizeof(cx)), *inv = xcalloc(UU, sizeof(cx)), *m = xcalloc(UU, sizeof(cx));
+  cx *t = xcalloc(UU, sizeof(cx)), *term = xcalloc(UU, sizeof(cx)), *nx = xcalloc(UU, sizeof(cx));
+  cx *col = xcalloc(U, sizeof(cx)), *bv = xcalloc(U, sizeof(cx)), *xh = xcalloc(U, sizeof(cx));
+  cx *sv = xcalloc(U, sizeof(cx)), *dv = xcalloc(U, sizeof(cx)), *qv = xcalloc((size_t)B + U, sizeof(cx));
+  double *gd = xcalloc(U, sizeof(double)), *ad = xcalloc(U, sizeof(double)), *dinv = xcalloc(U, sizeof(double));
+  double *f = xcalloc(U, sizeof(double)), *f1 = xcalloc(U, sizeof(double)), *f2 = xcalloc(U, sizeof(double));
+  double *mus = xcalloc(U, sizeof(double)), *rhos = xcalloc(U, sizeof(double));
+  for (long sc = 0; sc < n_sc; ++sc) {
+    load_cx(H + 2 * sc * B * U, (long)B * U, h);
+    int fail = bad;
+    if (!fail && method != 2) {
+      gram(h, B, U, 0, rho_inv, a);
+      fail = method == 0 ? chol_inverse(a, U, inv, m, col)
+                         : neumann_inverse(a, U, K, inv, t, term, nx, dinv);
+    }
+    if (!fail && method == 0) { /* detect.cpp:154-178, channel only */
+      for (int i = 0; i < U; ++i) {
+        const cx vii = inv[(long)i * U + i];
+        mus[i] = 1.0 - rho_inv * creal(vii);
+        double interference = 0.0, colnorm2 = 0.0;
+        for (int j = 0; j < U; ++j) {
+          const cx v = inv[(long)i * U + j];
+          if (j != i) {
+            const double er = -rho_inv * creal(v), ei = -rho_inv * cimag(v);
+            interference += er * er + ei * ei;
+          }
+          const cx w = inv[(long)j * U + i];
+          colnorm2 += creal(w) * creal(w) + cimag(w) * cimag(w);
+        }
+        const double noise = n0 * (creal(vii) - rho_inv * colnorm2);
+        rhos[i] = safe_rho(mus[i], es * interference + noise);
+      }
+    }
+    if (!fail && method == 3) { /* detect.cpp:299-323 */
+      for (int i = 0; i < U; ++i) {
+        if (K == 1) {
+          mus[i] = creal(inv[(long)i * U + i]) * (creal(a[(long)i * U + i]) - rho_inv);
+        } else {
+          cx dg = 0.0;
+          for (int j = 0; j < U; ++j) {
+            const cx gji = j == i ? creal(a[(long)j * U + j]) - rho_inv : a[(long)j * U + i];
+            dg += inv[(long)i * U + j] * gji;
+          }
+          mus[i] = creal(dg);
+        }
+        double nu2 = es * (mus[i] - mus[i] * mus[i]);
+        if (nu2 < 1e-12) nu2 = 1e-12;
+        rhos[i] = safe_rho(mus[i], nu2);
+      }
+    }
+    if (!fail && method == 2) {
+      for (int i = 0; i < U; ++i) {
+        double d = 0.0;
+        for (int b = 0; b < B; ++b) {
+          const cx v = h[(long)b * U + i];
+          d += creal(v) * creal(v) + cimag(v) * cimag(v);
+        }
+        gd[i] = d;
+        ad[i] = d + rho_inv;
+      }
+    }
+    for (int s = 0; s < S; ++s) {
+      const long inst = sc * S + s;
+      double* xo = xhat + 2 * inst * U;
+      double* mo = mu + inst * U;
+      double* ro = rho + inst * U;
+      double* lo = llr + inst * U * qam_bits;
+      status[inst] = fail ? 4 : 0;
+      if (fail) goto zero;
+      load_cx(Y + 2 * inst * B, B, y);
+      if (method != 2) {
+        for (int u = 0; u < U; ++u) bv[u] = 0.0;
+        for (int b = 0; b < B; ++b)
+          for (int u = 0; u < U; ++u) bv[u] += conj(h[(long)b * U + u]) * y[b];
+        if (method == 3 && K == 1) {
+          for (int i = 0; i < U; ++i) xh[i] = creal(inv[(long)i * U + i]) * bv[i];
+        } else {
+          hmatvec(inv, U, bv, xh);
+        }
+        for (int i = 0; i < U; ++i) { mo[i] = mus[i]; ro[i] = rhos[i]; }
+      } else {
+        /* residual-space vectors carry B + U entries; y_aug = [y; 0] */
+        const double aug = sqrt(rho_inv);
+        for (int i = 0; i < U; ++i) y[B + i] = 0.0;
+        for (int i = 0; i < U; ++i) { xh[i] = 0.0; f[i] = f1[i] = f2[i] = 0.0; }
+        for (int u = 0; u < U; ++u) sv[u] = 0.0;
+        for (int b = 0; b < B; ++b)
+          for (int u = 0; u < U; ++u) sv[u] += conj(h[(long)b * U + u]) * y[b];
+        memcpy(dv, sv, sizeof(cx) * U);
+        double gamma = norm2_sq(sv, U);
+        const double gamma0 = gamma;
+        double am1 = 1.0, am2 = 1.0, bm1 = 0.0, bm2 = 0.0;
+        int broke = 0;
+        for (int k = 1; k <= K; ++k) {
+          double alpha = 1.0, beta = 0.0;
+          if (!(gamma <= 1e-28 * gamma0)) {
+            for (int b = 0; b < B; ++b) {
+              cx acc = 0.0;
+              for (int j = 0; j < U; ++j) acc += h[(long)b * U + j] * dv[j];
+              qv[b] = acc;
+            }
+            for (int j = 0; j < U; ++j) qv[B + j] = aug * dv[j];
+            const double qn2 = norm2_sq(qv, B + U);
+            if (qn2 < 1e-30) { broke = 1; break; }
+            alpha = gamma / qn2;
+            for (int j = 0; j < U; ++j) xh[j] += alpha * dv[j];
+            for (int b = 0; b < B + U; ++b) y[b] -= alpha * qv[b];
+            for (int u = 0; u < U; ++u) sv[u] = 0.0;
+            for (int b = 0; b < B; ++b)
+              for (int u = 0; u < U; ++u) sv[u] += conj(h[(long)b * U + u]) * y[b];
+            for (int u = 0; u < U; ++u) sv[u] += aug * y[B + u];
+            const double gn = norm2_sq(sv, U);
+            beta = gn / gamma;
+            gamma = gn;
+            for (int u = 0; u < U; ++u) dv[u] = sv[u] + beta * dv[u];
+          }
+          /* ApproxSinrTracker::step (detect.cpp:400-428) */
+          for (int i = 0; i < U; ++i) {
+            double nxv;
+            if (k == 1) {
+              nxv = alpha;
+            } else {
+              const double c1 = alpha * (1.0 + bm1) / am1, c2 = alpha * bm2 / am2;
+              nxv = f[i] + (c1 - alpha * ad[i]) * (f[i] - f1[i]) - c2 * (f1[i] - f2[i]);
+            }
+            f2[i] = f1[i];
+            f1[i] = f[i];
+            f[i] = nxv;
+          }
+          am2 = am1; am1 = alpha; bm2 = bm1; bm1 = beta;
+        }
+        if (broke) { status[inst] = 1; goto zero; }
+        for (int i = 0; i < U; ++i) { /* detect.cpp:430-441 */
+          mo[i] = f[i] * gd[i];
+          ro[i] = n0 > 0.0 ? gd[i] / n0 : 0.0;
+        }
+      }
+      store_cx(xh, U, xo);
+      for (int i = 0; i < U; ++i) llrs_one(xh[i], mo[i], ro[i], &c, lo + (long)i * qam_bits);
+      continue;
+    zero:
+      memset(xo, 0, sizeof(double) * 2 * U);
+      memset(mo, 0, sizeof(double) * U);
+      memset(ro, 0, sizeof(double) * U);
+      memset(lo, 0, sizeof(double) * U * qam_bits);
+    }
+  }
+  free(h); free(y); free(a); free(inv); free(m); free(t); free(term); free(nx); free(col);
+  free(bv); free(xh); free(sv); free(dv); free(qv); free(gd); free(ad); free(dinv);
+  free(f); free(f1); free(f2); free(mus); free(rhos);
+  return 0;
+}
+
+int orc_detect_cholesky(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                        double rho_u, double n0, double es, int qam_bits, double* xhat,
+                        double* mu, double* rho, double* llr, uint8_t* status) {
+  return detect_alt(0, B, U, n_sc, S, H, Y, rho_u, n0, es, qam_bits, 1, xhat, mu, rho, llr, status);
+}
+int orc_detect_cgls(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                    double rho_u, double n0, double es, int qam_bits, int K, double* xhat,
+                    double* mu, double* rho, double* llr, uint8_t* status) {
+  return detect_alt(2, B, U, n_sc, S, H, Y, rho_u, n0, es, qam_bits, K, xhat, mu, rho, llr, status);
+}
+int orc_detect_neumann(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                       double rho_u, double n0, double es, int qam_bits, int K, double* xhat,
+                       double* mu, double* rho, double* llr, uint8_t* status) {
+  return detect_alt(3, B, U, n_sc, S, H, Y, rho_u, n0, es, qam_bits, K, xhat, mu, rho, llr, status);
+}
+
 /* src/precode.cpp:22-36 normalize: s = q/||q||, zero_input when ||q|| < 1e-300 */
 static uint8_t normalize(const cx* q, int B, double* qo, double* so, double* gain) {
   const double g = sqrt(norm2_sq(q, B));
@@ -553,12 +771,18 @@ static uint8_t normalize(const cx* q, int B, double* qo, double* so, double* gai
 }
 
 /* src/precode.cpp:38-71: A_d = H_d H_d^H + rho_d^-1 I, CG on t, q = H_d^H v
- * (mode 0), or v = inv(A_d) t (mode 1, precode.cpp:45-54). */
+ * (mode 0), or v = inv(A_d) t (mode 1, precode.cpp:45-54), v = Neumann
+ * series of A_d applied to t (mode 3, precode.cpp:84-93); mode 2 is
+ * precode_cgls (precode.cpp:73-82): min-norm CGLS (solvers.cpp:196-235)
+ * accumulating q = H_d^H inner directly. */
 static int precode_common(int mode, int B, int U, long n_sc, int S, const double* Hd,
                           const double* T, double rho_d, int K, double* q, double* s_out,
                           double* gain, uint8_t* status) {
-  const int bad = !(rho_d > 0.0) || (mode == 0 && K < 1);
+  const int bad = !(rho_d > 0.0) || (mode != 1 && K < 1);
   cx* h = xcalloc((size_t)U * B, sizeof(cx));
+  cx *nt = xcalloc((size_t)U * U, sizeof(cx)), *nterm = xcalloc((size_t)U * U, sizeof(cx));
+  cx *nnext = xcalloc((size_t)U * U, sizeof(cx)), *wv = xcalloc(B, sizeof(cx));
+  double* dinv = xcalloc(U, sizeof(double));
   cx* a = xcalloc((size_t)U * U, sizeof(cx));
   cx* inv = xcalloc((size_t)U * U, sizeof(cx));
   cx* m = xcalloc((size_t)U * U, sizeof(cx));
@@ -572,6 +796,7 @@ static int precode_common(int mode, int B, int U, long n_sc, int S, const double
     if (!bad) {
       gram(h, B, U, 1, 1.0 / rho_d, a);
       if (mode == 1) notpd = chol_inverse(a, U, inv, m, col);
+      if (mode == 3) notpd = neumann_inverse(a, U, K, inv, nt, nterm, nnext, dinv);
     }
     for (int s = 0; s < S; ++s) {
       const long inst = sc * S + s;
@@ -582,6 +807,36 @@ static int precode_common(int mode, int B, int U, long n_sc, int S, const double
         load_cx(T + 2 * inst * U, U, t);
         if (mode == 0) {
           if (cg_run(a, t, U, K, v, NULL, r, p, e)) st = 1;
+        } else if (mode == 2) {
+          const double rho_inv = 1.0 / rho_d;
+          for (int b = 0; b < B; ++b) qv[b] = 0.0;
+          memcpy(r, t, sizeof(cx) * U);
+          memcpy(p, t, sizeof(cx) * U);
+          double rn2 = norm2_sq(r, U);
+          const double rn0 = rn2;
+          for (int k = 1; k <= K && !st; ++k) {
+            if (rn2 <= 1e-28 * rn0) continue;
+            for (int b = 0; b < B; ++b) { /* w = H_d^H p */
+              cx acc = 0.0;
+              for (int u = 0; u < U; ++u) acc += conj(h[(long)u * B + b]) * p[u];
+              wv[b] = acc;
+            }
+            double curv = 0.0;
+            for (int u = 0; u < U; ++u) { /* e = H_d w + rho^-1 p */
+              cx acc = 0.0;
+              for (int b = 0; b < B; ++b) acc += h[(long)u * B + b] * wv[b];
+              e[u] = acc + rho_inv * p[u];
+              curv += creal(conj(p[u]) * e[u]);
+            }
+            if (curv < 1e-30) { st = 1; break; }
+            const double alpha = rn2 / curv;
+            for (int b = 0; b < B; ++b) qv[b] += alpha * wv[b];
+            for (int u = 0; u < U; ++u) r[u] -= alpha * e[u];
+            const double rn = norm2_sq(r, U);
+            const double beta = rn / rn2;
+            rn2 = rn;
+            for (int u = 0; u < U; ++u) p[u] = r[u] + beta * p[u];
+          }
         } else {
           hmatvec(inv, U, t, v);
         }
@@ -594,14 +849,16 @@ static int precode_common(int mode, int B, int U, long n_sc, int S, const double
         continue;
       }
       /* q = H_d^H v (linalg.cpp:116-126) */
-      for (int b = 0; b < B; ++b) qv[b] = 0.0;
-      for (int u = 0; u < U; ++u)
-        for (int b = 0; b < B; ++b) qv[b] += conj(h[(long)u * B + b]) * v[u];
+      if (mode != 2) {
+        for (int b = 0; b < B; ++b) qv[b] = 0.0;
+        for (int u = 0; u < U; ++u)
+          for (int b = 0; b < B; ++b) qv[b] += conj(h[(long)u * B + b]) * v[u];
+      }
       status[inst] = normalize(qv, B, qo, so, gain + inst);
     }
   }
   free(h); free(a); free(inv); free(m); free(col); free(t); free(v); free(r); free(p);
-  free(e); free(qv);
+  free(e); free(qv); free(nt); free(nterm); free(nnext); free(wv); free(dinv);
   return 0;
 }
 
@@ -613,6 +870,16 @@ int orc_precode_cg(int B, int U, long n_sc, int S, const double* Hd, const doubl
 int orc_precode_explicit(int B, int U, long n_sc, int S, const double* Hd, const double* T,
                          double rho_d, double* q, double* s, double* gain, uint8_t* status) {
   return precode_common(1, B, U, n_sc, S, Hd, T, rho_d, 1, q, s, gain, status);
+}
+
+int orc_precode_cgls(int B, int U, long n_sc, int S, const double* Hd, const double* T,
+                     double rho_d, int K, double* q, double* s, double* gain, uint8_t* status) {
+  return precode_common(2, B, U, n_sc, S, Hd, T, rho_d, K, q, s, gain, status);
+}
+
+int orc_precode_neumann(int B, int U, long n_sc, int S, const double* Hd, const double* T,
+                        double rho_d, int K, double* q, double* s, double* gain, uint8_t* status) {
+  return precode_common(3, B, U, n_sc, S, Hd, T, rho_d, K, q, s, gain, status);
 }
 
 /* --------------------------------------------------------------- coding */

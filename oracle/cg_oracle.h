@@ -27,6 +27,21 @@ int orc_precode_cg(int B, int U, long n_sc, int S, const double* Hd, const doubl
 int orc_precode_explicit(int B, int U, long n_sc, int S, const double* Hd, const double* T,
                          double rho_d, double* q, double* s, double* gain, uint8_t* status);
 
+/* the trade-off study's other solvers (detect.cpp:122-326, precode.cpp:45-93) */
+int orc_detect_cholesky(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                        double rho_u, double n0, double es, int qam_bits, double* xhat,
+                        double* mu, double* rho, double* llr, uint8_t* status);
+int orc_detect_cgls(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                    double rho_u, double n0, double es, int qam_bits, int K, double* xhat,
+                    double* mu, double* rho, double* llr, uint8_t* status);
+int orc_detect_neumann(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                       double rho_u, double n0, double es, int qam_bits, int K, double* xhat,
+                       double* mu, double* rho, double* llr, uint8_t* status);
+int orc_precode_cgls(int B, int U, long n_sc, int S, const double* Hd, const double* T,
+                     double rho_d, int K, double* q, double* s, double* gain, uint8_t* status);
+int orc_precode_neumann(int B, int U, long n_sc, int S, const double* Hd, const double* T,
+                        double rho_d, int K, double* q, double* s, double* gain, uint8_t* status);
+
 void orc_rng_u64(uint64_t key, const uint64_t* forks, int n_forks, long n, uint64_t* out);
 void orc_rng_cgaussian(uint64_t key, const uint64_t* forks, int n_forks, double variance,
                        long n, double* out);

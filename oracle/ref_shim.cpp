@@ -7,6 +7,8 @@
 //
 //   detect::detect_cg        (detect.hpp:58-61, detect.cpp:182-237)
 //   detect::detect_explicit  (detect.hpp:44-49, detect.cpp:94-126)
+//   detect::detect_cholesky / detect_cgls / detect_neumann (detect.cpp:122-326)
+//   precode::precode_cgls / precode_neumann (precode.cpp:73-93)
 //   precode::precode_cg      (precode.hpp:31-33, precode.cpp:56-71)
 //   precode::precode_explicit(precode.hpp:26-27, precode.cpp:45-54)
 //   detect::compute_llrs     (detect.cpp:68-86)
@@ -104,7 +106,8 @@ void store_soft(const detect::SoftOutput& o, std::size_t users, int bits, double
   }
 }
 
-// mode 0 = detect_cg, 1 = detect_explicit, 2 = detect_cholesky
+// mode 0 = detect_cg, 1 = detect_explicit, 2 = detect_cholesky, 3 = detect_cgls,
+// 4 = detect_neumann
 int detect_batch(int mode, int B, int U, long n_sc, int S, const double* H, const double* Y,
                  double rho_u, double n0, double es, int qam_bits, int K, int tracker,
                  double* xhat, double* mu, double* rho, double* llr, uint8_t* status,
@@ -133,8 +136,12 @@ int detect_batch(int mode, int B, int U, long n_sc, int S, const double* H, cons
           o = detect::detect_cg(h, y, rho_u, n0, es, c, static_cast<std::size_t>(K), trk);
         else if (mode == 1)
           o = detect::detect_explicit(h, y, rho_u, n0, es, c);
-        else
+        else if (mode == 2)
           o = detect::detect_cholesky(h, y, rho_u, n0, es, c);
+        else if (mode == 3)
+          o = detect::detect_cgls(h, y, rho_u, n0, es, c, static_cast<std::size_t>(K));
+        else
+          o = detect::detect_neumann(h, y, rho_u, n0, es, c, static_cast<std::size_t>(K));
         store_soft(o, users, qam_bits, xo, mo, ro, lo);
       } catch (const solvers::SolverBreakdown&) {
         st = 1;
@@ -166,9 +173,12 @@ int precode_batch(int mode, int B, int U, long n_sc, int S, const double* Hd, co
       double* so = s_out ? s_out + 2 * inst * bs : nullptr;
       uint8_t st = 0;
       try {
+        const auto k = static_cast<std::size_t>(K);
         const precode::PrecodeResult r =
-            mode == 0 ? precode::precode_cg(hd, t, rho_d, static_cast<std::size_t>(K))
-                      : precode::precode_explicit(hd, t, rho_d);
+            mode == 0   ? precode::precode_cg(hd, t, rho_d, k)
+            : mode == 1 ? precode::precode_explicit(hd, t, rho_d)
+            : mode == 2 ? precode::precode_cgls(hd, t, rho_d, k)
+                        : precode::precode_neumann(hd, t, rho_d, k);
         store_vector(r.precoded, qo);
         if (so) store_vector(r.transmit, so);
         gain[inst] = r.gain;
@@ -213,6 +223,32 @@ int ref_detect_cholesky(int B, int U, long n_sc, int S, const double* H, const d
                         double* mu, double* rho, double* llr, uint8_t* status, int threads) {
   return detect_batch(2, B, U, n_sc, S, H, Y, rho_u, n0, es, qam_bits, 1, 0, xhat, mu, rho,
                       llr, status, threads);
+}
+
+int ref_detect_cgls(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                    double rho_u, double n0, double es, int qam_bits, int K, double* xhat,
+                    double* mu, double* rho, double* llr, uint8_t* status, int threads) {
+  return detect_batch(3, B, U, n_sc, S, H, Y, rho_u, n0, es, qam_bits, K, 1, xhat, mu, rho,
+                      llr, status, threads);
+}
+
+int ref_detect_neumann(int B, int U, long n_sc, int S, const double* H, const double* Y,
+                       double rho_u, double n0, double es, int qam_bits, int K, double* xhat,
+                       double* mu, double* rho, double* llr, uint8_t* status, int threads) {
+  return detect_batch(4, B, U, n_sc, S, H, Y, rho_u, n0, es, qam_bits, K, 1, xhat, mu, rho,
+                      llr, status, threads);
+}
+
+int ref_precode_cgls(int B, int U, long n_sc, int S, const double* Hd, const double* T,
+                     double rho_d, int K, double* q, double* s, double* gain, uint8_t* status,
+                     int threads) {
+  return precode_batch(2, B, U, n_sc, S, Hd, T, rho_d, K, q, s, gain, status, threads);
+}
+
+int ref_precode_neumann(int B, int U, long n_sc, int S, const double* Hd, const double* T,
+                        double rho_d, int K, double* q, double* s, double* gain, uint8_t* status,
+                        int threads) {
+  return precode_batch(3, B, U, n_sc, S, Hd, T, rho_d, K, q, s, gain, status, threads);
 }
 
 int ref_precode_cg(int B, int U, long n_sc, int S, const double* Hd, const double* T,

@@ -16,6 +16,8 @@ CGM_OK, CGM_EINVAL, CGM_EBREAKDOWN, CGM_ECUDA, CGM_ENCCL, CGM_ENOMEM = range(6)
 CGM_TRACKER_EXACT, CGM_TRACKER_APPROX = 0, 1
 CGM_DEVICE_POINTERS = 0x1
 CGM_HD_UPLINK_LAYOUT = 0x2
+# sim::Method order (sim.hpp:34)
+METHODS = {"chol": 0, "cholesky": 0, "explicit": 0, "cg": 1, "cgls": 2, "neumann": 3}
 
 _vp = C.c_void_p
 _int = C.c_int
@@ -39,6 +41,10 @@ SIGNATURES = {
                              _int, _vp, _vp, _vp, _vp, _vp, C.c_uint]),
     "cgm_precode_cg": (_int, [_vp, _int, _int, _long, _int, _vp, _vp, _dbl, _int, _vp, _vp, _vp,
                               _vp, C.c_uint]),
+    "cgm_detect": (_int, [_vp, _int, _int, _int, _long, _int, _vp, _vp, _dbl, _dbl, _dbl, _int,
+                          _int, _int, _vp, _vp, _vp, _vp, _vp, C.c_uint]),
+    "cgm_precode": (_int, [_vp, _int, _int, _int, _long, _int, _vp, _vp, _dbl, _int, _vp, _vp,
+                           _vp, _vp, C.c_uint]),
     "cgm_detect_precode_cg": (_int, [_vp, _int, _int, _long, _int, _vp, _vp, _dbl, _dbl, _dbl,
                                      _int, _int, _int, _vp, _vp, _vp, _vp, _vp, _int, _vp, _dbl,
                                      _int, _vp, _vp, _vp, _vp, C.c_uint]),

@@ -154,8 +154,17 @@ class Context:
         return out
 
     # ------------------------------------------------------------- detect
+    def detect(self, method, H, Y, rho_u, n0, es, qam_bits, iters=1, tracker="approx", out=None,
+               want=("xhat", "mu", "rho", "llr", "status")):
+        """Batched detect_<method> (cgm_detect): method "cholesky" (alias
+        "chol"), "cg", "cgls" or "neumann" (iters = series terms)."""
+        if method not in _lib.METHODS:
+            raise ValueError(f"unknown method {method!r}")
+        return self.detect_cg(H, Y, rho_u, n0, es, qam_bits, iters, tracker, out, want,
+                              method=method)
+
     def detect_cg(self, H, Y, rho_u, n0, es, qam_bits, iters, tracker="exact", out=None,
-                  want=("xhat", "mu", "rho", "llr", "status")):
+                  want=("xhat", "mu", "rho", "llr", "status"), method="cg"):
         """Batched detect_cg.  Returns dict with the requested outputs."""
         device = _is_torch(H)
         n_sc, B, U, S = detect_dims(H, Y)
@@ -173,17 +182,28 @@ class Context:
         if device:
             flags |= _lib.CGM_DEVICE_POINTERS
             self._bind_torch_stream()
-        rc = self.lib.cgm_detect_cg(self.h, B, U, n_sc, S, _ptr(H), _ptr(Y), float(rho_u),
-                                    float(n0), float(es), int(qam_bits), int(iters),
-                                    TRACKERS[tracker], _ptr(out.get("xhat")), _ptr(out.get("mu")),
-                                    _ptr(out.get("rho")), _ptr(out.get("llr")),
-                                    _ptr(out.get("status")), flags)
+        args = (B, U, n_sc, S, _ptr(H), _ptr(Y), float(rho_u), float(n0), float(es),
+                int(qam_bits), int(iters), TRACKERS[tracker], _ptr(out.get("xhat")),
+                _ptr(out.get("mu")), _ptr(out.get("rho")), _ptr(out.get("llr")),
+                _ptr(out.get("status")), flags)
+        if method == "cg":
+            rc = self.lib.cgm_detect_cg(self.h, *args)
+        else:
+            rc = self.lib.cgm_detect(self.h, _lib.METHODS[method], *args)
         self._check(rc)
         return out
 
     # ------------------------------------------------------------ precode
+    def precode(self, method, Hd, T, rho_d, iters=1, uplink_layout=False, out=None,
+                want=("q", "s", "gain", "status")):
+        """Batched precode_<method> (cgm_precode): "explicit" (Cholesky,
+        alias "cholesky"), "cg", "cgls" or "neumann" (iters = series terms)."""
+        if method not in _lib.METHODS:
+            raise ValueError(f"unknown method {method!r}")
+        return self.precode_cg(Hd, T, rho_d, iters, uplink_layout, out, want, method=method)
+
     def precode_cg(self, Hd, T, rho_d, iters, uplink_layout=False, out=None,
-                   want=("q", "s", "gain", "status")):
+                   want=("q", "s", "gain", "status"), method="cg"):
         """Batched precode_cg.  Hd (n_sc, U, B); with uplink_layout=True the
         matrix is H_u (n_sc, B, U) and H_d = H_u^H (TDD reciprocity)."""
         device = _is_torch(Hd)
@@ -199,9 +219,12 @@ class Context:
         if device:
             flags |= _lib.CGM_DEVICE_POINTERS
             self._bind_torch_stream()
-        rc = self.lib.cgm_precode_cg(self.h, B, U, n_sc, S, _ptr(Hd), _ptr(T), float(rho_d),
-                                     int(iters), _ptr(out.get("q")), _ptr(out.get("s")),
-                                     _ptr(out.get("gain")), _ptr(out.get("status")), flags)
+        args = (B, U, n_sc, S, _ptr(Hd), _ptr(T), float(rho_d), int(iters), _ptr(out.get("q")),
+                _ptr(out.get("s")), _ptr(out.get("gain")), _ptr(out.get("status")), flags)
+        if method == "cg":
+            rc = self.lib.cgm_precode_cg(self.h, *args)
+        else:
+            rc = self.lib.cgm_precode(self.h, _lib.METHODS[method], *args)
         self._check(rc)
         return out
 

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/cgmimo_b200.h"
+#include "cgm_alt.cuh"
 #include "cgm_solve32.cuh"
 #include "cgm_tc.cuh"
 
@@ -338,8 +339,39 @@ int dispatch_exact(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t 
                : plan_and_launch<UP, NT, false>(ctx, p, st);
 }
 
+// Cholesky / CGLS / Neumann detection and precoding (cgm_alt.cuh): one CTA
+// per subcarrier, persistent over the chunk.
+int launch_alt(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
+  cgm::alt::AltSmem L;
+  L.plan(p.B, p.U, p.St > 0 ? p.St : p.S, p.method);
+  const size_t smem = static_cast<size_t>(L.total) * sizeof(float2);
+  if (smem > static_cast<size_t>(ctx->max_smem))
+    return fail(ctx, CGM_EINVAL, "B = %d, U = %d: %zu bytes of shared memory per subcarrier exceed %d",
+                p.B, p.U, smem, ctx->max_smem);
+  auto k = cgm::alt::alt_kernel;
+  CGM_CUDA(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int occ = 0;
+  CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, cgm::alt::NT, smem));
+  const long grid = std::max<long>(1, std::min<long>(p.n_sc, static_cast<long>(std::max(occ, 1)) * ctx->sms));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->profiling) {
+    e0 = prof_event(ctx);
+    e1 = prof_event(ctx);
+    cudaEventRecord(e0, st);
+  }
+  k<<<static_cast<unsigned>(grid), cgm::alt::NT, smem, st>>>(p);
+  CGM_CUDA(ctx, cudaGetLastError());
+  if (ctx->profiling) {
+    cudaEventRecord(e1, st);
+    ctx->ev_log.push_back({2, {e0, e1}});
+  }
+  ++ctx->launches;
+  return CGM_OK;
+}
+
 int launch(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
   if (p.n_sc <= 0) return CGM_OK;
+  if (p.method != cgm::alt::kCg) return launch_alt(ctx, p, st);
   const int UP = up_of(p.U);
   const uintptr_t a = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
   p.use_tma = (!p.hd_layout && p.U == UP && (p.B % 2) == 0 && (p.S % 2) == 0 && (a & 15u) == 0)
@@ -363,6 +395,7 @@ int launch(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
 // ------------------------------------------------------------ validation
 struct Job {
   int B = 0, U = 0, S = 0, St = 0, K = 0, Kt = 0, bits = 0, tracker = 0;
+  int method = cgm::alt::kCg;
   long n_sc = 0;
   double rho_u = 1, n0 = 1, es = 1, rho_d = 1;
   bool hd_layout = false;
@@ -384,8 +417,9 @@ int validate(cgm_ctx* ctx, const Job& j) {
     // detect.cpp:186-188
     if (!(j.rho_u > 0.0 && j.n0 > 0.0 && j.es > 0.0))
       return fail(ctx, CGM_EINVAL, "detect_cg: bad parameters (rho_u, N0, Es must be > 0)");
-    if (j.K < 1) return fail(ctx, CGM_EINVAL, "detect_cg: need at least one iteration");
-    if (j.K > cgm::kMaxK) return fail(ctx, CGM_EINVAL, "K = %d > %d", j.K, cgm::kMaxK);
+    if (j.K < 1) return fail(ctx, CGM_EINVAL, "detect: need at least one iteration / series term");
+    if (j.K > (j.method == cgm::alt::kCg ? cgm::kMaxK : 256))
+      return fail(ctx, CGM_EINVAL, "K = %d is above the supported maximum", j.K);
     if (j.bits != 2 && j.bits != 4 && j.bits != 6)
       return fail(ctx, CGM_EINVAL, "qam_bits must be 2, 4 or 6");
     if (j.tracker != CGM_TRACKER_EXACT && j.tracker != CGM_TRACKER_APPROX)
@@ -395,8 +429,9 @@ int validate(cgm_ctx* ctx, const Job& j) {
   if (j.St > 0) {
     // precode.cpp:59-60, solvers.cpp:39-40
     if (!(j.rho_d > 0.0)) return fail(ctx, CGM_EINVAL, "precode_cg: rho_d must be positive");
-    if (j.Kt < 1) return fail(ctx, CGM_EINVAL, "cg_solve: need at least one iteration");
-    if (j.Kt > cgm::kMaxK) return fail(ctx, CGM_EINVAL, "K = %d > %d", j.Kt, cgm::kMaxK);
+    if (j.Kt < 1) return fail(ctx, CGM_EINVAL, "precode: need at least one iteration / series term");
+    if (j.Kt > (j.method == cgm::alt::kCg ? cgm::kMaxK : 256))
+      return fail(ctx, CGM_EINVAL, "K = %d is above the supported maximum", j.Kt);
     if (!j.H || !j.T) return fail(ctx, CGM_EINVAL, "H and T are required");
   }
   return CGM_OK;
@@ -431,6 +466,7 @@ cgm::KernelParams params_of(const Job& j, long n_sc) {
   p.n0 = static_cast<float>(j.n0);
   if (const char* dbg = std::getenv("CGMIMO_DEBUG_WS")) p.debug = std::atoi(dbg);
   p.es = static_cast<float>(j.es);
+  p.method = j.method;
   return p;
 }
 
@@ -710,6 +746,38 @@ int cgm_precode_cg(cgm_ctx* ctx, int B, int U, long n_sc, int S, const float* Hd
   j.hd_layout = !(flags & CGM_HD_UPLINK_LAYOUT);
   j.q = q; j.s = s; j.gain = gain; j.pstatus = status;
   if (S < 1) return fail(ctx, CGM_EINVAL, "precode_cg: S must be >= 1");
+  return run_job(ctx, j, flags);
+}
+
+int cgm_detect(cgm_ctx* ctx, int method, int B, int U, long n_sc, int S, const float* H,
+               const float* Y, double rho_u, double n0, double es, int qam_bits, int iters,
+               int tracker, float* xhat, float* mu, float* rho, float* llr, uint8_t* status,
+               unsigned flags) {
+  if (method < CGM_METHOD_CHOLESKY || method > CGM_METHOD_NEUMANN)
+    return fail(ctx, CGM_EINVAL, "unknown method %d", method);
+  if (method == CGM_METHOD_CHOLESKY) iters = 1;  // no iteration count (detect.cpp:122-125)
+  if (method != CGM_METHOD_CG) tracker = CGM_TRACKER_APPROX;
+  Job j;
+  j.method = method;
+  j.B = B; j.U = U; j.n_sc = n_sc; j.S = S; j.H = H; j.Y = Y;
+  j.rho_u = rho_u; j.n0 = n0; j.es = es; j.bits = qam_bits; j.K = iters; j.tracker = tracker;
+  j.xhat = xhat; j.mu = mu; j.rho = rho; j.llr = llr; j.status = status;
+  if (S < 1) return fail(ctx, CGM_EINVAL, "detect: S must be >= 1");
+  return run_job(ctx, j, flags);
+}
+
+int cgm_precode(cgm_ctx* ctx, int method, int B, int U, long n_sc, int S, const float* Hd,
+                const float* T, double rho_d, int iters, float* q, float* s, float* gain,
+                uint8_t* status, unsigned flags) {
+  if (method < CGM_METHOD_CHOLESKY || method > CGM_METHOD_NEUMANN)
+    return fail(ctx, CGM_EINVAL, "unknown method %d", method);
+  if (method == CGM_METHOD_CHOLESKY) iters = 1;  // precode_explicit (precode.cpp:45-54)
+  Job j;
+  j.method = method;
+  j.B = B; j.U = U; j.n_sc = n_sc; j.St = S; j.H = Hd; j.T = T; j.rho_d = rho_d; j.Kt = iters;
+  j.hd_layout = !(flags & CGM_HD_UPLINK_LAYOUT);
+  j.q = q; j.s = s; j.gain = gain; j.pstatus = status;
+  if (S < 1) return fail(ctx, CGM_EINVAL, "precode: S must be >= 1");
   return run_job(ctx, j, flags);
 }
 

@@ -60,6 +60,7 @@ struct KernelParams {
   long sc_base;   // split path: first subcarrier of this chunk
   int k1_pair, k1_spl, k1_wpp;  // channel kernel: subcarriers per CTA, k-parts, warps per part
   unsigned long long* trace;    // microbenchmarks only: per-CTA event clocks (null in production)
+  int method;                   // sim::Method order: 0 Cholesky, 1 CG, 2 CGLS, 3 Neumann (cgm_alt.cuh)
 };
 
 // Per-axis Gray amplitude subsets (constellation.cpp:75-84), [qam][p][k],

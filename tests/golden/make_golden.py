@@ -92,12 +92,35 @@ def coding_fixtures(ref):
     return d
 
 
+def alt_fixtures(ref):
+    """The trade-off study's other solvers (detect.cpp:122-326,
+    precode.cpp:45-93) on one small seeded uplink and downlink batch."""
+    rng = np.random.default_rng(20261020)
+    n_sc, B, U, S = 6, 24, 6, 2
+    H = cn(rng, (n_sc, B, U)).astype(np.complex64)
+    Y = cn(rng, (n_sc, B, S), 3.0).astype(np.complex64)
+    Hd = cn(rng, (n_sc, U, B)).astype(np.complex64)
+    T = cn(rng, (n_sc, S, U)).astype(np.complex64)
+    d = dict(H=H, Y=Y, Hd=Hd, T=T)
+    for m, K in (("cholesky", 1), ("cgls", 3), ("neumann", 1), ("neumann", 3)):
+        r = ref.detect(H, Y, 8.0, 0.125, 1.0, 4, K, method=m)
+        for k, v in r.items():
+            d[f"det_{m}{K}_{k}"] = v
+    for m, K in (("explicit", 1), ("cgls", 2), ("neumann", 2)):
+        r = ref.precode(Hd, T, 8.0, K, method=m)
+        for k, v in r.items():
+            d[f"pre_{m}{K}_{k}"] = v
+    return d
+
+
 def main():
     ref = oracle.Oracle("ref")
-    if "--only-coding" in sys.argv:
-        np.savez_compressed(os.path.join(HERE, "coding.npz"), **coding_fixtures(ref))
-        print("wrote coding.npz")
-        return
+    only = {"--only-coding": ("coding", coding_fixtures), "--only-alt": ("alt", alt_fixtures)}
+    for flag, (name, fn) in only.items():
+        if flag in sys.argv:
+            np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **fn(ref))
+            print(f"wrote {name}.npz")
+            return
     rng = np.random.default_rng(20260419)
     out = {}
     for name, B, U, S, K, trk, bits, snr, n_sc in DETECT_CASES:
@@ -153,6 +176,7 @@ def main():
                       gauss=ref.rng_cgaussian(99, [3, 11], 0.5, 8),
                       rayleigh=ref.rayleigh(5, [2, 3], 8, 4))
     out["coding"] = coding_fixtures(ref)
+    out["alt"] = alt_fixtures(ref)
     for name, d in out.items():
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
     print(f"wrote {len(out)} fixtures to {HERE}")

@@ -223,3 +223,63 @@ def test_port_coding_rejects_reference_bad_lengths(oracle_port):
         oracle_port.viterbi_decode(np.zeros(7))  # not whole periods
     with pytest.raises(ValueError):
         oracle_port.viterbi_decode(np.zeros(6))  # 5 steps < tail 6
+
+
+# ------------------------------------- trade-off study solvers (section 8(f) row 4)
+ALT_DETECT = (("cholesky", 1), ("cgls", 3), ("neumann", 1), ("neumann", 3))
+ALT_PRECODE = (("explicit", 1), ("cgls", 2), ("neumann", 2))
+
+
+def test_port_alt_solvers_match_reference_fixture(oracle_port):
+    d = load("alt")
+    for m, K in ALT_DETECT:
+        got = oracle_port.detect(d["H"], d["Y"], 8.0, 0.125, 1.0, 4, K, method=m)
+        for k, v in got.items():
+            assert np.array_equal(v, d[f"det_{m}{K}_{k}"]), (m, K, k)
+    for m, K in ALT_PRECODE:
+        got = oracle_port.precode(d["Hd"], d["T"], 8.0, K, method=m)
+        for k, v in got.items():
+            assert np.array_equal(v, d[f"pre_{m}{K}_{k}"]), (m, K, k)
+
+
+@pytest.mark.parametrize("B,U,S", [(32, 8, 2), (12, 12, 1), (20, 7, 3)])
+def test_port_alt_solvers_bitwise_equal_reference(oracle_ref, oracle_port, B, U, S):
+    rng = np.random.default_rng(B + U)
+    n_sc = 4
+    H = cplx_randn(rng, (n_sc, B, U)).astype(np.complex64)
+    Y = (cplx_randn(rng, (n_sc, B, S)) * 2).astype(np.complex64)
+    for m, K in ALT_DETECT + (("cgls", U + 2), ("neumann", 5)):
+        a = oracle_ref.detect(H, Y, 5.0, 0.2, 1.0, 6, K, method=m)
+        b = oracle_port.detect(H, Y, 5.0, 0.2, 1.0, 6, K, method=m)
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (m, K, k)
+    Hd = np.ascontiguousarray(np.conj(np.transpose(H, (0, 2, 1))))
+    T = cplx_randn(rng, (n_sc, S, U)).astype(np.complex64)
+    for m, K in ALT_PRECODE + (("cgls", U + 2), ("neumann", 4)):
+        a = oracle_ref.precode(Hd, T, 5.0, K, method=m)
+        b = oracle_port.precode(Hd, T, 5.0, K, method=m)
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (m, K, k)
+
+
+def test_port_alt_solver_identities(oracle_port):
+    """Cholesky detection == explicit MMSE (detect.cpp:88-120 vs :122-181);
+    min-norm CGLS precoding == CG precoding (same Krylov iterates,
+    precode.cpp:56-82); Neumann with 1 term is the diagonal inverse."""
+    rng = np.random.default_rng(3)
+    H = cplx_randn(rng, (3, 32, 8))
+    Y = cplx_randn(rng, (3, 32, 2)) * 2
+    a = oracle_port.detect(H, Y, 5.0, 0.2, 1.0, 4, method="cholesky")
+    b = oracle_port.detect(H, Y, 5.0, 0.2, 1.0, 4, method="explicit")
+    for k in ("xhat", "mu", "rho"):
+        np.testing.assert_allclose(a[k], b[k], rtol=1e-9, atol=1e-12)
+    Hd = np.conj(np.transpose(H, (0, 2, 1)))
+    T = cplx_randn(rng, (3, 2, 8))
+    c = oracle_port.precode(Hd, T, 5.0, 3, method="cgls")
+    g = oracle_port.precode(Hd, T, 5.0, 3, method="cg")
+    np.testing.assert_allclose(c["q"], g["q"], rtol=1e-9, atol=1e-12)
+    n1 = oracle_port.detect(H, Y, 5.0, 0.2, 1.0, 4, 1, method="neumann")
+    G = np.einsum("nbi,nbj->nij", H.conj(), H)
+    d = np.real(np.diagonal(G, axis1=1, axis2=2)) + 0.2
+    mf = np.einsum("nbi,nbs->nsi", H.conj(), Y)
+    np.testing.assert_allclose(n1["xhat"], mf / d[:, None, :], rtol=1e-12)
