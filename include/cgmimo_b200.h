@@ -179,6 +179,14 @@ int cgm_uplink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K,
 int cgm_downlink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K,
                         double snr_db, long n_trials, const uint64_t* trial_keys,
                         uint32_t* user_errors, uint8_t* breakdown);
+/* Either direction with any sim::Method (the trade-off study, sim.cpp:
+ * 120-145): direction 1 = uplink (cgm_detect with `method`, `iters`,
+ * `tracker`), 2 = downlink (cgm_precode with `method`, `iters`).  A solver
+ * input that is not positive definite (status bit2) fails the call with
+ * CGM_EINVAL, as the reference's exception leaves run_point. */
+int cgm_sweep_trials(cgm_ctx* ctx, int direction, int method, int B, int U, int n_sc,
+                     int qam_bits, int iters, int tracker, double snr_db, long n_trials,
+                     const uint64_t* trial_keys, uint32_t* user_errors, uint8_t* breakdown);
 uint64_t cgm_sweep_trial_key(uint64_t seed, int direction, long point, long trial);
 /* Soft max-log Viterbi decoding of n_cw rate-5/6 codewords (coding.cpp:90-147):
  * llrs [n_cw][coded_len] in coded-bit order (positive favours 1), coded_len a

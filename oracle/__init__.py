@@ -70,6 +70,8 @@ class Oracle:
         self._threaded = kind == "ref"
         for nm in ("conv_encode", "viterbi_decode"):
             self._fn(nm).restype = C.c_long
+        if kind == "ref":
+            self.lib.ref_sweep.restype = C.c_long
 
     def _fn(self, name):
         return getattr(self.lib, self.pfx + name)
@@ -221,6 +223,48 @@ class Oracle:
         if rc != 0:
             raise RuntimeError("run_downlink_sweep raised")
         return dict(zip(("frames", "block_errors", "breakdowns", "trials_run"), map(int, out)))
+
+    def sweep(self, direction, method, B, U, qam_bits, iters, tracker, snr_start, snr_stop,
+              snr_step, trials, n_sc, seed, max_block_errors=0, max_breakdown_fraction=1.0,
+              threads=0) -> list:
+        """sim::run_uplink_sweep / run_downlink_sweep (sim.cpp:365-405) with
+        any sim::Method: one dict per SNR point (SnrPointResult fields)."""
+        self._need_ref("sweep")
+        out = np.zeros((256, 9))
+        m = {"chol": 0, "cholesky": 0, "cg": 1, "cgls": 2, "neumann": 3}[method]
+        n = self.lib.ref_sweep(
+            C.c_int({"uplink": 1, "downlink": 2}[direction]), C.c_int(m), C.c_int(B), C.c_int(U),
+            C.c_int(qam_bits), C.c_int(iters), C.c_int(0 if tracker == "exact" else 1),
+            C.c_double(snr_start), C.c_double(snr_stop), C.c_double(snr_step), C.c_long(trials),
+            C.c_long(n_sc), C.c_uint64(seed), C.c_long(max_block_errors),
+            C.c_double(max_breakdown_fraction), C.c_int(threads), out.ctypes.data_as(C.c_void_p),
+            C.c_long(256))
+        if n < 0:
+            raise RuntimeError({-1: "ConfigError", -2: "BreakdownBudgetExceeded"}.get(n, "error"))
+        keys = ("snr_db", "frames", "block_errors", "bler", "bler_lo", "bler_hi",
+                "real_mults_mean", "breakdowns", "trials_run")
+        return [dict(zip(keys, row)) for row in out[:n]]
+
+    def tradeoff_row(self, method, B, U, iters, snr, frames, errors, target):
+        """sim::tradeoff_table for one sweep -> (real_mults, snr_at_target or None)."""
+        self._need_ref("tradeoff_row")
+        m = {"chol": 0, "cholesky": 0, "cg": 1, "cgls": 2, "neumann": 3}[method]
+        snr = np.ascontiguousarray(snr, dtype=np.float64)
+        fr = np.ascontiguousarray(frames, dtype=np.uint64)
+        er = np.ascontiguousarray(errors, dtype=np.uint64)
+        rm = C.c_uint64(0)
+        st = C.c_double(0.0)
+        ok = self.lib.ref_tradeoff_row(C.c_int(m), C.c_int(B), C.c_int(U), C.c_int(iters),
+                                       snr.ctypes.data_as(C.c_void_p), fr.ctypes.data_as(C.c_void_p),
+                                       er.ctypes.data_as(C.c_void_p), C.c_long(len(snr)),
+                                       C.c_double(target), C.byref(rm), C.byref(st))
+        return int(rm.value), (st.value if ok else None)
+
+    def wilson(self, errors, total):
+        self._need_ref("wilson")
+        lo, hi = C.c_double(0), C.c_double(0)
+        self.lib.ref_wilson(C.c_uint64(errors), C.c_uint64(total), C.byref(lo), C.byref(hi))
+        return lo.value, hi.value
 
     def rng_u64(self, key: int, forks, n: int) -> np.ndarray:
         fk = np.ascontiguousarray(forks, dtype=np.uint64)

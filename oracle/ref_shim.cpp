@@ -469,4 +469,84 @@ int ref_downlink_sweep_point(int B, int U, int qam_bits, int K, double snr_db, l
   return sweep_point(true, B, U, qam_bits, K, 1, snr_db, trials, n_sc, seed, threads, out);
 }
 
+// A whole sweep (sim::run_uplink_sweep / run_downlink_sweep, sim.cpp:365-405)
+// with any method and SNR grid.  out[p * 9 + ...] = {snr_db, frames,
+// block_errors, bler, bler_lo, bler_hi, real_mults_mean, breakdowns,
+// trials_run}; returns the number of points (<= max_points), -1 on
+// ConfigError, -2 on BreakdownBudgetExceeded, -3 on any other exception.
+long ref_sweep(int direction, int method, int B, int U, int qam_bits, int iters, int tracker,
+               double snr_start, double snr_stop, double snr_step, long trials, long n_sc,
+               uint64_t seed, long max_block_errors, double max_breakdown_fraction, int threads,
+               double* out, long max_points) {
+  try {
+    sim::SweepConfig cfg;
+    cfg.bs_antennas = static_cast<std::size_t>(B);
+    cfg.users = static_cast<std::size_t>(U);
+    cfg.modulation = modulation_of(qam_bits);
+    cfg.method = static_cast<sim::Method>(method);
+    cfg.iterations = static_cast<std::size_t>(iters);
+    cfg.tracker = tracker == 0 ? detect::SinrTracker::kExact : detect::SinrTracker::kApprox;
+    cfg.snr_start_db = snr_start;
+    cfg.snr_stop_db = snr_stop;
+    cfg.snr_step_db = snr_step;
+    cfg.trials = static_cast<std::size_t>(trials);
+    cfg.subcarriers = static_cast<std::size_t>(n_sc);
+    cfg.seed = seed;
+    cfg.threads = static_cast<std::size_t>(threads);
+    cfg.max_block_errors = static_cast<std::size_t>(max_block_errors);
+    cfg.max_breakdown_fraction = max_breakdown_fraction;
+    const auto r = direction == 2 ? sim::run_downlink_sweep(cfg) : sim::run_uplink_sweep(cfg);
+    long n = 0;
+    for (const auto& p : r.points) {
+      if (n >= max_points) break;
+      double* o = out + 9 * n++;
+      o[0] = p.snr_db; o[1] = static_cast<double>(p.frames);
+      o[2] = static_cast<double>(p.block_errors); o[3] = p.bler; o[4] = p.bler_lo;
+      o[5] = p.bler_hi; o[6] = p.real_mults_mean; o[7] = static_cast<double>(p.breakdowns);
+      o[8] = static_cast<double>(p.trials_run);
+    }
+    return n;
+  } catch (const sim::ConfigError&) {
+    return -1;
+  } catch (const sim::BreakdownBudgetExceeded&) {
+    return -2;
+  } catch (const std::exception&) {
+    return -3;
+  }
+}
+
+// sim::tradeoff_table (sim.cpp:475-497) for ONE sweep given by its points
+// (snr, frames, block_errors per point; bler recomputed as the reference
+// does): writes real_mults and snr_db_at_target; returns 1 when the target
+// is bracketed, 0 when not (nullopt).
+int ref_tradeoff_row(int method, int B, int U, int iters, const double* snr,
+                     const uint64_t* frames, const uint64_t* errors, long n, double target,
+                     uint64_t* real_mults, double* snr_at_target) {
+  sim::SweepResult sw;
+  sw.config.bs_antennas = static_cast<std::size_t>(B);
+  sw.config.users = static_cast<std::size_t>(U);
+  sw.config.method = static_cast<sim::Method>(method);
+  sw.config.iterations = static_cast<std::size_t>(iters);
+  for (long i = 0; i < n; ++i) {
+    sim::SnrPointResult p;
+    p.snr_db = snr[i];
+    p.frames = frames[i];
+    p.block_errors = errors[i];
+    p.bler = p.frames > 0 ? static_cast<double>(p.block_errors) / static_cast<double>(p.frames) : 0.0;
+    sw.points.push_back(p);
+  }
+  const auto rows = sim::tradeoff_table({sw}, target);
+  *real_mults = rows.at(0).real_mults;
+  if (!rows[0].snr_db_at_target) return 0;
+  *snr_at_target = *rows[0].snr_db_at_target;
+  return 1;
+}
+
+// sim::wilson_interval (sim.cpp:78-92)
+void ref_wilson(uint64_t errors, uint64_t total, double* lo, double* hi) {
+  const auto w = sim::wilson_interval(errors, total);
+  *lo = w.first;
+  *hi = w.second;
+}
+
 }  // extern "C"

@@ -57,6 +57,8 @@ SIGNATURES = {
                                               _dbl, _vp, _vp, _vp, _vp]),
     "cgm_uplink_trials": (_int, [_vp, _int, _int, _int, _int, _int, _int, _dbl, _long, _vp, _vp,
                                  _vp]),
+    "cgm_sweep_trials": (_int, [_vp, _int, _int, _int, _int, _int, _int, _int, _int, _dbl, _long,
+                                _vp, _vp, _vp]),
     "cgm_downlink_trials": (_int, [_vp, _int, _int, _int, _int, _int, _dbl, _long, _vp, _vp,
                                    _vp]),
     "cgm_sweep_trial_key": (_u64, [_u64, _int, _long, _long]),

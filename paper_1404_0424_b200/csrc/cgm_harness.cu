@@ -450,8 +450,8 @@ extern "C" {
 namespace {
 
 // run_uplink_trial / run_downlink_trial (sim.cpp:147-275) for a batch of trials
-int run_trials(cgm_ctx* ctx, bool downlink, int B, int U, int n_sc, int qam_bits, int K,
-               int tracker, double snr_db, long n_trials, const uint64_t* trial_keys,
+int run_trials(cgm_ctx* ctx, bool downlink, int method, int B, int U, int n_sc, int qam_bits,
+               int K, int tracker, double snr_db, long n_trials, const uint64_t* trial_keys,
                uint32_t* user_errors, uint8_t* breakdown) {
   const char* who = downlink ? "cgm_downlink_trials" : "cgm_uplink_trials";
   void* stv = nullptr;
@@ -561,9 +561,9 @@ int run_trials(cgm_ctx* ctx, bool downlink, int B, int U, int n_sc, int qam_bits
     mark("channel+y");
     // ---- ONE batched detection over every subcarrier of every trial
     if (e == cudaSuccess)
-      rc = cgm_detect_cg(ctx, B, U, n_tot, S, static_cast<float*>(dH), static_cast<float*>(dY),
-                         1.0 / n0, n0, 1.0, qam_bits, K, tracker, nullptr, nullptr, nullptr,
-                         static_cast<float*>(dLlr), static_cast<uint8_t*>(dSt), CGM_DEVICE_POINTERS);
+      rc = cgm_detect(ctx, method, B, U, n_tot, S, static_cast<float*>(dH), static_cast<float*>(dY),
+                      1.0 / n0, n0, 1.0, qam_bits, K, tracker, nullptr, nullptr, nullptr,
+                      static_cast<float*>(dLlr), static_cast<uint8_t*>(dSt), CGM_DEVICE_POINTERS);
   } else {
     gen_transmit_trials<<<grid(n_tot * S * U), 256, 0, st>>>(
         static_cast<float2*>(dT), static_cast<uint8_t*>(dLab), bps, n_tot * S * U);
@@ -574,9 +574,9 @@ int run_trials(cgm_ctx* ctx, bool downlink, int B, int U, int n_sc, int qam_bits
     // trial; H_d = H^H from the uplink-layout draws (sim.cpp:223); the
     // transmit vectors s land in dY (same size)
     if (e == cudaSuccess)
-      rc = cgm_precode_cg(ctx, B, U, n_tot, S, static_cast<float*>(dH), static_cast<float*>(dT),
-                          1.0 / n0, K, nullptr, static_cast<float*>(dY), nullptr,
-                          static_cast<uint8_t*>(dSt), CGM_DEVICE_POINTERS | CGM_HD_UPLINK_LAYOUT);
+      rc = cgm_precode(ctx, method, B, U, n_tot, S, static_cast<float*>(dH), static_cast<float*>(dT),
+                       1.0 / n0, K, nullptr, static_cast<float*>(dY), nullptr,
+                       static_cast<uint8_t*>(dSt), CGM_DEVICE_POINTERS | CGM_HD_UPLINK_LAYOUT);
     if (rc == CGM_OK) {
       downlink_receive<<<static_cast<unsigned>(std::min<long>(n_tot * S, 32L * sms)), 64,
                          B * sizeof(double2), st>>>(
@@ -608,6 +608,9 @@ int run_trials(cgm_ctx* ctx, bool downlink, int B, int U, int n_sc, int qam_bits
   mark("d2h+free");
   if (rc != CGM_OK) return rc;
   if (e != cudaSuccess) return cgm_internal_fail(ctx, CGM_ECUDA, cudaGetErrorString(e));
+  for (uint8_t v : stat)
+    if (v & 4u)  // NotPositiveDefinite / domain_error propagate out of run_point in the reference
+      return cgm_internal_fail(ctx, CGM_EINVAL, (std::string(who) + ": solver input not positive definite").c_str());
   for (long t = 0; t < n_trials; ++t) {
     bool broke = false;
     for (long i = t * n_sc * S; i < (t + 1) * n_sc * S; ++i) broke |= (stat[i] & 1u) != 0;
@@ -626,15 +629,27 @@ extern "C" {
 int cgm_uplink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K, int tracker,
                       double snr_db, long n_trials, const uint64_t* trial_keys,
                       uint32_t* user_errors, uint8_t* breakdown) {
-  return run_trials(ctx, false, B, U, n_sc, qam_bits, K, tracker, snr_db, n_trials, trial_keys,
+  return run_trials(ctx, false, CGM_METHOD_CG, B, U, n_sc, qam_bits, K, tracker, snr_db, n_trials,
+                    trial_keys, user_errors, breakdown);
+}
+
+int cgm_sweep_trials(cgm_ctx* ctx, int direction, int method, int B, int U, int n_sc,
+                     int qam_bits, int iters, int tracker, double snr_db, long n_trials,
+                     const uint64_t* trial_keys, uint32_t* user_errors, uint8_t* breakdown) {
+  if (direction != 1 && direction != 2)
+    return cgm_internal_fail(ctx, CGM_EINVAL, "cgm_sweep_trials: direction must be 1 (uplink) or 2 (downlink)");
+  if (method < CGM_METHOD_CHOLESKY || method > CGM_METHOD_NEUMANN)
+    return cgm_internal_fail(ctx, CGM_EINVAL, "cgm_sweep_trials: unknown method");
+  return run_trials(ctx, direction == 2, method, B, U, n_sc, qam_bits, iters,
+                    direction == 2 ? CGM_TRACKER_APPROX : tracker, snr_db, n_trials, trial_keys,
                     user_errors, breakdown);
 }
 
 int cgm_downlink_trials(cgm_ctx* ctx, int B, int U, int n_sc, int qam_bits, int K,
                         double snr_db, long n_trials, const uint64_t* trial_keys,
                         uint32_t* user_errors, uint8_t* breakdown) {
-  return run_trials(ctx, true, B, U, n_sc, qam_bits, K, CGM_TRACKER_APPROX, snr_db, n_trials,
-                    trial_keys, user_errors, breakdown);
+  return run_trials(ctx, true, CGM_METHOD_CG, B, U, n_sc, qam_bits, K, CGM_TRACKER_APPROX, snr_db,
+                    n_trials, trial_keys, user_errors, breakdown);
 }
 
 int cgm_viterbi_decode(cgm_ctx* ctx, const double* llrs, long coded_len, long n_cw,

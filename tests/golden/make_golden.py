@@ -50,8 +50,10 @@ PRECODE_CASES = [
 SWEEP_CASES = [
     (32, 8, 6, 4, "approx", 14.0, 128, 48),   # reference SweepConfig defaults (sim.hpp)
     (32, 8, 6, 3, "exact", 12.0, 128, 32),
-    (64, 16, 4, 3, "approx", 6.0, 60, 32),    # 16-QAM, 2 OFDM symbols per frame
+    (64, 16, 4, 3, "approx", 6.0, 60, 32),    # 16-QAM
     (16, 4, 2, 2, "exact", 2.0, 90, 32),      # QPSK
+    (16, 4, 2, 2, "approx", 2.0, 65, 32),     # QPSK, 3 OFDM symbols per frame
+    (32, 8, 4, 3, "exact", 8.0, 61, 24),      # 16-QAM, 3 OFDM symbols per frame
 ]
 
 # run_downlink_sweep points (sim.cpp:386-405): (B, U, qam_bits, K, snr_db, n_sc, trials), seed 7
@@ -60,6 +62,7 @@ DL_SWEEP_CASES = [
     (64, 16, 4, 3, 7.0, 60, 32),
     (16, 4, 2, 2, 0.0, 90, 32),
     (32, 8, 6, 1, 12.0, 128, 32),   # K = 1: matched-filter direction
+    (16, 4, 2, 2, 0.0, 65, 32),     # QPSK, 3 OFDM symbols per frame
 ]
 
 
@@ -113,9 +116,43 @@ def alt_fixtures(ref):
     return d
 
 
+# the trade-off study (sim.cpp:365-516): (direction, method, iters, tracker,
+# max_block_errors) on the reference SweepConfig's array / frame (32 x 8,
+# 64-QAM, 128 subcarriers), SNR 10:16:2 dB, 24 trials, seed 1
+TRADEOFF_SWEEPS = [
+    ("uplink", "chol", 1, "approx", 0),
+    ("uplink", "cg", 3, "approx", 0),
+    ("uplink", "cg", 4, "exact", 0),
+    ("uplink", "cgls", 3, "approx", 0),
+    ("uplink", "neumann", 3, "approx", 0),
+    ("uplink", "chol", 1, "approx", 40),      # early stop (sim.cpp:315-332)
+    ("downlink", "chol", 1, "approx", 0),
+    ("downlink", "cgls", 2, "approx", 0),
+    ("downlink", "neumann", 2, "approx", 0),
+]
+TRADEOFF_GRID = (10.0, 16.0, 2.0)
+TRADEOFF_TRIALS = 24
+
+
+def tradeoff_fixtures(ref):
+    d = {}
+    for i, (direction, m, K, trk, mbe) in enumerate(TRADEOFF_SWEEPS):
+        pts = ref.sweep(direction, m, 32, 8, 6, K, trk, *TRADEOFF_GRID, TRADEOFF_TRIALS, 128, 1,
+                        max_block_errors=mbe, threads=8)
+        d[f"sweep{i}"] = np.array([[p[k] for k in ("snr_db", "frames", "block_errors", "bler",
+                                                   "bler_lo", "bler_hi", "real_mults_mean",
+                                                   "breakdowns", "trials_run")] for p in pts])
+        rm, snr = ref.tradeoff_row(m, 32, 8, K, d[f"sweep{i}"][:, 0],
+                                   d[f"sweep{i}"][:, 1].astype(np.uint64),
+                                   d[f"sweep{i}"][:, 2].astype(np.uint64), 0.1)
+        d[f"row{i}"] = np.array([rm, np.nan if snr is None else snr])
+    return d
+
+
 def main():
     ref = oracle.Oracle("ref")
-    only = {"--only-coding": ("coding", coding_fixtures), "--only-alt": ("alt", alt_fixtures)}
+    only = {"--only-coding": ("coding", coding_fixtures), "--only-alt": ("alt", alt_fixtures),
+            "--only-tradeoff": ("tradeoff", tradeoff_fixtures)}
     for flag, (name, fn) in only.items():
         if flag in sys.argv:
             np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **fn(ref))
@@ -177,6 +214,7 @@ def main():
                       rayleigh=ref.rayleigh(5, [2, 3], 8, 4))
     out["coding"] = coding_fixtures(ref)
     out["alt"] = alt_fixtures(ref)
+    out["tradeoff"] = tradeoff_fixtures(ref)
     for name, d in out.items():
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **d)
     print(f"wrote {len(out)} fixtures to {HERE}")

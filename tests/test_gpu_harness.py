@@ -89,3 +89,32 @@ def test_trial_keys_follow_reference_forks(oracle_port):
     keys = sim.trial_keys(7, 2, 3)
     for t, k in enumerate(keys):
         assert oracle_port.rng_u64(int(k), [], 1)[0] == oracle_port.rng_u64(7, [1, 2, t], 1)[0]
+
+
+@pytest.mark.parametrize("case", range(9))
+def test_tradeoff_sweeps_match_reference(gpu_ctx, case):
+    """Whole sweeps of the trade-off study (every sim::Method, both
+    directions, early stop) against run_*_sweep's SnrPointResults and the
+    trade-off rows (tests/golden/tradeoff.npz)."""
+    from make_golden import TRADEOFF_GRID, TRADEOFF_SWEEPS, TRADEOFF_TRIALS
+
+    direction, m, K, trk, mbe = TRADEOFF_SWEEPS[case]
+    cfg = sim.SweepConfig(bs_antennas=32, users=8, qam_bits=6, method=m, iterations=K,
+                          tracker=trk, snr_start_db=TRADEOFF_GRID[0],
+                          snr_stop_db=TRADEOFF_GRID[1], snr_step_db=TRADEOFF_GRID[2],
+                          trials=TRADEOFF_TRIALS, subcarriers=128, seed=1,
+                          max_breakdown_fraction=1.0, max_block_errors=mbe)
+    res = sim.run_sweep(gpu_ctx, cfg, direction, batch=16)
+    d = np.load(os.path.join(HERE, "golden", "tradeoff.npz"))
+    want = d[f"sweep{case}"]
+    assert len(res.points) == len(want)
+    for p, w in zip(res.points, want):
+        assert (p.snr_db, p.frames, p.block_errors, p.breakdowns, p.trials_run) == \
+            (w[0], int(w[1]), int(w[2]), int(w[7]), int(w[8])), (p, w)
+        assert (p.bler, p.bler_lo, p.bler_hi) == (w[3], w[4], w[5])
+        if p.real_mults_mean is not None:
+            assert p.real_mults_mean == w[6]
+    row = sim.tradeoff_table([res], 0.1)[0]
+    rm, snr = d[f"row{case}"]
+    assert row.real_mults == int(rm)
+    assert (row.snr_db_at_target is None) if np.isnan(snr) else (row.snr_db_at_target == snr)
