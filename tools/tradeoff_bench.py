@@ -61,6 +61,13 @@ def main():
                         diffs.append([m, K, p.snr_db, p.block_errors, int(q["block_errors"]),
                                       p.frames])
         line["disagreements"] = diffs
+        ref_rows = [ref.tradeoff_row(m, a.B, a.U, K, [q["snr_db"] for q in rs],
+                                     [int(q["frames"]) for q in rs],
+                                     [int(q["block_errors"]) for q in rs], 0.1)
+                    for (m, K), rs in zip(ROWS, ref_sweeps)]
+        line["ref_table"] = [[m, K, rm, snr] for (m, K), (rm, snr) in zip(ROWS, ref_rows)]
+        line["table_agrees"] = all((r.real_mults, r.snr_db_at_target) == rr
+                                   for r, rr in zip(rows, ref_rows))
         line.update({"ref_trials_per_point": a.ref_trials, "ref_threads": os.cpu_count(),
                      "ref_s": round(ref_s, 3),
                      "speedup_per_trial": (ref_s / a.ref_trials) / (gpu_s / a.trials),
