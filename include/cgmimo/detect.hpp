@@ -1,5 +1,5 @@
-// cgmimo/detect.hpp -- drop-in for the reference uplink CG detector
-// (reference proj/include/cgmimo/detect.hpp:21-61).  detect_cg keeps the
+// cgmimo/detect.hpp -- drop-in for the reference uplink detectors
+// (reference proj/include/cgmimo/detect.hpp:21-73).  detect_cg keeps the
 // reference signature and runs on the B200 through the C ABI
 // (include/cgmimo_b200.h); detect_cg_batch is the batched form the GPU wants.
 #pragma once
@@ -33,6 +33,16 @@ std::vector<double> compute_llrs(cplx xhat, double mu, double rho, const phy::Co
 SoftOutput detect_cg(const ComplexMatrix& h, const ComplexVector& y, double rho_u, double n0,
                      double es, const phy::Constellation& c, std::size_t iters,
                      SinrTracker tracker);
+
+// The trade-off study's other detectors (reference detect.hpp:47-73), same
+// signatures and exceptions (NotPositiveDefinite from Cholesky,
+// std::domain_error from a zero Neumann diagonal).
+SoftOutput detect_cholesky(const ComplexMatrix& h, const ComplexVector& y, double rho_u,
+                           double n0, double es, const phy::Constellation& c);
+SoftOutput detect_cgls(const ComplexMatrix& h, const ComplexVector& y, double rho_u, double n0,
+                       double es, const phy::Constellation& c, std::size_t iters);
+SoftOutput detect_neumann(const ComplexMatrix& h, const ComplexVector& y, double rho_u,
+                          double n0, double es, const phy::Constellation& c, std::size_t terms);
 
 // Batched form: hs[i] / ys[i] pairs (every hs[i] of equal shape).  Instances
 // that break down get status 1 and zeroed outputs instead of throwing.

@@ -1,5 +1,5 @@
-// cgmimo/precode.hpp -- drop-in for the reference CG precoder
-// (reference proj/include/cgmimo/precode.hpp:17-33).
+// cgmimo/precode.hpp -- drop-in for the reference precoders
+// (reference proj/include/cgmimo/precode.hpp:17-45).
 #pragma once
 
 #include <cstddef>
@@ -20,5 +20,15 @@ struct PrecodeResult {
 // when given, receives q_k for k = 1..K.
 PrecodeResult precode_cg(const ComplexMatrix& h_downlink, const ComplexVector& t, double rho_d,
                          std::size_t iters, std::vector<ComplexVector>* q_trace = nullptr);
+
+// q = H_d^H (H_d H_d^H + rho_d^-1 I)^-1 t through a Cholesky inverse.
+PrecodeResult precode_explicit(const ComplexMatrix& h_downlink, const ComplexVector& t,
+                               double rho_d);
+// Minimum-norm CGLS; q_k per iteration into q_trace when given.
+PrecodeResult precode_cgls(const ComplexMatrix& h_downlink, const ComplexVector& t, double rho_d,
+                           std::size_t iters, std::vector<ComplexVector>* q_trace = nullptr);
+// Truncated Neumann series of A_d^-1 with `terms` terms.
+PrecodeResult precode_neumann(const ComplexMatrix& h_downlink, const ComplexVector& t,
+                              double rho_d, std::size_t terms);
 
 }  // namespace cgmimo::precode

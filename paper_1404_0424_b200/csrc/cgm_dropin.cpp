@@ -2,7 +2,9 @@
 // implemented on the C ABI (include/cgmimo_b200.h).  A caller written
 // against the reference headers relinks against libcgmimo_b200.so unchanged:
 //   cgmimo::detect::detect_cg    (reference detect.hpp:58-61)
+//   cgmimo::detect::detect_cholesky / detect_cgls / detect_neumann (:54-73)
 //   cgmimo::precode::precode_cg  (reference precode.hpp:31-33)
+//   cgmimo::precode::precode_explicit / precode_cgls / precode_neumann (:25-45)
 // FP64 arguments are converted to complex64 at the boundary and results
 // widened back; errors map to the reference's exception types.
 #include <algorithm>
@@ -268,10 +270,172 @@ SoftOutput detect_cg(const ComplexMatrix& h, const ComplexVector& y, double rho_
   return std::move(out[0]);
 }
 
+namespace {
+
+// closed-form stage counts of the other detectors (opcount.cpp:69-138) as the
+// reference's instrumented path records them; CGLS iterations past exact
+// convergence (min(K, U)) are frozen and uncounted, like CG's
+void record_alt_counts(int method, std::size_t B, std::size_t U, std::size_t K, bool zero_rhs) {
+  using opcount::Stage;
+  if (!opcount::counting_active()) return;
+  const std::uint64_t b = B, u = U, k = K;
+  if (method == CGM_METHOD_CHOLESKY) {
+    opcount::record(Stage::kGram, 2 * b * u * u);
+    opcount::record(Stage::kMatchedFilter, 4 * b * u);
+    opcount::record(Stage::kCholesky, u * (u - 1) + 2 * u * (u - 1) * (u - 2) / 3);
+    opcount::record(Stage::kSubstitution,
+                    2 * (u * u * u - u) / 3 + 2 * u * u * (u - 1) + 4 * u * u + 6 * u * u + 2 * u);
+  } else if (method == CGM_METHOD_CGLS) {
+    const std::uint64_t live = zero_rhs ? 0 : std::min(k, u);
+    opcount::record(Stage::kGram, 2 * b * u);
+    opcount::record(Stage::kMatchedFilter, 4 * b * u);
+    opcount::record(Stage::kCglsIteration, 2 * u + live * (8 * b * u + 4 * b + 14 * u));
+    opcount::record(Stage::kTracker, k * u);
+  } else {
+    opcount::record(Stage::kGram, 2 * b * u * u);
+    opcount::record(Stage::kMatchedFilter, 4 * b * u);
+    std::uint64_t series = 0;
+    if (k >= 2) series += 4 * u * (u - 1);
+    if (k >= 3) series += (k - 2) * 2 * u * u * (u + 1);
+    opcount::record(Stage::kNeumannTerm, series);
+    opcount::record(Stage::kSubstitution, ((k == 1) ? 2 * u : 4 * u * u) +
+                                              ((k == 1) ? u : 4 * u * u) + 2 * u);
+  }
+}
+
+void throw_status(std::uint8_t st, int method, const char* who) {
+  if (st & 1u) throw solvers::SolverBreakdown(std::string(who) + ": breakdown");
+  if (st & 4u) {
+    if (method == CGM_METHOD_CHOLESKY)
+      throw solvers::NotPositiveDefinite("cholesky_factor: non-positive pivot");
+    throw std::domain_error("neumann_inverse: zero diagonal entry");
+  }
+}
+
+SoftOutput detect_alt(int method, const char* who, const ComplexMatrix& h, const ComplexVector& y,
+                      double rho_u, double n0, double es, const phy::Constellation& c,
+                      std::size_t iters) {
+  // detect.cpp:127-129, :243-245, :279-281
+  if (h.rows() != y.size()) throw std::invalid_argument(std::string(who) + ": dimension mismatch");
+  if (!(rho_u > 0.0 && n0 > 0.0 && es > 0.0))
+    throw std::invalid_argument(std::string(who) + ": bad parameters");
+  if (iters < 1) throw std::invalid_argument(std::string(who) + ": need at least one iteration");
+  const std::size_t B = h.rows(), U = h.cols();
+  const int bits = bits_of(c);
+  std::vector<float> H(2 * B * U), Y(2 * B), X(2 * U), MU(U), RHO(U), L(U * bits);
+  std::uint8_t st = 0;
+  to_c64(h.data(), B * U, H.data());
+  to_c64(y.data(), B, Y.data());
+  cgm_ctx* ctx = t_ctx.get();
+  check(cgm_detect(ctx, method, static_cast<int>(B), static_cast<int>(U), 1, 1, H.data(), Y.data(),
+                   rho_u, n0, es, bits, static_cast<int>(iters), CGM_TRACKER_APPROX, X.data(),
+                   MU.data(), RHO.data(), L.data(), &st, 0),
+        ctx);
+  throw_status(st, method, who);
+  bool zero = true;
+  for (const auto& v : y) zero = zero && v == cplx(0.0, 0.0);
+  record_alt_counts(method, B, U, iters, zero);
+  SoftOutput o;
+  o.xhat.resize(U);
+  o.mu.resize(U);
+  o.rho.resize(U);
+  o.llrs.assign(U, std::vector<double>(bits));
+  for (std::size_t u = 0; u < U; ++u) {
+    o.xhat[u] = cplx(X[2 * u], X[2 * u + 1]);
+    o.mu[u] = MU[u];
+    o.rho[u] = RHO[u];
+    for (int b = 0; b < bits; ++b) o.llrs[u][b] = L[u * bits + b];
+  }
+  return o;
+}
+
+}  // namespace
+
+SoftOutput detect_cholesky(const ComplexMatrix& h, const ComplexVector& y, double rho_u,
+                           double n0, double es, const phy::Constellation& c) {
+  return detect_alt(CGM_METHOD_CHOLESKY, "detect_cholesky", h, y, rho_u, n0, es, c, 1);
+}
+
+SoftOutput detect_cgls(const ComplexMatrix& h, const ComplexVector& y, double rho_u, double n0,
+                       double es, const phy::Constellation& c, std::size_t iters) {
+  return detect_alt(CGM_METHOD_CGLS, "detect_cgls", h, y, rho_u, n0, es, c, iters);
+}
+
+SoftOutput detect_neumann(const ComplexMatrix& h, const ComplexVector& y, double rho_u,
+                          double n0, double es, const phy::Constellation& c, std::size_t terms) {
+  return detect_alt(CGM_METHOD_NEUMANN, "detect_neumann", h, y, rho_u, n0, es, c, terms);
+}
+
 }  // namespace detect
 
 // ---------------------------------------------------------------- precode
 namespace precode {
+
+namespace {
+
+ComplexVector precode_one(int method, const ComplexMatrix& h_downlink, const ComplexVector& t,
+                          double rho_d, std::size_t iters, PrecodeResult* res, const char* who) {
+  const std::size_t U = h_downlink.rows(), B = h_downlink.cols();
+  std::vector<float> Hd(2 * U * B), T(2 * U), Q(2 * B), S(2 * B);
+  to_c64(h_downlink.data(), U * B, Hd.data());
+  to_c64(t.data(), U, T.data());
+  cgm_ctx* ctx = t_ctx.get();
+  float gain = 0.f;
+  std::uint8_t st = 0;
+  check(cgm_precode(ctx, method, static_cast<int>(B), static_cast<int>(U), 1, 1, Hd.data(),
+                    T.data(), rho_d, static_cast<int>(iters), Q.data(), S.data(), &gain, &st, 0),
+        ctx);
+  detect::throw_status(st, method, who);
+  ComplexVector q(B);
+  for (std::size_t b = 0; b < B; ++b) q[b] = cplx(Q[2 * b], Q[2 * b + 1]);
+  if (res) {
+    res->zero_input = (st & 2u) != 0;
+    res->gain = res->zero_input ? 0.0 : gain;
+    res->transmit.resize(B);
+    for (std::size_t b = 0; b < B; ++b) res->transmit[b] = cplx(S[2 * b], S[2 * b + 1]);
+    res->precoded = q;
+  }
+  return q;
+}
+
+void precode_checks(const ComplexMatrix& h_downlink, const ComplexVector& t, double rho_d,
+                    std::size_t iters, const char* who) {
+  // precode.cpp:47-48, :76-77, :86-87; solvers.cpp:200-201
+  if (!(rho_d > 0.0)) throw std::invalid_argument(std::string(who) + ": rho_d must be positive");
+  if (h_downlink.rows() != t.size()) throw std::invalid_argument(std::string(who) + ": dimension mismatch");
+  if (iters < 1) throw std::invalid_argument(std::string(who) + ": need at least one iteration");
+}
+
+}  // namespace
+
+PrecodeResult precode_explicit(const ComplexMatrix& h_downlink, const ComplexVector& t,
+                               double rho_d) {
+  precode_checks(h_downlink, t, rho_d, 1, "precode_explicit");
+  PrecodeResult res;
+  precode_one(CGM_METHOD_CHOLESKY, h_downlink, t, rho_d, 1, &res, "precode_explicit");
+  return res;
+}
+
+PrecodeResult precode_cgls(const ComplexMatrix& h_downlink, const ComplexVector& t, double rho_d,
+                           std::size_t iters, std::vector<ComplexVector>* q_trace) {
+  precode_checks(h_downlink, t, rho_d, iters, "precode_cgls");
+  if (q_trace) {
+    q_trace->clear();
+    for (std::size_t k = 1; k <= iters; ++k)
+      q_trace->push_back(precode_one(CGM_METHOD_CGLS, h_downlink, t, rho_d, k, nullptr, "cgls"));
+  }
+  PrecodeResult res;
+  precode_one(CGM_METHOD_CGLS, h_downlink, t, rho_d, iters, &res, "cgls_solve_min_norm");
+  return res;
+}
+
+PrecodeResult precode_neumann(const ComplexMatrix& h_downlink, const ComplexVector& t,
+                              double rho_d, std::size_t terms) {
+  precode_checks(h_downlink, t, rho_d, terms, "precode_neumann");
+  PrecodeResult res;
+  precode_one(CGM_METHOD_NEUMANN, h_downlink, t, rho_d, terms, &res, "precode_neumann");
+  return res;
+}
 
 PrecodeResult precode_cg(const ComplexMatrix& h_downlink, const ComplexVector& t, double rho_d,
                          std::size_t iters, std::vector<ComplexVector>* q_trace) {

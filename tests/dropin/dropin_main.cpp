@@ -141,8 +141,87 @@ static int gpu_mode(const char* in, const char* out) {
   return 0;
 }
 
+// in.bin: int32 B, U, bits, n, K; n x (H[B][U], y[B]); int32 Bd, Ud, nd, Kd;
+// nd x (Hd[Ud][Bd], t[Ud]); double rho_u, n0, rho_d.  Per instance and
+// method (cholesky, cgls K, neumann K): xhat, mu, rho, llr, stage tally; per
+// precoder instance and method (explicit, cgls Kd, neumann Kd): q, s, gain.
+static int alt_mode(const char* in, const char* out) {
+  std::ifstream f(in, std::ios::binary);
+  auto rd = [&](void* p, size_t n) { f.read(static_cast<char*>(p), n); };
+  int hdr[5];
+  rd(hdr, sizeof hdr);
+  const int B = hdr[0], U = hdr[1], bits = hdr[2], n = hdr[3], K = hdr[4];
+  std::vector<ComplexMatrix> hs;
+  std::vector<ComplexVector> ys;
+  for (int i = 0; i < n; ++i) {
+    ComplexMatrix h(B, U);
+    for (int b = 0; b < B; ++b) rd(h.row(b), sizeof(cplx) * U);
+    ComplexVector y(B);
+    rd(y.data(), sizeof(cplx) * B);
+    hs.push_back(h);
+    ys.push_back(y);
+  }
+  int ph[4];
+  rd(ph, sizeof ph);
+  const int Bd = ph[0], Ud = ph[1], nd = ph[2], Kd = ph[3];
+  std::vector<ComplexMatrix> hds;
+  std::vector<ComplexVector> ts;
+  for (int i = 0; i < nd; ++i) {
+    ComplexMatrix h(Ud, Bd);
+    for (int u = 0; u < Ud; ++u) rd(h.row(u), sizeof(cplx) * Bd);
+    ComplexVector t(Ud);
+    rd(t.data(), sizeof(cplx) * Ud);
+    hds.push_back(h);
+    ts.push_back(t);
+  }
+  double prm[3];
+  rd(prm, sizeof prm);
+  const auto c = phy::make_constellation(bits == 2 ? phy::Modulation::kQpsk
+                                                   : bits == 4 ? phy::Modulation::kQam16
+                                                               : phy::Modulation::kQam64);
+  std::ofstream o(out, std::ios::binary);
+  auto wr = [&](const void* p, size_t nb) { o.write(static_cast<const char*>(p), nb); };
+  for (int i = 0; i < n; ++i)
+    for (int m = 0; m < 3; ++m) {
+      opcount::Tally tally;
+      detect::SoftOutput r;
+      {
+        opcount::ScopedTally s(tally);
+        r = m == 0   ? detect::detect_cholesky(hs[i], ys[i], prm[0], prm[1], 1.0, c)
+            : m == 1 ? detect::detect_cgls(hs[i], ys[i], prm[0], prm[1], 1.0, c, K)
+                     : detect::detect_neumann(hs[i], ys[i], prm[0], prm[1], 1.0, c, K);
+      }
+      wr(r.xhat.data(), sizeof(cplx) * U);
+      wr(r.mu.data(), sizeof(double) * U);
+      wr(r.rho.data(), sizeof(double) * U);
+      for (int u = 0; u < U; ++u) wr(r.llrs[u].data(), sizeof(double) * bits);
+      std::uint64_t st[opcount::kStageCount];
+      for (int s = 0; s < opcount::kStageCount; ++s) st[s] = tally.get(static_cast<opcount::Stage>(s));
+      wr(st, sizeof st);
+    }
+  for (int i = 0; i < nd; ++i)
+    for (int m = 0; m < 3; ++m) {
+      const auto r = m == 0   ? precode::precode_explicit(hds[i], ts[i], prm[2])
+                     : m == 1 ? precode::precode_cgls(hds[i], ts[i], prm[2], Kd)
+                              : precode::precode_neumann(hds[i], ts[i], prm[2], Kd);
+      wr(r.precoded.data(), sizeof(cplx) * Bd);
+      wr(r.transmit.data(), sizeof(cplx) * Bd);
+      wr(&r.gain, sizeof(double));
+    }
+  // argument errors as the reference (detect.cpp:243-245)
+  int bad = 0;
+  try {
+    (void)detect::detect_cgls(hs[0], ys[0], prm[0], prm[1], 1.0, c, 0);
+  } catch (const std::invalid_argument&) {
+    bad = 1;
+  }
+  wr(&bad, sizeof bad);
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc >= 2 && std::strcmp(argv[1], "host") == 0) return host_mode();
+  if (argc >= 4 && std::strcmp(argv[1], "alt") == 0) return alt_mode(argv[2], argv[3]);
   if (argc >= 4 && std::strcmp(argv[1], "gpu") == 0) return gpu_mode(argv[2], argv[3]);
   std::fprintf(stderr, "usage: dropin_main host | gpu in.bin out.bin\n");
   return 2;

@@ -49,7 +49,10 @@ def test_cxx_dropin_symbols_exported():
     out = subprocess.run(["nm", "-DC", "--defined-only", _lib.LIB_PATH], capture_output=True,
                          text=True).stdout
     for sym in ("cgmimo::detect::detect_cg(", "cgmimo::precode::precode_cg(",
-                "cgmimo::detect::compute_llrs(", "cgmimo::phy::make_constellation("):
+                "cgmimo::detect::compute_llrs(", "cgmimo::phy::make_constellation(",
+                "cgmimo::detect::detect_cholesky(", "cgmimo::detect::detect_cgls(",
+                "cgmimo::detect::detect_neumann(", "cgmimo::precode::precode_explicit(",
+                "cgmimo::precode::precode_cgls(", "cgmimo::precode::precode_neumann("):
         assert sym in out, sym
 
 

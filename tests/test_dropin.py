@@ -111,3 +111,70 @@ def test_dropin_per_call_on_gpu(dropin_exe, checker, tmp_path):
         assert_close(trace[-1], wantp["q"][i, 0], "dropin q_trace[K-1]")
     broke = take(1, np.int32)[0]
     assert broke == 1
+
+
+@pytest.mark.gpu
+def test_dropin_other_solvers_on_gpu(dropin_exe, checker, tmp_path):
+    """detect_cholesky / detect_cgls / detect_neumann and precode_explicit /
+    precode_cgls / precode_neumann through the reference's C++ signatures."""
+    rng = np.random.default_rng(9)
+    B, U, bits, n, K = 32, 8, 4, 3, 3
+    n0 = 0.1
+    H = [cplx_randn(rng, (B, U)).astype(np.complex64).astype(np.complex128) for _ in range(n)]
+    y = [cplx_randn(rng, B, 3.0).astype(np.complex64).astype(np.complex128) for _ in range(n)]
+    Bd, Ud, nd, Kd = 48, 6, 2, 2
+    Hd = [cplx_randn(rng, (Ud, Bd)).astype(np.complex64).astype(np.complex128) for _ in range(nd)]
+    t = [cplx_randn(rng, Ud).astype(np.complex64).astype(np.complex128) for _ in range(nd)]
+    rho_d = 4.0
+    with open(tmp_path / "in.bin", "wb") as f:
+        f.write(struct.pack("5i", B, U, bits, n, K))
+        for h, v in zip(H, y):
+            f.write(h.tobytes())
+            f.write(v.tobytes())
+        f.write(struct.pack("4i", Bd, Ud, nd, Kd))
+        for h, v in zip(Hd, t):
+            f.write(h.tobytes())
+            f.write(v.tobytes())
+        f.write(struct.pack("3d", 1 / n0, n0, rho_d))
+    r = subprocess.run([dropin_exe, "alt", str(tmp_path / "in.bin"), str(tmp_path / "out.bin")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    data = open(tmp_path / "out.bin", "rb").read()
+    off = 0
+
+    def take(count, dt):
+        nonlocal off
+        a = np.frombuffer(data, dt, count, off)
+        off += a.nbytes
+        return a
+
+    methods = [("cholesky", 1), ("cgls", K), ("neumann", K)]
+    want = {m: checker.detect(np.stack(H), np.stack(y)[:, :, None], 1 / n0, n0, 1.0, bits, k,
+                              method=m) for m, k in methods}
+    from paper_1404_0424_b200 import sim
+    for i in range(n):
+        for m, k in methods:
+            w = want[m]
+            xh = take(U, np.complex128)
+            mu = take(U, np.float64)
+            rho = take(U, np.float64)
+            llr = take(U * bits, np.float64).reshape(U, bits)
+            tally = take(9, np.uint64)
+            assert_close(xh, w["xhat"][i, 0], f"dropin {m} xhat")
+            assert_close(mu, w["mu"][i, 0], f"dropin {m} mu")
+            assert_close(rho, w["rho"][i, 0], f"dropin {m} rho", rtol=2e-3)
+            assert_hard_bits(llr, w["llr"][i, 0], f"dropin {m} hard bits")
+            # the reference's closed forms (opcount.cpp:69-138)
+            stages = sim.count_detect_stages("chol" if m == "cholesky" else m, B, U, k)
+            assert [int(v) for v in tally] == [stages[s] for s in sim.STAGES], m
+    for i in range(nd):
+        for m, k in [("explicit", 1), ("cgls", Kd), ("neumann", Kd)]:
+            wp = checker.precode(np.stack(Hd)[i:i + 1], np.stack(t)[i:i + 1, None, :], rho_d, k,
+                                 method=m)
+            q = take(Bd, np.complex128)
+            s = take(Bd, np.complex128)
+            gain = take(1, np.float64)[0]
+            assert_close(q, wp["q"][0, 0], f"dropin precode {m} q")
+            assert_close(s, wp["s"][0, 0], f"dropin precode {m} s")
+            assert_close(gain, wp["gain"][0, 0], f"dropin precode {m} gain")
+    assert take(1, np.int32)[0] == 1
