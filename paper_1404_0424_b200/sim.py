@@ -197,25 +197,49 @@ def count_detect(method: str, B: int, U: int, K: int) -> int:
 
 
 # -------------------------------------------------------------- the sweeps
-def _run_point(ctx, cfg: SweepConfig, direction: int, pi: int, snr: float, batch: int):
+def _sharded(run, start: int, count: int, group):
+    """Trials [start, start + count) split into contiguous blocks over the
+    ranks of `group` (torch.distributed, one process per GPU); every rank gets
+    every trial's (errors, breakdown) back in trial order.  Trials are pure
+    functions of their keys, so the split does not change any result."""
+    if group is None:
+        return run(start, count)
+    import torch
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    per = -(-count // world)
+    lo = min(count, rank * per)
+    n = min(count, lo + per) - lo
+    e, b = run(start + lo, n) if n > 0 else (np.zeros(0, np.uint32), np.zeros(0, np.uint8))
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    mine = torch.full((2, per), -1, dtype=torch.int64, device=dev)
+    mine[0, :n] = torch.from_numpy(e.astype(np.int64)).to(dev)
+    mine[1, :n] = torch.from_numpy(b.astype(np.int64)).to(dev)
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    full = torch.cat(parts, dim=1).cpu().numpy()
+    full = full[:, full[0] >= 0][:, :count]
+    return full[0].astype(np.uint32), full[1].astype(np.uint8)
+
+
+def _fold_point(run, cfg: SweepConfig, snr: float, batch: int, group=None) -> SnrPointResult:
     """sim.cpp:307-361 run_point: fixed trials, or waves with the in-order
-    early-stop fold when max_block_errors > 0 (scheduling independent)."""
-    method = METHOD_NAMES.index(cfg.method)
-    trk = 0 if cfg.tracker == "exact" else 1
-    lib = ctx.lib
+    early-stop fold when max_block_errors > 0 (scheduling independent).
+    run(first, count) -> (user_errors, breakdown) of trials [first, first + count)."""
     errs = np.zeros(cfg.trials, np.uint32)
     brk = np.zeros(cfg.trials, np.uint8)
-    folded = cfg.trials
+    folded = 0 if cfg.max_block_errors else cfg.trials
     done, errors_so_far = 0, 0
-    if cfg.max_block_errors:
-        folded = 0
+    world = 1
+    if group is not None:
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group)
     while done < cfg.trials:
-        end = min(cfg.trials, done + batch)
-        keys = trial_keys(cfg.seed, pi, end - done, direction, first=done)
-        ctx._check(lib.cgm_sweep_trials(
-            ctx.h, direction, method, cfg.bs_antennas, cfg.users, cfg.subcarriers, cfg.qam_bits,
-            cfg.iterations, trk, float(snr), end - done, keys.ctypes.data_as(C.c_void_p),
-            errs[done:end].ctypes.data_as(C.c_void_p), brk[done:end].ctypes.data_as(C.c_void_p)))
+        end = min(cfg.trials, done + batch * world)
+        errs[done:end], brk[done:end] = _sharded(run, done, end - done, group)
         if cfg.max_block_errors:
             stop = False
             for t in range(done, end):
@@ -237,6 +261,25 @@ def _run_point(ctx, cfg: SweepConfig, direction: int, pi: int, snr: float, batch
         raise BreakdownBudgetExceeded("solver breakdowns exceeded the configured budget")
     pt.bler = pt.block_errors / pt.frames if pt.frames > 0 else 0.0
     pt.bler_lo, pt.bler_hi = wilson_interval(pt.block_errors, pt.frames)
+    return pt
+
+
+def _run_point(ctx, cfg: SweepConfig, direction: int, pi: int, snr: float, batch: int,
+               group=None):
+    method = METHOD_NAMES.index(cfg.method)
+    trk = 0 if cfg.tracker == "exact" else 1
+
+    def run(first, count):
+        e = np.zeros(count, np.uint32)
+        b = np.zeros(count, np.uint8)
+        keys = trial_keys(cfg.seed, pi, count, direction, first=first)
+        ctx._check(ctx.lib.cgm_sweep_trials(
+            ctx.h, direction, method, cfg.bs_antennas, cfg.users, cfg.subcarriers, cfg.qam_bits,
+            cfg.iterations, trk, float(snr), count, keys.ctypes.data_as(C.c_void_p),
+            e.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p)))
+        return e, b
+
+    pt = _fold_point(run, cfg, snr, batch, group)
     # per equalised vector: the closed form where the reference's opcount has
     # one (uplink, all methods except the exact tracker; sim.cpp:359)
     if direction == 1 and not (cfg.method == "cg" and cfg.tracker == "exact") and pt.frames:
@@ -245,22 +288,25 @@ def _run_point(ctx, cfg: SweepConfig, direction: int, pi: int, snr: float, batch
     return pt
 
 
-def run_sweep(ctx, cfg: SweepConfig, direction: str = "uplink", batch: int = 64) -> SweepResult:
-    """sim::run_uplink_sweep / run_downlink_sweep (sim.cpp:365-405)."""
+def run_sweep(ctx, cfg: SweepConfig, direction: str = "uplink", batch: int = 64,
+              group=None) -> SweepResult:
+    """sim::run_uplink_sweep / run_downlink_sweep (sim.cpp:365-405).  With a
+    torch.distributed `group` (one process per GPU) every SNR point's trials
+    are sharded over the ranks and all ranks return the same result."""
     validate_config(cfg)
     d = {"uplink": 1, "downlink": 2}[direction]
     res = SweepResult(config=replace(cfg), direction=direction)
     for pi, snr in enumerate(snr_grid(cfg)):
-        res.points.append(_run_point(ctx, cfg, d, pi, snr, batch))
+        res.points.append(_run_point(ctx, cfg, d, pi, snr, batch, group))
     return res
 
 
-def run_uplink_sweep(ctx, cfg: SweepConfig, batch: int = 64) -> SweepResult:
-    return run_sweep(ctx, cfg, "uplink", batch)
+def run_uplink_sweep(ctx, cfg: SweepConfig, batch: int = 64, group=None) -> SweepResult:
+    return run_sweep(ctx, cfg, "uplink", batch, group)
 
 
-def run_downlink_sweep(ctx, cfg: SweepConfig, batch: int = 64) -> SweepResult:
-    return run_sweep(ctx, cfg, "downlink", batch)
+def run_downlink_sweep(ctx, cfg: SweepConfig, batch: int = 64, group=None) -> SweepResult:
+    return run_sweep(ctx, cfg, "downlink", batch, group)
 
 
 def snr_at_target_bler(result: SweepResult, target: float) -> Optional[float]:

@@ -118,3 +118,30 @@ def test_tradeoff_sweeps_match_reference(gpu_ctx, case):
     rm, snr = d[f"row{case}"]
     assert row.real_mults == int(rm)
     assert (row.snr_db_at_target is None) if np.isnan(snr) else (row.snr_db_at_target == snr)
+
+
+def test_sweep_through_a_process_group_matches_reference(gpu_ctx):
+    """The sharded sweep path (sim._sharded: all_gather of per-trial
+    outcomes) on a one-rank group reproduces the early-stop sweep."""
+    import socket
+
+    import torch.distributed as dist
+    from make_golden import TRADEOFF_GRID, TRADEOFF_SWEEPS, TRADEOFF_TRIALS
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        direction, m, K, trk, mbe = TRADEOFF_SWEEPS[5]
+        cfg = sim.SweepConfig(method=m, iterations=K, tracker=trk, snr_start_db=TRADEOFF_GRID[0],
+                              snr_stop_db=TRADEOFF_GRID[1], snr_step_db=TRADEOFF_GRID[2],
+                              trials=TRADEOFF_TRIALS, max_breakdown_fraction=1.0,
+                              max_block_errors=mbe)
+        res = sim.run_sweep(gpu_ctx, cfg, direction, batch=4, group=dist.group.WORLD)
+    finally:
+        dist.destroy_process_group()
+    want = np.load(os.path.join(HERE, "golden", "tradeoff.npz"))["sweep5"]
+    assert [(p.frames, p.block_errors, p.trials_run) for p in res.points] == \
+        [(int(w[1]), int(w[2]), int(w[8])) for w in want]

@@ -64,3 +64,52 @@ def test_two_rank_shard_and_gather_equals_single(n_sc):
     o, H, Y = _inputs(n_sc)
     want = o.detect(H, Y, 2.0, 0.5, 1.0, 4, 3, "exact")["llr"].astype(np.float32).reshape(-1)
     assert np.array_equal(got, want)
+
+
+# --------------------------------------------- sharded BLER sweeps (sim.py)
+def _fake_trials(first, count):
+    """Deterministic stand-in for cgm_sweep_trials: errors and breakdowns as
+    functions of the trial index only (as real trials are of their keys)."""
+    t = np.arange(first, first + count)
+    return ((t * 7919) % 5).astype(np.uint32), ((t % 13) == 4).astype(np.uint8)
+
+
+def _sweep_worker(rank, world, port, cfgs, outq):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1404_0424_b200 import sim
+
+    res = []
+    for kw in cfgs:
+        cfg = sim.SweepConfig(**kw)
+        res.append(sim._fold_point(_fake_trials, cfg, 10.0, batch=7, group=dist.group.WORLD))
+    outq.put((rank, [(p.frames, p.block_errors, p.breakdowns, p.trials_run) for p in res]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_sharded_sweep_point_equals_single():
+    """Trials split over 2 ranks (contiguous blocks, all_gather, in-order fold)
+    give the single-process SnrPointResult, with and without the early stop."""
+    sys.path.insert(0, ROOT)
+    from paper_1404_0424_b200 import sim
+
+    cfgs = [dict(trials=50, max_breakdown_fraction=1.0), dict(trials=49, max_breakdown_fraction=1.0,
+                                                            max_block_errors=33),
+            dict(trials=3, max_breakdown_fraction=1.0)]
+    want = []
+    for kw in cfgs:
+        p = sim._fold_point(_fake_trials, sim.SweepConfig(**kw), 10.0, batch=7)
+        want.append((p.frames, p.block_errors, p.breakdowns, p.trials_run))
+    assert want[1][3] < 49  # the early stop fired
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sweep_worker, args=(r, 2, port, cfgs, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert got[0] == want and got[1] == want
