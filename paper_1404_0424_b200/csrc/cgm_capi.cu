@@ -234,6 +234,25 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       smem2 = T2.total;
     }
   }
+  // persistent K2 with the next subcarrier's G + MF prefetched: measured
+  // faster with many systems per subcarrier (cfg5, S + St = 32: 14.4 vs
+  // 15.7 ms) and slower with few (cfg2 45.8 vs 43.3 us, cfg4 +13-40%: the
+  // static subcarrier split loses the hardware's dynamic balancing), so on
+  // from 24 systems; CGMIMO_SOLVE=pf / nopf force it either way
+  bool use_pf = false;
+  {
+    const char* force = std::getenv("CGMIMO_SOLVE");
+    const bool want = force ? std::strcmp(force, "pf") == 0
+                            : (p.S + p.St >= 24);
+    if (!use_s32 && want) {
+      const int need = 128 + 2 * cgm::k2_pre_bytes(UP, p.S) + L2.total;
+      if (need <= ctx->max_smem) {
+        use_pf = true;
+        k2 = cgm::solve_kernel_pf<UP, EXACT>;
+        smem2 = need;
+      }
+    }
+  }
   CGM_CUDA(ctx, cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
   int occ1 = 0;
   CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k1, nt1, smem1));
@@ -247,6 +266,12 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   if (EXACT) nw2 = std::max(nw2, std::max(4, UP / 32));
   nw2 = std::max(1, std::min(8, nw2));
   if (use_s32) nw2 = ((nsys + ts2 - 1) / ts2 * 8 + 31) / 32;  // 8 threads per tile, whole warps
+  long g2cap = 1L << 40;
+  if (use_pf) {
+    int occ2 = 0;
+    CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k2, 32 * nw2, smem2));
+    g2cap = static_cast<long>(std::max(occ2, 1)) * ctx->sms;
+  }
   // chunk so that workspace + channel (+ Y) of a chunk fit comfortably in L2
   const size_t per_sc = static_cast<size_t>(W.stride) * 8 + static_cast<size_t>(p.B) * p.U * 8 +
                         static_cast<size_t>(p.B) * p.S * 8;
@@ -309,7 +334,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       CGM_CUDA(ctx, cudaStreamWaitEvent(s2, ctx->ov_ev[1 + half], 0));
     }
     if (ctx->profiling) cudaEventRecord(e2, s2);
-    k2<<<static_cast<unsigned>(n), 32 * nw2, smem2, s2>>>(p);
+    k2<<<static_cast<unsigned>(std::min(n, g2cap)), 32 * nw2, smem2, s2>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
     if (ctx->profiling) {
       cudaEventRecord(e3, s2);

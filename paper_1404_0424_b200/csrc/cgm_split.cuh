@@ -596,7 +596,7 @@ __device__ __forceinline__ void k2_precode_tail(const KernelParams& p, long sc, 
 // epilogue warps of channel_tc_kernel.
 template <int UP, bool EXACT, int NSO = 0, bool GREG = false, class Sync>
 __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsigned char* smem,
-                                         int nt, Sync&& sync) {
+                                         int nt, Sync&& sync, const float2* pre = nullptr) {
   using GE = K2Geo<UP, NSO>;
   static_assert(!GREG || (UP == 32 && GE::NS == 1), "GREG needs U = 32, one system per warp");
   constexpr int G = GE::G, RU = GE::RU, GPW = GE::GPW, NS = GE::NS;
@@ -607,7 +607,9 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
   L.plan(B, S, St, Kmax, EXACT);
   WsOffsets W;
   W.plan(UP, S, p.K, EXACT);
-  float2* Gs = reinterpret_cast<float2*>(smem + L.gs);
+  // G (and the matched filters) from the prefetched shared-memory copy of
+  // the workspace when the persistent kernel staged one
+  const float2* Gs = pre ? pre + W.g : reinterpret_cast<float2*>(smem + L.gs);
   float2* Ps = reinterpret_cast<float2*>(smem + L.ps);
   float2* Vs = reinterpret_cast<float2*>(smem + L.vs);
   float2* Qs = reinterpret_cast<float2*>(smem + L.qs);
@@ -622,12 +624,13 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
   const long sc = p.sc_base + lsc;
   const float2* ws = p.ws + lsc * W.stride;
 
-  {  // G <- workspace
+  const float2* mfsrc = pre ? pre + W.mf : ws + W.mf;
+  if (!pre) {  // G <- workspace
     const float4* src = reinterpret_cast<const float4*>(ws + W.g);
-    float4* dst = reinterpret_cast<float4*>(Gs);
+    float4* dst = reinterpret_cast<float4*>(smem + L.gs);
     for (int e = tid; e < UP * UP / 2; e += nt) dst[e] = src[e];
+    sync();
   }
-  sync();
 
   // ------------------------------------------------------------------ CG
   {
@@ -662,7 +665,7 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
           float2 b = make_float2(0.f, 0.f);
           if (live[s] && u < U)
             b = down[s] ? p.T[(sc * St + (sys[s] - S)) * static_cast<long>(U) + u]
-                        : ws[W.mf + sys[s] * UP + u];
+                        : mfsrc[sys[s] * UP + u];
           v[s][m] = make_float2(0.f, 0.f);
           r[s][m] = b;
           pp[s][m] = b;
@@ -867,6 +870,46 @@ template <int UP, bool EXACT, int MINB = 3, int NSO = 0, bool GREG = false>
 __global__ void __launch_bounds__(256, MINB) solve_kernel(const KernelParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   solve_sc<UP, EXACT, NSO, GREG>(p, blockIdx.x, smem, blockDim.x, [] { __syncthreads(); });
+}
+
+// Persistent variant: each CTA walks subcarriers blockIdx.x, +gridDim.x, ...
+// and bulk-copies the next one's G + matched filters (one contiguous
+// workspace span) into a second shared-memory buffer while solving the
+// current one, so the per-subcarrier load latency leaves the critical path.
+__host__ __device__ inline int k2_pre_bytes(int UP, int S) {
+  return ((UP * UP + S * UP + 2) * 8 + 127) & ~127;
+}
+
+template <int UP, bool EXACT, int MINB = 3>
+__global__ void __launch_bounds__(256, MINB) solve_kernel_pf(const KernelParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  WsOffsets W;
+  W.plan(UP, p.S, p.K, EXACT);
+  const int pb = k2_pre_bytes(UP, p.S);
+  const uint32_t bytes = static_cast<uint32_t>(W.cd * 8);  // G + MF
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  float2* buf[2] = {reinterpret_cast<float2*>(smem + 128), reinterpret_cast<float2*>(smem + 128 + pb)};
+  unsigned char* rest = smem + 128 + 2 * pb;
+  const long n_local = p.n_sc > blockIdx.x ? (p.n_sc - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  __syncthreads();
+  auto issue = [&](long i) {
+    const long lsc = blockIdx.x + i * gridDim.x;
+    fence_proxy_async();  // generic reads of this buffer (two uses ago) before the async write
+    mbar_expect_tx(bar + (i & 1), bytes);
+    bulk_g2s(buf[i & 1], p.ws + lsc * W.stride, bytes, bar + (i & 1));
+  };
+  if (threadIdx.x == 0 && n_local > 0) issue(0);
+  for (long i = 0; i < n_local; ++i) {
+    if (threadIdx.x == 0 && i + 1 < n_local) issue(i + 1);
+    mbar_wait(bar + (i & 1), static_cast<uint32_t>((i >> 1) & 1));
+    solve_sc<UP, EXACT>(p, blockIdx.x + i * gridDim.x, rest, blockDim.x, [] { __syncthreads(); },
+                        buf[i & 1]);
+    __syncthreads();
+  }
 }
 
 }  // namespace cgm
