@@ -60,13 +60,13 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // alias the staged channel when it is large enough (it is dead once the
 // Gram matrix and matched filters are formed; the precoder restages it).
 struct AltSmem {
-  int hs, a, g, inv, term, next, mf, xs, vec, part, red, total;
+  int hs, a, g, inv, term, next, mf, xs, vec, red, total;
   bool alias;
   __host__ __device__ void plan(int B, int U, int S, int method) {
     const int UU = U * U;
     const bool mat = method != kCgls, neu = method == kNeumann;
     int o = 0;
-    hs = o;   o += B * U;             // H_u [b][u] (downlink: conj(H_d)^T)
+    hs = o;   o += B * (mat ? U : U + 1);  // H_u [b][u] (downlink: conj(H_d)^T), row stride U (+1 CGLS)
     a = o;    o += mat ? UU : 0;      // A = G + reg I (Cholesky: then L in place)
     g = o;    o += neu ? UU : 0;      // unregularised Gram G (Neumann mu)
     inv = o;  o += mat ? UU : 0;      // A^-1 (Cholesky) / Neumann sum
@@ -75,8 +75,7 @@ struct AltSmem {
     next = alias ? hs + UU : o; o += (neu && !alias) ? UU : 0;
     mf = o;   o += S * U;             // matched filters / transmit vectors per system
     xs = o;   o += S * U;             // equalised outputs per system
-    vec = o;  o += 3 * B + 8 * U;     // CGLS vectors (x, r, d, q, s, w) + 6 U floats
-    part = o; o += NT;                // partial sums of H^H r
+    vec = o;  o += (mat ? B : NW * (B + U)) + 2 * U;  // q [B] / CGLS per-warp r|w [B], d [U]; 3 U floats
     red = o;  o += NW;                // block reduction
     total = o;
   }
@@ -89,29 +88,6 @@ __device__ __forceinline__ void mv(const float2* Hs, int B, int U, const float2*
     for (int u = 0; u < U; ++u) acc = cadd(acc, cmul(Hs[b * U + u], v[u]));
     out[b] = acc;
   }
-}
-
-// out[u] = sum_b conj(Hs[b][u]) r[b] (+ extra[u] when given), split over
-// NT / U parts of b, partials in `part`
-__device__ __forceinline__ void mvh(const float2* Hs, int B, int U, const float2* r, float2* out,
-                                    float2* part, float aug = 0.f, const float2* r_aug = nullptr) {
-  const int P = NT / U > 0 ? NT / U : 1;
-  const int chunk = (B + P - 1) / P;
-  for (int e = threadIdx.x; e < P * U; e += NT) {
-    const int pp = e / U, u = e - pp * U;
-    const int b0 = pp * chunk, b1 = min(B, b0 + chunk);
-    float2 acc = make_float2(0.f, 0.f);
-    for (int b = b0; b < b1; ++b) acc = cadd(acc, cmulc(Hs[b * U + u], r[b]));
-    part[e] = acc;
-  }
-  __syncthreads();
-  for (int u = threadIdx.x; u < U; u += NT) {
-    float2 acc = make_float2(0.f, 0.f);
-    for (int pp = 0; pp < P; ++pp) acc = cadd(acc, part[pp * U + u]);
-    if (r_aug) acc = cadd(acc, cscale(aug, r_aug[u]));
-    out[u] = acc;
-  }
-  __syncthreads();
 }
 
 // G = Hs^H Hs (one triangle + conjugate mirror, real diagonal:
@@ -298,6 +274,243 @@ __device__ __forceinline__ void put_detect(const KernelParams& p, long sc, int s
   }
 }
 
+// ---------------------------------------------------------------- CGLS
+// One warp per system: lane l owns users u = l + 32m (m < 2, U <= 64) and
+// antenna rows b = l + 32k.  H sits in shared memory with row stride U + 1,
+// so both the row reads of H d (lane <-> row) and the column reads of H^H r
+// (lane <-> user) are conflict-free; the vector each product broadcasts
+// (d, or r / w) goes through the warp's own shared-memory slot.
+constexpr int kRU = 2;  // users per lane
+constexpr int kRB = 8;  // antenna rows per lane (B <= 256)
+
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// detect_cgls (detect.cpp:238-272): cgls_solve_regularized (solvers.cpp:
+// 141-194) on [H; sqrt(rho^-1) I] over cgls_core (:87-139), the approximate
+// tracker on the Gram diagonal, extraction (detect.cpp:430-441).
+__device__ void cgls_detect_warps(const KernelParams& p, long sc, const float2* Hs, int HS,
+                                  float2* V, const float* gdg, const float* adg, float reg) {
+  const int B = p.B, U = p.U, S = p.S, K = p.K;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  float2* rv = V + w * (B + U);  // residual rows [B]
+  float2* dv = rv + B;           // direction [U]
+  const float aug = sqrtf(reg);
+  for (int s = w; s < S; s += NW) {
+    float2 x[kRU], d[kRU], ra[kRU];  // solution, direction, residual tail (identity block)
+    float f0[kRU], f1[kRU], f2[kRU];
+    for (int k = 0; k < kRB; ++k) {
+      const int b = l + 32 * k;
+      if (b < B) rv[b] = p.Y[(sc * B + b) * static_cast<long>(S) + s];
+    }
+    __syncwarp();
+    float gs = 0.f;
+#pragma unroll
+    for (int m = 0; m < kRU; ++m) {
+      const int u = l + 32 * m;
+      x[m] = d[m] = ra[m] = make_float2(0.f, 0.f);
+      f0[m] = f1[m] = f2[m] = 0.f;
+      if (u < U) {  // first adjoint: the matched filter H^H y
+        float2 acc = make_float2(0.f, 0.f);
+        for (int b = 0; b < B; ++b) acc = cadd(acc, cmulc(Hs[b * HS + u], rv[b]));
+        d[m] = acc;
+        dv[u] = acc;
+        gs += cabs2(acc);
+      }
+    }
+    float gamma = warp_sum(gs);
+    const float gamma0 = gamma;
+    float am1 = 1.f, am2 = 1.f, bm1 = 0.f, bm2 = 0.f;
+    bool broke = false;
+    for (int k = 1; k <= K; ++k) {
+      float alpha = 1.f, beta = 0.f;
+      if (!(gamma <= 1e-28f * gamma0)) {
+        __syncwarp();
+        float2 q[kRB];
+        float qs = 0.f;
+#pragma unroll
+        for (int kb = 0; kb < kRB; ++kb) {
+          const int b = l + 32 * kb;
+          q[kb] = make_float2(0.f, 0.f);
+          if (b < B) {
+            const float2* hr = Hs + b * HS;
+            for (int u = 0; u < U; ++u) q[kb] = cadd(q[kb], cmul(hr[u], dv[u]));
+            qs += cabs2(q[kb]);
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < kRU; ++m)
+          if (l + 32 * m < U) qs += aug * aug * cabs2(d[m]);
+        const float qn2 = warp_sum(qs);
+        if (qn2 < 1e-30f) {  // solvers.cpp:115-116
+          broke = true;
+          break;
+        }
+        alpha = gamma / qn2;
+#pragma unroll
+        for (int m = 0; m < kRU; ++m) {
+          x[m] = cadd(x[m], cscale(alpha, d[m]));
+          ra[m] = csub(ra[m], cscale(alpha * aug, d[m]));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int kb = 0; kb < kRB; ++kb) {
+          const int b = l + 32 * kb;
+          if (b < B) rv[b] = csub(rv[b], cscale(alpha, q[kb]));
+        }
+        __syncwarp();
+        float gn = 0.f;
+        float2 sv[kRU];
+#pragma unroll
+        for (int m = 0; m < kRU; ++m) {
+          const int u = l + 32 * m;
+          sv[m] = make_float2(0.f, 0.f);
+          if (u < U) {
+            float2 acc = cscale(aug, ra[m]);
+            for (int b = 0; b < B; ++b) acc = cadd(acc, cmulc(Hs[b * HS + u], rv[b]));
+            sv[m] = acc;
+            gn += cabs2(acc);
+          }
+        }
+        gn = warp_sum(gn);
+        beta = gn / gamma;
+        gamma = gn;
+#pragma unroll
+        for (int m = 0; m < kRU; ++m) {
+          const int u = l + 32 * m;
+          d[m] = cadd(sv[m], cscale(beta, d[m]));
+          if (u < U) dv[u] = d[m];
+        }
+      }
+      // ApproxSinrTracker::step (detect.cpp:400-428)
+#pragma unroll
+      for (int m = 0; m < kRU; ++m) {
+        const int u = l + 32 * m;
+        float nx = alpha;
+        if (k > 1 && u < U) {
+          const float c1 = alpha * (1.f + bm1) / am1, c2 = alpha * bm2 / am2;
+          nx = f0[m] + (c1 - alpha * adg[u]) * (f0[m] - f1[m]) - c2 * (f1[m] - f2[m]);
+        }
+        f2[m] = f1[m];
+        f1[m] = f0[m];
+        f0[m] = nx;
+      }
+      am2 = am1; am1 = alpha; bm2 = bm1; bm1 = beta;
+    }
+#pragma unroll
+    for (int m = 0; m < kRU; ++m) {
+      const int u = l + 32 * m;
+      if (u < U)
+        put_detect(p, sc, s, u, x[m], f0[m] * gdg[u], p.n0 > 0.f ? gdg[u] / p.n0 : 0.f, !broke);
+    }
+    if (l == 0 && p.status) p.status[sc * S + s] = broke ? 1 : 0;
+    __syncwarp();
+  }
+}
+
+// precode_cgls (precode.cpp:73-82): cgls_solve_min_norm (solvers.cpp:196-235),
+// q accumulated as x += alpha H_d^H p, then normalize (precode.cpp:22-36).
+__device__ void cgls_precode_warps(const KernelParams& p, long sc, const float2* Hs, int HS,
+                                   float2* V, float reg) {
+  const int B = p.B, U = p.U, S = p.St, K = p.Kt;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  float2* wv = V + w * (B + U);  // w = H_d^H p [B]
+  float2* dv = wv + B;           // direction [U]
+  for (int s = w; s < S; s += NW) {
+    float2 r[kRU], d[kRU], x[kRB];
+    float rs = 0.f;
+#pragma unroll
+    for (int m = 0; m < kRU; ++m) {
+      const int u = l + 32 * m;
+      r[m] = u < U ? p.T[(sc * S + s) * static_cast<long>(U) + u] : make_float2(0.f, 0.f);
+      d[m] = r[m];
+      if (u < U) dv[u] = d[m];
+      rs += cabs2(r[m]);
+    }
+#pragma unroll
+    for (int kb = 0; kb < kRB; ++kb) x[kb] = make_float2(0.f, 0.f);
+    float rn2 = warp_sum(rs);
+    const float rn0 = rn2;
+    bool broke = false;
+    for (int k = 1; k <= K; ++k) {
+      if (rn2 <= 1e-28f * rn0) continue;  // frozen (solvers.cpp:25-27)
+      __syncwarp();
+      float2 wr[kRB];
+#pragma unroll
+      for (int kb = 0; kb < kRB; ++kb) {
+        const int b = l + 32 * kb;
+        wr[kb] = make_float2(0.f, 0.f);
+        if (b < B) {
+          const float2* hr = Hs + b * HS;
+          for (int u = 0; u < U; ++u) wr[kb] = cadd(wr[kb], cmul(hr[u], dv[u]));
+          wv[b] = wr[kb];
+        }
+      }
+      __syncwarp();
+      float2 e[kRU];
+      float cs = 0.f;
+#pragma unroll
+      for (int m = 0; m < kRU; ++m) {
+        const int u = l + 32 * m;
+        e[m] = make_float2(0.f, 0.f);
+        if (u < U) {
+          float2 acc = cscale(reg, d[m]);
+          for (int b = 0; b < B; ++b) acc = cadd(acc, cmulc(Hs[b * HS + u], wv[b]));
+          e[m] = acc;
+          cs += cmulc(d[m], acc).x;
+        }
+      }
+      const float curv = warp_sum(cs);
+      if (curv < 1e-30f) {  // solvers.cpp:217-218
+        broke = true;
+        break;
+      }
+      const float alpha = rn2 / curv;
+#pragma unroll
+      for (int kb = 0; kb < kRB; ++kb) x[kb] = cadd(x[kb], cscale(alpha, wr[kb]));
+      float rsn = 0.f;
+#pragma unroll
+      for (int m = 0; m < kRU; ++m) {
+        r[m] = csub(r[m], cscale(alpha, e[m]));
+        rsn += cabs2(r[m]);
+      }
+      const float rn = warp_sum(rsn);
+      const float beta = rn / rn2;
+      rn2 = rn;
+#pragma unroll
+      for (int m = 0; m < kRU; ++m) {
+        const int u = l + 32 * m;
+        d[m] = cadd(r[m], cscale(beta, d[m]));
+        if (u < U) dv[u] = d[m];
+      }
+    }
+    float qs = 0.f;
+#pragma unroll
+    for (int kb = 0; kb < kRB; ++kb) qs += cabs2(x[kb]);
+    const float gain = sqrtf(warp_sum(qs));
+    const bool zero = gain < 1e-30f;
+    const long o = (sc * S + s) * static_cast<long>(B);
+#pragma unroll
+    for (int kb = 0; kb < kRB; ++kb) {
+      const int b = l + 32 * kb;
+      if (b >= B) continue;
+      const float2 qv = broke ? make_float2(0.f, 0.f) : x[kb];
+      if (p.q) p.q[o + b] = qv;
+      if (p.s_out) p.s_out[o + b] = (broke || zero) ? make_float2(0.f, 0.f) : cscale(1.f / gain, qv);
+    }
+    if (l == 0) {
+      if (p.gain) p.gain[sc * S + s] = (broke || zero) ? 0.f : gain;
+      if (p.pstatus) p.pstatus[sc * S + s] = broke ? 1 : (zero ? 2 : 0);
+    }
+    __syncwarp();
+  }
+}
+
+// One instantiation per method (M = sim::Method): each gets its own register
+// allocation (the CGLS warps hold 8 antenna rows per lane in registers).
+template <int M>
 __global__ void __launch_bounds__(NT) alt_kernel(const KernelParams p) {
   extern __shared__ float2 sm[];
   const bool down = p.St > 0;
@@ -305,7 +518,8 @@ __global__ void __launch_bounds__(NT) alt_kernel(const KernelParams p) {
   const int K = down ? p.Kt : p.K;
   const float reg = down ? p.rho_inv_d : p.rho_inv_u;
   AltSmem L;
-  L.plan(B, U, S, p.method);
+  L.plan(B, U, S, M);
+  const int HS = M == kCgls ? U + 1 : U;  // staged row stride of H
   float2* Hs = sm + L.hs;
   float2* A = sm + L.a;
   float2* G = sm + L.g;
@@ -315,23 +529,14 @@ __global__ void __launch_bounds__(NT) alt_kernel(const KernelParams p) {
   float2* MF = sm + L.mf;
   float2* XS = sm + L.xs;
   float2* V = sm + L.vec;
-  float2* part = sm + L.part;
   float* red = reinterpret_cast<float*>(sm + L.red);
-  // CGLS vectors: x[U], r[B + U], d[U], q[B + U], s[U], w[B]; then 6 x U
-  // floats: tracker filt, filt_m1, filt_m2, a_diag, g_diag, 1 / diag
-  float2* vx = V;
-  float2* vr = vx + U;
-  float2* vd = vr + B + U;
-  float2* vq = vd + U;
-  float2* vs = vq + B + U;
-  float2* vw = vs + U;
-  float* fl = reinterpret_cast<float*>(vw + B);
-  float* f0 = fl;
-  float* f1 = fl + U;
-  float* f2 = fl + 2 * U;
-  float* adg = fl + 3 * U;
-  float* gdg = fl + 4 * U;
-  float* dinv = fl + 5 * U;
+  // CGLS: per-warp slots V[w (B + U) ..] (cgls_*_warps); explicit / Neumann
+  // precoding: q = H_d^H v in V[0 .. B); then 3 x U floats: a_diag, g_diag, 1 / diag
+  float2* vq = V;
+  float* fl = reinterpret_cast<float*>(V + (M == kCgls ? NW * (B + U) : B));
+  float* adg = fl;
+  float* gdg = fl + U;
+  float* dinv = fl + 2 * U;
 
   for (long sc = blockIdx.x; sc < p.n_sc; sc += gridDim.x) {
     // ---- stage H_u (downlink: H_u = H_d^H)
@@ -341,79 +546,35 @@ __global__ void __launch_bounds__(NT) alt_kernel(const KernelParams p) {
         for (int e = threadIdx.x; e < U * B; e += NT) {
           const int u = e / B, b = e - u * B;
           const float2 h = src[e];
-          Hs[b * U + u] = make_float2(h.x, -h.y);
+          Hs[b * HS + u] = make_float2(h.x, -h.y);
         }
       } else {
         const float2* src = p.H + sc * static_cast<long>(B) * U;
-        for (int e = threadIdx.x; e < U * B; e += NT) Hs[e] = src[e];
+        if (HS == U) {
+          for (int e = threadIdx.x; e < U * B; e += NT) Hs[e] = src[e];
+        } else {
+          for (int e = threadIdx.x; e < U * B; e += NT) {
+            const int b = e / U, u = e - b * U;
+            Hs[b * HS + u] = src[e];
+          }
+        }
       }
       __syncthreads();
     };
     stage_h();
     if (!down) {
       // ================================================= detection
-      if (p.method == kCgls) {
+      if (M == kCgls) {
         // only the Gram diagonal (detect.cpp:249-256)
         for (int i = threadIdx.x; i < U; i += NT) {
           float d = 0.f;
-          for (int b = 0; b < B; ++b) d += cabs2(Hs[b * U + i]);
+          for (int b = 0; b < B; ++b) d += cabs2(Hs[b * HS + i]);
           gdg[i] = d;
           adg[i] = d + reg;
         }
         __syncthreads();
-        const float aug = sqrtf(reg);
-        for (int s = 0; s < S; ++s) {
-          // cgls_solve_regularized (solvers.cpp:141-194) over cgls_core (:87-139)
-          for (int b = threadIdx.x; b < B + U; b += NT) {
-            vr[b] = b < B ? p.Y[(sc * B + b) * static_cast<long>(S) + s] : make_float2(0.f, 0.f);
-          }
-          for (int i = threadIdx.x; i < U; i += NT) {
-            vx[i] = make_float2(0.f, 0.f);
-            f0[i] = f1[i] = f2[i] = 0.f;
-          }
-          __syncthreads();
-          mvh(Hs, B, U, vr, vs, part);  // first adjoint: the matched filter
-          for (int i = threadIdx.x; i < U; i += NT) vd[i] = vs[i];
-          float gsum = 0.f;
-          for (int i = threadIdx.x; i < U; i += NT) gsum += cabs2(vs[i]);
-          float gamma = block_sum(gsum, red);
-          const float gamma0 = gamma;
-          Tracker tr;
-          bool broke = false;
-          for (int k = 1; k <= K && !broke; ++k) {
-            float alpha = 1.f, beta = 0.f;
-            if (!(gamma <= 1e-28f * gamma0)) {
-              mv(Hs, B, U, vd, vq);
-              for (int i = threadIdx.x; i < U; i += NT) vq[B + i] = cscale(aug, vd[i]);
-              __syncthreads();
-              float qs = 0.f;
-              for (int b = threadIdx.x; b < B + U; b += NT) qs += cabs2(vq[b]);
-              const float qn2 = block_sum(qs, red);
-              if (qn2 < 1e-30f) {  // solvers.cpp:115-116
-                broke = true;
-                break;
-              }
-              alpha = gamma / qn2;
-              for (int i = threadIdx.x; i < U; i += NT) vx[i] = cadd(vx[i], cscale(alpha, vd[i]));
-              for (int b = threadIdx.x; b < B + U; b += NT) vr[b] = csub(vr[b], cscale(alpha, vq[b]));
-              __syncthreads();
-              mvh(Hs, B, U, vr, vs, part, aug, vr + B);
-              float gs = 0.f;
-              for (int i = threadIdx.x; i < U; i += NT) gs += cabs2(vs[i]);
-              const float gn = block_sum(gs, red);
-              beta = gn / gamma;
-              gamma = gn;
-              for (int i = threadIdx.x; i < U; i += NT) vd[i] = cadd(vs[i], cscale(beta, vd[i]));
-              __syncthreads();
-            }
-            tr.step(f0, f1, f2, adg, U, alpha, beta);
-          }
-          // ApproxSinrTracker::extract (detect.cpp:430-441)
-          for (int i = threadIdx.x; i < U; i += NT)
-            put_detect(p, sc, s, i, vx[i], f0[i] * gdg[i], p.n0 > 0.f ? gdg[i] / p.n0 : 0.f, !broke);
-          if (threadIdx.x == 0 && p.status) p.status[sc * S + s] = broke ? 1 : 0;
-          __syncthreads();
-        }
+        cgls_detect_warps(p, sc, Hs, HS, V, gdg, adg, reg);
+        __syncthreads();
         continue;
       }
       gram(Hs, B, U, reg, G, A);
@@ -427,7 +588,7 @@ __global__ void __launch_bounds__(NT) alt_kernel(const KernelParams p) {
       }
       __syncthreads();
       bool ok;
-      if (p.method == kCholesky) {
+      if (M == kCholesky) {
         ok = cholesky_inverse(A, Inv, U);
         apply(Inv, MF, XS, U, S);  // xhat_s = A^-1 b_s (detect.cpp:145-152)
         __syncthreads();
@@ -476,70 +637,16 @@ __global__ void __launch_bounds__(NT) alt_kernel(const KernelParams p) {
     }
     // =================================================== precoding
     const long ob = static_cast<long>(B);
-    if (p.method == kCgls) {
-      // cgls_solve_min_norm (solvers.cpp:196-235): x = H_d^H inner
-      for (int s = 0; s < S; ++s) {
-        for (int i = threadIdx.x; i < U; i += NT) {
-          const float2 t = p.T[(sc * S + s) * static_cast<long>(U) + i];
-          vr[i] = t;
-          vd[i] = t;
-        }
-        for (int b = threadIdx.x; b < B; b += NT) vq[b] = make_float2(0.f, 0.f);  // x
-        __syncthreads();
-        float rs = 0.f;
-        for (int i = threadIdx.x; i < U; i += NT) rs += cabs2(vr[i]);
-        float rn2 = block_sum(rs, red);
-        const float rn0 = rn2;
-        bool broke = false;
-        for (int k = 1; k <= K; ++k) {
-          if (rn2 <= 1e-28f * rn0) continue;  // frozen (solvers.cpp:25-27)
-          mv(Hs, B, U, vd, vw);  // w = H_d^H p
-          __syncthreads();
-          mvh(Hs, B, U, vw, vs, part, reg, vd);  // e = H_d w + rho^-1 p
-          float cs = 0.f;
-          for (int i = threadIdx.x; i < U; i += NT) cs += cmulc(vd[i], vs[i]).x;
-          const float curv = block_sum(cs, red);
-          if (curv < 1e-30f) {  // solvers.cpp:217-218
-            broke = true;
-            break;
-          }
-          const float alpha = rn2 / curv;
-          for (int b = threadIdx.x; b < B; b += NT) vq[b] = cadd(vq[b], cscale(alpha, vw[b]));
-          for (int i = threadIdx.x; i < U; i += NT) vr[i] = csub(vr[i], cscale(alpha, vs[i]));
-          __syncthreads();
-          float rs2 = 0.f;
-          for (int i = threadIdx.x; i < U; i += NT) rs2 += cabs2(vr[i]);
-          const float rn = block_sum(rs2, red);
-          const float beta = rn / rn2;
-          rn2 = rn;
-          for (int i = threadIdx.x; i < U; i += NT) vd[i] = cadd(vr[i], cscale(beta, vd[i]));
-          __syncthreads();
-        }
-        // normalize (precode.cpp:22-36)
-        float qs = 0.f;
-        for (int b = threadIdx.x; b < B; b += NT) qs += cabs2(vq[b]);
-        const float gain = sqrtf(block_sum(qs, red));
-        const bool zero = gain < 1e-30f;
-        const long o = (sc * S + s) * ob;
-        for (int b = threadIdx.x; b < B; b += NT) {
-          const float2 qv = broke ? make_float2(0.f, 0.f) : vq[b];
-          if (p.q) p.q[o + b] = qv;
-          if (p.s_out)
-            p.s_out[o + b] = (broke || zero) ? make_float2(0.f, 0.f) : cscale(1.f / gain, qv);
-        }
-        if (threadIdx.x == 0) {
-          if (p.gain) p.gain[sc * S + s] = (broke || zero) ? 0.f : gain;
-          if (p.pstatus) p.pstatus[sc * S + s] = broke ? 1 : (zero ? 2 : 0);
-        }
-        __syncthreads();
-      }
+    if (M == kCgls) {
+      cgls_precode_warps(p, sc, Hs, HS, V, reg);
+      __syncthreads();
       continue;
     }
     // explicit (Cholesky) / Neumann: v_s = A_d^-1 t_s, q_s = H_d^H v_s
     gram(Hs, B, U, reg, G, A);
     for (int e = threadIdx.x; e < S * U; e += NT) MF[e] = p.T[(sc * S) * static_cast<long>(U) + e];
     __syncthreads();
-    const bool ok = p.method == kCholesky ? cholesky_inverse(A, Inv, U)
+    const bool ok = M == kCholesky ? cholesky_inverse(A, Inv, U)
                                           : neumann_inverse(A, Inv, term, nxt, dinv, U, K);
     apply(Inv, MF, XS, U, S);  // v_s = A_d^-1 t_s
     __syncthreads();

@@ -373,7 +373,9 @@ int launch_alt(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
   if (smem > static_cast<size_t>(ctx->max_smem))
     return fail(ctx, CGM_EINVAL, "B = %d, U = %d: %zu bytes of shared memory per subcarrier exceed %d",
                 p.B, p.U, smem, ctx->max_smem);
-  auto k = cgm::alt::alt_kernel;
+  auto k = p.method == cgm::alt::kCholesky ? cgm::alt::alt_kernel<cgm::alt::kCholesky>
+           : p.method == cgm::alt::kCgls   ? cgm::alt::alt_kernel<cgm::alt::kCgls>
+                                           : cgm::alt::alt_kernel<cgm::alt::kNeumann>;
   CGM_CUDA(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int occ = 0;
   CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, cgm::alt::NT, smem));

@@ -669,6 +669,7 @@ __global__ void __launch_bounds__(NT, 2) subcarrier_kernel(const KernelParams p)
           }
           // approx uplink: mu = Ltilde G_ii, rho = G_ii / N0 (detect.cpp:435-441)
           // then the LLR epilogue and stores straight from the lane
+          if constexpr (!EXACT)
 #pragma unroll
           for (int m = 0; m < RU; ++m) {
             const int u = gl + m * G;

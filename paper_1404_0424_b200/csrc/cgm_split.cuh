@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p
   float2* Tm = T1 + UP * UP;
   float* misc = reinterpret_cast<float*>(smem + L.misc);
   const int nt = blockDim.x;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int B = p.B, S = p.S, U = p.U;
   const int nb = UP / 4, n_gram = nb * (nb + 1) / 2, nsb = (S + 3) / 4;
   const int n_tiles = n_gram + nb * nsb;
@@ -835,6 +835,7 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
         }
         // approx uplink: mu = Ltilde G_ii, rho = G_ii / N0 (detect.cpp:435-441),
         // LLRs and stores straight from the lane
+        if constexpr (!EXACT)
 #pragma unroll
         for (int m = 0; m < RU; ++m) {
           const int u = gl + m * G;
