@@ -349,12 +349,19 @@ __global__ void __launch_bounds__(32 * kVitWarps) viterbi_decode(
   const double* L = coded + cw * coded_len;
   uint2* D = dec + cw * total;
   double* sl = stage[wib];
-  // branch outputs (a << 1 | b) for (pred 2k or 2k+1) x (input 0 or 1)
-  unsigned o[2][2];
+  // branch metric of (pred 2k+q, input u) = (+-la) + (+-lb) with the signs of
+  // its output bits (a, b) -- the reference's bm[(a << 1) | b] table
+  // (coding.cpp:114-116) -- formed as fma(lb, sb, la * sa): the product by
+  // +-1 is exact, so it rounds once, exactly like the table's addition.  (An
+  // indexed bm[4] table would live in local memory: lane-dependent index.)
+  double sa[2][2], sb[2][2];
+#pragma unroll
   for (int q = 0; q < 2; ++q)
+#pragma unroll
     for (int u = 0; u < 2; ++u) {
       const unsigned word = (static_cast<unsigned>(u) << kTail) | static_cast<unsigned>(2 * lane + q);
-      o[q][u] = (parity(word & kGenA) << 1) | parity(word & kGenB);
+      sa[q][u] = parity(word & kGenA) ? 1.0 : -1.0;
+      sb[q][u] = parity(word & kGenB) ? 1.0 : -1.0;
     }
   const double ninf = -static_cast<double>(INFINITY);
   double m0 = lane == 0 ? 0.0 : ninf;  // state lane
@@ -391,16 +398,17 @@ __global__ void __launch_bounds__(32 * kVitWarps) viterbi_decode(
       constexpr int offB[5] = {1, -1, 3, -1, 5};
       const double la = offA[ph] >= 0 ? lv[offA[ph] < 0 ? 0 : offA[ph]] : 0.0;
       const double lb = offB[ph] >= 0 ? lv[offB[ph] < 0 ? 0 : offB[ph]] : 0.0;
-      const double bm[4] = {-la - lb, -la + lb, la - lb, la + lb};
       // metrics of states 2k and 2k+1 (lane (2k)&31, half (2k)>>5)
       const double a0 = __shfl_sync(0xffffffffu, m0, src0), a1 = __shfl_sync(0xffffffffu, m1, src0);
       const double b0 = __shfl_sync(0xffffffffu, m0, src1), b1 = __shfl_sync(0xffffffffu, m1, src1);
       const double p0 = upper ? a1 : a0, p1 = upper ? b1 : b0;
-      const double c00 = p0 + bm[o[0][0]], c10 = p1 + bm[o[1][0]];
+      const double bm00 = fma(lb, sb[0][0], la * sa[0][0]), bm10 = fma(lb, sb[1][0], la * sa[1][0]);
+      const double bm01 = fma(lb, sb[0][1], la * sa[0][1]), bm11 = fma(lb, sb[1][1], la * sa[1][1]);
+      const double c00 = p0 + bm00, c10 = p1 + bm10;
       const bool d0 = c10 > c00;
       const double n0 = d0 ? c10 : c00;
       // next state lane + 32 (input 1) is not reachable in the tail
-      const double c01 = p0 + bm[o[0][1]], c11 = p1 + bm[o[1][1]];
+      const double c01 = p0 + bm01, c11 = p1 + bm11;
       const bool d1 = c11 > c01;
       const double n1 = tt < info_len ? (d1 ? c11 : c01) : ninf;
       const unsigned w0 = __ballot_sync(0xffffffffu, d0), w1 = __ballot_sync(0xffffffffu, d1);
