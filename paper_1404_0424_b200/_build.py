@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -42,13 +43,17 @@ def build(verbose: bool = False) -> str:
     hdeps = [os.path.join(CSRC, h) for h in HDRS] + [os.path.join(ROOT, "include", "cgmimo_b200.h")]
     objs = []
     log = ""
+    jobs = []
     for src in CU:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src + ".o")
         objs.append(o)
         if _newer(o, [s] + hdeps + [__file__]):
-            log += _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v",
+            jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v",
                          "-Xcompiler", "-fPIC", *inc, "-c", s, "-o", o])
+    with ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:  # translation units in parallel
+        for out in ex.map(_run, jobs):
+            log += out
     for src in CPP:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src + ".o")

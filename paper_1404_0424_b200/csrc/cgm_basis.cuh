@@ -1,0 +1,170 @@
+// cgm_basis.cuh -- the exact tracker's Chebyshev basis as its own kernel.
+//
+// The exact SINR tracker (detect.cpp:330-395) needs, per subcarrier, the
+// matrices T_1..T_K of Ahat = (A - cI)/d, A = G + rho^-1 I (cgm_split.cuh
+// explains the basis argument): (K - 1) Hermitian U x U products
+//   T_{m+1} = 2 Ahat T_m - T_{m-1},  T_0 = I,
+// which dominate the FLOPs of the exact configurations (cfg4: U^3 per
+// product against U^2 B for the Gram).  Inside the channel kernels they ran
+// on the 8 epilogue warps of a one-CTA-per-SM tensor-core pipeline; here
+// they get a kernel of their own, sized for the FP32 pipe:
+//   * one thread per 4 x 4 tile of the LOWER triangle (the product of two
+//     commuting Hermitian matrices is Hermitian; the upper triangle is the
+//     conjugate mirror), (UP/4)(UP/4 + 1)/2 tiles per subcarrier;
+//   * Ahat, T_m, T_{m-1} of each subcarrier in shared memory; per k the
+//     thread reads four entries of row k of Ahat (= conj of column k, the
+//     matrix is Hermitian) and four of row k of T_m (two LDS.128 each) and
+//     issues 32 packed FFMA2:
+//       a += (t.x, t.y) * ahat.x,  b += (t.x, t.y) * ahat.y,
+//       conj(ahat) t = (a.x + b.y, a.y - b.x);
+//   * U = 32: three subcarriers per 128-thread CTA (108 busy threads),
+//     U = 64: one per 160-thread CTA (136 busy).
+// The centre / half-width (c, d) comes from the same power iteration as
+// before (cheb_interval, one warp per subcarrier).  Output: (c, d) and
+// T_1..T_K in the workspace, the layout K2's extraction reads.
+#pragma once
+
+#include "cgm_rows32.cuh"  // f2dup_lo / f2dup_hi
+
+namespace cgm {
+
+template <int UP>
+struct BasisGeo {
+  static constexpr int NB = UP / 4;                  // tile rows
+  static constexpr int NTILE = NB * (NB + 1) / 2;    // lower-triangle tiles
+  static constexpr int SPC = UP == 32 ? 3 : 1;       // subcarriers per CTA
+  static constexpr int NT = ((SPC * NTILE + 31) / 32) * 32;
+  static constexpr int LD = UP + 2;                  // padded row (bank spread, 16 B aligned)
+  static constexpr int MAT = UP * LD;                // float2 per matrix in smem
+  static constexpr int SMEM = SPC * 3 * MAT * 8;     // Ahat, T_m, T_{m-1}
+};
+
+template <int UP>
+__global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 3 : 2) basis_kernel(const KernelParams p) {
+  using BG = BasisGeo<UP>;
+  constexpr int MAT = BG::MAT, SPC = BG::SPC, LD = BG::LD;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float2* base = reinterpret_cast<float2*>(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = p.K;
+  WsOffsets W;
+  W.plan(UP, p.S, K, true);
+  const long sc0 = static_cast<long>(blockIdx.x) * SPC;
+  const int nsc = static_cast<int>(p.n_sc - sc0 < SPC ? p.n_sc - sc0 : SPC);
+  auto Ah = [&](int s) { return base + (s * 3 + 0) * MAT; };
+  // --------------------------------------------------------------- G in
+  // (padded smem matrix) <-> (dense UP x UP workspace matrix), float4 = 2 entries
+  auto load = [&](float2* dst, const float2* src) {
+    for (int e = tid; e < UP * UP / 2; e += BG::NT) {
+      const int r = e / (UP / 2), c2 = e - r * (UP / 2);
+      *reinterpret_cast<float4*>(dst + r * LD + 2 * c2) = reinterpret_cast<const float4*>(src)[e];
+    }
+  };
+  auto store = [&](float2* dst, const float2* src) {
+    for (int e = tid; e < UP * UP / 2; e += BG::NT) {
+      const int r = e / (UP / 2), c2 = e - r * (UP / 2);
+      reinterpret_cast<float4*>(dst)[e] = *reinterpret_cast<const float4*>(src + r * LD + 2 * c2);
+    }
+  };
+  for (int s = 0; s < nsc; ++s) load(Ah(s), p.ws + (sc0 + s) * W.stride + W.g);
+  __syncthreads();
+  // ------------------------------------- (c, d) by power iteration, warp s
+  __shared__ float2 cds[SPC];
+  if (warp < nsc) {
+    const float2 cd = cheb_interval<UP, LD>(Ah(warp), p.rho_inv_u, base + (warp * 3 + 1) * MAT, lane);
+    if (lane == 0) {
+      cds[warp] = cd;
+      p.ws[(sc0 + warp) * W.stride + W.cd] = cd;
+    }
+  }
+  __syncthreads();
+  // --------------------------------------- T_1 = Ahat = (A - cI)/d, in place
+  for (int s = 0; s < nsc; ++s) {
+    const float cc = cds[s].x, invd = 1.f / cds[s].y;
+    float2* a = Ah(s);
+    float2* Tw = p.ws + (sc0 + s) * W.stride + W.t;
+    for (int e = tid; e < UP * UP; e += BG::NT) {
+      const int r = e / UP, c = e - r * UP;
+      float2 v = a[r * LD + c];
+      if (r == c) v.x += p.rho_inv_u - cc;
+      v = cscale(invd, v);
+      a[r * LD + c] = v;
+      Tw[e] = v;
+    }
+  }
+  __syncthreads();
+  // ------------------------------------------------------------ products
+  const int slot = tid / BG::NTILE;
+  const int tile = tid - slot * BG::NTILE;
+  int rb = 0;
+  while ((rb + 1) * (rb + 2) / 2 <= tile) ++rb;
+  const int cb = tile - rb * (rb + 1) / 2;
+  const bool busy = slot < nsc;
+  const int i0 = rb * 4, j0 = cb * 4;
+  const float2* A = base + (slot * 3 + 0) * MAT;
+  // T_m in buffer `cur`, T_{m-1} in `prv` (1 and 2 alternate)
+  int cur = 0, prv = 1;  // cur 0 == Ahat itself for m = 1
+  for (int m = 1; m < K; ++m) {
+    if (busy) {
+      const float2* Tc = base + (slot * 3 + cur) * MAT;
+      unsigned long long a[4][4], b[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a[r][c] = b[r][c] = 0ull;
+#pragma unroll 2
+      for (int k = 0; k < UP; ++k) {
+        const ulonglong2 a01 = *reinterpret_cast<const ulonglong2*>(A + k * LD + i0);
+        const ulonglong2 a23 = *reinterpret_cast<const ulonglong2*>(A + k * LD + i0 + 2);
+        const ulonglong2 t01 = *reinterpret_cast<const ulonglong2*>(Tc + k * LD + j0);
+        const ulonglong2 t23 = *reinterpret_cast<const ulonglong2*>(Tc + k * LD + j0 + 2);
+        const unsigned long long ah[4] = {a01.x, a01.y, a23.x, a23.y};
+        const unsigned long long t[4] = {t01.x, t01.y, t23.x, t23.y};
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            ffma2(a[r][c], t[c], f2dup_lo(ah[r]));
+            ffma2(b[r][c], t[c], f2dup_hi(ah[r]));
+          }
+      }
+      // T_{m+1} = 2 Ahat T_m - T_{m-1} into the T_{m-1} buffer (lower +
+      // mirror; only this thread reads these lower entries of T_{m-1})
+      float2* Tn = base + (slot * 3 + (m == 1 ? 1 : prv)) * MAT;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int i = i0 + r, j = j0 + c;
+          if (j > i) continue;
+          const float2 A2 = f2unpack(a[r][c]), B2 = f2unpack(b[r][c]);
+          const float2 prod = make_float2(A2.x + B2.y, A2.y - B2.x);
+          const float2 prev = m == 1 ? make_float2(i == j ? 1.f : 0.f, 0.f) : Tn[i * LD + j];
+          float2 val = make_float2(2.f * prod.x - prev.x, 2.f * prod.y - prev.y);
+          if (i == j) val.y = 0.f;
+          Tn[i * LD + j] = val;
+          if (i != j) Tn[j * LD + i] = cconj(val);
+        }
+    }
+    __syncthreads();
+    {  // T_{m+1} -> workspace, coalesced
+      const int nb = m == 1 ? 1 : prv;
+      for (int s = 0; s < nsc; ++s)
+        store(p.ws + (sc0 + s) * W.stride + W.t + m * UP * UP, base + (s * 3 + nb) * MAT);
+    }
+    // rotate: T_{m+1} (just written) becomes current, T_m previous
+    const int nw = m == 1 ? 1 : prv;
+    prv = m == 1 ? 2 : cur;
+    cur = nw;
+    if (m == 1) {  // T_1 (= Ahat, buffer 0) must stay intact: copy it to buffer 2 as T_{m-1}
+      for (int s = 0; s < nsc; ++s) {
+        const float4* src = reinterpret_cast<const float4*>(Ah(s));
+        float4* dst = reinterpret_cast<float4*>(base + (s * 3 + 2) * MAT);
+        for (int e = tid; e < MAT / 2; e += BG::NT) dst[e] = src[e];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace cgm

@@ -18,6 +18,8 @@
 
 #include "../../include/cgmimo_b200.h"
 #include "cgm_alt.cuh"
+#include "cgm_basis.cuh"
+#include "cgm_rows32.cuh"
 #include "cgm_solve32.cuh"
 #include "cgm_tc.cuh"
 
@@ -46,6 +48,12 @@ struct cgm_ctx {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_log;  // kind, (start, stop)
   size_t ev_next = 0;
+  // per kernel: dynamic shared memory already granted, occupancy per (threads, smem)
+  struct KernInfo {
+    const void* fn;
+    int smem_set, nt, smem, occ;
+  };
+  std::vector<KernInfo> kinfo;
   std::string err;
 };
 
@@ -60,6 +68,10 @@ cudaEvent_t prof_event(cgm_ctx* ctx) {
   }
   return ctx->ev_pool[ctx->ev_next++];
 }
+
+// Environment overrides (A/B switches for the kernel variants; read per call
+// so tests can flip them inside one process).
+const char* env(const char* name) { return std::getenv(name); }
 
 int fail(cgm_ctx* ctx, int code, const char* fmt, ...) {
   char buf[512];
@@ -77,6 +89,41 @@ int fail(cgm_ctx* ctx, int code, const char* fmt, ...) {
     if (e_ != cudaSuccess)                                                         \
       return fail(ctx, CGM_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
                   __FILE__, __LINE__);                                             \
+  } while (0)
+
+// cudaFuncSetAttribute + occupancy query, cached per context: the two calls
+// cost tens of microseconds per launch otherwise (host-bound small batches).
+template <class F>
+int kern_prep(cgm_ctx* ctx, F* fn, int nt, int smem, int* occ) {
+  const void* key = reinterpret_cast<const void*>(fn);
+  cgm_ctx::KernInfo* ki = nullptr;
+  for (auto& k : ctx->kinfo)
+    if (k.fn == key) ki = &k;
+  if (!ki) {
+    ctx->kinfo.push_back({key, -1, -1, -1, 0});
+    ki = &ctx->kinfo.back();
+  }
+  if (smem > ki->smem_set) {
+    CGM_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ki->smem_set = smem;
+  }
+  if (occ) {
+    if (ki->nt != nt || ki->smem != smem) {
+      int o = 0;
+      CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, nt, smem));
+      ki->nt = nt;
+      ki->smem = smem;
+      ki->occ = o;
+    }
+    *occ = ki->occ;
+  }
+  return CGM_OK;
+}
+
+#define CGM_PREP(ctx, fn, nt, smem, occ)               \
+  do {                                                 \
+    const int rc_ = kern_prep(ctx, fn, nt, smem, occ); \
+    if (rc_) return rc_;                               \
   } while (0)
 
 unsigned gray_decode(unsigned g) {
@@ -130,9 +177,8 @@ int plan_and_launch(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
                 "per-subcarrier working set %d B exceeds shared memory (%d B): reduce B or S",
                 L.total, ctx->max_smem);
   auto kern = cgm::subcarrier_kernel<UP, NT, EXACT>;
-  CGM_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total));
   int occ = 0;
-  CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, L.total));
+  CGM_PREP(ctx, kern, NT, L.total, &occ);
   if (occ < 1) return fail(ctx, CGM_EINVAL, "kernel does not fit on an SM (smem %d)", L.total);
   long grid = std::min<long>(p.n_sc, static_cast<long>(occ) * ctx->sms);
   if (grid < 1) grid = 1;
@@ -188,7 +234,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   // the tensor cores (cgm_tc.cuh); CGMIMO_CHANNEL=ffma keeps the FFMA kernel
   bool use_tc = false;
   if constexpr (UP == 32) {
-    const char* force = std::getenv("CGMIMO_CHANNEL");
+    const char* force = env("CGMIMO_CHANNEL");
     if (cgm::tc::supported(p.U, p.B, p.S, p.use_tma) && !(force && std::strcmp(force, "ffma") == 0)) {
       cgm::tc::Smem T;
       int nstg = 3;
@@ -203,7 +249,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
         // approx 8 + 8 specialised, exact 8 unified (the basis products
         // then use all worker warps)
         int nep = 8, nsp = EXACT ? 0 : 8;
-        if (const char* w = std::getenv("CGMIMO_TC_WARPS")) std::sscanf(w, "%d,%d", &nep, &nsp);
+        if (const char* w = env("CGMIMO_TC_WARPS")) std::sscanf(w, "%d,%d", &nep, &nsp);
         if (nep == 16 && nsp == 0)
           k1 = cgm::channel_tc_kernel<EXACT, 16, 0>;
         else if (nep == 4 && nsp == 8)
@@ -216,7 +262,6 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       }
     }
   }
-  CGM_CUDA(ctx, cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));
   // K2: lane-per-row kernel by default; CGMIMO_SOLVE=tiles selects the
   // block-tiled FFMA2 CG (cgm_solve32.cuh, U = 32, >= 8 systems), which
   // issues ~25% fewer instructions but measured slower on cfg2 / cfg5 (lower
@@ -224,8 +269,8 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   bool use_s32 = false;
   int ts2 = 2;
   if constexpr (UP == 32) {
-    const char* force = std::getenv("CGMIMO_SOLVE");
-    if (const char* t = std::getenv("CGMIMO_SOLVE_TS")) ts2 = std::atoi(t) == 4 ? 4 : 2;
+    const char* force = env("CGMIMO_SOLVE");
+    if (const char* t = env("CGMIMO_SOLVE_TS")) ts2 = std::atoi(t) == 4 ? 4 : 2;
     cgm::S32Smem T2;
     T2.plan(p.B, p.S, p.St, Kmax, EXACT, ts2);
     if (p.S + p.St >= 8 && T2.total <= ctx->max_smem && force && std::strcmp(force, "tiles") == 0) {
@@ -241,7 +286,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   // from 24 systems; CGMIMO_SOLVE=pf / nopf force it either way
   bool use_pf = false;
   {
-    const char* force = std::getenv("CGMIMO_SOLVE");
+    const char* force = env("CGMIMO_SOLVE");
     const bool want = force ? std::strcmp(force, "pf") == 0
                             : (p.S + p.St >= 24);
     if (!use_s32 && want) {
@@ -253,9 +298,50 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       }
     }
   }
-  CGM_CUDA(ctx, cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+  // U = 32: Gram row in registers, packed FFMA2 matvec (cgm_rows32.cuh).
+  // Default for the approximate-tracker uplink (one warp per system pair:
+  // cfg2 43.4 -> 35.2 us); CGMIMO_SOLVE=rows also selects the CTA-per-
+  // subcarrier form for exact / downlink systems, CGMIMO_SOLVE=lanes never
+  bool use_rows = false, use_pairs = false;
+  if constexpr (UP == 32) {
+    const char* force = env("CGMIMO_SOLVE");
+    const bool want = force ? std::strcmp(force, "rows") == 0 : (!EXACT && p.St == 0);
+    if (!use_s32 && !use_pf && want) {
+      cgm::Rows32Smem R;
+      R.plan(p.B, p.S, p.St, Kmax, EXACT);
+      if (!EXACT && p.St == 0) {  // approx uplink: one warp per pair of systems
+        use_rows = use_pairs = true;
+        k2 = cgm::solve_rows32_pairs_kernel;
+        smem2 = 0;
+      } else if (R.total <= ctx->max_smem) {
+        use_rows = true;
+        k2 = cgm::solve_rows32_kernel<EXACT>;
+        smem2 = R.total;
+      }
+    }
+  }
+  CGM_PREP(ctx, k2, 32, smem2, nullptr);
+  // exact tracker, U = 32 / 64: the Chebyshev basis products in their own
+  // kernel (cgm_basis.cuh) instead of the channel kernel's epilogue;
+  // CGMIMO_BASIS=inline keeps them in the channel kernel
+  void (*kb)(cgm::KernelParams) = nullptr;
+  int nb_t = 0, nb_smem = 0, nb_spc = 1;
+  if constexpr (EXACT && (UP == 32 || UP == 64)) {
+    const char* e = env("CGMIMO_BASIS");
+    if (p.S > 0 && p.K > 0 && !(e && std::strcmp(e, "inline") == 0)) {
+      using BG = cgm::BasisGeo<UP>;
+      if (BG::SMEM <= ctx->max_smem) {
+        kb = cgm::basis_kernel<UP>;
+        nb_t = BG::NT;
+        nb_smem = BG::SMEM;
+        nb_spc = BG::SPC;
+        CGM_PREP(ctx, kb, nb_t, nb_smem, nullptr);
+      }
+    }
+  }
+  p.basis_ext = kb ? 1 : 0;
   int occ1 = 0;
-  CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, k1, nt1, smem1));
+  CGM_PREP(ctx, k1, nt1, smem1, &occ1);
   if (occ1 < 1) return fail(ctx, CGM_EINVAL, "channel kernel does not fit on an SM");
   if (use_tc) occ1 = 1;  // one CTA (and all 512 TMEM columns) per SM
   // K2 block: enough lane groups for every system at once (>= UP threads
@@ -266,10 +352,14 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   if (EXACT) nw2 = std::max(nw2, std::max(4, UP / 32));
   nw2 = std::max(1, std::min(8, nw2));
   if (use_s32) nw2 = ((nsys + ts2 - 1) / ts2 * 8 + 31) / 32;  // 8 threads per tile, whole warps
+  if (use_rows) {
+    nw2 = 2;
+    if (const char* e = env("CGMIMO_ROWS_WARPS")) nw2 = std::max(1, std::min(8, std::atoi(e)));
+  }
   long g2cap = 1L << 40;
   if (use_pf) {
     int occ2 = 0;
-    CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k2, 32 * nw2, smem2));
+    CGM_PREP(ctx, k2, 32 * nw2, smem2, &occ2);
     g2cap = static_cast<long>(std::max(occ2, 1)) * ctx->sms;
   }
   // chunk so that workspace + channel (+ Y) of a chunk fit comfortably in L2
@@ -277,11 +367,14 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
                         static_cast<size_t>(p.B) * p.S * 8;
   long chunk = static_cast<long>((80ull << 20) / std::max<size_t>(per_sc, 1));
   chunk = std::max<long>(chunk, static_cast<long>(ctx->sms) * occ1);
+  // external basis: the basis products need several full waves per launch
+  // more than they need the workspace in L2 (T_1..T_K then round-trips HBM)
+  if (kb) chunk = std::max<long>(chunk, static_cast<long>(ctx->sms) * 32);
   chunk = std::min(chunk, p.n_sc);
   // overlap K1(c+1) with K2(c): at least `ovl` chunks (CGMIMO_OVERLAP_CHUNKS,
   // default 1 = off: measured slower on cfg2/cfg3/cfg5)
   int ovl = 1;
-  if (const char* e = std::getenv("CGMIMO_OVERLAP_CHUNKS")) ovl = std::max(1, std::atoi(e));
+  if (const char* e = env("CGMIMO_OVERLAP_CHUNKS")) ovl = std::max(1, std::atoi(e));
   const long min_chunk = static_cast<long>(ctx->sms) * occ1;
   if (ovl > 1 && p.n_sc >= 2 * min_chunk)
     chunk = std::min(chunk, std::max(min_chunk, (p.n_sc + ovl - 1) / ovl));
@@ -328,13 +421,21 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
     }
     k1<<<static_cast<unsigned>(g1), nt1, smem1, s1>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
+    if (kb) {
+      kb<<<static_cast<unsigned>((n + nb_spc - 1) / nb_spc), nb_t, nb_smem, s1>>>(p);
+      CGM_CUDA(ctx, cudaGetLastError());
+      ctx->launches += 1;
+    }
     if (ctx->profiling) cudaEventRecord(e1, s1);
     if (overlap) {
       CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[1 + half], s1));
       CGM_CUDA(ctx, cudaStreamWaitEvent(s2, ctx->ov_ev[1 + half], 0));
     }
     if (ctx->profiling) cudaEventRecord(e2, s2);
-    k2<<<static_cast<unsigned>(std::min(n, g2cap)), 32 * nw2, smem2, s2>>>(p);
+    if (use_pairs)  // 4 warps per CTA, one (subcarrier, system pair) per warp
+      k2<<<static_cast<unsigned>((n * ((p.S + 1) / 2) + 3) / 4), 128, 0, s2>>>(p);
+    else
+      k2<<<static_cast<unsigned>(std::min(n, g2cap)), 32 * nw2, smem2, s2>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
     if (ctx->profiling) {
       cudaEventRecord(e3, s2);
@@ -376,9 +477,8 @@ int launch_alt(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
   auto k = p.method == cgm::alt::kCholesky ? cgm::alt::alt_kernel<cgm::alt::kCholesky>
            : p.method == cgm::alt::kCgls   ? cgm::alt::alt_kernel<cgm::alt::kCgls>
                                            : cgm::alt::alt_kernel<cgm::alt::kNeumann>;
-  CGM_CUDA(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int occ = 0;
-  CGM_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, cgm::alt::NT, smem));
+  CGM_PREP(ctx, k, cgm::alt::NT, static_cast<int>(smem), &occ);
   const long grid = std::max<long>(1, std::min<long>(p.n_sc, static_cast<long>(std::max(occ, 1)) * ctx->sms));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (ctx->profiling) {
@@ -491,7 +591,7 @@ cgm::KernelParams params_of(const Job& j, long n_sc) {
   p.rho_inv_u = j.S > 0 ? static_cast<float>(1.0 / j.rho_u) : 0.f;
   p.rho_inv_d = j.St > 0 ? static_cast<float>(1.0 / j.rho_d) : 0.f;
   p.n0 = static_cast<float>(j.n0);
-  if (const char* dbg = std::getenv("CGMIMO_DEBUG_WS")) p.debug = std::atoi(dbg);
+  if (const char* dbg = env("CGMIMO_DEBUG_WS")) p.debug = std::atoi(dbg);
   p.es = static_cast<float>(j.es);
   p.method = j.method;
   return p;
@@ -545,7 +645,7 @@ int run_job(cgm_ctx* ctx, const Job& j, unsigned flags) {
   long chunk = static_cast<long>(std::max<size_t>(1, budget / std::max<size_t>(per_sc, 1)));
   chunk = std::min(chunk, j.n_sc);
   int nch = 8;
-  if (const char* e = std::getenv("CGMIMO_HOST_CHUNKS")) nch = std::max(1, std::atoi(e));
+  if (const char* e = env("CGMIMO_HOST_CHUNKS")) nch = std::max(1, std::atoi(e));
   const long min_chunk = std::max<long>(1, ctx->sms);  // keep each launch >= one wave
   if (j.n_sc >= 2 * min_chunk)
     chunk = std::min(chunk, std::max(min_chunk, (j.n_sc + nch - 1) / nch));

@@ -61,6 +61,7 @@ struct KernelParams {
   int k1_pair, k1_spl, k1_wpp;  // channel kernel: subcarriers per CTA, k-parts, warps per part
   unsigned long long* trace;    // microbenchmarks only: per-CTA event clocks (null in production)
   int method;                   // sim::Method order: 0 Cholesky, 1 CG, 2 CGLS, 3 Neumann (cgm_alt.cuh)
+  int basis_ext;                // exact tracker: the Chebyshev basis comes from basis_kernel (cgm_basis.cuh)
 };
 
 // Per-axis Gray amplitude subsets (constellation.cpp:75-84), [qam][p][k],
@@ -210,7 +211,7 @@ __device__ __forceinline__ void tile_pass(int n_lower, int n_other, int nsb, con
 // sqrt(U) reached below 0 at weak regularisation and lost up to 1.5e-3 in
 // rho at K = 16 (tools/fp32_tracker_study.py "weak": 1.5e-6 with this one).
 // One warp; G Hermitian in smem (read by columns); xs: UP float2 scratch.
-template <int UP>
+template <int UP, int LDG = UP>
 __device__ __forceinline__ float2 cheb_interval(const float2* Gs, float reg, float2* xs, int lane) {
   constexpr int RU = UP < 32 ? 1 : UP / 32;
   float2 xr[RU];
@@ -231,7 +232,7 @@ __device__ __forceinline__ float2 cheb_interval(const float2* Gs, float reg, flo
       y[m] = make_float2(0.f, 0.f);
       if (i < UP) {
         // (A x)_i = sum_j conj(G[j][i]) x_j + reg x_i  (G Hermitian; column reads)
-        for (int j = 0; j < UP; ++j) cfma_conj(y[m], Gs[j * UP + i], xs[j]);
+        for (int j = 0; j < UP; ++j) cfma_conj(y[m], Gs[j * LDG + i], xs[j]);
         y[m].x = fmaf(reg, xr[m].x, y[m].x);
         y[m].y = fmaf(reg, xr[m].y, y[m].y);
       }

@@ -1,0 +1,308 @@
+// cgm_rows32.cuh -- K2 for U = 32 with the Gram row in registers.
+//
+// Same mathematics and outputs as solve_sc (cgm_split.cuh): K CG iterations
+// on G + rho^-1 I per system (solvers.cpp:37-72, freeze / breakdown rules),
+// the approximate tracker (detect.cpp:397-441) or the exact tracker's
+// (alpha, beta) history for k2_exact_tail, LLRs, the precoder tail.
+//
+// Layout: lane u of a warp owns user row u; the warp keeps row u of G
+// (G[u][j] = conj(G[j][u]), 64 registers) for the whole subcarrier and runs
+// the systems of that subcarrier two at a time.  The matvec e_u = sum_j
+// G[u][j] p_j is then 2 packed FFMA2 per (j, system) with p_j broadcast
+// from shared memory (one LDS.128 per two columns) and no G traffic at all:
+//   a += (g.x, g.y) * (p.x, p.x),  b += (g.x, g.y) * (p.y, p.y)
+//   e = (a.x - b.y, b.x + a.y)
+// versus the lane-per-row kernel's 4 FFMA + shared G loads per (j, system).
+// Two warps per subcarrier (one CTA), so the per-subcarrier G row load is
+// paid by 64 threads and ~16 warps share an SM.
+#pragma once
+
+#include "cgm_split.cuh"
+
+namespace cgm {
+
+struct Rows32Smem {
+  int k2, ps4, total;  // K2Smem plan first (Vs, hist, tails), then the p broadcast rows
+  __host__ __device__ void plan(int B, int S, int St, int K, bool exact) {
+    K2Smem<32> L;
+    L.plan(B, S, St, K, exact);
+    k2 = 0;
+    ps4 = L.total;
+    total = ps4 + 2 * 8 * 32 * 8;  // two broadcast rows per warp, up to 8 warps
+  }
+};
+
+__device__ __forceinline__ unsigned long long f2dup_lo(unsigned long long v) {
+  unsigned long long r;
+  asm("{ .reg .f32 lo, hi; mov.b64 {lo, hi}, %1; mov.b64 %0, {lo, lo}; }" : "=l"(r) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2dup_hi(unsigned long long v) {
+  unsigned long long r;
+  asm("{ .reg .f32 lo, hi; mov.b64 {lo, hi}, %1; mov.b64 %0, {hi, hi}; }" : "=l"(r) : "l"(v));
+  return r;
+}
+
+// sum over the 32 lanes of two values at once: 5 + 1 shuffles instead of 10
+__device__ __forceinline__ void warp_sum2(float& a, float& b) {
+  const int lane = threadIdx.x & 31;
+  const bool hi = lane & 16;
+  // lanes < 16 keep a's half-sums, lanes >= 16 b's
+  const float send = hi ? a : b;
+  const float keep = hi ? b : a;
+  float v = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const float other = __shfl_xor_sync(0xffffffffu, v, 16);
+  a = hi ? other : v;
+  b = hi ? v : other;
+}
+
+// CG for the systems base, base + 1 of subcarrier sc on one warp (lane =
+// user row), with row `lane` of G in `grow`; Ps = this warp's two broadcast
+// rows.  Approx uplink systems write their outputs here; exact / downlink
+// systems leave v in Vs and (exact) the (alpha, beta) history in hist.
+// UPONLY: every system is an uplink vector with the same K (the
+// approximate-tracker pairs kernel), so the per-system direction / iteration
+// count branches fold away.
+template <bool EXACT, bool UPONLY = false>
+__device__ __forceinline__ void rows32_pair(const KernelParams& p, long sc, const float2* mfsrc,
+                                            int base, const unsigned long long (&grow)[32],
+                                            float gdiag, float2* Ps, float* hist, float2* Vs,
+                                            uint8_t* sys_st) {
+  constexpr int UP = 32, NS = 2;
+  const int S = p.S, St = p.St, U = p.U;
+  const int nsys = S + St;
+  const int Kmax = UPONLY ? p.K : (p.K > p.Kt ? p.K : p.Kt);
+  const int lane = threadIdx.x & 31;
+  int sys[NS];
+  bool live[NS], down[NS], broke[NS];
+  float reg[NS], rn[NS], rn0[NS];
+  int iters[NS];
+  float2 v[NS], r[NS], pp[NS];
+  // approximate tracker state; ia = 1 / alpha of the previous iterations
+  float f0[NS], f1[NS], f2[NS], ia1[NS], ia2[NS], bm1[NS], bm2[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    sys[s] = base + s;
+    live[s] = sys[s] < nsys;
+    down[s] = UPONLY ? false : sys[s] >= S;
+    reg[s] = down[s] ? p.rho_inv_d : p.rho_inv_u;
+    iters[s] = live[s] ? (down[s] ? p.Kt : p.K) : 0;
+    float2 b = make_float2(0.f, 0.f);
+    if (live[s] && lane < U)
+      b = down[s] ? p.T[(sc * St + (sys[s] - S)) * static_cast<long>(U) + lane]
+                  : mfsrc[sys[s] * UP + lane];
+    v[s] = make_float2(0.f, 0.f);
+    r[s] = b;
+    pp[s] = b;
+    Ps[s * UP + lane] = b;  // this warp's broadcast row for slot s
+    rn[s] = cnorm(b);
+    broke[s] = false;
+    ia1[s] = ia2[s] = 1.f;
+    bm1[s] = bm2[s] = 0.f;
+    f0[s] = f1[s] = f2[s] = 0.f;
+  }
+  warp_sum2(rn[0], rn[1]);
+  rn0[0] = rn[0];
+  rn0[1] = rn[1];
+  __syncwarp();
+  for (int k = 1; k <= Kmax; ++k) {
+    // e = (G + reg I) p on the packed pipe
+    unsigned long long a0[NS], b0[NS], a1[NS], b1[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) a0[s] = b0[s] = a1[s] = b1[s] = 0ull;
+#pragma unroll
+    for (int j = 0; j < UP; j += 2) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const ulonglong2 pj =
+            *reinterpret_cast<const ulonglong2*>(Ps + s * UP + j);
+        ffma2(a0[s], grow[j], f2dup_lo(pj.x));
+        ffma2(b0[s], grow[j], f2dup_hi(pj.x));
+        ffma2(a1[s], grow[j + 1], f2dup_lo(pj.y));
+        ffma2(b1[s], grow[j + 1], f2dup_hi(pj.y));
+      }
+    }
+    float2 e[NS];
+    float curv[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const float2 A0 = f2unpack(a0[s]), B0 = f2unpack(b0[s]);
+      const float2 A1 = f2unpack(a1[s]), B1 = f2unpack(b1[s]);
+      e[s].x = (A0.x - B0.y) + (A1.x - B1.y);
+      e[s].y = (B0.x + A0.y) + (B1.x + A1.y);
+      e[s].x = fmaf(reg[s], pp[s].x, e[s].x);
+      e[s].y = fmaf(reg[s], pp[s].y, e[s].y);
+      curv[s] = pp[s].x * e[s].x + pp[s].y * e[s].y;  // Re p^H e
+    }
+    warp_sum2(curv[0], curv[1]);
+    float alpha[NS], beta[NS], rnx[NS];
+    bool upd[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const bool step = UPONLY ? live[s] : k <= iters[s];
+      const bool frozen = !(rn[s] > 1e-28f * rn0[s]);  // solvers.cpp:21,25-27
+      const bool go = step && !frozen && !broke[s];
+      if (go && curv[s] < 1e-30f) broke[s] = true;  // solvers.cpp:55-57
+      upd[s] = go && !broke[s];
+      alpha[s] = upd[s] ? rn[s] * __frcp_rn(curv[s]) : 1.f;
+      beta[s] = 0.f;
+      if (upd[s]) {
+        v[s].x = fmaf(alpha[s], pp[s].x, v[s].x);
+        v[s].y = fmaf(alpha[s], pp[s].y, v[s].y);
+        r[s].x = fmaf(-alpha[s], e[s].x, r[s].x);
+        r[s].y = fmaf(-alpha[s], e[s].y, r[s].y);
+      }
+      rnx[s] = cnorm(r[s]);
+    }
+    warp_sum2(rnx[0], rnx[1]);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      float ia = 1.f;  // 1 / alpha
+      if (upd[s]) {
+        const float irn = __frcp_rn(rn[s]);
+        beta[s] = rnx[s] * irn;
+        ia = curv[s] * irn;
+        rn[s] = rnx[s];
+        pp[s].x = fmaf(beta[s], pp[s].x, r[s].x);
+        pp[s].y = fmaf(beta[s], pp[s].y, r[s].y);
+      }
+      if (UPONLY || k <= iters[s]) {
+        if (!down[s]) {
+          if (EXACT) {
+            if (lane == 0) {
+              hist[(sys[s] * Kmax + (k - 1)) * 2 + 0] = alpha[s];
+              hist[(sys[s] * Kmax + (k - 1)) * 2 + 1] = beta[s];
+            }
+          } else {
+            // Eq. (11) on the diagonal (detect.cpp:409-427)
+            // k = 1: L_1 = alpha_1 (a select, not a branch)
+            const float c1 = alpha[s] * (1.f + bm1[s]) * ia1[s];
+            const float c2 = alpha[s] * bm2[s] * ia2[s];
+            const float nk = f0[s] + (c1 - alpha[s] * (gdiag + reg[s])) * (f0[s] - f1[s]) -
+                             c2 * (f1[s] - f2[s]);
+            const float nf = k == 1 ? alpha[s] : nk;
+            f2[s] = f1[s];
+            f1[s] = f0[s];
+            f0[s] = nf;
+          }
+        }
+        ia2[s] = ia1[s]; ia1[s] = ia;
+        bm2[s] = bm1[s]; bm1[s] = beta[s];
+      }
+    }
+    __syncwarp();  // every lane's matvec reads of Ps are done
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (upd[s]) Ps[s * UP + lane] = pp[s];
+    __syncwarp();
+  }
+  // ------------------------------------------------ per-system epilogue
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    if (!live[s]) continue;
+    if ((EXACT || down[s]) && lane == 0) sys_st[sys[s]] = broke[s] ? 1 : 0;  // read by the tails
+    if (EXACT || down[s]) {
+      Vs[sys[s] * UP + lane] = v[s];
+      continue;
+    }
+    if constexpr (!EXACT) {
+      // approx uplink: mu = Ltilde G_ii, rho = G_ii / N0 (detect.cpp:435-441)
+      if (lane < U) {
+        const long o = (sc * S + sys[s]) * static_cast<long>(U) + lane;
+        const bool ok = !broke[s];
+        const float2 xh = ok ? v[s] : make_float2(0.f, 0.f);
+        const float mu_u = ok ? f0[s] * gdiag : 0.f;
+        const float rho_u = ok ? gdiag / p.n0 : 0.f;
+        if (p.xhat) p.xhat[o] = xh;
+        if (p.mu) p.mu[o] = mu_u;
+        if (p.rho) p.rho[o] = rho_u;
+        if (p.llr) store_llrs_fast(xh, mu_u, rho_u, p.bits, p.llr + o * p.bits);
+        if (p.status && lane == 0) p.status[sc * S + sys[s]] = ok ? 0 : 1;
+      }
+    }
+  }
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(256, 2) solve_rows32_kernel(const KernelParams p) {
+  constexpr int UP = 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int S = p.S, St = p.St, B = p.B, U = p.U;
+  const int nsys = S + St;
+  const int Kmax = p.K > p.Kt ? p.K : p.Kt;
+  Rows32Smem R;
+  R.plan(B, S, St, Kmax, EXACT);
+  K2Smem<UP> L;
+  L.plan(B, S, St, Kmax, EXACT);
+  WsOffsets W;
+  W.plan(UP, S, p.K, EXACT);
+  float2* Vs = reinterpret_cast<float2*>(smem + L.vs);
+  float2* Qs = reinterpret_cast<float2*>(smem + L.qs);
+  float* hist = reinterpret_cast<float*>(smem + L.hist);
+  uint8_t* sys_st = reinterpret_cast<uint8_t*>(smem + L.sys_st);
+  float* MUs = reinterpret_cast<float*>(smem + L.mu);
+  float* RHOs = reinterpret_cast<float*>(smem + L.rho);
+  float* coef = reinterpret_cast<float*>(smem + L.coef);
+  float* gpart = reinterpret_cast<float*>(smem + L.gpart);
+  float2* Ps = reinterpret_cast<float2*>(smem + R.ps4);
+  const int nt = blockDim.x, nw = nt >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long lsc = blockIdx.x;
+  const long sc = p.sc_base + lsc;
+  const float2* ws = p.ws + lsc * W.stride;
+  const float2* mfsrc = ws + W.mf;
+
+  // row `lane` of G: G[u][j] = conj(G[j][u]) -- column reads, coalesced
+  unsigned long long grow[UP];
+#pragma unroll
+  for (int j = 0; j < UP; ++j) {
+    const float2 g = __ldg(ws + W.g + j * UP + lane);
+    grow[j] = f2pack(g.x, -g.y);
+  }
+  const float gdiag = __ldg(ws + W.g + lane * UP + lane).x;
+
+  for (int base = warp * 2; base < nsys; base += nw * 2)
+    rows32_pair<EXACT>(p, sc, mfsrc, base, grow, gdiag, Ps + warp * 2 * UP, hist, Vs, sys_st);
+  auto sync = [] { __syncthreads(); };
+  if (EXACT && S > 0) {
+    sync();
+    k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st, nt, sync);
+  }
+  if (St > 0) {
+    sync();
+    k2_precode_tail<UP>(p, sc, Vs, Qs, gpart, sys_st, nt, sync);
+  }
+}
+
+
+// Approximate-tracker uplink (no CTA-wide tail): one warp per (subcarrier,
+// pair of systems) work item, so the grid is many short warps that the
+// hardware scheduler balances (a CTA per subcarrier at 16 warps / SM leaves
+// a 1.01-wave tail on cfg2's 1200 subcarriers).  Each warp reads its G row
+// straight from the L2-resident workspace.
+__global__ void __launch_bounds__(128, 4) solve_rows32_pairs_kernel(const KernelParams p) {
+  constexpr int UP = 32;
+  __shared__ __align__(16) float2 Ps_all[4][2 * UP];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int npairs = (p.S + 1) >> 1;
+  const long item = static_cast<long>(blockIdx.x) * (blockDim.x >> 5) + warp;
+  if (item >= p.n_sc * npairs) return;
+  const long lsc = item / npairs;
+  const int base = static_cast<int>(item - lsc * npairs) * 2;
+  WsOffsets W;
+  W.plan(UP, p.S, p.K, false);
+  const float2* ws = p.ws + lsc * W.stride;
+  unsigned long long grow[UP];
+#pragma unroll
+  for (int j = 0; j < UP; ++j) {
+    const float2 g = __ldg(ws + W.g + j * UP + lane);
+    grow[j] = f2pack(g.x, -g.y);
+  }
+  const float gdiag = __ldg(ws + W.g + lane * UP + lane).x;
+  rows32_pair<false, true>(p, p.sc_base + lsc, ws + W.mf, base, grow, gdiag, Ps_all[warp],
+                           nullptr, nullptr, nullptr);
+}
+
+}  // namespace cgm

@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p
       float4* dst = reinterpret_cast<float4*>(ws + W.g);
       for (int e = tid; e < UP * UP / 2; e += nt) dst[e] = src[e];
     }
-    if (EXACT && S > 0) exact_basis<UP>(p, W, ws, Gs, T1, Tm, misc, nt, [] { __syncthreads(); });
+    if (EXACT && S > 0 && !p.basis_ext) exact_basis<UP>(p, W, ws, Gs, T1, Tm, misc, nt, [] { __syncthreads(); });
     __syncthreads();  // Gs is rewritten by the next subcarrier
   }
 }

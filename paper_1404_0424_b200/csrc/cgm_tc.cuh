@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
     }
     named_sync(1, NTE);
     if (tid == 0) tc_trace(p, e, 11);
-    if (EXACT && S > 0) exact_basis<UP>(p, W, ws, Gs, T1, Tm, misc, NTE, [] { named_sync(1, NTE); });
+    if (EXACT && S > 0 && !p.basis_ext) exact_basis<UP>(p, W, ws, Gs, T1, Tm, misc, NTE, [] { named_sync(1, NTE); });
     if (tid == 0) tc_trace(p, e, 12);
   };
 

@@ -221,3 +221,47 @@ def test_precode_uplink_layout_equals_downlink_layout(gpu_ctx, U, B, K):
     for k in ("q", "s"):
         d = float((a[k] - b[k]).abs().max() / b[k].abs().max())
         assert d < 1e-5, (k, d)
+
+
+@pytest.mark.parametrize("name,var,val", [
+    ("cfg2", "CGMIMO_SOLVE", "lanes"),       # default: Gram-row-in-registers pairs kernel
+    ("cfg4a_K8", "CGMIMO_SOLVE", "rows"),    # CTA-per-subcarrier rows kernel, exact tail
+    ("cfg5", "CGMIMO_SOLVE", "rows"),        # ... with precoder systems
+    ("cfg4a_K8", "CGMIMO_BASIS", "inline"),  # default: basis_kernel (cgm_basis.cuh)
+    ("cfg4b_K4", "CGMIMO_BASIS", "inline"),
+    ("cfg5", "CGMIMO_BASIS", "inline"),
+])
+def test_solve_and_basis_variants_agree(gpu_ctx, checker, monkeypatch, name, var, val):
+    """Every K2 / basis variant gives the default's results to FP32 rounding,
+    and the default matches the oracle on a subsample."""
+    cfg = get_config(name).scaled(400)
+    H, Y = gen(gpu_ctx, cfg)
+    if cfg.kind == "both":
+        T = gpu_ctx.generate_symbols(cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits)
+        call = lambda: gpu_ctx.detect_precode_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits,
+                                                 cfg.K, cfg.tracker, T, cfg.rho_d, cfg.K)
+    else:
+        call = lambda: gpu_ctx.detect_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                                         cfg.tracker)
+    a = call()
+    torch.cuda.synchronize()
+    l0 = gpu_ctx.kernel_launches
+    monkeypatch.setenv(var, val)
+    b = call()
+    torch.cuda.synchronize()
+    monkeypatch.delenv(var)
+    assert gpu_ctx.kernel_launches > l0
+    for k in a:
+        if a[k].dtype == torch.uint8:
+            assert torch.equal(a[k], b[k]), k
+            continue
+        x, y = a[k], b[k]
+        if x.is_complex():
+            x, y = torch.view_as_real(x), torch.view_as_real(y)
+        tol = 1e-4 + 1e-3 * float(x.abs().max()) if k != "llr" else 1e-3 * 64
+        assert float((x - y).abs().max()) <= tol, k
+    idx = np.random.default_rng(5).choice(cfg.n_sc, size=6, replace=False)
+    want = checker.detect(H[idx].cpu().numpy(), Y[idx].cpu().numpy(), cfg.rho_u, cfg.n0, cfg.es,
+                          cfg.qam_bits, cfg.K, cfg.tracker, threads=8)
+    got = {k: v[idx].cpu().numpy() for k, v in a.items() if k in ("xhat", "mu", "rho", "llr", "status")}
+    check_detect(got, want, name + " default")

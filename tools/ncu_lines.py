@@ -40,7 +40,7 @@ def main():
     tot = sum(x[0] for x in lines) or 1
     tote = sum(x[1] for x in lines) or 1
     print(f"total samples {tot}, instructions {tote}")
-    for s, e, loc, src, st in sorted(lines, reverse=True)[:top]:
+    for s, e, loc, src, st in sorted(lines, key=lambda x: x[1 if __import__("os").environ.get("BY_INST") else 0], reverse=True)[:top]:
         print(f"{100*s/tot:5.1f}% {100*e/tote:5.1f}%i {loc:22s} {src:70s} {[(k[6:], v) for v, k in st]}")
 
 
