@@ -19,6 +19,7 @@
 #include "../../include/cgmimo_b200.h"
 #include "cgm_alt.cuh"
 #include "cgm_basis.cuh"
+#include "cgm_precode_small.cuh"
 #include "cgm_rows32.cuh"
 #include "cgm_solve32.cuh"
 #include "cgm_tc.cuh"
@@ -496,10 +497,51 @@ int launch_alt(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
   return CGM_OK;
 }
 
+// Fused small-U CG precoder (cgm_precode_small.cuh): pure precode calls with
+// H_d in the reference layout, U <= 16.  CGMIMO_PRECODE=split keeps the
+// channel + solve pair.
+template <int UP>
+int launch_precode_small(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
+  cgm::PrecodeSmallSmem L;
+  L.plan(UP, p.B, p.St);
+  auto k = cgm::precode_small_kernel<UP>;
+  int occ = 0;
+  CGM_PREP(ctx, k, cgm::PrecodeSmallGeo<UP>::NT, L.total, &occ);
+  const long grid = std::max<long>(1, std::min<long>(p.n_sc, static_cast<long>(std::max(occ, 1)) * ctx->sms));
+  p.use_tma = ((p.B % 2) == 0 && (reinterpret_cast<uintptr_t>(p.H) & 15u) == 0) ? 1 : 0;
+  p.sc_base = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->profiling) {
+    e0 = prof_event(ctx);
+    e1 = prof_event(ctx);
+    cudaEventRecord(e0, st);
+  }
+  k<<<static_cast<unsigned>(grid), cgm::PrecodeSmallGeo<UP>::NT, L.total, st>>>(p);
+  CGM_CUDA(ctx, cudaGetLastError());
+  if (ctx->profiling) {
+    cudaEventRecord(e1, st);
+    ctx->ev_log.push_back({2, {e0, e1}});
+  }
+  ++ctx->launches;
+  return CGM_OK;
+}
+
+bool precode_small_ok(cgm_ctx* ctx, const cgm::KernelParams& p) {
+  if (!(p.S == 0 && p.St > 0 && p.hd_layout && p.U <= 16 && p.B <= 512 && p.B >= 4 && p.B % 2 == 0))
+    return false;
+  const char* e = env("CGMIMO_PRECODE");
+  if (e && std::strcmp(e, "split") == 0) return false;
+  cgm::PrecodeSmallSmem L;
+  L.plan(up_of(p.U), p.B, p.St);
+  return L.total <= ctx->max_smem;
+}
+
 int launch(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
   if (p.n_sc <= 0) return CGM_OK;
   if (p.method != cgm::alt::kCg) return launch_alt(ctx, p, st);
   const int UP = up_of(p.U);
+  if (ctx->policy == 0 && precode_small_ok(ctx, p))
+    return UP == 8 ? launch_precode_small<8>(ctx, p, st) : launch_precode_small<16>(ctx, p, st);
   const uintptr_t a = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
   p.use_tma = (!p.hd_layout && p.U == UP && (p.B % 2) == 0 && (p.S % 2) == 0 && (a & 15u) == 0)
                   ? 1 : 0;

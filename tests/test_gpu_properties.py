@@ -265,3 +265,32 @@ def test_solve_and_basis_variants_agree(gpu_ctx, checker, monkeypatch, name, var
                           cfg.qam_bits, cfg.K, cfg.tracker, threads=8)
     got = {k: v[idx].cpu().numpy() for k, v in a.items() if k in ("xhat", "mu", "rho", "llr", "status")}
     check_detect(got, want, name + " default")
+
+
+@pytest.mark.parametrize("U,B,S,K", [(16, 128, 1, 3), (8, 64, 3, 4), (5, 30, 2, 2), (13, 96, 4, 5)])
+def test_fused_small_precoder_matches_split_and_oracle(gpu_ctx, checker, monkeypatch, U, B, S, K):
+    """The fused U <= 16 precoder (cgm_precode_small.cuh: one HBM read of H_d)
+    agrees with the channel + solve pair to FP32 rounding and with the
+    oracle, ragged U and B included (B = 30: no TMA, plain copies)."""
+    g = torch.Generator().manual_seed(100 + U)
+    n_sc = 300
+    Hd = torch.complex(torch.randn(n_sc, U, B, generator=g), torch.randn(n_sc, U, B, generator=g))
+    T = torch.complex(torch.randn(n_sc, S, U, generator=g), torch.randn(n_sc, S, U, generator=g))
+    Hd, T = (Hd / 2 ** 0.5).cuda(), (T / 2 ** 0.5).cuda()
+    T[7] = 0  # zero transmit vectors: zero_input status, gain 0
+    l0 = gpu_ctx.kernel_launches
+    a = gpu_ctx.precode_cg(Hd, T, 0.625, K)
+    torch.cuda.synchronize()
+    assert gpu_ctx.kernel_launches - l0 == 1  # one fused launch
+    monkeypatch.setenv("CGMIMO_PRECODE", "split")
+    b = gpu_ctx.precode_cg(Hd, T, 0.625, K)
+    torch.cuda.synchronize()
+    monkeypatch.delenv("CGMIMO_PRECODE")
+    assert torch.equal(a["status"], b["status"])
+    assert int(a["status"][7].min()) == 2
+    for k in ("q", "s", "gain"):
+        d = float((a[k] - b[k]).abs().max() / b[k].abs().max())
+        assert d < 2e-5, (k, d)
+    idx = np.arange(0, n_sc, 37)
+    want = checker.precode(Hd[idx].cpu().numpy(), T[idx].cpu().numpy(), 0.625, K, threads=8)
+    check_precode({k: v[idx].cpu().numpy() for k, v in a.items()}, want, f"fused U={U} B={B}")
