@@ -236,7 +236,11 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   bool use_tc = false;
   if constexpr (UP == 32) {
     const char* force = env("CGMIMO_CHANNEL");
-    if (cgm::tc::supported(p.U, p.B, p.S, p.use_tma) && !(force && std::strcmp(force, "ffma") == 0)) {
+    // the tensor-core kernel stages Y per 64-antenna block (64 S complex,
+    // always a 16-byte multiple), so odd S is fine there (cfg4: S = 1)
+    const uintptr_t al = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
+    const int tc_tma = (!p.hd_layout && p.U == UP && (al & 15u) == 0) ? 1 : 0;
+    if (cgm::tc::supported(p.U, p.B, p.S, tc_tma) && !(force && std::strcmp(force, "ffma") == 0)) {
       cgm::tc::Smem T;
       int nstg = 3;
       T.plan(p.S, EXACT, nstg);
@@ -300,22 +304,26 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
     }
   }
   // U = 32: Gram row in registers, packed FFMA2 matvec (cgm_rows32.cuh).
-  // Default for the approximate-tracker uplink (one warp per system pair:
-  // cfg2 43.4 -> 35.2 us); CGMIMO_SOLVE=rows also selects the CTA-per-
-  // subcarrier form for exact / downlink systems, CGMIMO_SOLVE=lanes never
+  // Default for uplink-only calls (St = 0): one warp per (subcarrier, system
+  // pair), approximate (cfg2 43.4 -> 35.2 us) or exact tracker with the
+  // extraction inside the warp; CGMIMO_SOLVE=rows selects the CTA-per-
+  // subcarrier form (any systems, CTA-wide tails), CGMIMO_SOLVE=lanes the
+  // lane-per-row kernel
   bool use_rows = false, use_pairs = false;
   if constexpr (UP == 32) {
     const char* force = env("CGMIMO_SOLVE");
-    const bool want = force ? std::strcmp(force, "rows") == 0 : (!EXACT && p.St == 0);
-    if (!use_s32 && !use_pf && want) {
+    const bool cta = force && std::strcmp(force, "rows") == 0;
+    if (!use_s32 && !force && p.St == 0 && p.K <= cgm::kMaxK) {
+      use_rows = use_pairs = true;
+      use_pf = false;
+      k2 = EXACT ? cgm::solve_rows32_exact_pairs_kernel : cgm::solve_rows32_pairs_kernel;
+      smem2 = 0;
+    } else if (!use_s32 && cta) {
       cgm::Rows32Smem R;
       R.plan(p.B, p.S, p.St, Kmax, EXACT);
-      if (!EXACT && p.St == 0) {  // approx uplink: one warp per pair of systems
-        use_rows = use_pairs = true;
-        k2 = cgm::solve_rows32_pairs_kernel;
-        smem2 = 0;
-      } else if (R.total <= ctx->max_smem) {
+      if (R.total <= ctx->max_smem) {
         use_rows = true;
+        use_pf = false;
         k2 = cgm::solve_rows32_kernel<EXACT>;
         smem2 = R.total;
       }
@@ -526,6 +534,45 @@ int launch_precode_small(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   return CGM_OK;
 }
 
+// Fully fused U = 32 approximate-tracker detector (one warp per subcarrier,
+// cgm_rows32.cuh): Gram + matched filters + every system's CG in one kernel.
+// Opt-in (CGMIMO_FUSED=1): measured 111 us on cfg2 against 67 us for the
+// tensor-core channel kernel + pairs solve kernel -- eight warps per SM
+// leave the fourteen sequential CG chains of a subcarrier latency-exposed.
+bool fused_rows32_ok(cgm_ctx* ctx, const cgm::KernelParams& p, bool exact) {
+  if (exact || p.U != 32 || p.St != 0 || p.S < 1 || p.S > 16 || p.hd_layout || (p.B % 2) != 0)
+    return false;
+  const uintptr_t al = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
+  if (al & 15u) return false;
+  const char* e = env("CGMIMO_FUSED");
+  if (!(e && std::strcmp(e, "1") == 0)) return false;
+  cgm::FusedSmem L;
+  L.plan(p.B, p.S);
+  return L.total <= ctx->max_smem;
+}
+
+int launch_fused_rows32(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
+  cgm::FusedSmem L;
+  L.plan(p.B, p.S);
+  auto k = cgm::fused_rows32_approx_kernel<16>;
+  CGM_PREP(ctx, k, 32, L.total, nullptr);
+  p.sc_base = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->profiling) {
+    e0 = prof_event(ctx);
+    e1 = prof_event(ctx);
+    cudaEventRecord(e0, st);
+  }
+  k<<<static_cast<unsigned>(p.n_sc), 32, L.total, st>>>(p);
+  CGM_CUDA(ctx, cudaGetLastError());
+  if (ctx->profiling) {
+    cudaEventRecord(e1, st);
+    ctx->ev_log.push_back({2, {e0, e1}});
+  }
+  ++ctx->launches;
+  return CGM_OK;
+}
+
 bool precode_small_ok(cgm_ctx* ctx, const cgm::KernelParams& p) {
   if (!(p.S == 0 && p.St > 0 && p.hd_layout && p.U <= 16 && p.B <= 512 && p.B >= 4 && p.B % 2 == 0))
     return false;
@@ -540,6 +587,7 @@ int launch(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
   if (p.n_sc <= 0) return CGM_OK;
   if (p.method != cgm::alt::kCg) return launch_alt(ctx, p, st);
   const int UP = up_of(p.U);
+  if (ctx->policy == 0 && fused_rows32_ok(ctx, p, exact)) return launch_fused_rows32(ctx, p, st);
   if (ctx->policy == 0 && precode_small_ok(ctx, p))
     return UP == 8 ? launch_precode_small<8>(ctx, p, st) : launch_precode_small<16>(ctx, p, st);
   const uintptr_t a = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);

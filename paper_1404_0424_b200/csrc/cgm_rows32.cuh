@@ -17,6 +17,8 @@
 // paid by 64 threads and ~16 warps share an SM.
 #pragma once
 
+#include <type_traits>
+
 #include "cgm_split.cuh"
 
 namespace cgm {
@@ -303,6 +305,283 @@ __global__ void __launch_bounds__(128, 4) solve_rows32_pairs_kernel(const Kernel
   const float gdiag = __ldg(ws + W.g + lane * UP + lane).x;
   rows32_pair<false, true>(p, p.sc_base + lsc, ws + W.mf, base, grow, gdiag, Ps_all[warp],
                            nullptr, nullptr, nullptr);
+}
+
+// Exact-tracker uplink (St = 0), same one-warp-per-(subcarrier, system pair)
+// grid: CG as above with the (alpha, beta) history kept per warp, then the
+// tail of k2_exact_tail done inside the warp -- lanes 0 / 1 run the FP64
+// coefficient recursion of system 0 / 1 (detect.cpp:336-368 on the
+// Chebyshev basis), lane i extracts row i of B = L_K G and L_K from the
+// basis T_1..T_K (coalesced row reads, T Hermitian) and forms mu, nu^2, rho
+// (detect.cpp:375-395) and the LLRs.  Replaces the CTA-per-subcarrier tail
+// whose extraction serialised on one lane group for S = 1 (cfg4).
+__global__ void __launch_bounds__(128, 4) solve_rows32_exact_pairs_kernel(const KernelParams p) {
+  constexpr int UP = 32, NW = 4;
+  __shared__ __align__(16) float2 Ps_all[NW][2 * UP];
+  __shared__ __align__(16) float2 Vs_all[NW][2 * UP];
+  __shared__ float hist_all[NW][2 * kMaxK * 2];
+  __shared__ float coef_all[NW][2][2 * (kMaxK + 2)];
+  __shared__ uint8_t st_all[NW][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = p.S, U = p.U, K = p.K;
+  const int npairs = (S + 1) >> 1;
+  const long item = static_cast<long>(blockIdx.x) * NW + warp;
+  if (item >= p.n_sc * npairs) return;
+  const long lsc = item / npairs;
+  const int base = static_cast<int>(item - lsc * npairs) * 2;
+  const long sc = p.sc_base + lsc;
+  WsOffsets W;
+  W.plan(UP, S, K, true);
+  const float2* ws = p.ws + lsc * W.stride;
+  unsigned long long grow[UP];
+#pragma unroll
+  for (int j = 0; j < UP; ++j) {
+    const float2 g = __ldg(ws + W.g + j * UP + lane);
+    grow[j] = f2pack(g.x, -g.y);
+  }
+  const float gdiag = __ldg(ws + W.g + lane * UP + lane).x;
+  // per-warp arrays indexed by the subcarrier-wide system number (base, base + 1)
+  float* hist = hist_all[warp] - base * K * 2;
+  float2* Vs = Vs_all[warp] - base * UP;
+  uint8_t* sys_st = st_all[warp] - base;
+  rows32_pair<true, true>(p, sc, ws + W.mf, base, grow, gdiag, Ps_all[warp], hist, Vs, sys_st);
+  __syncwarp();
+  // ---------------- coefficient recursion, lane s <-> system base + s (FP64)
+  const float2 cdv = ws[W.cd];
+  const double cc = cdv.x, dd = cdv.y;
+  const int n = K + 2;
+  if (lane < 2 && base + lane < S) {
+    const int sy = base + lane;
+    double l0[kMaxK + 2], l1[kMaxK + 2], l2[kMaxK + 2], tmp[kMaxK + 2], d1[kMaxK + 2];
+    for (int m = 0; m < n; ++m) l0[m] = l1[m] = l2[m] = 0.0;
+    double a_m1 = 1.0, a_m2 = 1.0, b_m1 = 0.0, b_m2 = 0.0;
+    auto mulA = [&](const double* x, double* out) {
+      // A T_0 = c T_0 + d T_1;  A T_m = c T_m + d/2 (T_{m+1} + T_{m-1})
+      for (int m = 0; m < n; ++m) out[m] = cc * x[m];
+      for (int m = 0; m < n; ++m) {
+        const double h = dd * x[m];
+        if (m == 0) {
+          out[1] += h;
+        } else {
+          if (m + 1 < n) out[m + 1] += 0.5 * h;
+          out[m - 1] += 0.5 * h;
+        }
+      }
+    };
+    for (int k = 1; k <= K; ++k) {
+      const double a = hist[(sy * K + (k - 1)) * 2 + 0];
+      const double bb = hist[(sy * K + (k - 1)) * 2 + 1];
+      if (k == 1) {
+        for (int m = 0; m < n; ++m) { l2[m] = l1[m]; l1[m] = l0[m]; l0[m] = 0.0; }
+        l0[0] = a;  // L_1 = alpha_1 I
+      } else {
+        const double c1 = a * (1.0 + b_m1) / a_m1, c2 = a * b_m2 / a_m2;
+        for (int m = 0; m < n; ++m) d1[m] = l0[m] - l1[m];
+        mulA(d1, tmp);
+        for (int m = 0; m < n; ++m) {
+          const double nx = l0[m] + c1 * d1[m] - a * tmp[m] - c2 * (l1[m] - l2[m]);
+          l2[m] = l1[m];
+          l1[m] = l0[m];
+          l0[m] = nx;
+        }
+      }
+      a_m2 = a_m1; a_m1 = a; b_m2 = b_m1; b_m1 = bb;
+    }
+    mulA(l0, tmp);  // B = L (A - rho^-1 I)
+    float* cl = coef_all[warp][lane];
+    float* cbq = cl + (kMaxK + 2);
+    for (int m = 0; m < n; ++m) {
+      cl[m] = static_cast<float>(l0[m]);
+      cbq[m] = static_cast<float>(tmp[m] - static_cast<double>(p.rho_inv_u) * l0[m]);
+    }
+  }
+  __syncwarp();
+  // ---------------- extraction, lane i <-> row i of both systems
+  const float* cl0 = coef_all[warp][0];
+  const float* cb0 = cl0 + (kMaxK + 2);
+  const float* cl1 = coef_all[warp][1];
+  const float* cb1 = cl1 + (kMaxK + 2);
+  const bool has1 = base + 1 < S;
+  const float2* Tw = ws + W.t;
+  const int i = lane;
+  float ib2[2] = {0.f, 0.f}, ibl[2] = {0.f, 0.f}, mu_i[2] = {0.f, 0.f};
+  // the K basis entries of a column pair are loaded together (predicated,
+  // K rounded up to KM) so the L2 / HBM latency is paid once per batch
+  auto extract = [&](auto km_tag) {
+    constexpr int KM = decltype(km_tag)::value;
+#pragma unroll 1
+    for (int j0 = 0; j0 < UP; j0 += 2) {
+      float2 t[2][KM];
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+        for (int m = 1; m <= KM; ++m)
+          t[jj][m - 1] = m <= K ? __ldg(Tw + (m - 1) * UP * UP + (j0 + jj) * UP + i)
+                                : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const int j = j0 + jj;
+        float2 B0 = make_float2(i == j ? cb0[0] : 0.f, 0.f);
+        float2 L0 = make_float2(i == j ? cl0[0] : 0.f, 0.f);
+        float2 B1 = make_float2(i == j ? cb1[0] : 0.f, 0.f);
+        float2 L1 = make_float2(i == j ? cl1[0] : 0.f, 0.f);
+#pragma unroll
+        for (int m = 1; m <= KM; ++m) {
+          if (m > K) break;
+          const float2 tv = cconj(t[jj][m - 1]);  // T_m[i][j] = conj(T_m[j][i])
+          B0.x = fmaf(cb0[m], tv.x, B0.x); B0.y = fmaf(cb0[m], tv.y, B0.y);
+          B1.x = fmaf(cb1[m], tv.x, B1.x); B1.y = fmaf(cb1[m], tv.y, B1.y);
+          if (m < K) {
+            L0.x = fmaf(cl0[m], tv.x, L0.x); L0.y = fmaf(cl0[m], tv.y, L0.y);
+            L1.x = fmaf(cl1[m], tv.x, L1.x); L1.y = fmaf(cl1[m], tv.y, L1.y);
+          }
+        }
+        if (j == i) { mu_i[0] = B0.x; mu_i[1] = B1.x; }
+        else { ib2[0] += cnorm(B0); ib2[1] += cnorm(B1); }
+        ibl[0] += B0.x * L0.x + B0.y * L0.y;  // Re(B_ij conj(L_ij))
+        ibl[1] += B1.x * L1.x + B1.y * L1.y;
+      }
+    }
+  };
+  if (K <= 4) extract(std::integral_constant<int, 4>{});
+  else if (K <= 8) extract(std::integral_constant<int, 8>{});
+  else extract(std::integral_constant<int, kMaxK>{});
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    if (t == 1 && !has1) break;
+    const int sy = base + t;
+    const float nu2 = ib2[t] * p.es + ibl[t] * p.n0;
+    const bool ok = st_all[warp][t] == 0;
+    const float mu = ok ? mu_i[t] : 0.f;
+    const float rr = ok ? (nu2 <= 0.f ? 0.f : mu_i[t] * mu_i[t] / nu2) : 0.f;  // safe_rho
+    const float2 xh = ok ? Vs_all[warp][t * UP + i] : make_float2(0.f, 0.f);
+    if (i < U) {
+      const long o = (sc * S + sy) * static_cast<long>(U) + i;
+      if (p.xhat) p.xhat[o] = xh;
+      if (p.mu) p.mu[o] = mu;
+      if (p.rho) p.rho[o] = rr;
+      if (p.llr) store_llrs_fast(xh, mu, rr, p.bits, p.llr + o * p.bits);
+    }
+    if (p.status && i == 0) p.status[sc * S + sy] = ok ? 0 : 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fully fused approximate-tracker uplink for U = 32 (cfg2): ONE warp per
+// subcarrier does the Gram, the matched filters and all S systems' CG with
+// no workspace round trip and no second kernel.
+//   * H [B][32] and Y [B][S] stream through a two-slot ring of CB-antenna
+//     chunks (cp.async.bulk + one mbarrier per slot, per warp);
+//   * lane u accumulates row u of G = H^H H and its S matched-filter entries
+//     in registers on the packed pipe: per antenna b, with hu = H[b][u],
+//       acc_j += (h_j.x, h_j.y) * hu.x  +  (h_j.y, h_j.x) * (hu.y, -hu.y)
+//     = conj(hu) h_j, H[b][:] and Y[b][:] read as broadcast LDS.128;
+//   * the G row then IS the register-resident row rows32_pair uses, so the
+//     systems run pair by pair straight out of the Gram.
+// The full G row per lane is twice the one-triangle FLOPs, traded for zero
+// synchronisation: the split path's tensor-core channel kernel plus solve
+// kernel spend their time in per-subcarrier pipeline latency, not FLOPs.
+__device__ __forceinline__ unsigned long long f2swap_hl(unsigned long long v) {
+  unsigned long long r;
+  asm("{ .reg .f32 lo, hi; mov.b64 {lo, hi}, %1; mov.b64 %0, {hi, lo}; }" : "=l"(r) : "l"(v));
+  return r;
+}
+
+struct FusedSmem {
+  int bar, ring, slot, hbytes, ybytes, mf, ps, total, cb;
+  __host__ __device__ void plan(int B, int S) {
+    cb = 16;  // antennas per chunk
+    while (cb > 1 && B % cb) cb >>= 1;
+    hbytes = cb * 32 * 8;
+    ybytes = cb * S * 8;
+    slot = (hbytes + ybytes + 15) & ~15;
+    bar = 0;
+    ring = 16;
+    mf = ring + 2 * slot;
+    ps = mf + S * 32 * 8;
+    total = ps + 2 * 32 * 8;
+  }
+};
+
+template <int MAXS>
+__global__ void __launch_bounds__(32) fused_rows32_approx_kernel(const KernelParams p) {
+  constexpr int UP = 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int B = p.B, S = p.S;
+  FusedSmem L;
+  L.plan(B, S);
+  const int CB = L.cb, nch = B / CB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  float2* Ms = reinterpret_cast<float2*>(smem + L.mf);
+  float2* Ps = reinterpret_cast<float2*>(smem + L.ps);
+  const int lane = threadIdx.x;
+  const long sc = p.sc_base + blockIdx.x;
+  const float2* Hg = p.H + sc * static_cast<long>(B) * UP;
+  const float2* Yg = p.Y + sc * static_cast<long>(B) * S;
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  __syncwarp();
+  auto slot_h = [&](int c) { return reinterpret_cast<float2*>(smem + L.ring + (c & 1) * L.slot); };
+  auto issue = [&](int c) {
+    float2* hs = slot_h(c);
+    fence_proxy_async();
+    mbar_expect_tx(bar + (c & 1), static_cast<uint32_t>(L.hbytes + L.ybytes));
+    bulk_g2s(hs, Hg + static_cast<long>(c) * CB * UP, L.hbytes, bar + (c & 1));
+    bulk_g2s(reinterpret_cast<unsigned char*>(hs) + L.hbytes, Yg + static_cast<long>(c) * CB * S,
+             L.ybytes, bar + (c & 1));
+  };
+  if (lane == 0) {
+    issue(0);
+    if (nch > 1) issue(1);
+  }
+  unsigned long long acc[UP], mf[MAXS];
+#pragma unroll
+  for (int j = 0; j < UP; ++j) acc[j] = 0ull;
+#pragma unroll
+  for (int s = 0; s < MAXS; ++s) mf[s] = 0ull;
+  for (int c = 0; c < nch; ++c) {
+    mbar_wait(bar + (c & 1), static_cast<uint32_t>((c >> 1) & 1));
+    const float2* hs = slot_h(c);
+    const float2* ys = reinterpret_cast<const float2*>(reinterpret_cast<const unsigned char*>(hs) + L.hbytes);
+#pragma unroll 2
+    for (int k = 0; k < CB; ++k) {
+      const float2 hu = hs[k * UP + lane];
+      const unsigned long long ux = f2pack(hu.x, hu.x), uy = f2pack(hu.y, -hu.y);
+      const ulonglong2* row = reinterpret_cast<const ulonglong2*>(hs + k * UP);
+#pragma unroll
+      for (int j2 = 0; j2 < UP / 2; ++j2) {
+        const ulonglong2 h2 = row[j2];
+        ffma2(acc[2 * j2], h2.x, ux);
+        ffma2(acc[2 * j2], f2swap_hl(h2.x), uy);
+        ffma2(acc[2 * j2 + 1], h2.y, ux);
+        ffma2(acc[2 * j2 + 1], f2swap_hl(h2.y), uy);
+      }
+      const unsigned long long* yr = reinterpret_cast<const unsigned long long*>(ys + k * S);
+#pragma unroll
+      for (int s = 0; s < MAXS; ++s) {
+        if (s < S) {
+          const unsigned long long y = yr[s];
+          ffma2(mf[s], y, ux);
+          ffma2(mf[s], f2swap_hl(y), uy);
+        }
+      }
+    }
+    __syncwarp();  // every lane done with this slot
+    if (lane == 0 && c + 2 < nch) issue(c + 2);
+  }
+  // matched filters to shared memory ([sys][u], the layout rows32_pair reads)
+#pragma unroll
+  for (int s = 0; s < MAXS; ++s)
+    if (s < S) Ms[s * UP + lane] = f2unpack(mf[s]);
+  float gdiag = 0.f;
+#pragma unroll
+  for (int j = 0; j < UP; ++j)
+    if (j == lane) gdiag = f2unpack(acc[j]).x;
+  __syncwarp();
+  for (int base = 0; base < S; base += 2)
+    rows32_pair<false, true>(p, sc, Ms, base, acc, gdiag, Ps, nullptr, nullptr, nullptr);
 }
 
 }  // namespace cgm
