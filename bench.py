@@ -232,11 +232,11 @@ def ours_arm(args, rank, world, local_rank):
     for i in range(args.steps):
         step(args.warmup + i)
     torch.cuda.synchronize()
-    ch_ms, sv_ms, n_pairs = ctx.kernel_times()
+    ch_ms, bs_ms, sv_ms, n_pairs = ctx.kernel_times_ex()
     ctx.set_profiling(False)
     value = world * cfg.vectors * args.steps / (total_ms / 1e3)
     # the hot path of one step is one channel + one solve launch per L2 chunk
-    kernel_ms = (ch_ms + sv_ms) / args.steps
+    kernel_ms = (ch_ms + bs_ms + sv_ms) / args.steps
 
     # ------------------------------------------------------------ e2e (host)
     def pinned(shape, dtype):
@@ -343,9 +343,19 @@ def ours_arm(args, rank, world, local_rank):
             "algorithmic_bytes": cfg.solve_bytes_per_vector() * cfg.vectors,
             "ms": sv_s * 1e3, "traffic": traffic.get("solve")}
     k_sv["achieved"] = k_sv["algorithmic_flops"] / sv_s / 1e12 if sv_s > 0 else None
-    for k in (k_ch, k_sv):
-        k["frac"] = k["achieved"] / k["peak"] if k["achieved"] else None
-    dom = k_sv if sv_s >= ch_s else k_ch
+    bs_s = bs_ms / args.steps / 1e3
+    k_bs = None
+    if bs_s > 0:  # exact tracker: Chebyshev basis products (cgm_basis.cuh), FP32 bound
+        k_bs = {"kernel": "basis (exact tracker: (K-1) Hermitian U x U products per subcarrier)",
+                "bound": "fp32", "unit": "TFLOP/s", "peak": fp32_peak, "peak_source": fp32_src,
+                "algorithmic_flops": cfg.basis_flops_per_vector() * cfg.vectors,
+                "ms": bs_s * 1e3, "traffic": traffic.get("basis")}
+        k_bs["achieved"] = k_bs["algorithmic_flops"] / bs_s / 1e12
+    for k in (k_ch, k_sv, k_bs):
+        if k is not None:
+            k["frac"] = k["achieved"] / k["peak"] if k["achieved"] else None
+    shares = [(sv_s, k_sv), (ch_s, k_ch)] + ([(bs_s, k_bs)] if k_bs else [])
+    dom_s, dom = max(shares, key=lambda x: x[0])
     if ch_s == 0 and sv_s > 0:
         # one fused kernel does the whole path (U <= 16 precoder,
         # cgm_precode_small.cuh): its roofline is the path's, HBM or FP32
@@ -362,12 +372,13 @@ def ours_arm(args, rank, world, local_rank):
         dom["achieved"] = (bytes_launch / sv_s / 1e9) if hbm else (flops_launch / sv_s / 1e12)
         dom["frac"] = dom["achieved"] / dom["peak"]
         k_sv = dom
+        dom_s = sv_s
         k_ch = {"kernel": "(fused into the single kernel)", "ms": 0.0, "frac": None}
     roof = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
             "unit": dom["unit"], "frac": dom["frac"], "traffic": dom["traffic"],
             "peak_source": dom["peak_source"], "kernel": dom["kernel"],
-            "share_of_step": (sv_s if dom is k_sv else ch_s) / max(ch_s + sv_s, 1e-12),
-            "kernels": {"channel": k_ch, "solve": k_sv},
+            "share_of_step": dom_s / max(ch_s + bs_s + sv_s, 1e-12),
+            "kernels": {"channel": k_ch, "solve": k_sv, **({"basis": k_bs} if k_bs else {})},
             "pair": {"kernel_ms": kernel_ms, "launch_pairs_per_step": n_pairs / args.steps,
                      "algorithmic_flops": flops_launch, "algorithmic_bytes": bytes_launch,
                      "tflops": flops_launch / (kernel_ms / 1e3) / 1e12,

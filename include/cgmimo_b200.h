@@ -77,6 +77,10 @@ int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy);
  * number of channel-kernel launches since profiling was (re)enabled. */
 int cgm_ctx_set_profiling(cgm_ctx* ctx, int on);
 int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, long* launches);
+/* Same, with the exact tracker's Chebyshev basis kernel (cgm_basis.cuh)
+ * reported on its own (cgm_ctx_kernel_times adds it to channel_ms). */
+int cgm_ctx_kernel_times_ex(cgm_ctx* ctx, double* channel_ms, double* basis_ms, double* solve_ms,
+                            long* launches);
 const char* cgm_last_error(const cgm_ctx* ctx);
 /* kernels this context has launched since creation (the bench's gpu_launches) */
 long cgm_kernel_launches(const cgm_ctx* ctx);

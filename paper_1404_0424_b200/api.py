@@ -97,6 +97,14 @@ class Context:
     def set_profiling(self, on: bool):
         self._check(self.lib.cgm_ctx_set_profiling(self.h, 1 if on else 0))
 
+    def kernel_times_ex(self):
+        """(channel_ms, basis_ms, solve_ms, launches) summed since profiling was
+        enabled; basis = the exact tracker's Chebyshev basis kernel."""
+        a, b, c, n = C.c_double(), C.c_double(), C.c_double(), C.c_long()
+        self._check(self.lib.cgm_ctx_kernel_times_ex(self.h, C.byref(a), C.byref(b), C.byref(c),
+                                                     C.byref(n)))
+        return a.value, b.value, c.value, n.value
+
     def kernel_times(self):
         """(channel_ms, solve_ms, launches) summed since profiling was enabled."""
         a, b, n = C.c_double(), C.c_double(), C.c_long()

@@ -95,8 +95,23 @@ class Config:
             b += 8 * self.B
         return b
 
+    def tracker_basis_flops_per_vector(self) -> float:
+        """The exact tracker's U^3 recursion, (K-1) 4U(U+1)(U+2) per VECTOR in
+        the reference (detect.cpp:336-368) -- part of flops_per_vector."""
+        if self.kind not in ("uplink", "both") or self.tracker != "exact":
+            return 0.0
+        U, K = self.U, self.K
+        return (K - 1) * 4 * U * (U + 1) * (U + 2)
+
+    def basis_flops_per_vector(self) -> float:
+        """What the basis kernel (cgm_basis.cuh) does: the same (K-1) Hermitian
+        products once per SUBCARRIER, shared by its S vectors."""
+        return self.tracker_basis_flops_per_vector() / self.S
+
     def solve_flops_per_vector(self) -> float:
-        return self.flops_per_vector() - self.channel_flops_per_vector()
+        """CG, tracker extraction, LLRs (+ precoder): the rest of the path."""
+        return (self.flops_per_vector() - self.channel_flops_per_vector()
+                - self.tracker_basis_flops_per_vector())
 
     def solve_bytes_per_vector(self) -> float:
         """Outputs written by the solve kernel (+ t read, H re-read by the precoder)."""

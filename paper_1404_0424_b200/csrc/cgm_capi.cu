@@ -430,12 +430,22 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
     }
     k1<<<static_cast<unsigned>(g1), nt1, smem1, s1>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
+    if (ctx->profiling) cudaEventRecord(e1, s1);
     if (kb) {
+      cudaEvent_t b0 = nullptr, b1 = nullptr;
+      if (ctx->profiling) {
+        b0 = prof_event(ctx);
+        b1 = prof_event(ctx);
+        cudaEventRecord(b0, s1);
+      }
       kb<<<static_cast<unsigned>((n + nb_spc - 1) / nb_spc), nb_t, nb_smem, s1>>>(p);
       CGM_CUDA(ctx, cudaGetLastError());
+      if (ctx->profiling) {
+        cudaEventRecord(b1, s1);
+        ctx->ev_log.push_back({3, {b0, b1}});
+      }
       ctx->launches += 1;
     }
-    if (ctx->profiling) cudaEventRecord(e1, s1);
     if (overlap) {
       CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[1 + half], s1));
       CGM_CUDA(ctx, cudaStreamWaitEvent(s2, ctx->ov_ev[1 + half], 0));
@@ -912,18 +922,26 @@ int cgm_ctx_set_profiling(cgm_ctx* ctx, int on) {
   return CGM_OK;
 }
 
-int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, long* launches) {
-  if (!ctx || !channel_ms || !solve_ms || !launches) return CGM_EINVAL;
-  *channel_ms = *solve_ms = 0.0;
+int cgm_ctx_kernel_times_ex(cgm_ctx* ctx, double* channel_ms, double* basis_ms, double* solve_ms,
+                            long* launches) {
+  if (!ctx || !channel_ms || !basis_ms || !solve_ms || !launches) return CGM_EINVAL;
+  *channel_ms = *basis_ms = *solve_ms = 0.0;
   *launches = 0;
   for (auto& rec : ctx->ev_log) {
     CGM_CUDA(ctx, cudaEventSynchronize(rec.second.second));
     float ms = 0.f;
     CGM_CUDA(ctx, cudaEventElapsedTime(&ms, rec.second.first, rec.second.second));
-    (rec.first == 1 ? *channel_ms : *solve_ms) += ms;
+    (rec.first == 1 ? *channel_ms : rec.first == 3 ? *basis_ms : *solve_ms) += ms;
     if (rec.first == 1) ++*launches;
   }
   return CGM_OK;
+}
+
+int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, long* launches) {
+  double basis = 0.0;
+  const int rc = cgm_ctx_kernel_times_ex(ctx, channel_ms, &basis, solve_ms, launches);
+  if (rc == CGM_OK) *channel_ms += basis;  // basis products counted with the channel stage
+  return rc;
 }
 
 int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy) {
