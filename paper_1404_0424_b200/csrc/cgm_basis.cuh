@@ -14,9 +14,9 @@
 //   * Ahat, T_m, T_{m-1} of each subcarrier in shared memory; per k the
 //     thread reads four entries of row k of Ahat (= conj of column k, the
 //     matrix is Hermitian) and four of row k of T_m (two LDS.128 each) and
-//     issues 32 packed FFMA2:
-//       a += (t.x, t.y) * ahat.x,  b += (t.x, t.y) * ahat.y,
-//       conj(ahat) t = (a.x + b.y, a.y - b.x);
+//     issues 32 packed FFMA2 into one accumulator pair per entry:
+//       acc += (t.x, t.y) * ahat.x + (t.y, t.x) * (ahat.y, -ahat.y)
+//          = conj(ahat) t  (swap / negated broadcast are operand modifiers);
 //   * U = 32: three subcarriers per 128-thread CTA (108 busy threads),
 //     U = 64: one per 160-thread CTA (136 busy).
 // The centre / half-width (c, d) comes from the same power iteration as
@@ -107,26 +107,37 @@ __global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 3 : 2) basis_kern
   for (int m = 1; m < K; ++m) {
     if (busy) {
       const float2* Tc = base + (slot * 3 + cur) * MAT;
-      unsigned long long a[4][4], b[4][4];
+      // one packed accumulator per entry: conj(ahat) t = t * ahat.x + swap(t) * (ahat.y, -ahat.y)
+      // (the swap and the negated broadcast are FFMA2 operand modifiers);
+      // operands of row k + 1 are loaded while row k is consumed
+      unsigned long long acc[4][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) a[r][c] = b[r][c] = 0ull;
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0ull;
+      auto ld = [&](int k, ulonglong2 (&av)[2], ulonglong2 (&tv)[2]) {
+        av[0] = *reinterpret_cast<const ulonglong2*>(A + k * LD + i0);
+        av[1] = *reinterpret_cast<const ulonglong2*>(A + k * LD + i0 + 2);
+        tv[0] = *reinterpret_cast<const ulonglong2*>(Tc + k * LD + j0);
+        tv[1] = *reinterpret_cast<const ulonglong2*>(Tc + k * LD + j0 + 2);
+      };
+      ulonglong2 av[2], tv[2];
+      ld(0, av, tv);
 #pragma unroll 2
       for (int k = 0; k < UP; ++k) {
-        const ulonglong2 a01 = *reinterpret_cast<const ulonglong2*>(A + k * LD + i0);
-        const ulonglong2 a23 = *reinterpret_cast<const ulonglong2*>(A + k * LD + i0 + 2);
-        const ulonglong2 t01 = *reinterpret_cast<const ulonglong2*>(Tc + k * LD + j0);
-        const ulonglong2 t23 = *reinterpret_cast<const ulonglong2*>(Tc + k * LD + j0 + 2);
-        const unsigned long long ah[4] = {a01.x, a01.y, a23.x, a23.y};
-        const unsigned long long t[4] = {t01.x, t01.y, t23.x, t23.y};
+        const unsigned long long ah[4] = {av[0].x, av[0].y, av[1].x, av[1].y};
+        const unsigned long long t[4] = {tv[0].x, tv[0].y, tv[1].x, tv[1].y};
+        if (k + 1 < UP) ld(k + 1, av, tv);
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < 4; ++r) {
+          const float2 a2 = f2unpack(ah[r]);
+          const unsigned long long ax = f2pack(a2.x, a2.x), ay = f2pack(a2.y, -a2.y);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            ffma2(a[r][c], t[c], f2dup_lo(ah[r]));
-            ffma2(b[r][c], t[c], f2dup_hi(ah[r]));
+            ffma2(acc[r][c], t[c], ax);
+            ffma2(acc[r][c], f2swap_hl(t[c]), ay);
           }
+        }
       }
       // T_{m+1} = 2 Ahat T_m - T_{m-1} into the T_{m-1} buffer (lower +
       // mirror; only this thread reads these lower entries of T_{m-1})
@@ -137,8 +148,7 @@ __global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 3 : 2) basis_kern
         for (int c = 0; c < 4; ++c) {
           const int i = i0 + r, j = j0 + c;
           if (j > i) continue;
-          const float2 A2 = f2unpack(a[r][c]), B2 = f2unpack(b[r][c]);
-          const float2 prod = make_float2(A2.x + B2.y, A2.y - B2.x);
+          const float2 prod = f2unpack(acc[r][c]);
           const float2 prev = m == 1 ? make_float2(i == j ? 1.f : 0.f, 0.f) : Tn[i * LD + j];
           float2 val = make_float2(2.f * prod.x - prev.x, 2.f * prod.y - prev.y);
           if (i == j) val.y = 0.f;

@@ -310,13 +310,18 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   // subcarrier form (any systems, CTA-wide tails), CGMIMO_SOLVE=lanes the
   // lane-per-row kernel
   bool use_rows = false, use_pairs = false;
+  int rows_ns = 2;  // systems per warp of the pairs kernels
   if constexpr (UP == 32) {
     const char* force = env("CGMIMO_SOLVE");
     const bool cta = force && std::strcmp(force, "rows") == 0;
     if (!use_s32 && !force && p.St == 0 && p.K <= cgm::kMaxK) {
       use_rows = use_pairs = true;
       use_pf = false;
-      k2 = EXACT ? cgm::solve_rows32_exact_pairs_kernel : cgm::solve_rows32_pairs_kernel;
+      k2 = EXACT ? cgm::solve_rows32_exact_pairs_kernel : cgm::solve_rows32_pairs_kernel<2>;
+      if (!EXACT && env("CGMIMO_ROWS_NS") && std::atoi(env("CGMIMO_ROWS_NS")) == 4) {
+        k2 = cgm::solve_rows32_pairs_kernel<4>;
+        rows_ns = 4;
+      }
       smem2 = 0;
     } else if (!use_s32 && cta) {
       cgm::Rows32Smem R;
@@ -452,7 +457,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
     }
     if (ctx->profiling) cudaEventRecord(e2, s2);
     if (use_pairs)  // 4 warps per CTA, one (subcarrier, system pair) per warp
-      k2<<<static_cast<unsigned>((n * ((p.S + 1) / 2) + 3) / 4), 128, 0, s2>>>(p);
+      k2<<<static_cast<unsigned>((n * ((p.S + rows_ns - 1) / rows_ns) + 3) / 4), 128, 0, s2>>>(p);
     else
       k2<<<static_cast<unsigned>(std::min(n, g2cap)), 32 * nw2, smem2, s2>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());

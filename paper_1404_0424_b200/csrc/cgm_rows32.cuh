@@ -67,12 +67,13 @@ __device__ __forceinline__ void warp_sum2(float& a, float& b) {
 // UPONLY: every system is an uplink vector with the same K (the
 // approximate-tracker pairs kernel), so the per-system direction / iteration
 // count branches fold away.
-template <bool EXACT, bool UPONLY = false>
+template <bool EXACT, bool UPONLY = false, int NS = 2>
 __device__ __forceinline__ void rows32_pair(const KernelParams& p, long sc, const float2* mfsrc,
                                             int base, const unsigned long long (&grow)[32],
                                             float gdiag, float2* Ps, float* hist, float2* Vs,
                                             uint8_t* sys_st) {
-  constexpr int UP = 32, NS = 2;
+  constexpr int UP = 32;
+  static_assert(NS % 2 == 0, "systems in pairs");
   const int S = p.S, St = p.St, U = p.U;
   const int nsys = S + St;
   const int Kmax = UPONLY ? p.K : (p.K > p.Kt ? p.K : p.Kt);
@@ -105,9 +106,10 @@ __device__ __forceinline__ void rows32_pair(const KernelParams& p, long sc, cons
     bm1[s] = bm2[s] = 0.f;
     f0[s] = f1[s] = f2[s] = 0.f;
   }
-  warp_sum2(rn[0], rn[1]);
-  rn0[0] = rn[0];
-  rn0[1] = rn[1];
+#pragma unroll
+  for (int q = 0; q < NS; q += 2) warp_sum2(rn[q], rn[q + 1]);
+#pragma unroll
+  for (int q = 0; q < NS; ++q) rn0[q] = rn[q];
   __syncwarp();
   for (int k = 1; k <= Kmax; ++k) {
     // e = (G + reg I) p on the packed pipe
@@ -138,7 +140,8 @@ __device__ __forceinline__ void rows32_pair(const KernelParams& p, long sc, cons
       e[s].y = fmaf(reg[s], pp[s].y, e[s].y);
       curv[s] = pp[s].x * e[s].x + pp[s].y * e[s].y;  // Re p^H e
     }
-    warp_sum2(curv[0], curv[1]);
+  #pragma unroll
+  for (int q = 0; q < NS; q += 2) warp_sum2(curv[q], curv[q + 1]);
     float alpha[NS], beta[NS], rnx[NS];
     bool upd[NS];
 #pragma unroll
@@ -158,7 +161,8 @@ __device__ __forceinline__ void rows32_pair(const KernelParams& p, long sc, cons
       }
       rnx[s] = cnorm(r[s]);
     }
-    warp_sum2(rnx[0], rnx[1]);
+  #pragma unroll
+  for (int q = 0; q < NS; q += 2) warp_sum2(rnx[q], rnx[q + 1]);
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       float ia = 1.f;  // 1 / alpha
@@ -284,15 +288,16 @@ __global__ void __launch_bounds__(256, 2) solve_rows32_kernel(const KernelParams
 // hardware scheduler balances (a CTA per subcarrier at 16 warps / SM leaves
 // a 1.01-wave tail on cfg2's 1200 subcarriers).  Each warp reads its G row
 // straight from the L2-resident workspace.
-__global__ void __launch_bounds__(128, 4) solve_rows32_pairs_kernel(const KernelParams p) {
+template <int NS>
+__global__ void __launch_bounds__(128, NS == 2 ? 4 : 3) solve_rows32_pairs_kernel(const KernelParams p) {
   constexpr int UP = 32;
-  __shared__ __align__(16) float2 Ps_all[4][2 * UP];
+  __shared__ __align__(16) float2 Ps_all[4][NS * UP];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int npairs = (p.S + 1) >> 1;
+  const int npairs = (p.S + NS - 1) / NS;
   const long item = static_cast<long>(blockIdx.x) * (blockDim.x >> 5) + warp;
   if (item >= p.n_sc * npairs) return;
   const long lsc = item / npairs;
-  const int base = static_cast<int>(item - lsc * npairs) * 2;
+  const int base = static_cast<int>(item - lsc * npairs) * NS;
   WsOffsets W;
   W.plan(UP, p.S, p.K, false);
   const float2* ws = p.ws + lsc * W.stride;
@@ -303,8 +308,8 @@ __global__ void __launch_bounds__(128, 4) solve_rows32_pairs_kernel(const Kernel
     grow[j] = f2pack(g.x, -g.y);
   }
   const float gdiag = __ldg(ws + W.g + lane * UP + lane).x;
-  rows32_pair<false, true>(p, p.sc_base + lsc, ws + W.mf, base, grow, gdiag, Ps_all[warp],
-                           nullptr, nullptr, nullptr);
+  rows32_pair<false, true, NS>(p, p.sc_base + lsc, ws + W.mf, base, grow, gdiag, Ps_all[warp],
+                               nullptr, nullptr, nullptr);
 }
 
 // Exact-tracker uplink (St = 0), same one-warp-per-(subcarrier, system pair)
