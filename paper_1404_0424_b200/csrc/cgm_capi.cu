@@ -20,6 +20,7 @@
 #include "cgm_alt.cuh"
 #include "cgm_basis.cuh"
 #include "cgm_precode_small.cuh"
+#include "cgm_uplink_small.cuh"
 #include "cgm_rows32.cuh"
 #include "cgm_solve32.cuh"
 #include "cgm_tc.cuh"
@@ -588,6 +589,45 @@ int launch_fused_rows32(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   return CGM_OK;
 }
 
+// Fused small-U CG detector (cgm_uplink_small.cuh): uplink-only calls with
+// U <= 16, one warp per subcarrier.  CGMIMO_UPSMALL=split keeps the pair.
+bool uplink_small_ok(cgm_ctx* ctx, const cgm::KernelParams& p, bool exact) {
+  if (!(p.St == 0 && p.S >= 1 && !p.hd_layout && p.U <= 16 && p.K >= 1 && p.K <= cgm::kMaxK))
+    return false;
+  const char* e = env("CGMIMO_UPSMALL");
+  if (e && std::strcmp(e, "split") == 0) return false;
+  cgm::UpSmallSmem L;
+  L.plan(up_of(p.U), p.B, p.U, p.S, p.K, exact);
+  return L.total <= ctx->max_smem;
+}
+
+template <int UP, bool EXACT>
+int launch_uplink_small(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
+  cgm::UpSmallSmem L;
+  L.plan(UP, p.B, p.U, p.S, p.K, EXACT);
+  auto k = cgm::uplink_small_kernel<UP, EXACT>;
+  int occ = 0;
+  CGM_PREP(ctx, k, 32, L.total, &occ);
+  const long grid = std::max<long>(1, std::min<long>(p.n_sc, static_cast<long>(std::max(occ, 1)) * ctx->sms));
+  const uintptr_t al = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
+  p.use_tma = ((p.B * p.U) % 2 == 0 && (p.B * p.S) % 2 == 0 && (al & 15u) == 0) ? 1 : 0;
+  p.sc_base = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->profiling) {
+    e0 = prof_event(ctx);
+    e1 = prof_event(ctx);
+    cudaEventRecord(e0, st);
+  }
+  k<<<static_cast<unsigned>(grid), 32, L.total, st>>>(p);
+  CGM_CUDA(ctx, cudaGetLastError());
+  if (ctx->profiling) {
+    cudaEventRecord(e1, st);
+    ctx->ev_log.push_back({2, {e0, e1}});
+  }
+  ++ctx->launches;
+  return CGM_OK;
+}
+
 bool precode_small_ok(cgm_ctx* ctx, const cgm::KernelParams& p) {
   if (!(p.S == 0 && p.St > 0 && p.hd_layout && p.U <= 16 && p.B <= 512 && p.B >= 4 && p.B % 2 == 0))
     return false;
@@ -603,6 +643,10 @@ int launch(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
   if (p.method != cgm::alt::kCg) return launch_alt(ctx, p, st);
   const int UP = up_of(p.U);
   if (ctx->policy == 0 && fused_rows32_ok(ctx, p, exact)) return launch_fused_rows32(ctx, p, st);
+  if (ctx->policy == 0 && uplink_small_ok(ctx, p, exact)) {
+    if (UP == 8) return exact ? launch_uplink_small<8, true>(ctx, p, st) : launch_uplink_small<8, false>(ctx, p, st);
+    return exact ? launch_uplink_small<16, true>(ctx, p, st) : launch_uplink_small<16, false>(ctx, p, st);
+  }
   if (ctx->policy == 0 && precode_small_ok(ctx, p))
     return UP == 8 ? launch_precode_small<8>(ctx, p, st) : launch_precode_small<16>(ctx, p, st);
   const uintptr_t a = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);

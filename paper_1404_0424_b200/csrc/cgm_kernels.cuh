@@ -211,6 +211,55 @@ __device__ __forceinline__ void tile_pass(int n_lower, int n_other, int nsb, con
 // sqrt(U) reached below 0 at weak regularisation and lost up to 1.5e-3 in
 // rho at K = 16 (tools/fp32_tracker_study.py "weak": 1.5e-6 with this one).
 // One warp; G Hermitian in smem (read by columns); xs: UP float2 scratch.
+// Exact tracker's three-term recursion (detect.cpp:336-368) on the
+// Chebyshev coefficients of L_k, WARP-PARALLEL: lane m holds coefficient m
+// of L_k, L_{k-1}, L_{k-2} (FP64), the multiplication by A = c + d Ahat
+// couples neighbouring coefficients through shuffles:
+//   A T_0 = c T_0 + d T_1,  A T_m = c T_m + d/2 (T_{m+1} + T_{m-1}).
+// hist: the K (alpha, beta) pairs of one system.  Writes the coefficients of
+// L_K (cl) and of B = L_K (A - rho^-1 I) (cb), K + 2 floats each.  Same
+// values as the per-thread loops of k2_exact_tail (FP64; only the order of
+// two or three additions per coefficient differs).  All 32 lanes must call.
+__device__ __forceinline__ void cheb_coef_warp(const float* hist, int K, double cc, double dd,
+                                               double rho_inv, float* cl, float* cb) {
+  const int m = threadIdx.x & 31;
+  const int n = K + 2;
+  auto mulA = [&](double x) {
+    const double up = __shfl_down_sync(0xffffffffu, x, 1);  // x[m + 1]
+    const double dn = __shfl_up_sync(0xffffffffu, x, 1);    // x[m - 1]
+    double out = cc * x;
+    if (m + 1 < n) out += 0.5 * dd * up;
+    if (m == 1) out += dd * dn;
+    else if (m >= 2 && m < n) out += 0.5 * dd * dn;
+    return m < n ? out : 0.0;
+  };
+  double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+  double a_m1 = 1.0, a_m2 = 1.0, b_m1 = 0.0, b_m2 = 0.0;
+  for (int k = 1; k <= K; ++k) {
+    const double a = hist[(k - 1) * 2 + 0];
+    const double bb = hist[(k - 1) * 2 + 1];
+    if (k == 1) {
+      l2 = l1;
+      l1 = l0;
+      l0 = m == 0 ? a : 0.0;  // L_1 = alpha_1 I
+    } else {
+      const double c1 = a * (1.0 + b_m1) / a_m1, c2 = a * b_m2 / a_m2;
+      const double d1 = l0 - l1;
+      const double t = mulA(d1);
+      const double nx = l0 + c1 * d1 - a * t - c2 * (l1 - l2);
+      l2 = l1;
+      l1 = l0;
+      l0 = m < n ? nx : 0.0;
+    }
+    a_m2 = a_m1; a_m1 = a; b_m2 = b_m1; b_m1 = bb;
+  }
+  const double t = mulA(l0);  // B = L (A - rho^-1 I)
+  if (m < n) {
+    cl[m] = static_cast<float>(l0);
+    cb[m] = static_cast<float>(t - rho_inv * l0);
+  }
+}
+
 template <int UP, int LDG = UP>
 __device__ __forceinline__ float2 cheb_interval(const float2* Gs, float reg, float2* xs, int lane) {
   constexpr int RU = UP < 32 ? 1 : UP / 32;

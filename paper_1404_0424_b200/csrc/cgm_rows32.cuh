@@ -351,55 +351,12 @@ __global__ void __launch_bounds__(128, 4) solve_rows32_exact_pairs_kernel(const 
   uint8_t* sys_st = st_all[warp] - base;
   rows32_pair<true, true>(p, sc, ws + W.mf, base, grow, gdiag, Ps_all[warp], hist, Vs, sys_st);
   __syncwarp();
-  // ---------------- coefficient recursion, lane s <-> system base + s (FP64)
+  // ---------------- coefficient recursion of both systems, warp-parallel (FP64)
   const float2 cdv = ws[W.cd];
-  const double cc = cdv.x, dd = cdv.y;
-  const int n = K + 2;
-  if (lane < 2 && base + lane < S) {
-    const int sy = base + lane;
-    double l0[kMaxK + 2], l1[kMaxK + 2], l2[kMaxK + 2], tmp[kMaxK + 2], d1[kMaxK + 2];
-    for (int m = 0; m < n; ++m) l0[m] = l1[m] = l2[m] = 0.0;
-    double a_m1 = 1.0, a_m2 = 1.0, b_m1 = 0.0, b_m2 = 0.0;
-    auto mulA = [&](const double* x, double* out) {
-      // A T_0 = c T_0 + d T_1;  A T_m = c T_m + d/2 (T_{m+1} + T_{m-1})
-      for (int m = 0; m < n; ++m) out[m] = cc * x[m];
-      for (int m = 0; m < n; ++m) {
-        const double h = dd * x[m];
-        if (m == 0) {
-          out[1] += h;
-        } else {
-          if (m + 1 < n) out[m + 1] += 0.5 * h;
-          out[m - 1] += 0.5 * h;
-        }
-      }
-    };
-    for (int k = 1; k <= K; ++k) {
-      const double a = hist[(sy * K + (k - 1)) * 2 + 0];
-      const double bb = hist[(sy * K + (k - 1)) * 2 + 1];
-      if (k == 1) {
-        for (int m = 0; m < n; ++m) { l2[m] = l1[m]; l1[m] = l0[m]; l0[m] = 0.0; }
-        l0[0] = a;  // L_1 = alpha_1 I
-      } else {
-        const double c1 = a * (1.0 + b_m1) / a_m1, c2 = a * b_m2 / a_m2;
-        for (int m = 0; m < n; ++m) d1[m] = l0[m] - l1[m];
-        mulA(d1, tmp);
-        for (int m = 0; m < n; ++m) {
-          const double nx = l0[m] + c1 * d1[m] - a * tmp[m] - c2 * (l1[m] - l2[m]);
-          l2[m] = l1[m];
-          l1[m] = l0[m];
-          l0[m] = nx;
-        }
-      }
-      a_m2 = a_m1; a_m1 = a; b_m2 = b_m1; b_m1 = bb;
-    }
-    mulA(l0, tmp);  // B = L (A - rho^-1 I)
-    float* cl = coef_all[warp][lane];
-    float* cbq = cl + (kMaxK + 2);
-    for (int m = 0; m < n; ++m) {
-      cl[m] = static_cast<float>(l0[m]);
-      cbq[m] = static_cast<float>(tmp[m] - static_cast<double>(p.rho_inv_u) * l0[m]);
-    }
-  }
+  for (int t = 0; t < 2; ++t)
+    if (base + t < S)
+      cheb_coef_warp(hist_all[warp] + t * K * 2, K, cdv.x, cdv.y, p.rho_inv_u, coef_all[warp][t],
+                     coef_all[warp][t] + (kMaxK + 2));
   __syncwarp();
   // ---------------- extraction, lane i <-> row i of both systems
   const float* cl0 = coef_all[warp][0];
