@@ -17,7 +17,8 @@
 //     issues 32 packed FFMA2 into one accumulator pair per entry:
 //       acc += (t.x, t.y) * ahat.x + (t.y, t.x) * (ahat.y, -ahat.y)
 //          = conj(ahat) t  (swap / negated broadcast are operand modifiers);
-//   * U = 32: three subcarriers per 128-thread CTA (108 busy threads),
+//   * U = 32: two subcarriers per 96-thread CTA (72 busy threads; four CTAs
+//     fit the shared memory of an SM),
 //     U = 64: one per 160-thread CTA (136 busy).
 // The centre / half-width (c, d) comes from the same power iteration as
 // before (cheb_interval, one warp per subcarrier).  Output: (c, d) and
@@ -32,7 +33,7 @@ template <int UP>
 struct BasisGeo {
   static constexpr int NB = UP / 4;                  // tile rows
   static constexpr int NTILE = NB * (NB + 1) / 2;    // lower-triangle tiles
-  static constexpr int SPC = UP == 32 ? 3 : 1;       // subcarriers per CTA
+  static constexpr int SPC = UP == 32 ? 2 : 1;       // subcarriers per CTA (smem: 4 CTAs / SM)
   static constexpr int NT = ((SPC * NTILE + 31) / 32) * 32;
   static constexpr int LD = UP + 2;                  // padded row (bank spread, 16 B aligned)
   static constexpr int MAT = UP * LD;                // float2 per matrix in smem
@@ -40,7 +41,7 @@ struct BasisGeo {
 };
 
 template <int UP>
-__global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 3 : 2) basis_kernel(const KernelParams p) {
+__global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 4 : 2) basis_kernel(const KernelParams p) {
   using BG = BasisGeo<UP>;
   constexpr int MAT = BG::MAT, SPC = BG::SPC, LD = BG::LD;
   extern __shared__ __align__(128) unsigned char smem[];
