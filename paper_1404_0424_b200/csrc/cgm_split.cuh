@@ -22,6 +22,8 @@
 // warps -- fusing them into one CTA serialises the two regimes.
 #pragma once
 
+#include <type_traits>
+
 #include "cgm_kernels.cuh"
 
 namespace cgm {
@@ -395,52 +397,11 @@ __device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float
     const int K = p.K;
     const float2 cdv = ws[W.cd];
     const double cc = cdv.x, dd = cdv.y;
-    for (int s = tid; s < S; s += nt) {
-      // three-term recursion (detect.cpp:336-368) on Chebyshev coefficients, FP64
-      double l0[kMaxK + 2], l1[kMaxK + 2], l2[kMaxK + 2], tmp[kMaxK + 2], d1[kMaxK + 2];
-      const int n = K + 2;
-      for (int m = 0; m < n; ++m) l0[m] = l1[m] = l2[m] = 0.0;
-      double a_m1 = 1.0, a_m2 = 1.0, b_m1 = 0.0, b_m2 = 0.0;
-      auto mulA = [&](const double* x, double* out) {
-        // A T_0 = c T_0 + d T_1;  A T_m = c T_m + d/2 (T_{m+1} + T_{m-1})
-        for (int m = 0; m < n; ++m) out[m] = cc * x[m];
-        for (int m = 0; m < n; ++m) {
-          const double h = dd * x[m];
-          if (m == 0) {
-            out[1] += h;
-          } else {
-            if (m + 1 < n) out[m + 1] += 0.5 * h;
-            out[m - 1] += 0.5 * h;
-          }
-        }
-      };
-      for (int k = 1; k <= K; ++k) {
-        const double a = hist[(s * Kmax + (k - 1)) * 2 + 0];
-        const double bb = hist[(s * Kmax + (k - 1)) * 2 + 1];
-        if (k == 1) {
-          for (int m = 0; m < n; ++m) { l2[m] = l1[m]; l1[m] = l0[m]; l0[m] = 0.0; }
-          l0[0] = a;  // L_1 = alpha_1 I
-        } else {
-          const double c1 = a * (1.0 + b_m1) / a_m1, c2 = a * b_m2 / a_m2;
-          for (int m = 0; m < n; ++m) d1[m] = l0[m] - l1[m];
-          mulA(d1, tmp);
-          for (int m = 0; m < n; ++m) {
-            const double nx = l0[m] + c1 * d1[m] - a * tmp[m] - c2 * (l1[m] - l2[m]);
-            l2[m] = l1[m];
-            l1[m] = l0[m];
-            l0[m] = nx;
-          }
-        }
-        a_m2 = a_m1; a_m1 = a; b_m2 = b_m1; b_m1 = bb;
-      }
-      // B = L (A - rho^-1 I)  (G = unregularised A, detect.cpp:215)
-      mulA(l0, tmp);
+    // three-term recursion (detect.cpp:336-368) on the Chebyshev
+    // coefficients, FP64, one warp per system (cheb_coef_warp)
+    for (int s = tid >> 5; s < S; s += nt >> 5) {
       float* cl = coef + s * 2 * (K + 2);
-      float* cb = cl + (K + 2);
-      for (int m = 0; m < n; ++m) {
-        cl[m] = static_cast<float>(l0[m]);
-        cb[m] = static_cast<float>(tmp[m] - static_cast<double>(p.rho_inv_u) * l0[m]);
-      }
+      cheb_coef_warp(hist + s * Kmax * 2, K, cc, dd, p.rho_inv_u, cl, cl + (K + 2));
     }
     sync();
     // extraction (detect.cpp:375-395): thread <-> (row i, pair of systems);
@@ -457,25 +418,47 @@ __device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float
         const float* cl1 = coef + (has1 ? s1 : s0) * 2 * (K + 2);
         const float* cb1 = cl1 + (K + 2);
         float ib2[2] = {0.f, 0.f}, ibl[2] = {0.f, 0.f}, mu_i[2] = {0.f, 0.f};
-        for (int j = 0; j < UP; ++j) {
-          float2 B0 = make_float2(i == j ? cb0[0] : 0.f, 0.f);
-          float2 L0 = make_float2(i == j ? cl0[0] : 0.f, 0.f);
-          float2 B1 = make_float2(i == j ? cb1[0] : 0.f, 0.f);
-          float2 L1 = make_float2(i == j ? cl1[0] : 0.f, 0.f);
-          for (int m = 1; m <= K; ++m) {
-            const float2 t = cconj(__ldg(Tw + (m - 1) * UP * UP + j * UP + i));  // T_m[i][j]
-            B0.x = fmaf(cb0[m], t.x, B0.x); B0.y = fmaf(cb0[m], t.y, B0.y);
-            B1.x = fmaf(cb1[m], t.x, B1.x); B1.y = fmaf(cb1[m], t.y, B1.y);
-            if (m < K) {
-              L0.x = fmaf(cl0[m], t.x, L0.x); L0.y = fmaf(cl0[m], t.y, L0.y);
-              L1.x = fmaf(cl1[m], t.x, L1.x); L1.y = fmaf(cl1[m], t.y, L1.y);
+        // the K basis entries of a column pair are loaded together
+        // (predicated, K rounded up to KM): one L2 latency per batch
+        auto extract = [&](auto km_tag) {
+          constexpr int KM = decltype(km_tag)::value;
+#pragma unroll 1
+          for (int j0 = 0; j0 < UP; j0 += 2) {
+            float2 tv[2][KM];
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+              for (int m = 1; m <= KM; ++m)
+                tv[jj][m - 1] = m <= K ? __ldg(Tw + (m - 1) * UP * UP + (j0 + jj) * UP + i)
+                                       : make_float2(0.f, 0.f);
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              const int j = j0 + jj;
+              float2 B0 = make_float2(i == j ? cb0[0] : 0.f, 0.f);
+              float2 L0 = make_float2(i == j ? cl0[0] : 0.f, 0.f);
+              float2 B1 = make_float2(i == j ? cb1[0] : 0.f, 0.f);
+              float2 L1 = make_float2(i == j ? cl1[0] : 0.f, 0.f);
+#pragma unroll
+              for (int m = 1; m <= KM; ++m) {
+                if (m > K) break;
+                const float2 t = cconj(tv[jj][m - 1]);  // T_m[i][j]
+                B0.x = fmaf(cb0[m], t.x, B0.x); B0.y = fmaf(cb0[m], t.y, B0.y);
+                B1.x = fmaf(cb1[m], t.x, B1.x); B1.y = fmaf(cb1[m], t.y, B1.y);
+                if (m < K) {
+                  L0.x = fmaf(cl0[m], t.x, L0.x); L0.y = fmaf(cl0[m], t.y, L0.y);
+                  L1.x = fmaf(cl1[m], t.x, L1.x); L1.y = fmaf(cl1[m], t.y, L1.y);
+                }
+              }
+              if (j == i) { mu_i[0] = B0.x; mu_i[1] = B1.x; }
+              else { ib2[0] += cnorm(B0); ib2[1] += cnorm(B1); }
+              ibl[0] += B0.x * L0.x + B0.y * L0.y;  // Re(B_ij conj(L_ij))
+              ibl[1] += B1.x * L1.x + B1.y * L1.y;
             }
           }
-          if (j == i) { mu_i[0] = B0.x; mu_i[1] = B1.x; }
-          else { ib2[0] += cnorm(B0); ib2[1] += cnorm(B1); }
-          ibl[0] += B0.x * L0.x + B0.y * L0.y;  // Re(B_ij conj(L_ij))
-          ibl[1] += B1.x * L1.x + B1.y * L1.y;
-        }
+        };
+        if (K <= 4) extract(std::integral_constant<int, 4>{});
+        else if (K <= 8) extract(std::integral_constant<int, 8>{});
+        else extract(std::integral_constant<int, kMaxK>{});
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           if (t == 1 && !has1) break;
@@ -540,7 +523,7 @@ __device__ __forceinline__ void k2_precode_tail(const KernelParams& p, long sc, 
           }
         } else {
           const float2* hu = p.H + sc * static_cast<long>(B) * UP + bb * UP;  // row b of H_u
-#pragma unroll 4
+#pragma unroll 8
           for (int u = 0; u < UP; u += 2) {
             const float4 h = __ldg(reinterpret_cast<const float4*>(hu + u));
 #pragma unroll
