@@ -298,3 +298,29 @@ def test_fused_small_precoder_matches_split_and_oracle(gpu_ctx, checker, monkeyp
     idx = np.arange(0, n_sc, 37)
     want = checker.precode(Hd[idx].cpu().numpy(), T[idx].cpu().numpy(), 0.625, K, threads=8)
     check_precode({k: v[idx].cpu().numpy() for k, v in a.items()}, want, f"fused U={U} B={B}")
+
+
+@pytest.mark.parametrize("B,U,S,K,tracker,bits", [
+    (40, 20, 3, 3, "approx", 4),   # U in 17..31: pairs kernel with padded lanes
+    (40, 20, 3, 3, "exact", 4),    # exact pairs kernel, odd S
+    (64, 27, 1, 6, "exact", 6),
+    (96, 31, 2, 5, "approx", 6),
+    (33, 13, 5, 4, "exact", 4),    # fused U <= 16 kernel, odd B (no bulk copies)
+    (48, 3, 7, 2, "exact", 2),     # several systems per warp group, QPSK
+    (50, 16, 4, 8, "approx", 6),
+])
+def test_ragged_shapes_match_oracle(gpu_ctx, checker, B, U, S, K, tracker, bits):
+    """Ragged U (between the kernels' row widths), odd B and S, several
+    systems per subcarrier: the default kernels against the oracle."""
+    g = torch.Generator().manual_seed(B * 100 + U)
+    n_sc = 50
+    H = torch.complex(torch.randn(n_sc, B, U, generator=g), torch.randn(n_sc, B, U, generator=g))
+    Y = torch.complex(torch.randn(n_sc, B, S, generator=g), torch.randn(n_sc, B, S, generator=g))
+    H, Y = (H / 2 ** 0.5).cuda(), (Y * 2.0).cuda()
+    n0 = 0.3 * U / B
+    out = gpu_ctx.detect_cg(H, Y, 1.0 / n0, n0, 1.0, bits, K, tracker)
+    torch.cuda.synchronize()
+    want = checker.detect(H.cpu().numpy(), Y.cpu().numpy(), 1.0 / n0, n0, 1.0, bits, K, tracker,
+                          threads=8)
+    check_detect({k: v.cpu().numpy() for k, v in out.items()}, want,
+                 f"B={B} U={U} S={S} K={K} {tracker}")
