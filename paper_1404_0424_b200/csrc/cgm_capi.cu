@@ -312,6 +312,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   // lane-per-row kernel
   bool use_rows = false, use_pairs = false;
   int rows_ns = 2;  // systems per warp of the pairs kernels
+  bool rows_pf = false;
   if constexpr (UP == 32) {
     const char* force = env("CGMIMO_SOLVE");
     const bool cta = force && std::strcmp(force, "rows") == 0;
@@ -319,11 +320,15 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       use_rows = use_pairs = true;
       use_pf = false;
       k2 = EXACT ? cgm::solve_rows32_exact_pairs_kernel : cgm::solve_rows32_pairs_kernel<2>;
+      smem2 = 0;
       if (!EXACT && env("CGMIMO_ROWS_NS") && std::atoi(env("CGMIMO_ROWS_NS")) == 4) {
         k2 = cgm::solve_rows32_pairs_kernel<4>;
         rows_ns = 4;
+      } else if (!EXACT && env("CGMIMO_ROWS_PF") && std::atoi(env("CGMIMO_ROWS_PF")) == 1) {
+        k2 = cgm::solve_rows32_pairs_pf_kernel;  // persistent, next item prefetched
+        rows_pf = true;
+        smem2 = 4 * (32 * 32 + 6 * 32) * 8;
       }
-      smem2 = 0;
     } else if (!use_s32 && cta) {
       cgm::Rows32Smem R;
       R.plan(p.B, p.S, p.St, Kmax, EXACT);
@@ -457,7 +462,10 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       CGM_CUDA(ctx, cudaStreamWaitEvent(s2, ctx->ov_ev[1 + half], 0));
     }
     if (ctx->profiling) cudaEventRecord(e2, s2);
-    if (use_pairs)  // 4 warps per CTA, one (subcarrier, system pair) per warp
+    if (use_pairs && rows_pf)  // persistent: four CTAs per SM
+      k2<<<static_cast<unsigned>(std::min<long>((n * ((p.S + 1) / 2) + 3) / 4, 4L * ctx->sms)), 128,
+           smem2, s2>>>(p);
+    else if (use_pairs)  // 4 warps per CTA, one (subcarrier, system pair) per warp
       k2<<<static_cast<unsigned>((n * ((p.S + rows_ns - 1) / rows_ns) + 3) / 4), 128, 0, s2>>>(p);
     else
       k2<<<static_cast<unsigned>(std::min(n, g2cap)), 32 * nw2, smem2, s2>>>(p);

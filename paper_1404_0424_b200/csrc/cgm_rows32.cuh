@@ -312,6 +312,68 @@ __global__ void __launch_bounds__(128, NS == 2 ? 4 : 3) solve_rows32_pairs_kerne
                                nullptr, nullptr, nullptr);
 }
 
+// Persistent form of the approximate pairs kernel: warp w walks items w,
+// w + (warps in the grid), ... and copies the NEXT item's G (8 KB) and
+// matched filters into its shared slot with cp.async while the current
+// item's CG runs, so the per-item L2 latency of the G row / b loads (the
+// largest stall of the one-shot kernel) leaves the critical path.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__global__ void __launch_bounds__(128, 4) solve_rows32_pairs_pf_kernel(const KernelParams p) {
+  constexpr int UP = 32, NW = 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  // per warp: G [32][32], next-item MF [2][32], current MF [2][32], Ps [2][32]
+  constexpr int SLOT = (UP * UP + 6 * UP) * 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float2* Gb = reinterpret_cast<float2*>(smem + warp * SLOT);
+  float2* MFn = Gb + UP * UP;
+  float2* MFc = MFn + 2 * UP;
+  float2* Ps = MFc + 2 * UP;
+  const int S = p.S;
+  const int npairs = (S + 1) >> 1;
+  const long n_items = p.n_sc * npairs;
+  const long stride = static_cast<long>(gridDim.x) * NW;
+  WsOffsets W;
+  W.plan(UP, S, p.K, false);
+  auto prefetch = [&](long item) {
+    const long lsc = item / npairs;
+    const int base = static_cast<int>(item - lsc * npairs) * 2;
+    const float2* ws = p.ws + lsc * W.stride;
+#pragma unroll
+    for (int c = 0; c < UP * UP / 2 / 32; ++c)  // 16 B chunks of G, coalesced
+      cp_async16(Gb + 2 * (c * 32 + lane), ws + W.g + 2 * (c * 32 + lane));
+    // the pair's two matched-filter rows (one row when base + 1 == S)
+    if (lane < (base + 1 < S ? 32 : 16)) cp_async16(MFn + 2 * lane, ws + W.mf + base * UP + 2 * lane);
+    cp_async_commit();
+  };
+  long item = static_cast<long>(blockIdx.x) * NW + warp;
+  if (item < n_items) prefetch(item);
+  for (; item < n_items; item += stride) {
+    cp_async_wait_all();
+    __syncwarp();
+    const long lsc = item / npairs;
+    const int base = static_cast<int>(item - lsc * npairs) * 2;
+    unsigned long long grow[UP];
+#pragma unroll
+    for (int j = 0; j < UP; ++j) {
+      const float2 g = Gb[j * UP + lane];  // G[j][u]: row u of G = conj of column u
+      grow[j] = f2pack(g.x, -g.y);
+    }
+    const float gdiag = Gb[lane * UP + lane].x;
+    MFc[lane] = MFn[lane];
+    MFc[UP + lane] = MFn[UP + lane];
+    __syncwarp();  // Gb / MFn consumed: the next item may land there
+    if (item + stride < n_items) prefetch(item + stride);
+    rows32_pair<false, true, 2>(p, p.sc_base + lsc, MFc - base * UP, base, grow, gdiag, Ps,
+                                nullptr, nullptr, nullptr);
+    __syncwarp();
+  }
+}
+
 // Exact-tracker uplink (St = 0), same one-warp-per-(subcarrier, system pair)
 // grid: CG as above with the (alpha, beta) history kept per warp, then the
 // tail of k2_exact_tail done inside the warp -- lanes 0 / 1 run the FP64
