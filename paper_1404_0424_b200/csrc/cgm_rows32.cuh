@@ -235,7 +235,7 @@ template <bool EXACT>
 __global__ void __launch_bounds__(256, 2) solve_rows32_kernel(const KernelParams p) {
   constexpr int UP = 32;
   extern __shared__ __align__(128) unsigned char smem[];
-  const int S = p.S, St = p.St, B = p.B, U = p.U;
+  const int S = p.S, St = p.St, B = p.B;
   const int nsys = S + St;
   const int Kmax = p.K > p.Kt ? p.K : p.Kt;
   Rows32Smem R;
@@ -325,7 +325,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 __global__ void __launch_bounds__(128, 4) solve_rows32_pairs_pf_kernel(const KernelParams p) {
   constexpr int UP = 32, NW = 4;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   // per warp: G [32][32], next-item MF [2][32], current MF [2][32], Ps [2][32]
   constexpr int SLOT = (UP * UP + 6 * UP) * 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
