@@ -360,30 +360,36 @@ def ours_arm(args, rank, world, local_rank):
     ch_s = ch_ms / args.steps / 1e3
     sv_s = sv_ms / args.steps / 1e3
     traffic = read_traffic(cfg.name) or {}
-    k_ch = {"kernel": "channel (Gram + matched filter [+ Chebyshev basis]; tcgen05 for U = 32)",
-            "bound": "hbm", "unit": "GB/s", "peak": peaks["hbm_gbs"],
-            "peak_source": f"hbm_gbs of {peaks['source']}",
-            "algorithmic_bytes": cfg.channel_bytes_per_vector() * cfg.vectors,
-            "algorithmic_flops": cfg.channel_flops_per_vector() * cfg.vectors,
-            "ms": ch_s * 1e3, "traffic": traffic.get("channel")}
-    k_ch["achieved"] = k_ch["algorithmic_bytes"] / ch_s / 1e9 if ch_s > 0 else None
-    k_sv = {"kernel": "solve (CG + SINR tracker + LLR [+ precoder])", "bound": "fp32",
-            "unit": "TFLOP/s", "peak": fp32_peak, "peak_source": fp32_src,
-            "algorithmic_flops": cfg.solve_flops_per_vector() * cfg.vectors,
-            "algorithmic_bytes": cfg.solve_bytes_per_vector() * cfg.vectors,
-            "ms": sv_s * 1e3, "traffic": traffic.get("solve")}
-    k_sv["achieved"] = k_sv["algorithmic_flops"] / sv_s / 1e12 if sv_s > 0 else None
+
+    def kernel_roof(name, flops, nbytes, secs, trf):
+        """north_star's roofline for one kernel: the slower of its algorithmic
+        FLOPs at the FP32 peak and its algorithmic bytes at the HBM peak
+        (SURVEY 8(d)); achieved / frac in that bound's unit."""
+        t_fp = flops / (fp32_peak * 1e12)
+        t_hbm = nbytes / (peaks["hbm_gbs"] * 1e9)
+        hbm = t_hbm >= t_fp
+        k = {"kernel": name, "bound": "hbm" if hbm else "fp32",
+             "unit": "GB/s" if hbm else "TFLOP/s",
+             "peak": peaks["hbm_gbs"] if hbm else fp32_peak,
+             "peak_source": f"hbm_gbs of {peaks['source']}" if hbm else fp32_src,
+             "algorithmic_flops": flops, "algorithmic_bytes": nbytes,
+             "roofline_ms": max(t_fp, t_hbm) * 1e3, "ms": secs * 1e3, "traffic": trf}
+        k["achieved"] = ((nbytes / secs / 1e9) if hbm else (flops / secs / 1e12)) if secs > 0 else None
+        k["frac"] = k["achieved"] / k["peak"] if k["achieved"] else None
+        return k
+
+    k_ch = kernel_roof("channel (Gram + matched filter; tcgen05 for U = 32)",
+                       cfg.channel_flops_per_vector() * cfg.vectors,
+                       cfg.channel_bytes_per_vector() * cfg.vectors, ch_s, traffic.get("channel"))
+    k_sv = kernel_roof("solve (CG + SINR tracker + LLR [+ precoder])",
+                       cfg.solve_flops_per_vector() * cfg.vectors,
+                       cfg.solve_bytes_per_vector() * cfg.vectors, sv_s, traffic.get("solve"))
     bs_s = bs_ms / args.steps / 1e3
     k_bs = None
-    if bs_s > 0:  # exact tracker: Chebyshev basis products (cgm_basis.cuh), FP32 bound
-        k_bs = {"kernel": "basis (exact tracker: (K-1) Hermitian U x U products per subcarrier)",
-                "bound": "fp32", "unit": "TFLOP/s", "peak": fp32_peak, "peak_source": fp32_src,
-                "algorithmic_flops": cfg.basis_flops_per_vector() * cfg.vectors,
-                "ms": bs_s * 1e3, "traffic": traffic.get("basis")}
-        k_bs["achieved"] = k_bs["algorithmic_flops"] / bs_s / 1e12
-    for k in (k_ch, k_sv, k_bs):
-        if k is not None:
-            k["frac"] = k["achieved"] / k["peak"] if k["achieved"] else None
+    if bs_s > 0:  # exact tracker: Chebyshev basis products (cgm_basis.cuh)
+        k_bs = kernel_roof("basis (exact tracker: (K-1) Hermitian U x U products per subcarrier)",
+                           cfg.basis_flops_per_vector() * cfg.vectors, 0.0, bs_s,
+                           traffic.get("basis"))
     shares = [(sv_s, k_sv), (ch_s, k_ch)] + ([(bs_s, k_bs)] if k_bs else [])
     dom_s, dom = max(shares, key=lambda x: x[0])
     if ch_s == 0 and sv_s > 0:
