@@ -151,7 +151,7 @@ __device__ __forceinline__ void rows32_pair(const KernelParams& p, long sc, cons
       const bool go = step && !frozen && !broke[s];
       if (go && curv[s] < 1e-30f) broke[s] = true;  // solvers.cpp:55-57
       upd[s] = go && !broke[s];
-      alpha[s] = upd[s] ? rn[s] * __frcp_rn(curv[s]) : 1.f;
+      alpha[s] = upd[s] ? __fdividef(rn[s], curv[s]) : 1.f;
       beta[s] = 0.f;
       if (upd[s]) {
         v[s].x = fmaf(alpha[s], pp[s].x, v[s].x);
@@ -167,7 +167,7 @@ __device__ __forceinline__ void rows32_pair(const KernelParams& p, long sc, cons
     for (int s = 0; s < NS; ++s) {
       float ia = 1.f;  // 1 / alpha
       if (upd[s]) {
-        const float irn = __frcp_rn(rn[s]);
+        const float irn = __fdividef(1.f, rn[s]);  // MUFU.RCP: no IEEE slow-path call
         beta[s] = rnx[s] * irn;
         ia = curv[s] * irn;
         rn[s] = rnx[s];
