@@ -274,7 +274,8 @@ __global__ void __launch_bounds__(256, 2) solve_rows32_kernel(const KernelParams
   auto sync = [] { __syncthreads(); };
   if (EXACT && S > 0) {
     sync();
-    k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st, nt, sync);
+    k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st, nt, sync,
+                      reinterpret_cast<float*>(smem + L.xp));
   }
   if (St > 0) {
     sync();

@@ -362,7 +362,7 @@ struct K2Geo {
 
 template <int UP>
 struct K2Smem {
-  int gs, ps, vs, qs, hist, sys_st, mu, rho, coef, gpart, total;
+  int gs, ps, vs, qs, hist, sys_st, mu, rho, coef, gpart, xp, total;
   __host__ __device__ static int align(int x) { return (x + 127) & ~127; }
   __host__ __device__ void plan(int B, int S, int St, int K, bool exact) {
     const int nsys = S + St;
@@ -377,6 +377,7 @@ struct K2Smem {
     rho = o; o = align(o + (exact ? S * UP * 4 : 0));
     coef = o; o = align(o + (exact ? S * 2 * (K + 2) * 4 : 0));
     gpart = o; o = align(o + ((B + 31) / 32) * (St > 0 ? St : 1) * 4);
+    xp = o; o = align(o + (exact ? 3 * 8 * UP * 4 : 0));  // S = 1 extraction partials
     total = o;
   }
 };
@@ -391,7 +392,8 @@ __device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float
                                               const WsOffsets& W, long sc, int Kmax,
                                               const float* hist, float* coef, float* MUs,
                                               float* RHOs, const float2* Vs,
-                                              const uint8_t* sys_st, int nt, Sync&& sync) {
+                                              const uint8_t* sys_st, int nt, Sync&& sync,
+                                              float* xp = nullptr) {
   const int tid = threadIdx.x;
   const int S = p.S, U = p.U;
     const int K = p.K;
@@ -409,9 +411,13 @@ __device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float
     const float2* Tw = ws + W.t;
     const int ngrp = nt / UP;
     const int i = tid % UP, g = tid / UP;
+    // one vector per subcarrier (cfg4): the groups split the columns j of the
+    // single system instead of idling at the barrier, partial sums in xp
+    const bool jsplit = xp != nullptr && S == 1 && ngrp > 1 && ngrp <= 8;
     if (g < ngrp) {
-      for (int s0 = g; s0 < S; s0 += 2 * ngrp) {
-        const int s1 = s0 + ngrp;
+      for (int s0 = jsplit ? 0 : g; s0 < S; s0 += jsplit ? S : 2 * ngrp) {
+        const int s1 = jsplit ? S : s0 + ngrp;
+        const int jb = jsplit ? g * (UP / ngrp) : 0, je = jsplit ? jb + UP / ngrp : UP;
         const bool has1 = s1 < S;
         const float* cl0 = coef + s0 * 2 * (K + 2);
         const float* cb0 = cl0 + (K + 2);
@@ -423,7 +429,7 @@ __device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float
         auto extract = [&](auto km_tag) {
           constexpr int KM = decltype(km_tag)::value;
 #pragma unroll 1
-          for (int j0 = 0; j0 < UP; j0 += 2) {
+          for (int j0 = jb; j0 < je; j0 += 2) {
             float2 tv[2][KM];
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj)
@@ -459,6 +465,12 @@ __device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float
         if (K <= 4) extract(std::integral_constant<int, 4>{});
         else if (K <= 8) extract(std::integral_constant<int, 8>{});
         else extract(std::integral_constant<int, kMaxK>{});
+        if (jsplit) {
+          xp[(g * 3 + 0) * UP + i] = ib2[0];
+          xp[(g * 3 + 1) * UP + i] = ibl[0];
+          xp[(g * 3 + 2) * UP + i] = mu_i[0];
+          continue;
+        }
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           if (t == 1 && !has1) break;
@@ -467,6 +479,20 @@ __device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float
           MUs[s * UP + i] = mu_i[t];
           RHOs[s * UP + i] = nu2 <= 0.f ? 0.f : mu_i[t] * mu_i[t] / nu2;  // safe_rho
         }
+      }
+    }
+    if (jsplit) {
+      sync();
+      if (g == 0) {  // fixed-order sum of the column parts
+        float b2 = 0.f, bl = 0.f, mu = 0.f;
+        for (int q = 0; q < ngrp; ++q) {
+          b2 += xp[(q * 3 + 0) * UP + i];
+          bl += xp[(q * 3 + 1) * UP + i];
+          mu += xp[(q * 3 + 2) * UP + i];
+        }
+        const float nu2 = b2 * p.es + bl * p.n0;
+        MUs[i] = mu;
+        RHOs[i] = nu2 <= 0.f ? 0.f : mu * mu / nu2;  // safe_rho
       }
     }
     sync();
@@ -841,7 +867,8 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
   // ------------------------------------------ exact tracker extraction
   if (EXACT && S > 0) {
     sync();
-    k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st, nt, sync);
+    k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st, nt, sync,
+                      reinterpret_cast<float*>(smem + L.xp));
   }
   // ------------------------------------------------ precode q = H_d^H v
   if (St > 0) {
