@@ -210,11 +210,22 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   // K1: persistent, two TMA stages (prefetch one subcarrier ahead)
   cgm::K1Split sp;
   sp.plan(UP, p.B, p.S);
+  // exact tracker, U = 32 / 64: the Chebyshev basis products run in their
+  // own kernel (cgm_basis.cuh), so the channel kernel needs no basis buffers;
+  // CGMIMO_BASIS=inline keeps them in the channel kernel
+  bool basis_ext = false;
+  if constexpr (EXACT && (UP == 32 || UP == 64)) {
+    const char* e = env("CGMIMO_BASIS");
+    basis_ext = p.S > 0 && p.K > 0 && !(e && std::strcmp(e, "inline") == 0) &&
+                cgm::BasisGeo<UP>::SMEM <= ctx->max_smem;
+  }
+  p.basis_ext = basis_ext ? 1 : 0;
+  const bool k1_basis = EXACT && !basis_ext;
   cgm::K1Smem<UP> L1;
-  L1.plan(p.B, p.S, EXACT, 2);
+  L1.plan(p.B, p.S, k1_basis, 2);
   if (L1.total > ctx->max_smem) {  // very large B: single stage
     sp.nstage = 1;
-    L1.plan(p.B, p.S, EXACT, 1);
+    L1.plan(p.B, p.S, k1_basis, 1);
   }
   p.k1_pair = sp.nstage;
   p.k1_spl = sp.spl;
@@ -347,19 +358,15 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   void (*kb)(cgm::KernelParams) = nullptr;
   int nb_t = 0, nb_smem = 0, nb_spc = 1;
   if constexpr (EXACT && (UP == 32 || UP == 64)) {
-    const char* e = env("CGMIMO_BASIS");
-    if (p.S > 0 && p.K > 0 && !(e && std::strcmp(e, "inline") == 0)) {
+    if (basis_ext) {
       using BG = cgm::BasisGeo<UP>;
-      if (BG::SMEM <= ctx->max_smem) {
-        kb = cgm::basis_kernel<UP>;
-        nb_t = BG::NT;
-        nb_smem = BG::SMEM;
-        nb_spc = BG::SPC;
-        CGM_PREP(ctx, kb, nb_t, nb_smem, nullptr);
-      }
+      kb = cgm::basis_kernel<UP>;
+      nb_t = BG::NT;
+      nb_smem = BG::SMEM;
+      nb_spc = BG::SPC;
+      CGM_PREP(ctx, kb, nb_t, nb_smem, nullptr);
     }
   }
-  p.basis_ext = kb ? 1 : 0;
   int occ1 = 0;
   CGM_PREP(ctx, k1, nt1, smem1, &occ1);
   if (occ1 < 1) return fail(ctx, CGM_EINVAL, "channel kernel does not fit on an SM");

@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p
   extern __shared__ __align__(128) unsigned char smem[];
   const int spl = p.k1_spl, nstage = p.k1_pair;
   K1Smem<UP> L;
-  L.plan(p.B, p.S, EXACT, nstage);
+  L.plan(p.B, p.S, EXACT && !p.basis_ext, nstage);  // no basis buffers when basis_kernel runs
   WsOffsets W;
   W.plan(UP, p.S, p.K, EXACT);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar);
