@@ -335,6 +335,9 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       if (!EXACT && env("CGMIMO_ROWS_NS") && std::atoi(env("CGMIMO_ROWS_NS")) == 4) {
         k2 = cgm::solve_rows32_pairs_kernel<4>;
         rows_ns = 4;
+      } else if (!EXACT && env("CGMIMO_ROWS_NS") && std::atoi(env("CGMIMO_ROWS_NS")) == 1) {
+        k2 = cgm::solve_rows32_pairs_kernel<1>;
+        rows_ns = 1;
       } else if (!EXACT && env("CGMIMO_ROWS_PF") && std::atoi(env("CGMIMO_ROWS_PF")) == 1) {
         k2 = cgm::solve_rows32_pairs_pf_kernel;  // persistent, next item prefetched
         rows_pf = true;

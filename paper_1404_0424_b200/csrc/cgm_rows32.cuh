@@ -73,7 +73,7 @@ __device__ __forceinline__ void rows32_pair(const KernelParams& p, long sc, cons
                                             float gdiag, float2* Ps, float* hist, float2* Vs,
                                             uint8_t* sys_st) {
   constexpr int UP = 32;
-  static_assert(NS % 2 == 0, "systems in pairs");
+  static_assert(NS == 1 || NS % 2 == 0, "one system or systems in pairs");
   const int S = p.S, St = p.St, U = p.U;
   const int nsys = S + St;
   const int Kmax = UPONLY ? p.K : (p.K > p.Kt ? p.K : p.Kt);
@@ -106,8 +106,12 @@ __device__ __forceinline__ void rows32_pair(const KernelParams& p, long sc, cons
     bm1[s] = bm2[s] = 0.f;
     f0[s] = f1[s] = f2[s] = 0.f;
   }
+  if constexpr (NS == 1) {
+    rn[0] = group_sum<32>(rn[0]);
+  } else {
 #pragma unroll
-  for (int q = 0; q < NS; q += 2) warp_sum2(rn[q], rn[q + 1]);
+    for (int q = 0; q < NS; q += 2) warp_sum2(rn[q], rn[q + 1 < NS ? q + 1 : q]);
+  }
 #pragma unroll
   for (int q = 0; q < NS; ++q) rn0[q] = rn[q];
   __syncwarp();
@@ -140,8 +144,12 @@ __device__ __forceinline__ void rows32_pair(const KernelParams& p, long sc, cons
       e[s].y = fmaf(reg[s], pp[s].y, e[s].y);
       curv[s] = pp[s].x * e[s].x + pp[s].y * e[s].y;  // Re p^H e
     }
-  #pragma unroll
-  for (int q = 0; q < NS; q += 2) warp_sum2(curv[q], curv[q + 1]);
+    if constexpr (NS == 1) {
+    curv[0] = group_sum<32>(curv[0]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < NS; q += 2) warp_sum2(curv[q], curv[q + 1 < NS ? q + 1 : q]);
+  }
     float alpha[NS], beta[NS], rnx[NS];
     bool upd[NS];
 #pragma unroll
@@ -161,8 +169,12 @@ __device__ __forceinline__ void rows32_pair(const KernelParams& p, long sc, cons
       }
       rnx[s] = cnorm(r[s]);
     }
-  #pragma unroll
-  for (int q = 0; q < NS; q += 2) warp_sum2(rnx[q], rnx[q + 1]);
+    if constexpr (NS == 1) {
+    rnx[0] = group_sum<32>(rnx[0]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < NS; q += 2) warp_sum2(rnx[q], rnx[q + 1 < NS ? q + 1 : q]);
+  }
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       float ia = 1.f;  // 1 / alpha
@@ -290,7 +302,7 @@ __global__ void __launch_bounds__(256, 2) solve_rows32_kernel(const KernelParams
 // a 1.01-wave tail on cfg2's 1200 subcarriers).  Each warp reads its G row
 // straight from the L2-resident workspace.
 template <int NS>
-__global__ void __launch_bounds__(128, NS == 2 ? 4 : 3) solve_rows32_pairs_kernel(const KernelParams p) {
+__global__ void __launch_bounds__(128, NS == 1 ? 5 : NS == 2 ? 4 : 3) solve_rows32_pairs_kernel(const KernelParams p) {
   constexpr int UP = 32;
   __shared__ __align__(16) float2 Ps_all[4][NS * UP];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

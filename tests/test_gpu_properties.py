@@ -227,6 +227,7 @@ def test_precode_uplink_layout_equals_downlink_layout(gpu_ctx, U, B, K):
     ("cfg2", "CGMIMO_FUSED", "1"),           # opt-in: one fused warp per subcarrier
     ("cfg2", "CGMIMO_SOLVE", "lanes"),       # default: Gram-row-in-registers pairs kernel
     ("cfg2", "CGMIMO_ROWS_NS", "4"),         # four systems per warp
+    ("cfg2", "CGMIMO_ROWS_NS", "1"),         # one system per warp
     ("cfg2", "CGMIMO_ROWS_PF", "1"),         # persistent, next item prefetched
     ("cfg4a_K8", "CGMIMO_SOLVE", "rows"),    # CTA-per-subcarrier rows kernel, exact tail
     ("cfg4a_K2", "CGMIMO_SOLVE", "lanes"),   # default: exact pairs kernel (tail in the warp)
