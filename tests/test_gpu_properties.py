@@ -327,3 +327,43 @@ def test_ragged_shapes_match_oracle(gpu_ctx, checker, B, U, S, K, tracker, bits)
                           threads=8)
     check_detect({k: v.cpu().numpy() for k, v in out.items()}, want,
                  f"B={B} U={U} S={S} K={K} {tracker}")
+
+
+@pytest.mark.parametrize("U,tracker", [(8, "exact"), (8, "approx"), (32, "approx"), (32, "exact"),
+                                       (20, "exact"), (64, "exact")])
+def test_uplink_breakdown_flagged_per_instance_every_kernel(gpu_ctx, U, tracker):
+    """Curvature below 1e-30 (solvers.cpp:55-57) in one subcarrier: its
+    vectors are flagged (status 1) with zeroed outputs, the neighbours are
+    untouched -- through each uplink kernel family (fused U <= 16, U = 32
+    pairs, U = 64 lane-per-row)."""
+    g = torch.Generator().manual_seed(U)
+    n_sc, B, S = 5, 2 * U + 16, 3
+    H = torch.complex(torch.randn(n_sc, B, U, generator=g), torch.randn(n_sc, B, U, generator=g))
+    Y = torch.complex(torch.randn(n_sc, B, S, generator=g), torch.randn(n_sc, B, S, generator=g))
+    H[2] *= 1e-10  # p^H A p ~ 1e-40 with rho^-1 = 1e-35: breakdown, while r0 != 0
+    H, Y = H.cuda(), Y.cuda()
+    out = gpu_ctx.detect_cg(H, Y, 1e35, 1.0, 1.0, 4, 3, tracker)
+    torch.cuda.synchronize()
+    st = out["status"].cpu()
+    assert (st[2] == 1).all(), st
+    assert (st[[0, 1, 3, 4]] == 0).all(), st
+    for k in ("xhat", "mu", "rho", "llr"):
+        assert float(out[k][2].abs().max()) == 0.0, k
+        assert float(out[k][[0, 1, 3, 4]].abs().max()) > 0.0, k
+
+
+@pytest.mark.parametrize("U,tracker", [(32, "approx"), (32, "exact"), (12, "exact"), (64, "approx")])
+def test_zero_observation_every_kernel(gpu_ctx, U, tracker):
+    """y = 0 gives x_hat = 0 and LLR exactly 0 on the sign bits (16-QAM bits
+    0 and 2; test_detect.cpp:406-422), status 0 (frozen, not broken), through
+    each uplink kernel family."""
+    g = torch.Generator().manual_seed(7 + U)
+    n_sc, B, S = 4, 2 * U + 8, 2
+    H = torch.complex(torch.randn(n_sc, B, U, generator=g), torch.randn(n_sc, B, U, generator=g))
+    Y = torch.zeros(n_sc, B, S, dtype=torch.complex64)
+    out = gpu_ctx.detect_cg(H.cuda(), Y.cuda(), 3.0, 0.3, 1.0, 4, 3, tracker)
+    torch.cuda.synchronize()
+    assert int(out["status"].sum()) == 0
+    assert float(out["xhat"].abs().max()) == 0.0
+    llr = out["llr"].cpu()
+    assert float(llr[..., 0].abs().max()) == 0.0 and float(llr[..., 2].abs().max()) == 0.0
