@@ -326,7 +326,9 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   bool rows_pf = false;
   if constexpr (UP == 32) {
     const char* force = env("CGMIMO_SOLVE");
-    const bool cta = force && std::strcmp(force, "rows") == 0;
+    // uplink + precoding on the same channels (cfg5): the CTA-per-subcarrier
+    // rows kernel with 8 warps (11.6 vs 12.7 ms for the persistent lane kernel)
+    const bool cta = force ? std::strcmp(force, "rows") == 0 : (p.S > 0 && p.St > 0);
     if (!use_s32 && !force && p.St == 0 && p.K <= cgm::kMaxK) {
       use_rows = use_pairs = true;
       use_pf = false;
@@ -383,7 +385,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   nw2 = std::max(1, std::min(8, nw2));
   if (use_s32) nw2 = ((nsys + ts2 - 1) / ts2 * 8 + 31) / 32;  // 8 threads per tile, whole warps
   if (use_rows) {
-    nw2 = 2;
+    nw2 = (p.S + p.St) >= 16 ? 8 : 2;
     if (const char* e = env("CGMIMO_ROWS_WARPS")) nw2 = std::max(1, std::min(8, std::atoi(e)));
   }
   long g2cap = 1L << 40;

@@ -232,7 +232,7 @@ def test_precode_uplink_layout_equals_downlink_layout(gpu_ctx, U, B, K):
     ("cfg4a_K8", "CGMIMO_SOLVE", "rows"),    # CTA-per-subcarrier rows kernel, exact tail
     ("cfg4a_K2", "CGMIMO_SOLVE", "lanes"),   # default: exact pairs kernel (tail in the warp)
     ("cfg4a_K8", "CGMIMO_SOLVE", "lanes"),
-    ("cfg5", "CGMIMO_SOLVE", "rows"),        # ... with precoder systems
+    ("cfg5", "CGMIMO_SOLVE", "pf"),          # default: CTA rows kernel; pf = persistent lane kernel
     ("cfg1", "CGMIMO_UPSMALL", "split"),     # default: fused U <= 16 detector, one warp per subcarrier
     ("cfg4a_K8", "CGMIMO_BASIS", "inline"),  # default: basis_kernel (cgm_basis.cuh)
     ("cfg4b_K4", "CGMIMO_BASIS", "inline"),
