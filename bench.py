@@ -378,17 +378,25 @@ def ours_arm(args, rank, world, local_rank):
         k["frac"] = k["achieved"] / k["peak"] if k["achieved"] else None
         return k
 
+    # one vector per subcarrier, U in 17..64, exact: the basis kernel also
+    # does the extraction (basis_kernel<UP, true>, p.fx in the C ABI) -- its
+    # FLOPs move from the solve kernel's credit to the basis kernel's
+    fx = (cfg.kind == "uplink" and cfg.tracker == "exact" and cfg.S == 1 and 16 < cfg.U <= 64
+          and os.environ.get("CGMIMO_FX") != "0" and not os.environ.get("CGMIMO_SOLVE")
+          and os.environ.get("CGMIMO_BASIS") != "inline")
+    f_ext = cfg.tracker_extract_flops_per_vector() * cfg.vectors if fx else 0.0
     k_ch = kernel_roof("channel (Gram + matched filter; tcgen05 for U = 32)",
                        cfg.channel_flops_per_vector() * cfg.vectors,
                        cfg.channel_bytes_per_vector() * cfg.vectors, ch_s, traffic.get("channel"))
-    k_sv = kernel_roof("solve (CG + SINR tracker + LLR [+ precoder])",
-                       cfg.solve_flops_per_vector() * cfg.vectors,
+    k_sv = kernel_roof("solve (CG + SINR tracker + LLR [+ precoder])" if not fx else "solve (CG)",
+                       cfg.solve_flops_per_vector() * cfg.vectors - f_ext,
                        cfg.solve_bytes_per_vector() * cfg.vectors, sv_s, traffic.get("solve"))
     bs_s = bs_ms / args.steps / 1e3
     k_bs = None
     if bs_s > 0:  # exact tracker: Chebyshev basis products (cgm_basis.cuh)
-        k_bs = kernel_roof("basis (exact tracker: (K-1) Hermitian U x U products per subcarrier)",
-                           cfg.basis_flops_per_vector() * cfg.vectors, 0.0, bs_s,
+        k_bs = kernel_roof("basis (exact tracker: (K-1) Hermitian U x U products per subcarrier"
+                           + (" + extraction + LLRs, fused)" if fx else ")"),
+                           cfg.basis_flops_per_vector() * cfg.vectors + f_ext, 0.0, bs_s,
                            traffic.get("basis"))
     shares = [(sv_s, k_sv), (ch_s, k_ch)] + ([(bs_s, k_bs)] if k_bs else [])
     dom_s, dom = max(shares, key=lambda x: x[0])

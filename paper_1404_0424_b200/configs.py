@@ -103,6 +103,13 @@ class Config:
         U, K = self.U, self.K
         return (K - 1) * 4 * U * (U + 1) * (U + 2)
 
+    def tracker_extract_flops_per_vector(self) -> float:
+        """The exact tracker's extraction (detect.cpp:370-395), per vector."""
+        if self.kind not in ("uplink", "both") or self.tracker != "exact":
+            return 0.0
+        U = self.U
+        return 4 * U * U * (U + 1) + 8 * U * U
+
     def basis_flops_per_vector(self) -> float:
         """What the basis kernel (cgm_basis.cuh) does: the same (K-1) Hermitian
         products once per SUBCARRIER, shared by its S vectors."""

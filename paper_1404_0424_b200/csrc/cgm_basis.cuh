@@ -40,7 +40,13 @@ struct BasisGeo {
   static constexpr int SMEM = SPC * 3 * MAT * 8;     // Ahat, T_m, T_{m-1}
 };
 
-template <int UP>
+// FX (one vector per subcarrier, p.fx): the basis never leaves the chip --
+// the CG kernel left (alpha, beta) in the workspace, the coefficients of L_K
+// and B = L_K G are formed here first, every tile accumulates its entries of
+// B and L while the products run, and the extraction (detect.cpp:375-395)
+// and the LLRs finish in this kernel.  Saves writing and re-reading K U x U
+// matrices per subcarrier (cfg4b K = 8: 34 GB of HBM traffic).
+template <int UP, bool FX = false>
 __global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 4 : 2) basis_kernel(const KernelParams p) {
   using BG = BasisGeo<UP>;
   constexpr int MAT = BG::MAT, SPC = BG::SPC, LD = BG::LD;
@@ -49,7 +55,7 @@ __global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 4 : 2) basis_kern
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = p.K;
   WsOffsets W;
-  W.plan(UP, p.S, K, true);
+  W.plan(UP, p.S, K, true, p.fx);
   const long sc0 = static_cast<long>(blockIdx.x) * SPC;
   const int nsc = static_cast<int>(p.n_sc - sc0 < SPC ? p.n_sc - sc0 : SPC);
   auto Ah = [&](int s) { return base + (s * 3 + 0) * MAT; };
@@ -71,11 +77,18 @@ __global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 4 : 2) basis_kern
   __syncthreads();
   // ------------------------------------- (c, d) by power iteration, warp s
   __shared__ float2 cds[SPC];
+  // FX: also the Chebyshev coefficients of L_K and B from the CG history
+  __shared__ float coefs[FX ? SPC : 1][2][kMaxK + 2];
   if (warp < nsc) {
+    // cheb_interval returns the same (c, d) on every lane of the warp
     const float2 cd = cheb_interval<UP, LD>(Ah(warp), p.rho_inv_u, base + (warp * 3 + 1) * MAT, lane);
     if (lane == 0) {
       cds[warp] = cd;
       p.ws[(sc0 + warp) * W.stride + W.cd] = cd;
+    }
+    if (FX) {
+      const float* hist = reinterpret_cast<const float*>(p.ws + (sc0 + warp) * W.stride + W.t);
+      cheb_coef_warp(hist, K, cd.x, cd.y, p.rho_inv_u, coefs[warp][0], coefs[warp][1]);
     }
   }
   __syncthreads();
@@ -90,7 +103,7 @@ __global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 4 : 2) basis_kern
       if (r == c) v.x += p.rho_inv_u - cc;
       v = cscale(invd, v);
       a[r * LD + c] = v;
-      Tw[e] = v;
+      if (!FX) Tw[e] = v;
     }
   }
   __syncthreads();
@@ -103,6 +116,23 @@ __global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 4 : 2) basis_kern
   const bool busy = slot < nsc;
   const int i0 = rb * 4, j0 = cb * 4;
   const float2* A = base + (slot * 3 + 0) * MAT;
+  // FX: this tile's entries of B = sum_m cb_m T_m and L = sum_{m<K} cl_m T_m
+  float2 Bacc[FX ? 4 : 1][FX ? 4 : 1], Lacc[FX ? 4 : 1][FX ? 4 : 1];
+  if constexpr (FX) {
+    const float* cl = coefs[busy ? slot : 0][0];
+    const float* cbq = coefs[busy ? slot : 0][1];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = i0 + r, j = j0 + c;
+        const float2 t1 = busy ? A[i * LD + j] : make_float2(0.f, 0.f);  // T_1
+        const float d0 = i == j ? 1.f : 0.f;                             // T_0 = I
+        Bacc[r][c] = make_float2(cbq[0] * d0 + cbq[1] * t1.x, cbq[1] * t1.y);
+        Lacc[r][c] = K > 1 ? make_float2(cl[0] * d0 + cl[1] * t1.x, cl[1] * t1.y)
+                           : make_float2(cl[0] * d0, 0.f);
+      }
+  }
   // T_m in buffer `cur`, T_{m-1} in `prv` (1 and 2 alternate)
   int cur = 0, prv = 1;  // cur 0 == Ahat itself for m = 1
   for (int m = 1; m < K; ++m) {
@@ -155,10 +185,20 @@ __global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 4 : 2) basis_kern
           if (i == j) val.y = 0.f;
           Tn[i * LD + j] = val;
           if (i != j) Tn[j * LD + i] = cconj(val);
+          if constexpr (FX) {  // T_{m+1} into this tile's B and L
+            const float cbm = coefs[slot][1][m + 1];
+            Bacc[r][c].x = fmaf(cbm, val.x, Bacc[r][c].x);
+            Bacc[r][c].y = fmaf(cbm, val.y, Bacc[r][c].y);
+            if (m + 1 < K) {
+              const float clm = coefs[slot][0][m + 1];
+              Lacc[r][c].x = fmaf(clm, val.x, Lacc[r][c].x);
+              Lacc[r][c].y = fmaf(clm, val.y, Lacc[r][c].y);
+            }
+          }
         }
     }
     __syncthreads();
-    {  // T_{m+1} -> workspace, coalesced
+    if (!FX) {  // T_{m+1} -> workspace, coalesced
       const int nb = m == 1 ? 1 : prv;
       for (int s = 0; s < nsc; ++s)
         store(p.ws + (sc0 + s) * W.stride + W.t + m * UP * UP, base + (s * 3 + nb) * MAT);
@@ -174,6 +214,73 @@ __global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 4 : 2) basis_kern
         for (int e = tid; e < MAT / 2; e += BG::NT) dst[e] = src[e];
       }
       __syncthreads();
+    }
+  }
+  if constexpr (FX) {
+    // ---------------- extraction (detect.cpp:375-395) from the tile sums:
+    // per lower entry (i, j): |B_ij|^2 and Re(B_ij conj(L_ij)) count for row
+    // i and (i != j, Hermitian) for row j; mu_i = Re B_ii.  Row parts go to
+    // Rb[i][cb], column parts to Cb[j][rb] (each slot written by one tile),
+    // summed in a fixed order below.  Both alias a T buffer no longer read.
+    constexpr int NB = BG::NB;
+    float* Rb = reinterpret_cast<float*>(base + (slot * 3 + 1) * MAT);  // [UP][NB][2]
+    float* Cb = Rb + UP * NB * 2;                                       // [UP][NB][2]
+    float* Mb = Cb + UP * NB * 2;                                       // [UP]
+    static_assert(2 * 2 * 32 * (32 / 4) + 32 <= 32 * (32 + 2) * 2, "partials fit a T buffer");
+    // T buffer 1 may still hold T_K (read by no one now); all products ended at the barrier above
+    if (busy) {
+      float rr2[4] = {0.f, 0.f, 0.f, 0.f}, rrl[4] = {0.f, 0.f, 0.f, 0.f};
+      float cc2[4] = {0.f, 0.f, 0.f, 0.f}, ccl[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int i = i0 + r, j = j0 + c;
+          if (j > i) continue;
+          const float2 b = Bacc[r][c], l = Lacc[r][c];
+          const float wl = b.x * l.x + b.y * l.y;
+          if (i == j) {
+            Mb[i] = b.x;
+            rrl[r] += wl;
+          } else {
+            const float w2 = cnorm(b);
+            rr2[r] += w2; rrl[r] += wl;
+            cc2[c] += w2; ccl[c] += wl;
+          }
+        }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        Rb[((i0 + r) * NB + cb) * 2 + 0] = rr2[r];
+        Rb[((i0 + r) * NB + cb) * 2 + 1] = rrl[r];
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        Cb[((j0 + c) * NB + rb) * 2 + 0] = cc2[c];
+        Cb[((j0 + c) * NB + rb) * 2 + 1] = ccl[c];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < nsc * UP; e += BG::NT) {
+      const int s = e / UP, i = e - s * UP;
+      if (i >= p.U) continue;
+      const float* R = reinterpret_cast<const float*>(base + (s * 3 + 1) * MAT);
+      const float* C = R + UP * NB * 2;
+      const float* M = C + UP * NB * 2;
+      const int rbi = i / 4;
+      float ib2 = 0.f, ibl = 0.f;
+      for (int q = 0; q <= rbi; ++q) { ib2 += R[(i * NB + q) * 2]; ibl += R[(i * NB + q) * 2 + 1]; }
+      for (int q = rbi; q < NB; ++q) { ib2 += C[(i * NB + q) * 2]; ibl += C[(i * NB + q) * 2 + 1]; }
+      const long sc = p.sc_base + sc0 + s;  // S = 1: vector index == subcarrier
+      const long o = sc * static_cast<long>(p.U) + i;
+      const bool ok = p.status ? p.status[sc] == 0 : true;
+      const float mu_i = M[i];
+      const float nu2 = ib2 * p.es + ibl * p.n0;
+      const float mu = ok ? mu_i : 0.f;
+      const float rho = ok ? (nu2 <= 0.f ? 0.f : mu_i * mu_i / nu2) : 0.f;  // safe_rho
+      const float2 xh = p.xhat ? p.xhat[o] : make_float2(0.f, 0.f);
+      if (p.mu) p.mu[o] = mu;
+      if (p.rho) p.rho[o] = rho;
+      if (p.llr) store_llrs_fast(xh, mu, rho, p.bits, p.llr + o * p.bits);
     }
   }
 }

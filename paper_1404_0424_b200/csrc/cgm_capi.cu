@@ -220,6 +220,15 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
                 cgm::BasisGeo<UP>::SMEM <= ctx->max_smem;
   }
   p.basis_ext = basis_ext ? 1 : 0;
+  // one vector per subcarrier (cfg4): the basis kernel also does the
+  // extraction and the LLRs (basis_kernel<UP, true>), run after the CG; the
+  // workspace carries the CG history instead of T_1..T_K.  CGMIMO_FX=0 keeps
+  // the materialised basis; forced solve variants keep it too.
+  {
+    const char* fxe = env("CGMIMO_FX");
+    p.fx = (basis_ext && p.S == 1 && p.St == 0 && !env("CGMIMO_SOLVE") &&
+            !(fxe && std::strcmp(fxe, "0") == 0)) ? 1 : 0;
+  }
   const bool k1_basis = EXACT && !basis_ext;
   cgm::K1Smem<UP> L1;
   L1.plan(p.B, p.S, k1_basis, 2);
@@ -238,7 +247,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
                 "per-subcarrier working set (%d / %d B) exceeds shared memory (%d B)", L1.total,
                 L2.total, ctx->max_smem);
   cgm::WsOffsets W;
-  W.plan(UP, p.S, p.K, EXACT);
+  W.plan(UP, p.S, p.K, EXACT, p.fx);
   void (*k1)(cgm::KernelParams) = cgm::channel_kernel<UP, EXACT>;
   void (*k2)(cgm::KernelParams) = cgm::solve_kernel<UP, EXACT>;
   int smem2 = L2.total;
@@ -365,7 +374,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   if constexpr (EXACT && (UP == 32 || UP == 64)) {
     if (basis_ext) {
       using BG = cgm::BasisGeo<UP>;
-      kb = cgm::basis_kernel<UP>;
+      kb = p.fx ? cgm::basis_kernel<UP, true> : cgm::basis_kernel<UP, false>;
       nb_t = BG::NT;
       nb_smem = BG::SMEM;
       nb_spc = BG::SPC;
@@ -454,7 +463,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
     k1<<<static_cast<unsigned>(g1), nt1, smem1, s1>>>(p);
     CGM_CUDA(ctx, cudaGetLastError());
     if (ctx->profiling) cudaEventRecord(e1, s1);
-    if (kb) {
+    if (kb && !p.fx) {
       cudaEvent_t b0 = nullptr, b1 = nullptr;
       if (ctx->profiling) {
         b0 = prof_event(ctx);
@@ -486,6 +495,21 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       cudaEventRecord(e3, s2);
       ctx->ev_log.push_back({1, {e0, e1}});
       ctx->ev_log.push_back({2, {e2, e3}});
+    }
+    if (kb && p.fx) {  // basis + extraction after the CG
+      cudaEvent_t b0 = nullptr, b1 = nullptr;
+      if (ctx->profiling) {
+        b0 = prof_event(ctx);
+        b1 = prof_event(ctx);
+        cudaEventRecord(b0, s2);
+      }
+      kb<<<static_cast<unsigned>((n + nb_spc - 1) / nb_spc), nb_t, nb_smem, s2>>>(p);
+      CGM_CUDA(ctx, cudaGetLastError());
+      if (ctx->profiling) {
+        cudaEventRecord(b1, s2);
+        ctx->ev_log.push_back({3, {b0, b1}});
+      }
+      ctx->launches += 1;
     }
     if (overlap) CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[3 + half], s2));
     ctx->launches += 2;

@@ -62,6 +62,7 @@ struct KernelParams {
   unsigned long long* trace;    // microbenchmarks only: per-CTA event clocks (null in production)
   int method;                   // sim::Method order: 0 Cholesky, 1 CG, 2 CGLS, 3 Neumann (cgm_alt.cuh)
   int basis_ext;                // exact tracker: the Chebyshev basis comes from basis_kernel (cgm_basis.cuh)
+  int fx;                       // exact tracker, one vector per subcarrier: basis + extraction fused (basis_extract_kernel); the workspace holds the CG history instead of T_1..T_K
 };
 
 // Per-axis Gray amplitude subsets (constellation.cpp:75-84), [qam][p][k],

@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(256, 2) solve_rows32_kernel(const KernelParams
   K2Smem<UP> L;
   L.plan(B, S, St, Kmax, EXACT);
   WsOffsets W;
-  W.plan(UP, S, p.K, EXACT);
+  W.plan(UP, S, p.K, EXACT, p.fx);
   float2* Vs = reinterpret_cast<float2*>(smem + L.vs);
   float2* Qs = reinterpret_cast<float2*>(smem + L.qs);
   float* hist = reinterpret_cast<float*>(smem + L.hist);
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(128, NS == 1 ? 5 : NS == 2 ? 4 : 3) solve_rows
   const long lsc = item / npairs;
   const int base = static_cast<int>(item - lsc * npairs) * NS;
   WsOffsets W;
-  W.plan(UP, p.S, p.K, false);
+  W.plan(UP, p.S, p.K, false, p.fx);
   const float2* ws = p.ws + lsc * W.stride;
   unsigned long long grow[UP];
 #pragma unroll
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(128, 4) solve_rows32_pairs_pf_kernel(const Ker
   const long n_items = p.n_sc * npairs;
   const long stride = static_cast<long>(gridDim.x) * NW;
   WsOffsets W;
-  W.plan(UP, S, p.K, false);
+  W.plan(UP, S, p.K, false, p.fx);
   auto prefetch = [&](long item) {
     const long lsc = item / npairs;
     const int base = static_cast<int>(item - lsc * npairs) * 2;
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(128, 4) solve_rows32_exact_pairs_kernel(const 
   const int base = static_cast<int>(item - lsc * npairs) * 2;
   const long sc = p.sc_base + lsc;
   WsOffsets W;
-  W.plan(UP, S, K, true);
+  W.plan(UP, S, K, true, p.fx);
   const float2* ws = p.ws + lsc * W.stride;
   unsigned long long grow[UP];
 #pragma unroll
@@ -426,6 +426,22 @@ __global__ void __launch_bounds__(128, 4) solve_rows32_exact_pairs_kernel(const 
   uint8_t* sys_st = st_all[warp] - base;
   rows32_pair<true, true>(p, sc, ws + W.mf, base, grow, gdiag, Ps_all[warp], hist, Vs, sys_st);
   __syncwarp();
+  if (p.fx) {  // basis_extract_kernel finishes: x_hat and status now, the history for it
+    float2* hw = const_cast<float2*>(ws) + W.t;
+    for (int t = 0; t < 2; ++t) {
+      const int sy = base + t;
+      if (sy >= S) break;
+      const bool ok = st_all[warp][t] == 0;
+      if (lane < U && p.xhat)
+        p.xhat[(sc * S + sy) * static_cast<long>(U) + lane] = ok ? Vs_all[warp][t * UP + lane]
+                                                                : make_float2(0.f, 0.f);
+      if (lane < K)
+        hw[sy * K + lane] = make_float2(hist_all[warp][(t * K + lane) * 2],
+                                        hist_all[warp][(t * K + lane) * 2 + 1]);
+      if (lane == 0 && p.status) p.status[sc * S + sy] = ok ? 0 : 1;
+    }
+    return;
+  }
   // ---------------- coefficient recursion of both systems, warp-parallel (FP64)
   const float2 cdv = ws[W.cd];
   for (int t = 0; t < 2; ++t)

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256, 2) solve32_kernel(const KernelParams p) {
   S32Smem L;
   L.plan(p.B, S, St, Kmax, EXACT, TS);
   WsOffsets W;
-  W.plan(UP, S, p.K, EXACT);
+  W.plan(UP, S, p.K, EXACT, p.fx);
   const int nsp = L.nsp;
   float2* Vs = reinterpret_cast<float2*>(smem + L.vs);
   float2* Qs = reinterpret_cast<float2*>(smem + L.qs);

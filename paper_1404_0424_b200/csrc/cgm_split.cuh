@@ -31,12 +31,14 @@ namespace cgm {
 // workspace layout per subcarrier (float2 units)
 struct WsOffsets {
   int g, mf, cd, t, stride;
-  __host__ __device__ void plan(int UP, int S, int K, bool exact) {
+  // fx: the exact tracker's basis is not stored (basis_extract_kernel builds
+  // it on chip); t then holds each system's (alpha, beta) history, K float2
+  __host__ __device__ void plan(int UP, int S, int K, bool exact, int fx = 0) {
     g = 0;
     mf = UP * UP;
     cd = mf + S * UP;
     t = cd + 2;
-    stride = t + (exact ? K * UP * UP : 0);
+    stride = t + (exact ? (fx ? S * K : K * UP * UP) : 0);
     stride = (stride + 1) & ~1;
   }
 };
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p
   K1Smem<UP> L;
   L.plan(p.B, p.S, EXACT && !p.basis_ext, nstage);  // no basis buffers when basis_kernel runs
   WsOffsets W;
-  W.plan(UP, p.S, p.K, EXACT);
+  W.plan(UP, p.S, p.K, EXACT, p.fx);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar);
   float2* Gs = reinterpret_cast<float2*>(smem + L.gs);
   float2* T1 = reinterpret_cast<float2*>(smem + L.tb);
@@ -615,7 +617,7 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
   K2Smem<UP> L;
   L.plan(B, S, St, Kmax, EXACT);
   WsOffsets W;
-  W.plan(UP, S, p.K, EXACT);
+  W.plan(UP, S, p.K, EXACT, p.fx);
   // G (and the matched filters) from the prefetched shared-memory copy of
   // the workspace when the persistent kernel staged one
   const float2* Gs = pre ? pre + W.g : reinterpret_cast<float2*>(smem + L.gs);
@@ -865,7 +867,21 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
   }
 
   // ------------------------------------------ exact tracker extraction
-  if (EXACT && S > 0) {
+  if (EXACT && S > 0 && p.fx) {  // basis_extract_kernel finishes: x_hat, status, history
+    sync();
+    float2* hw = const_cast<float2*>(ws) + W.t;
+    for (int e = tid; e < S * U; e += nt) {
+      const int s = e / U, u = e - s * U;
+      if (p.xhat) p.xhat[(sc * S + s) * static_cast<long>(U) + u] =
+          sys_st[s] == 0 ? Vs[s * UP + u] : make_float2(0.f, 0.f);
+    }
+    for (int e = tid; e < S * p.K; e += nt) {
+      const int s = e / p.K, k = e - s * p.K;
+      hw[e] = make_float2(hist[(s * Kmax + k) * 2], hist[(s * Kmax + k) * 2 + 1]);
+    }
+    if (p.status)
+      for (int s = tid; s < S; s += nt) p.status[sc * S + s] = sys_st[s];
+  } else if (EXACT && S > 0) {
     sync();
     k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st, nt, sync,
                       reinterpret_cast<float*>(smem + L.xp));
@@ -895,7 +911,7 @@ template <int UP, bool EXACT, int MINB = 3>
 __global__ void __launch_bounds__(256, MINB) solve_kernel_pf(const KernelParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   WsOffsets W;
-  W.plan(UP, p.S, p.K, EXACT);
+  W.plan(UP, p.S, p.K, EXACT, p.fx);
   const int pb = k2_pre_bytes(UP, p.S);
   const uint32_t bytes = static_cast<uint32_t>(W.cd * 8);  // G + MF
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
