@@ -13,7 +13,7 @@ for c in cfg1 cfg3 cfg4a_K2 cfg4a_K4 cfg4a_K8 cfg4b_K2 cfg4b_K4 cfg4b_K8 cfg5; d
 done
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_cfg2.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > $O/ncu_launch.log 2>&1
-for spec in "cfg2 channel_tc" "cfg2 solve_rows32_pairs" "cfg1 uplink_small" "cfg3 precode_small" "cfg4a_K8 basis_kernel" "cfg4a_K8 solve_rows32_exact" "cfg5 solve_kernel_pf"; do
+for spec in "cfg2 channel_tc" "cfg2 solve_rows32_pairs" "cfg1 uplink_small" "cfg3 precode_small" "cfg4a_K8 basis_kernel" "cfg4a_K8 solve_rows32_exact" "cfg5 solve_rows32_kernel"; do
   set -- $spec
   ncu --set full --import-source on --clock-control none -k regex:$2 --launch-skip 3 --launch-count 1 \
       -o $O/full_$1_$2 -f python tools/quick_time.py $1 > /dev/null 2>&1
