@@ -178,6 +178,7 @@ int plan_and_launch(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
     return fail(ctx, CGM_EINVAL,
                 "per-subcarrier working set %d B exceeds shared memory (%d B): reduce B or S",
                 L.total, ctx->max_smem);
+  if (p.use_tma == 2) p.use_tma = 0;  // the fused A/B kernel stages Y by bulk copy only
   auto kern = cgm::subcarrier_kernel<UP, NT, EXACT>;
   int occ = 0;
   CGM_PREP(ctx, kern, NT, L.total, &occ);
@@ -694,8 +695,10 @@ int launch(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
   if (ctx->policy == 0 && precode_small_ok(ctx, p))
     return UP == 8 ? launch_precode_small<8>(ctx, p, st) : launch_precode_small<16>(ctx, p, st);
   const uintptr_t a = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
-  p.use_tma = (!p.hd_layout && p.U == UP && (p.B % 2) == 0 && (p.S % 2) == 0 && (a & 15u) == 0)
-                  ? 1 : 0;
+  // 1: H and Y by bulk copy; 2 (odd S, channel_kernel only): H by bulk copy,
+  // the padded Y rows by the threads
+  p.use_tma = (!p.hd_layout && p.U == UP && (p.B % 2) == 0 && (a & 15u) == 0)
+                  ? ((p.S % 2) == 0 ? 1 : 2) : 0;
   if (ctx->policy == 0) {
     switch (UP) {
       case 8: return dispatch_split<8>(ctx, p, exact, st);

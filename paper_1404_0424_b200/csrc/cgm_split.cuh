@@ -93,11 +93,12 @@ struct K1Split {
 __device__ __forceinline__ void k1_issue(const KernelParams& p, float2* Hs, float2* Ys,
                                          uint64_t* bar, long sc, int UP) {
   const uint32_t hbytes = static_cast<uint32_t>(p.B) * UP * 8u;
-  const uint32_t ybytes = static_cast<uint32_t>(p.B) * p.S * 8u;
+  // use_tma == 2 (odd S): Y rows are padded in shared memory, loaded by threads
+  const uint32_t ybytes = p.use_tma == 1 ? static_cast<uint32_t>(p.B) * p.S * 8u : 0u;
   fence_proxy_async();
   mbar_expect_tx(bar, hbytes + ybytes);
   bulk_g2s(Hs, p.H + sc * static_cast<long>(p.B) * UP, hbytes, bar);
-  if (p.S > 0) bulk_g2s(Ys, p.Y + sc * static_cast<long>(p.B) * p.S, ybytes, bar);
+  if (p.S > 0 && ybytes) bulk_g2s(Ys, p.Y + sc * static_cast<long>(p.B) * p.S, ybytes, bar);
 }
 
 // Exact tracker, per subcarrier (detect.cpp:336-368 restated on a Chebyshev
@@ -234,7 +235,14 @@ __global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p
     // ------------------------------------------------------ stage H, Y
     const int Sp = (S + 1) & ~1;
     if (p.use_tma) {
+      if (p.use_tma == 2) {  // H by bulk copy, the (padded) Y rows by the threads
+        for (int e = tid; e < Sp * B; e += nt) {
+          const int b = e / Sp, s = e - b * Sp;
+          Ys[e] = s < S ? p.Y[(sc * B + b) * static_cast<long>(S) + s] : make_float2(0.f, 0.f);
+        }
+      }
       mbar_wait(bars + st, ph);
+      if (p.use_tma == 2) __syncthreads();
     } else {
       if (p.hd_layout) {
         // downlink H_d [U][B] -> Hs[b][u] = conj(H_d[u][b])  (= H_u = H_d^H)
