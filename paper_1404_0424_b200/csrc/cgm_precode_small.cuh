@@ -91,6 +91,13 @@ __global__ void __launch_bounds__(32) precode_small_kernel(const KernelParams p)
 
   uint32_t phase = 0;
   for (long sc = blockIdx.x; sc < p.n_sc; sc += gridDim.x) {
+    // the first pass's transmit vectors, loaded now so the latency hides
+    // under the channel staging and the Gram
+    float2 t_first = make_float2(0.f, 0.f);
+    {
+      const int grp = lane / GL, gl = lane - grp * GL;
+      if (grp < St && gl < U) t_first = p.T[(sc * St + grp) * static_cast<long>(U) + gl];
+    }
     // ------------------------------------------------------ stage H_d rows
     const float2* src = p.H + sc * static_cast<long>(U) * B;
     if (tma) {
@@ -172,7 +179,8 @@ __global__ void __launch_bounds__(32) precode_small_kernel(const KernelParams p)
         const int sys = base + grp;
         const bool live = sys < St;
         float2 b = make_float2(0.f, 0.f);
-        if (live && gl < U) b = p.T[(sc * St + sys) * static_cast<long>(U) + gl];
+        if (live && gl < U)
+          b = base == 0 ? t_first : p.T[(sc * St + sys) * static_cast<long>(U) + gl];
         float2 v = make_float2(0.f, 0.f), r = b, pp = b;
         Pw[gl] = b;
         float rn = cnorm(b);
