@@ -272,10 +272,10 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
         p.k1_pair = nstg;
         smem1 = T.total;
         // epilogue / split warps (CGMIMO_TC_WARPS=EP,SP; SP = 0: the same
-        // warps do both).  Measured best (tools/microbench/tc_bench.cu):
-        // approx 8 + 8 specialised, exact 8 unified (the basis products
-        // then use all worker warps)
-        int nep = 8, nsp = EXACT ? 0 : 8;
+        // warps do both).  Measured best (tools/microbench/tc_bench.cu and
+        // bench.py, cfg2: 16 unified 37.9 us vs 8 + 8 specialised 39.4 us):
+        // approx 16 unified, exact 8 unified
+        int nep = EXACT ? 8 : 16, nsp = 0;
         if (const char* w = env("CGMIMO_TC_WARPS")) std::sscanf(w, "%d,%d", &nep, &nsp);
         if (nep == 16 && nsp == 0)
           k1 = cgm::channel_tc_kernel<EXACT, 16, 0>;
