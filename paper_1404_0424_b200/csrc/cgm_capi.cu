@@ -274,8 +274,10 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
         // epilogue / split warps (CGMIMO_TC_WARPS=EP,SP; SP = 0: the same
         // warps do both).  Measured best (tools/microbench/tc_bench.cu and
         // bench.py, cfg2: 16 unified 37.9 us vs 8 + 8 specialised 39.4 us):
-        // approx 16 unified, exact 8 unified
-        int nep = EXACT ? 8 : 16, nsp = 0;
+        // approx 16 unified; exact 8 unified for few vectors per subcarrier
+        // (cfg4a: 2.28 vs 2.37 ms for 8 + 8), 8 + 8 specialised for many
+        // (cfg5, S = 16: 15.7 vs 16.1 ms per step)
+        int nep = EXACT ? 8 : 16, nsp = (EXACT && p.S >= 8) ? 8 : 0;
         if (const char* w = env("CGMIMO_TC_WARPS")) std::sscanf(w, "%d,%d", &nep, &nsp);
         if (nep == 16 && nsp == 0)
           k1 = cgm::channel_tc_kernel<EXACT, 16, 0>;
