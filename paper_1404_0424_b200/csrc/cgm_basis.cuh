@@ -75,6 +75,19 @@ __global__ void __launch_bounds__(BasisGeo<UP>::NT, UP == 32 ? 4 : 2) basis_kern
   };
   for (int s = 0; s < nsc; ++s) load(Ah(s), p.ws + (sc0 + s) * W.stride + W.g);
   __syncthreads();
+  if (FX && p.fx == 2) {  // exact Hermitian from the lower triangle (the fused Gram writes full rows)
+    for (int e = tid; e < nsc * UP * UP; e += BG::NT) {
+      const int s = e / (UP * UP), r = (e / UP) % UP, c = e % UP;
+      float2* a = Ah(s);
+      if (c == r) a[r * LD + c].y = 0.f;
+    }
+    for (int e = tid; e < nsc * UP * UP; e += BG::NT) {
+      const int s = e / (UP * UP), r = (e / UP) % UP, c = e % UP;
+      float2* a = Ah(s);
+      if (c > r) a[r * LD + c] = cconj(a[c * LD + r]);
+    }
+    __syncthreads();
+  }
   // ------------------------------------- (c, d) by power iteration, warp s
   __shared__ float2 cds[SPC];
   // FX: also the Chebyshev coefficients of L_K and B from the CG history

@@ -230,6 +230,22 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
     p.fx = (basis_ext && p.S == 1 && p.St == 0 && !env("CGMIMO_SOLVE") &&
             !(fxe && std::strcmp(fxe, "0") == 0)) ? 1 : 0;
   }
+  // fx with U = 32, opt-in (CGMIMO_FXFUSED=1): one warp per subcarrier does
+  // Gram + matched filter + CG (fused_rows32_approx_kernel<16, true>) in place
+  // of the tensor-core channel kernel and the CG kernel -- measured slower on
+  // cfg4a (1.54 ms against 1.21 + 0.21 ms, K = 2)
+  bool fxfused = false;
+  int fx_smem = 0;
+  if constexpr (EXACT && UP == 32) {
+    const char* e = env("CGMIMO_FXFUSED");
+    const uintptr_t al = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
+    cgm::FusedSmem FL;
+    FL.plan(p.B, p.S);
+    fxfused = p.fx && p.U == 32 && p.S <= 16 && !p.hd_layout && (p.B % 2) == 0 && (al & 15u) == 0 &&
+              FL.total <= ctx->max_smem && e && std::strcmp(e, "1") == 0;
+    fx_smem = FL.total;
+    if (fxfused) p.fx = 2;  // G rows not exactly Hermitian: the basis kernel symmetrises
+  }
   const bool k1_basis = EXACT && !basis_ext;
   cgm::K1Smem<UP> L1;
   L1.plan(p.B, p.S, k1_basis, 2);
@@ -463,7 +479,13 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       e3 = prof_event(ctx);
       cudaEventRecord(e0, s1);
     }
-    k1<<<static_cast<unsigned>(g1), nt1, smem1, s1>>>(p);
+    if (fxfused) {
+      auto kf = cgm::fused_rows32_approx_kernel<16, EXACT>;
+      CGM_PREP(ctx, kf, 32, fx_smem, nullptr);
+      kf<<<static_cast<unsigned>(n), 32, fx_smem, s1>>>(p);
+    } else {
+      k1<<<static_cast<unsigned>(g1), nt1, smem1, s1>>>(p);
+    }
     CGM_CUDA(ctx, cudaGetLastError());
     if (ctx->profiling) cudaEventRecord(e1, s1);
     if (kb && !p.fx) {
@@ -486,7 +508,9 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       CGM_CUDA(ctx, cudaStreamWaitEvent(s2, ctx->ov_ev[1 + half], 0));
     }
     if (ctx->profiling) cudaEventRecord(e2, s2);
-    if (use_pairs && rows_pf)  // persistent: four CTAs per SM
+    if (fxfused)
+      ;  // the CG ran inside the fused kernel
+    else if (use_pairs && rows_pf)  // persistent: four CTAs per SM
       k2<<<static_cast<unsigned>(std::min<long>((n * ((p.S + 1) / 2) + 3) / 4, 4L * ctx->sms)), 128,
            smem2, s2>>>(p);
     else if (use_pairs)  // 4 warps per CTA, one (subcarrier, system pair) per warp

@@ -541,7 +541,7 @@ __device__ __forceinline__ unsigned long long f2swap_hl(unsigned long long v) {
 }
 
 struct FusedSmem {
-  int bar, ring, slot, hbytes, ybytes, mf, ps, total, cb;
+  int bar, ring, slot, hbytes, ybytes, mf, ps, xh, total, cb;
   __host__ __device__ void plan(int B, int S) {
     cb = 16;  // antennas per chunk
     while (cb > 1 && B % cb) cb >>= 1;
@@ -552,11 +552,15 @@ struct FusedSmem {
     ring = 16;
     mf = ring + 2 * slot;
     ps = mf + S * 32 * 8;
-    total = ps + 2 * 32 * 8;
+    xh = ps + 2 * 32 * 8;  // exact: per-pair (alpha, beta) history, v rows, status
+    total = xh + (2 * kMaxK * 2 * 4 + 2 * 32 * 8 + 16);
   }
 };
 
-template <int MAXS>
+// EXACT (one vector per subcarrier, p.fx): the same warp then runs the CG
+// with the (alpha, beta) history, writes x_hat / status / history and its G
+// row to the workspace, and basis_kernel<32, true> finishes the tracker.
+template <int MAXS, bool EXACT = false>
 __global__ void __launch_bounds__(32) fused_rows32_approx_kernel(const KernelParams p) {
   constexpr int UP = 32;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -633,8 +637,37 @@ __global__ void __launch_bounds__(32) fused_rows32_approx_kernel(const KernelPar
   for (int j = 0; j < UP; ++j)
     if (j == lane) gdiag = f2unpack(acc[j]).x;
   __syncwarp();
-  for (int base = 0; base < S; base += 2)
-    rows32_pair<false, true>(p, sc, Ms, base, acc, gdiag, Ps, nullptr, nullptr, nullptr);
+  if constexpr (!EXACT) {
+    for (int base = 0; base < S; base += 2)
+      rows32_pair<false, true>(p, sc, Ms, base, acc, gdiag, Ps, nullptr, nullptr, nullptr);
+  } else {
+    const int K = p.K;
+    WsOffsets W;
+    W.plan(UP, S, K, true, p.fx);
+    float2* ws = p.ws + static_cast<long>(blockIdx.x) * W.stride;
+#pragma unroll
+    for (int j = 0; j < UP; ++j) ws[W.g + lane * UP + j] = f2unpack(acc[j]);  // row u of G
+    float* histw = reinterpret_cast<float*>(smem + L.xh);
+    float2* Vsw = reinterpret_cast<float2*>(histw + 2 * kMaxK * 2);
+    uint8_t* stw = reinterpret_cast<uint8_t*>(Vsw + 2 * UP);
+    for (int base = 0; base < S; base += 2) {
+      rows32_pair<true, true>(p, sc, Ms, base, acc, gdiag, Ps, histw - base * K * 2, Vsw - base * UP,
+                              stw - base);
+      __syncwarp();
+      for (int t = 0; t < 2; ++t) {
+        const int sy = base + t;
+        if (sy >= S) break;
+        const bool ok = stw[t] == 0;
+        if (p.xhat)
+          p.xhat[(sc * S + sy) * static_cast<long>(UP) + lane] = ok ? Vsw[t * UP + lane]
+                                                                    : make_float2(0.f, 0.f);
+        if (lane < K) ws[W.t + sy * K + lane] = make_float2(histw[(t * K + lane) * 2],
+                                                           histw[(t * K + lane) * 2 + 1]);
+        if (lane == 0 && p.status) p.status[sc * S + sy] = ok ? 0 : 1;
+      }
+      __syncwarp();
+    }
+  }
 }
 
 }  // namespace cgm

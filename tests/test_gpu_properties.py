@@ -236,6 +236,8 @@ def test_precode_uplink_layout_equals_downlink_layout(gpu_ctx, U, B, K):
     ("cfg1", "CGMIMO_UPSMALL", "split"),     # default: fused U <= 16 detector, one warp per subcarrier
     ("cfg4a_K8", "CGMIMO_BASIS", "inline"),  # default: basis_kernel (cgm_basis.cuh)
     ("cfg4a_K2", "CGMIMO_FX", "0"),          # default S = 1: basis + extraction fused (no T in HBM)
+    ("cfg4a_K2", "CGMIMO_FXFUSED", "1"),     # opt-in U = 32, S = 1: Gram + MF + CG in one warp
+    ("cfg4a_K8", "CGMIMO_FXFUSED", "1"),
     ("cfg4a_K8", "CGMIMO_FX", "0"),
     ("cfg4b_K4", "CGMIMO_FX", "0"),
     ("cfg4b_K4", "CGMIMO_BASIS", "inline"),
