@@ -13,8 +13,28 @@ from paper_1404_0424_b200 import Context, get_config  # noqa: E402
 ctx = Context(0)
 for name in sys.argv[1:]:
     cfg = get_config(name)
-    H, Y = ctx.generate_uplink(cfg.B, cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits, cfg.n0)
     pin = lambda t: torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True).numpy()
+    if cfg.kind == "downlink":  # precode_cg with host buffers
+        Hd, T = ctx.generate_downlink(cfg.B, cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits)
+        hHd, hT = pin(Hd), pin(T)
+        hHd[...] = Hd.cpu().numpy()
+        hT[...] = T.cpu().numpy()
+        out = {"q": pin(torch.empty((cfg.n_sc, cfg.S, cfg.B), dtype=torch.complex64)),
+               "s": pin(torch.empty((cfg.n_sc, cfg.S, cfg.B), dtype=torch.complex64)),
+               "gain": pin(torch.empty((cfg.n_sc, cfg.S))),
+               "status": pin(torch.empty((cfg.n_sc, cfg.S), dtype=torch.uint8))}
+        call = lambda: ctx.precode_cg(hHd, hT, cfg.rho_d, cfg.K, out=out)
+        for _ in range(3):
+            call()
+        n = 20
+        t0 = time.perf_counter()
+        for _ in range(n):
+            call()
+        dt = (time.perf_counter() - t0) / n
+        print(json.dumps({"cfg": name, "e2e_ms": round(dt * 1e3, 4), "e2e_vec_per_s": cfg.vectors / dt}),
+              flush=True)
+        continue
+    H, Y = ctx.generate_uplink(cfg.B, cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits, cfg.n0)
     hH, hY = pin(H), pin(Y)
     hH[...] = H.cpu().numpy()
     hY[...] = Y.cpu().numpy()
