@@ -287,6 +287,26 @@ class Oracle:
                              C.c_int(U), _ptr(out))
         return out
 
+    def gen_uplink(self, seed: int, B: int, U: int, sc0: int, n_sc: int, S: int,
+                   qam_bits: int, n0: float, rsqrt=None, with_t: bool = False,
+                   threads: int = 1):
+        """The device generator's inputs (csrc/cgm_generate.cu) drawn on the host
+        with the reference Rng: H (n_sc,B,U), Y (n_sc,B,S) [, T (n_sc,S,U)] complex64."""
+        self._need_ref("gen_uplink")
+        H = np.zeros((n_sc, B, U), np.complex64)
+        Y = np.zeros((n_sc, B, S), np.complex64)
+        T = np.zeros((n_sc, S, U), np.complex64) if with_t else None
+        _fp = C.POINTER(C.c_float)
+        R = None if rsqrt is None else np.ascontiguousarray(rsqrt, dtype=np.float32)
+        rc = self.lib.ref_gen_uplink(C.c_uint64(seed), C.c_int(B), C.c_int(U), C.c_long(sc0),
+                                     C.c_long(n_sc), C.c_int(S), C.c_int(qam_bits),
+                                     C.c_double(n0), None if R is None else _ptr(R, _fp),
+                                     _ptr(H, _fp), _ptr(Y, _fp),
+                                     None if T is None else _ptr(T, _fp), C.c_int(threads))
+        if rc != 0:
+            raise ValueError("ref_gen_uplink: bad arguments")
+        return (H, Y, T) if with_t else (H, Y)
+
     # reference-only probes ------------------------------------------------
     def count_detect_stages(self, method: int, B: int, U: int, K: int) -> np.ndarray:
         out = np.zeros(16, np.uint64)

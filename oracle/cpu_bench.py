@@ -53,7 +53,34 @@ def synth(cfg, n_sc, seed=7):
     return out
 
 
-def run(config: str, n_sc: int, threads: int, passes: int, warmup: int) -> dict:
+def device_inputs(cfg, n_sc, threads):
+    """The GPU arm's inputs for subcarriers [0, n_sc) of its frame 0 (rank 0):
+    the same seeded streams as the device generator (csrc/cgm_generate.cu),
+    drawn on the host with the reference Rng (oracle/ref_shim.cpp
+    ref_gen_uplink) -- identical complex64 values up to the last ulp of the
+    FP64 libm transcendentals."""
+    import oracle
+
+    o = oracle.Oracle("ref")
+    if cfg.kind == "downlink":
+        raise ValueError("device_inputs: uplink / both configs only")
+    rs = cfg.rsqrt()
+    out = o.gen_uplink(cfg.seed, cfg.B, cfg.U, 0, n_sc, cfg.S, cfg.qam_bits, cfg.n0,
+                       rsqrt=None if rs is None else rs.astype(np.float32),
+                       with_t=cfg.kind == "both", threads=threads)
+    d = dict(H=out[0], Y=out[1])
+    if cfg.kind == "both":
+        d["T"] = out[2]
+    return d
+
+
+def run(config: str, n_sc: int, threads: int, passes: int, warmup: int,
+        min_seconds: float = 0.0) -> dict:
+    """Best of `passes` timed passes of the reference over n_sc subcarriers
+    (all S vectors of each).  With min_seconds > 0 the sample is grown (from
+    a calibration pass) until one pass takes at least that long, capped at
+    the config's own size; the rate is extrapolated linearly (instances are
+    independent)."""
     import oracle
     from paper_1404_0424_b200.configs import get_config
 
@@ -62,33 +89,52 @@ def run(config: str, n_sc: int, threads: int, passes: int, warmup: int) -> dict:
     kind = "reference" if o.kind == "ref" else "port"
     if kind == "port":
         threads = 1  # the C restatement is single-threaded
-    data = synth(cfg, n_sc)
-    H128 = {k: v.astype(np.complex128) for k, v in data.items()}
+    same = kind == "reference" and cfg.kind != "downlink"
 
-    def one():
+    def make(n):
+        return device_inputs(cfg, n, threads) if same else synth(cfg, n)
+
+    def one(d):
         if cfg.kind in ("uplink", "both"):
-            o.detect(H128["H"], H128["Y"], cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+            o.detect(d["H"], d["Y"], cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
                      cfg.tracker, threads=threads)
         if cfg.kind == "downlink":
-            o.precode(H128["Hd"], H128["T"], cfg.rho_d, cfg.K, threads=threads)
+            o.precode(d["Hd"], d["T"], cfg.rho_d, cfg.K, threads=threads)
         if cfg.kind == "both":
-            Hd = np.ascontiguousarray(np.conj(np.transpose(H128["H"], (0, 2, 1))))
-            o.precode(Hd, H128["T"], cfg.rho_d, cfg.K, threads=threads)
+            Hd = np.ascontiguousarray(np.conj(np.transpose(d["H"], (0, 2, 1))))
+            o.precode(Hd, d["T"], cfg.rho_d, cfg.K, threads=threads)
 
+    def timed(d):
+        t0 = time.perf_counter()
+        one(d)
+        return time.perf_counter() - t0
+
+    n_sc = max(1, min(n_sc, cfg.n_sc))
+    if min_seconds > 0:
+        n_cal = max(1, min(n_sc, 4 * threads))
+        dt = timed(make(n_cal))
+        while dt < 0.5 and n_cal < cfg.n_sc:  # calibrate on >= 0.5 s of work
+            n_cal = min(cfg.n_sc, n_cal * 4)
+            dt = timed(make(n_cal))
+        n_sc = min(cfg.n_sc, max(n_sc, int(np.ceil(n_cal * min_seconds * 1.25 / dt))))
+    data = {k: v.astype(np.complex128) for k, v in make(n_sc).items()}
     for _ in range(warmup):
-        one()
+        one(data)
     best = None
     for _ in range(passes):
-        t0 = time.perf_counter()
-        one()
-        dt = time.perf_counter() - t0
+        dt = timed(data)
         best = dt if best is None else min(best, dt)
     vectors = n_sc * cfg.S
+    src = ("the GPU arm's own complex64 inputs (subcarriers 0..%d of frame 0, rank 0; "
+           "device generator streams re-drawn with the reference Rng)" % (n_sc - 1)
+           if same else "numpy synthetic inputs of the config's shapes and distributions")
     return dict(value=vectors / best, unit="vectors/s", cores=threads, kind=kind,
-                seconds_per_pass=best, vectors=vectors,
-                sample=f"{config}: {n_sc} subcarriers x {cfg.S} vectors, best of {passes} passes "
-                       f"after {warmup} warm-up, per-call FP64 reference over a {threads}-thread "
-                       f"pool, GLIBC_TUNABLES malloc protocol")
+                seconds_per_pass=best, vectors=vectors, n_sc=n_sc,
+                sample=f"{config}: {n_sc} of {cfg.n_sc} subcarriers x {cfg.S} vectors "
+                       f"({vectors} instances, {best:.1f} s per pass; rate extrapolated "
+                       f"linearly), best of {passes} passes after {warmup} warm-up, per-call "
+                       f"FP64 reference over a {threads}-thread pool, GLIBC_TUNABLES malloc "
+                       f"protocol; inputs: {src}")
 
 
 def main():
@@ -98,22 +144,24 @@ def main():
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
     ap.add_argument("--passes", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--min-seconds", type=float, default=0.0)
     a = ap.parse_args()
     from paper_1404_0424_b200.configs import get_config
 
     n_sc = a.n_sc or get_config(a.config).n_sc
-    print(json.dumps(run(a.config, n_sc, a.threads, a.passes, a.warmup)))
+    print(json.dumps(run(a.config, n_sc, a.threads, a.passes, a.warmup, a.min_seconds)))
 
 
 def spawn(config: str, n_sc: int, threads: int, passes: int = 3, warmup: int = 2,
-          timeout: float = 600.0) -> dict:
+          timeout: float = 600.0, min_seconds: float = 0.0) -> dict:
     """Run main() in a fresh interpreter with the allocator protocol set."""
     import subprocess
 
     env = dict(os.environ, GLIBC_TUNABLES=GLIBC_TUNABLES, PYTHONPATH=ROOT)
     r = subprocess.run([sys.executable, "-m", "oracle.cpu_bench", "--config", config,
                         "--n-sc", str(n_sc), "--threads", str(threads), "--passes", str(passes),
-                        "--warmup", str(warmup)], capture_output=True, text=True, env=env,
+                        "--warmup", str(warmup),
+                        "--min-seconds", str(min_seconds)], capture_output=True, text=True, env=env,
                        cwd=ROOT, timeout=timeout)
     if r.returncode != 0:
         raise RuntimeError("cpu_bench failed: " + r.stderr[-2000:])

@@ -324,6 +324,94 @@ void ref_rayleigh(uint64_t key, const uint64_t* forks, int n_forks, int B, int U
     }
 }
 
+// The device generator's uplink inputs (repo: csrc/cgm_generate.cu) drawn on
+// the host with the reference's own Rng and constellation, so the CPU
+// baseline times the SAME complex64 values the GPU arm detects:
+//   H  [n_sc][B][U] c64 from Rng(seed).fork(2).fork(sc)  (channel.cpp:10-17 draw order)
+//      correlated (rsqrt != null, B x B float): H_w [U][B] from that stream,
+//      H[b][u] = sum_k conj(H_w[u][k]) rsqrt[k][b]  (FP64 sum, then c64)
+//   labels of instance i = sc*S + s: Rng(seed).fork(1).fork(i), bits next_u64() & 1
+//   Y  [n_sc][B][S] c64: (H x)_b in FP64 from the c64 H, plus
+//      sqrt(N0/2) (next_gaussian, next_gaussian) of Rng(seed).fork(3).fork(i) (channel.cpp:21-30)
+//   T  [n_sc][S][U] c64 (optional): transmit symbols, Rng(seed).fork(4).fork(i)
+int ref_gen_uplink(uint64_t seed, int B, int U, long sc0, long n_sc, int S, int qam_bits,
+                   double n0, const float* rsqrt, float* H, float* Y, float* T, int threads) {
+  try {
+    const auto c = phy::make_constellation(modulation_of(qam_bits));
+    const phy::Rng root(seed);
+    const phy::Rng chan = root.fork(2), lab = root.fork(1), noise = root.fork(3), sym = root.fork(4);
+    const double sd = std::sqrt(0.5 * n0);
+    auto label = [&](phy::Rng r, int u) {
+      (void)u;
+      unsigned l = 0;
+      for (int b = 0; b < qam_bits; ++b) l = (l << 1) | static_cast<unsigned>(r.next_u64() & 1u);
+      return l;
+    };
+    parallel_for(n_sc, threads, [&](long i) {
+      const long sc = sc0 + i;
+      float* h = H + 2 * i * static_cast<long>(B) * U;
+      phy::Rng r = chan.fork(static_cast<uint64_t>(sc));
+      if (!rsqrt) {
+        for (int e = 0; e < B * U; ++e) {
+          const auto z = r.next_cgaussian(1.0);
+          h[2 * e] = static_cast<float>(z.real());
+          h[2 * e + 1] = static_cast<float>(z.imag());
+        }
+      } else {
+        std::vector<float> hw(2 * static_cast<size_t>(U) * B);
+        for (int e = 0; e < U * B; ++e) {
+          const auto z = r.next_cgaussian(1.0);
+          hw[2 * e] = static_cast<float>(z.real());
+          hw[2 * e + 1] = static_cast<float>(z.imag());
+        }
+        for (int b = 0; b < B; ++b)
+          for (int u = 0; u < U; ++u) {
+            double re = 0.0, im = 0.0;
+            for (int k = 0; k < B; ++k) {
+              const double rr = rsqrt[static_cast<size_t>(k) * B + b];
+              re += static_cast<double>(hw[2 * (u * B + k)]) * rr;
+              im -= static_cast<double>(hw[2 * (u * B + k) + 1]) * rr;
+            }
+            h[2 * (b * U + u)] = static_cast<float>(re);
+            h[2 * (b * U + u) + 1] = static_cast<float>(im);
+          }
+      }
+      std::vector<cplx> x(U);
+      for (int s = 0; s < S; ++s) {
+        const uint64_t inst = static_cast<uint64_t>(sc * S + s);
+        phy::Rng lr = lab.fork(inst);
+        for (int u = 0; u < U; ++u) x[u] = c.map_label(label(lr, u));
+        phy::Rng nr = noise.fork(inst);
+        for (int b = 0; b < B; ++b) {
+          double re = 0.0, im = 0.0;
+          for (int u = 0; u < U; ++u) {
+            const double hx = h[2 * (b * U + u)], hy = h[2 * (b * U + u) + 1];
+            re += hx * x[u].real() - hy * x[u].imag();
+            im += hx * x[u].imag() + hy * x[u].real();
+          }
+          const double nre = nr.next_gaussian();
+          const double nim = nr.next_gaussian();
+          float* y = Y + 2 * ((i * B + b) * static_cast<long>(S) + s);
+          y[0] = static_cast<float>(re + sd * nre);
+          y[1] = static_cast<float>(im + sd * nim);
+        }
+        if (T) {
+          phy::Rng tr = sym.fork(inst);
+          float* t = T + 2 * (i * static_cast<long>(S) + s) * U;
+          for (int u = 0; u < U; ++u) {
+            const cplx v = c.map_label(label(tr, u));
+            t[2 * u] = static_cast<float>(v.real());
+            t[2 * u + 1] = static_cast<float>(v.imag());
+          }
+        }
+      }
+    });
+    return 0;
+  } catch (const std::exception&) {
+    return 2;
+  }
+}
+
 double ref_uplink_noise_variance(double snr_db, int users) {
   return phy::uplink_noise_variance(snr_db, users);
 }

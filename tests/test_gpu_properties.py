@@ -372,3 +372,24 @@ def test_zero_observation_every_kernel(gpu_ctx, U, tracker):
     assert float(out["xhat"].abs().max()) == 0.0
     llr = out["llr"].cpu()
     assert float(llr[..., 0].abs().max()) == 0.0 and float(llr[..., 2].abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("name", ["cfg5", "cfg2"])
+def test_host_generator_matches_device(gpu_ctx, oracle_ref, name):
+    """The CPU baseline times the GPU arm's own inputs: the device generator
+    and the host re-draw with the reference Rng (oracle ref_gen_uplink) give
+    the same complex64 values (to the last ulp of the FP64 libm calls)."""
+    cfg = get_config(name)
+    n = 6
+    H, Y = gen(gpu_ctx, cfg, sc0=3, n_sc=n)
+    T = gpu_ctx.generate_symbols(cfg.U, n, cfg.S, cfg.seed, cfg.qam_bits, sc0=3)
+    torch.cuda.synchronize()
+    rs = cfg.rsqrt()
+    Hh, Yh, Th = oracle_ref.gen_uplink(cfg.seed, cfg.B, cfg.U, 3, n, cfg.S, cfg.qam_bits, cfg.n0,
+                                       rsqrt=None if rs is None else rs.astype(np.float32),
+                                       with_t=True, threads=4)
+    np.testing.assert_array_max_ulp(H.cpu().numpy().view(np.float32), Hh.view(np.float32),
+                                    maxulp=2)
+    y, yh = Y.cpu().numpy(), Yh
+    np.testing.assert_allclose(y, yh, rtol=0, atol=1e-5 * float(np.abs(yh).max()))
+    np.testing.assert_array_equal(T.cpu().numpy(), Th)
