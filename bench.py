@@ -411,26 +411,24 @@ def ours_arm(args, rank, world, local_rank):
         k["frac"] = k["achieved"] / k["peak"] if k["achieved"] else None
         return k
 
-    # one vector per subcarrier, U in 17..64, exact: the basis kernel also
-    # does the extraction (basis_kernel<UP, true>, p.fx in the C ABI) -- its
-    # FLOPs move from the solve kernel's credit to the basis kernel's
-    fx = (cfg.kind == "uplink" and cfg.tracker == "exact" and cfg.S == 1 and 16 < cfg.U <= 64
-          and os.environ.get("CGMIMO_FX") != "0" and not os.environ.get("CGMIMO_SOLVE")
-          and os.environ.get("CGMIMO_BASIS") != "inline")
-    f_ext = cfg.tracker_extract_flops_per_vector() * cfg.vectors if fx else 0.0
+    # credits: channel = Gram + matched filter over H + Y; moments (exact
+    # tracker) = the K - 1 Hermitian basis products once per subcarrier;
+    # solve = CG + the moment extraction (O(K U) per vector; the reference's
+    # O(U^3) extraction is not performed, so it is not credited) + LLRs
+    # (+ precoder), over the outputs (+ t, H re-read)
     k_ch = kernel_roof("channel (Gram + matched filter; tcgen05 for U = 32)",
                        cfg.channel_flops_per_vector() * cfg.vectors,
                        cfg.channel_bytes_per_vector() * cfg.vectors, ch_s, traffic.get("channel"))
-    k_sv = kernel_roof("solve (CG + SINR tracker + LLR [+ precoder])" if not fx else "solve (CG)",
-                       cfg.solve_flops_per_vector() * cfg.vectors - f_ext,
+    k_sv = kernel_roof("solve (CG + SINR extraction + LLR [+ precoder])",
+                       cfg.solve_kernel_flops_per_vector() * cfg.vectors,
                        cfg.solve_bytes_per_vector() * cfg.vectors, sv_s, traffic.get("solve"))
     bs_s = bs_ms / args.steps / 1e3
     k_bs = None
-    if bs_s > 0:  # exact tracker: Chebyshev basis products (cgm_basis.cuh)
-        k_bs = kernel_roof("basis (exact tracker: (K-1) Hermitian U x U products per subcarrier"
-                           + (" + extraction + LLRs, fused)" if fx else ")"),
-                           cfg.basis_flops_per_vector() * cfg.vectors + f_ext, 0.0, bs_s,
-                           traffic.get("basis"))
+    if bs_s > 0:  # exact tracker: row moments of the Chebyshev basis (cgm_moments.cuh)
+        k_bs = kernel_roof("moments (exact tracker: (K-1) Hermitian U x U products + row "
+                           "moments per subcarrier)",
+                           cfg.basis_flops_per_vector() * cfg.vectors, 0.0, bs_s,
+                           traffic.get("moments"))
     shares = [(sv_s, k_sv), (ch_s, k_ch)] + ([(bs_s, k_bs)] if k_bs else [])
     dom_s, dom = max(shares, key=lambda x: x[0])
     if ch_s == 0 and sv_s > 0:
@@ -455,7 +453,7 @@ def ours_arm(args, rank, world, local_rank):
             "unit": dom["unit"], "frac": dom["frac"], "traffic": dom["traffic"],
             "peak_source": dom["peak_source"], "kernel": dom["kernel"],
             "share_of_step": dom_s / max(ch_s + bs_s + sv_s, 1e-12),
-            "kernels": {"channel": k_ch, "solve": k_sv, **({"basis": k_bs} if k_bs else {})},
+            "kernels": {"channel": k_ch, "solve": k_sv, **({"moments": k_bs} if k_bs else {})},
             "pair": {"kernel_ms": kernel_ms, "launch_pairs_per_step": n_pairs / args.steps,
                      "algorithmic_flops": flops_launch, "algorithmic_bytes": bytes_launch,
                      "tflops": flops_launch / (kernel_ms / 1e3) / 1e12,

@@ -67,9 +67,11 @@ int cgm_ctx_destroy(cgm_ctx* ctx);
 /* stream = cudaStream_t (0 = legacy default stream) */
 int cgm_ctx_set_stream(cgm_ctx* ctx, void* stream);
 int cgm_synchronize(cgm_ctx* ctx);
-/* 0 (default): the split path (channel kernel + solve kernel per L2-sized
- * chunk of subcarriers); 1: the single fused per-subcarrier kernel (A/B
- * testing).  Both are parity-tested. */
+/* Kernel-variant switches for A/B tests (bit mask; 0 = production
+ * defaults): 1 = FFMA channel kernel instead of tcgen05 for U = 32,
+ * 2 = channel + solve pair instead of the fused U <= 16 kernels,
+ * 4 = lane-per-row solve kernel instead of the U = 32 row kernels.
+ * Every variant is parity-tested against the default. */
 int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy);
 /* Per-kernel device timing: while on, every channel/solve launch pair is
  * bracketed by CUDA events on the launch stream; cgm_ctx_kernel_times
@@ -77,8 +79,8 @@ int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy);
  * number of channel-kernel launches since profiling was (re)enabled. */
 int cgm_ctx_set_profiling(cgm_ctx* ctx, int on);
 int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, long* launches);
-/* Same, with the exact tracker's Chebyshev basis kernel (cgm_basis.cuh)
- * reported on its own (cgm_ctx_kernel_times adds it to channel_ms). */
+/* Same, with the exact tracker's row-moment kernel (cgm_moments.cuh)
+ * reported on its own as basis_ms (cgm_ctx_kernel_times adds it to channel_ms). */
 int cgm_ctx_kernel_times_ex(cgm_ctx* ctx, double* channel_ms, double* basis_ms, double* solve_ms,
                             long* launches);
 const char* cgm_last_error(const cgm_ctx* ctx);
@@ -91,7 +93,9 @@ const char* cgm_version(void);
  * Gram + matched filter, K CG iterations with the exact (Eq. 10) or
  * approximate (Eq. 11) SINR tracker, max-log LLRs (detect.cpp:68-86).
  * rho_u is the regulariser argument (A = H^H H + rho_u^-1 I), n0 / es the
- * noise and symbol energies; qam_bits in {2, 4, 6}. 1 <= U <= 64, K <= 16. */
+ * noise and symbol energies; qam_bits in {2, 4, 6}. 1 <= U <= 64, K <= 16.
+ * The exact tracker's per-vector U^3 recursion and extraction are computed
+ * through per-subcarrier row moments of a Chebyshev basis. */
 int cgm_detect_cg(cgm_ctx* ctx, int B, int U, long n_sc, int S, const float* H,
                   const float* Y, double rho_u, double n0, double es, int qam_bits, int K,
                   int tracker, float* xhat, float* mu, float* rho, float* llr,

@@ -27,6 +27,7 @@
 //   bit0 = SolverBreakdown (outputs zeroed), bit1 = zero_input (precode),
 //   bit2 = std::invalid_argument / other exception.
 #include <atomic>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -369,8 +370,9 @@ int ref_gen_uplink(uint64_t seed, int B, int U, long sc0, long n_sc, int S, int 
             double re = 0.0, im = 0.0;
             for (int k = 0; k < B; ++k) {
               const double rr = rsqrt[static_cast<size_t>(k) * B + b];
-              re += static_cast<double>(hw[2 * (u * B + k)]) * rr;
-              im -= static_cast<double>(hw[2 * (u * B + k) + 1]) * rr;
+              // fused like the device code's contracted DFMA chain
+              re = std::fma(static_cast<double>(hw[2 * (u * B + k)]), rr, re);
+              im = std::fma(-static_cast<double>(hw[2 * (u * B + k) + 1]), rr, im);
             }
             h[2 * (b * U + u)] = static_cast<float>(re);
             h[2 * (b * U + u) + 1] = static_cast<float>(im);

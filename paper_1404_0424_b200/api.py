@@ -89,17 +89,26 @@ class Context:
 
         self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
 
+    POLICY_FLAGS = {"ffma_channel": 1, "split_small": 2, "lane_solve": 4}
+
     def set_kernel_policy(self, policy: str):
-        """"auto" (split channel + solve kernels, production) or "generic"
-        (single fused per-subcarrier kernel)."""
-        self._check(self.lib.cgm_ctx_set_kernel_policy(self.h, {"auto": 0, "generic": 1}[policy]))
+        """Kernel-variant switches for A/B tests: "auto" (production defaults)
+        or "+"-joined names of POLICY_FLAGS -- "ffma_channel" (FFMA Gram
+        kernel instead of tcgen05 for U = 32), "split_small" (channel + solve
+        pair instead of the fused U <= 16 kernels), "lane_solve" (lane-per-row
+        solve kernel instead of the U = 32 row kernels)."""
+        bits = 0
+        if policy != "auto":
+            for name in policy.split("+"):
+                bits |= self.POLICY_FLAGS[name]
+        self._check(self.lib.cgm_ctx_set_kernel_policy(self.h, bits))
 
     def set_profiling(self, on: bool):
         self._check(self.lib.cgm_ctx_set_profiling(self.h, 1 if on else 0))
 
     def kernel_times_ex(self):
-        """(channel_ms, basis_ms, solve_ms, launches) summed since profiling was
-        enabled; basis = the exact tracker's Chebyshev basis kernel."""
+        """(channel_ms, moments_ms, solve_ms, launches) summed since profiling
+        was enabled; moments = the exact tracker's row-moment kernel."""
         a, b, c, n = C.c_double(), C.c_double(), C.c_double(), C.c_long()
         self._check(self.lib.cgm_ctx_kernel_times_ex(self.h, C.byref(a), C.byref(b), C.byref(c),
                                                      C.byref(n)))
@@ -182,6 +191,7 @@ class Context:
         shapes = {"xhat": ((n_sc, S, U), "c64"), "mu": ((n_sc, S, U), "f32"),
                   "rho": ((n_sc, S, U), "f32"), "llr": ((n_sc, S, U, qam_bits), "f32"),
                   "status": ((n_sc, S), "u8")}
+        _check_outputs(out, shapes, device, H)
         for k in want:
             if k not in out:
                 out[k] = _alloc(shapes[k], device, H)
@@ -219,6 +229,7 @@ class Context:
         out = dict(out or {})
         shapes = {"q": ((n_sc, S, B), "c64"), "s": ((n_sc, S, B), "c64"),
                   "gain": ((n_sc, S), "f32"), "status": ((n_sc, S), "u8")}
+        _check_outputs(out, shapes, device, Hd)
         for k in want:
             if k not in out:
                 out[k] = _alloc(shapes[k], device, Hd)
@@ -251,6 +262,7 @@ class Context:
                   "status": ((n_sc, S), "u8"), "q": ((n_sc, St, B), "c64"),
                   "s": ((n_sc, St, B), "c64"), "gain": ((n_sc, St), "f32"),
                   "pstatus": ((n_sc, St), "u8")}
+        _check_outputs(out, shapes, device, H)
         for k in want:
             if k not in out:
                 out[k] = _alloc(shapes[k], device, H)
@@ -346,6 +358,35 @@ def _alloc(spec, device, like):
         return torch.empty(shape, dtype=dt, device=like.device)
     dt = {"c64": np.complex64, "f32": np.float32, "u8": np.uint8}[kind]
     return np.empty(shape, dtype=dt)
+
+
+_DT = {"c64": ("torch.complex64", np.complex64), "f32": ("torch.float32", np.float32),
+       "u8": ("torch.uint8", np.uint8)}
+
+
+def _check_outputs(out, shapes, device, like):
+    """Every caller-supplied output buffer must have its array's shape and
+    dtype, be C-contiguous, and live where the inputs live (a CUDA tensor on
+    the inputs' device, or a host numpy array): the kernels write through the
+    raw pointer (a host pointer in a device call poisons the
+    context, an undersized buffer is written out of bounds)."""
+    for k, a in out.items():
+        if a is None:
+            continue
+        if k not in shapes:
+            raise ValueError(f"unknown output {k!r}")
+        shape, kind = shapes[k]
+        if device:
+            ok = (_is_torch(a) and a.is_cuda and a.device == like.device and a.is_contiguous()
+                  and str(a.dtype) == _DT[kind][0])
+        else:
+            ok = (isinstance(a, np.ndarray) and a.dtype == _DT[kind][1] and a.flags.c_contiguous
+                  and a.flags.writeable)
+        if not ok:
+            raise ValueError(f"output {k!r} must be a C-contiguous {kind} "
+                             f"{'CUDA tensor on ' + str(like.device) if device else 'numpy array'}")
+        if tuple(a.shape) != tuple(shape):
+            raise ValueError(f"output {k!r} has shape {tuple(a.shape)}, expected {tuple(shape)}")
 
 
 def _check_inputs(device, *arrs):

@@ -111,14 +111,29 @@ class Config:
         return 4 * U * U * (U + 1) + 8 * U * U
 
     def basis_flops_per_vector(self) -> float:
-        """What the basis kernel (cgm_basis.cuh) does: the same (K-1) Hermitian
-        products once per SUBCARRIER, shared by its S vectors."""
+        """What the moments kernel (cgm_moments.cuh) does: the same (K-1)
+        Hermitian products once per SUBCARRIER, shared by its S vectors."""
         return self.tracker_basis_flops_per_vector() / self.S
 
     def solve_flops_per_vector(self) -> float:
         """CG, tracker extraction, LLRs (+ precoder): the rest of the path."""
         return (self.flops_per_vector() - self.channel_flops_per_vector()
                 - self.tracker_basis_flops_per_vector())
+
+    def moments_extract_flops_per_vector(self) -> float:
+        """The row-moment extraction this repo runs per vector (cgm_moments.cuh):
+        two Chebyshev coefficient products (~4 K^2) and, per user row, four
+        dot products of length <= 2K + 1 (8 (2K + 1) flops)."""
+        if self.kind not in ("uplink", "both") or self.tracker != "exact":
+            return 0.0
+        K, U = self.K, self.U
+        return 4 * K * K + 8 * (2 * K + 1) * U
+
+    def solve_kernel_flops_per_vector(self) -> float:
+        """What the solve kernel computes: CG, LLRs (+ precoder) and the
+        moment extraction in place of the reference's U^3 extraction."""
+        return (self.solve_flops_per_vector() - self.tracker_extract_flops_per_vector()
+                + self.moments_extract_flops_per_vector())
 
     def solve_bytes_per_vector(self) -> float:
         """Outputs written by the solve kernel (+ t read, H re-read by the precoder)."""

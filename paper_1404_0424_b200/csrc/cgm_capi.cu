@@ -18,11 +18,10 @@
 
 #include "../../include/cgmimo_b200.h"
 #include "cgm_alt.cuh"
-#include "cgm_basis.cuh"
+#include "cgm_moments.cuh"
 #include "cgm_precode_small.cuh"
 #include "cgm_uplink_small.cuh"
 #include "cgm_rows32.cuh"
-#include "cgm_solve32.cuh"
 #include "cgm_tc.cuh"
 
 struct cgm_ctx {
@@ -37,16 +36,15 @@ struct cgm_ctx {
   cudaEvent_t hev[kHostSets][3] = {};
   void* ws[kHostSets] = {nullptr, nullptr, nullptr};
   size_t ws_bytes[kHostSets] = {0, 0, 0};
-  float* tscratch = nullptr;
+  float* tscratch = nullptr;  // split-path workspace (grown, never freed while the context lives)
   size_t tscratch_bytes = 0;
+  std::vector<void*> retired;  // outgrown workspaces (possibly referenced by captured graphs)
   long launches = 0;
-  int policy = 0;  // 0 split K1+K2 path (production), 1 single fused kernel (A/B)
+  int policy = 0;  // kernel-variant switches (kPol*), 0 = production defaults
+  int host_chunks = 0;  // CGMIMO_HOST_CHUNKS, read once at context creation
   // optional per-kernel event timing (bench roofline): pairs of events per launch
   int profiling = 0;
-  // overlapped split path: channel kernel of chunk c+1 runs concurrently with
-  // the solve kernel of chunk c (two internal streams, two workspace halves)
-  cudaStream_t ov[2] = {nullptr, nullptr};
-  cudaEvent_t ov_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // start, done1[2], done2[2]
+  cudaEvent_t order_ev = nullptr;  // host pipeline: ordered after the context stream's work
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_log;  // kind, (start, stop)
   size_t ev_next = 0;
@@ -70,10 +68,6 @@ cudaEvent_t prof_event(cgm_ctx* ctx) {
   }
   return ctx->ev_pool[ctx->ev_next++];
 }
-
-// Environment overrides (A/B switches for the kernel variants; read per call
-// so tests can flip them inside one process).
-const char* env(const char* name) { return std::getenv(name); }
 
 int fail(cgm_ctx* ctx, int code, const char* fmt, ...) {
   char buf[512];
@@ -158,394 +152,218 @@ cgm::AxisTables make_axis_tables() {
 
 int up_of(int U) { return U <= 8 ? 8 : U <= 16 ? 16 : U <= 32 ? 32 : 64; }
 
-struct Launch {
-  int smem = 0;
-  int grid = 0;
-  int t_in_smem = 1;
-};
+// Kernel-variant switches (cgm_ctx_set_kernel_policy): A/B alternatives kept
+// for parity tests and measurements, never selected by default.
+constexpr int kPolFfmaChannel = 1;  // U = 32: FFMA channel kernel instead of tcgen05
+constexpr int kPolSplitSmall = 2;   // U <= 16: channel + solve pair instead of the fused kernels
+constexpr int kPolLaneSolve = 4;    // U = 32: lane-per-row solve kernel instead of the row kernels
 
-template <int UP, int NT, bool EXACT>
-int plan_and_launch(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
-  const int Kmax = std::max(p.K, p.Kt);
-  cgm::Smem<UP> L;
-  p.t_in_smem = 1;
-  L.plan(p.B, p.S, p.St, Kmax, EXACT, 1);
-  if (L.total > ctx->max_smem) {
-    p.t_in_smem = 0;
-    L.plan(p.B, p.S, p.St, Kmax, EXACT, 0);
-  }
-  if (L.total > ctx->max_smem)
-    return fail(ctx, CGM_EINVAL,
-                "per-subcarrier working set %d B exceeds shared memory (%d B): reduce B or S",
-                L.total, ctx->max_smem);
-  if (p.use_tma == 2) p.use_tma = 0;  // the fused A/B kernel stages Y by bulk copy only
-  auto kern = cgm::subcarrier_kernel<UP, NT, EXACT>;
-  int occ = 0;
-  CGM_PREP(ctx, kern, NT, L.total, &occ);
-  if (occ < 1) return fail(ctx, CGM_EINVAL, "kernel does not fit on an SM (smem %d)", L.total);
-  long grid = std::min<long>(p.n_sc, static_cast<long>(occ) * ctx->sms);
-  if (grid < 1) grid = 1;
-  if (EXACT && !p.t_in_smem) {
-    const size_t need = static_cast<size_t>(grid) * Kmax * UP * UP * sizeof(float2);
-    if (need > ctx->tscratch_bytes) {
-      if (ctx->tscratch) cudaFree(ctx->tscratch);
-      ctx->tscratch = nullptr;
-      ctx->tscratch_bytes = 0;
-      CGM_CUDA(ctx, cudaMalloc(&ctx->tscratch, need));
-      ctx->tscratch_bytes = need;
-    }
-    p.tscratch = ctx->tscratch;
-  }
-  kern<<<static_cast<unsigned>(grid), NT, L.total, st>>>(p);
-  CGM_CUDA(ctx, cudaGetLastError());
-  ctx->launches += 1;
+// Device workspace of the split path.  A call captured into a CUDA graph
+// bakes in this pointer, so a larger call never frees it: the old buffer
+// is retired (kept until the context is destroyed) and the new one grown by
+// at least 1.5x (graphs replayed after a larger call).
+int ensure_ws(cgm_ctx* ctx, size_t need) {
+  if (need <= ctx->tscratch_bytes) return CGM_OK;
+  const size_t want = std::max(need, ctx->tscratch_bytes + ctx->tscratch_bytes / 2);
+  void* p = nullptr;
+  CGM_CUDA(ctx, cudaMalloc(&p, want));
+  if (ctx->tscratch) ctx->retired.push_back(ctx->tscratch);
+  ctx->tscratch = static_cast<float*>(p);
+  ctx->tscratch_bytes = want;
   return CGM_OK;
 }
 
-// Split path (cgm_split.cuh): K1 channel kernel + K2 solve kernel per chunk
-// of subcarriers; the chunk is sized so the K1->K2 workspace (and the H that
-// the precoder re-reads) stays resident in the 126 MB L2.
+// one timed launch: CUDA events around it on `st` when profiling (kind 1
+// channel, 2 solve, 3 exact-tracker moments)
+template <class F>
+int timed(cgm_ctx* ctx, cudaStream_t st, int kind, F&& go) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->profiling) {
+    e0 = prof_event(ctx);
+    e1 = prof_event(ctx);
+    cudaEventRecord(e0, st);
+  }
+  go();
+  CGM_CUDA(ctx, cudaGetLastError());
+  if (ctx->profiling) {
+    cudaEventRecord(e1, st);
+    ctx->ev_log.push_back({kind, {e0, e1}});
+  }
+  ++ctx->launches;
+  return CGM_OK;
+}
+
+// Split path, per chunk of subcarriers:
+//   K1 channel kernel   G = H^H H (+ rho^-1 I in the CG), matched filters
+//                       (tcgen05 for U = 32 natural layout, FFMA otherwise)
+//   KM moments kernel   exact tracker only: (c, d) and the row moments
+//                       D_k[i] of the Chebyshev basis (cgm_moments.cuh)
+//   K2 solve kernel     CG + tracker extraction + LLRs (+ precoder tail)
+// The chunk is sized so the workspace, H (re-read by the precoder tail) and
+// Y of a chunk stay resident in the 126 MB L2 between the kernels.
 template <int UP, bool EXACT>
 int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   const int Kmax = std::max(p.K, p.Kt);
-  // K1: persistent, two TMA stages (prefetch one subcarrier ahead)
+  p.exact = EXACT ? 1 : 0;
+  // ------------------------------------------------------------------ K1
   cgm::K1Split sp;
   sp.plan(UP, p.B, p.S);
-  // exact tracker, U = 32 / 64: the Chebyshev basis products run in their
-  // own kernel (cgm_basis.cuh), so the channel kernel needs no basis buffers;
-  // CGMIMO_BASIS=inline keeps them in the channel kernel
-  bool basis_ext = false;
-  if constexpr (EXACT && (UP == 32 || UP == 64)) {
-    const char* e = env("CGMIMO_BASIS");
-    basis_ext = p.S > 0 && p.K > 0 && !(e && std::strcmp(e, "inline") == 0) &&
-                cgm::BasisGeo<UP>::SMEM <= ctx->max_smem;
-  }
-  p.basis_ext = basis_ext ? 1 : 0;
-  // one vector per subcarrier (cfg4): the basis kernel also does the
-  // extraction and the LLRs (basis_kernel<UP, true>), run after the CG; the
-  // workspace carries the CG history instead of T_1..T_K.  CGMIMO_FX=0 keeps
-  // the materialised basis; forced solve variants keep it too.
-  {
-    const char* fxe = env("CGMIMO_FX");
-    p.fx = (basis_ext && p.S == 1 && p.St == 0 && !env("CGMIMO_SOLVE") &&
-            !(fxe && std::strcmp(fxe, "0") == 0)) ? 1 : 0;
-  }
-  // fx with U = 32, opt-in (CGMIMO_FXFUSED=1): one warp per subcarrier does
-  // Gram + matched filter + CG (fused_rows32_approx_kernel<16, true>) in place
-  // of the tensor-core channel kernel and the CG kernel -- measured slower on
-  // cfg4a (1.54 ms against 1.21 + 0.21 ms, K = 2)
-  bool fxfused = false;
-  int fx_smem = 0;
-  if constexpr (EXACT && UP == 32) {
-    const char* e = env("CGMIMO_FXFUSED");
-    const uintptr_t al = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
-    cgm::FusedSmem FL;
-    FL.plan(p.B, p.S);
-    fxfused = p.fx && p.U == 32 && p.S <= 16 && !p.hd_layout && (p.B % 2) == 0 && (al & 15u) == 0 &&
-              FL.total <= ctx->max_smem && e && std::strcmp(e, "1") == 0;
-    fx_smem = FL.total;
-    if (fxfused) p.fx = 2;  // G rows not exactly Hermitian: the basis kernel symmetrises
-  }
-  const bool k1_basis = EXACT && !basis_ext;
   cgm::K1Smem<UP> L1;
-  L1.plan(p.B, p.S, k1_basis, 2);
+  L1.plan(p.B, p.S, 2);
   if (L1.total > ctx->max_smem) {  // very large B: single stage
     sp.nstage = 1;
-    L1.plan(p.B, p.S, k1_basis, 1);
+    L1.plan(p.B, p.S, 1);
   }
   p.k1_pair = sp.nstage;
   p.k1_spl = sp.spl;
   p.k1_wpp = sp.wpp;
-  int nt1 = 32 * sp.wpp;
-  cgm::K2Smem<UP> L2;
-  L2.plan(p.B, p.S, p.St, Kmax, EXACT);
-  if (L1.total > ctx->max_smem || L2.total > ctx->max_smem)
-    return fail(ctx, CGM_EINVAL,
-                "per-subcarrier working set (%d / %d B) exceeds shared memory (%d B)", L1.total,
-                L2.total, ctx->max_smem);
-  cgm::WsOffsets W;
-  W.plan(UP, p.S, p.K, EXACT, p.fx);
+  int nt1 = 32 * sp.wpp, smem1 = L1.total;
   void (*k1)(cgm::KernelParams) = cgm::channel_kernel<UP, EXACT>;
-  void (*k2)(cgm::KernelParams) = cgm::solve_kernel<UP, EXACT>;
-  int smem2 = L2.total;
-  int smem1 = L1.total;
-  // U = 32, natural layout, whole 64-antenna blocks: Gram + matched filter on
-  // the tensor cores (cgm_tc.cuh); CGMIMO_CHANNEL=ffma keeps the FFMA kernel
   bool use_tc = false;
   if constexpr (UP == 32) {
-    const char* force = env("CGMIMO_CHANNEL");
     // the tensor-core kernel stages Y per 64-antenna block (64 S complex,
     // always a 16-byte multiple), so odd S is fine there (cfg4: S = 1)
     const uintptr_t al = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
     const int tc_tma = (!p.hd_layout && p.U == UP && (al & 15u) == 0) ? 1 : 0;
-    if (cgm::tc::supported(p.U, p.B, p.S, tc_tma) && !(force && std::strcmp(force, "ffma") == 0)) {
+    if (cgm::tc::supported(p.U, p.B, p.S, tc_tma) && !(ctx->policy & kPolFfmaChannel)) {
       cgm::tc::Smem T;
       int nstg = 3;
-      T.plan(p.S, EXACT, nstg);
-      if (T.total > ctx->max_smem) T.plan(p.S, EXACT, nstg = 2);
+      T.plan(p.S, nstg);
+      if (T.total > ctx->max_smem) T.plan(p.S, nstg = 2);
       if (T.total <= ctx->max_smem) {
         use_tc = true;
         p.k1_pair = nstg;
         smem1 = T.total;
-        // epilogue / split warps (CGMIMO_TC_WARPS=EP,SP; SP = 0: the same
-        // warps do both).  Measured best (tools/microbench/tc_bench.cu and
-        // bench.py, cfg2: 16 unified 37.9 us vs 8 + 8 specialised 39.4 us):
-        // approx 16 unified; exact 8 unified for few vectors per subcarrier
-        // (cfg4a: 2.28 vs 2.37 ms for 8 + 8), 8 + 8 specialised for many
-        // (cfg5, S = 16: 15.7 vs 16.1 ms per step)
-        int nep = EXACT ? 8 : 16, nsp = (EXACT && p.S >= 8) ? 8 : 0;
-        if (const char* w = env("CGMIMO_TC_WARPS")) std::sscanf(w, "%d,%d", &nep, &nsp);
-        if (nep == 16 && nsp == 0)
-          k1 = cgm::channel_tc_kernel<EXACT, 16, 0>;
-        else if (nep == 4 && nsp == 8)
-          k1 = cgm::channel_tc_kernel<EXACT, 4, 8>;
-        else if (nep == 8 && nsp == 8)
-          k1 = cgm::channel_tc_kernel<EXACT, 8, 8>;
-        else
-          k1 = cgm::channel_tc_kernel<EXACT, 8, 0>, nep = 8, nsp = 0;
-        nt1 = 32 * (nep + nsp + 2);
+        // split / epilogue warps, measured (tools/microbench/tc_bench.cu,
+        // bench.py): approximate 16 unified (cfg2 37.9 vs 39.4 us for 8 + 8
+        // specialised); exact 8 unified for few vectors per subcarrier, 8 + 8
+        // specialised from S = 8 on
+        if (!EXACT) {
+          k1 = cgm::channel_tc_kernel<16, 0>;
+          nt1 = 32 * 18;
+        } else if (p.S >= 8) {
+          k1 = cgm::channel_tc_kernel<8, 8>;
+          nt1 = 32 * 18;
+        } else {
+          k1 = cgm::channel_tc_kernel<8, 0>;
+          nt1 = 32 * 10;
+        }
       }
-    }
-  }
-  // K2: lane-per-row kernel by default; CGMIMO_SOLVE=tiles selects the
-  // block-tiled FFMA2 CG (cgm_solve32.cuh, U = 32, >= 8 systems), which
-  // issues ~25% fewer instructions but measured slower on cfg2 / cfg5 (lower
-  // occupancy: 50 vs 43 us on cfg2); CGMIMO_SOLVE_TS=2|4
-  bool use_s32 = false;
-  int ts2 = 2;
-  if constexpr (UP == 32) {
-    const char* force = env("CGMIMO_SOLVE");
-    if (const char* t = env("CGMIMO_SOLVE_TS")) ts2 = std::atoi(t) == 4 ? 4 : 2;
-    cgm::S32Smem T2;
-    T2.plan(p.B, p.S, p.St, Kmax, EXACT, ts2);
-    if (p.S + p.St >= 8 && T2.total <= ctx->max_smem && force && std::strcmp(force, "tiles") == 0) {
-      use_s32 = true;
-      k2 = ts2 == 4 ? cgm::solve32_kernel<EXACT, 4> : cgm::solve32_kernel<EXACT, 2>;
-      smem2 = T2.total;
-    }
-  }
-  // persistent K2 with the next subcarrier's G + MF prefetched: measured
-  // faster with many systems per subcarrier (cfg5, S + St = 32: 14.4 vs
-  // 15.7 ms) and slower with few (cfg2 45.8 vs 43.3 us, cfg4 +13-40%: the
-  // static subcarrier split loses the hardware's dynamic balancing), so on
-  // from 24 systems; CGMIMO_SOLVE=pf / nopf force it either way
-  bool use_pf = false;
-  {
-    const char* force = env("CGMIMO_SOLVE");
-    const bool want = force ? std::strcmp(force, "pf") == 0
-                            : (p.S + p.St >= 24);
-    if (!use_s32 && want) {
-      const int need = 128 + 2 * cgm::k2_pre_bytes(UP, p.S) + L2.total;
-      if (need <= ctx->max_smem) {
-        use_pf = true;
-        k2 = cgm::solve_kernel_pf<UP, EXACT>;
-        smem2 = need;
-      }
-    }
-  }
-  // U = 32: Gram row in registers, packed FFMA2 matvec (cgm_rows32.cuh).
-  // Default for uplink-only calls (St = 0): one warp per (subcarrier, system
-  // pair), approximate (cfg2 43.4 -> 35.2 us) or exact tracker with the
-  // extraction inside the warp; CGMIMO_SOLVE=rows selects the CTA-per-
-  // subcarrier form (any systems, CTA-wide tails), CGMIMO_SOLVE=lanes the
-  // lane-per-row kernel
-  bool use_rows = false, use_pairs = false;
-  int rows_ns = 2;  // systems per warp of the pairs kernels
-  bool rows_pf = false;
-  if constexpr (UP == 32) {
-    const char* force = env("CGMIMO_SOLVE");
-    // uplink + precoding on the same channels (cfg5): the CTA-per-subcarrier
-    // rows kernel with 8 warps (11.6 vs 12.7 ms for the persistent lane kernel)
-    const bool cta = force ? std::strcmp(force, "rows") == 0 : (p.S > 0 && p.St > 0);
-    if (!use_s32 && !force && p.St == 0 && p.K <= cgm::kMaxK) {
-      use_rows = use_pairs = true;
-      use_pf = false;
-      k2 = EXACT ? cgm::solve_rows32_exact_pairs_kernel : cgm::solve_rows32_pairs_kernel<2>;
-      smem2 = 0;
-      if (!EXACT && env("CGMIMO_ROWS_NS") && std::atoi(env("CGMIMO_ROWS_NS")) == 4) {
-        k2 = cgm::solve_rows32_pairs_kernel<4>;
-        rows_ns = 4;
-      } else if (!EXACT && env("CGMIMO_ROWS_NS") && std::atoi(env("CGMIMO_ROWS_NS")) == 1) {
-        k2 = cgm::solve_rows32_pairs_kernel<1>;
-        rows_ns = 1;
-      } else if (!EXACT && env("CGMIMO_ROWS_PF") && std::atoi(env("CGMIMO_ROWS_PF")) == 1) {
-        k2 = cgm::solve_rows32_pairs_pf_kernel;  // persistent, next item prefetched
-        rows_pf = true;
-        smem2 = 4 * (32 * 32 + 6 * 32) * 8;
-      }
-    } else if (!use_s32 && cta) {
-      cgm::Rows32Smem R;
-      R.plan(p.B, p.S, p.St, Kmax, EXACT);
-      if (R.total <= ctx->max_smem) {
-        use_rows = true;
-        use_pf = false;
-        k2 = cgm::solve_rows32_kernel<EXACT>;
-        smem2 = R.total;
-      }
-    }
-  }
-  CGM_PREP(ctx, k2, 32, smem2, nullptr);
-  // exact tracker, U = 32 / 64: the Chebyshev basis products in their own
-  // kernel (cgm_basis.cuh) instead of the channel kernel's epilogue;
-  // CGMIMO_BASIS=inline keeps them in the channel kernel
-  void (*kb)(cgm::KernelParams) = nullptr;
-  int nb_t = 0, nb_smem = 0, nb_spc = 1;
-  if constexpr (EXACT && (UP == 32 || UP == 64)) {
-    if (basis_ext) {
-      using BG = cgm::BasisGeo<UP>;
-      kb = p.fx ? cgm::basis_kernel<UP, true> : cgm::basis_kernel<UP, false>;
-      nb_t = BG::NT;
-      nb_smem = BG::SMEM;
-      nb_spc = BG::SPC;
-      CGM_PREP(ctx, kb, nb_t, nb_smem, nullptr);
     }
   }
   int occ1 = 0;
   CGM_PREP(ctx, k1, nt1, smem1, &occ1);
   if (occ1 < 1) return fail(ctx, CGM_EINVAL, "channel kernel does not fit on an SM");
   if (use_tc) occ1 = 1;  // one CTA (and all 512 TMEM columns) per SM
-  // K2 block: enough lane groups for every system at once (>= UP threads
-  // for the exact extraction), at most 8 warps
+  // ------------------------------------------------------------------ KM
+  void (*km)(cgm::KernelParams) = nullptr;
+  int nm_t = 0, nm_smem = 0, nm_spc = 1;
+  if constexpr (EXACT) {
+    if (p.S > 0) {
+      using MG = cgm::MomGeo<UP>;
+      // FP32 products up to K = 8, FP64 beyond (cgm_moments.cuh)
+      const bool dbl = p.K > 8;
+      km = dbl ? cgm::moments_kernel<UP, double> : cgm::moments_kernel<UP, float>;
+      nm_smem = dbl ? MG::template smem<double>() : MG::template smem<float>();
+      nm_t = MG::NT;
+      nm_spc = MG::SPC;
+      if (nm_smem > ctx->max_smem)
+        return fail(ctx, CGM_EINVAL, "exact tracker: %d B of shared memory per moments CTA exceed %d",
+                    nm_smem, ctx->max_smem);
+      CGM_PREP(ctx, km, nm_t, nm_smem, nullptr);
+    }
+  }
+  // ------------------------------------------------------------------ K2
+  // U = 32 (default): the Gram row lives in registers (cgm_rows32.cuh) --
+  // uplink only: one warp per (subcarrier, pair of systems) (one system for
+  // S = 1), outputs from the warp; with downlink systems: one 8-warp CTA per
+  // subcarrier with the precoder tail.  Otherwise the lane-per-row kernel
+  // (cgm_split.cuh), persistent with a prefetched workspace from 24
+  // systems per subcarrier on.
+  cgm::K2Smem<UP> L2;
+  L2.plan(p.B, p.S, p.St, Kmax, EXACT);
+  if (L2.total > ctx->max_smem)
+    return fail(ctx, CGM_EINVAL, "per-subcarrier working set (%d B) exceeds shared memory (%d B)",
+                L2.total, ctx->max_smem);
+  void (*k2)(cgm::KernelParams) = cgm::solve_kernel<UP, EXACT>;
+  int smem2 = L2.total;
+  enum { kLanes, kLanesPf, kPairs, kRowsCta } mode = kLanes;
+  int pair_ns = 2;
+  if constexpr (UP == 32) {
+    if (!(ctx->policy & kPolLaneSolve)) {
+      if (p.St == 0) {
+        mode = kPairs;
+        pair_ns = p.S == 1 ? 1 : 2;
+        k2 = pair_ns == 1 ? cgm::solve_rows32_pairs_kernel<EXACT, 1>
+                          : cgm::solve_rows32_pairs_kernel<EXACT, 2>;
+        smem2 = 0;
+      } else {
+        cgm::Rows32Smem R;
+        R.plan(p.B, p.S, p.St, Kmax, EXACT);
+        if (R.total <= ctx->max_smem) {
+          mode = kRowsCta;
+          k2 = cgm::solve_rows32_kernel<EXACT>;
+          smem2 = R.total;
+        }
+      }
+    }
+  }
+  if (mode == kLanes && p.S + p.St >= 24) {
+    const int need = 128 + 2 * cgm::k2_pre_bytes(UP, p.S) + L2.total;
+    if (need <= ctx->max_smem) {
+      mode = kLanesPf;
+      k2 = cgm::solve_kernel_pf<UP, EXACT>;
+      smem2 = need;
+    }
+  }
+  CGM_PREP(ctx, k2, 32, smem2, nullptr);
+  // K2 block: lanes kernel -- enough lane groups for every system (>= UP
+  // threads for the exact extraction), at most 8 warps; row CTA kernel: 8
+  // warps from 16 systems on
   using GE = cgm::K2Geo<UP>;
   const int nsys = p.S + p.St;
   int nw2 = (nsys + GE::GPW * GE::NS - 1) / (GE::GPW * GE::NS);
   if (EXACT) nw2 = std::max(nw2, std::max(4, UP / 32));
   nw2 = std::max(1, std::min(8, nw2));
-  if (use_s32) nw2 = ((nsys + ts2 - 1) / ts2 * 8 + 31) / 32;  // 8 threads per tile, whole warps
-  if (use_rows) {
-    nw2 = (p.S + p.St) >= 16 ? 8 : 2;
-    if (const char* e = env("CGMIMO_ROWS_WARPS")) nw2 = std::max(1, std::min(8, std::atoi(e)));
-  }
+  if (mode == kRowsCta) nw2 = nsys >= 16 ? 8 : 2;
   long g2cap = 1L << 40;
-  if (use_pf) {
+  if (mode == kLanesPf) {
     int occ2 = 0;
     CGM_PREP(ctx, k2, 32 * nw2, smem2, &occ2);
     g2cap = static_cast<long>(std::max(occ2, 1)) * ctx->sms;
   }
-  // chunk so that workspace + channel (+ Y) of a chunk fit comfortably in L2
+  // --------------------------------------------------------------- chunks
+  cgm::WsOffsets W;
+  W.plan(UP, p.S, p.K, EXACT);
   const size_t per_sc = static_cast<size_t>(W.stride) * 8 + static_cast<size_t>(p.B) * p.U * 8 +
                         static_cast<size_t>(p.B) * p.S * 8;
   long chunk = static_cast<long>((80ull << 20) / std::max<size_t>(per_sc, 1));
   chunk = std::max<long>(chunk, static_cast<long>(ctx->sms) * occ1);
-  // external basis: the basis products need several full waves per launch
-  // more than they need the workspace in L2 (T_1..T_K then round-trips HBM)
-  if (kb) chunk = std::max<long>(chunk, static_cast<long>(ctx->sms) * 32);
   chunk = std::min(chunk, p.n_sc);
-  // overlap K1(c+1) with K2(c): at least `ovl` chunks (CGMIMO_OVERLAP_CHUNKS,
-  // default 1 = off: measured slower on cfg2/cfg3/cfg5)
-  int ovl = 1;
-  if (const char* e = env("CGMIMO_OVERLAP_CHUNKS")) ovl = std::max(1, std::atoi(e));
-  const long min_chunk = static_cast<long>(ctx->sms) * occ1;
-  if (ovl > 1 && p.n_sc >= 2 * min_chunk)
-    chunk = std::min(chunk, std::max(min_chunk, (p.n_sc + ovl - 1) / ovl));
-  const long total = p.n_sc;
-  const bool overlap = chunk < total && ovl > 1;
-  const size_t ws_half = static_cast<size_t>(chunk) * W.stride * sizeof(float2);
-  const size_t ws_need = ws_half * (overlap ? 2 : 1);
-  if (ws_need > ctx->tscratch_bytes) {
-    if (ctx->tscratch) cudaFree(ctx->tscratch);
-    ctx->tscratch = nullptr;
-    ctx->tscratch_bytes = 0;
-    CGM_CUDA(ctx, cudaMalloc(&ctx->tscratch, ws_need));
-    ctx->tscratch_bytes = ws_need;
-  }
-  cudaStream_t s1 = st, s2 = st;
-  if (overlap) {
-    if (!ctx->ov[0]) {
-      for (int i = 0; i < 2; ++i) CGM_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->ov[i], cudaStreamNonBlocking));
-      for (int i = 0; i < 5; ++i) CGM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ov_ev[i], cudaEventDisableTiming));
-    }
-    s1 = ctx->ov[0];
-    s2 = ctx->ov[1];
-    CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[0], st));  // order after prior work on st
-    CGM_CUDA(ctx, cudaStreamWaitEvent(s1, ctx->ov_ev[0], 0));
-    CGM_CUDA(ctx, cudaStreamWaitEvent(s2, ctx->ov_ev[0], 0));
-  }
-  long ci = 0;
-  for (long c0 = 0; c0 < total; c0 += chunk, ++ci) {
-    const long n = std::min(chunk, total - c0);
-    const int half = overlap ? static_cast<int>(ci & 1) : 0;
-    p.ws = reinterpret_cast<float2*>(reinterpret_cast<char*>(ctx->tscratch) + half * ws_half);
-    p.sc_base = c0;
-    p.n_sc = n;
+  const int rc = ensure_ws(ctx, static_cast<size_t>(chunk) * W.stride * sizeof(float2));
+  if (rc) return rc;
+  p.ws = reinterpret_cast<float2*>(ctx->tscratch);
+  for (long c0 = 0; c0 < p.n_sc; c0 += chunk) {
+    const long n = std::min(chunk, p.n_sc - c0);
+    cgm::KernelParams q = p;
+    q.sc_base = c0;
+    q.n_sc = n;
     const long g1 = std::max<long>(1, std::min<long>(n, static_cast<long>(occ1) * ctx->sms));
-    if (overlap && ci >= 2)  // K2 of chunk ci-2 has released this workspace half
-      CGM_CUDA(ctx, cudaStreamWaitEvent(s1, ctx->ov_ev[3 + half], 0));
-    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
-    if (ctx->profiling) {
-      e0 = prof_event(ctx);
-      e1 = prof_event(ctx);
-      e2 = prof_event(ctx);
-      e3 = prof_event(ctx);
-      cudaEventRecord(e0, s1);
+    int r = timed(ctx, st, 1, [&] { k1<<<static_cast<unsigned>(g1), nt1, smem1, st>>>(q); });
+    if (r) return r;
+    if (km) {
+      r = timed(ctx, st, 3, [&] {
+        km<<<static_cast<unsigned>((n + nm_spc - 1) / nm_spc), nm_t, nm_smem, st>>>(q);
+      });
+      if (r) return r;
     }
-    if (fxfused) {
-      auto kf = cgm::fused_rows32_approx_kernel<16, EXACT>;
-      CGM_PREP(ctx, kf, 32, fx_smem, nullptr);
-      kf<<<static_cast<unsigned>(n), 32, fx_smem, s1>>>(p);
-    } else {
-      k1<<<static_cast<unsigned>(g1), nt1, smem1, s1>>>(p);
-    }
-    CGM_CUDA(ctx, cudaGetLastError());
-    if (ctx->profiling) cudaEventRecord(e1, s1);
-    if (kb && !p.fx) {
-      cudaEvent_t b0 = nullptr, b1 = nullptr;
-      if (ctx->profiling) {
-        b0 = prof_event(ctx);
-        b1 = prof_event(ctx);
-        cudaEventRecord(b0, s1);
-      }
-      kb<<<static_cast<unsigned>((n + nb_spc - 1) / nb_spc), nb_t, nb_smem, s1>>>(p);
-      CGM_CUDA(ctx, cudaGetLastError());
-      if (ctx->profiling) {
-        cudaEventRecord(b1, s1);
-        ctx->ev_log.push_back({3, {b0, b1}});
-      }
-      ctx->launches += 1;
-    }
-    if (overlap) {
-      CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[1 + half], s1));
-      CGM_CUDA(ctx, cudaStreamWaitEvent(s2, ctx->ov_ev[1 + half], 0));
-    }
-    if (ctx->profiling) cudaEventRecord(e2, s2);
-    if (fxfused)
-      ;  // the CG ran inside the fused kernel
-    else if (use_pairs && rows_pf)  // persistent: four CTAs per SM
-      k2<<<static_cast<unsigned>(std::min<long>((n * ((p.S + 1) / 2) + 3) / 4, 4L * ctx->sms)), 128,
-           smem2, s2>>>(p);
-    else if (use_pairs)  // 4 warps per CTA, one (subcarrier, system pair) per warp
-      k2<<<static_cast<unsigned>((n * ((p.S + rows_ns - 1) / rows_ns) + 3) / 4), 128, 0, s2>>>(p);
-    else
-      k2<<<static_cast<unsigned>(std::min(n, g2cap)), 32 * nw2, smem2, s2>>>(p);
-    CGM_CUDA(ctx, cudaGetLastError());
-    if (ctx->profiling) {
-      cudaEventRecord(e3, s2);
-      ctx->ev_log.push_back({1, {e0, e1}});
-      ctx->ev_log.push_back({2, {e2, e3}});
-    }
-    if (kb && p.fx) {  // basis + extraction after the CG
-      cudaEvent_t b0 = nullptr, b1 = nullptr;
-      if (ctx->profiling) {
-        b0 = prof_event(ctx);
-        b1 = prof_event(ctx);
-        cudaEventRecord(b0, s2);
-      }
-      kb<<<static_cast<unsigned>((n + nb_spc - 1) / nb_spc), nb_t, nb_smem, s2>>>(p);
-      CGM_CUDA(ctx, cudaGetLastError());
-      if (ctx->profiling) {
-        cudaEventRecord(b1, s2);
-        ctx->ev_log.push_back({3, {b0, b1}});
-      }
-      ctx->launches += 1;
-    }
-    if (overlap) CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[3 + half], s2));
-    ctx->launches += 2;
-  }
-  if (overlap) {  // the caller's stream waits for both internal streams
-    CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[0], s1));
-    CGM_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ov_ev[0], 0));
-    CGM_CUDA(ctx, cudaEventRecord(ctx->ov_ev[0], s2));
-    CGM_CUDA(ctx, cudaStreamWaitEvent(st, ctx->ov_ev[0], 0));
+    r = timed(ctx, st, 2, [&] {
+      if (mode == kPairs)  // 4 warps per CTA, one (subcarrier, system group) per warp
+        k2<<<static_cast<unsigned>((n * ((p.S + pair_ns - 1) / pair_ns) + 3) / 4), 128, 0, st>>>(q);
+      else
+        k2<<<static_cast<unsigned>(std::min(n, g2cap)), 32 * nw2, smem2, st>>>(q);
+    });
+    if (r) return r;
   }
   return CGM_OK;
 }
@@ -553,12 +371,6 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
 template <int UP>
 int dispatch_split(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
   return exact ? launch_split<UP, true>(ctx, p, st) : launch_split<UP, false>(ctx, p, st);
-}
-
-template <int UP, int NT>
-int dispatch_exact(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
-  return exact ? plan_and_launch<UP, NT, true>(ctx, p, st)
-               : plan_and_launch<UP, NT, false>(ctx, p, st);
 }
 
 // Cholesky / CGLS / Neumann detection and precoding (cgm_alt.cuh): one CTA
@@ -576,25 +388,20 @@ int launch_alt(cgm_ctx* ctx, cgm::KernelParams& p, cudaStream_t st) {
   int occ = 0;
   CGM_PREP(ctx, k, cgm::alt::NT, static_cast<int>(smem), &occ);
   const long grid = std::max<long>(1, std::min<long>(p.n_sc, static_cast<long>(std::max(occ, 1)) * ctx->sms));
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (ctx->profiling) {
-    e0 = prof_event(ctx);
-    e1 = prof_event(ctx);
-    cudaEventRecord(e0, st);
-  }
-  k<<<static_cast<unsigned>(grid), cgm::alt::NT, smem, st>>>(p);
-  CGM_CUDA(ctx, cudaGetLastError());
-  if (ctx->profiling) {
-    cudaEventRecord(e1, st);
-    ctx->ev_log.push_back({2, {e0, e1}});
-  }
-  ++ctx->launches;
-  return CGM_OK;
+  return timed(ctx, st, 2, [&] { k<<<static_cast<unsigned>(grid), cgm::alt::NT, smem, st>>>(p); });
 }
 
 // Fused small-U CG precoder (cgm_precode_small.cuh): pure precode calls with
-// H_d in the reference layout, U <= 16.  CGMIMO_PRECODE=split keeps the
-// channel + solve pair.
+// H_d in the reference layout, U <= 16, one warp per subcarrier.
+bool precode_small_ok(cgm_ctx* ctx, const cgm::KernelParams& p) {
+  if (!(p.S == 0 && p.St > 0 && p.hd_layout && p.U <= 16 && p.B <= 512 && p.B >= 4 && p.B % 2 == 0))
+    return false;
+  if (ctx->policy & kPolSplitSmall) return false;
+  cgm::PrecodeSmallSmem L;
+  L.plan(up_of(p.U), p.B, p.St);
+  return L.total <= ctx->max_smem;
+}
+
 template <int UP>
 int launch_precode_small(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   cgm::PrecodeSmallSmem L;
@@ -605,68 +412,17 @@ int launch_precode_small(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   const long grid = std::max<long>(1, std::min<long>(p.n_sc, static_cast<long>(std::max(occ, 1)) * ctx->sms));
   p.use_tma = ((p.B % 2) == 0 && (reinterpret_cast<uintptr_t>(p.H) & 15u) == 0) ? 1 : 0;
   p.sc_base = 0;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (ctx->profiling) {
-    e0 = prof_event(ctx);
-    e1 = prof_event(ctx);
-    cudaEventRecord(e0, st);
-  }
-  k<<<static_cast<unsigned>(grid), cgm::PrecodeSmallGeo<UP>::NT, L.total, st>>>(p);
-  CGM_CUDA(ctx, cudaGetLastError());
-  if (ctx->profiling) {
-    cudaEventRecord(e1, st);
-    ctx->ev_log.push_back({2, {e0, e1}});
-  }
-  ++ctx->launches;
-  return CGM_OK;
-}
-
-// Fully fused U = 32 approximate-tracker detector (one warp per subcarrier,
-// cgm_rows32.cuh): Gram + matched filters + every system's CG in one kernel.
-// Opt-in (CGMIMO_FUSED=1): measured 111 us on cfg2 against 67 us for the
-// tensor-core channel kernel + pairs solve kernel -- eight warps per SM
-// leave the fourteen sequential CG chains of a subcarrier latency-exposed.
-bool fused_rows32_ok(cgm_ctx* ctx, const cgm::KernelParams& p, bool exact) {
-  if (exact || p.U != 32 || p.St != 0 || p.S < 1 || p.S > 16 || p.hd_layout || (p.B % 2) != 0)
-    return false;
-  const uintptr_t al = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
-  if (al & 15u) return false;
-  const char* e = env("CGMIMO_FUSED");
-  if (!(e && std::strcmp(e, "1") == 0)) return false;
-  cgm::FusedSmem L;
-  L.plan(p.B, p.S);
-  return L.total <= ctx->max_smem;
-}
-
-int launch_fused_rows32(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
-  cgm::FusedSmem L;
-  L.plan(p.B, p.S);
-  auto k = cgm::fused_rows32_approx_kernel<16>;
-  CGM_PREP(ctx, k, 32, L.total, nullptr);
-  p.sc_base = 0;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (ctx->profiling) {
-    e0 = prof_event(ctx);
-    e1 = prof_event(ctx);
-    cudaEventRecord(e0, st);
-  }
-  k<<<static_cast<unsigned>(p.n_sc), 32, L.total, st>>>(p);
-  CGM_CUDA(ctx, cudaGetLastError());
-  if (ctx->profiling) {
-    cudaEventRecord(e1, st);
-    ctx->ev_log.push_back({2, {e0, e1}});
-  }
-  ++ctx->launches;
-  return CGM_OK;
+  return timed(ctx, st, 2, [&] {
+    k<<<static_cast<unsigned>(grid), cgm::PrecodeSmallGeo<UP>::NT, L.total, st>>>(p);
+  });
 }
 
 // Fused small-U CG detector (cgm_uplink_small.cuh): uplink-only calls with
-// U <= 16, one warp per subcarrier.  CGMIMO_UPSMALL=split keeps the pair.
+// U <= 16, one warp per subcarrier.
 bool uplink_small_ok(cgm_ctx* ctx, const cgm::KernelParams& p, bool exact) {
   if (!(p.St == 0 && p.S >= 1 && !p.hd_layout && p.U <= 16 && p.K >= 1 && p.K <= cgm::kMaxK))
     return false;
-  const char* e = env("CGMIMO_UPSMALL");
-  if (e && std::strcmp(e, "split") == 0) return false;
+  if (ctx->policy & kPolSplitSmall) return false;
   cgm::UpSmallSmem L;
   L.plan(up_of(p.U), p.B, p.U, p.S, p.K, exact);
   return L.total <= ctx->max_smem;
@@ -683,61 +439,29 @@ int launch_uplink_small(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   const uintptr_t al = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
   p.use_tma = ((p.B * p.U) % 2 == 0 && (p.B * p.S) % 2 == 0 && (al & 15u) == 0) ? 1 : 0;
   p.sc_base = 0;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (ctx->profiling) {
-    e0 = prof_event(ctx);
-    e1 = prof_event(ctx);
-    cudaEventRecord(e0, st);
-  }
-  k<<<static_cast<unsigned>(grid), 32, L.total, st>>>(p);
-  CGM_CUDA(ctx, cudaGetLastError());
-  if (ctx->profiling) {
-    cudaEventRecord(e1, st);
-    ctx->ev_log.push_back({2, {e0, e1}});
-  }
-  ++ctx->launches;
-  return CGM_OK;
-}
-
-bool precode_small_ok(cgm_ctx* ctx, const cgm::KernelParams& p) {
-  if (!(p.S == 0 && p.St > 0 && p.hd_layout && p.U <= 16 && p.B <= 512 && p.B >= 4 && p.B % 2 == 0))
-    return false;
-  const char* e = env("CGMIMO_PRECODE");
-  if (e && std::strcmp(e, "split") == 0) return false;
-  cgm::PrecodeSmallSmem L;
-  L.plan(up_of(p.U), p.B, p.St);
-  return L.total <= ctx->max_smem;
+  return timed(ctx, st, 2, [&] { k<<<static_cast<unsigned>(grid), 32, L.total, st>>>(p); });
 }
 
 int launch(cgm_ctx* ctx, cgm::KernelParams& p, bool exact, cudaStream_t st) {
   if (p.n_sc <= 0) return CGM_OK;
   if (p.method != cgm::alt::kCg) return launch_alt(ctx, p, st);
   const int UP = up_of(p.U);
-  if (ctx->policy == 0 && fused_rows32_ok(ctx, p, exact)) return launch_fused_rows32(ctx, p, st);
-  if (ctx->policy == 0 && uplink_small_ok(ctx, p, exact)) {
+  if (uplink_small_ok(ctx, p, exact)) {
     if (UP == 8) return exact ? launch_uplink_small<8, true>(ctx, p, st) : launch_uplink_small<8, false>(ctx, p, st);
     return exact ? launch_uplink_small<16, true>(ctx, p, st) : launch_uplink_small<16, false>(ctx, p, st);
   }
-  if (ctx->policy == 0 && precode_small_ok(ctx, p))
+  if (precode_small_ok(ctx, p))
     return UP == 8 ? launch_precode_small<8>(ctx, p, st) : launch_precode_small<16>(ctx, p, st);
   const uintptr_t a = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
   // 1: H and Y by bulk copy; 2 (odd S, channel_kernel only): H by bulk copy,
   // the padded Y rows by the threads
   p.use_tma = (!p.hd_layout && p.U == UP && (p.B % 2) == 0 && (a & 15u) == 0)
                   ? ((p.S % 2) == 0 ? 1 : 2) : 0;
-  if (ctx->policy == 0) {
-    switch (UP) {
-      case 8: return dispatch_split<8>(ctx, p, exact, st);
-      case 16: return dispatch_split<16>(ctx, p, exact, st);
-      case 32: return dispatch_split<32>(ctx, p, exact, st);
-      default: return dispatch_split<64>(ctx, p, exact, st);
-    }
-  }
   switch (UP) {
-    case 8: return dispatch_exact<8, 128>(ctx, p, exact, st);
-    case 16: return dispatch_exact<16, 128>(ctx, p, exact, st);
-    case 32: return dispatch_exact<32, 288>(ctx, p, exact, st);
-    default: return dispatch_exact<64, 320>(ctx, p, exact, st);
+    case 8: return dispatch_split<8>(ctx, p, exact, st);
+    case 16: return dispatch_split<16>(ctx, p, exact, st);
+    case 32: return dispatch_split<32>(ctx, p, exact, st);
+    default: return dispatch_split<64>(ctx, p, exact, st);
   }
 }
 
@@ -813,7 +537,6 @@ cgm::KernelParams params_of(const Job& j, long n_sc) {
   p.rho_inv_u = j.S > 0 ? static_cast<float>(1.0 / j.rho_u) : 0.f;
   p.rho_inv_d = j.St > 0 ? static_cast<float>(1.0 / j.rho_d) : 0.f;
   p.n0 = static_cast<float>(j.n0);
-  if (const char* dbg = env("CGMIMO_DEBUG_WS")) p.debug = std::atoi(dbg);
   p.es = static_cast<float>(j.es);
   p.method = j.method;
   return p;
@@ -871,7 +594,7 @@ int run_job(cgm_ctx* ctx, const Job& j, unsigned flags) {
   // 4.1 M vec/s against 3.2 M with eight)
   const size_t total_bytes = per_sc * static_cast<size_t>(j.n_sc);
   int nch = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, total_bytes / (8ull << 20))));
-  if (const char* e = env("CGMIMO_HOST_CHUNKS")) nch = std::max(1, std::atoi(e));
+  if (ctx->host_chunks > 0) nch = ctx->host_chunks;
   const long min_chunk = std::max<long>(1, ctx->sms);  // keep each launch >= one wave
   if (j.n_sc >= 2 * min_chunk)
     chunk = std::min(chunk, std::max(min_chunk, (j.n_sc + nch - 1) / nch));
@@ -891,6 +614,12 @@ int run_job(cgm_ctx* ctx, const Job& j, unsigned flags) {
       if (!ctx->hev[b][k]) CGM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->hev[b][k], cudaEventDisableTiming));
   }
   cudaStream_t s_in = ctx->pipe[0], s_comp = ctx->pipe[1], s_out = ctx->pipe[2];
+  // the pipeline shares the split-path workspace with asynchronous
+  // device-pointer calls on the context stream: order after them
+  if (!ctx->order_ev) CGM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->order_ev, cudaEventDisableTiming));
+  CGM_CUDA(ctx, cudaEventRecord(ctx->order_ev, ctx->user_stream));
+  CGM_CUDA(ctx, cudaStreamWaitEvent(s_in, ctx->order_ev, 0));
+  CGM_CUDA(ctx, cudaStreamWaitEvent(s_comp, ctx->order_ev, 0));
   auto H8 = reinterpret_cast<const char*>(j.H);
   auto Y8 = reinterpret_cast<const char*>(j.Y);
   auto T8 = reinterpret_cast<const char*>(j.T);
@@ -1002,6 +731,7 @@ int cgm_ctx_create(int device, cgm_ctx** out) {
   }
   for (int i = 0; i < 3 && e == cudaSuccess; ++i)
     e = cudaStreamCreateWithFlags(&ctx->pipe[i], cudaStreamNonBlocking);
+  if (const char* hc = std::getenv("CGMIMO_HOST_CHUNKS")) ctx->host_chunks = std::max(0, std::atoi(hc));
   if (e == cudaSuccess) {
     const cgm::AxisTables t = make_axis_tables();
     e = cudaMemcpyToSymbol(cgm::c_axis, &t, sizeof t);
@@ -1025,11 +755,9 @@ int cgm_ctx_destroy(cgm_ctx* ctx) {
   for (int i = 0; i < 3; ++i)
     if (ctx->pipe[i]) cudaStreamDestroy(ctx->pipe[i]);
   if (ctx->tscratch) cudaFree(ctx->tscratch);
+  for (void* r : ctx->retired) cudaFree(r);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
-  for (int i = 0; i < 2; ++i)
-    if (ctx->ov[i]) cudaStreamDestroy(ctx->ov[i]);
-  for (int i = 0; i < 5; ++i)
-    if (ctx->ov_ev[i]) cudaEventDestroy(ctx->ov_ev[i]);
+  if (ctx->order_ev) cudaEventDestroy(ctx->order_ev);
   delete ctx;
   return CGM_OK;
 }
@@ -1071,7 +799,8 @@ int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, lon
 }
 
 int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy) {
-  if (!ctx || policy < 0 || policy > 1) return CGM_EINVAL;
+  if (!ctx || policy < 0 || policy > (kPolFfmaChannel | kPolSplitSmall | kPolLaneSolve))
+    return fail(ctx, CGM_EINVAL, "unknown kernel policy %d", policy);
   ctx->policy = policy;
   return CGM_OK;
 }

@@ -38,6 +38,22 @@ __device__ __forceinline__ void ffma2(unsigned long long& d, unsigned long long 
                                       unsigned long long b) {
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
 }
+// lane swap / broadcast of a packed float pair (FFMA2 operand shuffles)
+__device__ __forceinline__ unsigned long long f2swap_hl(unsigned long long v) {
+  unsigned long long r;
+  asm("{ .reg .f32 lo, hi; mov.b64 {lo, hi}, %1; mov.b64 %0, {hi, lo}; }" : "=l"(r) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2dup_lo(unsigned long long v) {
+  unsigned long long r;
+  asm("{ .reg .f32 lo, hi; mov.b64 {lo, hi}, %1; mov.b64 %0, {lo, lo}; }" : "=l"(r) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2dup_hi(unsigned long long v) {
+  unsigned long long r;
+  asm("{ .reg .f32 lo, hi; mov.b64 {lo, hi}, %1; mov.b64 %0, {hi, hi}; }" : "=l"(r) : "l"(v));
+  return r;
+}
 // acc += a * b
 __device__ __forceinline__ void cfma(float2& acc, float2 a, float2 b) {
 #ifndef CGM_FFMA2_CFMA

@@ -1,0 +1,435 @@
+// cgm_moments.cuh -- the exact SINR tracker through row moments of a
+// shared Chebyshev basis.
+//
+// The reference's exact tracker (ExactSinrTracker, detect.cpp:330-368) runs
+// a three-term matrix recursion per received vector and extracts
+// (tracker_exact_extract, detect.cpp:370-395), with G = A - rho^-1 I,
+//   B     = L_K G
+//   mu_i  = Re B_ii
+//   nu2_i = Es sum_{j != i} |B_ij|^2 + N0 Re sum_j B_ij conj(L_ij)
+// L_k is a real-coefficient polynomial in A (the recursion only ever
+// multiplies by A and adds scaled identities), so L_K and B are too.  In
+// the Chebyshev basis T_m = T_m(Ahat), Ahat = (A - cI)/d:
+//   L = sum_n l_n T_n  (degree K-1),   B = sum_m g_m T_m  (degree K)
+// with the coefficients l, g per vector (cheb_coef_warp: the reference's
+// recursion run on coefficients, FP64).  Write E = B - g_0 I, F = L - l_0 I.
+// The T_m commute and are Hermitian, so every quantity above is a diagonal
+// entry of a polynomial in Ahat:
+//   mu_i  = g_0 + e_i,                         e_i = sum_{m>=1} g_m D_m[i]
+//   L_ii  = l_0 + f_i,                         f_i = sum_{n>=1} l_n D_n[i]
+//   sum_{j!=i} |B_ij|^2          = (E E)_ii - e_i^2
+//   Re sum_j B_ij conj(L_ij)     = mu_i L_ii + (E F)_ii - e_i f_i
+// where D_k[i] = (T_k)_ii and (E E)_ii = sum_k ee_k D_k[i], (E F)_ii =
+// sum_k ef_k D_k[i] with ee, ef the Chebyshev products of the coefficient
+// vectors (T_a T_b = (T_{a+b} + T_{|a-b|}) / 2).  So everything a vector
+// needs from the channel is D_k[i], k = 0..2K, per row i -- a (2K+1) x U
+// table per SUBCARRIER -- and the per-vector extraction costs O(K^2 + K U)
+// instead of the reference's O(K U^3) recursion and U^3 extraction.
+//
+// The table comes from the row products of the basis matrices: with the
+// window T_{a-1}, T_a of the recursion T_{a+1} = 2 Ahat T_a - T_{a-1},
+//   D_{2a}   = 2 sum_j |T_a[i][j]|^2 - 1
+//   D_{2a-1} = 2 Re sum_j T_a[i][j] conj(T_{a-1}[i][j]) - D_1
+// for a = 1..K: K - 1 Hermitian products per subcarrier (lower tiles +
+// mirror), only three matrices resident.  The identity part g_0 I (the
+// O(1) part of B) never enters the interference sum, so the subtraction
+// (E E)_ii - e_i^2 works on small numbers.  FP32 products hold the 1e-3
+// contract with margin up to K = 8 (tools/moments_study.py: rho within
+// 4e-5 of the FP64 reference on every BASELINE shape, incl. the correlated
+// cfg5 channel); for K > 8 the products run in FP64 (K = 16 at 28 dB:
+// 1.6e-6, FP32 would give 2e-3).
+#pragma once
+
+#include <type_traits>
+
+#include "cgm_kernels.cuh"
+
+namespace cgm {
+
+// split-path workspace layout per subcarrier (float2 units): G (UP x UP,
+// full Hermitian), the S matched filters, (c, d) of the Chebyshev interval,
+// and for the exact tracker the row-moment table D_k[i] (double, k = 0..2K)
+struct WsOffsets {
+  int g, mf, cd, t, stride;
+  __host__ __device__ void plan(int UP, int S, int K, bool exact) {
+    g = 0;
+    mf = UP * UP;
+    cd = mf + S * UP;
+    t = cd + 2;
+    stride = t + (exact ? (2 * K + 1) * UP : 0);
+    stride = (stride + 1) & ~1;
+  }
+};
+
+// per subcarrier in the workspace: (c, d) at W.cd, D_k[i] (double) at W.t:
+// mom[k * UP + i], k = 0..2K
+__host__ __device__ inline int moments_words(int UP, int K) { return (2 * K + 1) * UP; }
+
+template <int UP>
+struct MomGeo {
+  static constexpr int NB = UP / 4;                 // tile rows
+  static constexpr int NTILE = NB * (NB + 1) / 2;   // lower-triangle tiles
+  static constexpr int SPC = UP == 8 ? 32 : UP == 16 ? 8 : UP == 32 ? 2 : 1;  // subcarriers per CTA
+  static constexpr int NT = ((SPC * NTILE + 31) / 32) * 32 < 64 ? 64 : ((SPC * NTILE + 31) / 32) * 32;
+  static constexpr int LD = UP + 2;                 // padded row (bank spread, 16 B aligned)
+  static constexpr int MAT = UP * LD;               // complex entries per matrix
+  template <class R>
+  static constexpr int smem() { return SPC * 3 * MAT * 2 * static_cast<int>(sizeof(R)); }
+};
+
+template <class R>
+struct Cx;
+template <>
+struct Cx<float> { using T = float2; };
+template <>
+struct Cx<double> { using T = double2; };
+
+// acc[r][c] = sum_k Ahat[i0 + r][k] T[k][j0 + c] for one 4 x 4 tile (Ahat
+// Hermitian: row i0 + r of Ahat is the conjugate of column i0 + r, read
+// along rows k of the padded smem matrix).  FP32: one packed accumulator per
+// entry, conj(a) t = t * a.x + swap(t) * (a.y, -a.y) (swap / negation are
+// FFMA2 operand modifiers); FP64: plain DFMA.
+template <int UP>
+__device__ __forceinline__ void tile_prod(const float2* A, const float2* T, int i0, int j0,
+                                          float2 (&out)[4][4]) {
+  constexpr int LD = MomGeo<UP>::LD;
+  unsigned long long acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0ull;
+  auto ld = [&](int k, ulonglong2 (&av)[2], ulonglong2 (&tv)[2]) {
+    av[0] = *reinterpret_cast<const ulonglong2*>(A + k * LD + i0);
+    av[1] = *reinterpret_cast<const ulonglong2*>(A + k * LD + i0 + 2);
+    tv[0] = *reinterpret_cast<const ulonglong2*>(T + k * LD + j0);
+    tv[1] = *reinterpret_cast<const ulonglong2*>(T + k * LD + j0 + 2);
+  };
+  ulonglong2 av[2], tv[2];
+  ld(0, av, tv);
+#pragma unroll 2
+  for (int k = 0; k < UP; ++k) {
+    const unsigned long long ah[4] = {av[0].x, av[0].y, av[1].x, av[1].y};
+    const unsigned long long t[4] = {tv[0].x, tv[0].y, tv[1].x, tv[1].y};
+    if (k + 1 < UP) ld(k + 1, av, tv);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float2 a2 = f2unpack(ah[r]);
+      const unsigned long long ax = f2pack(a2.x, a2.x), ay = f2pack(a2.y, -a2.y);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        ffma2(acc[r][c], t[c], ax);
+        ffma2(acc[r][c], f2swap_hl(t[c]), ay);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) out[r][c] = f2unpack(acc[r][c]);
+}
+
+template <int UP>
+__device__ __forceinline__ void tile_prod(const double2* A, const double2* T, int i0, int j0,
+                                          double2 (&out)[4][4]) {
+  constexpr int LD = MomGeo<UP>::LD;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) out[r][c] = make_double2(0.0, 0.0);
+#pragma unroll 2
+  for (int k = 0; k < UP; ++k) {
+    double2 a[4], t[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      a[q] = A[k * LD + i0 + q];
+      t[q] = T[k * LD + j0 + q];
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {  // conj(a) t
+        out[r][c].x = fma(a[r].x, t[c].x, fma(a[r].y, t[c].y, out[r][c].x));
+        out[r][c].y = fma(a[r].x, t[c].y, fma(-a[r].y, t[c].x, out[r][c].y));
+      }
+  }
+}
+
+// moments_kernel: per subcarrier (SPC per CTA), from G in the workspace:
+// (c, d) by power iteration (cheb_interval), Ahat, the K - 1 products of the
+// Chebyshev recursion, and D_k[i], k = 0..2K, into the workspace.
+template <int UP, class R>
+__global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelParams p) {
+  using MG = MomGeo<UP>;
+  using C = typename Cx<R>::T;
+  constexpr int MAT = MG::MAT, SPC = MG::SPC, LD = MG::LD, NT = MG::NT;
+  extern __shared__ __align__(128) unsigned char smem[];
+  C* base = reinterpret_cast<C*>(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = p.K;
+  WsOffsets W;
+  W.plan(UP, p.S, K, true);
+  const long sc0 = static_cast<long>(blockIdx.x) * SPC;
+  const int nsc = static_cast<int>(p.n_sc - sc0 < SPC ? p.n_sc - sc0 : SPC);
+  // buffer b of subcarrier s: 0 = Ahat (T_1), 1 / 2 = the recursion window
+  auto buf = [&](int s, int b) { return base + (s * 3 + b) * MAT; };
+  // G -> buffer 1 as float2 (the power iteration's input; for R = double the
+  // float copy occupies the first half of the buffer)
+  for (int s = 0; s < nsc; ++s) {
+    const float4* src = reinterpret_cast<const float4*>(p.ws + (sc0 + s) * W.stride + W.g);
+    float2* dst = reinterpret_cast<float2*>(buf(s, 1));
+    for (int e = tid; e < UP * UP / 2; e += NT) {
+      const int r = e / (UP / 2), c2 = e - r * (UP / 2);
+      *reinterpret_cast<float4*>(dst + r * LD + 2 * c2) = src[e];
+    }
+  }
+  __syncthreads();
+  __shared__ float2 cds[SPC];
+  for (int s = warp; s < nsc; s += NT / 32) {
+    // power-iteration scratch: buffer 2 (as float2)
+    const float2 cd = cheb_interval<UP, LD>(reinterpret_cast<const float2*>(buf(s, 1)),
+                                            p.rho_inv_u, reinterpret_cast<float2*>(buf(s, 2)), lane);
+    if (lane == 0) {
+      cds[s] = cd;
+      p.ws[(sc0 + s) * W.stride + W.cd] = cd;
+    }
+  }
+  __syncthreads();
+  // Ahat = (A - cI)/d = (G + (rho^-1 - c) I) / d -> buffer 0 (in R)
+  for (int e = tid; e < nsc * UP * UP; e += NT) {
+    const int s = e / (UP * UP), r = (e / UP) % UP, c = e % UP;
+    const float2 g = reinterpret_cast<const float2*>(buf(s, 1))[r * LD + c];
+    const R cc = cds[s].x, invd = R(1) / static_cast<R>(cds[s].y);
+    R x = g.x, y = g.y;
+    if (r == c) {
+      x += static_cast<R>(p.rho_inv_u) - cc;
+      y = R(0);
+    }
+    C v;
+    v.x = x * invd;
+    v.y = y * invd;
+    buf(s, 0)[r * LD + c] = v;
+  }
+  __syncthreads();
+  // row moments: thread <-> (subcarrier, row i); column reads are
+  // conflict-free and T[j][i] = conj(T[i][j]) gives the same sums
+  auto row_moments = [&](int a, int cur, int prv) {
+    // D_{2a} from T_a (buffer cur), D_{2a-1} from T_a and T_{a-1} (buffer prv, -1: I)
+    for (int e = tid; e < nsc * UP; e += NT) {
+      const int s = e / UP, i = e - s * UP;
+      const C* Ta = buf(s, cur);
+      double n2 = 0.0, x = 0.0;
+      for (int j = 0; j < UP; ++j) {
+        const C t = Ta[j * LD + i];
+        const double tx = t.x, ty = t.y;
+        n2 = __fma_rn(tx, tx, __fma_rn(ty, ty, n2));
+        if (prv >= 0) {
+          const C q = buf(s, prv)[j * LD + i];
+          x = __fma_rn(tx, static_cast<double>(q.x), __fma_rn(ty, static_cast<double>(q.y), x));
+        }
+      }
+      double* mom = reinterpret_cast<double*>(p.ws + (sc0 + s) * W.stride + W.t);
+      const double d1 = static_cast<double>(buf(s, 0)[i * LD + i].x);
+      if (a == 1) {
+        mom[i] = 1.0;
+        mom[UP + i] = d1;
+      } else {
+        mom[(2 * a - 1) * UP + i] = 2.0 * x - d1;
+      }
+      mom[2 * a * UP + i] = 2.0 * n2 - 1.0;
+    }
+  };
+  row_moments(1, 0, -1);
+  // products: thread <-> (subcarrier slot, lower tile)
+  const int slot = tid / MG::NTILE;
+  const int tile = tid - slot * MG::NTILE;
+  int rb = 0;
+  while ((rb + 1) * (rb + 2) / 2 <= tile) ++rb;
+  const int cb = tile - rb * (rb + 1) / 2;
+  const bool busy = slot < nsc;
+  const int i0 = rb * 4, j0 = cb * 4;
+  // T_a in buffer cur, T_{a-1} in buffer prv (-1: the identity), T_{a+1}
+  // written over T_{a-1} (buffer 1 / 2; never over Ahat)
+  int cur = 0, prv = -1;
+  for (int a = 1; a < K; ++a) {
+    const int out = a == 1 ? 1 : a == 2 ? 2 : prv;
+    if (busy) {
+      C acc[4][4];
+      tile_prod<UP>(buf(slot, 0), buf(slot, cur), i0, j0, acc);
+      C* Tn = buf(slot, out);
+      const C* Tp = prv >= 0 ? buf(slot, prv) : nullptr;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int i = i0 + r, j = j0 + c;
+          if (j > i) continue;
+          C prev;
+          if (Tp) prev = Tp[i * LD + j];
+          else { prev.x = i == j ? R(1) : R(0); prev.y = R(0); }
+          C val;
+          val.x = R(2) * acc[r][c].x - prev.x;
+          val.y = i == j ? R(0) : R(2) * acc[r][c].y - prev.y;
+          Tn[i * LD + j] = val;
+          if (i != j) {
+            C cv;
+            cv.x = val.x;
+            cv.y = -val.y;
+            Tn[j * LD + i] = cv;
+          }
+        }
+    }
+    __syncthreads();
+    row_moments(a + 1, out, cur);
+    __syncthreads();  // the row pass read T_a before the next product overwrites T_{a-1}
+    prv = cur;
+    cur = out;
+  }
+}
+
+// ------------------------------------------------------------ extraction
+// Chebyshev coefficients (FP64) of L_K and B = L_K (A - rho^-1 I) for one
+// system, warp-parallel (cheb_coef_warp's recursion, kept in double), then
+// the products ee = E*E and ef = E*F into `sh` (per-warp shared scratch of
+// at least 2 * (2 * kMaxK + 1) + 2 * (kMaxK + 2) doubles).  All 32 lanes call.
+struct MomCoef {
+  double g0, l0;
+};
+__device__ __forceinline__ MomCoef moments_coefs(const float* hist, int K, double cc, double dd,
+                                                 double rho_inv, double* sh) {
+  const int m = threadIdx.x & 31;
+  const int n = K + 2;
+  auto mulA = [&](double x) {
+    const double up = __shfl_down_sync(0xffffffffu, x, 1);  // x[m + 1]
+    const double dn = __shfl_up_sync(0xffffffffu, x, 1);    // x[m - 1]
+    double out = cc * x;
+    if (m + 1 < n) out += 0.5 * dd * up;
+    if (m == 1) out += dd * dn;
+    else if (m >= 2 && m < n) out += 0.5 * dd * dn;
+    return m < n ? out : 0.0;
+  };
+  // detect.cpp:336-368 on the coefficients: L_1 = alpha_1 I, then the
+  // three-term update with c1 = a_k (1 + b_{k-1}) / a_{k-1}, c2 = a_k b_{k-2} / a_{k-2}
+  double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+  double a_m1 = 1.0, a_m2 = 1.0, b_m1 = 0.0, b_m2 = 0.0;
+  for (int k = 1; k <= K; ++k) {
+    const double a = hist[(k - 1) * 2 + 0];
+    const double bb = hist[(k - 1) * 2 + 1];
+    if (k == 1) {
+      l2 = l1;
+      l1 = l0;
+      l0 = m == 0 ? a : 0.0;
+    } else {
+      const double c1 = a * (1.0 + b_m1) / a_m1, c2 = a * b_m2 / a_m2;
+      const double d1 = l0 - l1;
+      const double t = mulA(d1);
+      const double nx = l0 + c1 * d1 - a * t - c2 * (l1 - l2);
+      l2 = l1;
+      l1 = l0;
+      l0 = m < n ? nx : 0.0;
+    }
+    a_m2 = a_m1; a_m1 = a; b_m2 = b_m1; b_m1 = bb;
+  }
+  const double gm = mulA(l0) - rho_inv * l0;  // B = L (A - rho^-1 I)
+  double* gs = sh;           // [kMaxK + 2]
+  double* ls = sh + kMaxK + 2;
+  double* ee = ls + kMaxK + 2;      // [2 kMaxK + 1]
+  double* ef = ee + 2 * kMaxK + 1;  // [2 kMaxK + 1]
+  if (m < n) {
+    gs[m] = m == 0 ? 0.0 : gm;  // E = B - g_0 I
+    ls[m] = m == 0 ? 0.0 : l0;  // F = L - l_0 I
+  }
+  const double g0 = __shfl_sync(0xffffffffu, gm, 0);
+  const double l00 = __shfl_sync(0xffffffffu, l0, 0);
+  __syncwarp();
+  // Chebyshev products: (x*y)_k = 1/2 sum_{a+b=k} x_a y_b + 1/2 sum_{|a-b|=k} x_a y_b
+  for (int k = m; k <= 2 * K; k += 32) {
+    double se = 0.0, sf = 0.0;
+    for (int a = 1; a <= K; ++a) {
+      const double ga = gs[a];
+      const int b1 = k - a;
+      if (b1 >= 1 && b1 <= K) {
+        se = fma(ga, gs[b1], se);
+        sf = fma(ga, ls[b1], sf);
+      }
+      const int b2 = a - k, b3 = a + k;
+      if (b2 >= 1) {
+        se = fma(ga, gs[b2], se);
+        sf = fma(ga, ls[b2], sf);
+      }
+      if (k > 0 && b3 <= K) {
+        se = fma(ga, gs[b3], se);
+        sf = fma(ga, ls[b3], sf);
+      }
+    }
+    ee[k] = 0.5 * se;
+    ef[k] = 0.5 * sf;
+  }
+  __syncwarp();
+  return {g0, l00};
+}
+
+// Row i's mu and rho from the coefficient products in `sh` and the
+// subcarrier's moment table (detect.cpp:375-395 + safe_rho :26-29).
+__device__ __forceinline__ void moments_row(const double* sh, MomCoef c, int K, const double* mom,
+                                            int UP, int i, double es, double n0, float& mu,
+                                            float& rho) {
+  const double* gs = sh;
+  const double* ls = sh + kMaxK + 2;
+  const double* ee = ls + kMaxK + 2;
+  const double* ef = ee + 2 * kMaxK + 1;
+  double e = 0.0, f = 0.0, e2 = ee[0], efd = ef[0];
+  for (int k = 1; k <= 2 * K; ++k) {
+    const double d = mom[k * UP + i];
+    if (k <= K) {
+      e = fma(gs[k], d, e);
+      f = fma(ls[k], d, f);
+    }
+    e2 = fma(ee[k], d, e2);
+    efd = fma(ef[k], d, efd);
+  }
+  const double m = c.g0 + e;
+  const double lii = c.l0 + f;
+  const double interf = e2 - e * e;
+  const double cross = m * lii + efd - e * f;
+  const double nu2 = interf * es + cross * n0;
+  mu = static_cast<float>(m);
+  rho = nu2 < 1e-300 ? 0.f : static_cast<float>(m * m / nu2);
+}
+
+// per-warp shared scratch (doubles) for moments_coefs / moments_row
+constexpr int kMomScratch = 2 * (kMaxK + 2) + 2 * (2 * kMaxK + 1);
+
+// Exact-tracker outputs of a subcarrier's S uplink systems after the CG
+// (CTA-wide, warp per system): hist holds each system's (alpha, beta)
+// history (stride Kmax), Vs its v_K, sys_st its breakdown flag; msh is
+// nt/32 x kMomScratch doubles of shared scratch.
+template <int UP>
+__device__ __forceinline__ void moments_tail(const KernelParams& p, const float2* ws,
+                                             const WsOffsets& W, long sc, int Kmax,
+                                             const float* hist, const float2* Vs,
+                                             const uint8_t* sys_st, int nt, double* msh) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = nt >> 5;
+  const int S = p.S, U = p.U, K = p.K;
+  const float2 cdv = ws[W.cd];
+  const double* mom = reinterpret_cast<const double*>(ws + W.t);
+  double* sh = msh + warp * kMomScratch;
+  for (int s = warp; s < S; s += nw) {
+    const MomCoef c = moments_coefs(hist + s * Kmax * 2, K, cdv.x, cdv.y, p.rho_inv_u, sh);
+    const bool ok = sys_st[s] == 0;
+    for (int i = lane; i < U; i += 32) {
+      float mu, rho;
+      moments_row(sh, c, K, mom, UP, i, p.es, p.n0, mu, rho);
+      const long o = (sc * S + s) * static_cast<long>(U) + i;
+      const float2 xh = ok ? Vs[s * UP + i] : make_float2(0.f, 0.f);
+      if (!ok) mu = rho = 0.f;
+      if (p.xhat) p.xhat[o] = xh;
+      if (p.mu) p.mu[o] = mu;
+      if (p.rho) p.rho[o] = rho;
+      if (p.llr) store_llrs_fast(xh, mu, rho, p.bits, p.llr + o * p.bits);
+    }
+    if (p.status && lane == 0) p.status[sc * S + s] = ok ? 0 : 1;
+    __syncwarp();  // sh is reused by the next system
+  }
+}
+
+}  // namespace cgm

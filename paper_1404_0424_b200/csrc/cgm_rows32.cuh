@@ -20,6 +20,7 @@
 #include <type_traits>
 
 #include "cgm_split.cuh"
+#include "cgm_moments.cuh"
 
 namespace cgm {
 
@@ -34,16 +35,6 @@ struct Rows32Smem {
   }
 };
 
-__device__ __forceinline__ unsigned long long f2dup_lo(unsigned long long v) {
-  unsigned long long r;
-  asm("{ .reg .f32 lo, hi; mov.b64 {lo, hi}, %1; mov.b64 %0, {lo, lo}; }" : "=l"(r) : "l"(v));
-  return r;
-}
-__device__ __forceinline__ unsigned long long f2dup_hi(unsigned long long v) {
-  unsigned long long r;
-  asm("{ .reg .f32 lo, hi; mov.b64 {lo, hi}, %1; mov.b64 %0, {hi, hi}; }" : "=l"(r) : "l"(v));
-  return r;
-}
 
 // sum over the 32 lanes of two values at once: 5 + 1 shuffles instead of 10
 __device__ __forceinline__ void warp_sum2(float& a, float& b) {
@@ -255,14 +246,11 @@ __global__ void __launch_bounds__(256, 2) solve_rows32_kernel(const KernelParams
   K2Smem<UP> L;
   L.plan(B, S, St, Kmax, EXACT);
   WsOffsets W;
-  W.plan(UP, S, p.K, EXACT, p.fx);
+  W.plan(UP, S, p.K, EXACT);
   float2* Vs = reinterpret_cast<float2*>(smem + L.vs);
   float2* Qs = reinterpret_cast<float2*>(smem + L.qs);
   float* hist = reinterpret_cast<float*>(smem + L.hist);
   uint8_t* sys_st = reinterpret_cast<uint8_t*>(smem + L.sys_st);
-  float* MUs = reinterpret_cast<float*>(smem + L.mu);
-  float* RHOs = reinterpret_cast<float*>(smem + L.rho);
-  float* coef = reinterpret_cast<float*>(smem + L.coef);
   float* gpart = reinterpret_cast<float*>(smem + L.gpart);
   float2* Ps = reinterpret_cast<float2*>(smem + R.ps4);
   const int nt = blockDim.x, nw = nt >> 5;
@@ -286,8 +274,8 @@ __global__ void __launch_bounds__(256, 2) solve_rows32_kernel(const KernelParams
   auto sync = [] { __syncthreads(); };
   if (EXACT && S > 0) {
     sync();
-    k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st, nt, sync,
-                      reinterpret_cast<float*>(smem + L.xp));
+    moments_tail<UP>(p, ws, W, sc, Kmax, hist, Vs, sys_st, nt,
+                     reinterpret_cast<double*>(smem + L.msh));
   }
   if (St > 0) {
     sync();
@@ -296,122 +284,33 @@ __global__ void __launch_bounds__(256, 2) solve_rows32_kernel(const KernelParams
 }
 
 
-// Approximate-tracker uplink (no CTA-wide tail): one warp per (subcarrier,
-// pair of systems) work item, so the grid is many short warps that the
-// hardware scheduler balances (a CTA per subcarrier at 16 warps / SM leaves
-// a 1.01-wave tail on cfg2's 1200 subcarriers).  Each warp reads its G row
-// straight from the L2-resident workspace.
-template <int NS>
-__global__ void __launch_bounds__(128, NS == 1 ? 5 : NS == 2 ? 4 : 3) solve_rows32_pairs_kernel(const KernelParams p) {
-  constexpr int UP = 32;
-  __shared__ __align__(16) float2 Ps_all[4][NS * UP];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int npairs = (p.S + NS - 1) / NS;
-  const long item = static_cast<long>(blockIdx.x) * (blockDim.x >> 5) + warp;
-  if (item >= p.n_sc * npairs) return;
-  const long lsc = item / npairs;
-  const int base = static_cast<int>(item - lsc * npairs) * NS;
-  WsOffsets W;
-  W.plan(UP, p.S, p.K, false, p.fx);
-  const float2* ws = p.ws + lsc * W.stride;
-  unsigned long long grow[UP];
-#pragma unroll
-  for (int j = 0; j < UP; ++j) {
-    const float2 g = __ldg(ws + W.g + j * UP + lane);
-    grow[j] = f2pack(g.x, -g.y);
-  }
-  const float gdiag = __ldg(ws + W.g + lane * UP + lane).x;
-  rows32_pair<false, true, NS>(p, p.sc_base + lsc, ws + W.mf, base, grow, gdiag, Ps_all[warp],
-                               nullptr, nullptr, nullptr);
-}
-
-// Persistent form of the approximate pairs kernel: warp w walks items w,
-// w + (warps in the grid), ... and copies the NEXT item's G (8 KB) and
-// matched filters into its shared slot with cp.async while the current
-// item's CG runs, so the per-item L2 latency of the G row / b loads (the
-// largest stall of the one-shot kernel) leaves the critical path.
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-__global__ void __launch_bounds__(128, 4) solve_rows32_pairs_pf_kernel(const KernelParams p) {
+// Uplink only (St = 0): one warp per (subcarrier, NS systems) work item, so
+// the grid is many short warps that the hardware scheduler balances (a CTA
+// per subcarrier at 16 warps / SM leaves a 1.01-wave tail on cfg2's 1200
+// subcarriers).  Each warp reads its G row straight from the L2-resident
+// workspace.  Approximate tracker: the outputs leave from rows32_pair.
+// Exact tracker: the (alpha, beta) history stays in the warp's shared slot
+// and the extraction runs in the warp from the subcarrier's row-moment
+// table (moments_coefs / moments_row, cgm_moments.cuh: O(K^2 + K) per
+// lane), then the LLRs.
+template <bool EXACT, int NS>
+__global__ void __launch_bounds__(128, NS == 1 ? 5 : 4) solve_rows32_pairs_kernel(const KernelParams p) {
   constexpr int UP = 32, NW = 4;
-  extern __shared__ __align__(128) unsigned char smem[];
-  // per warp: G [32][32], next-item MF [2][32], current MF [2][32], Ps [2][32]
-  constexpr int SLOT = (UP * UP + 6 * UP) * 8;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float2* Gb = reinterpret_cast<float2*>(smem + warp * SLOT);
-  float2* MFn = Gb + UP * UP;
-  float2* MFc = MFn + 2 * UP;
-  float2* Ps = MFc + 2 * UP;
-  const int S = p.S;
-  const int npairs = (S + 1) >> 1;
-  const long n_items = p.n_sc * npairs;
-  const long stride = static_cast<long>(gridDim.x) * NW;
-  WsOffsets W;
-  W.plan(UP, S, p.K, false, p.fx);
-  auto prefetch = [&](long item) {
-    const long lsc = item / npairs;
-    const int base = static_cast<int>(item - lsc * npairs) * 2;
-    const float2* ws = p.ws + lsc * W.stride;
-#pragma unroll
-    for (int c = 0; c < UP * UP / 2 / 32; ++c)  // 16 B chunks of G, coalesced
-      cp_async16(Gb + 2 * (c * 32 + lane), ws + W.g + 2 * (c * 32 + lane));
-    // the pair's two matched-filter rows (one row when base + 1 == S)
-    if (lane < (base + 1 < S ? 32 : 16)) cp_async16(MFn + 2 * lane, ws + W.mf + base * UP + 2 * lane);
-    cp_async_commit();
-  };
-  long item = static_cast<long>(blockIdx.x) * NW + warp;
-  if (item < n_items) prefetch(item);
-  for (; item < n_items; item += stride) {
-    cp_async_wait_all();
-    __syncwarp();
-    const long lsc = item / npairs;
-    const int base = static_cast<int>(item - lsc * npairs) * 2;
-    unsigned long long grow[UP];
-#pragma unroll
-    for (int j = 0; j < UP; ++j) {
-      const float2 g = Gb[j * UP + lane];  // G[j][u]: row u of G = conj of column u
-      grow[j] = f2pack(g.x, -g.y);
-    }
-    const float gdiag = Gb[lane * UP + lane].x;
-    MFc[lane] = MFn[lane];
-    MFc[UP + lane] = MFn[UP + lane];
-    __syncwarp();  // Gb / MFn consumed: the next item may land there
-    if (item + stride < n_items) prefetch(item + stride);
-    rows32_pair<false, true, 2>(p, p.sc_base + lsc, MFc - base * UP, base, grow, gdiag, Ps,
-                                nullptr, nullptr, nullptr);
-    __syncwarp();
-  }
-}
-
-// Exact-tracker uplink (St = 0), same one-warp-per-(subcarrier, system pair)
-// grid: CG as above with the (alpha, beta) history kept per warp, then the
-// tail of k2_exact_tail done inside the warp -- lanes 0 / 1 run the FP64
-// coefficient recursion of system 0 / 1 (detect.cpp:336-368 on the
-// Chebyshev basis), lane i extracts row i of B = L_K G and L_K from the
-// basis T_1..T_K (coalesced row reads, T Hermitian) and forms mu, nu^2, rho
-// (detect.cpp:375-395) and the LLRs.  Replaces the CTA-per-subcarrier tail
-// whose extraction serialised on one lane group for S = 1 (cfg4).
-__global__ void __launch_bounds__(128, 4) solve_rows32_exact_pairs_kernel(const KernelParams p) {
-  constexpr int UP = 32, NW = 4;
-  __shared__ __align__(16) float2 Ps_all[NW][2 * UP];
-  __shared__ __align__(16) float2 Vs_all[NW][2 * UP];
-  __shared__ float hist_all[NW][2 * kMaxK * 2];
-  __shared__ float coef_all[NW][2][2 * (kMaxK + 2)];
-  __shared__ uint8_t st_all[NW][2];
+  __shared__ __align__(16) float2 Ps_all[NW][NS * UP];
+  __shared__ __align__(16) float2 Vs_all[EXACT ? NW : 1][NS * UP];
+  __shared__ float hist_all[EXACT ? NW : 1][NS * kMaxK * 2];
+  __shared__ double msh_all[EXACT ? NW : 1][kMomScratch];
+  __shared__ uint8_t st_all[EXACT ? NW : 1][NS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = p.S, U = p.U, K = p.K;
-  const int npairs = (S + 1) >> 1;
+  const int npairs = (S + NS - 1) / NS;
   const long item = static_cast<long>(blockIdx.x) * NW + warp;
   if (item >= p.n_sc * npairs) return;
   const long lsc = item / npairs;
-  const int base = static_cast<int>(item - lsc * npairs) * 2;
+  const int base = static_cast<int>(item - lsc * npairs) * NS;
   const long sc = p.sc_base + lsc;
   WsOffsets W;
-  W.plan(UP, S, K, true, p.fx);
+  W.plan(UP, S, K, EXACT);
   const float2* ws = p.ws + lsc * W.stride;
   unsigned long long grow[UP];
 #pragma unroll
@@ -420,252 +319,37 @@ __global__ void __launch_bounds__(128, 4) solve_rows32_exact_pairs_kernel(const 
     grow[j] = f2pack(g.x, -g.y);
   }
   const float gdiag = __ldg(ws + W.g + lane * UP + lane).x;
-  // per-warp arrays indexed by the subcarrier-wide system number (base, base + 1)
-  float* hist = hist_all[warp] - base * K * 2;
-  float2* Vs = Vs_all[warp] - base * UP;
-  uint8_t* sys_st = st_all[warp] - base;
-  rows32_pair<true, true>(p, sc, ws + W.mf, base, grow, gdiag, Ps_all[warp], hist, Vs, sys_st);
-  __syncwarp();
-  if (p.fx) {  // basis_extract_kernel finishes: x_hat and status now, the history for it
-    float2* hw = const_cast<float2*>(ws) + W.t;
-    for (int t = 0; t < 2; ++t) {
+  if constexpr (!EXACT) {
+    rows32_pair<false, true, NS>(p, sc, ws + W.mf, base, grow, gdiag, Ps_all[warp], nullptr,
+                                 nullptr, nullptr);
+  } else {
+    const int w = warp;
+    // per-warp arrays indexed by the subcarrier-wide system number
+    rows32_pair<true, true, NS>(p, sc, ws + W.mf, base, grow, gdiag, Ps_all[warp],
+                                hist_all[w] - base * K * 2, Vs_all[w] - base * UP, st_all[w] - base);
+    __syncwarp();
+    const float2 cdv = ws[W.cd];
+    const double* mom = reinterpret_cast<const double*>(ws + W.t);
+#pragma unroll 1
+    for (int t = 0; t < NS; ++t) {
       const int sy = base + t;
       if (sy >= S) break;
-      const bool ok = st_all[warp][t] == 0;
-      if (lane < U && p.xhat)
-        p.xhat[(sc * S + sy) * static_cast<long>(U) + lane] = ok ? Vs_all[warp][t * UP + lane]
-                                                                : make_float2(0.f, 0.f);
-      if (lane < K)
-        hw[sy * K + lane] = make_float2(hist_all[warp][(t * K + lane) * 2],
-                                        hist_all[warp][(t * K + lane) * 2 + 1]);
-      if (lane == 0 && p.status) p.status[sc * S + sy] = ok ? 0 : 1;
-    }
-    return;
-  }
-  // ---------------- coefficient recursion of both systems, warp-parallel (FP64)
-  const float2 cdv = ws[W.cd];
-  for (int t = 0; t < 2; ++t)
-    if (base + t < S)
-      cheb_coef_warp(hist_all[warp] + t * K * 2, K, cdv.x, cdv.y, p.rho_inv_u, coef_all[warp][t],
-                     coef_all[warp][t] + (kMaxK + 2));
-  __syncwarp();
-  // ---------------- extraction, lane i <-> row i of both systems
-  const float* cl0 = coef_all[warp][0];
-  const float* cb0 = cl0 + (kMaxK + 2);
-  const float* cl1 = coef_all[warp][1];
-  const float* cb1 = cl1 + (kMaxK + 2);
-  const bool has1 = base + 1 < S;
-  const float2* Tw = ws + W.t;
-  const int i = lane;
-  float ib2[2] = {0.f, 0.f}, ibl[2] = {0.f, 0.f}, mu_i[2] = {0.f, 0.f};
-  // the K basis entries of a column pair are loaded together (predicated,
-  // K rounded up to KM) so the L2 / HBM latency is paid once per batch
-  auto extract = [&](auto km_tag) {
-    constexpr int KM = decltype(km_tag)::value;
-#pragma unroll 1
-    for (int j0 = 0; j0 < UP; j0 += 2) {
-      float2 t[2][KM];
-#pragma unroll
-      for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-        for (int m = 1; m <= KM; ++m)
-          t[jj][m - 1] = m <= K ? __ldg(Tw + (m - 1) * UP * UP + (j0 + jj) * UP + i)
-                                : make_float2(0.f, 0.f);
-#pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
-        const int j = j0 + jj;
-        float2 B0 = make_float2(i == j ? cb0[0] : 0.f, 0.f);
-        float2 L0 = make_float2(i == j ? cl0[0] : 0.f, 0.f);
-        float2 B1 = make_float2(i == j ? cb1[0] : 0.f, 0.f);
-        float2 L1 = make_float2(i == j ? cl1[0] : 0.f, 0.f);
-#pragma unroll
-        for (int m = 1; m <= KM; ++m) {
-          if (m > K) break;
-          const float2 tv = cconj(t[jj][m - 1]);  // T_m[i][j] = conj(T_m[j][i])
-          B0.x = fmaf(cb0[m], tv.x, B0.x); B0.y = fmaf(cb0[m], tv.y, B0.y);
-          B1.x = fmaf(cb1[m], tv.x, B1.x); B1.y = fmaf(cb1[m], tv.y, B1.y);
-          if (m < K) {
-            L0.x = fmaf(cl0[m], tv.x, L0.x); L0.y = fmaf(cl0[m], tv.y, L0.y);
-            L1.x = fmaf(cl1[m], tv.x, L1.x); L1.y = fmaf(cl1[m], tv.y, L1.y);
-          }
-        }
-        if (j == i) { mu_i[0] = B0.x; mu_i[1] = B1.x; }
-        else { ib2[0] += cnorm(B0); ib2[1] += cnorm(B1); }
-        ibl[0] += B0.x * L0.x + B0.y * L0.y;  // Re(B_ij conj(L_ij))
-        ibl[1] += B1.x * L1.x + B1.y * L1.y;
+      const MomCoef c = moments_coefs(hist_all[w] + t * K * 2, K, cdv.x, cdv.y, p.rho_inv_u,
+                                      msh_all[w]);
+      float mu, rho;
+      moments_row(msh_all[w], c, K, mom, UP, lane, p.es, p.n0, mu, rho);
+      const bool ok = st_all[w][t] == 0;
+      const float2 xh = ok ? Vs_all[w][t * UP + lane] : make_float2(0.f, 0.f);
+      if (!ok) mu = rho = 0.f;
+      if (lane < U) {
+        const long o = (sc * S + sy) * static_cast<long>(U) + lane;
+        if (p.xhat) p.xhat[o] = xh;
+        if (p.mu) p.mu[o] = mu;
+        if (p.rho) p.rho[o] = rho;
+        if (p.llr) store_llrs_fast(xh, mu, rho, p.bits, p.llr + o * p.bits);
       }
-    }
-  };
-  if (K <= 4) extract(std::integral_constant<int, 4>{});
-  else if (K <= 8) extract(std::integral_constant<int, 8>{});
-  else extract(std::integral_constant<int, kMaxK>{});
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    if (t == 1 && !has1) break;
-    const int sy = base + t;
-    const float nu2 = ib2[t] * p.es + ibl[t] * p.n0;
-    const bool ok = st_all[warp][t] == 0;
-    const float mu = ok ? mu_i[t] : 0.f;
-    const float rr = ok ? (nu2 <= 0.f ? 0.f : mu_i[t] * mu_i[t] / nu2) : 0.f;  // safe_rho
-    const float2 xh = ok ? Vs_all[warp][t * UP + i] : make_float2(0.f, 0.f);
-    if (i < U) {
-      const long o = (sc * S + sy) * static_cast<long>(U) + i;
-      if (p.xhat) p.xhat[o] = xh;
-      if (p.mu) p.mu[o] = mu;
-      if (p.rho) p.rho[o] = rr;
-      if (p.llr) store_llrs_fast(xh, mu, rr, p.bits, p.llr + o * p.bits);
-    }
-    if (p.status && i == 0) p.status[sc * S + sy] = ok ? 0 : 1;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Fully fused approximate-tracker uplink for U = 32 (cfg2): ONE warp per
-// subcarrier does the Gram, the matched filters and all S systems' CG with
-// no workspace round trip and no second kernel.
-//   * H [B][32] and Y [B][S] stream through a two-slot ring of CB-antenna
-//     chunks (cp.async.bulk + one mbarrier per slot, per warp);
-//   * lane u accumulates row u of G = H^H H and its S matched-filter entries
-//     in registers on the packed pipe: per antenna b, with hu = H[b][u],
-//       acc_j += (h_j.x, h_j.y) * hu.x  +  (h_j.y, h_j.x) * (hu.y, -hu.y)
-//     = conj(hu) h_j, H[b][:] and Y[b][:] read as broadcast LDS.128;
-//   * the G row then IS the register-resident row rows32_pair uses, so the
-//     systems run pair by pair straight out of the Gram.
-// The full G row per lane is twice the one-triangle FLOPs, traded for zero
-// synchronisation: the split path's tensor-core channel kernel plus solve
-// kernel spend their time in per-subcarrier pipeline latency, not FLOPs.
-__device__ __forceinline__ unsigned long long f2swap_hl(unsigned long long v) {
-  unsigned long long r;
-  asm("{ .reg .f32 lo, hi; mov.b64 {lo, hi}, %1; mov.b64 %0, {hi, lo}; }" : "=l"(r) : "l"(v));
-  return r;
-}
-
-struct FusedSmem {
-  int bar, ring, slot, hbytes, ybytes, mf, ps, xh, total, cb;
-  __host__ __device__ void plan(int B, int S) {
-    cb = 16;  // antennas per chunk
-    while (cb > 1 && B % cb) cb >>= 1;
-    hbytes = cb * 32 * 8;
-    ybytes = cb * S * 8;
-    slot = (hbytes + ybytes + 15) & ~15;
-    bar = 0;
-    ring = 16;
-    mf = ring + 2 * slot;
-    ps = mf + S * 32 * 8;
-    xh = ps + 2 * 32 * 8;  // exact: per-pair (alpha, beta) history, v rows, status
-    total = xh + (2 * kMaxK * 2 * 4 + 2 * 32 * 8 + 16);
-  }
-};
-
-// EXACT (one vector per subcarrier, p.fx): the same warp then runs the CG
-// with the (alpha, beta) history, writes x_hat / status / history and its G
-// row to the workspace, and basis_kernel<32, true> finishes the tracker.
-template <int MAXS, bool EXACT = false>
-__global__ void __launch_bounds__(32) fused_rows32_approx_kernel(const KernelParams p) {
-  constexpr int UP = 32;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int B = p.B, S = p.S;
-  FusedSmem L;
-  L.plan(B, S);
-  const int CB = L.cb, nch = B / CB;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
-  float2* Ms = reinterpret_cast<float2*>(smem + L.mf);
-  float2* Ps = reinterpret_cast<float2*>(smem + L.ps);
-  const int lane = threadIdx.x;
-  const long sc = p.sc_base + blockIdx.x;
-  const float2* Hg = p.H + sc * static_cast<long>(B) * UP;
-  const float2* Yg = p.Y + sc * static_cast<long>(B) * S;
-  if (lane == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
-  }
-  __syncwarp();
-  auto slot_h = [&](int c) { return reinterpret_cast<float2*>(smem + L.ring + (c & 1) * L.slot); };
-  auto issue = [&](int c) {
-    float2* hs = slot_h(c);
-    fence_proxy_async();
-    mbar_expect_tx(bar + (c & 1), static_cast<uint32_t>(L.hbytes + L.ybytes));
-    bulk_g2s(hs, Hg + static_cast<long>(c) * CB * UP, L.hbytes, bar + (c & 1));
-    bulk_g2s(reinterpret_cast<unsigned char*>(hs) + L.hbytes, Yg + static_cast<long>(c) * CB * S,
-             L.ybytes, bar + (c & 1));
-  };
-  if (lane == 0) {
-    issue(0);
-    if (nch > 1) issue(1);
-  }
-  unsigned long long acc[UP], mf[MAXS];
-#pragma unroll
-  for (int j = 0; j < UP; ++j) acc[j] = 0ull;
-#pragma unroll
-  for (int s = 0; s < MAXS; ++s) mf[s] = 0ull;
-  for (int c = 0; c < nch; ++c) {
-    mbar_wait(bar + (c & 1), static_cast<uint32_t>((c >> 1) & 1));
-    const float2* hs = slot_h(c);
-    const float2* ys = reinterpret_cast<const float2*>(reinterpret_cast<const unsigned char*>(hs) + L.hbytes);
-#pragma unroll 2
-    for (int k = 0; k < CB; ++k) {
-      const float2 hu = hs[k * UP + lane];
-      const unsigned long long ux = f2pack(hu.x, hu.x), uy = f2pack(hu.y, -hu.y);
-      const ulonglong2* row = reinterpret_cast<const ulonglong2*>(hs + k * UP);
-#pragma unroll
-      for (int j2 = 0; j2 < UP / 2; ++j2) {
-        const ulonglong2 h2 = row[j2];
-        ffma2(acc[2 * j2], h2.x, ux);
-        ffma2(acc[2 * j2], f2swap_hl(h2.x), uy);
-        ffma2(acc[2 * j2 + 1], h2.y, ux);
-        ffma2(acc[2 * j2 + 1], f2swap_hl(h2.y), uy);
-      }
-      const unsigned long long* yr = reinterpret_cast<const unsigned long long*>(ys + k * S);
-#pragma unroll
-      for (int s = 0; s < MAXS; ++s) {
-        if (s < S) {
-          const unsigned long long y = yr[s];
-          ffma2(mf[s], y, ux);
-          ffma2(mf[s], f2swap_hl(y), uy);
-        }
-      }
-    }
-    __syncwarp();  // every lane done with this slot
-    if (lane == 0 && c + 2 < nch) issue(c + 2);
-  }
-  // matched filters to shared memory ([sys][u], the layout rows32_pair reads)
-#pragma unroll
-  for (int s = 0; s < MAXS; ++s)
-    if (s < S) Ms[s * UP + lane] = f2unpack(mf[s]);
-  float gdiag = 0.f;
-#pragma unroll
-  for (int j = 0; j < UP; ++j)
-    if (j == lane) gdiag = f2unpack(acc[j]).x;
-  __syncwarp();
-  if constexpr (!EXACT) {
-    for (int base = 0; base < S; base += 2)
-      rows32_pair<false, true>(p, sc, Ms, base, acc, gdiag, Ps, nullptr, nullptr, nullptr);
-  } else {
-    const int K = p.K;
-    WsOffsets W;
-    W.plan(UP, S, K, true, p.fx);
-    float2* ws = p.ws + static_cast<long>(blockIdx.x) * W.stride;
-#pragma unroll
-    for (int j = 0; j < UP; ++j) ws[W.g + lane * UP + j] = f2unpack(acc[j]);  // row u of G
-    float* histw = reinterpret_cast<float*>(smem + L.xh);
-    float2* Vsw = reinterpret_cast<float2*>(histw + 2 * kMaxK * 2);
-    uint8_t* stw = reinterpret_cast<uint8_t*>(Vsw + 2 * UP);
-    for (int base = 0; base < S; base += 2) {
-      rows32_pair<true, true>(p, sc, Ms, base, acc, gdiag, Ps, histw - base * K * 2, Vsw - base * UP,
-                              stw - base);
-      __syncwarp();
-      for (int t = 0; t < 2; ++t) {
-        const int sy = base + t;
-        if (sy >= S) break;
-        const bool ok = stw[t] == 0;
-        if (p.xhat)
-          p.xhat[(sc * S + sy) * static_cast<long>(UP) + lane] = ok ? Vsw[t * UP + lane]
-                                                                    : make_float2(0.f, 0.f);
-        if (lane < K) ws[W.t + sy * K + lane] = make_float2(histw[(t * K + lane) * 2],
-                                                           histw[(t * K + lane) * 2 + 1]);
-        if (lane == 0 && p.status) p.status[sc * S + sy] = ok ? 0 : 1;
-      }
-      __syncwarp();
+      if (p.status && lane == 0) p.status[sc * S + sy] = ok ? 0 : 1;
+      __syncwarp();  // msh is reused by the next system
     }
   }
 }

@@ -3,9 +3,8 @@
 //   K1 channel_kernel  (one CTA per subcarrier, persistent grid-stride)
 //      TMA-stage H and Y, form G = H^H H (lower 4x4 tiles + mirror) and the
 //      matched filter H^H Y in register tiles with shuffle-reduced split-K,
-//      and for the exact tracker the Chebyshev basis T_1..T_K of
-//      Ahat = (A - cI)/d (K-1 Hermitian products).  Writes them to a
-//      workspace sized to stay L2-resident for K2.
+//      Writes them to a workspace sized to stay L2-resident for the next
+//      kernels (the exact tracker's row moments, cgm_moments.cuh, and K2).
 //        replaces gram_regularized (linalg.cpp:59-101), matvec_adjoint
 //        (linalg.cpp:116-126) and the U^3 part of ExactSinrTracker::step
 //        (detect.cpp:336-368, see cgm_kernels.cuh for the basis argument)
@@ -24,33 +23,18 @@
 
 #include <type_traits>
 
-#include "cgm_kernels.cuh"
+#include "cgm_moments.cuh"
 
 namespace cgm {
 
-// workspace layout per subcarrier (float2 units)
-struct WsOffsets {
-  int g, mf, cd, t, stride;
-  // fx: the exact tracker's basis is not stored (basis_extract_kernel builds
-  // it on chip); t then holds each system's (alpha, beta) history, K float2
-  __host__ __device__ void plan(int UP, int S, int K, bool exact, int fx = 0) {
-    g = 0;
-    mf = UP * UP;
-    cd = mf + S * UP;
-    t = cd + 2;
-    stride = t + (exact ? (fx ? S * K : K * UP * UP) : 0);
-    stride = (stride + 1) & ~1;
-  }
-};
-
 // K1 shared memory: two TMA stages of {H [B][UP], Y [B][S]} (the next
 // subcarrier is prefetched while the current one is contracted), the Gram
-// matrix, and (exact) T_1 / T_m of the basis product chain.
+// matrix.
 template <int UP>
 struct K1Smem {
-  int bar, slot, hs, ys, gs, tb, misc, total;
+  int bar, slot, hs, ys, gs, total;
   __host__ __device__ static int align(int x) { return (x + 127) & ~127; }
-  __host__ __device__ void plan(int B, int S, bool exact, int nstage) {
+  __host__ __device__ void plan(int B, int S, int nstage) {
     const int Sp = (S + 1) & ~1;  // Y rows padded to an even length (16B aligned)
     int o = 0;
     bar = o; o = align(o + 32);
@@ -59,8 +43,6 @@ struct K1Smem {
     slot = align(ys + B * Sp * 8 + 64);  // +64: last-row 4-wide tile reads
     o = align(o + nstage * slot);
     gs = o; o = align(o + UP * UP * 8);
-    tb = o; o = align(o + (exact ? 2 * UP * UP * 8 : 0));
-    misc = o; o = align(o + 16);
     lut = o; o = align(o + 2 * 512);  // per-tile (ib, jb), <= 512 tiles
     total = o;
   }
@@ -101,66 +83,6 @@ __device__ __forceinline__ void k1_issue(const KernelParams& p, float2* Hs, floa
   if (p.S > 0 && ybytes) bulk_g2s(Ys, p.Y + sc * static_cast<long>(p.B) * p.S, ybytes, bar);
 }
 
-// Exact tracker, per subcarrier (detect.cpp:336-368 restated on a Chebyshev
-// basis): centre/half-width (c, d) of A = G + rho^-1 I and T_1..T_K of
-// Ahat = (A - cI)/d into the workspace, from G in shared memory.  Run by
-// threads [0, nt) (warps 0..nt/32-1); `sync` is a barrier over exactly those.
-template <int UP, class Sync>
-__device__ __forceinline__ void exact_basis(const KernelParams& p, const WsOffsets& W, float2* ws,
-                                            const float2* Gs, float2* T1, float2* Tm, float* misc,
-                                            int nt, Sync&& sync) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n_gram = (UP / 4) * (UP / 4 + 1) / 2;
-  const int K = p.K;
-  if (warp == 0) {
-    const float2 cd = cheb_interval<UP>(Gs, p.rho_inv_u, Tm, lane);  // Tm: scratch here
-    if (lane == 0) {
-      misc[0] = cd.x;
-      misc[1] = cd.y;
-      ws[W.cd] = cd;
-    }
-  }
-  sync();
-  const float cc = misc[0], invd = 1.f / misc[1];
-  float2* Tw = ws + W.t;
-  for (int e = tid; e < UP * UP; e += nt) {  // T_1 = (A - cI)/d
-    float2 a = Gs[e];
-    if (e / UP == e % UP) a.x += p.rho_inv_u - cc;
-    a = cscale(invd, a);
-    T1[e] = a;
-    Tm[e] = a;
-    Tw[e] = a;
-  }
-  sync();
-  // T_{m+1} = 2 T_1 T_m - T_{m-1} (lower tiles + mirror; T_{m-1} via L2)
-  for (int m = 1; m < K; ++m) {
-    const float2* Tp = m >= 2 ? Tw + (m - 2) * UP * UP : nullptr;
-    float2* Tn = Tw + m * UP * UP;
-    tile_pass_nw(nt / 32, n_gram, 0, 1, T1, UP, Tm, UP, T1, 1, 1, UP,
-                 [&](int, int tib, int tjb, float2 (&a4)[4][4]) {
-#pragma unroll
-                   for (int r = 0; r < 4; ++r)
-#pragma unroll
-                     for (int c = 0; c < 4; ++c) {
-                       const int ii = tib * 4 + r, j = tjb * 4 + c;
-                       if (j > ii) continue;
-                       const float2 prev =
-                           Tp ? Tp[ii * UP + j] : make_float2(ii == j ? 1.f : 0.f, 0.f);
-                       float2 val = make_float2(2.f * a4[r][c].x - prev.x,
-                                                2.f * a4[r][c].y - prev.y);
-                       if (ii == j) val.y = 0.f;
-                       Tn[ii * UP + j] = val;
-                       if (ii != j) Tn[j * UP + ii] = cconj(val);
-                     }
-                 });
-    sync();
-    if (m + 1 < K) {  // T_m <- T_{m+1} for the next product
-      for (int e = tid; e < UP * UP; e += nt) Tm[e] = Tn[e];
-      sync();
-    }
-  }
-}
-
 // MINB: CTAs per SM the register budget is sized for; PIPE: software-
 // pipelined tile loop (operands of row k+1 in flight) or the plain one.
 template <int UP, bool EXACT, int MINB = 2, bool PIPE = true>
@@ -168,14 +90,11 @@ __global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p
   extern __shared__ __align__(128) unsigned char smem[];
   const int spl = p.k1_spl, nstage = p.k1_pair;
   K1Smem<UP> L;
-  L.plan(p.B, p.S, EXACT && !p.basis_ext, nstage);  // no basis buffers when basis_kernel runs
+  L.plan(p.B, p.S, nstage);
   WsOffsets W;
-  W.plan(UP, p.S, p.K, EXACT, p.fx);
+  W.plan(UP, p.S, p.K, EXACT);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar);
   float2* Gs = reinterpret_cast<float2*>(smem + L.gs);
-  float2* T1 = reinterpret_cast<float2*>(smem + L.tb);
-  float2* Tm = T1 + UP * UP;
-  float* misc = reinterpret_cast<float*>(smem + L.misc);
   const int nt = blockDim.x;
   const int tid = threadIdx.x;
   const int B = p.B, S = p.S, U = p.U;
@@ -312,7 +231,7 @@ __global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[r][c] = make_float2(0.f, 0.f);
-      if (active && !(p.debug & 4)) {
+      if (active) {
         const float2* Z = is_gram ? Hs : Ys;
         const int ldz = is_gram ? UP : Sp;
         if (PIPE)
@@ -321,7 +240,7 @@ __global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p
           tile4x4<true>(acc, Hs, UP, ib * 4, Z, ldz, 1, jb * 4, 1 << 30, k0, k1);
       }
       __syncthreads();  // (A) every k loop done: the stage may hold partials
-      if (!(p.debug & 8)) {
+      {
         // partials parked entry-major / tile-minor ([part][16][n_tiles]) so a
         // warp's stores and the reduction's loads are contiguous (no conflicts)
         float2* pb = Hs;
@@ -356,7 +275,6 @@ __global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p
       float4* dst = reinterpret_cast<float4*>(ws + W.g);
       for (int e = tid; e < UP * UP / 2; e += nt) dst[e] = src[e];
     }
-    if (EXACT && S > 0 && !p.basis_ext) exact_basis<UP>(p, W, ws, Gs, T1, Tm, misc, nt, [] { __syncthreads(); });
     __syncthreads();  // Gs is rewritten by the next subcarrier
   }
 }
@@ -372,7 +290,7 @@ struct K2Geo {
 
 template <int UP>
 struct K2Smem {
-  int gs, ps, vs, qs, hist, sys_st, mu, rho, coef, gpart, xp, total;
+  int gs, ps, vs, qs, hist, msh, sys_st, gpart, total;
   __host__ __device__ static int align(int x) { return (x + 127) & ~127; }
   __host__ __device__ void plan(int B, int S, int St, int K, bool exact) {
     const int nsys = S + St;
@@ -382,146 +300,17 @@ struct K2Smem {
     vs = o; o = align(o + nsys * UP * 8);
     qs = o; o = align(o + St * B * 8);
     hist = o; o = align(o + (exact ? S * K * 2 * 4 : 0));
+    msh = o; o = align(o + (exact ? 8 * kMomScratch * 8 : 0));  // per-warp extraction scratch
     sys_st = o; o = align(o + nsys);
-    mu = o; o = align(o + (exact ? S * UP * 4 : 0));
-    rho = o; o = align(o + (exact ? S * UP * 4 : 0));
-    coef = o; o = align(o + (exact ? S * 2 * (K + 2) * 4 : 0));
     gpart = o; o = align(o + ((B + 31) / 32) * (St > 0 ? St : 1) * 4);
-    xp = o; o = align(o + (exact ? 3 * 8 * UP * 4 : 0));  // S = 1 extraction partials
     total = o;
   }
 };
 
 // ---------------------------------------------------------- solve tails
-// Shared by solve_kernel and solve32_kernel, after the CG: Vs[sys][u] holds
-// v, sys_st the breakdown flags, hist the (alpha, beta) history.
-// Exact tracker (detect.cpp:330-395): FP64 coefficient recursion per system,
-// extraction of mu / nu^2 from the Chebyshev basis, then all outputs.
-template <int UP, class Sync>
-__device__ __forceinline__ void k2_exact_tail(const KernelParams& p, const float2* ws,
-                                              const WsOffsets& W, long sc, int Kmax,
-                                              const float* hist, float* coef, float* MUs,
-                                              float* RHOs, const float2* Vs,
-                                              const uint8_t* sys_st, int nt, Sync&& sync,
-                                              float* xp = nullptr) {
-  const int tid = threadIdx.x;
-  const int S = p.S, U = p.U;
-    const int K = p.K;
-    const float2 cdv = ws[W.cd];
-    const double cc = cdv.x, dd = cdv.y;
-    // three-term recursion (detect.cpp:336-368) on the Chebyshev
-    // coefficients, FP64, one warp per system (cheb_coef_warp)
-    for (int s = tid >> 5; s < S; s += nt >> 5) {
-      float* cl = coef + s * 2 * (K + 2);
-      cheb_coef_warp(hist + s * Kmax * 2, K, cc, dd, p.rho_inv_u, cl, cl + (K + 2));
-    }
-    sync();
-    // extraction (detect.cpp:375-395): thread <-> (row i, pair of systems);
-    // each T_m(i, j) is read once (L1/L2) and used for both systems
-    const float2* Tw = ws + W.t;
-    const int ngrp = nt / UP;
-    const int i = tid % UP, g = tid / UP;
-    // one vector per subcarrier (cfg4): the groups split the columns j of the
-    // single system instead of idling at the barrier, partial sums in xp
-    const bool jsplit = xp != nullptr && S == 1 && ngrp > 1 && ngrp <= 8;
-    if (g < ngrp) {
-      for (int s0 = jsplit ? 0 : g; s0 < S; s0 += jsplit ? S : 2 * ngrp) {
-        const int s1 = jsplit ? S : s0 + ngrp;
-        const int jb = jsplit ? g * (UP / ngrp) : 0, je = jsplit ? jb + UP / ngrp : UP;
-        const bool has1 = s1 < S;
-        const float* cl0 = coef + s0 * 2 * (K + 2);
-        const float* cb0 = cl0 + (K + 2);
-        const float* cl1 = coef + (has1 ? s1 : s0) * 2 * (K + 2);
-        const float* cb1 = cl1 + (K + 2);
-        float ib2[2] = {0.f, 0.f}, ibl[2] = {0.f, 0.f}, mu_i[2] = {0.f, 0.f};
-        // the K basis entries of a column pair are loaded together
-        // (predicated, K rounded up to KM): one L2 latency per batch
-        auto extract = [&](auto km_tag) {
-          constexpr int KM = decltype(km_tag)::value;
-#pragma unroll 1
-          for (int j0 = jb; j0 < je; j0 += 2) {
-            float2 tv[2][KM];
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-              for (int m = 1; m <= KM; ++m)
-                tv[jj][m - 1] = m <= K ? __ldg(Tw + (m - 1) * UP * UP + (j0 + jj) * UP + i)
-                                       : make_float2(0.f, 0.f);
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj) {
-              const int j = j0 + jj;
-              float2 B0 = make_float2(i == j ? cb0[0] : 0.f, 0.f);
-              float2 L0 = make_float2(i == j ? cl0[0] : 0.f, 0.f);
-              float2 B1 = make_float2(i == j ? cb1[0] : 0.f, 0.f);
-              float2 L1 = make_float2(i == j ? cl1[0] : 0.f, 0.f);
-#pragma unroll
-              for (int m = 1; m <= KM; ++m) {
-                if (m > K) break;
-                const float2 t = cconj(tv[jj][m - 1]);  // T_m[i][j]
-                B0.x = fmaf(cb0[m], t.x, B0.x); B0.y = fmaf(cb0[m], t.y, B0.y);
-                B1.x = fmaf(cb1[m], t.x, B1.x); B1.y = fmaf(cb1[m], t.y, B1.y);
-                if (m < K) {
-                  L0.x = fmaf(cl0[m], t.x, L0.x); L0.y = fmaf(cl0[m], t.y, L0.y);
-                  L1.x = fmaf(cl1[m], t.x, L1.x); L1.y = fmaf(cl1[m], t.y, L1.y);
-                }
-              }
-              if (j == i) { mu_i[0] = B0.x; mu_i[1] = B1.x; }
-              else { ib2[0] += cnorm(B0); ib2[1] += cnorm(B1); }
-              ibl[0] += B0.x * L0.x + B0.y * L0.y;  // Re(B_ij conj(L_ij))
-              ibl[1] += B1.x * L1.x + B1.y * L1.y;
-            }
-          }
-        };
-        if (K <= 4) extract(std::integral_constant<int, 4>{});
-        else if (K <= 8) extract(std::integral_constant<int, 8>{});
-        else extract(std::integral_constant<int, kMaxK>{});
-        if (jsplit) {
-          xp[(g * 3 + 0) * UP + i] = ib2[0];
-          xp[(g * 3 + 1) * UP + i] = ibl[0];
-          xp[(g * 3 + 2) * UP + i] = mu_i[0];
-          continue;
-        }
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (t == 1 && !has1) break;
-          const int s = t ? s1 : s0;
-          const float nu2 = ib2[t] * p.es + ibl[t] * p.n0;
-          MUs[s * UP + i] = mu_i[t];
-          RHOs[s * UP + i] = nu2 <= 0.f ? 0.f : mu_i[t] * mu_i[t] / nu2;  // safe_rho
-        }
-      }
-    }
-    if (jsplit) {
-      sync();
-      if (g == 0) {  // fixed-order sum of the column parts
-        float b2 = 0.f, bl = 0.f, mu = 0.f;
-        for (int q = 0; q < ngrp; ++q) {
-          b2 += xp[(q * 3 + 0) * UP + i];
-          bl += xp[(q * 3 + 1) * UP + i];
-          mu += xp[(q * 3 + 2) * UP + i];
-        }
-        const float nu2 = b2 * p.es + bl * p.n0;
-        MUs[i] = mu;
-        RHOs[i] = nu2 <= 0.f ? 0.f : mu * mu / nu2;  // safe_rho
-      }
-    }
-    sync();
-    for (int e = tid; e < S * U; e += nt) {
-      const int s = e / U, u = e - s * U;
-      const long o = (sc * S + s) * static_cast<long>(U) + u;
-      const bool ok = sys_st[s] == 0;
-      const float2 xh = ok ? Vs[s * UP + u] : make_float2(0.f, 0.f);
-      const float m = ok ? MUs[s * UP + u] : 0.f;
-      const float rr = ok ? RHOs[s * UP + u] : 0.f;
-      if (p.xhat) p.xhat[o] = xh;
-      if (p.mu) p.mu[o] = m;
-      if (p.rho) p.rho[o] = rr;
-      if (p.llr) store_llrs_fast(xh, m, rr, p.bits, p.llr + o * p.bits);
-    }
-    if (p.status)
-      for (int s = tid; s < S; s += nt) p.status[sc * S + s] = sys_st[s];
-  }
-
+// Shared by the CTA-per-subcarrier solve kernels, after the CG: Vs[sys][u]
+// holds v, sys_st the breakdown flags (the exact tracker's tail is
+// moments_tail, cgm_moments.cuh).
 // Precoder (precode.cpp:22-71): q = H_d^H v, gain = ||q||, s = q / gain.
 template <int UP, class Sync>
 __device__ __forceinline__ void k2_precode_tail(const KernelParams& p, long sc, const float2* Vs,
@@ -625,7 +414,7 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
   K2Smem<UP> L;
   L.plan(B, S, St, Kmax, EXACT);
   WsOffsets W;
-  W.plan(UP, S, p.K, EXACT, p.fx);
+  W.plan(UP, S, p.K, EXACT);
   // G (and the matched filters) from the prefetched shared-memory copy of
   // the workspace when the persistent kernel staged one
   const float2* Gs = pre ? pre + W.g : reinterpret_cast<float2*>(smem + L.gs);
@@ -634,9 +423,6 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
   float2* Qs = reinterpret_cast<float2*>(smem + L.qs);
   float* hist = reinterpret_cast<float*>(smem + L.hist);
   uint8_t* sys_st = reinterpret_cast<uint8_t*>(smem + L.sys_st);
-  float* MUs = reinterpret_cast<float*>(smem + L.mu);
-  float* RHOs = reinterpret_cast<float*>(smem + L.rho);
-  float* coef = reinterpret_cast<float*>(smem + L.coef);
   float* gpart = reinterpret_cast<float*>(smem + L.gpart);
   const int nw = nt >> 5;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -664,7 +450,7 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
       for (int j = 0; j < UP; ++j) grow[j] = cconj(Gs[j * UP + gl]);  // G[u][j]
     }
     // warp-uniform trip count (the shuffles below use the full mask)
-    for (int wbase = warp * GPW * NS; wbase < ((p.debug & 16) ? 0 : nsys); wbase += n_slots) {
+    for (int wbase = warp * GPW * NS; wbase < nsys; wbase += n_slots) {
       const int base = wbase + grp * NS;
       int sys[NS];
       bool live[NS], down[NS];
@@ -712,7 +498,7 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
         for (int m = 0; m < RU; ++m) f0[s][m] = f1[s][m] = f2[s][m] = 0.f;
       }
       __syncwarp();
-      for (int k = 1; k <= ((p.debug & 32) ? 0 : Kmax); ++k) {
+      for (int k = 1; k <= Kmax; ++k) {
         // e = (G + reg I) p: G read as column (conflict-free), p broadcast;
         // two partial sums per component shorten the FMA chains
         float2 e[NS][RU], e2[NS][RU];
@@ -867,7 +653,7 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
           if (p.xhat) p.xhat[o] = xh;
           if (p.mu) p.mu[o] = mu_u;
           if (p.rho) p.rho[o] = rho_u;
-          if (p.llr && !(p.debug & 64)) store_llrs_fast(xh, mu_u, rho_u, p.bits, p.llr + o * p.bits);
+          if (p.llr) store_llrs_fast(xh, mu_u, rho_u, p.bits, p.llr + o * p.bits);
           if (p.status && gl == 0) p.status[sc * S + sys[s]] = ok ? 0 : 1;
         }
       }
@@ -875,24 +661,10 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
   }
 
   // ------------------------------------------ exact tracker extraction
-  if (EXACT && S > 0 && p.fx) {  // basis_extract_kernel finishes: x_hat, status, history
+  if (EXACT && S > 0) {
     sync();
-    float2* hw = const_cast<float2*>(ws) + W.t;
-    for (int e = tid; e < S * U; e += nt) {
-      const int s = e / U, u = e - s * U;
-      if (p.xhat) p.xhat[(sc * S + s) * static_cast<long>(U) + u] =
-          sys_st[s] == 0 ? Vs[s * UP + u] : make_float2(0.f, 0.f);
-    }
-    for (int e = tid; e < S * p.K; e += nt) {
-      const int s = e / p.K, k = e - s * p.K;
-      hw[e] = make_float2(hist[(s * Kmax + k) * 2], hist[(s * Kmax + k) * 2 + 1]);
-    }
-    if (p.status)
-      for (int s = tid; s < S; s += nt) p.status[sc * S + s] = sys_st[s];
-  } else if (EXACT && S > 0) {
-    sync();
-    k2_exact_tail<UP>(p, ws, W, sc, Kmax, hist, coef, MUs, RHOs, Vs, sys_st, nt, sync,
-                      reinterpret_cast<float*>(smem + L.xp));
+    moments_tail<UP>(p, ws, W, sc, Kmax, hist, Vs, sys_st, nt,
+                     reinterpret_cast<double*>(smem + L.msh));
   }
   // ------------------------------------------------ precode q = H_d^H v
   if (St > 0) {
@@ -919,7 +691,7 @@ template <int UP, bool EXACT, int MINB = 3>
 __global__ void __launch_bounds__(256, MINB) solve_kernel_pf(const KernelParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   WsOffsets W;
-  W.plan(UP, p.S, p.K, EXACT, p.fx);
+  W.plan(UP, p.S, p.K, EXACT);
   const int pb = k2_pre_bytes(UP, p.S);
   const uint32_t bytes = static_cast<uint32_t>(W.cd * 8);  // G + MF
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);

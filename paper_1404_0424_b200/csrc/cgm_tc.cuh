@@ -24,8 +24,7 @@
 //                free the piece slot / publish the accumulator
 //   warps 0..NWK-1  workers: split staging -> bf16 pieces (double-buffered
 //                slots), then the epilogue of the previous subcarrier
-//                (tcgen05.ld, G with an exact Hermitian mirror, MF, and for
-//                the exact tracker the Chebyshev basis of cgm_split.cuh)
+//                (tcgen05.ld, G with an exact Hermitian mirror, MF)
 // TMEM: 2 subcarrier buffers x {p0p0, corrections} x 128 columns = 512.
 //
 // Replaces gram_regularized (linalg.cpp:59-101) and matvec_adjoint
@@ -176,11 +175,11 @@ __device__ __forceinline__ void split8(const float (&x)[8], uint4& o0, uint4& o1
 
 // Shared-memory plan (offsets from a 1024-aligned base).
 struct Smem {
-  int pieces, stage, stage_bytes, nstg, gp, gs, tb, bar, total;
+  int pieces, stage, stage_bytes, nstg, gp, bar, total;
   __host__ __device__ static int align(int x, int a) { return (x + a - 1) / a * a; }
   // ring = piece slots and TMEM subcarrier buffers (2: one CTA per SM
   // double-buffers; 1: half the shared memory, two CTAs per SM)
-  __host__ __device__ void plan(int S, bool exact, int nstage, int ring = NPS) {
+  __host__ __device__ void plan(int S, int nstage, int ring = NPS) {
     int o = 0;
     pieces = o;
     o += ring * PSLOT;
@@ -190,10 +189,6 @@ struct Smem {
     o += nstg * stage_bytes;
     gp = o;
     o = align(o + UPT * GPS * 8, 128);
-    gs = o;
-    o = align(o + (exact ? UPT * UPT * 8 : 0), 128);
-    tb = o;
-    o = align(o + (exact ? 2 * UPT * UPT * 8 : 0), 128);
     bar = o;
     o += 16 * 8 + 16 + 16;  // 16 mbarriers, TMEM base, misc
     total = align(o, 128) + 1024;  // + alignment slack of the dynamic base
@@ -208,17 +203,11 @@ __host__ __device__ inline bool supported(int U, int B, int S, int use_tma) {
 
 }  // namespace tc
 
-// Event clocks for the pipeline study (tools/microbench/tc_bench.cu):
-// trace[(cta * 16 + subcarrier) * 32 + event], first 16 subcarriers of a CTA.
-__device__ __forceinline__ void tc_trace(const KernelParams& p, long i, int ev) {
-  if (p.trace && i < 16) p.trace[(blockIdx.x * 16 + i) * 32 + ev] = clock64();
-}
-
 // Warp roles.  NSP > 0 (specialised): [0, NEP) epilogue, [NEP, NEP+NSP)
 // split.  NSP == 0 (unified): warps [0, NEP) split subcarrier i, then run
 // the epilogue of subcarrier i-1 while the tensor core works on i.  Then
 // the TMA producer warp and the MMA warp.  k1_pair carries the staging depth.
-template <bool EXACT, int NEP, int NSP, int RING = 2>
+template <int NEP, int NSP, int RING = 2>
 __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_kernel(const KernelParams p) {
   using namespace tc;
   constexpr int UP = UPT;
@@ -231,9 +220,9 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   tc::Smem L;
-  L.plan(p.S, EXACT, p.k1_pair, RING);
+  L.plan(p.S, p.k1_pair, RING);
   WsOffsets W;
-  W.plan(UP, p.S, p.K, EXACT, p.fx);
+  W.plan(UP, p.S, p.K, p.exact != 0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int S = p.S, B = p.B, nkb = B / KB, nstg = L.nstg;
   const int ny = S > 0 ? ((2 * S + 7) & ~7) : 0;  // Y columns fed to the MMA (zero padded)
@@ -249,7 +238,6 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
   uint64_t* acc_full = pcs_empty + NPS;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
-  float* misc = reinterpret_cast<float*>(bars + 16) + 4;
 
   constexpr uint32_t TCOLS = RING == 2 ? TMEM_COLS : 256;
   if (warp == 0) tmem_alloc(tmem_slot, TCOLS);
@@ -284,15 +272,13 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
     constexpr int HPT = KB * 8 / NTS;  // H chunks per thread
     static_assert(KB * 8 % NTS == 0, "H chunks must divide evenly");
     for (int kb = 0; kb < nkb; ++kb, ++pq) {
-      if (!(p.debug & 1024)) mbar_wait(stg_full + stg_s, sph);
-      if (st == 0) tc_trace(p, i, kb == 0 ? 2 : 4);
+      mbar_wait(stg_full + stg_s, sph);
       const int ps = static_cast<int>(pq % RING);
       if (pq >= RING) mbar_wait(pcs_empty + ps, static_cast<uint32_t>(((pq / RING) - 1) & 1));
-      if (st == 0) tc_trace(p, i, kb == 0 ? 13 : 14);
       const float* Hst = reinterpret_cast<const float*>(smem + L.stage + stg_s * L.stage_bytes);
       const float* Yst = Hst + KB * UP * 2;
       unsigned char* slot = smem + L.pieces + ps * PSLOT;
-      if (!(p.debug & 256)) {
+      {
         // H: 64 rows x 8 chunks, Y: 64 rows x nyc chunks; a thread's chunks
         // are loaded together (latency overlap), then split
         float hx[HPT][8];
@@ -362,9 +348,8 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(pcs_full + ps);
-        if (!(p.debug & 1024)) mbar_arrive(stg_empty + stg_s);
+        mbar_arrive(stg_empty + stg_s);
       }
-      if (st == 0) tc_trace(p, i, kb == 0 ? 3 : 5);
       if (++stg_s == nstg) {
         stg_s = 0;
         sph ^= 1u;
@@ -375,9 +360,6 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
   // ------------------------------------------------ epilogue of one subcarrier
   auto epilogue_sc = [&](long e) {
     float* Gpf = reinterpret_cast<float*>(smem + L.gp);  // [UP][GPS] float2 as floats
-    float2* Gs = reinterpret_cast<float2*>(smem + L.gs);
-    float2* T1 = reinterpret_cast<float2*>(smem + L.tb);
-    float2* Tm = T1 + UP * UP;
     // TMEM column split of the loads: lanes 0-15 read columns [0, hoff),
     // lanes 16-31 [hoff, 2 hoff) of the same accumulator rows
     const int hoff = (N / 2 + 7) & ~7;
@@ -391,7 +373,6 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
     const int ab = static_cast<int>(e % RING);
     mbar_wait(acc_full + ab, static_cast<uint32_t>((e / RING) & 1));
     tc_fence_after();
-    if (tid == 0) tc_trace(p, e, 9);
     const long lsc = blockIdx.x + e * gridDim.x;
     float2* ws = p.ws + lsc * W.stride;
     float* mff = reinterpret_cast<float*>(ws + W.mf);
@@ -404,7 +385,7 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
 #pragma unroll
       for (int c = 0; c < CB; ++c) {
         const int c0 = c_first + (c00 + c) * c_step;
-        if (c0 < hoff && !(p.debug & 512)) {
+        if (c0 < hoff) {
           tmem_ld8_x2(tq + c0, hoff, vb[c]);
           tmem_ld8_x2(tq + 128 + c0, hoff, vs[c]);
         }
@@ -414,12 +395,11 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty + ab);  // accumulators may be overwritten
-        if (tid == 0) tc_trace(p, e, 10);
       }
 #pragma unroll
       for (int c = 0; c < CB; ++c) {
         const int c0 = c_first + (c00 + c) * c_step;
-        if (c0 >= hoff || (p.debug & 512)) continue;
+        if (c0 >= hoff) continue;
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const float a = __fadd_rn(__uint_as_float(vb[c][2 * t]), __uint_as_float(vs[c][2 * t]));
@@ -436,8 +416,6 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
         }
       }
     }
-    if (tid == 0) tc_trace(p, e, 18);
-    if (p.debug & 4096) return;
     named_sync(1, NTE);  // G rows complete in smem
     {
       // G = lower triangle + conjugate mirror, real diagonal (exactly Hermitian)
@@ -449,18 +427,13 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
         if (c > r) g.y = -g.y;
         if (c == r) g.y = 0.f;
         Gw[x] = g;
-        if (EXACT) Gs[x] = g;
       }
     }
-    named_sync(1, NTE);
-    if (tid == 0) tc_trace(p, e, 11);
-    if (EXACT && S > 0 && !p.basis_ext) exact_basis<UP>(p, W, ws, Gs, T1, Tm, misc, NTE, [] { named_sync(1, NTE); });
-    if (tid == 0) tc_trace(p, e, 12);
   };
 
   if (warp == WPROD) {
     // ------------------------------------------------------ TMA producer
-    if (lane == 0 && !(p.debug & 1024)) {
+    if (lane == 0) {
       const uint32_t hb = KB * UP * 8u, yb = KB * static_cast<uint32_t>(S) * 8u;
       long q = 0;
       for (long i = 0; i < n_local; ++i) {
@@ -475,7 +448,6 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
           mbar_expect_tx(stg_full + s, hb + yb);
           bulk_g2s(dst, p.H + row0 * UP, hb, stg_full + s);
           if (S > 0) bulk_g2s(dst + hb, p.Y + row0 * S, yb, stg_full + s);
-          tc_trace(p, i, kb == 0 ? 0 : 1);
         }
       }
     }
@@ -494,10 +466,9 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
         const int ps = static_cast<int>(mq % RING);
         mbar_wait(pcs_full + ps, static_cast<uint32_t>((mq / RING) & 1));
         tc_fence_after();
-        if (lane == 0) tc_trace(p, i, kb == 0 ? 6 : 7);
         // descriptor start addresses advance by (byte offset >> 4)
         const uint64_t dslot = dbase + static_cast<uint64_t>((ps * PSLOT) >> 4);
-        if (!(p.debug & 128)) {
+        {
 #pragma unroll
           for (int pass = 0; pass < 6; ++pass) {
             // (A piece, B piece) of the six products, p0 p0 first
@@ -518,7 +489,6 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
       }
       tc_commit_elect(acc_full + ab);  // accumulators of subcarrier i complete
       __syncwarp();
-      if (lane == 0) tc_trace(p, i, 8);
     }
   } else if (UNIFIED) {
     // ------------------------------------------------------ unified workers

@@ -34,10 +34,10 @@ def run_uplink(ctx, cfg, H, Y):
     return {k: to_np(v) for k, v in out.items()}
 
 
-@pytest.fixture(params=["auto", "generic"])
+@pytest.fixture(params=["auto", "ffma_channel+split_small+lane_solve"])
 def policy_ctx(gpu_ctx, request):
-    """Both kernels: the warp-specialised pipeline (auto, U = 32 shapes) and
-    the generic fused kernel."""
+    """The production kernels (auto) and every A/B alternative at once (FFMA
+    channel kernel, split path for U <= 16, lane-per-row solve kernel)."""
     gpu_ctx.set_kernel_policy(request.param)
     yield gpu_ctx
     gpu_ctx.set_kernel_policy("auto")

@@ -23,6 +23,26 @@ def gen(ctx, cfg, sc0=0, n_sc=None):
     return H, Y
 
 
+def assert_contract(a, b, what):
+    """Two GPU variants' outputs agree within the north_star contract,
+    elementwise: |a - b| <= 1e-4 + 1e-3 |b|; status bytes equal; hard LLR
+    bits equal wherever |LLR| >= 1e-4."""
+    for k in a:
+        if a[k] is None or k not in b:
+            continue
+        x, y = a[k], b[k]
+        if x.dtype == torch.uint8:
+            assert torch.equal(x, y), (what, k)
+            continue
+        if x.is_complex():
+            x, y = torch.view_as_real(x), torch.view_as_real(y)
+        bad = (x - y).abs() > 1e-4 + 1e-3 * y.abs()
+        assert int(bad.sum()) == 0, (what, k, float((x - y).abs().max()), int(bad.sum()))
+        if k == "llr":
+            flip = ((x > 0) != (y > 0)) & (y.abs() >= 1e-4)
+            assert int(flip.sum()) == 0, (what, "hard bits", int(flip.sum()))
+
+
 def run(ctx, cfg, H, Y):
     out = ctx.detect_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K, cfg.tracker)
     torch.cuda.synchronize()
@@ -136,22 +156,8 @@ def test_kernel_launch_accounting(gpu_ctx):
     assert gpu_ctx.kernel_launches - mid >= 1  # the hot path ran native kernels
 
 
-def test_overlapped_chunks_bitwise_equal(gpu_ctx, monkeypatch):
-    """The optional two-stream chunk overlap (CGMIMO_OVERLAP_CHUNKS) gives the
-    same bits as the default serial chunk loop."""
-    cfg = get_config("cfg2")
-    H, Y = gen(gpu_ctx, cfg)
-    a = run(gpu_ctx, cfg, H, Y)
-    monkeypatch.setenv("CGMIMO_OVERLAP_CHUNKS", "3")
-    b = run(gpu_ctx, cfg, H, Y)
-    monkeypatch.setenv("CGMIMO_OVERLAP_CHUNKS", "4")
-    c = run(gpu_ctx, cfg, H, Y)
-    for k in a:
-        assert torch.equal(a[k], b[k]) and torch.equal(a[k], c[k]), k
-
-
 @pytest.mark.parametrize("name", ["cfg2", "cfg4a_K8", "cfg5"])
-def test_tensor_core_channel_matches_ffma_channel(gpu_ctx, checker, monkeypatch, name):
+def test_tensor_core_channel_matches_ffma_channel(gpu_ctx, checker, name):
     """The tcgen05 channel kernel (bf16 x3 split, cgm_tc.cuh) and the FP32
     FFMA channel kernel agree to FP32 rounding, and both match the oracle on
     a subsample (U = 32, B a multiple of 64: the shapes the tensor-core path
@@ -159,50 +165,17 @@ def test_tensor_core_channel_matches_ffma_channel(gpu_ctx, checker, monkeypatch,
     cfg = get_config(name).scaled(600)
     H, Y = gen(gpu_ctx, cfg)
     tc = run(gpu_ctx, cfg, H, Y)
-    monkeypatch.setenv("CGMIMO_CHANNEL", "ffma")
-    ff = run(gpu_ctx, cfg, H, Y)
-    monkeypatch.delenv("CGMIMO_CHANNEL")
-    for k in ("xhat", "mu", "rho"):
-        a, b = tc[k], ff[k]
-        if a.is_complex():
-            a, b = torch.view_as_real(a), torch.view_as_real(b)
-        assert float((a - b).abs().max()) <= 1e-4 + 1e-3 * float(b.abs().max()), k
+    gpu_ctx.set_kernel_policy("ffma_channel")
+    try:
+        ff = run(gpu_ctx, cfg, H, Y)
+    finally:
+        gpu_ctx.set_kernel_policy("auto")
+    assert_contract(tc, ff, "tcgen05 vs FFMA channel")
     assert int(tc["status"].sum()) == 0
     idx = np.random.default_rng(2).choice(cfg.n_sc, size=8, replace=False)
     want = checker.detect(H[idx].cpu().numpy(), Y[idx].cpu().numpy(), cfg.rho_u, cfg.n0, cfg.es,
                           cfg.qam_bits, cfg.K, cfg.tracker, threads=8)
     check_detect({k: v[idx].cpu().numpy() for k, v in tc.items()}, want, name + " tensor-core")
-
-
-@pytest.mark.parametrize("name", ["cfg2", "cfg5"])
-def test_tiled_cg_kernel_matches_default(gpu_ctx, monkeypatch, name):
-    """The optional block-tiled FFMA2 CG kernel (CGMIMO_SOLVE=tiles,
-    cgm_solve32.cuh) agrees with the default lane-per-row kernel to FP32
-    rounding, uplink and (cfg5) downlink."""
-    cfg = get_config(name).scaled(300)
-    H, Y = gen(gpu_ctx, cfg)
-    if cfg.kind == "both":
-        T = gpu_ctx.generate_symbols(cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits)
-        call = lambda: gpu_ctx.detect_precode_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits,
-                                                 cfg.K, cfg.tracker, T, cfg.rho_d, cfg.K)
-    else:
-        call = lambda: gpu_ctx.detect_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
-                                         cfg.tracker)
-    a = call()
-    torch.cuda.synchronize()
-    monkeypatch.setenv("CGMIMO_SOLVE", "tiles")
-    b = call()
-    torch.cuda.synchronize()
-    monkeypatch.delenv("CGMIMO_SOLVE")
-    for k in a:
-        if a[k].dtype == torch.uint8:
-            assert torch.equal(a[k], b[k]), k
-            continue
-        x, y = a[k], b[k]
-        if x.is_complex():
-            x, y = torch.view_as_real(x), torch.view_as_real(y)
-        tol = 1e-4 + 1e-3 * float(x.abs().max()) if k != "llr" else 1e-3 * 64
-        assert float((x - y).abs().max()) <= tol, k
 
 
 @pytest.mark.parametrize("U,B,K", [(4, 16, 2), (8, 32, 4), (16, 64, 3), (32, 128, 4)])
@@ -223,29 +196,19 @@ def test_precode_uplink_layout_equals_downlink_layout(gpu_ctx, U, B, K):
         assert d < 1e-5, (k, d)
 
 
-@pytest.mark.parametrize("name,var,val", [
-    ("cfg2", "CGMIMO_FUSED", "1"),           # opt-in: one fused warp per subcarrier
-    ("cfg2", "CGMIMO_SOLVE", "lanes"),       # default: Gram-row-in-registers pairs kernel
-    ("cfg2", "CGMIMO_ROWS_NS", "4"),         # four systems per warp
-    ("cfg2", "CGMIMO_ROWS_NS", "1"),         # one system per warp
-    ("cfg2", "CGMIMO_ROWS_PF", "1"),         # persistent, next item prefetched
-    ("cfg4a_K8", "CGMIMO_SOLVE", "rows"),    # CTA-per-subcarrier rows kernel, exact tail
-    ("cfg4a_K2", "CGMIMO_SOLVE", "lanes"),   # default: exact pairs kernel (tail in the warp)
-    ("cfg4a_K8", "CGMIMO_SOLVE", "lanes"),
-    ("cfg5", "CGMIMO_SOLVE", "pf"),          # default: CTA rows kernel; pf = persistent lane kernel
-    ("cfg1", "CGMIMO_UPSMALL", "split"),     # default: fused U <= 16 detector, one warp per subcarrier
-    ("cfg4a_K8", "CGMIMO_BASIS", "inline"),  # default: basis_kernel (cgm_basis.cuh)
-    ("cfg4a_K2", "CGMIMO_FX", "0"),          # default S = 1: basis + extraction fused (no T in HBM)
-    ("cfg4a_K2", "CGMIMO_FXFUSED", "1"),     # opt-in U = 32, S = 1: Gram + MF + CG in one warp
-    ("cfg4a_K8", "CGMIMO_FXFUSED", "1"),
-    ("cfg4a_K8", "CGMIMO_FX", "0"),
-    ("cfg4b_K4", "CGMIMO_FX", "0"),
-    ("cfg4b_K4", "CGMIMO_BASIS", "inline"),
-    ("cfg5", "CGMIMO_BASIS", "inline"),
+@pytest.mark.parametrize("name,policy", [
+    ("cfg2", "lane_solve"),        # default: Gram-row-in-registers pairs kernel
+    ("cfg4a_K2", "lane_solve"),    # default: exact pairs kernel, one system per warp (S = 1)
+    ("cfg4a_K8", "lane_solve"),
+    ("cfg4a_K8", "ffma_channel"),  # default: tcgen05 channel kernel
+    ("cfg5", "lane_solve"),        # default: 8-warp row CTA with the precoder tail
+    ("cfg5", "ffma_channel"),
+    ("cfg1", "split_small"),       # default: fused U <= 16 detector, one warp per subcarrier
 ])
-def test_solve_and_basis_variants_agree(gpu_ctx, checker, monkeypatch, name, var, val):
-    """Every K2 / basis variant gives the default's results to FP32 rounding,
-    and the default matches the oracle on a subsample."""
+def test_kernel_variants_agree(gpu_ctx, checker, name, policy):
+    """Every kernel variant gives the default's results within the north_star
+    contract elementwise (|a - b| <= 1e-4 + 1e-3 |b|, hard bits equal where
+    |LLR| >= 1e-4), and the default matches the oracle on a subsample."""
     cfg = get_config(name).scaled(400)
     H, Y = gen(gpu_ctx, cfg)
     if cfg.kind == "both":
@@ -258,20 +221,14 @@ def test_solve_and_basis_variants_agree(gpu_ctx, checker, monkeypatch, name, var
     a = call()
     torch.cuda.synchronize()
     l0 = gpu_ctx.kernel_launches
-    monkeypatch.setenv(var, val)
-    b = call()
-    torch.cuda.synchronize()
-    monkeypatch.delenv(var)
+    gpu_ctx.set_kernel_policy(policy)
+    try:
+        b = call()
+        torch.cuda.synchronize()
+    finally:
+        gpu_ctx.set_kernel_policy("auto")
     assert gpu_ctx.kernel_launches > l0
-    for k in a:
-        if a[k].dtype == torch.uint8:
-            assert torch.equal(a[k], b[k]), k
-            continue
-        x, y = a[k], b[k]
-        if x.is_complex():
-            x, y = torch.view_as_real(x), torch.view_as_real(y)
-        tol = 1e-4 + 1e-3 * float(x.abs().max()) if k != "llr" else 1e-3 * 64
-        assert float((x - y).abs().max()) <= tol, k
+    assert_contract(a, b, f"{name} {policy}")
     idx = np.random.default_rng(5).choice(cfg.n_sc, size=6, replace=False)
     want = checker.detect(H[idx].cpu().numpy(), Y[idx].cpu().numpy(), cfg.rho_u, cfg.n0, cfg.es,
                           cfg.qam_bits, cfg.K, cfg.tracker, threads=8)
@@ -280,7 +237,7 @@ def test_solve_and_basis_variants_agree(gpu_ctx, checker, monkeypatch, name, var
 
 
 @pytest.mark.parametrize("U,B,S,K", [(16, 128, 1, 3), (8, 64, 3, 4), (5, 30, 2, 2), (13, 96, 4, 5)])
-def test_fused_small_precoder_matches_split_and_oracle(gpu_ctx, checker, monkeypatch, U, B, S, K):
+def test_fused_small_precoder_matches_split_and_oracle(gpu_ctx, checker, U, B, S, K):
     """The fused U <= 16 precoder (cgm_precode_small.cuh: one HBM read of H_d)
     agrees with the channel + solve pair to FP32 rounding and with the
     oracle, ragged U and B included (B = 30: no TMA, plain copies)."""
@@ -294,10 +251,12 @@ def test_fused_small_precoder_matches_split_and_oracle(gpu_ctx, checker, monkeyp
     a = gpu_ctx.precode_cg(Hd, T, 0.625, K)
     torch.cuda.synchronize()
     assert gpu_ctx.kernel_launches - l0 == 1  # one fused launch
-    monkeypatch.setenv("CGMIMO_PRECODE", "split")
-    b = gpu_ctx.precode_cg(Hd, T, 0.625, K)
-    torch.cuda.synchronize()
-    monkeypatch.delenv("CGMIMO_PRECODE")
+    gpu_ctx.set_kernel_policy("split_small")
+    try:
+        b = gpu_ctx.precode_cg(Hd, T, 0.625, K)
+        torch.cuda.synchronize()
+    finally:
+        gpu_ctx.set_kernel_policy("auto")
     assert torch.equal(a["status"], b["status"])
     assert int(a["status"][7].min()) == 2
     for k in ("q", "s", "gain"):
@@ -388,8 +347,29 @@ def test_host_generator_matches_device(gpu_ctx, oracle_ref, name):
     Hh, Yh, Th = oracle_ref.gen_uplink(cfg.seed, cfg.B, cfg.U, 3, n, cfg.S, cfg.qam_bits, cfg.n0,
                                        rsqrt=None if rs is None else rs.astype(np.float32),
                                        with_t=True, threads=4)
-    np.testing.assert_array_max_ulp(H.cpu().numpy().view(np.float32), Hh.view(np.float32),
-                                    maxulp=2)
+    # FP64 sums rounded to complex64: equal up to one rounding of the sum
+    h = H.cpu().numpy()
+    np.testing.assert_allclose(h, Hh, rtol=0, atol=2e-7 * float(np.abs(Hh).max()))
+    assert np.mean(h == Hh) > 0.99
     y, yh = Y.cpu().numpy(), Yh
-    np.testing.assert_allclose(y, yh, rtol=0, atol=1e-5 * float(np.abs(yh).max()))
+    np.testing.assert_allclose(y, yh, rtol=0, atol=2e-7 * float(np.abs(yh).max()))
+    assert np.mean(y == yh) > 0.99
     np.testing.assert_array_equal(T.cpu().numpy(), Th)
+
+
+@pytest.mark.parametrize("name", ["cfg4a_K4", "cfg4b_K2", "cfg5", "cfg1", "cfg2"])
+def test_partial_output_requests_match_full(gpu_ctx, name):
+    """Any subset of the outputs may be requested (NULL pointers for the
+    rest): the results do not depend on which other outputs exist -- the
+    exact tracker's extraction reads v_K and the breakdown flags from its
+    own state, never from the caller's buffers."""
+    cfg = get_config(name).scaled(64)
+    H, Y = gen(gpu_ctx, cfg)
+    full = run(gpu_ctx, cfg, H, Y)
+    for want in (("llr",), ("llr", "mu"), ("rho",), ("xhat", "status")):
+        part = gpu_ctx.detect_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                                 cfg.tracker, want=want)
+        torch.cuda.synchronize()
+        assert set(part) == set(want)
+        for k in want:
+            assert torch.equal(part[k], full[k]), (name, want, k)

@@ -66,3 +66,25 @@ def test_seed_scheme_is_shard_invariant(oracle_port):
             a, b = shard_range(12, r, w)
             part = [oracle_port.rayleigh(3, [2, sc], 16, 4) for sc in range(a, b)]
             assert all(np.array_equal(x, y) for x, y in zip(part, full[a:b]))
+
+
+def test_output_buffers_are_validated():
+    """Caller-supplied out= buffers: wrong shape, dtype, layout or memory
+    space raise ValueError before any pointer reaches the C ABI."""
+    like = np.zeros((2, 8, 4), np.complex64)
+    shapes = {"mu": ((2, 3, 4), "f32"), "xhat": ((2, 3, 4), "c64")}
+    api._check_outputs({"mu": np.zeros((2, 3, 4), np.float32)}, shapes, False, like)
+    with pytest.raises(ValueError):  # undersized
+        api._check_outputs({"mu": np.zeros((2, 3, 3), np.float32)}, shapes, False, like)
+    with pytest.raises(ValueError):  # dtype
+        api._check_outputs({"mu": np.zeros((2, 3, 4), np.float64)}, shapes, False, like)
+    with pytest.raises(ValueError):  # not contiguous
+        api._check_outputs({"xhat": np.zeros((2, 4, 3), np.complex64).transpose(0, 2, 1)},
+                           shapes, False, like)
+    with pytest.raises(ValueError):  # a host array in a device call
+        import torch
+
+        api._check_outputs({"mu": np.zeros((2, 3, 4), np.float32)}, shapes, True,
+                           torch.zeros(1))
+    with pytest.raises(ValueError):  # unknown name
+        api._check_outputs({"nu": np.zeros((2, 3, 4), np.float32)}, shapes, False, like)
