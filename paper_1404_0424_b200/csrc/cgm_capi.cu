@@ -261,8 +261,8 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   if constexpr (EXACT) {
     if (p.S > 0) {
       using MG = cgm::MomGeo<UP>;
-      // FP32 products up to K = 8, FP64 beyond (cgm_moments.cuh)
-      const bool dbl = p.K > 8;
+      // FP32 products up to K = 6, FP64 beyond (cgm_moments.cuh)
+      const bool dbl = p.K > 6;
       km = dbl ? cgm::moments_kernel<UP, double> : cgm::moments_kernel<UP, float>;
       nm_smem = dbl ? MG::template smem<double>() : MG::template smem<float>();
       nm_t = MG::NT;
