@@ -42,6 +42,7 @@ struct cgm_ctx {
   long launches = 0;
   int policy = 0;  // kernel-variant switches (kPol*), 0 = production defaults
   int host_chunks = 0;  // CGMIMO_HOST_CHUNKS, read once at context creation
+  size_t chunk_bytes = 80ull << 20;  // split-path chunk budget (CGMIMO_CHUNK_MB)
   // optional per-kernel event timing (bench roofline): pairs of events per launch
   int profiling = 0;
   cudaEvent_t order_ev = nullptr;  // host pipeline: ordered after the context stream's work
@@ -205,6 +206,9 @@ template <int UP, bool EXACT>
 int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   const int Kmax = std::max(p.K, p.Kt);
   p.exact = EXACT ? 1 : 0;
+  // one vector per subcarrier: the CG runs before the moments kernel, which
+  // then does the per-vector extraction itself (moments_kernel<..., FX>)
+  p.fx = (EXACT && p.S == 1 && p.St == 0) ? 1 : 0;
   // ------------------------------------------------------------------ K1
   cgm::K1Split sp;
   sp.plan(UP, p.B, p.S);
@@ -261,9 +265,11 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   if constexpr (EXACT) {
     if (p.S > 0) {
       using MG = cgm::MomGeo<UP>;
-      // FP32 products up to K = 6, FP64 beyond (cgm_moments.cuh)
-      const bool dbl = p.K > 6;
-      km = dbl ? cgm::moments_kernel<UP, double> : cgm::moments_kernel<UP, float>;
+      // moment table: FP32 products up to K = 6, FP64 beyond; FX (one
+      // vector per subcarrier): FP32 entrywise sums (cgm_moments.cuh)
+      const bool dbl = !p.fx && p.K > 6;
+      km = p.fx ? cgm::moments_kernel<UP, float, true>
+                : dbl ? cgm::moments_kernel<UP, double> : cgm::moments_kernel<UP, float>;
       nm_smem = dbl ? MG::template smem<double>() : MG::template smem<float>();
       nm_t = MG::NT;
       nm_spc = MG::SPC;
@@ -334,10 +340,10 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   }
   // --------------------------------------------------------------- chunks
   cgm::WsOffsets W;
-  W.plan(UP, p.S, p.K, EXACT);
+  W.plan(UP, p.S, p.K, EXACT, p.fx);
   const size_t per_sc = static_cast<size_t>(W.stride) * 8 + static_cast<size_t>(p.B) * p.U * 8 +
                         static_cast<size_t>(p.B) * p.S * 8;
-  long chunk = static_cast<long>((80ull << 20) / std::max<size_t>(per_sc, 1));
+  long chunk = static_cast<long>(ctx->chunk_bytes / std::max<size_t>(per_sc, 1));
   chunk = std::max<long>(chunk, static_cast<long>(ctx->sms) * occ1);
   chunk = std::min(chunk, p.n_sc);
   const int rc = ensure_ws(ctx, static_cast<size_t>(chunk) * W.stride * sizeof(float2));
@@ -351,12 +357,12 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
     const long g1 = std::max<long>(1, std::min<long>(n, static_cast<long>(occ1) * ctx->sms));
     int r = timed(ctx, st, 1, [&] { k1<<<static_cast<unsigned>(g1), nt1, smem1, st>>>(q); });
     if (r) return r;
-    if (km) {
-      r = timed(ctx, st, 3, [&] {
+    auto moments = [&] {
+      return timed(ctx, st, 3, [&] {
         km<<<static_cast<unsigned>((n + nm_spc - 1) / nm_spc), nm_t, nm_smem, st>>>(q);
       });
-      if (r) return r;
-    }
+    };
+    if (km && !p.fx && (r = moments())) return r;
     r = timed(ctx, st, 2, [&] {
       if (mode == kPairs)  // 4 warps per CTA, one (subcarrier, system group) per warp
         k2<<<static_cast<unsigned>((n * ((p.S + pair_ns - 1) / pair_ns) + 3) / 4), 128, 0, st>>>(q);
@@ -364,6 +370,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
         k2<<<static_cast<unsigned>(std::min(n, g2cap)), 32 * nw2, smem2, st>>>(q);
     });
     if (r) return r;
+    if (km && p.fx && (r = moments())) return r;
   }
   return CGM_OK;
 }
@@ -732,6 +739,7 @@ int cgm_ctx_create(int device, cgm_ctx** out) {
   for (int i = 0; i < 3 && e == cudaSuccess; ++i)
     e = cudaStreamCreateWithFlags(&ctx->pipe[i], cudaStreamNonBlocking);
   if (const char* hc = std::getenv("CGMIMO_HOST_CHUNKS")) ctx->host_chunks = std::max(0, std::atoi(hc));
+  if (const char* cm = std::getenv("CGMIMO_CHUNK_MB")) ctx->chunk_bytes = static_cast<size_t>(std::max(1, std::atoi(cm))) << 20;
   if (e == cudaSuccess) {
     const cgm::AxisTables t = make_axis_tables();
     e = cudaMemcpyToSymbol(cgm::c_axis, &t, sizeof t);

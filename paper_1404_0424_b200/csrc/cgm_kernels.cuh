@@ -31,6 +31,7 @@ struct KernelParams {
   int hd_layout;  // 1: H is the downlink matrix [U][B] (precode only)
   int use_tma;    // bulk-copy staging (U == UP, B even, 16B aligned)
   int exact;      // uplink systems use the exact tracker (the workspace carries the row moments)
+  int fx;         // exact, one vector per subcarrier: the CG runs before moments_kernel<..., FX>
   float rho_inv_u, rho_inv_d, n0, es;
   float2* ws;     // split path: per-subcarrier workspace (G, MF, (c, d), row moments)
   long sc_base;   // split path: first subcarrier of this chunk

@@ -49,14 +49,17 @@ namespace cgm {
 // split-path workspace layout per subcarrier (float2 units): G (UP x UP,
 // full Hermitian), the S matched filters, (c, d) of the Chebyshev interval,
 // and for the exact tracker the row-moment table D_k[i] (double, k = 0..2K)
+// fx (exact, one vector per subcarrier): instead of the moment table, the
+// CG's (alpha, beta) history (K float2), v_K (UP float2) and the breakdown
+// flag (1 float2) for moments_kernel<..., FX>
 struct WsOffsets {
   int g, mf, cd, t, stride;
-  __host__ __device__ void plan(int UP, int S, int K, bool exact) {
+  __host__ __device__ void plan(int UP, int S, int K, bool exact, bool fx = false) {
     g = 0;
     mf = UP * UP;
     cd = mf + S * UP;
     t = cd + 2;
-    stride = t + (exact ? (2 * K + 1) * UP : 0);
+    stride = t + (exact ? (fx ? K + UP + 1 : (2 * K + 1) * UP) : 0);
     stride = (stride + 1) & ~1;
   }
 };
@@ -156,18 +159,29 @@ __device__ __forceinline__ void tile_prod(const double2* A, const double2* T, in
 
 // moments_kernel: per subcarrier (SPC per CTA), from G in the workspace:
 // (c, d) by power iteration (cheb_interval), Ahat, the K - 1 products of the
-// Chebyshev recursion, and D_k[i], k = 0..2K, into the workspace.
-template <int UP, class R>
+// Chebyshev recursion, and
+//   FX = false: D_k[i], k = 0..2K, into the workspace (any S);
+//   FX = true (one vector per subcarrier, S = 1): the CG kernel ran first and
+//     left its (alpha, beta) history, v_K and status in the workspace; the
+//     coefficients of L_K and B are formed here and every tile thread
+//     accumulates its entries of B = sum g_m T_m and L = sum l_m T_m while the
+//     products produce T_2..T_K, then the extraction (detect.cpp:375-395) and
+//     the LLRs finish in this kernel.  With a single vector the per-vector
+//     U^3 work is unavoidable, and the entrywise sums keep FP32 accurate to
+//     K = 16 (the moment table's quadratic forms need FP64 products from
+//     K = 7 on).
+template <int UP, class R, bool FX = false>
 __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelParams p) {
   using MG = MomGeo<UP>;
   using C = typename Cx<R>::T;
-  constexpr int MAT = MG::MAT, SPC = MG::SPC, LD = MG::LD, NT = MG::NT;
+  static_assert(!FX || std::is_same<R, float>::value, "FX runs in FP32");
+  constexpr int MAT = MG::MAT, SPC = MG::SPC, LD = MG::LD, NT = MG::NT, NB = MG::NB;
   extern __shared__ __align__(128) unsigned char smem[];
   C* base = reinterpret_cast<C*>(smem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = p.K;
   WsOffsets W;
-  W.plan(UP, p.S, K, true);
+  W.plan(UP, p.S, K, true, FX);
   const long sc0 = static_cast<long>(blockIdx.x) * SPC;
   const int nsc = static_cast<int>(p.n_sc - sc0 < SPC ? p.n_sc - sc0 : SPC);
   // buffer b of subcarrier s: 0 = Ahat (T_1), 1 / 2 = the recursion window
@@ -184,6 +198,8 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
   }
   __syncthreads();
   __shared__ float2 cds[SPC];
+  // FX: the Chebyshev coefficients of L_K and B per subcarrier (cl, cb)
+  __shared__ float coefs[FX ? SPC : 1][2][kMaxK + 2];
   for (int s = warp; s < nsc; s += NT / 32) {
     // power-iteration scratch: buffer 2 (as float2)
     const float2 cd = cheb_interval<UP, LD>(reinterpret_cast<const float2*>(buf(s, 1)),
@@ -191,6 +207,11 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
     if (lane == 0) {
       cds[s] = cd;
       p.ws[(sc0 + s) * W.stride + W.cd] = cd;
+    }
+    if constexpr (FX) {
+      const float2* hw = p.ws + (sc0 + s) * W.stride + W.t;  // K (alpha, beta) pairs
+      cheb_coef_warp(reinterpret_cast<const float*>(hw), K, cd.x, cd.y, p.rho_inv_u,
+                     coefs[s][0], coefs[s][1]);
     }
   }
   __syncthreads();
@@ -210,8 +231,8 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
     buf(s, 0)[r * LD + c] = v;
   }
   __syncthreads();
-  // row moments: thread <-> (subcarrier, row i); column reads are
-  // conflict-free and T[j][i] = conj(T[i][j]) gives the same sums
+  // row moments (FX = false): thread <-> (subcarrier, row i); column reads
+  // are conflict-free and T[j][i] = conj(T[i][j]) gives the same sums
   auto row_moments = [&](int a, int cur, int prv) {
     // D_{2a} from T_a (buffer cur), D_{2a-1} from T_a and T_{a-1} (buffer prv, -1: I)
     for (int e = tid; e < nsc * UP; e += NT) {
@@ -238,7 +259,7 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
       mom[2 * a * UP + i] = 2.0 * n2 - 1.0;
     }
   };
-  row_moments(1, 0, -1);
+  if (!FX) row_moments(1, 0, -1);
   // products: thread <-> (subcarrier slot, lower tile)
   const int slot = tid / MG::NTILE;
   const int tile = tid - slot * MG::NTILE;
@@ -247,6 +268,24 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
   const int cb = tile - rb * (rb + 1) / 2;
   const bool busy = slot < nsc;
   const int i0 = rb * 4, j0 = cb * 4;
+  // FX: this tile's entries of B = sum_m cb_m T_m and L = sum_{m<K} cl_m T_m
+  float2 Bacc[FX ? 4 : 1][FX ? 4 : 1], Lacc[FX ? 4 : 1][FX ? 4 : 1];
+  if constexpr (FX) {
+    const float* cl = coefs[busy ? slot : 0][0];
+    const float* cbq = coefs[busy ? slot : 0][1];
+    const C* A = buf(busy ? slot : 0, 0);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = i0 + r, j = j0 + c;
+        const float2 t1 = busy ? A[i * LD + j] : make_float2(0.f, 0.f);  // T_1
+        const float d0 = i == j ? 1.f : 0.f;                             // T_0 = I
+        Bacc[r][c] = make_float2(cbq[0] * d0 + cbq[1] * t1.x, cbq[1] * t1.y);
+        Lacc[r][c] = K > 1 ? make_float2(cl[0] * d0 + cl[1] * t1.x, cl[1] * t1.y)
+                           : make_float2(cl[0] * d0, 0.f);
+      }
+  }
   // T_a in buffer cur, T_{a-1} in buffer prv (-1: the identity), T_{a+1}
   // written over T_{a-1} (buffer 1 / 2; never over Ahat)
   int cur = 0, prv = -1;
@@ -276,13 +315,94 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
             cv.y = -val.y;
             Tn[j * LD + i] = cv;
           }
+          if constexpr (FX) {  // T_{a+1} into this tile's B and L
+            const float cbm = coefs[slot][1][a + 1];
+            Bacc[r][c].x = fmaf(cbm, val.x, Bacc[r][c].x);
+            Bacc[r][c].y = fmaf(cbm, val.y, Bacc[r][c].y);
+            if (a + 1 < K) {
+              const float clm = coefs[slot][0][a + 1];
+              Lacc[r][c].x = fmaf(clm, val.x, Lacc[r][c].x);
+              Lacc[r][c].y = fmaf(clm, val.y, Lacc[r][c].y);
+            }
+          }
         }
     }
     __syncthreads();
-    row_moments(a + 1, out, cur);
-    __syncthreads();  // the row pass read T_a before the next product overwrites T_{a-1}
+    if (!FX) {
+      row_moments(a + 1, out, cur);
+      __syncthreads();  // the row pass read T_a before the next product overwrites T_{a-1}
+    }
     prv = cur;
     cur = out;
+  }
+  if constexpr (FX) {
+    // ---------------- extraction (detect.cpp:375-395) from the tile sums:
+    // per lower entry (i, j): |B_ij|^2 and Re(B_ij conj(L_ij)) count for row
+    // i and (i != j, Hermitian) for row j; mu_i = Re B_ii.  Row parts go to
+    // Rb[i][cb], column parts to Cb[j][rb] (each slot written by one tile),
+    // summed in a fixed order.  They alias window buffer 1 or 2 -- whichever
+    // does not hold T_K, read by no one now (all products ended at the
+    // barrier above).
+    const int pb = cur == 1 ? 2 : 1;
+    float* Rb = reinterpret_cast<float*>(buf(busy ? slot : 0, pb));  // [UP][NB][2]
+    float* Cb = Rb + UP * NB * 2;                                    // [UP][NB][2]
+    float* Mb = Cb + UP * NB * 2;                                    // [UP]
+    static_assert(4 * UP * (UP / 4) + UP <= 2 * UP * (UP + 2), "partials fit a T buffer");
+    if (busy) {
+      float rr2[4] = {0.f, 0.f, 0.f, 0.f}, rrl[4] = {0.f, 0.f, 0.f, 0.f};
+      float cc2[4] = {0.f, 0.f, 0.f, 0.f}, ccl[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int i = i0 + r, j = j0 + c;
+          if (j > i) continue;
+          const float2 b = Bacc[r][c], l = Lacc[r][c];
+          const float wl = b.x * l.x + b.y * l.y;
+          if (i == j) {
+            Mb[i] = b.x;
+            rrl[r] += wl;
+          } else {
+            const float w2 = cnorm(b);
+            rr2[r] += w2; rrl[r] += wl;
+            cc2[c] += w2; ccl[c] += wl;
+          }
+        }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        Rb[((i0 + r) * NB + cb) * 2 + 0] = rr2[r];
+        Rb[((i0 + r) * NB + cb) * 2 + 1] = rrl[r];
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        Cb[((j0 + c) * NB + rb) * 2 + 0] = cc2[c];
+        Cb[((j0 + c) * NB + rb) * 2 + 1] = ccl[c];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < nsc * UP; e += NT) {
+      const int s = e / UP, i = e - s * UP;
+      if (i >= p.U) continue;
+      const float* Rr = reinterpret_cast<const float*>(buf(s, pb));
+      const float* Cc = Rr + UP * NB * 2;
+      const float* M = Cc + UP * NB * 2;
+      const int rbi = i / 4;
+      float ib2 = 0.f, ibl = 0.f;
+      for (int q = 0; q <= rbi; ++q) { ib2 += Rr[(i * NB + q) * 2]; ibl += Rr[(i * NB + q) * 2 + 1]; }
+      for (int q = rbi; q < NB; ++q) { ib2 += Cc[(i * NB + q) * 2]; ibl += Cc[(i * NB + q) * 2 + 1]; }
+      const float2* wsx = p.ws + (sc0 + s) * W.stride;
+      const bool ok = wsx[W.t + K + UP].x == 0.f;  // the CG's breakdown flag
+      const long sc = p.sc_base + sc0 + s;           // S = 1: vector index == subcarrier
+      const long o = sc * static_cast<long>(p.U) + i;
+      const float mu_i = M[i];
+      const float nu2 = ib2 * p.es + ibl * p.n0;
+      const float mu = ok ? mu_i : 0.f;
+      const float rho = ok ? (nu2 <= 0.f ? 0.f : mu_i * mu_i / nu2) : 0.f;  // safe_rho
+      const float2 xh = ok ? wsx[W.t + K + i] : make_float2(0.f, 0.f);
+      if (p.mu) p.mu[o] = mu;
+      if (p.rho) p.rho[o] = rho;
+      if (p.llr) store_llrs_fast(xh, mu, rho, p.bits, p.llr + o * p.bits);
+    }
   }
 }
 
@@ -394,6 +514,31 @@ __device__ __forceinline__ void moments_row(const double* sh, MomCoef c, int K, 
   const double nu2 = interf * es + cross * n0;
   mu = static_cast<float>(m);
   rho = nu2 < 1e-300 ? 0.f : static_cast<float>(m * m / nu2);
+}
+
+// FX mode, one vector per subcarrier (S = 1): after the CG, x_hat and the
+// status leave now; the (alpha, beta) history, v_K and the breakdown flag go
+// to the workspace for moments_kernel<..., FX>, which finishes mu / rho /
+// LLRs.  Threads [t0, t0 + nt) of the caller take part.
+template <int UP>
+__device__ __forceinline__ void fx_handoff(const KernelParams& p, float2* ws, const WsOffsets& W,
+                                           long sc, const float* hist, int hstride,
+                                           const float2* v, uint8_t broke, int t, int nt) {
+  const int K = p.K;
+  const bool ok = broke == 0;
+  for (int e = t; e < UP + K + 1; e += nt) {
+    if (e < K) {
+      ws[W.t + e] = make_float2(hist[e * 2], hist[e * 2 + 1]);
+    } else if (e < K + UP) {
+      const int u = e - K;
+      ws[W.t + e] = v[u];
+      if (u < p.U && p.xhat) p.xhat[sc * static_cast<long>(p.U) + u] = ok ? v[u] : make_float2(0.f, 0.f);
+    } else {
+      ws[W.t + e] = make_float2(ok ? 0.f : 1.f, 0.f);
+      if (p.status) p.status[sc] = ok ? 0 : 1;
+    }
+  }
+  (void)hstride;
 }
 
 // per-warp shared scratch (doubles) for moments_coefs / moments_row

@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(256, 2) solve_rows32_kernel(const KernelParams
   K2Smem<UP> L;
   L.plan(B, S, St, Kmax, EXACT);
   WsOffsets W;
-  W.plan(UP, S, p.K, EXACT);
+  W.plan(UP, S, p.K, EXACT, p.fx);
   float2* Vs = reinterpret_cast<float2*>(smem + L.vs);
   float2* Qs = reinterpret_cast<float2*>(smem + L.qs);
   float* hist = reinterpret_cast<float*>(smem + L.hist);
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(128, NS == 1 ? 5 : 4) solve_rows32_pairs_kerne
   const int base = static_cast<int>(item - lsc * npairs) * NS;
   const long sc = p.sc_base + lsc;
   WsOffsets W;
-  W.plan(UP, S, K, EXACT);
+  W.plan(UP, S, K, EXACT, p.fx);
   const float2* ws = p.ws + lsc * W.stride;
   unsigned long long grow[UP];
 #pragma unroll
@@ -328,6 +328,11 @@ __global__ void __launch_bounds__(128, NS == 1 ? 5 : 4) solve_rows32_pairs_kerne
     rows32_pair<true, true, NS>(p, sc, ws + W.mf, base, grow, gdiag, Ps_all[warp],
                                 hist_all[w] - base * K * 2, Vs_all[w] - base * UP, st_all[w] - base);
     __syncwarp();
+    if (p.fx) {  // S = 1: moments_kernel<..., FX> finishes from the workspace
+      fx_handoff<UP>(p, const_cast<float2*>(ws), W, sc, hist_all[w], K, Vs_all[w], st_all[w][0],
+                     lane, 32);
+      return;
+    }
     const float2 cdv = ws[W.cd];
     const double* mom = reinterpret_cast<const double*>(ws + W.t);
 #pragma unroll 1
