@@ -342,7 +342,7 @@ int ref_gen_uplink(uint64_t seed, int B, int U, long sc0, long n_sc, int S, int 
     const phy::Rng root(seed);
     const phy::Rng chan = root.fork(2), lab = root.fork(1), noise = root.fork(3), sym = root.fork(4);
     const double sd = std::sqrt(0.5 * n0);
-    auto label = [&](phy::Rng r, int u) {
+    auto label = [&](phy::Rng& r, int u) {
       (void)u;
       unsigned l = 0;
       for (int b = 0; b < qam_bits; ++b) l = (l << 1) | static_cast<unsigned>(r.next_u64() & 1u);

@@ -89,14 +89,18 @@ class Context:
 
         self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
 
-    POLICY_FLAGS = {"ffma_channel": 1, "split_small": 2, "lane_solve": 4}
+    POLICY_FLAGS = {"ffma_channel": 1, "split_small": 2, "lane_solve": 4, "block_uplink": 8,
+                    "rows_cta": 16}
 
     def set_kernel_policy(self, policy: str):
         """Kernel-variant switches for A/B tests: "auto" (production defaults)
         or "+"-joined names of POLICY_FLAGS -- "ffma_channel" (FFMA Gram
         kernel instead of tcgen05 for U = 32), "split_small" (channel + solve
         pair instead of the fused U <= 16 kernels), "lane_solve" (lane-per-row
-        solve kernel instead of the U = 32 row kernels)."""
+        solve kernel instead of the U = 32 row kernels), "block_uplink" (the
+        shared-G block kernel for U = 32 uplink-only calls instead of the pairs
+        kernel), "rows_cta" (the 8-warp row CTA instead of the block kernel
+        for calls with transmit vectors)."""
         bits = 0
         if policy != "auto":
             for name in policy.split("+"):

@@ -1,0 +1,425 @@
+// cgm_block32.cuh -- K2 for U = 32 with many systems per subcarrier (cfg5:
+// 16 uplink vectors + 16 transmit vectors on the same channel).
+//
+// Persistent CTAs walk the subcarriers; the NEXT subcarrier's workspace
+// span (G, matched filters, Chebyshev interval, row moments: one contiguous
+// block) and transmit vectors land in a second shared-memory buffer by
+// cp.async.bulk while the current one is solved, so the per-subcarrier load
+// latency leaves the critical path.  G is shared by every warp; each warp
+// runs NS = 4 systems of the subcarrier at once (lane u = user row u):
+//   * matvec e_u = sum_j G[u][j] p_j: lane u reads conj(G[j][u]) (one
+//     conflict-free LDS.64 per column, reused by the NS systems) and each
+//     system's p_j pair by a broadcast LDS.128; 2 packed FFMA2 per
+//     (column, system) -- 16 FFMA2 per 6 loads for two columns;
+//   * the 2 x NS dot products of an iteration (curvature, residual norm) are
+//     reduced together: warp_sum4 sums four values over the 32 lanes with 9
+//     shuffles instead of 20;
+//   * K CG iterations with the reference's freeze (||r||^2 <= 1e-28 ||r0||^2
+//     -> alpha = 1, beta = 0) and breakdown (p^H A p < 1e-30) rules
+//     (solvers.cpp:21-27, 37-72), the approximate tracker's Eq. (11)
+//     (detect.cpp:409-427) or the exact tracker's (alpha, beta) history.
+// Tails: the exact tracker's extraction from the row moments (moments_tail,
+// cgm_moments.cuh, CTA-wide); transmit vectors leave v_K and their status in
+// the workspace for precode_q_kernel: thread b owns antenna row b and forms
+// q_b = sum_u H[b][u] v_u for every transmit vector with packed FFMA2 (H
+// row from L2 / HBM, v broadcast from shared memory), the norms ||q|| by a
+// fixed-order reduction, then writes q and s = q / ||q|| straight from
+// registers (precode.cpp:22-71).
+#pragma once
+
+#include "cgm_rows32.cuh"
+
+namespace cgm {
+
+constexpr int kBlkNS = 4;    // systems per warp
+constexpr int kBlkMaxW = 8;  // warps per CTA
+
+struct Block32Smem {
+  int bar, buf, bufb, tb, ps, vs, hist, msh, sys_st, gpart, total;
+  __host__ __device__ static int align(int x) { return (x + 127) & ~127; }
+  // span = bytes of the workspace prefix [g, z) of one subcarrier
+  __host__ __device__ void plan(int S, int St, int K, bool exact, int span) {
+    const int nsys = S + St;
+    int o = 0;
+    bar = o; o = align(o + 16);
+    tb = align(span);                       // T of the subcarrier after its ws span
+    bufb = align(tb + St * 32 * 8);         // bytes per buffer
+    buf = o; o = align(o + 2 * bufb);
+    ps = o; o = align(o + (nsys + kBlkNS - 1) / kBlkNS * kBlkNS * 32 * 8);
+    vs = o; o = align(o + (exact ? S * 32 * 8 : 0));
+    hist = o; o = align(o + (exact ? S * K * 2 * 4 : 0));
+    msh = o; o = align(o + (exact ? kBlkMaxW * kMomScratch * 8 : 0));
+    sys_st = o; o = align(o + nsys);
+    gpart = o; o = align(o + (kBlkMaxW + 2) * 16 * 4);  // precoder: per-warp norms, 1/gain, flags
+    total = o;
+  }
+};
+
+// sum over the 32 lanes of four values at once (10 shuffles): halve the
+// value set at xor 16 and xor 8, finish one value per 8-lane group, gather
+__device__ __forceinline__ void warp_sum4(float (&v)[4]) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = lane & 16, b3 = lane & 8;
+  float k0 = b4 ? v[2] : v[0], k1 = b4 ? v[3] : v[1];
+  const float s0 = b4 ? v[0] : v[2], s1 = b4 ? v[1] : v[3];
+  k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+  float k = b3 ? k1 : k0;
+  k += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  // lane L now holds the sum of value (L >> 3) & 3: gather all four
+#pragma unroll
+  for (int q = 0; q < 4; ++q) v[q] = __shfl_sync(0xffffffffu, k, q << 3);
+}
+
+// CG for the systems base .. base + NS - 1 of subcarrier sc on one warp;
+// Gs = the subcarrier's G in shared memory, Ps = this warp's NS broadcast
+// rows.  Approximate uplink systems write their outputs; exact / downlink
+// systems leave v in Vs and (exact) the history in hist.
+template <bool EXACT>
+__device__ __forceinline__ void block32_cg(const KernelParams& p, long sc, const float2* mfsrc,
+                                           const float2* Ts, int base, const float2* Gs,
+                                           float2* Ps, float* hist, float2* Vs, uint8_t* sys_st,
+                                           float2* zout) {
+  constexpr int UP = 32, NS = kBlkNS;
+  const int S = p.S, St = p.St, U = p.U;
+  const int nsys = S + St;
+  const int Kmax = p.K > p.Kt ? p.K : p.Kt;
+  const int lane = threadIdx.x & 31;
+  const float gdiag = Gs[lane * UP + lane].x;
+  int sys[NS], iters[NS];
+  bool live[NS], down[NS], broke[NS];
+  float reg[NS], rn[NS], rn0[NS];
+  float2 v[NS], r[NS], pp[NS];
+  float f0[NS], f1[NS], f2[NS], ia1[NS], ia2[NS], bm1[NS], bm2[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    sys[s] = base + s;
+    live[s] = sys[s] < nsys;
+    down[s] = sys[s] >= S;
+    reg[s] = down[s] ? p.rho_inv_d : p.rho_inv_u;
+    iters[s] = live[s] ? (down[s] ? p.Kt : p.K) : 0;
+    float2 b = make_float2(0.f, 0.f);
+    if (live[s] && lane < U)
+      b = down[s] ? Ts[(sys[s] - S) * U + lane] : mfsrc[sys[s] * UP + lane];
+    v[s] = make_float2(0.f, 0.f);
+    r[s] = b;
+    pp[s] = b;
+    Ps[s * UP + lane] = b;
+    rn[s] = cnorm(b);
+    broke[s] = false;
+    ia1[s] = ia2[s] = 1.f;
+    bm1[s] = bm2[s] = 0.f;
+    f0[s] = f1[s] = f2[s] = 0.f;
+  }
+  warp_sum4(rn);
+#pragma unroll
+  for (int s = 0; s < NS; ++s) rn0[s] = rn[s];
+  __syncwarp();
+  for (int k = 1; k <= Kmax; ++k) {
+    // e = (G + reg I) p on the packed pipe; G[u][j] = conj(G[j][u])
+    unsigned long long a0[NS], b0[NS], a1[NS], b1[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) a0[s] = b0[s] = a1[s] = b1[s] = 0ull;
+#pragma unroll 4
+    for (int j = 0; j < UP; j += 2) {
+      const float2 gj0 = Gs[j * UP + lane], gj1 = Gs[(j + 1) * UP + lane];
+      const unsigned long long g0 = f2pack(gj0.x, -gj0.y), g1 = f2pack(gj1.x, -gj1.y);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const ulonglong2 pj = *reinterpret_cast<const ulonglong2*>(Ps + s * UP + j);
+        ffma2(a0[s], g0, f2dup_lo(pj.x));
+        ffma2(b0[s], g0, f2dup_hi(pj.x));
+        ffma2(a1[s], g1, f2dup_lo(pj.y));
+        ffma2(b1[s], g1, f2dup_hi(pj.y));
+      }
+    }
+    float2 e[NS];
+    float curv[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const float2 A0 = f2unpack(a0[s]), B0 = f2unpack(b0[s]);
+      const float2 A1 = f2unpack(a1[s]), B1 = f2unpack(b1[s]);
+      e[s].x = (A0.x - B0.y) + (A1.x - B1.y);
+      e[s].y = (B0.x + A0.y) + (B1.x + A1.y);
+      e[s].x = fmaf(reg[s], pp[s].x, e[s].x);
+      e[s].y = fmaf(reg[s], pp[s].y, e[s].y);
+      curv[s] = pp[s].x * e[s].x + pp[s].y * e[s].y;  // Re p^H e
+    }
+    warp_sum4(curv);
+    float alpha[NS], beta[NS], rnx[NS];
+    bool upd[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const bool step = k <= iters[s];
+      const bool frozen = !(rn[s] > 1e-28f * rn0[s]);  // solvers.cpp:21,25-27
+      const bool go = step && !frozen && !broke[s];
+      if (go && curv[s] < 1e-30f) broke[s] = true;  // solvers.cpp:55-57
+      upd[s] = go && !broke[s];
+      alpha[s] = upd[s] ? __fdividef(rn[s], curv[s]) : 1.f;
+      beta[s] = 0.f;
+      if (upd[s]) {
+        v[s].x = fmaf(alpha[s], pp[s].x, v[s].x);
+        v[s].y = fmaf(alpha[s], pp[s].y, v[s].y);
+        r[s].x = fmaf(-alpha[s], e[s].x, r[s].x);
+        r[s].y = fmaf(-alpha[s], e[s].y, r[s].y);
+      }
+      rnx[s] = cnorm(r[s]);
+    }
+    warp_sum4(rnx);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      float ia = 1.f;  // 1 / alpha
+      if (upd[s]) {
+        const float irn = __fdividef(1.f, rn[s]);
+        beta[s] = rnx[s] * irn;
+        ia = curv[s] * irn;
+        rn[s] = rnx[s];
+        pp[s].x = fmaf(beta[s], pp[s].x, r[s].x);
+        pp[s].y = fmaf(beta[s], pp[s].y, r[s].y);
+      }
+      if (k <= iters[s]) {
+        if (!down[s]) {
+          if (EXACT) {
+            if (lane == 0) {
+              hist[(sys[s] * Kmax + (k - 1)) * 2 + 0] = alpha[s];
+              hist[(sys[s] * Kmax + (k - 1)) * 2 + 1] = beta[s];
+            }
+          } else {
+            // Eq. (11) on the diagonal (detect.cpp:409-427); k = 1: L_1 = alpha_1
+            const float c1 = alpha[s] * (1.f + bm1[s]) * ia1[s];
+            const float c2 = alpha[s] * bm2[s] * ia2[s];
+            const float nk = f0[s] + (c1 - alpha[s] * (gdiag + reg[s])) * (f0[s] - f1[s]) -
+                             c2 * (f1[s] - f2[s]);
+            const float nf = k == 1 ? alpha[s] : nk;
+            f2[s] = f1[s];
+            f1[s] = f0[s];
+            f0[s] = nf;
+          }
+        }
+        ia2[s] = ia1[s]; ia1[s] = ia;
+        bm2[s] = bm1[s]; bm1[s] = beta[s];
+      }
+    }
+    __syncwarp();  // every lane's matvec reads of Ps are done
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+      if (upd[s]) Ps[s * UP + lane] = pp[s];
+    __syncwarp();
+  }
+  // ------------------------------------------------ per-system epilogue
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    if (!live[s]) continue;
+    if (down[s]) {  // v_K and the breakdown flag for precode_q_kernel
+      const int ts = sys[s] - S;
+      zout[ts * UP + lane] = v[s];
+      if (lane == 0) zout[St * UP + ts] = make_float2(broke[s] ? 1.f : 0.f, 0.f);
+      continue;
+    }
+    if (EXACT && lane == 0) sys_st[sys[s]] = broke[s] ? 1 : 0;
+    if (EXACT) {
+      Vs[sys[s] * UP + lane] = v[s];
+      continue;
+    }
+    if constexpr (!EXACT) {
+      // approx uplink: mu = Ltilde G_ii, rho = G_ii / N0 (detect.cpp:435-441)
+      if (lane < U) {
+        const long o = (sc * S + sys[s]) * static_cast<long>(U) + lane;
+        const bool ok = !broke[s];
+        const float2 xh = ok ? v[s] : make_float2(0.f, 0.f);
+        const float mu_u = ok ? f0[s] * gdiag : 0.f;
+        const float rho_u = ok ? gdiag / p.n0 : 0.f;
+        if (p.xhat) p.xhat[o] = xh;
+        if (p.mu) p.mu[o] = mu_u;
+        if (p.rho) p.rho[o] = rho_u;
+        if (p.llr) store_llrs_fast(xh, mu_u, rho_u, p.bits, p.llr + o * p.bits);
+        if (p.status && lane == 0) p.status[sc * S + sys[s]] = ok ? 0 : 1;
+      }
+    }
+  }
+}
+
+// Persistent solve kernel: subcarriers blockIdx.x, + gridDim.x, ...; the
+// next one's workspace span and transmit vectors are bulk-copied into the
+// other buffer while the current one is solved.
+template <bool EXACT>
+__global__ void __launch_bounds__(256, 2) block32_kernel(const KernelParams p) {
+  constexpr int UP = 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int S = p.S, St = p.St, U = p.U;
+  const int nsys = S + St;
+  const int Kmax = p.K > p.Kt ? p.K : p.Kt;
+  WsOffsets W;
+  W.plan(UP, S, p.K, EXACT, p.fx, p.zs);
+  const uint32_t span = static_cast<uint32_t>(W.z) * 8u, tbytes = static_cast<uint32_t>(St * U) * 8u;
+  Block32Smem L;
+  L.plan(S, St, Kmax, EXACT, static_cast<int>(span));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  float2* Ps = reinterpret_cast<float2*>(smem + L.ps);
+  float2* Vs = reinterpret_cast<float2*>(smem + L.vs);
+  float* hist = reinterpret_cast<float*>(smem + L.hist);
+  uint8_t* sys_st = reinterpret_cast<uint8_t*>(smem + L.sys_st);
+  const int nt = blockDim.x, nw = nt >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const long n_local = p.n_sc > blockIdx.x ? (p.n_sc - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto bufp = [&](long i) { return smem + L.buf + (i & 1) * L.bufb; };
+  auto issue = [&](long i) {
+    const long lsc = blockIdx.x + i * gridDim.x;
+    unsigned char* dst = bufp(i);
+    fence_proxy_async();  // generic reads of this buffer (two subcarriers ago) before the async write
+    mbar_expect_tx(bar + (i & 1), span + tbytes);
+    bulk_g2s(dst, p.ws + lsc * W.stride, span, bar + (i & 1));
+    if (St > 0) bulk_g2s(dst + L.tb, p.T + (p.sc_base + lsc) * St * U, tbytes, bar + (i & 1));
+  };
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  __syncthreads();
+  if (tid == 0 && n_local > 0) issue(0);
+  for (long i = 0; i < n_local; ++i) {
+    if (tid == 0 && i + 1 < n_local) issue(i + 1);
+    mbar_wait(bar + (i & 1), static_cast<uint32_t>((i >> 1) & 1));
+    const long lsc = blockIdx.x + i * gridDim.x;
+    const long sc = p.sc_base + lsc;
+    const float2* wsb = reinterpret_cast<const float2*>(bufp(i));  // smem copy of the ws span
+    const float2* Ts = reinterpret_cast<const float2*>(bufp(i) + L.tb);
+    float2* zout = p.ws + lsc * W.stride + W.z;
+    for (int base = warp * kBlkNS; base < nsys; base += nw * kBlkNS)
+      block32_cg<EXACT>(p, sc, wsb + W.mf, Ts, base, wsb + W.g, Ps + base * UP, hist, Vs, sys_st,
+                        zout);
+    if (EXACT && S > 0) {
+      __syncthreads();
+      moments_tail<UP>(p, wsb, W, sc, Kmax, hist, Vs, sys_st, nt,
+                       reinterpret_cast<double*>(smem + L.msh));
+    }
+    __syncthreads();  // buffer i & 1 and the per-subcarrier scratch are free
+  }
+}
+
+// Precoder (precode.cpp:22-71) for the transmit vectors solved by
+// block32_kernel: one CTA per subcarrier, two resident per SM (one stages
+// while the other computes), thread b <-> antenna row b (B <= 256, natural
+// H_u layout, U = 32).  The subcarrier's H rows (64 KB) and v_K vectors are
+// staged by coalesced 16-byte cp.async into rows padded to 34 complex
+// (272 B), so the 8 lanes of an LDS.128 phase hit 8 distinct bank groups;
+// v_K is a broadcast.  q_b = sum_u H_u[b][u] v_u (precode.cpp:69 with
+// H_d = H_u^H) for 16 vectors per pass on packed accumulators
+// (a += (h.x, h.y) v.x, b += (h.x, h.y) v.y, q = (a.x - b.y, a.y + b.x)),
+// gain = ||q|| by a fixed-order reduction, s = q / gain, zero_input when the
+// gain vanishes (precode.cpp:22-36).
+struct PrecodeQSmem {
+  static constexpr int LDH = 34;  // padded H row (float2)
+  int h, z, gpart, total;
+  __host__ __device__ static int align(int x) { return (x + 127) & ~127; }
+  __host__ __device__ void plan(int B, int St) {
+    h = 0;
+    z = align(B * LDH * 8);
+    gpart = align(z + St * 33 * 8);  // v_K rows + status slots, as in the workspace
+    total = gpart + (kBlkMaxW + 2) * 16 * 4;
+  }
+};
+
+__global__ void __launch_bounds__(256, 2) precode_q_kernel(const KernelParams p) {
+  constexpr int UP = 32, NQ = 16, LDH = PrecodeQSmem::LDH;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nt = blockDim.x, nw = nt >> 5;
+  const int St = p.St, B = p.B;
+  WsOffsets W;
+  W.plan(UP, p.S, p.K, p.exact != 0, p.fx != 0, p.zs);
+  PrecodeQSmem L;
+  L.plan(B, St);
+  float* gpart = reinterpret_cast<float*>(smem + L.gpart);
+  float* ginv = gpart + kBlkMaxW * NQ;  // [NQ] inverse gains, [NQ] flags
+  const bool okb = tid < B;
+  const long lsc = blockIdx.x;
+  const long sc = p.sc_base + lsc;
+  {
+    const float2* hsrc = p.H + sc * static_cast<long>(B) * UP;
+    float2* hdst = reinterpret_cast<float2*>(smem + L.h);
+    for (int j = tid; j < B * (UP / 2); j += nt) {  // 16 B chunks, coalesced reads
+      const int row = j >> 4, ch = j & 15;
+      cp_async16(hdst + row * LDH + 2 * ch, hsrc + row * UP + 2 * ch);
+    }
+    const float2* zsrc = p.ws + lsc * W.stride + W.z;
+    float2* zdst = reinterpret_cast<float2*>(smem + L.z);
+    const int zch = (St * (UP + 1) + 1) / 2;
+    for (int j = tid; j < zch; j += nt) cp_async16(zdst + 2 * j, zsrc + 2 * j);
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
+  __syncthreads();
+  const float2* hrow = reinterpret_cast<const float2*>(smem + L.h) + (okb ? tid : 0) * LDH;
+  const float2* Zs = reinterpret_cast<const float2*>(smem + L.z);
+  for (int t0 = 0; t0 < St; t0 += NQ) {
+    const int nq = St - t0 < NQ ? St - t0 : NQ;
+    unsigned long long qa[NQ], qb[NQ];
+#pragma unroll
+    for (int t = 0; t < NQ; ++t) qa[t] = qb[t] = 0ull;
+#pragma unroll 2
+    for (int u = 0; u < UP; u += 2) {
+      const ulonglong2 h = *reinterpret_cast<const ulonglong2*>(hrow + u);
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        if (t < nq) {
+          const ulonglong2 vv = *reinterpret_cast<const ulonglong2*>(Zs + (t0 + t) * UP + u);
+          ffma2(qa[t], h.x, f2dup_lo(vv.x));
+          ffma2(qb[t], h.x, f2dup_hi(vv.x));
+          ffma2(qa[t], h.y, f2dup_lo(vv.y));
+          ffma2(qb[t], h.y, f2dup_hi(vv.y));
+        }
+      }
+    }
+    float2 q[NQ];
+    float nrm[NQ];
+#pragma unroll
+    for (int t = 0; t < NQ; ++t) {
+      const float2 A = f2unpack(qa[t]), Bq = f2unpack(qb[t]);
+      q[t] = make_float2(A.x - Bq.y, A.y + Bq.x);
+      nrm[t] = okb ? cnorm(q[t]) : 0.f;
+    }
+    // per-warp sums of the 16 norms (4 x warp_sum4); thread t < 16 sums
+    // vector t over the warps in a fixed order and publishes 1 / gain
+#pragma unroll
+    for (int g = 0; g < NQ; g += 4) {
+      float x4[4] = {nrm[g], nrm[g + 1], nrm[g + 2], nrm[g + 3]};
+      warp_sum4(x4);
+      if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) gpart[warp * NQ + g + k] = x4[k];
+    }
+    __syncthreads();
+    if (tid < nq) {
+      const int ts = t0 + tid;
+      float n2 = 0.f;
+      for (int w = 0; w < nw; ++w) n2 += gpart[w * NQ + tid];  // fixed order
+      const bool ok = Zs[St * UP + ts].x == 0.f;
+      const float g = sqrtf(n2);
+      const bool zero = ok && !(g > 0.f);
+      ginv[tid] = (ok && !zero) ? 1.f / g : 0.f;
+      ginv[NQ + tid] = ok ? 1.f : 0.f;
+      if (p.gain) p.gain[sc * St + ts] = (ok && !zero) ? g : 0.f;
+      if (p.pstatus) p.pstatus[sc * St + ts] = ok ? (zero ? 2 : 0) : 1;
+    }
+    __syncthreads();
+    if (okb) {
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        if (t < nq) {
+          const int ts = t0 + t;
+          const float inv = ginv[t];
+          const bool ok = ginv[NQ + t] != 0.f;
+          const long ob = (sc * St + ts) * static_cast<long>(B) + tid;
+          if (p.q) p.q[ob] = ok ? q[t] : make_float2(0.f, 0.f);
+          if (p.s_out) p.s_out[ob] = cscale(inv, q[t]);
+        }
+      }
+    }
+    __syncthreads();  // gpart / ginv reused by the next pass
+  }
+}
+
+}  // namespace cgm

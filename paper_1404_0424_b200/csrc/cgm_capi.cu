@@ -18,6 +18,7 @@
 
 #include "../../include/cgmimo_b200.h"
 #include "cgm_alt.cuh"
+#include "cgm_block32.cuh"
 #include "cgm_moments.cuh"
 #include "cgm_precode_small.cuh"
 #include "cgm_uplink_small.cuh"
@@ -42,7 +43,7 @@ struct cgm_ctx {
   long launches = 0;
   int policy = 0;  // kernel-variant switches (kPol*), 0 = production defaults
   int host_chunks = 0;  // CGMIMO_HOST_CHUNKS, read once at context creation
-  size_t chunk_bytes = 80ull << 20;  // split-path chunk budget (CGMIMO_CHUNK_MB)
+  size_t chunk_bytes = 512ull << 20;  // split-path chunk budget (CGMIMO_CHUNK_MB)
   // optional per-kernel event timing (bench roofline): pairs of events per launch
   int profiling = 0;
   cudaEvent_t order_ev = nullptr;  // host pipeline: ordered after the context stream's work
@@ -158,6 +159,8 @@ int up_of(int U) { return U <= 8 ? 8 : U <= 16 ? 16 : U <= 32 ? 32 : 64; }
 constexpr int kPolFfmaChannel = 1;  // U = 32: FFMA channel kernel instead of tcgen05
 constexpr int kPolSplitSmall = 2;   // U <= 16: channel + solve pair instead of the fused kernels
 constexpr int kPolLaneSolve = 4;    // U = 32: lane-per-row solve kernel instead of the row kernels
+constexpr int kPolBlockUp = 8;      // U = 32 uplink only: the shared-G block kernel instead of pairs
+constexpr int kPolRowsCta = 16;     // U = 32 with transmit vectors: the 8-warp row CTA instead of block
 
 // Device workspace of the split path.  A call captured into a CUDA graph
 // bakes in this pointer, so a larger call never frees it: the old buffer
@@ -293,10 +296,25 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
                 L2.total, ctx->max_smem);
   void (*k2)(cgm::KernelParams) = cgm::solve_kernel<UP, EXACT>;
   int smem2 = L2.total;
-  enum { kLanes, kLanesPf, kPairs, kRowsCta } mode = kLanes;
+  enum { kLanes, kLanesPf, kPairs, kRowsCta, kBlock } mode = kLanes;
   int pair_ns = 2;
   if constexpr (UP == 32) {
-    if (!(ctx->policy & kPolLaneSolve)) {
+    // persistent shared-G block kernel (+ precode_q_kernel for transmit
+    // vectors): its bulk copies need 16-byte aligned T rows and H rows
+    cgm::WsOffsets WB;
+    WB.plan(UP, p.S, p.K, EXACT, p.fx, p.St);
+    cgm::Block32Smem BL;
+    BL.plan(p.S, p.St, Kmax, EXACT, WB.z * 8);
+    const uintptr_t alt = reinterpret_cast<uintptr_t>(p.T) | reinterpret_cast<uintptr_t>(p.H);
+    const bool block_ok = BL.total <= ctx->max_smem && p.U == 32 && !p.hd_layout && !p.fx &&
+                          (p.St == 0 || (p.B <= 256 && (alt & 15u) == 0));
+    if (!(ctx->policy & kPolLaneSolve) && block_ok &&
+        (p.St > 0 ? !(ctx->policy & kPolRowsCta) : (ctx->policy & kPolBlockUp) != 0)) {
+      mode = kBlock;
+      k2 = cgm::block32_kernel<EXACT>;
+      smem2 = BL.total;
+      p.zs = p.St;  // the transmit vectors' v_K go through the workspace
+    } else if (!(ctx->policy & kPolLaneSolve)) {
       if (p.St == 0) {
         mode = kPairs;
         pair_ns = p.S == 1 ? 1 : 2;
@@ -332,7 +350,21 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   if (EXACT) nw2 = std::max(nw2, std::max(4, UP / 32));
   nw2 = std::max(1, std::min(8, nw2));
   if (mode == kRowsCta) nw2 = nsys >= 16 ? 8 : 2;
+  if (mode == kBlock)  // NS systems per warp
+    nw2 = std::min(cgm::kBlkMaxW, (nsys + cgm::kBlkNS - 1) / cgm::kBlkNS);
   long g2cap = 1L << 40;
+  if (mode == kBlock) {  // persistent
+    int occ2 = 0;
+    CGM_PREP(ctx, k2, 32 * nw2, smem2, &occ2);
+    g2cap = static_cast<long>(std::max(occ2, 1)) * ctx->sms;
+    if (p.St > 0) {
+      cgm::PrecodeQSmem PQ;
+      PQ.plan(p.B, p.St);
+      if (PQ.total > ctx->max_smem)
+        return fail(ctx, CGM_EINVAL, "precoder: %d B of shared memory exceed %d", PQ.total, ctx->max_smem);
+      CGM_PREP(ctx, cgm::precode_q_kernel, 256, PQ.total, nullptr);
+    }
+  }
   if (mode == kLanesPf) {
     int occ2 = 0;
     CGM_PREP(ctx, k2, 32 * nw2, smem2, &occ2);
@@ -340,7 +372,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   }
   // --------------------------------------------------------------- chunks
   cgm::WsOffsets W;
-  W.plan(UP, p.S, p.K, EXACT, p.fx);
+  W.plan(UP, p.S, p.K, EXACT, p.fx, p.zs);
   const size_t per_sc = static_cast<size_t>(W.stride) * 8 + static_cast<size_t>(p.B) * p.U * 8 +
                         static_cast<size_t>(p.B) * p.S * 8;
   long chunk = static_cast<long>(ctx->chunk_bytes / std::max<size_t>(per_sc, 1));
@@ -370,6 +402,14 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
         k2<<<static_cast<unsigned>(std::min(n, g2cap)), 32 * nw2, smem2, st>>>(q);
     });
     if (r) return r;
+    if (mode == kBlock && p.St > 0) {  // q = H_d^H v, gain, s
+      cgm::PrecodeQSmem PQ;
+      PQ.plan(p.B, p.St);
+      r = timed(ctx, st, 2, [&] {
+        cgm::precode_q_kernel<<<static_cast<unsigned>(n), (p.B + 31) / 32 * 32, PQ.total, st>>>(q);
+      });
+      if (r) return r;
+    }
     if (km && p.fx && (r = moments())) return r;
   }
   return CGM_OK;
@@ -807,7 +847,8 @@ int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, lon
 }
 
 int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy) {
-  if (!ctx || policy < 0 || policy > (kPolFfmaChannel | kPolSplitSmall | kPolLaneSolve))
+  if (!ctx || policy < 0 ||
+      policy > (kPolFfmaChannel | kPolSplitSmall | kPolLaneSolve | kPolBlockUp | kPolRowsCta))
     return fail(ctx, CGM_EINVAL, "unknown kernel policy %d", policy);
   ctx->policy = policy;
   return CGM_OK;

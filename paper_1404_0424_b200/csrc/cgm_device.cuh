@@ -144,6 +144,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// 16-byte asynchronous global->shared copy (cp.async, L2-only), grouped by
+// commit / wait_group: lets every thread place chunks at padded addresses
+// (bank-conflict-free row strides) that one bulk copy cannot produce.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // Order prior generic-proxy smem accesses before later async-proxy writes
 // into the same buffer (buffer reuse across subcarriers).
 __device__ __forceinline__ void fence_proxy_async() {

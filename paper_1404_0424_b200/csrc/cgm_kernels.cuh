@@ -32,6 +32,7 @@ struct KernelParams {
   int use_tma;    // bulk-copy staging (U == UP, B even, 16B aligned)
   int exact;      // uplink systems use the exact tracker (the workspace carries the row moments)
   int fx;         // exact, one vector per subcarrier: the CG runs before moments_kernel<..., FX>
+  int zs;         // transmit-vector slots in the workspace (separate precoder kernel), else 0
   float rho_inv_u, rho_inv_d, n0, es;
   float2* ws;     // split path: per-subcarrier workspace (G, MF, (c, d), row moments)
   long sc_base;   // split path: first subcarrier of this chunk

@@ -51,15 +51,20 @@ namespace cgm {
 // and for the exact tracker the row-moment table D_k[i] (double, k = 0..2K)
 // fx (exact, one vector per subcarrier): instead of the moment table, the
 // CG's (alpha, beta) history (K float2), v_K (UP float2) and the breakdown
-// flag (1 float2) for moments_kernel<..., FX>
+// flag (1 float2) for moments_kernel<..., FX>.  zs (St > 0 and a separate
+// precoder kernel, precode_q_kernel): each transmit vector's v_K (UP float2)
+// and its breakdown flag (one float2 per vector after the St rows).  The
+// span [g, z) is contiguous for one bulk copy.
 struct WsOffsets {
-  int g, mf, cd, t, stride;
-  __host__ __device__ void plan(int UP, int S, int K, bool exact, bool fx = false) {
+  int g, mf, cd, t, z, stride;
+  __host__ __device__ void plan(int UP, int S, int K, bool exact, bool fx = false, int zs = 0) {
     g = 0;
     mf = UP * UP;
     cd = mf + S * UP;
     t = cd + 2;
-    stride = t + (exact ? (fx ? K + UP + 1 : (2 * K + 1) * UP) : 0);
+    z = t + (exact ? (fx ? K + UP + 1 : (2 * K + 1) * UP) : 0);
+    z = (z + 1) & ~1;
+    stride = z + zs * (UP + 1);
     stride = (stride + 1) & ~1;
   }
 };
@@ -76,8 +81,15 @@ struct MomGeo {
   static constexpr int NT = ((SPC * NTILE + 31) / 32) * 32 < 64 ? 64 : ((SPC * NTILE + 31) / 32) * 32;
   static constexpr int LD = UP + 2;                 // padded row (bank spread, 16 B aligned)
   static constexpr int MAT = UP * LD;               // complex entries per matrix
+  static constexpr int PART = 4 * UP * NB;          // row / column partial slots (in R), 2 sums each
+  // per subcarrier: Ahat and the current T_a (the previous T_{a-1} stays in
+  // the tile threads' registers), plus the partial slots
   template <class R>
-  static constexpr int smem() { return SPC * 3 * MAT * 2 * static_cast<int>(sizeof(R)); }
+  __host__ __device__ static constexpr int slot_bytes() {
+    return 2 * MAT * 2 * static_cast<int>(sizeof(R)) + PART * static_cast<int>(sizeof(R));
+  }
+  template <class R>
+  __host__ __device__ static constexpr int smem() { return SPC * slot_bytes<R>(); }
 };
 
 template <class R>
@@ -170,6 +182,12 @@ __device__ __forceinline__ void tile_prod(const double2* A, const double2* T, in
 //     U^3 work is unavoidable, and the entrywise sums keep FP32 accurate to
 //     K = 16 (the moment table's quadratic forms need FP64 products from
 //     K = 7 on).
+// Only Ahat and the current T_a live in shared memory: each tile thread
+// keeps its own entries of T_{a-1} in registers (the recursion's "prev"
+// term only needs the thread's own tile), and the row sums behind D_k come
+// from the tiles too -- per lower entry, |T_{a+1}|^2 and Re T_{a+1} conj(T_a)
+// count for row i and (mirror, i != j) for row j -- through fixed slots
+// summed in a fixed order, so no separate row pass serialises the CTA.
 template <int UP, class R, bool FX = false>
 __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelParams p) {
   using MG = MomGeo<UP>;
@@ -177,33 +195,37 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
   static_assert(!FX || std::is_same<R, float>::value, "FX runs in FP32");
   constexpr int MAT = MG::MAT, SPC = MG::SPC, LD = MG::LD, NT = MG::NT, NB = MG::NB;
   extern __shared__ __align__(128) unsigned char smem[];
-  C* base = reinterpret_cast<C*>(smem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int K = p.K;
   WsOffsets W;
-  W.plan(UP, p.S, K, true, FX);
+  W.plan(UP, p.S, K, true, FX, p.zs);
   const long sc0 = static_cast<long>(blockIdx.x) * SPC;
   const int nsc = static_cast<int>(p.n_sc - sc0 < SPC ? p.n_sc - sc0 : SPC);
-  // buffer b of subcarrier s: 0 = Ahat (T_1), 1 / 2 = the recursion window
-  auto buf = [&](int s, int b) { return base + (s * 3 + b) * MAT; };
-  // G -> buffer 1 as float2 (the power iteration's input; for R = double the
-  // float copy occupies the first half of the buffer)
+  auto slotp = [&](int s) { return smem + s * MG::template slot_bytes<R>(); };
+  auto Abuf = [&](int s) { return reinterpret_cast<C*>(slotp(s)); };            // Ahat
+  auto Tbuf = [&](int s) { return reinterpret_cast<C*>(slotp(s)) + MAT; };      // T_a
+  // partial row sums in R: FP64 products need FP64 sums (K > 6)
+  auto Part = [&](int s) { return reinterpret_cast<R*>(slotp(s) + 2 * MAT * sizeof(C)); };
+  // G -> the T buffer as padded float2 rows (16-byte cp.async chunks,
+  // coalesced reads); the power iteration reads it there
   for (int s = 0; s < nsc; ++s) {
-    const float4* src = reinterpret_cast<const float4*>(p.ws + (sc0 + s) * W.stride + W.g);
-    float2* dst = reinterpret_cast<float2*>(buf(s, 1));
+    const float2* src = p.ws + (sc0 + s) * W.stride + W.g;
+    float2* dst = reinterpret_cast<float2*>(Tbuf(s));
     for (int e = tid; e < UP * UP / 2; e += NT) {
       const int r = e / (UP / 2), c2 = e - r * (UP / 2);
-      *reinterpret_cast<float4*>(dst + r * LD + 2 * c2) = src[e];
+      cp_async16(dst + r * LD + 2 * c2, src + 2 * e);
     }
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   __shared__ float2 cds[SPC];
   // FX: the Chebyshev coefficients of L_K and B per subcarrier (cl, cb)
   __shared__ float coefs[FX ? SPC : 1][2][kMaxK + 2];
   for (int s = warp; s < nsc; s += NT / 32) {
-    // power-iteration scratch: buffer 2 (as float2)
-    const float2 cd = cheb_interval<UP, LD>(reinterpret_cast<const float2*>(buf(s, 1)),
-                                            p.rho_inv_u, reinterpret_cast<float2*>(buf(s, 2)), lane);
+    // power-iteration scratch: the A buffer (as float2)
+    const float2 cd = cheb_interval<UP, LD>(reinterpret_cast<const float2*>(Tbuf(s)),
+                                            p.rho_inv_u, reinterpret_cast<float2*>(Abuf(s)), lane);
     if (lane == 0) {
       cds[s] = cd;
       p.ws[(sc0 + s) * W.stride + W.cd] = cd;
@@ -215,10 +237,10 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
     }
   }
   __syncthreads();
-  // Ahat = (A - cI)/d = (G + (rho^-1 - c) I) / d -> buffer 0 (in R)
+  // Ahat = (A - cI)/d = (G + (rho^-1 - c) I) / d -> A buffer (in R)
   for (int e = tid; e < nsc * UP * UP; e += NT) {
     const int s = e / (UP * UP), r = (e / UP) % UP, c = e % UP;
-    const float2 g = reinterpret_cast<const float2*>(buf(s, 1))[r * LD + c];
+    const float2 g = reinterpret_cast<const float2*>(Tbuf(s))[r * LD + c];
     const R cc = cds[s].x, invd = R(1) / static_cast<R>(cds[s].y);
     R x = g.x, y = g.y;
     if (r == c) {
@@ -228,39 +250,10 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
     C v;
     v.x = x * invd;
     v.y = y * invd;
-    buf(s, 0)[r * LD + c] = v;
+    Abuf(s)[r * LD + c] = v;
   }
   __syncthreads();
-  // row moments (FX = false): thread <-> (subcarrier, row i); column reads
-  // are conflict-free and T[j][i] = conj(T[i][j]) gives the same sums
-  auto row_moments = [&](int a, int cur, int prv) {
-    // D_{2a} from T_a (buffer cur), D_{2a-1} from T_a and T_{a-1} (buffer prv, -1: I)
-    for (int e = tid; e < nsc * UP; e += NT) {
-      const int s = e / UP, i = e - s * UP;
-      const C* Ta = buf(s, cur);
-      double n2 = 0.0, x = 0.0;
-      for (int j = 0; j < UP; ++j) {
-        const C t = Ta[j * LD + i];
-        const double tx = t.x, ty = t.y;
-        n2 = __fma_rn(tx, tx, __fma_rn(ty, ty, n2));
-        if (prv >= 0) {
-          const C q = buf(s, prv)[j * LD + i];
-          x = __fma_rn(tx, static_cast<double>(q.x), __fma_rn(ty, static_cast<double>(q.y), x));
-        }
-      }
-      double* mom = reinterpret_cast<double*>(p.ws + (sc0 + s) * W.stride + W.t);
-      const double d1 = static_cast<double>(buf(s, 0)[i * LD + i].x);
-      if (a == 1) {
-        mom[i] = 1.0;
-        mom[UP + i] = d1;
-      } else {
-        mom[(2 * a - 1) * UP + i] = 2.0 * x - d1;
-      }
-      mom[2 * a * UP + i] = 2.0 * n2 - 1.0;
-    }
-  };
-  if (!FX) row_moments(1, 0, -1);
-  // products: thread <-> (subcarrier slot, lower tile)
+  // thread <-> (subcarrier slot, lower tile)
   const int slot = tid / MG::NTILE;
   const int tile = tid - slot * MG::NTILE;
   int rb = 0;
@@ -268,86 +261,163 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
   const int cb = tile - rb * (rb + 1) / 2;
   const bool busy = slot < nsc;
   const int i0 = rb * 4, j0 = cb * 4;
-  // FX: this tile's entries of B = sum_m cb_m T_m and L = sum_{m<K} cl_m T_m
-  float2 Bacc[FX ? 4 : 1][FX ? 4 : 1], Lacc[FX ? 4 : 1][FX ? 4 : 1];
-  if constexpr (FX) {
-    const float* cl = coefs[busy ? slot : 0][0];
-    const float* cbq = coefs[busy ? slot : 0][1];
-    const C* A = buf(busy ? slot : 0, 0);
+  const int ss = busy ? slot : 0;
+  // this tile's entries of T_{a-1} (prv) stay in registers; T_0 = I
+  C prv[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      prv[r][c].x = (i0 + r == j0 + c) ? R(1) : R(0);
+      prv[r][c].y = R(0);
+    }
+  auto load_tile = [&](const C* M, C (&t)[4][4]) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) t[r][c] = M[(i0 + r) * LD + j0 + c];
+  };
+  double* mom = reinterpret_cast<double*>(p.ws + (sc0 + ss) * W.stride + W.t);
+  // row / column partials of the tile's lower entries: [row][NB][2]
+  auto partials = [&](const C (&nw)[4][4], const C (&ol)[4][4], bool cross) {
+    R* Rp = Part(ss);
+    R* Cp = Rp + 2 * UP * NB;
+    R rn[4] = {0, 0, 0, 0}, rx[4] = {0, 0, 0, 0};
+    R cn[4] = {0, 0, 0, 0}, cx[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int i = i0 + r, j = j0 + c;
-        const float2 t1 = busy ? A[i * LD + j] : make_float2(0.f, 0.f);  // T_1
-        const float d0 = i == j ? 1.f : 0.f;                             // T_0 = I
+        if (j > i) continue;
+        const R n2 = nw[r][c].x * nw[r][c].x + nw[r][c].y * nw[r][c].y;
+        const R x2 = cross ? nw[r][c].x * ol[r][c].x + nw[r][c].y * ol[r][c].y : R(0);
+        rn[r] += n2; rx[r] += x2;
+        if (i != j) { cn[c] += n2; cx[c] += x2; }
+      }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      Rp[((i0 + r) * NB + cb) * 2 + 0] = rn[r];
+      Rp[((i0 + r) * NB + cb) * 2 + 1] = rx[r];
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      Cp[((j0 + c) * NB + rb) * 2 + 0] = cn[c];
+      Cp[((j0 + c) * NB + rb) * 2 + 1] = cx[c];
+    }
+  };
+  // fixed-order row sums of the partials -> D_{2a-1}, D_{2a} (thread = row)
+  auto row_sums = [&](int a) {
+    for (int e = tid; e < nsc * UP; e += NT) {
+      const int s = e / UP, i = e - s * UP;
+      const R* Rp = Part(s);
+      const R* Cp = Rp + 2 * UP * NB;
+      const int rbi = i / 4;
+      double n2 = 0.0, x2 = 0.0;
+      for (int q = 0; q <= rbi; ++q) { n2 += Rp[(i * NB + q) * 2]; x2 += Rp[(i * NB + q) * 2 + 1]; }
+      for (int q = rbi; q < NB; ++q) { n2 += Cp[(i * NB + q) * 2]; x2 += Cp[(i * NB + q) * 2 + 1]; }
+      double* m = reinterpret_cast<double*>(p.ws + (sc0 + s) * W.stride + W.t);
+      const double d1 = static_cast<double>(Abuf(s)[i * LD + i].x);
+      if (a == 1) {
+        m[i] = 1.0;
+        m[UP + i] = d1;
+      } else {
+        m[(2 * a - 1) * UP + i] = 2.0 * x2 - d1;
+      }
+      m[2 * a * UP + i] = 2.0 * n2 - 1.0;
+    }
+  };
+  (void)mom;
+  // FX: this tile's entries of B = sum_m cb_m T_m and L = sum_{m<K} cl_m T_m
+  float2 Bacc[FX ? 4 : 1][FX ? 4 : 1], Lacc[FX ? 4 : 1][FX ? 4 : 1];
+  if constexpr (FX) {
+    const float* cl = coefs[ss][0];
+    const float* cbq = coefs[ss][1];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const C a1 = Abuf(ss)[(i0 + r) * LD + j0 + c];
+        const float2 t1 = make_float2(a1.x, a1.y);  // T_1
+        const float d0 = (i0 + r == j0 + c) ? 1.f : 0.f;           // T_0 = I
         Bacc[r][c] = make_float2(cbq[0] * d0 + cbq[1] * t1.x, cbq[1] * t1.y);
         Lacc[r][c] = K > 1 ? make_float2(cl[0] * d0 + cl[1] * t1.x, cl[1] * t1.y)
                            : make_float2(cl[0] * d0, 0.f);
       }
+  } else {
+    if (busy) {  // D_2 from T_1 = Ahat
+      C t1[4][4];
+      load_tile(Abuf(ss), t1);
+      partials(t1, prv, false);
+    }
+    __syncthreads();
+    row_sums(1);
   }
-  // T_a in buffer cur, T_{a-1} in buffer prv (-1: the identity), T_{a+1}
-  // written over T_{a-1} (buffer 1 / 2; never over Ahat)
-  int cur = 0, prv = -1;
   for (int a = 1; a < K; ++a) {
-    const int out = a == 1 ? 1 : a == 2 ? 2 : prv;
+    // T_{a+1} = 2 Ahat T_a - T_{a-1}; T_a is Ahat itself for a = 1
+    C nx[4][4];
     if (busy) {
       C acc[4][4];
-      tile_prod<UP>(buf(slot, 0), buf(slot, cur), i0, j0, acc);
-      C* Tn = buf(slot, out);
-      const C* Tp = prv >= 0 ? buf(slot, prv) : nullptr;
+      tile_prod<UP>(Abuf(slot), a == 1 ? Abuf(slot) : Tbuf(slot), i0, j0, acc);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int i = i0 + r, j = j0 + c;
+          nx[r][c].x = R(2) * acc[r][c].x - prv[r][c].x;
+          nx[r][c].y = i == j ? R(0) : R(2) * acc[r][c].y - prv[r][c].y;
+        }
+    }
+    __syncthreads();  // every thread's reads of T_a are done: overwrite it with T_{a+1}
+    if (busy) {
+      C* Tn = Tbuf(slot);
+      C cur[4][4];  // this tile's T_a, the next step's T_{a-1}
+      load_tile(a == 1 ? Abuf(slot) : Tn, cur);
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int i = i0 + r, j = j0 + c;
           if (j > i) continue;
-          C prev;
-          if (Tp) prev = Tp[i * LD + j];
-          else { prev.x = i == j ? R(1) : R(0); prev.y = R(0); }
-          C val;
-          val.x = R(2) * acc[r][c].x - prev.x;
-          val.y = i == j ? R(0) : R(2) * acc[r][c].y - prev.y;
-          Tn[i * LD + j] = val;
+          Tn[i * LD + j] = nx[r][c];
           if (i != j) {
             C cv;
-            cv.x = val.x;
-            cv.y = -val.y;
+            cv.x = nx[r][c].x;
+            cv.y = -nx[r][c].y;
             Tn[j * LD + i] = cv;
           }
           if constexpr (FX) {  // T_{a+1} into this tile's B and L
             const float cbm = coefs[slot][1][a + 1];
-            Bacc[r][c].x = fmaf(cbm, val.x, Bacc[r][c].x);
-            Bacc[r][c].y = fmaf(cbm, val.y, Bacc[r][c].y);
+            Bacc[r][c].x = fmaf(cbm, nx[r][c].x, Bacc[r][c].x);
+            Bacc[r][c].y = fmaf(cbm, nx[r][c].y, Bacc[r][c].y);
             if (a + 1 < K) {
               const float clm = coefs[slot][0][a + 1];
-              Lacc[r][c].x = fmaf(clm, val.x, Lacc[r][c].x);
-              Lacc[r][c].y = fmaf(clm, val.y, Lacc[r][c].y);
+              Lacc[r][c].x = fmaf(clm, nx[r][c].x, Lacc[r][c].x);
+              Lacc[r][c].y = fmaf(clm, nx[r][c].y, Lacc[r][c].y);
             }
           }
         }
+      if (!FX) partials(nx, cur, true);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) prv[r][c] = cur[r][c];
     }
-    __syncthreads();
+    __syncthreads();  // T_{a+1} complete (and the partials)
     if (!FX) {
-      row_moments(a + 1, out, cur);
-      __syncthreads();  // the row pass read T_a before the next product overwrites T_{a-1}
+      row_sums(a + 1);
+      __syncthreads();  // the partial slots are reused by the next step
     }
-    prv = cur;
-    cur = out;
   }
   if constexpr (FX) {
     // ---------------- extraction (detect.cpp:375-395) from the tile sums:
     // per lower entry (i, j): |B_ij|^2 and Re(B_ij conj(L_ij)) count for row
     // i and (i != j, Hermitian) for row j; mu_i = Re B_ii.  Row parts go to
     // Rb[i][cb], column parts to Cb[j][rb] (each slot written by one tile),
-    // summed in a fixed order.  They alias window buffer 1 or 2 -- whichever
-    // does not hold T_K, read by no one now (all products ended at the
-    // barrier above).
-    const int pb = cur == 1 ? 2 : 1;
-    float* Rb = reinterpret_cast<float*>(buf(busy ? slot : 0, pb));  // [UP][NB][2]
-    float* Cb = Rb + UP * NB * 2;                                    // [UP][NB][2]
-    float* Mb = Cb + UP * NB * 2;                                    // [UP]
-    static_assert(4 * UP * (UP / 4) + UP <= 2 * UP * (UP + 2), "partials fit a T buffer");
+    // summed in a fixed order.
+    float* Rb = reinterpret_cast<float*>(Part(ss));  // [UP][NB][2]
+    float* Cb = Rb + 2 * UP * NB;                    // [UP][NB][2]
+    float* Mb = reinterpret_cast<float*>(Tbuf(ss));  // [UP] (T is dead now)
     if (busy) {
       float rr2[4] = {0.f, 0.f, 0.f, 0.f}, rrl[4] = {0.f, 0.f, 0.f, 0.f};
       float cc2[4] = {0.f, 0.f, 0.f, 0.f}, ccl[4] = {0.f, 0.f, 0.f, 0.f};
@@ -383,9 +453,9 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
     for (int e = tid; e < nsc * UP; e += NT) {
       const int s = e / UP, i = e - s * UP;
       if (i >= p.U) continue;
-      const float* Rr = reinterpret_cast<const float*>(buf(s, pb));
-      const float* Cc = Rr + UP * NB * 2;
-      const float* M = Cc + UP * NB * 2;
+      const float* Rr = reinterpret_cast<const float*>(Part(s));
+      const float* Cc = Rr + 2 * UP * NB;
+      const float* M = reinterpret_cast<const float*>(Tbuf(s));
       const int rbi = i / 4;
       float ib2 = 0.f, ibl = 0.f;
       for (int q = 0; q <= rbi; ++q) { ib2 += Rr[(i * NB + q) * 2]; ibl += Rr[(i * NB + q) * 2 + 1]; }
@@ -429,25 +499,26 @@ __device__ __forceinline__ MomCoef moments_coefs(const float* hist, int K, doubl
   };
   // detect.cpp:336-368 on the coefficients: L_1 = alpha_1 I, then the
   // three-term update with c1 = a_k (1 + b_{k-1}) / a_{k-1}, c2 = a_k b_{k-2} / a_{k-2}
-  double l0 = 0.0, l1 = 0.0, l2 = 0.0;
-  double a_m1 = 1.0, a_m2 = 1.0, b_m1 = 0.0, b_m2 = 0.0;
-  for (int k = 1; k <= K; ++k) {
-    const double a = hist[(k - 1) * 2 + 0];
-    const double bb = hist[(k - 1) * 2 + 1];
-    if (k == 1) {
-      l2 = l1;
-      l1 = l0;
-      l0 = m == 0 ? a : 0.0;
-    } else {
-      const double c1 = a * (1.0 + b_m1) / a_m1, c2 = a * b_m2 / a_m2;
-      const double d1 = l0 - l1;
-      const double t = mulA(d1);
-      const double nx = l0 + c1 * d1 - a * t - c2 * (l1 - l2);
-      l2 = l1;
-      l1 = l0;
-      l0 = m < n ? nx : 0.0;
-    }
-    a_m2 = a_m1; a_m1 = a; b_m2 = b_m1; b_m1 = bb;
+  // (a_0 = 1, b_0 = 0).  Lane k forms c1_k, c2_k (the FP64 divisions run in
+  // parallel, off the recursion's dependency chain), shuffled in below.
+  double c1v = 0.0, c2v = 0.0;
+  if (m >= 2 && m <= K) {
+    const double a = hist[(m - 1) * 2], am1 = hist[(m - 2) * 2], bm1 = hist[(m - 2) * 2 + 1];
+    const double am2 = m >= 3 ? static_cast<double>(hist[(m - 3) * 2]) : 1.0;
+    const double bm2 = m >= 3 ? static_cast<double>(hist[(m - 3) * 2 + 1]) : 0.0;
+    c1v = a * (1.0 + bm1) / am1;
+    c2v = a * bm2 / am2;
+  }
+  double l0 = m == 0 ? static_cast<double>(hist[0]) : 0.0, l1 = 0.0, l2 = 0.0;  // L_1 = alpha_1 I
+  for (int k = 2; k <= K; ++k) {
+    const double a = hist[(k - 1) * 2];
+    const double c1 = __shfl_sync(0xffffffffu, c1v, k), c2 = __shfl_sync(0xffffffffu, c2v, k);
+    const double d1 = l0 - l1;
+    const double t = mulA(d1);
+    const double nx = l0 + c1 * d1 - a * t - c2 * (l1 - l2);
+    l2 = l1;
+    l1 = l0;
+    l0 = m < n ? nx : 0.0;
   }
   const double gm = mulA(l0) - rho_inv * l0;  // B = L (A - rho^-1 I)
   double* gs = sh;           // [kMaxK + 2]

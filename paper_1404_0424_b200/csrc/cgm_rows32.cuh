@@ -46,9 +46,8 @@ __device__ __forceinline__ void warp_sum2(float& a, float& b) {
   float v = keep + __shfl_xor_sync(0xffffffffu, send, 16);
 #pragma unroll
   for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const float other = __shfl_xor_sync(0xffffffffu, v, 16);
-  a = hi ? other : v;
-  b = hi ? v : other;
+  a = __shfl_sync(0xffffffffu, v, 0);   // lanes < 16 hold sum(a)
+  b = __shfl_sync(0xffffffffu, v, 16);  // lanes >= 16 hold sum(b)
 }
 
 // CG for the systems base, base + 1 of subcarrier sc on one warp (lane =
@@ -246,7 +245,7 @@ __global__ void __launch_bounds__(256, 2) solve_rows32_kernel(const KernelParams
   K2Smem<UP> L;
   L.plan(B, S, St, Kmax, EXACT);
   WsOffsets W;
-  W.plan(UP, S, p.K, EXACT, p.fx);
+  W.plan(UP, S, p.K, EXACT, p.fx, p.zs);
   float2* Vs = reinterpret_cast<float2*>(smem + L.vs);
   float2* Qs = reinterpret_cast<float2*>(smem + L.qs);
   float* hist = reinterpret_cast<float*>(smem + L.hist);
@@ -310,7 +309,7 @@ __global__ void __launch_bounds__(128, NS == 1 ? 5 : 4) solve_rows32_pairs_kerne
   const int base = static_cast<int>(item - lsc * npairs) * NS;
   const long sc = p.sc_base + lsc;
   WsOffsets W;
-  W.plan(UP, S, K, EXACT, p.fx);
+  W.plan(UP, S, K, EXACT, p.fx, p.zs);
   const float2* ws = p.ws + lsc * W.stride;
   unsigned long long grow[UP];
 #pragma unroll

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(320, MINB) channel_kernel(const KernelParams p
   K1Smem<UP> L;
   L.plan(p.B, p.S, nstage);
   WsOffsets W;
-  W.plan(UP, p.S, p.K, EXACT, p.fx);
+  W.plan(UP, p.S, p.K, EXACT, p.fx, p.zs);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar);
   float2* Gs = reinterpret_cast<float2*>(smem + L.gs);
   const int nt = blockDim.x;
@@ -414,7 +414,7 @@ __device__ __forceinline__ void solve_sc(const KernelParams& p, long lsc, unsign
   K2Smem<UP> L;
   L.plan(B, S, St, Kmax, EXACT);
   WsOffsets W;
-  W.plan(UP, S, p.K, EXACT, p.fx);
+  W.plan(UP, S, p.K, EXACT, p.fx, p.zs);
   // G (and the matched filters) from the prefetched shared-memory copy of
   // the workspace when the persistent kernel staged one
   const float2* Gs = pre ? pre + W.g : reinterpret_cast<float2*>(smem + L.gs);
@@ -694,7 +694,7 @@ template <int UP, bool EXACT, int MINB = 3>
 __global__ void __launch_bounds__(256, MINB) solve_kernel_pf(const KernelParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   WsOffsets W;
-  W.plan(UP, p.S, p.K, EXACT, p.fx);
+  W.plan(UP, p.S, p.K, EXACT, p.fx, p.zs);
   const int pb = k2_pre_bytes(UP, p.S);
   const uint32_t bytes = static_cast<uint32_t>(W.cd * 8);  // G + MF
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);

@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
   tc::Smem L;
   L.plan(p.S, p.k1_pair, RING);
   WsOffsets W;
-  W.plan(UP, p.S, p.K, p.exact != 0, p.fx != 0);
+  W.plan(UP, p.S, p.K, p.exact != 0, p.fx != 0, p.zs);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int S = p.S, B = p.B, nkb = B / KB, nstg = L.nstg;
   const int ny = S > 0 ? ((2 * S + 7) & ~7) : 0;  // Y columns fed to the MMA (zero padded)

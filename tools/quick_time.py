@@ -4,6 +4,9 @@ import torch, numpy as np
 sys.path.insert(0, __import__('os').path.join(__import__('os').path.dirname(__file__), '..'))
 from paper_1404_0424_b200 import Context, get_config
 ctx = Context(0)
+import os as _os
+if _os.environ.get('POLICY'):
+    ctx.set_kernel_policy(_os.environ['POLICY'])
 def timeit(fn, reps=10, warm=3):
     for _ in range(warm): fn()
     torch.cuda.synchronize()

@@ -24,6 +24,8 @@ def main():
     if a.n_sc:
         cfg = cfg.scaled(a.n_sc)
     ctx = Context(0)
+    if os.environ.get('POLICY'):
+        ctx.set_kernel_policy(os.environ['POLICY'])
     rs = cfg.rsqrt()
     rs = None if rs is None else torch.tensor(rs)
     if cfg.kind == "downlink":
