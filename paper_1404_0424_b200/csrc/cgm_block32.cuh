@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(256, 2) block32_kernel(const KernelParams p) {
 // staged by coalesced 16-byte cp.async into rows padded to 34 complex
 // (272 B), so the 8 lanes of an LDS.128 phase hit 8 distinct bank groups;
 // v_K is a broadcast.  q_b = sum_u H_u[b][u] v_u (precode.cpp:69 with
-// H_d = H_u^H) for 16 vectors per pass on packed accumulators
+// H_d = H_u^H) for 8 vectors per pass on packed accumulators
 // (a += (h.x, h.y) v.x, b += (h.x, h.y) v.y, q = (a.x - b.y, a.y + b.x)),
 // gain = ||q|| by a fixed-order reduction, s = q / gain, zero_input when the
 // gain vanishes (precode.cpp:22-36).
@@ -323,8 +323,8 @@ struct PrecodeQSmem {
   }
 };
 
-__global__ void __launch_bounds__(256, 2) precode_q_kernel(const KernelParams p) {
-  constexpr int UP = 32, NQ = 16, LDH = PrecodeQSmem::LDH;
+__global__ void __launch_bounds__(256, 3) precode_q_kernel(const KernelParams p) {
+  constexpr int UP = 32, NQ = 8, LDH = PrecodeQSmem::LDH;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nt = blockDim.x, nw = nt >> 5;
   const int St = p.St, B = p.B;
@@ -381,8 +381,8 @@ __global__ void __launch_bounds__(256, 2) precode_q_kernel(const KernelParams p)
       q[t] = make_float2(A.x - Bq.y, A.y + Bq.x);
       nrm[t] = okb ? cnorm(q[t]) : 0.f;
     }
-    // per-warp sums of the 16 norms (4 x warp_sum4); thread t < 16 sums
-    // vector t over the warps in a fixed order and publishes 1 / gain
+    // per-warp sums of the NQ norms (warp_sum4); thread t < NQ sums vector t
+    // over the warps in a fixed order and publishes 1 / gain
 #pragma unroll
     for (int g = 0; g < NQ; g += 4) {
       float x4[4] = {nrm[g], nrm[g + 1], nrm[g + 2], nrm[g + 3]};
