@@ -43,7 +43,7 @@ struct cgm_ctx {
   long launches = 0;
   int policy = 0;  // kernel-variant switches (kPol*), 0 = production defaults
   int host_chunks = 0;  // CGMIMO_HOST_CHUNKS, read once at context creation
-  size_t chunk_bytes = 512ull << 20;  // split-path chunk budget (CGMIMO_CHUNK_MB)
+  size_t chunk_bytes = 1024ull << 20;  // split-path chunk budget (CGMIMO_CHUNK_MB)
   // optional per-kernel event timing (bench roofline): pairs of events per launch
   int profiling = 0;
   cudaEvent_t order_ev = nullptr;  // host pipeline: ordered after the context stream's work
