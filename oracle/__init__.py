@@ -36,6 +36,10 @@ def build(quiet: bool = True) -> None:
     targets = ["port"]
     if os.path.isdir(REF_SRC):
         targets.append("ref")
+        # the reference's sweep driver relinked against the product library
+        # (needs paper_1404_0424_b200/libcgmimo_b200.so built first)
+        if os.path.exists(os.path.join(_HERE, "..", "paper_1404_0424_b200", "libcgmimo_b200.so")):
+            targets.append("relink")
     out = subprocess.run(["make", "-C", _HERE, "-j8", *targets], capture_output=True, text=True)
     if out.returncode != 0:
         raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)

@@ -90,7 +90,7 @@ class Context:
         self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
 
     POLICY_FLAGS = {"ffma_channel": 1, "split_small": 2, "lane_solve": 4, "block_uplink": 8,
-                    "rows_cta": 16}
+                    "rows_cta": 16, "poison_ws": 32}
 
     def set_kernel_policy(self, policy: str):
         """Kernel-variant switches for A/B tests: "auto" (production defaults)
@@ -100,7 +100,8 @@ class Context:
         solve kernel instead of the U = 32 row kernels), "block_uplink" (the
         shared-G block kernel for U = 32 uplink-only calls instead of the pairs
         kernel), "rows_cta" (the 8-warp row CTA instead of the block kernel
-        for calls with transmit vectors)."""
+        for calls with transmit vectors), "poison_ws" (test only: NaN-fill the
+        workspace before every chunk)."""
         bits = 0
         if policy != "auto":
             for name in policy.split("+"):

@@ -161,6 +161,7 @@ constexpr int kPolSplitSmall = 2;   // U <= 16: channel + solve pair instead of 
 constexpr int kPolLaneSolve = 4;    // U = 32: lane-per-row solve kernel instead of the row kernels
 constexpr int kPolBlockUp = 8;      // U = 32 uplink only: the shared-G block kernel instead of pairs
 constexpr int kPolRowsCta = 16;     // U = 32 with transmit vectors: the 8-warp row CTA instead of block
+constexpr int kPolPoisonWs = 32;    // test only: fill the workspace with NaN before every chunk
 
 // Device workspace of the split path.  A call captured into a CUDA graph
 // bakes in this pointer, so a larger call never frees it: the old buffer
@@ -383,6 +384,10 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   p.ws = reinterpret_cast<float2*>(ctx->tscratch);
   for (long c0 = 0; c0 < p.n_sc; c0 += chunk) {
     const long n = std::min(chunk, p.n_sc - c0);
+    // poisoned workspace: a kernel reading workspace it did not write first
+    // turns its outputs into NaN (tests compare against an unpoisoned run)
+    if (ctx->policy & kPolPoisonWs)
+      CGM_CUDA(ctx, cudaMemsetAsync(ctx->tscratch, 0xFF, static_cast<size_t>(n) * W.stride * 8, st));
     cgm::KernelParams q = p;
     q.sc_base = c0;
     q.n_sc = n;
@@ -848,7 +853,8 @@ int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, lon
 
 int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy) {
   if (!ctx || policy < 0 ||
-      policy > (kPolFfmaChannel | kPolSplitSmall | kPolLaneSolve | kPolBlockUp | kPolRowsCta))
+      policy > (kPolFfmaChannel | kPolSplitSmall | kPolLaneSolve | kPolBlockUp | kPolRowsCta |
+                kPolPoisonWs))
     return fail(ctx, CGM_EINVAL, "unknown kernel policy %d", policy);
   ctx->policy = policy;
   return CGM_OK;

@@ -178,3 +178,27 @@ def test_dropin_other_solvers_on_gpu(dropin_exe, checker, tmp_path):
             assert_close(s, wp["s"][0, 0], f"dropin precode {m} s")
             assert_close(gain, wp["gain"][0, 0], f"dropin precode {m} gain")
     assert take(1, np.int32)[0] == 1
+
+
+RELINK = os.path.join(ROOT, "oracle", "_ref", "relink_sim")
+REFSIM = os.path.join(ROOT, "oracle", "_ref", "reference_sim")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tracker", ["1", "0"])
+def test_reference_sim_relinked_against_dropin(tracker):
+    """The reference's own caller, unmodified: sim.cpp's run_uplink_sweep /
+    run_downlink_sweep (equalize / run_precoder call detect::detect_cg and
+    precode::precode_cg per subcarrier, sim.cpp:120-145) compiled from the
+    reference sources and linked against libcgmimo_b200.so for every
+    detect:: / precode:: / constellation / opcount symbol (oracle/Makefile
+    `relink`), reproduces the block-error counts of the same driver linked
+    against the reference's own implementations, at every sweep point, for
+    the approximate (1) and exact (0) trackers."""
+    if not (os.path.exists(RELINK) and os.path.exists(REFSIM)):
+        pytest.skip("relinked reference driver not built (oracle/Makefile relink)")
+    want = subprocess.run([REFSIM, tracker], capture_output=True, text=True, timeout=600)
+    got = subprocess.run([RELINK, tracker], capture_output=True, text=True, timeout=600)
+    assert want.returncode == 0 and got.returncode == 0, (want.stderr, got.stderr)
+    assert got.stdout.split() == want.stdout.split(), (got.stdout, want.stdout)
+    assert len(got.stdout.splitlines()) == 4
