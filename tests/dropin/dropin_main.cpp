@@ -60,6 +60,27 @@ static int host_mode() {
     opcount::ScopedTally s(t);
     if (!opcount::counting_active()) return 14;
   }
+  {  // HermitianMatrix (reference linalg.hpp:42-65): packed lower triangle
+    HermitianMatrix h(3);
+    h.set(0, 0, cplx(2.0, 5.0));  // imaginary part dropped on the diagonal
+    h.set(1, 0, cplx(1.0, -0.5));
+    h.set(1, 1, 3.0);
+    h.set(2, 0, cplx(0.25, 0.75));
+    h.set(2, 1, cplx(-1.5, 2.0));
+    h.set(2, 2, 4.0);
+    const ComplexMatrix f = h.full();
+    std::printf("hermitian");
+    for (std::size_t i = 0; i < 3; ++i)
+      for (std::size_t j = 0; j < 3; ++j) std::printf(" %.17g %.17g", f(i, j).real(), f(i, j).imag());
+    std::printf(" %.17g %.17g\n", h.diag(0), h.real_diag()[2]);
+    bool threw = false;
+    try {
+      h.set(0, 1, 1.0);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    std::printf("hermitian_upper_set_throws %d\n", threw ? 1 : 0);
+  }
   std::printf("host ok\n");
   return 0;
 }

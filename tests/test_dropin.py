@@ -40,6 +40,15 @@ def test_dropin_host_behaviour(dropin_exe, oracle_port):
             pts = vals[0::2] + 1j * vals[1::2]
             want, _, _ = oracle_port.constellation(bits)
             assert np.array_equal(pts, want)
+    herm = [line for line in lines if line.startswith("hermitian ")][0].split()[1:]
+    v = np.array([float(x) for x in herm])
+    full = (v[0:18:2] + 1j * v[1:18:2]).reshape(3, 3)
+    want = np.array([[2, 1 + 0.5j, 0.25 - 0.75j], [1 - 0.5j, 3, -1.5 - 2j],
+                     [0.25 + 0.75j, -1.5 + 2j, 4]])
+    np.testing.assert_array_equal(full, want)  # exact conjugate mirror, real diagonal
+    assert np.array_equal(full, full.conj().T)
+    assert v[18] == 2.0 and v[19] == 4.0
+    assert "hermitian_upper_set_throws 1" in lines
     llrs = [np.array([float(x) for x in line.split()[1:]]) for line in lines if line.startswith("llr")]
     cases = [(0.9 + 0.9j, 1.0, 2.0, 4), (0.0 + 0.5j, 1.0, 2.0, 4), (0.9 + 0.9j, 1e-14, 10.0, 4),
              (0.3 - 1.1j, 0.8, 40.0, 6), (-0.2 + 0.05j, 1.2, -3.0, 6), (1.0 + 0.0j, 1.0, 1.5, 2)]
