@@ -1,27 +1,31 @@
-"""bench.py -- throughput of the B200 CG detection path on BASELINE's headline
-workload (configs[1] = cfg2: uplink 128x32, approximate SINR, K=4, 64-QAM,
-1200 subcarriers x 14 OFDM symbols = 16,800 vectors per step).
+"""bench.py -- throughput of the B200 CG detection + precoding path on
+BASELINE's multi-GPU workload (configs[4] = cfg5: B=256, U=32, correlated
+channel, exact SINR, K=4, 64-QAM, then CG precoding on the same channels;
+65,536 subcarriers x 16 symbols = 1,048,576 instances split over the GPUs).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg2]
+                    [--config cfg5]
 
-* a step = one pass of the fused kernel over one batch (16,800 vectors) with
-  inputs resident in HBM; steps rotate over R distinct frames whose inputs
-  total more than the 126 MB L2 (no L2 reuse between steps);
+* a step = one pass of the hot path (channel -> moments -> solve -> precoder
+  kernels, through the C ABI) over the rank's shard of the job with inputs
+  resident in HBM (6.4 GB of H + Y per GPU at N = 1, far above the 126 MB L2);
 * value = whole-job vectors/s (max device time over ranks, CUDA events on the
   launching stream); e2e = the same metric through the public host-buffer
-  API (pinned host H/Y in, LLR/xhat/mu/rho/status out, copies in the timed
-  region);
-* N > 1 (torchrun): every rank processes its own shard of subcarriers (weak
-  scaling, no data-path collective); the NCCL gather of LLRs to rank 0 is
-  timed separately and reported under "gather";
+  API (pinned host H/Y/T in, every output out, copies in the timed region);
+* N > 1 (torchrun): strong scaling, rank r takes shard_range(65536, r, N); no
+  data-path collective; the whole job with the chunked, overlapped gather of
+  LLRs + precoded vectors to rank 0 (cgm_gatherv, NCCL) is timed separately
+  and reported under "gather" with its NVLink roofline term;
+* other configs (--config cfg1..cfg4b) are weak-scaling parity/bench cases;
 * --impl reference: the unmodified reference (oracle/_ref, FP64 per-call
-  detect_cg over all host threads) on the same workload, rank 0 only.
+  detect_cg + precode_cg over all host threads) on a >= 10 s subsample of the
+  same workload and the same input values, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -170,6 +174,85 @@ def workload_config(cfg, frames=None, world=1):
         d["l2"] = (f"inputs larger than L2: steps rotate over {frames['n']} frame(s), "
                    f"{frames['bytes'] / 1e6:.0f} MB of H+Y per GPU in total (> 126 MB L2)")
     return d
+
+
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+
+
+def sharded_gather_pass(args, ctx, cfg_all, cfg, frame, rank, world, local_rank, barrier,
+                        max_over_ranks):
+    """cfg5 at N > 1, the whole job as north_star states it: each rank runs its
+    shard of subcarriers in chunks through the product C ABI and chunk c's
+    LLRs, precoded vectors q and s, gains and status bytes go to rank 0 by
+    cgm_gatherv (NCCL over NVLink) on a second stream while chunk c + 1 is
+    computed (parallel.ShardedPipeline).  Timed with CUDA events, max over
+    ranks; the gather term of the path roofline is the bytes that must reach
+    rank 0 over its NVLink at the measured per-direction bandwidth."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1404_0424_b200 import Context
+    from paper_1404_0424_b200.parallel import (Comm, NcclTransport, ShardedPipeline,
+                                               detect_precode_outputs)
+
+    uid = [Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm_ctx = Context(local_rank)
+    comm = Comm(comm_ctx, world, rank, uid[0])
+    spec = detect_precode_outputs(cfg_all)
+    n_chunks = args.gather_chunks
+    pipe = ShardedPipeline(cfg_all.n_sc, rank, world, spec, NcclTransport(comm),
+                           n_chunks=n_chunks, device=torch.device("cuda", local_rank))
+    H, Y, T = frame
+    S, U = cfg.S, cfg.U
+    dev = H.device
+    scratch = {"xhat": torch.empty((cfg.n_sc, S, U), dtype=torch.complex64, device=dev),
+               "mu": torch.empty((cfg.n_sc, S, U), dtype=torch.float32, device=dev),
+               "rho": torch.empty((cfg.n_sc, S, U), dtype=torch.float32, device=dev)}
+
+    def compute(a, b, views):
+        o = {k: v[a:b] for k, v in scratch.items()}
+        o.update(views)
+        ctx.detect_precode_cg(H[a:b], Y[a:b], cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                              cfg.tracker, T[a:b], cfg.rho_d, cfg.K, out=o)
+
+    def timed(gather, reps):
+        for _ in range(2):
+            pipe.run(compute, gather=gather)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st = torch.cuda.current_stream(dev)
+        e0.record(st)
+        for _ in range(reps):
+            pipe.run(compute, gather=gather)
+        e1.record(st)
+        torch.cuda.synchronize()
+        return max_over_ranks(e0.elapsed_time(e1) / reps)
+
+    reps = max(3, min(args.steps, 20))
+    ms_compute = timed(False, reps)
+    ms_total = timed(True, reps)
+    per_sc = sum(math.prod(s) * torch.empty((), dtype=d).element_size() for s, d in spec.values())
+    lo, hi = pipe.lo, pipe.hi
+    to_root = (cfg_all.n_sc - (hi - lo if rank == 0 else 0)) * per_sc
+    if rank != 0:
+        to_root = 0
+    t = torch.tensor([float(to_root)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    to_root = float(t.item())
+    comm.close()
+    gather_floor_ms = to_root / (NVLINK_GBS * 1e9) * 1e3
+    return {"what": ("chunked sharded job: LLRs, precoded vectors q and s, gains and status bytes "
+                     "of every rank to rank 0 by cgm_gatherv (NCCL over NVLink) on a second "
+                     "stream, overlapped with the next chunk's kernels"),
+            "outputs": sorted(spec), "chunks_per_rank": n_chunks,
+            "ms_compute_only": ms_compute, "ms_with_gather": ms_total,
+            "value_with_gather": cfg_all.vectors / (ms_total / 1e3),
+            "bytes_to_root": to_root,
+            "roofline": {"term": "bytes to rank 0 / measured NVLink peer bandwidth per direction",
+                         "nvlink_gbs": NVLINK_GBS, "gather_floor_ms": gather_floor_ms,
+                         "frac": gather_floor_ms / ms_total}}
 
 
 def ours_arm(args, rank, world, local_rank):
@@ -359,7 +442,10 @@ def ours_arm(args, rank, world, local_rank):
 
     # ---------------------------------------------------- gather (N > 1 only)
     gather = None
-    if world > 1 and "llr" in out:
+    if world > 1 and strong and cfg.kind == "both":
+        gather = sharded_gather_pass(args, ctx, cfg_all, cfg, frames[0], rank, world, local_rank,
+                                     barrier, max_over_ranks)
+    elif world > 1 and "llr" in out:
         from paper_1404_0424_b200.parallel import gather_to_root
 
         llr = out["llr"].reshape(-1)
@@ -517,6 +603,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg5")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--gather-chunks", type=int, default=4,
+                    help="N > 1, cfg5: chunks per rank of the overlapped output gather")
     ap.add_argument("--no-graphs", action="store_true",
                     help="time direct C-ABI calls instead of CUDA-graph replays of them")
     args = ap.parse_args()

@@ -227,6 +227,13 @@ int cgm_comm_create(cgm_ctx* ctx, int nranks, int rank, const unsigned char id[1
 int cgm_comm_destroy(cgm_comm* comm);
 int cgm_gather(cgm_ctx* ctx, cgm_comm* comm, const void* send, const size_t* counts, void* recv,
                int root);
+/* cgm_gatherv: like cgm_gather, but rank r's counts[r] bytes land at
+ * recv + displs[r] on the root (displs identical on every rank).  The
+ * chunked sharded pipeline uses it to drop chunk c of every rank's shard
+ * straight into its place in the whole-job output while chunk c + 1 is
+ * being computed (parallel.py ShardedPipeline). */
+int cgm_gatherv(cgm_ctx* ctx, cgm_comm* comm, const void* send, const size_t* counts,
+                const size_t* displs, void* recv, int root);
 
 #ifdef __cplusplus
 }

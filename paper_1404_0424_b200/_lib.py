@@ -69,6 +69,8 @@ SIGNATURES = {
     "cgm_comm_create": (_int, [_vp, _int, _int, C.c_char_p, C.POINTER(_vp)]),
     "cgm_comm_destroy": (_int, [_vp]),
     "cgm_gather": (_int, [_vp, _vp, _vp, C.POINTER(C.c_size_t), _vp, _int]),
+    "cgm_gatherv": (_int, [_vp, _vp, _vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), _vp,
+                           _int]),
 }
 
 _lib = None

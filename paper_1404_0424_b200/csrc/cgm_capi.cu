@@ -1033,9 +1033,9 @@ int cgm_comm_destroy(cgm_comm* comm) {
   return CGM_OK;
 }
 
-int cgm_gather(cgm_ctx* ctx, cgm_comm* comm, const void* send, const size_t* counts, void* recv,
-               int root) {
-  if (!ctx || !comm || !counts) return CGM_EINVAL;
+int cgm_gatherv(cgm_ctx* ctx, cgm_comm* comm, const void* send, const size_t* counts,
+                const size_t* displs, void* recv, int root) {
+  if (!ctx || !comm || !counts || !displs) return CGM_EINVAL;
   if (root < 0 || root >= comm->nranks)
     return fail(ctx, CGM_EINVAL, "cgm_gather: root %d of %d ranks", root, comm->nranks);
   NcclApi& n = nccl_api();
@@ -1043,26 +1043,24 @@ int cgm_gather(cgm_ctx* ctx, cgm_comm* comm, const void* send, const size_t* cou
   cudaStream_t st = ctx->user_stream;
   if (comm->rank == root) {
     if (!recv) return fail(ctx, CGM_EINVAL, "cgm_gather: root needs a receive buffer");
-    size_t off = 0;
     CGM_NCCL(ctx, n.GroupStart());
     for (int r = 0; r < comm->nranks; ++r) {
-      char* dst = static_cast<char*>(recv) + off;
-      if (counts[r] > 0) {
-        if (r == root) {
-          const cudaError_t e = cudaMemcpyAsync(dst, send, counts[r], cudaMemcpyDeviceToDevice, st);
-          if (e != cudaSuccess) {
-            n.GroupEnd();
-            return fail(ctx, CGM_ECUDA, "cgm_gather: %s", cudaGetErrorString(e));
-          }
-        } else {
-          const ncclResult_t rr = n.Recv(dst, counts[r], ncclInt8, r, comm->comm, st);
-          if (rr != ncclSuccess) {
-            n.GroupEnd();
-            return fail(ctx, CGM_ENCCL, "ncclRecv: %s", n.GetErrorString(rr));
-          }
+      char* dst = static_cast<char*>(recv) + displs[r];
+      if (counts[r] == 0) continue;
+      if (r == root) {
+        if (dst == send) continue;  // already in place
+        const cudaError_t e = cudaMemcpyAsync(dst, send, counts[r], cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) {
+          n.GroupEnd();
+          return fail(ctx, CGM_ECUDA, "cgm_gather: %s", cudaGetErrorString(e));
+        }
+      } else {
+        const ncclResult_t rr = n.Recv(dst, counts[r], ncclInt8, r, comm->comm, st);
+        if (rr != ncclSuccess) {
+          n.GroupEnd();
+          return fail(ctx, CGM_ENCCL, "ncclRecv: %s", n.GetErrorString(rr));
         }
       }
-      off += counts[r];
     }
     CGM_NCCL(ctx, n.GroupEnd());
   } else if (counts[comm->rank] > 0) {
@@ -1075,6 +1073,18 @@ int cgm_gather(cgm_ctx* ctx, cgm_comm* comm, const void* send, const size_t* cou
     CGM_NCCL(ctx, n.GroupEnd());
   }
   return CGM_OK;
+}
+
+int cgm_gather(cgm_ctx* ctx, cgm_comm* comm, const void* send, const size_t* counts, void* recv,
+               int root) {
+  if (!ctx || !comm || !counts) return CGM_EINVAL;
+  std::vector<size_t> displs(static_cast<size_t>(std::max(comm->nranks, 0)));
+  size_t off = 0;
+  for (int r = 0; r < comm->nranks; ++r) {
+    displs[r] = off;
+    off += counts[r];
+  }
+  return cgm_gatherv(ctx, comm, send, counts, displs.data(), recv, root);
 }
 
 }  // extern "C"

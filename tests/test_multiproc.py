@@ -113,3 +113,102 @@ def test_two_rank_sharded_sweep_point_equals_single():
     for p in procs:
         p.join(timeout=60)
     assert got[0] == want and got[1] == want
+
+
+# ------------------------- chunked sharded detect + precode with the q/s gather
+def _both_inputs(n_sc, B=16, U=4, S=3):
+    sys.path.insert(0, ROOT)
+    import oracle
+
+    o = oracle.Oracle("port")
+    H = np.stack([o.rayleigh(13, [2, sc], B, U) for sc in range(n_sc)]).astype(np.complex64)
+    Y = np.stack([o.rayleigh(13, [3, sc], B, S) for sc in range(n_sc)]).astype(np.complex64)
+    T = np.stack([o.rayleigh(13, [5, sc], S, U) for sc in range(n_sc)]).astype(np.complex64)
+    return o, H, Y, T
+
+
+def _both_compute(o, H, Y, T):
+    """The per-chunk hot path (the CPU oracle standing in for the GPU kernels):
+    detect_cg on (H, Y) and precode_cg on (H^H, T), as detect_precode_cg does."""
+    d = o.detect(H, Y, 2.0, 0.5, 1.0, 4, 3, "exact")
+    p = o.precode(np.conj(np.transpose(H, (0, 2, 1))), T, 3.0, 3)
+    return {"llr": d["llr"].astype(np.float32), "status": d["status"],
+            "q": p["q"].astype(np.complex64), "s": p["s"].astype(np.complex64),
+            "gain": p["gain"].astype(np.float32), "pstatus": p["status"]}
+
+
+_SPEC = {"llr": ((3, 4, 4), torch.float32), "status": ((3,), torch.uint8),
+         "q": ((3, 16), torch.complex64), "s": ((3, 16), torch.complex64),
+         "gain": ((3,), torch.float32), "pstatus": ((3,), torch.uint8)}
+
+
+def _pipeline_worker(rank, world, port, n_sc, n_chunks, outq):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1404_0424_b200.parallel import ShardedPipeline, TorchTransport
+
+    o, H, Y, T = _both_inputs(n_sc)
+    pipe = ShardedPipeline(n_sc, rank, world, _SPEC, TorchTransport(rank, world),
+                           n_chunks=n_chunks)
+    calls = []
+
+    def compute(a, b, views):
+        lo = pipe.lo
+        calls.append((a, b))
+        r = _both_compute(o, H[lo + a:lo + b], Y[lo + a:lo + b], T[lo + a:lo + b])
+        for k, v in views.items():
+            v.copy_(torch.from_numpy(r[k]))
+
+    res = pipe.run(compute)
+    # every local subcarrier computed exactly once, in order
+    assert [x for a, b in calls for x in range(a, b)] == list(range(pipe.n_local))
+    if rank == 0:
+        outq.put({k: v.numpy().copy() for k, v in res.items()})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_sc,n_chunks", [(7, 3), (4, 3), (9, 1)])
+def test_two_rank_chunked_pipeline_gathers_llr_and_precoded_vectors(n_sc, n_chunks):
+    """Strong-scaling shard (cfg5's split), chunked, with the gather of LLRs
+    AND the precoded vectors q, s (and gains, status bytes) to rank 0 chunk by
+    chunk: rank 0 ends with exactly the unsharded outputs.  Ragged shards
+    (n_sc = 7) and empty chunks (n_sc = 4 over 2 ranks x 3 chunks) included."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipeline_worker, args=(r, 2, port, n_sc, n_chunks, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    o, H, Y, T = _both_inputs(n_sc)
+    want = _both_compute(o, H, Y, T)
+    for k in _SPEC:
+        assert np.array_equal(got[k], want[k]), k
+
+
+def test_gather_layout_covers_every_subcarrier_once():
+    """The chunk layouts of all ranks tile [0, n_sc) exactly (pure host logic)."""
+    sys.path.insert(0, ROOT)
+    from paper_1404_0424_b200.parallel import ShardedPipeline
+
+    class _Null:
+        def gatherv(self, *a, **k):
+            pass
+
+    for n_sc, world, n_chunks in [(65536, 8, 4), (65536, 3, 5), (10, 4, 3), (3, 4, 2)]:
+        seen = np.zeros(n_sc, np.int64)
+        for r in range(world):
+            p = ShardedPipeline(n_sc, r, world, {"x": ((1,), torch.uint8)}, _Null(),
+                                n_chunks=n_chunks)
+            for c in range(n_chunks):
+                counts, displs = p.gather_layout(c, 1)
+                a, b = p.chunk_range(r, c)
+                assert counts[r] == b - a and displs[r] == p.lo + a
+                seen[displs[r]:displs[r] + counts[r]] += 1
+        assert (seen == 1).all(), (n_sc, world, n_chunks)
