@@ -27,6 +27,8 @@
 // registers (precode.cpp:22-71).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (type only)
+
 #include "cgm_rows32.cuh"
 
 namespace cgm {
@@ -301,121 +303,148 @@ __global__ void __launch_bounds__(256, 2) block32_kernel(const KernelParams p) {
 }
 
 // Precoder (precode.cpp:22-71) for the transmit vectors solved by
-// block32_kernel: one CTA per subcarrier, two resident per SM (one stages
-// while the other computes), thread b <-> antenna row b (B <= 256, natural
-// H_u layout, U = 32).  The subcarrier's H rows (64 KB) and v_K vectors are
-// staged by coalesced 16-byte cp.async into rows padded to 34 complex
-// (272 B), so the 8 lanes of an LDS.128 phase hit 8 distinct bank groups;
-// v_K is a broadcast.  q_b = sum_u H_u[b][u] v_u (precode.cpp:69 with
-// H_d = H_u^H) for 8 vectors per pass on packed accumulators
-// (a += (h.x, h.y) v.x, b += (h.x, h.y) v.y, q = (a.x - b.y, a.y + b.x)),
-// gain = ||q|| by a fixed-order reduction, s = q / gain, zero_input when the
-// gain vanishes (precode.cpp:22-36).
+// block32_kernel (B <= 256, natural H_u layout, U = 32): one 256-thread CTA
+// per subcarrier, several resident per SM so one CTA's loads overlap the
+// others' math and stores.  The subcarrier's H (64 KB) arrives as two 2-D
+// TMA tensor tiles (users 0-15 and 16-31: 128-byte rows, SWIZZLE_128B) on
+// two mbarriers, v_K + status slots (4 KB) as one bulk copy on the first,
+// so the first half's products start while the second half lands and no
+// thread issues a load.  Register tile per thread: 4 antenna rows
+// (rb + 64 i) x 4 vectors; warp w takes vectors 4 (w mod 4) .. + 3 and row
+// block rb = (w / 4) * 32 + lane, so an LDS.128 phase of 8 lanes reads 8 rows
+// with distinct (row mod 8) -- under the 128-byte swizzle (chunk c of row r
+// at c ^ (r mod 8)) 8 distinct bank groups -- and the v_K reads are
+// warp-wide broadcasts: 8 loads per 64 FFMA2.  q_b = sum_u H_u[b][u] v_u
+// (precode.cpp:69 with H_d = H_u^H) on packed accumulators
+// (a += (h.x, h.y) v.x, b += (h.x, h.y) v.y, q = (a.x - b.y, a.y + b.x));
+// gain = ||q|| by a fixed-order reduction (a thread's 4 rows, warp_sum4
+// over the lanes, the two row halves), s = q / gain, zero_input when the
+// gain vanishes (precode.cpp:22-36); q and s leave from registers as
+// coalesced 256-byte warp stores (streaming, evict-first).
 struct PrecodeQSmem {
-  static constexpr int LDH = 34;  // padded H row (float2)
-  int h, z, gpart, total;
-  __host__ __device__ static int align(int x) { return (x + 127) & ~127; }
+  static constexpr int NTH = 256;
+  int bar, h, z, gpart, total;
+  __host__ __device__ static int zbytes(int St) { return ((St * 33 + 1) & ~1) * 8; }
   __host__ __device__ void plan(int B, int St) {
-    h = 0;
-    z = align(B * LDH * 8);
-    gpart = align(z + St * 33 * 8);  // v_K rows + status slots, as in the workspace
-    total = gpart + (kBlkMaxW + 2) * 16 * 4;
+    bar = 0;
+    h = 1024;  // 128B-swizzled tiles: 1024-byte aligned
+    z = h + 2 * B * 128;
+    gpart = z + ((zbytes(St) + 127) & ~127);
+    total = gpart + 4 * 16 * 4 + 1024;  // + slack to align the base
   }
 };
 
-__global__ void __launch_bounds__(256, 3) precode_q_kernel(const KernelParams p) {
-  constexpr int UP = 32, NQ = 8, LDH = PrecodeQSmem::LDH;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nt = blockDim.x, nw = nt >> 5;
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) precode_q_kernel(const KernelParams p,
+                                                               const __grid_constant__ CUtensorMap tmH) {
+  constexpr int UP = 32, TR = 4, TV = 4;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int St = p.St, B = p.B;
   WsOffsets W;
   W.plan(UP, p.S, p.K, p.exact != 0, p.fx != 0, p.zs);
   PrecodeQSmem L;
   L.plan(B, St);
-  float* gpart = reinterpret_cast<float*>(smem + L.gpart);
-  float* ginv = gpart + kBlkMaxW * NQ;  // [NQ] inverse gains, [NQ] flags
-  const bool okb = tid < B;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  float* gpart = reinterpret_cast<float*>(smem + L.gpart);  // [2 row halves][16 vectors]
+  float* ginv = gpart + 2 * 16;                               // [16] 1/gain, [16] flags
   const long lsc = blockIdx.x;
   const long sc = p.sc_base + lsc;
-  {
-    const float2* hsrc = p.H + sc * static_cast<long>(B) * UP;
-    float2* hdst = reinterpret_cast<float2*>(smem + L.h);
-    for (int j = tid; j < B * (UP / 2); j += nt) {  // 16 B chunks, coalesced reads
-      const int row = j >> 4, ch = j & 15;
-      cp_async16(hdst + row * LDH + 2 * ch, hsrc + row * UP + 2 * ch);
-    }
-    const float2* zsrc = p.ws + lsc * W.stride + W.z;
-    float2* zdst = reinterpret_cast<float2*>(smem + L.z);
-    const int zch = (St * (UP + 1) + 1) / 2;
-    for (int j = tid; j < zch; j += nt) cp_async16(zdst + 2 * j, zsrc + 2 * j);
-    cp_async_commit();
-    cp_async_wait<0>();
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    const uint32_t zb = static_cast<uint32_t>(PrecodeQSmem::zbytes(St));
+    const int row = static_cast<int>(sc * B);
+    mbar_expect_tx(bar, static_cast<uint32_t>(B) * 128u + zb);
+    bulk_g2s(smem + L.z, p.ws + lsc * W.stride + W.z, zb, bar);
+    tma_load_2d(smem + L.h, &tmH, 0, row, bar);
+    mbar_expect_tx(bar + 1, static_cast<uint32_t>(B) * 128u);
+    tma_load_2d(smem + L.h + B * 128, &tmH, 32, row, bar + 1);
   }
-  __syncthreads();
-  const float2* hrow = reinterpret_cast<const float2*>(smem + L.h) + (okb ? tid : 0) * LDH;
+  __syncthreads();  // barrier init visible
   const float2* Zs = reinterpret_cast<const float2*>(smem + L.z);
-  for (int t0 = 0; t0 < St; t0 += NQ) {
-    const int nq = St - t0 < NQ ? St - t0 : NQ;
-    unsigned long long qa[NQ], qb[NQ];
+  const int tb = warp & 3, half = warp >> 2, rb = half * 32 + lane;
+  for (int t0 = 0; t0 < St; t0 += 16) {
+    const int nv = St - t0 < 16 ? St - t0 : 16;  // vectors of this pass
+    unsigned long long qa[TR][TV], qb[TR][TV];
 #pragma unroll
-    for (int t = 0; t < NQ; ++t) qa[t] = qb[t] = 0ull;
+    for (int r = 0; r < TR; ++r)
+#pragma unroll
+      for (int j = 0; j < TV; ++j) qa[r][j] = qb[r][j] = 0ull;
+    // vectors past St read the pass's first one (results discarded)
+    const float2* vb = Zs + (t0 + (tb * TV < nv ? tb * TV : 0)) * UP;
+    const int vlast = nv - 1 - tb * TV;  // vectors j > vlast of this thread are past St
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      mbar_wait(bar + hh, 0);
+      const unsigned char* ht = smem + L.h + hh * B * 128;
 #pragma unroll 2
-    for (int u = 0; u < UP; u += 2) {
-      const ulonglong2 h = *reinterpret_cast<const ulonglong2*>(hrow + u);
+      for (int c = 0; c < 8; ++c) {
+        ulonglong2 h[TR], v[TV];
 #pragma unroll
-      for (int t = 0; t < NQ; ++t) {
-        if (t < nq) {
-          const ulonglong2 vv = *reinterpret_cast<const ulonglong2*>(Zs + (t0 + t) * UP + u);
-          ffma2(qa[t], h.x, f2dup_lo(vv.x));
-          ffma2(qb[t], h.x, f2dup_hi(vv.x));
-          ffma2(qa[t], h.y, f2dup_lo(vv.y));
-          ffma2(qb[t], h.y, f2dup_hi(vv.y));
+        for (int r = 0; r < TR; ++r) {
+          const int row = rb + 64 * r;
+          h[r] = *reinterpret_cast<const ulonglong2*>(ht + (row < B ? row : 0) * 128 + ((c ^ (row & 7)) << 4));
         }
+        const int u = hh * 16 + 2 * c;
+#pragma unroll
+        for (int j = 0; j < TV; ++j)
+          v[j] = *reinterpret_cast<const ulonglong2*>(vb + (j <= vlast ? j : 0) * UP + u);
+#pragma unroll
+        for (int r = 0; r < TR; ++r)
+#pragma unroll
+          for (int j = 0; j < TV; ++j) {
+            ffma2(qa[r][j], h[r].x, f2dup_lo(v[j].x));
+            ffma2(qb[r][j], h[r].x, f2dup_hi(v[j].x));
+            ffma2(qa[r][j], h[r].y, f2dup_lo(v[j].y));
+            ffma2(qb[r][j], h[r].y, f2dup_hi(v[j].y));
+          }
       }
     }
-    float2 q[NQ];
-    float nrm[NQ];
+    float2 q[TR][TV];
+    float nrm[TV];
 #pragma unroll
-    for (int t = 0; t < NQ; ++t) {
-      const float2 A = f2unpack(qa[t]), Bq = f2unpack(qb[t]);
-      q[t] = make_float2(A.x - Bq.y, A.y + Bq.x);
-      nrm[t] = okb ? cnorm(q[t]) : 0.f;
+    for (int j = 0; j < TV; ++j) {
+      nrm[j] = 0.f;
+#pragma unroll
+      for (int r = 0; r < TR; ++r) {
+        const float2 A = f2unpack(qa[r][j]), Bq = f2unpack(qb[r][j]);
+        q[r][j] = make_float2(A.x - Bq.y, A.y + Bq.x);
+        if (rb + 64 * r < B) nrm[j] += cnorm(q[r][j]);  // rows in a fixed order
+      }
     }
-    // per-warp sums of the NQ norms (warp_sum4); thread t < NQ sums vector t
-    // over the warps in a fixed order and publishes 1 / gain
+    warp_sum4(nrm);
+    if (lane == 0)
 #pragma unroll
-    for (int g = 0; g < NQ; g += 4) {
-      float x4[4] = {nrm[g], nrm[g + 1], nrm[g + 2], nrm[g + 3]};
-      warp_sum4(x4);
-      if (lane == 0)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) gpart[warp * NQ + g + k] = x4[k];
-    }
+      for (int j = 0; j < TV; ++j) gpart[half * 16 + tb * TV + j] = nrm[j];
     __syncthreads();
-    if (tid < nq) {
+    if (tid < nv) {
       const int ts = t0 + tid;
-      float n2 = 0.f;
-      for (int w = 0; w < nw; ++w) n2 += gpart[w * NQ + tid];  // fixed order
+      const float n2 = gpart[tid] + gpart[16 + tid];  // fixed order
       const bool ok = Zs[St * UP + ts].x == 0.f;
       const float g = sqrtf(n2);
       const bool zero = ok && !(g > 0.f);
       ginv[tid] = (ok && !zero) ? 1.f / g : 0.f;
-      ginv[NQ + tid] = ok ? 1.f : 0.f;
+      ginv[16 + tid] = ok ? 1.f : 0.f;
       if (p.gain) p.gain[sc * St + ts] = (ok && !zero) ? g : 0.f;
       if (p.pstatus) p.pstatus[sc * St + ts] = ok ? (zero ? 2 : 0) : 1;
     }
     __syncthreads();
-    if (okb) {
 #pragma unroll
-      for (int t = 0; t < NQ; ++t) {
-        if (t < nq) {
-          const int ts = t0 + t;
-          const float inv = ginv[t];
-          const bool ok = ginv[NQ + t] != 0.f;
-          const long ob = (sc * St + ts) * static_cast<long>(B) + tid;
-          if (p.q) p.q[ob] = ok ? q[t] : make_float2(0.f, 0.f);
-          if (p.s_out) p.s_out[ob] = cscale(inv, q[t]);
-        }
+    for (int j = 0; j < TV; ++j) {
+      const int t = tb * TV + j;
+      if (t >= nv) continue;
+      const float inv = ginv[t];
+      const bool ok = ginv[16 + t] != 0.f;
+      const long ob = (sc * St + t0 + t) * static_cast<long>(B);
+#pragma unroll
+      for (int r = 0; r < TR; ++r) {
+        const int row = rb + 64 * r;
+        if (row >= B) continue;
+        if (p.q) __stcs(p.q + ob + row, ok ? q[r][j] : make_float2(0.f, 0.f));
+        if (p.s_out) __stcs(p.s_out + ob + row, cscale(inv, q[r][j]));
       }
     }
     __syncthreads();  // gpart / ginv reused by the next pass

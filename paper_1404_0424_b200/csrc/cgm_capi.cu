@@ -3,6 +3,8 @@
 // template dispatch of the fused subcarrier kernel, the chunked host-buffer
 // pipeline (H2D / kernel / D2H overlapped on two streams) and the seeded
 // device input generators.
+#include <cuda.h>  // CUtensorMap types only (the encoder comes from cudaGetDriverEntryPoint)
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>  // types only: the entry points are resolved at run time
@@ -153,6 +155,30 @@ cgm::AxisTables make_axis_tables() {
 }
 
 int up_of(int U) { return U <= 8 ? 8 : U <= 16 ? 16 : U <= 32 ? 32 : 64; }
+
+// 2-D tensor map of an H_u block [rows][32 complex] for the precoder's TMA
+// tiles: FP32 elements, inner extent 64 (one 256-byte antenna row), box
+// 32 x B (users 0-15 or 16-31 of all B rows of one subcarrier: 128-byte
+// rows), SWIZZLE_128B.  cuTensorMapEncodeTiled is resolved through the
+// runtime (no libcuda link).
+bool encode_h_tiles(CUtensorMap* m, const float2* H, long rows, int B) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {256};
+  const cuuint32_t box[2] = {32, static_cast<cuuint32_t>(B)};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float2*>(H), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 // Kernel-variant switches (cgm_ctx_set_kernel_policy): A/B alternatives kept
 // for parity tests and measurements, never selected by default.
@@ -354,6 +380,8 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   if (mode == kBlock)  // NS systems per warp
     nw2 = std::min(cgm::kBlkMaxW, (nsys + cgm::kBlkNS - 1) / cgm::kBlkNS);
   long g2cap = 1L << 40;
+  CUtensorMap tmH{};
+  auto pq_kernel = cgm::precode_q_kernel<2>;
   if (mode == kBlock) {  // persistent
     int occ2 = 0;
     CGM_PREP(ctx, k2, 32 * nw2, smem2, &occ2);
@@ -363,7 +391,9 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       PQ.plan(p.B, p.St);
       if (PQ.total > ctx->max_smem)
         return fail(ctx, CGM_EINVAL, "precoder: %d B of shared memory exceed %d", PQ.total, ctx->max_smem);
-      CGM_PREP(ctx, cgm::precode_q_kernel, 256, PQ.total, nullptr);
+      CGM_PREP(ctx, pq_kernel, cgm::PrecodeQSmem::NTH, PQ.total, nullptr);
+      if (!encode_h_tiles(&tmH, p.H, p.n_sc * static_cast<long>(p.B), p.B))
+        return fail(ctx, CGM_ECUDA, "cuTensorMapEncodeTiled failed for the precoder's H tiles");
     }
   }
   if (mode == kLanesPf) {
@@ -411,7 +441,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       cgm::PrecodeQSmem PQ;
       PQ.plan(p.B, p.St);
       r = timed(ctx, st, 2, [&] {
-        cgm::precode_q_kernel<<<static_cast<unsigned>(n), (p.B + 31) / 32 * 32, PQ.total, st>>>(q);
+        pq_kernel<<<static_cast<unsigned>(n), cgm::PrecodeQSmem::NTH, PQ.total, st>>>(q, tmH);
       });
       if (r) return r;
     }

@@ -144,6 +144,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// One 2-D TMA tensor tile (cp.async.bulk.tensor) global->shared through a
+// tensor map (__grid_constant__ kernel parameter), completing on `bar`.
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // 16-byte asynchronous global->shared copy (cp.async, L2-only), grouped by
 // commit / wait_group: lets every thread place chunks at padded addresses
 // (bank-conflict-free row strides) that one bulk copy cannot produce.
