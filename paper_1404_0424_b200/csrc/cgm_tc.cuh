@@ -281,12 +281,18 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
       {
         // H: 64 rows x 8 chunks, Y: 64 rows x nyc chunks; a thread's chunks
         // are loaded together (latency overlap), then split
+        // a thread's 32-byte chunk is two LDS.128; lanes 4-7 of every
+        // 8-lane phase read the halves in the opposite order, so a phase
+        // covers 8 distinct 16-byte bank groups (was 2-way conflicted)
+        const bool hswap = (lane >> 2) & 1;
         float hx[HPT][8];
 #pragma unroll
         for (int r = 0; r < HPT; ++r) {
           const int it = st + r * NTS, k = it >> 3, j = it & 7;
-          const float4 a = *reinterpret_cast<const float4*>(Hst + k * 64 + j * 8);
-          const float4 b = *reinterpret_cast<const float4*>(Hst + k * 64 + j * 8 + 4);
+          const float* src = Hst + k * 64 + j * 8;
+          const float4 a0 = *reinterpret_cast<const float4*>(src + (hswap ? 4 : 0));
+          const float4 b0 = *reinterpret_cast<const float4*>(src + (hswap ? 0 : 4));
+          const float4 a = hswap ? b0 : a0, b = hswap ? a0 : b0;
           hx[r][0] = a.x; hx[r][1] = a.y; hx[r][2] = a.z; hx[r][3] = a.w;
           hx[r][4] = b.x; hx[r][5] = b.y; hx[r][6] = b.z; hx[r][7] = b.w;
         }
@@ -294,7 +300,27 @@ __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_ker
         float yx[8];
         int yk = 0, yj = 0;
         const bool ylive = st < ycount && (st & ((1 << lg) - 1)) < nyc;
-        if (ylive) {
+        if (ylive && nyc == 4 && (S & 1) == 0) {
+          // 4 chunks per Y row (S = 13..16; 16-byte aligned rows for even S):
+          // lanes 0-3 / 4-7 of a phase take rows r and r + 4 -- distinct
+          // swizzled chunks for the piece stores (j ^ (k mod 8)) -- and read
+          // their halves in opposite orders (distinct bank groups)
+          const int t = st & 31;
+          yk = (st >> 5) * 8 + 4 * ((t >> 2) & 1) + (t >> 3);
+          yj = t & 3;
+          const float* src = Yst + yk * 2 * S + yj * 8;
+          const int c0 = yj * 8;
+          float4 h0 = make_float4(0.f, 0.f, 0.f, 0.f), h1 = h0;
+          if (hswap) {
+            if (c0 + 4 < 2 * S) h1 = *reinterpret_cast<const float4*>(src + 4);
+            h0 = *reinterpret_cast<const float4*>(src);
+          } else {
+            h0 = *reinterpret_cast<const float4*>(src);
+            if (c0 + 4 < 2 * S) h1 = *reinterpret_cast<const float4*>(src + 4);
+          }
+          yx[0] = h0.x; yx[1] = h0.y; yx[2] = h0.z; yx[3] = h0.w;
+          yx[4] = h1.x; yx[5] = h1.y; yx[6] = h1.z; yx[7] = h1.w;
+        } else if (ylive) {
           yk = st >> lg;
           yj = st & ((1 << lg) - 1);
 #pragma unroll
