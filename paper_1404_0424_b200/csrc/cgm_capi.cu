@@ -188,6 +188,7 @@ constexpr int kPolLaneSolve = 4;    // U = 32: lane-per-row solve kernel instead
 constexpr int kPolBlockUp = 8;      // U = 32 uplink only: the shared-G block kernel instead of pairs
 constexpr int kPolRowsCta = 16;     // U = 32 with transmit vectors: the 8-warp row CTA instead of block
 constexpr int kPolPoisonWs = 32;    // test only: fill the workspace with NaN before every chunk
+constexpr int kPolTileMoments = 64; // U = 32, FP32 moments: the 4x4-tile CTA kernel instead of warp rows
 
 // Device workspace of the split path.  A call captured into a CUDA graph
 // bakes in this pointer, so a larger call never frees it: the old buffer
@@ -303,6 +304,14 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       nm_smem = dbl ? MG::template smem<double>() : MG::template smem<float>();
       nm_t = MG::NT;
       nm_spc = MG::SPC;
+      if constexpr (UP == 32) {
+        if (!p.fx && !dbl && !(ctx->policy & kPolTileMoments)) {  // warp per subcarrier
+          km = cgm::moments_rows32_kernel;
+          nm_smem = cgm::MomRowsSmem::TOTAL;
+          nm_t = 32 * cgm::kMrW;
+          nm_spc = cgm::kMrW;
+        }
+      }
       if (nm_smem > ctx->max_smem)
         return fail(ctx, CGM_EINVAL, "exact tracker: %d B of shared memory per moments CTA exceed %d",
                     nm_smem, ctx->max_smem);
@@ -883,7 +892,7 @@ int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, lon
 
 int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy) {
   if (!ctx || policy < 0 ||
-      policy > (kPolFfmaChannel | kPolSplitSmall | kPolLaneSolve | kPolBlockUp | kPolRowsCta |
+      policy > (kPolFfmaChannel | kPolSplitSmall | kPolLaneSolve | kPolBlockUp | kPolRowsCta | kPolTileMoments |
                 kPolPoisonWs))
     return fail(ctx, CGM_EINVAL, "unknown kernel policy %d", policy);
   ctx->policy = policy;

@@ -476,6 +476,180 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
   }
 }
 
+// ------------------------------------------------- moments, warp per subcarrier
+// U = 32, FP32 moment table (K <= 6), several vectors per subcarrier (not
+// FX): the same (c, d) and D_k[i] as moments_kernel<32, float>, but one warp
+// owns a subcarrier end to end with no block barriers: lane i keeps row i
+// of G (then Ahat) in registers (conflict-free LDS.128 reads of the padded
+// rows), runs the power iteration of cheb_interval on its row, and forms its
+// row of every product T_{a+1} = 2 Ahat T_a - T_{a-1}: (Ahat T_a)[i][j] =
+// sum_k Ahat[i][k] T_a[k][j], Ahat[i][k] from registers, row k of T_a as
+// warp-wide broadcasts (one LDS.128 per two j), 2 packed FFMA2 per complex
+// MAC.  Full rows (2x the triangle's products) in exchange for no idle
+// lanes, no tile bookkeeping and no barriers; row i's moments
+// |T_{a+1}[i][:]|^2 and Re T_{a+1}[i][:] . conj(T_a[i][:]) are summed by
+// the lane in column order.  T_{a+1} overwrites T_{a-1} (each lane its own
+// row), so two padded U x U buffers per warp.
+constexpr int kMrW = 4;  // warps (subcarriers) per CTA
+struct MomRowsSmem {
+  static constexpr int LD = 34;                  // padded row (float2): conflict-free LDS.128 per lane
+  static constexpr int MAT = 32 * LD * 8;        // bytes
+  static constexpr int PER_WARP = 2 * MAT + 32 * 8;  // T_a, T_{a-1/a+1}, power-iteration vector
+  static constexpr int TOTAL = kMrW * PER_WARP;
+};
+
+__global__ void __launch_bounds__(32 * kMrW, 3) moments_rows32_kernel(const KernelParams p) {
+  constexpr int UP = 32, LD = MomRowsSmem::LD;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, i = threadIdx.x & 31;
+  const long lsc = static_cast<long>(blockIdx.x) * kMrW + warp;
+  if (lsc >= p.n_sc) return;
+  const int K = p.K;
+  WsOffsets W;
+  W.plan(UP, p.S, K, true, false, p.zs);
+  unsigned char* base = smem + warp * MomRowsSmem::PER_WARP;
+  float2* buf0 = reinterpret_cast<float2*>(base);
+  float2* buf1 = reinterpret_cast<float2*>(base + MomRowsSmem::MAT);
+  float2* xs = reinterpret_cast<float2*>(base + 2 * MomRowsSmem::MAT);
+  float2* ws = p.ws + lsc * W.stride;
+  // G row i -> registers (the workspace G is the full Hermitian matrix)
+  ulonglong2 g[UP / 2];
+  {
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(ws + W.g + i * UP);
+#pragma unroll
+    for (int c = 0; c < UP / 2; ++c) g[c] = src[c];
+  }
+  // power iteration on A = G + reg I (cheb_interval: x_0 = 1, 7 products,
+  // Rayleigh quotient from the second on)
+  const float reg = p.rho_inv_u;
+  float2 xr = make_float2(1.f, 0.f);
+  xs[i] = xr;
+  __syncwarp();
+  float lam = reg;
+  for (int it = 0; it <= 6; ++it) {
+    // (Ax)_i = sum_j G[i][j] x_j: a += g x.x, b += g x.y, even / odd columns
+    // in separate accumulators (half the dependent chain)
+    unsigned long long a0 = 0ull, b0 = 0ull, a1 = 0ull, b1 = 0ull;
+#pragma unroll
+    for (int c = 0; c < UP / 2; ++c) {
+      const ulonglong2 xv = *reinterpret_cast<const ulonglong2*>(xs + 2 * c);
+      ffma2(a0, g[c].x, f2dup_lo(xv.x));
+      ffma2(b0, g[c].x, f2dup_hi(xv.x));
+      ffma2(a1, g[c].y, f2dup_lo(xv.y));
+      ffma2(b1, g[c].y, f2dup_hi(xv.y));
+    }
+    const float2 A0 = f2unpack(a0), B0 = f2unpack(b0), A1 = f2unpack(a1), B1 = f2unpack(b1);
+    float2 y = make_float2((A0.x - B0.y) + (A1.x - B1.y), (A0.y + B0.x) + (A1.y + B1.x));
+    y.x = fmaf(reg, xr.x, y.x);
+    y.y = fmaf(reg, xr.y, y.y);
+    // ||y||^2 and x^H A x over the warp in one butterfly: lanes 0-15 carry
+    // the first sum, 16-31 the second after the xor-16 exchange
+    float nrm, ray;
+    {
+      const float v0 = cnorm(y), v1 = xr.x * y.x + xr.y * y.y;
+      const bool up = i & 16;
+      float k = up ? v1 : v0;
+      k += __shfl_xor_sync(0xffffffffu, up ? v0 : v1, 16);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+      nrm = __shfl_sync(0xffffffffu, k, 0);
+      ray = __shfl_sync(0xffffffffu, k, 16);
+    }
+    if (it > 0) lam = ray;
+    const float inv = nrm > 0.f ? rsqrtf(nrm) : 0.f;
+    __syncwarp();
+    xr = cscale(inv, y);
+    xs[i] = xr;
+    __syncwarp();
+  }
+  float2 cd;
+  {
+    const float lo = reg;
+    const float hi = fmaxf(1.1f * lam, 1.0001f * lo);
+    const float c = 0.5f * (lo + hi);
+    float d = 0.5f * (hi - lo);
+    if (!(d > 1e-6f * fmaxf(fabsf(c), 1e-30f))) d = fmaxf(fabsf(c), 1.f);
+    cd = make_float2(c, d);
+  }
+  if (i == 0) ws[W.cd] = cd;
+  // Ahat = (G + (reg - c) I) / d, row i in registers and as T_1 in buf0
+  const float invd = 1.f / cd.y, shift = reg - cd.x;
+  float dii = 0.f;  // Ahat[i][i]
+#pragma unroll
+  for (int c = 0; c < UP / 2; ++c) {
+    float2 e0 = f2unpack(g[c].x), e1 = f2unpack(g[c].y);
+    if (2 * c == i) { e0.x += shift; e0.y = 0.f; }
+    if (2 * c + 1 == i) { e1.x += shift; e1.y = 0.f; }
+    e0 = make_float2(e0.x * invd, e0.y * invd);
+    e1 = make_float2(e1.x * invd, e1.y * invd);
+    if (2 * c == i) dii = e0.x;
+    if (2 * c + 1 == i) dii = e1.x;
+    g[c].x = f2pack(e0.x, e0.y);
+    g[c].y = f2pack(e1.x, e1.y);
+    *reinterpret_cast<ulonglong2*>(buf0 + i * LD + 2 * c) = g[c];
+  }
+  double* mom = reinterpret_cast<double*>(ws + W.t);
+  const double d1 = static_cast<double>(dii);
+  {
+    float n2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < UP / 2; ++c) {
+      const float2 e0 = f2unpack(g[c].x), e1 = f2unpack(g[c].y);
+      n2 += cnorm(e0);
+      n2 += cnorm(e1);
+    }
+    mom[i] = 1.0;
+    mom[UP + i] = d1;
+    mom[2 * UP + i] = 2.0 * static_cast<double>(n2) - 1.0;  // D_2 = 2 diag(T_1^2) - 1
+  }
+  __syncwarp();
+  float2* cur = buf0;  // T_a
+  float2* prv = buf1;  // T_{a-1} (a = 1: T_0 = I, implicit)
+  for (int a = 1; a < K; ++a) {
+    unsigned long long acc[UP];
+#pragma unroll
+    for (int j = 0; j < UP; ++j) acc[j] = 0ull;
+#pragma unroll
+    for (int k = 0; k < UP; ++k) {
+      const float2 ak = f2unpack((k & 1) ? g[k >> 1].y : g[k >> 1].x);
+      const unsigned long long ax = f2pack(ak.x, ak.x), ay = f2pack(-ak.y, ak.y);
+      const float2* trow = cur + k * LD;
+#pragma unroll
+      for (int c = 0; c < UP / 2; ++c) {
+        const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(trow + 2 * c);
+        ffma2(acc[2 * c], t.x, ax);
+        ffma2(acc[2 * c], f2swap_hl(t.x), ay);
+        ffma2(acc[2 * c + 1], t.y, ax);
+        ffma2(acc[2 * c + 1], f2swap_hl(t.y), ay);
+      }
+    }
+    // T_{a+1} row i, its moments against T_a row i, then it replaces T_{a-1}
+    float n2 = 0.f, x2 = 0.f;
+    float2 nxt[UP];
+#pragma unroll
+    for (int j = 0; j < UP; ++j) {
+      const float2 pr = a == 1 ? make_float2(j == i ? 1.f : 0.f, 0.f) : prv[i * LD + j];
+      const float2 v = f2unpack(acc[j]);
+      float2 nx = make_float2(2.f * v.x - pr.x, 2.f * v.y - pr.y);
+      if (j == i) nx.y = 0.f;
+      const float2 cu = cur[i * LD + j];
+      n2 += cnorm(nx);
+      x2 += nx.x * cu.x + nx.y * cu.y;
+      nxt[j] = nx;
+    }
+    __syncwarp();  // every lane's reads of T_a rows are done before T_a becomes T_{a-1}
+#pragma unroll
+    for (int j = 0; j < UP; j += 2)
+      *reinterpret_cast<float4*>(prv + i * LD + j) = make_float4(nxt[j].x, nxt[j].y, nxt[j + 1].x, nxt[j + 1].y);
+    __syncwarp();
+    mom[(2 * a + 1) * UP + i] = 2.0 * static_cast<double>(x2) - d1;  // D_{2a+1}
+    mom[(2 * a + 2) * UP + i] = 2.0 * static_cast<double>(n2) - 1.0;  // D_{2a+2}
+    float2* t = cur;
+    cur = prv;
+    prv = t;
+  }
+}
+
 // ------------------------------------------------------------ extraction
 // Chebyshev coefficients (FP64) of L_K and B = L_K (A - rho^-1 I) for one
 // system, warp-parallel (cheb_coef_warp's recursion, kept in double), then
