@@ -737,11 +737,11 @@ __device__ __forceinline__ MomCoef moments_coefs(const float* hist, int K, doubl
 // subcarrier's moment table (detect.cpp:375-395 + safe_rho :26-29).
 __device__ __forceinline__ void moments_row(const double* sh, MomCoef c, int K, const double* mom,
                                             int UP, int i, double es, double n0, float& mu,
-                                            float& rho) {
-  const double* gs = sh;
-  const double* ls = sh + kMaxK + 2;
-  const double* ee = ls + kMaxK + 2;
-  const double* ef = ee + 2 * kMaxK + 1;
+                                            float& rho, int km = kMaxK) {
+  const double* gs = sh;  // scratch layout sized for K <= km
+  const double* ls = sh + km + 2;
+  const double* ee = ls + km + 2;
+  const double* ef = ee + 2 * km + 1;
   double e = 0.0, f = 0.0, e2 = ee[0], efd = ef[0];
   for (int k = 1; k <= 2 * K; ++k) {
     const double d = mom[k * UP + i];
@@ -789,6 +789,87 @@ __device__ __forceinline__ void fx_handoff(const KernelParams& p, float2* ws, co
 // per-warp shared scratch (doubles) for moments_coefs / moments_row
 constexpr int kMomScratch = 2 * (kMaxK + 2) + 2 * (2 * kMaxK + 1);
 
+// Lane-per-system form of moments_coefs for K <= kLaneK (compile-time K):
+// the same FP64 recursion and Chebyshev products with the K + 2
+// coefficients of L, B in registers, so the S systems of a subcarrier run in
+// parallel on S lanes (moments_coefs spends a whole warp, 6 to 9 of its lanes
+// busy and two shuffles per step, on each system).  Writes gs, ls, ee, ef in
+// moments_row's layout for km = kLaneK, then g_0 and l_0.
+constexpr int kLaneK = 6;
+constexpr int kLaneScratch = 2 * (kLaneK + 2) + 2 * (2 * kLaneK + 1) + 2;
+template <int K>
+__device__ __forceinline__ void moments_coefs_lane(const float* hist, double cc, double dd,
+                                                   double rho_inv, double* out) {
+  constexpr int n = K + 2;
+  double al[K + 1], be[K + 1];  // alpha_k, beta_k; alpha_0 = 1, beta_0 = 0
+  al[0] = 1.0;
+  be[0] = 0.0;
+#pragma unroll
+  for (int k = 1; k <= K; ++k) {
+    al[k] = hist[(k - 1) * 2];
+    be[k] = hist[(k - 1) * 2 + 1];
+  }
+  auto mulA = [&](const double (&x)[n], double (&o)[n]) {
+#pragma unroll
+    for (int m = 0; m < n; ++m) {
+      double v = cc * x[m];
+      if (m + 1 < n) v += 0.5 * dd * x[m + 1];
+      if (m == 1) v += dd * x[0];
+      else if (m >= 2) v += 0.5 * dd * x[m - 1];
+      o[m] = v;
+    }
+  };
+  double l0[n], l1[n], l2[n];
+#pragma unroll
+  for (int m = 0; m < n; ++m) l0[m] = l1[m] = l2[m] = 0.0;
+  l0[0] = al[1];  // L_1 = alpha_1 I
+#pragma unroll
+  for (int k = 2; k <= K; ++k) {  // detect.cpp:336-368 on the coefficients
+    const double c1 = al[k] * (1.0 + be[k - 1]) / al[k - 1];
+    const double c2 = al[k] * be[k - 2] / al[k - 2];
+    double d1[n], t[n];
+#pragma unroll
+    for (int m = 0; m < n; ++m) d1[m] = l0[m] - l1[m];
+    mulA(d1, t);
+#pragma unroll
+    for (int m = 0; m < n; ++m) {
+      const double nx = l0[m] + c1 * d1[m] - al[k] * t[m] - c2 * (l1[m] - l2[m]);
+      l2[m] = l1[m];
+      l1[m] = l0[m];
+      l0[m] = nx;
+    }
+  }
+  double gm[n];
+  mulA(l0, gm);
+#pragma unroll
+  for (int m = 0; m < n; ++m) gm[m] -= rho_inv * l0[m];  // B = L (A - rho^-1 I)
+  double* gs = out;
+  double* ls = out + kLaneK + 2;
+  double* ee = ls + kLaneK + 2;
+  double* ef = ee + 2 * kLaneK + 1;
+#pragma unroll
+  for (int m = 0; m < n; ++m) {
+    gs[m] = m == 0 ? 0.0 : gm[m];  // E = B - g_0 I
+    ls[m] = m == 0 ? 0.0 : l0[m];  // F = L - l_0 I
+  }
+  // (x*y)_k = 1/2 sum_{a+b=k} x_a y_b + 1/2 sum_{|a-b|=k} x_a y_b over a, b in 1..K
+#pragma unroll
+  for (int k = 0; k <= 2 * K; ++k) {
+    double se = 0.0, sf = 0.0;
+#pragma unroll
+    for (int a = 1; a <= K; ++a) {
+      const int b1 = k - a, b2 = a - k, b3 = a + k;
+      if (b1 >= 1 && b1 <= K) { se = fma(gm[a], gm[b1], se); sf = fma(gm[a], l0[b1], sf); }
+      if (b2 >= 1) { se = fma(gm[a], gm[b2], se); sf = fma(gm[a], l0[b2], sf); }
+      if (k > 0 && b3 <= K) { se = fma(gm[a], gm[b3], se); sf = fma(gm[a], l0[b3], sf); }
+    }
+    ee[k] = 0.5 * se;
+    ef[k] = 0.5 * sf;
+  }
+  out[kLaneScratch - 2] = gm[0];
+  out[kLaneScratch - 1] = l0[0];
+}
+
 // Exact-tracker outputs of a subcarrier's S uplink systems after the CG
 // (CTA-wide, warp per system): hist holds each system's (alpha, beta)
 // history (stride Kmax), Vs its v_K, sys_st its breakdown flag; msh is
@@ -802,6 +883,42 @@ __device__ __forceinline__ void moments_tail(const KernelParams& p, const float2
   const int S = p.S, U = p.U, K = p.K;
   const float2 cdv = ws[W.cd];
   const double* mom = reinterpret_cast<const double*>(ws + W.t);
+  if (K <= kLaneK && S * kLaneScratch <= nw * kMomScratch) {
+    // coefficients of all S systems at once, one lane each; then a warp
+    // per system, a lane per row
+    for (int s = threadIdx.x; s < S; s += nt) {
+      const float* hs = hist + s * Kmax * 2;
+      double* o = msh + s * kLaneScratch;
+      switch (K) {
+        case 1: moments_coefs_lane<1>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
+        case 2: moments_coefs_lane<2>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
+        case 3: moments_coefs_lane<3>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
+        case 4: moments_coefs_lane<4>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
+        case 5: moments_coefs_lane<5>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
+        default: moments_coefs_lane<6>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
+      }
+    }
+    __syncthreads();
+    for (int s = warp; s < S; s += nw) {
+      const double* sh = msh + s * kLaneScratch;
+      const MomCoef c = {sh[kLaneScratch - 2], sh[kLaneScratch - 1]};
+      const bool ok = sys_st[s] == 0;
+      for (int i = lane; i < U; i += 32) {
+        float mu, rho;
+        moments_row(sh, c, K, mom, UP, i, p.es, p.n0, mu, rho, kLaneK);
+        const long o = (sc * S + s) * static_cast<long>(U) + i;
+        const float2 xh = ok ? Vs[s * UP + i] : make_float2(0.f, 0.f);
+        if (!ok) mu = rho = 0.f;
+        if (p.xhat) p.xhat[o] = xh;
+        if (p.mu) p.mu[o] = mu;
+        if (p.rho) p.rho[o] = rho;
+        if (p.llr) store_llrs_fast(xh, mu, rho, p.bits, p.llr + o * p.bits);
+      }
+      if (p.status && lane == 0) p.status[sc * S + s] = ok ? 0 : 1;
+    }
+    __syncthreads();  // msh is reused by the next subcarrier
+    return;
+  }
   double* sh = msh + warp * kMomScratch;
   for (int s = warp; s < S; s += nw) {
     const MomCoef c = moments_coefs(hist + s * Kmax * 2, K, cdv.x, cdv.y, p.rho_inv_u, sh);
