@@ -16,7 +16,10 @@ def timeit(fn, reps=10, warm=3):
     e.record(); torch.cuda.synchronize()
     return s.elapsed_time(e) / reps
 for name in sys.argv[1:]:
-    cfg = get_config(name)
+    # name or name:n_sc (e.g. cfg1:16384 -- 16 frames of cfg1 in one call)
+    cfg = get_config(name.split(":")[0])
+    if ":" in name:
+        cfg = cfg.scaled(int(name.split(":")[1]))
     rs = cfg.rsqrt(); rs = None if rs is None else torch.tensor(rs)
     t0 = time.time()
     if cfg.kind == "downlink":
