@@ -57,25 +57,6 @@ struct Block32Smem {
   }
 };
 
-// sum over the 32 lanes of four values at once (10 shuffles): halve the
-// value set at xor 16 and xor 8, finish one value per 8-lane group, gather
-__device__ __forceinline__ void warp_sum4(float (&v)[4]) {
-  const int lane = threadIdx.x & 31;
-  const bool b4 = lane & 16, b3 = lane & 8;
-  float k0 = b4 ? v[2] : v[0], k1 = b4 ? v[3] : v[1];
-  const float s0 = b4 ? v[0] : v[2], s1 = b4 ? v[1] : v[3];
-  k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
-  k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
-  float k = b3 ? k1 : k0;
-  k += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
-  k += __shfl_xor_sync(0xffffffffu, k, 4);
-  k += __shfl_xor_sync(0xffffffffu, k, 2);
-  k += __shfl_xor_sync(0xffffffffu, k, 1);
-  // lane L now holds the sum of value (L >> 3) & 3: gather all four
-#pragma unroll
-  for (int q = 0; q < 4; ++q) v[q] = __shfl_sync(0xffffffffu, k, q << 3);
-}
-
 // CG for the systems base .. base + NS - 1 of subcarrier sc on one warp;
 // Gs = the subcarrier's G in shared memory, Ps = this warp's NS broadcast
 // rows.  Approximate uplink systems write their outputs; exact / downlink

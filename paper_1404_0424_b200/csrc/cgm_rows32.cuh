@@ -50,6 +50,25 @@ __device__ __forceinline__ void warp_sum2(float& a, float& b) {
   b = __shfl_sync(0xffffffffu, v, 16);  // lanes >= 16 hold sum(b)
 }
 
+// sum over the 32 lanes of four values at once (10 shuffles): halve the
+// value set at xor 16 and xor 8, finish one value per 8-lane group, gather
+__device__ __forceinline__ void warp_sum4(float (&v)[4]) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = lane & 16, b3 = lane & 8;
+  float k0 = b4 ? v[2] : v[0], k1 = b4 ? v[3] : v[1];
+  const float s0 = b4 ? v[0] : v[2], s1 = b4 ? v[1] : v[3];
+  k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+  float k = b3 ? k1 : k0;
+  k += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  // lane L now holds the sum of value (L >> 3) & 3: gather all four
+#pragma unroll
+  for (int q = 0; q < 4; ++q) v[q] = __shfl_sync(0xffffffffu, k, q << 3);
+}
+
 // CG for the systems base, base + 1 of subcarrier sc on one warp (lane =
 // user row), with row `lane` of G in `grow`; Ps = this warp's two broadcast
 // rows.  Approx uplink systems write their outputs here; exact / downlink
@@ -233,6 +252,151 @@ __device__ __forceinline__ void rows32_pair(const KernelParams& p, long sc, cons
   }
 }
 
+// The approximate-tracker pairs path with ONE reduction phase per CG
+// iteration (Chronopoulos-Gear): besides p and r the warp carries w = A r
+// and s = A p (s = w + beta s, so the matvec runs on r), and the two inner
+// products of an iteration, ||r||^2 and Re r^H w, are reduced together for
+// both systems (warp_sum4: one 10-shuffle butterfly where the two-phase
+// form needs two).  The curvature p^H A p is the recurrence
+// delta - beta gamma / alpha_prev (k = 1: delta).  Same decisions as
+// solvers.cpp:21-72 -- freeze (||r||^2 <= 1e-28 ||r_0||^2: alpha = 1,
+// beta = 0, no update), breakdown (curvature < 1e-30) -- and once an
+// iteration does not update, none after it does, so beta of a non-updating
+// iteration is 0 as in the reference.  The approximate tracker consumes
+// alpha_k, beta_{k-1}, beta_{k-2} in the same order (detect.cpp:409-427).
+__device__ __forceinline__ void rows32_pair_cg1(const KernelParams& p, long sc, const float2* mfsrc,
+                                                int base, const unsigned long long (&grow)[32],
+                                                float gdiag, float2* Ps) {
+  constexpr int UP = 32, NS = 2;
+  const int S = p.S, U = p.U, K = p.K;
+  const int lane = threadIdx.x & 31;
+  const float reg = p.rho_inv_u;
+  bool live[NS], broke[NS], updp[NS];
+  float gam[NS], gam0[NS], alp[NS];
+  float2 v[NS], r[NS], pp[NS], sv[NS], w[NS];
+  float f0[NS], f1[NS], f2[NS], ia1[NS], ia2[NS], bm1[NS], bm2[NS];
+  // w = (G + reg I) x for the NS broadcast rows in Ps
+  auto matvec = [&](const float2 (&x)[NS], float2 (&o)[NS]) {
+    unsigned long long a0[NS], b0[NS], a1[NS], b1[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) a0[s] = b0[s] = a1[s] = b1[s] = 0ull;
+#pragma unroll
+    for (int j = 0; j < UP; j += 2) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const ulonglong2 pj = *reinterpret_cast<const ulonglong2*>(Ps + s * UP + j);
+        ffma2(a0[s], grow[j], f2dup_lo(pj.x));
+        ffma2(b0[s], grow[j], f2dup_hi(pj.x));
+        ffma2(a1[s], grow[j + 1], f2dup_lo(pj.y));
+        ffma2(b1[s], grow[j + 1], f2dup_hi(pj.y));
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const float2 A0 = f2unpack(a0[s]), B0 = f2unpack(b0[s]);
+      const float2 A1 = f2unpack(a1[s]), B1 = f2unpack(b1[s]);
+      o[s].x = fmaf(reg, x[s].x, (A0.x - B0.y) + (A1.x - B1.y));
+      o[s].y = fmaf(reg, x[s].y, (B0.x + A0.y) + (B1.x + A1.y));
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    live[s] = base + s < S;
+    float2 b = make_float2(0.f, 0.f);
+    if (live[s] && lane < U) b = mfsrc[(base + s) * UP + lane];
+    v[s] = pp[s] = sv[s] = make_float2(0.f, 0.f);
+    r[s] = b;
+    Ps[s * UP + lane] = b;
+    broke[s] = false;
+    updp[s] = true;
+    alp[s] = 1.f;
+    ia1[s] = ia2[s] = 1.f;
+    bm1[s] = bm2[s] = 0.f;
+    f0[s] = f1[s] = f2[s] = 0.f;
+  }
+  __syncwarp();
+  matvec(r, w);  // w_0 = A r_0
+  float red[4] = {cnorm(r[0]), r[0].x * w[0].x + r[0].y * w[0].y, cnorm(r[1]),
+                  r[1].x * w[1].x + r[1].y * w[1].y};
+  warp_sum4(red);
+  float dlt[NS] = {red[1], red[3]};
+  gam[0] = gam0[0] = red[0];
+  gam[1] = gam0[1] = red[2];
+  float gold[NS] = {1.f, 1.f};
+  for (int k = 1; k <= K; ++k) {
+    float alpha[NS], beta[NS];
+    bool upd[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      // beta_{k-1} of the reference (0 when iteration k-1 did not update)
+      beta[s] = (k > 1 && updp[s]) ? __fdividef(gam[s], gold[s]) : 0.f;
+      const bool frozen = !(gam[s] > 1e-28f * gam0[s]);  // solvers.cpp:21,25-27
+      const bool go = live[s] && updp[s] && !frozen && !broke[s];
+      const float curv = k == 1 ? dlt[s] : dlt[s] - beta[s] * gam[s] * __fdividef(1.f, alp[s]);
+      if (go && curv < 1e-30f) broke[s] = true;  // solvers.cpp:55-57
+      upd[s] = go && !broke[s];
+      alpha[s] = upd[s] ? __fdividef(gam[s], curv) : 1.f;
+      // tracker bookkeeping: the previous iteration's beta, then Eq. (11)
+      bm2[s] = bm1[s];
+      bm1[s] = k > 1 ? beta[s] : 0.f;
+      if (live[s]) {
+        const float c1 = alpha[s] * (1.f + bm1[s]) * ia1[s];
+        const float c2 = alpha[s] * bm2[s] * ia2[s];
+        const float nk = f0[s] + (c1 - alpha[s] * (gdiag + reg)) * (f0[s] - f1[s]) -
+                         c2 * (f1[s] - f2[s]);
+        const float nf = k == 1 ? alpha[s] : nk;
+        f2[s] = f1[s];
+        f1[s] = f0[s];
+        f0[s] = nf;
+      }
+      ia2[s] = ia1[s];
+      ia1[s] = upd[s] ? __fdividef(1.f, alpha[s]) : 1.f;
+      if (upd[s]) {
+        pp[s].x = fmaf(beta[s], pp[s].x, r[s].x);
+        pp[s].y = fmaf(beta[s], pp[s].y, r[s].y);
+        sv[s].x = fmaf(beta[s], sv[s].x, w[s].x);
+        sv[s].y = fmaf(beta[s], sv[s].y, w[s].y);
+        v[s].x = fmaf(alpha[s], pp[s].x, v[s].x);
+        v[s].y = fmaf(alpha[s], pp[s].y, v[s].y);
+        r[s].x = fmaf(-alpha[s], sv[s].x, r[s].x);
+        r[s].y = fmaf(-alpha[s], sv[s].y, r[s].y);
+        alp[s] = alpha[s];
+      }
+      updp[s] = upd[s];
+    }
+    if (k == K) break;
+    __syncwarp();  // every lane's matvec reads of Ps are done
+#pragma unroll
+    for (int s = 0; s < NS; ++s) Ps[s * UP + lane] = r[s];
+    __syncwarp();
+    matvec(r, w);
+    float rd[4] = {cnorm(r[0]), r[0].x * w[0].x + r[0].y * w[0].y, cnorm(r[1]),
+                   r[1].x * w[1].x + r[1].y * w[1].y};
+    warp_sum4(rd);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      gold[s] = gam[s];
+      gam[s] = rd[2 * s];
+      dlt[s] = rd[2 * s + 1];
+    }
+  }
+  // outputs: mu = Ltilde G_ii, rho = G_ii / N0 (detect.cpp:435-441)
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    if (!live[s] || lane >= U) continue;
+    const long o = (sc * S + base + s) * static_cast<long>(U) + lane;
+    const bool ok = !broke[s];
+    const float2 xh = ok ? v[s] : make_float2(0.f, 0.f);
+    const float mu_u = ok ? f0[s] * gdiag : 0.f;
+    const float rho_u = ok ? gdiag / p.n0 : 0.f;
+    if (p.xhat) p.xhat[o] = xh;
+    if (p.mu) p.mu[o] = mu_u;
+    if (p.rho) p.rho[o] = rho_u;
+    if (p.llr) store_llrs_fast(xh, mu_u, rho_u, p.bits, p.llr + o * p.bits);
+    if (p.status && lane == 0) p.status[sc * S + base + s] = ok ? 0 : 1;
+  }
+}
+
 template <bool EXACT>
 __global__ void __launch_bounds__(256, 2) solve_rows32_kernel(const KernelParams p) {
   constexpr int UP = 32;
@@ -319,8 +483,11 @@ __global__ void __launch_bounds__(128, NS == 1 ? 5 : 4) solve_rows32_pairs_kerne
   }
   const float gdiag = __ldg(ws + W.g + lane * UP + lane).x;
   if constexpr (!EXACT) {
-    rows32_pair<false, true, NS>(p, sc, ws + W.mf, base, grow, gdiag, Ps_all[warp], nullptr,
-                                 nullptr, nullptr);
+    if constexpr (NS == 2)
+      rows32_pair_cg1(p, sc, ws + W.mf, base, grow, gdiag, Ps_all[warp]);
+    else
+      rows32_pair<false, true, NS>(p, sc, ws + W.mf, base, grow, gdiag, Ps_all[warp], nullptr,
+                                   nullptr, nullptr);
   } else {
     const int w = warp;
     // per-warp arrays indexed by the subcarrier-wide system number
