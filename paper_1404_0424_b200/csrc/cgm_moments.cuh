@@ -189,7 +189,7 @@ __device__ __forceinline__ void tile_prod(const double2* A, const double2* T, in
 // count for row i and (mirror, i != j) for row j -- through fixed slots
 // summed in a fixed order, so no separate row pass serialises the CTA.
 template <int UP, class R, bool FX = false>
-__global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelParams p) {
+__global__ void __launch_bounds__(MomGeo<UP>::NT, UP == 64 ? 2 : 1) moments_kernel(const KernelParams p) {
   using MG = MomGeo<UP>;
   using C = typename Cx<R>::T;
   static_assert(!FX || std::is_same<R, float>::value, "FX runs in FP32");
@@ -222,6 +222,78 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT) moments_kernel(const KernelPar
   __shared__ float2 cds[SPC];
   // FX: the Chebyshev coefficients of L_K and B per subcarrier (cl, cb)
   __shared__ float coefs[FX ? SPC : 1][2][kMaxK + 2];
+  if constexpr (SPC == 1) {
+    // one subcarrier per CTA (U = 64): the power iteration of cheb_interval
+    // on 2 U threads (row i, half of the columns each), so the other warps
+    // do not idle behind one warp's 7 sequential U x U products
+    if (nsc > 0) {
+      const float2* Gs = reinterpret_cast<const float2*>(Tbuf(0));
+      float2* xs = reinterpret_cast<float2*>(Abuf(0));  // scratch: x, then the two half products
+      float2* yp = xs + UP;
+      float* rd = reinterpret_cast<float*>(yp + 2 * UP);  // [warps][2]
+      const float reg = p.rho_inv_u;
+      float2 xr = make_float2(tid < UP ? 1.f : 0.f, 0.f);
+      if (tid < UP) xs[tid] = xr;
+      __syncthreads();
+      float lam = reg;
+      for (int it = 0; it <= 6; ++it) {
+        if (tid < 2 * UP) {
+          const int i = tid % UP, h = tid / UP;
+          float2 y = make_float2(0.f, 0.f);
+#pragma unroll 8
+          for (int j = h * (UP / 2); j < (h + 1) * (UP / 2); ++j) cfma_conj(y, Gs[j * LD + i], xs[j]);
+          yp[h * UP + i] = y;
+        }
+        __syncthreads();
+        float nrm = 0.f, ray = 0.f;
+        float2 y = make_float2(0.f, 0.f);
+        if (tid < UP) {
+          y = cadd(yp[tid], yp[UP + tid]);
+          y.x = fmaf(reg, xr.x, y.x);
+          y.y = fmaf(reg, xr.y, y.y);
+          nrm = cnorm(y);
+          ray = xr.x * y.x + xr.y * y.y;
+        }
+        nrm = group_sum<32>(nrm);
+        ray = group_sum<32>(ray);
+        if (lane == 0 && warp < UP / 32) {
+          rd[warp * 2] = nrm;
+          rd[warp * 2 + 1] = ray;
+        }
+        __syncthreads();
+        nrm = 0.f;
+        ray = 0.f;
+        for (int w = 0; w < UP / 32; ++w) {  // fixed order
+          nrm += rd[w * 2];
+          ray += rd[w * 2 + 1];
+        }
+        if (it > 0) lam = ray;
+        const float inv = nrm > 0.f ? rsqrtf(nrm) : 0.f;
+        if (tid < UP) {
+          xr = cscale(inv, y);
+          xs[tid] = xr;
+        }
+        __syncthreads();
+      }
+      if (warp == 0) {
+        const float lo = reg;
+        const float hi = fmaxf(1.1f * lam, 1.0001f * lo);
+        const float c = 0.5f * (lo + hi);
+        float d = 0.5f * (hi - lo);
+        if (!(d > 1e-6f * fmaxf(fabsf(c), 1e-30f))) d = fmaxf(fabsf(c), 1.f);
+        const float2 cd = make_float2(c, d);
+        if (lane == 0) {
+          cds[0] = cd;
+          p.ws[sc0 * W.stride + W.cd] = cd;
+        }
+        if constexpr (FX) {
+          const float2* hw = p.ws + sc0 * W.stride + W.t;  // K (alpha, beta) pairs
+          cheb_coef_warp(reinterpret_cast<const float*>(hw), K, cd.x, cd.y, p.rho_inv_u,
+                         coefs[0][0], coefs[0][1]);
+        }
+      }
+    }
+  } else
   for (int s = warp; s < nsc; s += NT / 32) {
     // power-iteration scratch: the A buffer (as float2)
     const float2 cd = cheb_interval<UP, LD>(reinterpret_cast<const float2*>(Tbuf(s)),
