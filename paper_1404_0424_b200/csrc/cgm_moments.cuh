@@ -554,14 +554,13 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT, UP == 64 ? 2 : 1) moments_kern
 // owns a subcarrier end to end with no block barriers: lane i keeps row i
 // of G (then Ahat) in registers (conflict-free LDS.128 reads of the padded
 // rows), runs the power iteration of cheb_interval on its row, and forms its
-// row of every product T_{a+1} = 2 Ahat T_a - T_{a-1}: (Ahat T_a)[i][j] =
-// sum_k Ahat[i][k] T_a[k][j], Ahat[i][k] from registers, row k of T_a as
-// warp-wide broadcasts (one LDS.128 per two j), 2 packed FFMA2 per complex
-// MAC.  Full rows (2x the triangle's products) in exchange for no idle
-// lanes, no tile bookkeeping and no barriers; row i's moments
-// |T_{a+1}[i][:]|^2 and Re T_{a+1}[i][:] . conj(T_a[i][:]) are summed by
-// the lane in column order.  T_{a+1} overwrites T_{a-1} (each lane its own
-// row), so two padded U x U buffers per warp.
+// part of every product T_{a+1} = 2 Ahat T_a - T_{a-1}: (Ahat T_a)[i][j] =
+// sum_k Ahat[i][k] T_a[k][j], Ahat[i][k] from registers, two lanes per
+// 16-byte chunk of row k of T_a (one LDS.128 per two j), 2 packed FFMA2 per
+// complex MAC, a Hermitian band of 18 of the 32 columns per row (see below)
+// -- every lane busy, no tile bookkeeping, no barriers; row i's moments |T_{a+1}[i][:]|^2 and
+// Re T_{a+1}[i][:] . conj(T_a[i][:]) are summed by the lane in column
+// order.  T_{a+1} overwrites T_{a-1}, so two padded U x U buffers per warp.
 constexpr int kMrW = 4;  // warps (subcarriers) per CTA
 struct MomRowsSmem {
   static constexpr int LD = 34;                  // padded row (float2): conflict-free LDS.128 per lane
@@ -677,43 +676,62 @@ __global__ void __launch_bounds__(32 * kMrW, 3) moments_rows32_kernel(const Kern
   __syncwarp();
   float2* cur = buf0;  // T_a
   float2* prv = buf1;  // T_{a-1} (a = 1: T_0 = I, implicit)
+  // T_{a+1} is Hermitian: lane i forms only the band of columns
+  // j = (i0 + q) mod 32, q = 0..17 (i0 = i rounded down to even, so the
+  // reads are aligned LDS.128 pairs), which covers every pair (i, j) with
+  // cyclic distance <= 16 from one side; the owner of a pair (distance
+  // d = j - i mod 32 in 0..15, or 16 for i < 16) writes it and its
+  // conjugate mirror -- 56% of the full-row products, exactly Hermitian
+  constexpr int NQ = 18;
+  const int i0 = i & ~1;
   for (int a = 1; a < K; ++a) {
-    unsigned long long acc[UP];
+    unsigned long long acc[NQ];
 #pragma unroll
-    for (int j = 0; j < UP; ++j) acc[j] = 0ull;
+    for (int q = 0; q < NQ; ++q) acc[q] = 0ull;
 #pragma unroll
     for (int k = 0; k < UP; ++k) {
       const float2 ak = f2unpack((k & 1) ? g[k >> 1].y : g[k >> 1].x);
       const unsigned long long ax = f2pack(ak.x, ak.x), ay = f2pack(-ak.y, ak.y);
       const float2* trow = cur + k * LD;
 #pragma unroll
-      for (int c = 0; c < UP / 2; ++c) {
-        const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(trow + 2 * c);
+      for (int c = 0; c < NQ / 2; ++c) {
+        const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(trow + ((i0 + 2 * c) & (UP - 1)));
         ffma2(acc[2 * c], t.x, ax);
         ffma2(acc[2 * c], f2swap_hl(t.x), ay);
         ffma2(acc[2 * c + 1], t.y, ax);
         ffma2(acc[2 * c + 1], f2swap_hl(t.y), ay);
       }
     }
-    // T_{a+1} row i, its moments against T_a row i, then it replaces T_{a-1}
-    float n2 = 0.f, x2 = 0.f;
-    float2 nxt[UP];
+    float2 nx[NQ];
 #pragma unroll
-    for (int j = 0; j < UP; ++j) {
+    for (int q = 0; q < NQ; ++q) {
+      const int j = (i0 + q) & (UP - 1);
       const float2 pr = a == 1 ? make_float2(j == i ? 1.f : 0.f, 0.f) : prv[i * LD + j];
-      const float2 v = f2unpack(acc[j]);
-      float2 nx = make_float2(2.f * v.x - pr.x, 2.f * v.y - pr.y);
-      if (j == i) nx.y = 0.f;
-      const float2 cu = cur[i * LD + j];
-      n2 += cnorm(nx);
-      x2 += nx.x * cu.x + nx.y * cu.y;
-      nxt[j] = nx;
+      const float2 v = f2unpack(acc[q]);
+      nx[q] = make_float2(2.f * v.x - pr.x, 2.f * v.y - pr.y);
+      if (j == i) nx[q].y = 0.f;
     }
-    __syncwarp();  // every lane's reads of T_a rows are done before T_a becomes T_{a-1}
+    __syncwarp();  // every lane's reads of T_{a-1} are done before it is overwritten
 #pragma unroll
-    for (int j = 0; j < UP; j += 2)
-      *reinterpret_cast<float4*>(prv + i * LD + j) = make_float4(nxt[j].x, nxt[j].y, nxt[j + 1].x, nxt[j + 1].y);
-    __syncwarp();
+    for (int q = 0; q < NQ; ++q) {
+      const int j = (i0 + q) & (UP - 1), d = (j - i) & (UP - 1);
+      if (d <= 15 || (d == 16 && i < 16)) {
+        prv[i * LD + j] = nx[q];
+        if (d != 0) prv[j * LD + i] = make_float2(nx[q].x, -nx[q].y);
+      }
+    }
+    __syncwarp();  // T_{a+1} complete
+    // row i's moments: |T_{a+1}[i][:]|^2 and Re T_{a+1}[i][:] . conj(T_a[i][:]), column order
+    float n2 = 0.f, x2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < UP / 2; ++c) {
+      const float4 nv = *reinterpret_cast<const float4*>(prv + i * LD + 2 * c);
+      const float4 cu = *reinterpret_cast<const float4*>(cur + i * LD + 2 * c);
+      n2 += nv.x * nv.x + nv.y * nv.y;
+      n2 += nv.z * nv.z + nv.w * nv.w;
+      x2 += nv.x * cu.x + nv.y * cu.y;
+      x2 += nv.z * cu.z + nv.w * cu.w;
+    }
     mom[(2 * a + 1) * UP + i] = 2.0 * static_cast<double>(x2) - d1;  // D_{2a+1}
     mom[(2 * a + 2) * UP + i] = 2.0 * static_cast<double>(n2) - 1.0;  // D_{2a+2}
     float2* t = cur;
