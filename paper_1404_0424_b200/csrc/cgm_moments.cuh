@@ -960,6 +960,54 @@ __device__ __forceinline__ void moments_coefs_lane(const float* hist, double cc,
   out[kLaneScratch - 1] = l0[0];
 }
 
+// moments_tail for K <= kLaneK: the coefficients of all S systems at once,
+// one lane each (moments_coefs_lane), then a warp per system, a lane per row.
+// Threads [0, nthr) take part and synchronise on named barrier `bar_id`
+// (0 with nthr = blockDim.x is __syncthreads); msh holds S x kLaneScratch
+// doubles.
+template <int UP>
+__device__ __forceinline__ void moments_tail_lanes(const KernelParams& p, const float2* ws,
+                                                   const WsOffsets& W, long sc, int Kmax,
+                                                   const float* hist, const float2* Vs,
+                                                   const uint8_t* sys_st, double* msh, int nthr,
+                                                   int bar_id) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = nthr >> 5;
+  const int S = p.S, U = p.U, K = p.K;
+  const float2 cdv = ws[W.cd];
+  const double* mom = reinterpret_cast<const double*>(ws + W.t);
+  for (int s = threadIdx.x; s < S; s += nthr) {
+    const float* hs = hist + s * Kmax * 2;
+    double* o = msh + s * kLaneScratch;
+    switch (K) {
+      case 1: moments_coefs_lane<1>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
+      case 2: moments_coefs_lane<2>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
+      case 3: moments_coefs_lane<3>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
+      case 4: moments_coefs_lane<4>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
+      case 5: moments_coefs_lane<5>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
+      default: moments_coefs_lane<6>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
+    }
+  }
+  named_sync(bar_id, nthr);
+  for (int s = warp; s < S; s += nw) {
+    const double* sh = msh + s * kLaneScratch;
+    const MomCoef c = {sh[kLaneScratch - 2], sh[kLaneScratch - 1]};
+    const bool ok = sys_st[s] == 0;
+    for (int i = lane; i < U; i += 32) {
+      float mu, rho;
+      moments_row(sh, c, K, mom, UP, i, p.es, p.n0, mu, rho, kLaneK);
+      const long o = (sc * S + s) * static_cast<long>(U) + i;
+      const float2 xh = ok ? Vs[s * UP + i] : make_float2(0.f, 0.f);
+      if (!ok) mu = rho = 0.f;
+      if (p.xhat) p.xhat[o] = xh;
+      if (p.mu) p.mu[o] = mu;
+      if (p.rho) p.rho[o] = rho;
+      if (p.llr) store_llrs_fast(xh, mu, rho, p.bits, p.llr + o * p.bits);
+    }
+    if (p.status && lane == 0) p.status[sc * S + s] = ok ? 0 : 1;
+  }
+  named_sync(bar_id, nthr);  // msh is reused by the next subcarrier
+}
+
 // Exact-tracker outputs of a subcarrier's S uplink systems after the CG
 // (CTA-wide, warp per system): hist holds each system's (alpha, beta)
 // history (stride Kmax), Vs its v_K, sys_st its breakdown flag; msh is
@@ -974,39 +1022,7 @@ __device__ __forceinline__ void moments_tail(const KernelParams& p, const float2
   const float2 cdv = ws[W.cd];
   const double* mom = reinterpret_cast<const double*>(ws + W.t);
   if (K <= kLaneK && S * kLaneScratch <= nw * kMomScratch) {
-    // coefficients of all S systems at once, one lane each; then a warp
-    // per system, a lane per row
-    for (int s = threadIdx.x; s < S; s += nt) {
-      const float* hs = hist + s * Kmax * 2;
-      double* o = msh + s * kLaneScratch;
-      switch (K) {
-        case 1: moments_coefs_lane<1>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
-        case 2: moments_coefs_lane<2>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
-        case 3: moments_coefs_lane<3>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
-        case 4: moments_coefs_lane<4>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
-        case 5: moments_coefs_lane<5>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
-        default: moments_coefs_lane<6>(hs, cdv.x, cdv.y, p.rho_inv_u, o); break;
-      }
-    }
-    __syncthreads();
-    for (int s = warp; s < S; s += nw) {
-      const double* sh = msh + s * kLaneScratch;
-      const MomCoef c = {sh[kLaneScratch - 2], sh[kLaneScratch - 1]};
-      const bool ok = sys_st[s] == 0;
-      for (int i = lane; i < U; i += 32) {
-        float mu, rho;
-        moments_row(sh, c, K, mom, UP, i, p.es, p.n0, mu, rho, kLaneK);
-        const long o = (sc * S + s) * static_cast<long>(U) + i;
-        const float2 xh = ok ? Vs[s * UP + i] : make_float2(0.f, 0.f);
-        if (!ok) mu = rho = 0.f;
-        if (p.xhat) p.xhat[o] = xh;
-        if (p.mu) p.mu[o] = mu;
-        if (p.rho) p.rho[o] = rho;
-        if (p.llr) store_llrs_fast(xh, mu, rho, p.bits, p.llr + o * p.bits);
-      }
-      if (p.status && lane == 0) p.status[sc * S + s] = ok ? 0 : 1;
-    }
-    __syncthreads();  // msh is reused by the next subcarrier
+    moments_tail_lanes<UP>(p, ws, W, sc, Kmax, hist, Vs, sys_st, msh, nt, 0);
     return;
   }
   double* sh = msh + warp * kMomScratch;
