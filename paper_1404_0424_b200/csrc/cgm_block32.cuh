@@ -61,6 +61,128 @@ struct Block32Smem {
 // Gs = the subcarrier's G in shared memory, Ps = this warp's NS broadcast
 // rows.  Approximate uplink systems write their outputs; exact / downlink
 // systems leave v in Vs and (exact) the history in hist.
+// Exact tracker (cfg5): the same CG with the per-system scalar work done by
+// the system's 8 owner lanes only.  After each reduction lane L holds the sum
+// of system (L >> 3) & 3 (warp_sum4_owned); it alone applies the freeze /
+// breakdown rules, forms alpha (then beta) and records the (alpha, beta)
+// history, and one shuffle per system hands the step lengths to the warp.
+// A system that does not update at iteration k never updates again (frozen
+// residuals stay frozen, breakdowns stick, k only grows past its iteration
+// count), so it is given alpha = 0 -- v and r unchanged -- and its p may be
+// overwritten freely.
+__device__ __forceinline__ void block32_cg_exact(const KernelParams& p, const float2* mfsrc,
+                                                 const float2* Ts, int base, const float2* Gs,
+                                                 float2* Ps, float* hist, float2* Vs,
+                                                 uint8_t* sys_st, float2* zout) {
+  constexpr int UP = 32, NS = kBlkNS;
+  const int S = p.S, St = p.St, U = p.U;
+  const int nsys = S + St;
+  const int Kmax = p.K > p.Kt ? p.K : p.Kt;
+  const int lane = threadIdx.x & 31;
+  float reg[NS];
+  float2 v[NS], r[NS], pp[NS];
+  float nrm[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int sy = base + s;
+    const bool live = sy < nsys, down = sy >= S;
+    reg[s] = down ? p.rho_inv_d : p.rho_inv_u;
+    float2 b = make_float2(0.f, 0.f);
+    if (live && lane < U) b = down ? Ts[(sy - S) * U + lane] : mfsrc[sy * UP + lane];
+    v[s] = make_float2(0.f, 0.f);
+    r[s] = b;
+    pp[s] = b;
+    Ps[s * UP + lane] = b;
+    nrm[s] = cnorm(b);
+  }
+  // this lane's system
+  const int my = (lane >> 3) & 3, sy_own = base + my;
+  const bool live_own = sy_own < nsys, down_own = sy_own >= S;
+  const int iters_own = live_own ? (down_own ? p.Kt : p.K) : 0;
+  float rn = warp_sum4_owned(nrm);
+  const float rn0 = rn;
+  bool broke = false;
+  __syncwarp();
+  for (int k = 1; k <= Kmax; ++k) {
+    // e = (G + reg I) p on the packed pipe; G[u][j] = conj(G[j][u])
+    unsigned long long a0[NS], b0[NS], a1[NS], b1[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) a0[s] = b0[s] = a1[s] = b1[s] = 0ull;
+#pragma unroll 4
+    for (int j = 0; j < UP; j += 2) {
+      const float2 gj0 = Gs[j * UP + lane], gj1 = Gs[(j + 1) * UP + lane];
+      const unsigned long long g0 = f2pack(gj0.x, -gj0.y), g1 = f2pack(gj1.x, -gj1.y);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const ulonglong2 pj = *reinterpret_cast<const ulonglong2*>(Ps + s * UP + j);
+        ffma2(a0[s], g0, f2dup_lo(pj.x));
+        ffma2(b0[s], g0, f2dup_hi(pj.x));
+        ffma2(a1[s], g1, f2dup_lo(pj.y));
+        ffma2(b1[s], g1, f2dup_hi(pj.y));
+      }
+    }
+    float2 e[NS];
+    float part[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const float2 A0 = f2unpack(a0[s]), B0 = f2unpack(b0[s]);
+      const float2 A1 = f2unpack(a1[s]), B1 = f2unpack(b1[s]);
+      e[s].x = (A0.x - B0.y) + (A1.x - B1.y);
+      e[s].y = (B0.x + A0.y) + (B1.x + A1.y);
+      e[s].x = fmaf(reg[s], pp[s].x, e[s].x);
+      e[s].y = fmaf(reg[s], pp[s].y, e[s].y);
+      part[s] = pp[s].x * e[s].x + pp[s].y * e[s].y;  // Re p^H e
+    }
+    const float curv = warp_sum4_owned(part);
+    // owner lanes: solvers.cpp:21-27 freeze, :55-57 breakdown
+    const bool step = k <= iters_own;
+    const bool frozen = !(rn > 1e-28f * rn0);
+    const bool go = step && !frozen && !broke;
+    if (go && curv < 1e-30f) broke = true;
+    const bool upd = go && !broke;
+    const float alpha = upd ? __fdividef(rn, curv) : 1.f;
+    const float a_eff = upd ? alpha : 0.f;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const float as = __shfl_sync(0xffffffffu, a_eff, s << 3);
+      v[s].x = fmaf(as, pp[s].x, v[s].x);
+      v[s].y = fmaf(as, pp[s].y, v[s].y);
+      r[s].x = fmaf(-as, e[s].x, r[s].x);
+      r[s].y = fmaf(-as, e[s].y, r[s].y);
+      part[s] = cnorm(r[s]);
+    }
+    const float rnx = warp_sum4_owned(part);
+    const float beta = upd ? rnx * __fdividef(1.f, rn) : 0.f;
+    if (upd) rn = rnx;
+    if (step && !down_own && (lane & 7) == 0) {  // the exact tracker's history
+      hist[(sy_own * Kmax + (k - 1)) * 2 + 0] = alpha;
+      hist[(sy_own * Kmax + (k - 1)) * 2 + 1] = beta;
+    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const float bs = __shfl_sync(0xffffffffu, beta, s << 3);
+      pp[s].x = fmaf(bs, pp[s].x, r[s].x);
+      pp[s].y = fmaf(bs, pp[s].y, r[s].y);
+    }
+    __syncwarp();  // every lane's matvec reads of Ps are done
+#pragma unroll
+    for (int s = 0; s < NS; ++s) Ps[s * UP + lane] = pp[s];
+    __syncwarp();
+  }
+  // ------------------------------------------------ per-system epilogue
+  if (live_own && (lane & 7) == 0) {
+    if (down_own) zout[St * UP + (sy_own - S)] = make_float2(broke ? 1.f : 0.f, 0.f);
+    else sys_st[sy_own] = broke ? 1 : 0;
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int sy = base + s;
+    if (sy >= nsys) continue;
+    if (sy >= S) zout[(sy - S) * UP + lane] = v[s];  // v_K for precode_q_kernel
+    else Vs[sy * UP + lane] = v[s];
+  }
+}
+
 template <bool EXACT>
 __device__ __forceinline__ void block32_cg(const KernelParams& p, long sc, const float2* mfsrc,
                                            const float2* Ts, int base, const float2* Gs,
@@ -271,9 +393,13 @@ __global__ void __launch_bounds__(256, 2) block32_kernel(const KernelParams p) {
     const float2* wsb = reinterpret_cast<const float2*>(bufp(i));  // smem copy of the ws span
     const float2* Ts = reinterpret_cast<const float2*>(bufp(i) + L.tb);
     float2* zout = p.ws + lsc * W.stride + W.z;
-    for (int base = warp * kBlkNS; base < nsys; base += nw * kBlkNS)
-      block32_cg<EXACT>(p, sc, wsb + W.mf, Ts, base, wsb + W.g, Ps + base * UP, hist, Vs, sys_st,
-                        zout);
+    for (int base = warp * kBlkNS; base < nsys; base += nw * kBlkNS) {
+      if constexpr (EXACT)
+        block32_cg_exact(p, wsb + W.mf, Ts, base, wsb + W.g, Ps + base * UP, hist, Vs, sys_st, zout);
+      else
+        block32_cg<EXACT>(p, sc, wsb + W.mf, Ts, base, wsb + W.g, Ps + base * UP, hist, Vs, sys_st,
+                          zout);
+    }
     if (EXACT && S > 0) {
       __syncthreads();
       moments_tail<UP>(p, wsb, W, sc, Kmax, hist, Vs, sys_st, nt,

@@ -69,6 +69,24 @@ __device__ __forceinline__ void warp_sum4(float (&v)[4]) {
   for (int q = 0; q < 4; ++q) v[q] = __shfl_sync(0xffffffffu, k, q << 3);
 }
 
+// warp_sum4 without the final gather: lane L returns the sum of value
+// (L >> 3) & 3 (5 shuffles + 1 select) -- for per-system scalar work done
+// once per system by its 8 owner lanes instead of by all 32 lanes per system
+__device__ __forceinline__ float warp_sum4_owned(const float (&v)[4]) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = lane & 16, b3 = lane & 8;
+  float k0 = b4 ? v[2] : v[0], k1 = b4 ? v[3] : v[1];
+  const float s0 = b4 ? v[0] : v[2], s1 = b4 ? v[1] : v[3];
+  k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+  float k = b3 ? k1 : k0;
+  k += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  return k;
+}
+
 // CG for the systems base, base + 1 of subcarrier sc on one warp (lane =
 // user row), with row `lane` of G in `grow`; Ps = this warp's two broadcast
 // rows.  Approx uplink systems write their outputs here; exact / downlink
