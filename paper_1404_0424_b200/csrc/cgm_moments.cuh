@@ -189,7 +189,7 @@ __device__ __forceinline__ void tile_prod(const double2* A, const double2* T, in
 // count for row i and (mirror, i != j) for row j -- through fixed slots
 // summed in a fixed order, so no separate row pass serialises the CTA.
 template <int UP, class R, bool FX = false>
-__global__ void __launch_bounds__(MomGeo<UP>::NT, UP == 64 ? 2 : 1) moments_kernel(const KernelParams p) {
+__global__ void __launch_bounds__(MomGeo<UP>::NT, UP == 32 ? 4 : 2) moments_kernel(const KernelParams p) {
   using MG = MomGeo<UP>;
   using C = typename Cx<R>::T;
   static_assert(!FX || std::is_same<R, float>::value, "FX runs in FP32");
@@ -848,7 +848,12 @@ __device__ __forceinline__ void moments_row(const double* sh, MomCoef c, int K, 
   const double cross = m * lii + efd - e * f;
   const double nu2 = interf * es + cross * n0;
   mu = static_cast<float>(m);
-  rho = nu2 < 1e-300 ? 0.f : static_cast<float>(m * m / nu2);
+  // safe_rho (detect.cpp:26-29); the quotient in FP32 (FP64 division is a
+  // long dependent sequence) unless nu2 leaves FP32's normal range
+  const double mm = m * m;
+  rho = nu2 < 1e-300 ? 0.f
+        : (nu2 > 1e-30 && mm < 1e30) ? __fdividef(static_cast<float>(mm), static_cast<float>(nu2))
+                                     : static_cast<float>(mm / nu2);
 }
 
 // FX mode, one vector per subcarrier (S = 1): after the CG, x_hat and the
@@ -915,8 +920,11 @@ __device__ __forceinline__ void moments_coefs_lane(const float* hist, double cc,
   l0[0] = al[1];  // L_1 = alpha_1 I
 #pragma unroll
   for (int k = 2; k <= K; ++k) {  // detect.cpp:336-368 on the coefficients
-    const double c1 = al[k] * (1.0 + be[k - 1]) / al[k - 1];
-    const double c2 = al[k] * be[k - 2] / al[k - 2];
+    // the ratios of the CG's FP32 step lengths in FP32 (off the FP64 chain)
+    const double c1 = static_cast<double>(__fdividef(static_cast<float>(al[k] * (1.0 + be[k - 1])),
+                                                     static_cast<float>(al[k - 1])));
+    const double c2 = static_cast<double>(__fdividef(static_cast<float>(al[k] * be[k - 2]),
+                                                     static_cast<float>(al[k - 2])));
     double d1[n], t[n];
 #pragma unroll
     for (int m = 0; m < n; ++m) d1[m] = l0[m] - l1[m];
