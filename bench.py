@@ -269,11 +269,16 @@ def ours_arm(args, rank, world, local_rank):
     # over the ranks (strong scaling); the small configs give every rank a
     # whole batch of its own subcarriers (weak scaling)
     strong = cfg_all.name == "cfg5"
+    fps = 1
     if strong:
         sc_lo, sc_hi = shard_range(cfg_all.n_sc, rank, world)
         cfg = cfg_all.scaled(sc_hi - sc_lo)
     else:
-        cfg = cfg_all
+        # small configs: a step is a stream of frames in one call (SURVEY 7,
+        # hard part 2) -- by default enough frames for ~0.5 M vectors per step
+        frame_in = cfg_all.n_sc * (cfg_all.B * cfg_all.U + cfg_all.S * cfg_all.B) * 8
+        fps = args.frames_per_step or max(1, int(1e9 // frame_in))  # ~1 GB of H + Y per step
+        cfg = cfg_all.scaled(cfg_all.n_sc * fps)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     ctx = Context(local_rank)
@@ -379,7 +384,7 @@ def ours_arm(args, rank, world, local_rank):
     torch.cuda.synchronize()
     ch_ms, bs_ms, sv_ms, n_pairs = ctx.kernel_times_ex()
     ctx.set_profiling(False)
-    job_vectors = cfg_all.vectors if strong else world * cfg.vectors  # per step, all ranks
+    job_vectors = cfg_all.vectors if strong else world * cfg.vectors  # per step, all ranks (x frames)
     value = job_vectors * args.steps / (total_ms / 1e3)
     # the hot path of one step is one channel + one solve launch per L2 chunk
     kernel_ms = (ch_ms + bs_ms + sv_ms) / args.steps
@@ -388,6 +393,10 @@ def ours_arm(args, rank, world, local_rank):
     def pinned(shape, dtype):
         return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
 
+    # e2e batches: at most ~512 MB of inputs per call (pinned host memory);
+    # the metric is the same vectors/s
+    per_sc_in = (cfg.B * cfg.U + cfg.S * cfg.B + (cfg.S * cfg.U if cfg.kind == "both" else 0)) * 8
+    e2e_sc = cfg.n_sc if strong else int(min(cfg.n_sc, max(1, 512e6 // per_sc_in)))
     h_frames = []
     for fr in frames[: min(2, n_frames)]:
         hf = []
@@ -395,27 +404,27 @@ def ours_arm(args, rank, world, local_rank):
             if t is None:
                 hf.append(None)
                 continue
-            a = pinned(tuple(t.shape), torch.complex64)
-            a[...] = t.cpu().numpy()
+            a = pinned((e2e_sc, *tuple(t.shape[1:])), torch.complex64)
+            a[...] = t[:e2e_sc].cpu().numpy()
             hf.append(a)
         h_frames.append(hf)
     S, U, B, bits = cfg.S, cfg.U, cfg.B, cfg.qam_bits
     if cfg.kind == "downlink":
-        h_out = {"q": pinned((cfg.n_sc, S, B), torch.complex64),
-                 "s": pinned((cfg.n_sc, S, B), torch.complex64),
-                 "gain": pinned((cfg.n_sc, S), torch.float32),
-                 "status": pinned((cfg.n_sc, S), torch.uint8)}
+        h_out = {"q": pinned((e2e_sc, S, B), torch.complex64),
+                 "s": pinned((e2e_sc, S, B), torch.complex64),
+                 "gain": pinned((e2e_sc, S), torch.float32),
+                 "status": pinned((e2e_sc, S), torch.uint8)}
     else:
-        h_out = {"xhat": pinned((cfg.n_sc, S, U), torch.complex64),
-                 "mu": pinned((cfg.n_sc, S, U), torch.float32),
-                 "rho": pinned((cfg.n_sc, S, U), torch.float32),
-                 "llr": pinned((cfg.n_sc, S, U, bits), torch.float32),
-                 "status": pinned((cfg.n_sc, S), torch.uint8)}
+        h_out = {"xhat": pinned((e2e_sc, S, U), torch.complex64),
+                 "mu": pinned((e2e_sc, S, U), torch.float32),
+                 "rho": pinned((e2e_sc, S, U), torch.float32),
+                 "llr": pinned((e2e_sc, S, U, bits), torch.float32),
+                 "status": pinned((e2e_sc, S), torch.uint8)}
         if cfg.kind == "both":
-            h_out.update({"q": pinned((cfg.n_sc, S, B), torch.complex64),
-                          "s": pinned((cfg.n_sc, S, B), torch.complex64),
-                          "gain": pinned((cfg.n_sc, S), torch.float32),
-                          "pstatus": pinned((cfg.n_sc, S), torch.uint8)})
+            h_out.update({"q": pinned((e2e_sc, S, B), torch.complex64),
+                          "s": pinned((e2e_sc, S, B), torch.complex64),
+                          "gain": pinned((e2e_sc, S), torch.float32),
+                          "pstatus": pinned((e2e_sc, S), torch.uint8)})
     h2d = sum(a.nbytes for a in h_frames[0] if a is not None)
     d2h = sum(a.nbytes for a in h_out.values())
 
@@ -438,7 +447,8 @@ def ours_arm(args, rank, world, local_rank):
         e2e_step(i)
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     barrier()
-    e2e_value = job_vectors * args.steps / e2e_s
+    e2e_vectors = cfg_all.vectors if strong else world * e2e_sc * cfg.S
+    e2e_value = e2e_vectors * args.steps / e2e_s
 
     # ---------------------------------------------------- gather (N > 1 only)
     gather = None
@@ -581,10 +591,12 @@ def ours_arm(args, rank, world, local_rank):
             "data": "synthetic (seeded device generator, reference Rng streams)",
             "config": {**workload_config(cfg_all, {"n": n_frames, "bytes": n_frames * frame_bytes},
                                          world=world),
-                       "cuda_graphs": graph_note},
+                       "cuda_graphs": graph_note,
+                       **({} if strong else {"frames_per_step": fps,
+                                             "vectors_per_step_per_gpu": cfg.vectors})},
             "llr_gbit_s": value * cfg.U * cfg.qam_bits / 1e9 if cfg.kind != "downlink" else None,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h, "vectors_per_call_per_gpu": e2e_sc * cfg.S},
             "gpu_launches": launches,
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -603,6 +615,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg5")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--frames-per-step", type=int, default=0,
+                    help="weak-scaling configs: frames of the config per step, in one call "
+                         "(default: ~1 GB of H + Y per step)")
     ap.add_argument("--gather-chunks", type=int, default=4,
                     help="N > 1, cfg5: chunks per rank of the overlapped output gather")
     ap.add_argument("--no-graphs", action="store_true",

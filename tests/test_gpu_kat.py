@@ -220,3 +220,40 @@ def test_c_abi_nccl_gather_single_rank(gpu_ctx):
     torch.cuda.synchronize()
     assert torch.equal(recv, send)
     comm.close()
+
+
+def test_sharded_pipeline_nccl_single_rank_equals_direct_call(gpu_ctx):
+    """parallel.ShardedPipeline through the product C ABI (NcclTransport ->
+    cgm_gatherv on a one-rank communicator) on a cfg5-shaped job, 3 chunks:
+    the chunked compute + in-place gather gives bitwise the one-call result
+    (the root's own chunks are computed straight into the whole-job buffers,
+    so cgm_gatherv's self-displacement path is exercised)."""
+    import torch
+
+    from paper_1404_0424_b200 import Context, get_config
+    from paper_1404_0424_b200.parallel import (Comm, NcclTransport, ShardedPipeline,
+                                               detect_precode_outputs)
+
+    cfg = get_config("cfg5").scaled(300)
+    rs = torch.tensor(cfg.rsqrt())
+    H, Y = gpu_ctx.generate_uplink(cfg.B, cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits, cfg.n0,
+                                   rsqrt=rs)
+    T = gpu_ctx.generate_symbols(cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits)
+    want = gpu_ctx.detect_precode_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                                     cfg.tracker, T, cfg.rho_d, cfg.K)
+    comm = Comm(Context(0), 1, 0, Comm.unique_id())
+    spec = detect_precode_outputs(cfg)
+    pipe = ShardedPipeline(cfg.n_sc, 0, 1, spec, NcclTransport(comm), n_chunks=3,
+                           device=torch.device("cuda", 0))
+
+    def compute(a, b, views):
+        o = dict(views)
+        gpu_ctx.detect_precode_cg(H[a:b], Y[a:b], cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                                  cfg.tracker, T[a:b], cfg.rho_d, cfg.K, out=o,
+                                  want=tuple(views))
+
+    got = pipe.run(compute)
+    torch.cuda.synchronize()
+    for k in spec:
+        assert torch.equal(got[k], want[k]), k
+    comm.close()
