@@ -382,12 +382,13 @@ def ours_arm(args, rank, world, local_rank):
     for i in range(args.steps):
         step(args.warmup + i)
     torch.cuda.synchronize()
-    ch_ms, bs_ms, sv_ms, n_pairs = ctx.kernel_times_ex()
+    kms, n_pairs = ctx.kernel_times_kinds()
+    ch_ms, bs_ms, sv_ms, pq_ms = kms["channel"], kms["moments"], kms["solve"], kms["precoder"]
     ctx.set_profiling(False)
     job_vectors = cfg_all.vectors if strong else world * cfg.vectors  # per step, all ranks (x frames)
     value = job_vectors * args.steps / (total_ms / 1e3)
     # the hot path of one step is one channel + one solve launch per L2 chunk
-    kernel_ms = (ch_ms + bs_ms + sv_ms) / args.steps
+    kernel_ms = (ch_ms + bs_ms + sv_ms + pq_ms) / args.steps
 
     # ------------------------------------------------------------ e2e (host)
     def pinned(shape, dtype):
@@ -515,9 +516,15 @@ def ours_arm(args, rank, world, local_rank):
     k_ch = kernel_roof("channel (Gram + matched filter; tcgen05 for U = 32)",
                        cfg.channel_flops_per_vector() * cfg.vectors,
                        cfg.channel_bytes_per_vector() * cfg.vectors, ch_s, traffic.get("channel"))
-    k_sv = kernel_roof("solve (CG + SINR extraction + LLR [+ precoder])",
-                       cfg.solve_kernel_flops_per_vector() * cfg.vectors,
-                       cfg.solve_bytes_per_vector() * cfg.vectors, sv_s, traffic.get("solve"))
+    pq_s = pq_ms / args.steps / 1e3
+    sep = pq_s > 0  # the precoder runs as its own kernel (detect + precode calls)
+    pf = cfg.precoder_flops_per_vector() * cfg.vectors if sep else 0.0
+    pb = cfg.precoder_bytes_per_vector() * cfg.vectors if sep else 0.0
+    k_sv = kernel_roof("solve (CG + SINR extraction + LLR" + ("" if sep else " [+ precoder]") + ")",
+                       cfg.solve_kernel_flops_per_vector() * cfg.vectors - pf,
+                       cfg.solve_bytes_per_vector() * cfg.vectors - pb, sv_s, traffic.get("solve"))
+    k_pq = (kernel_roof("precoder (q = H_d^H v, gain, s; H re-read)", pf, pb, pq_s,
+                        traffic.get("precoder")) if sep else None)
     bs_s = bs_ms / args.steps / 1e3
     k_bs = None
     if bs_s > 0:  # exact tracker: row moments of the Chebyshev basis (cgm_moments.cuh)
@@ -525,7 +532,8 @@ def ours_arm(args, rank, world, local_rank):
                            "moments per subcarrier)",
                            cfg.basis_flops_per_vector() * cfg.vectors, 0.0, bs_s,
                            traffic.get("moments"))
-    shares = [(sv_s, k_sv), (ch_s, k_ch)] + ([(bs_s, k_bs)] if k_bs else [])
+    shares = ([(sv_s, k_sv), (ch_s, k_ch)] + ([(bs_s, k_bs)] if k_bs else [])
+              + ([(pq_s, k_pq)] if k_pq else []))
     dom_s, dom = max(shares, key=lambda x: x[0])
     if ch_s == 0 and sv_s > 0:
         # one fused kernel does the whole path (U <= 16 precoder,
@@ -548,8 +556,9 @@ def ours_arm(args, rank, world, local_rank):
     roof = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"],
             "unit": dom["unit"], "frac": dom["frac"], "traffic": dom["traffic"],
             "peak_source": dom["peak_source"], "kernel": dom["kernel"],
-            "share_of_step": dom_s / max(ch_s + bs_s + sv_s, 1e-12),
-            "kernels": {"channel": k_ch, "solve": k_sv, **({"moments": k_bs} if k_bs else {})},
+            "share_of_step": dom_s / max(ch_s + bs_s + sv_s + pq_s, 1e-12),
+            "kernels": {"channel": k_ch, "solve": k_sv, **({"moments": k_bs} if k_bs else {}),
+                        **({"precoder": k_pq} if k_pq else {})},
             "pair": {"kernel_ms": kernel_ms, "launch_pairs_per_step": n_pairs / args.steps,
                      "algorithmic_flops": flops_launch, "algorithmic_bytes": bytes_launch,
                      "tflops": flops_launch / (kernel_ms / 1e3) / 1e12,

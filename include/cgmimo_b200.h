@@ -70,7 +70,10 @@ int cgm_synchronize(cgm_ctx* ctx);
 /* Kernel-variant switches for A/B tests (bit mask; 0 = production
  * defaults): 1 = FFMA channel kernel instead of tcgen05 for U = 32,
  * 2 = channel + solve pair instead of the fused U <= 16 kernels,
- * 4 = lane-per-row solve kernel instead of the U = 32 row kernels.
+ * 4 = lane-per-row solve kernel instead of the U = 32 row kernels,
+ * 8 = shared-G block kernel for uplink-only U = 32, 16 = 8-warp row CTA
+ * instead of the block kernel, 64 = 4x4-tile moments kernel instead of the
+ * warp-per-subcarrier one (32: test only, NaN-poisoned workspace).
  * Every variant is parity-tested against the default. */
 int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy);
 /* Per-kernel device timing: while on, every channel/solve launch pair is
@@ -83,6 +86,10 @@ int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, lon
  * reported on its own as basis_ms (cgm_ctx_kernel_times adds it to channel_ms). */
 int cgm_ctx_kernel_times_ex(cgm_ctx* ctx, double* channel_ms, double* basis_ms, double* solve_ms,
                             long* launches);
+/* Same, by kind: ms[0] channel, ms[1] exact-tracker moments, ms[2] solve
+ * (CG, extraction, LLRs), ms[3] the separate precoder kernel (q = H_d^H v,
+ * gain, s; cgm_ctx_kernel_times_ex counts it in solve_ms). */
+int cgm_ctx_kernel_times_kinds(cgm_ctx* ctx, double ms[4], long* launches);
 const char* cgm_last_error(const cgm_ctx* ctx);
 /* kernels this context has launched since creation (the bench's gpu_launches) */
 long cgm_kernel_launches(const cgm_ctx* ctx);

@@ -34,6 +34,7 @@ SIGNATURES = {
     "cgm_ctx_set_kernel_policy": (_int, [_vp, _int]),
     "cgm_ctx_set_profiling": (_int, [_vp, _int]),
     "cgm_ctx_kernel_times": (_int, [_vp, C.POINTER(_dbl), C.POINTER(_dbl), C.POINTER(_long)]),
+    "cgm_ctx_kernel_times_kinds": (_int, [_vp, C.POINTER(_dbl), C.POINTER(_long)]),
     "cgm_ctx_kernel_times_ex": (_int, [_vp, C.POINTER(_dbl), C.POINTER(_dbl), C.POINTER(_dbl),
                                        C.POINTER(_long)]),
     "cgm_last_error": (C.c_char_p, [_vp]),

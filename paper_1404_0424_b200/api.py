@@ -120,6 +120,14 @@ class Context:
                                                      C.byref(n)))
         return a.value, b.value, c.value, n.value
 
+    def kernel_times_kinds(self):
+        """({"channel", "moments", "solve", "precoder"}: ms, launches) summed since
+        profiling was enabled (the precoder kernel separate from the solve)."""
+        ms = (C.c_double * 4)()
+        n = C.c_long()
+        self._check(self.lib.cgm_ctx_kernel_times_kinds(self.h, ms, C.byref(n)))
+        return dict(zip(("channel", "moments", "solve", "precoder"), list(ms))), n.value
+
     def kernel_times(self):
         """(channel_ms, solve_ms, launches) summed since profiling was enabled."""
         a, b, n = C.c_double(), C.c_double(), C.c_long()

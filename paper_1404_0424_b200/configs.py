@@ -135,6 +135,17 @@ class Config:
         return (self.solve_flops_per_vector() - self.tracker_extract_flops_per_vector()
                 + self.moments_extract_flops_per_vector())
 
+    def precoder_flops_per_vector(self) -> float:
+        """q = H_d^H v (8 B U) and the gain ||q|| (4 B) of a transmit vector --
+        the separate precoder kernel of detect + precode calls (cgm_block32.cuh)."""
+        return 8 * self.B * self.U + 4 * self.B if self.kind == "both" else 0.0
+
+    def precoder_bytes_per_vector(self) -> float:
+        """H re-read (shared by S vectors), v_K in, q and s out, gain + status."""
+        if self.kind != "both":
+            return 0.0
+        return 8 * self.B * self.U / self.S + 8 * self.U + 16 * self.B + 5
+
     def solve_bytes_per_vector(self) -> float:
         """Outputs written by the solve kernel (+ t read, H re-read by the precoder)."""
         return self.bytes_per_vector() - self.channel_bytes_per_vector()

@@ -206,7 +206,7 @@ int ensure_ws(cgm_ctx* ctx, size_t need) {
 }
 
 // one timed launch: CUDA events around it on `st` when profiling (kind 1
-// channel, 2 solve, 3 exact-tracker moments)
+// channel, 2 solve, 3 exact-tracker moments, 4 the separate precoder kernel)
 template <class F>
 int timed(cgm_ctx* ctx, cudaStream_t st, int kind, F&& go) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -449,7 +449,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
     if (mode == kBlock && p.St > 0) {  // q = H_d^H v, gain, s
       cgm::PrecodeQSmem PQ;
       PQ.plan(p.B, p.St);
-      r = timed(ctx, st, 2, [&] {
+      r = timed(ctx, st, 4, [&] {
         pq_kernel<<<static_cast<unsigned>(n), cgm::PrecodeQSmem::NTH, PQ.total, st>>>(q, tmH);
       });
       if (r) return r;
@@ -877,7 +877,22 @@ int cgm_ctx_kernel_times_ex(cgm_ctx* ctx, double* channel_ms, double* basis_ms, 
     CGM_CUDA(ctx, cudaEventSynchronize(rec.second.second));
     float ms = 0.f;
     CGM_CUDA(ctx, cudaEventElapsedTime(&ms, rec.second.first, rec.second.second));
-    (rec.first == 1 ? *channel_ms : rec.first == 3 ? *basis_ms : *solve_ms) += ms;
+    (rec.first == 1 ? *channel_ms : rec.first == 3 ? *basis_ms : *solve_ms) += ms;  // 2, 4: solve
+    if (rec.first == 1) ++*launches;
+  }
+  return CGM_OK;
+}
+
+int cgm_ctx_kernel_times_kinds(cgm_ctx* ctx, double ms[4], long* launches) {
+  if (!ctx || !ms || !launches) return CGM_EINVAL;
+  for (int k = 0; k < 4; ++k) ms[k] = 0.0;
+  *launches = 0;
+  for (auto& rec : ctx->ev_log) {
+    CGM_CUDA(ctx, cudaEventSynchronize(rec.second.second));
+    float t = 0.f;
+    CGM_CUDA(ctx, cudaEventElapsedTime(&t, rec.second.first, rec.second.second));
+    static constexpr int slot[5] = {-1, 0, 2, 1, 3};  // kind 1 channel, 2 solve, 3 moments, 4 precoder
+    if (rec.first >= 1 && rec.first <= 4) ms[slot[rec.first]] += t;
     if (rec.first == 1) ++*launches;
   }
   return CGM_OK;
