@@ -377,11 +377,16 @@ def ours_arm(args, rank, world, local_rank):
     # per-kernel durations: the same K steps again with CUDA events around
     # every launch inside the C ABI (on the launch stream); a separate pass
     # so the event records do not perturb the headline timing
+    # (chunks serialised on one stream for this pass, so each kernel's window
+    # is its own: the timed steps above overlap consecutive chunks' kernels
+    # on two streams)
+    ctx.set_kernel_policy("serial_chunks")
     ctx.set_profiling(True)
     ctx.kernel_times()
     for i in range(args.steps):
         step(args.warmup + i)
     torch.cuda.synchronize()
+    ctx.set_kernel_policy("auto")
     kms, n_pairs = ctx.kernel_times_kinds()
     ch_ms, bs_ms, sv_ms, pq_ms = kms["channel"], kms["moments"], kms["solve"], kms["precoder"]
     ctx.set_profiling(False)

@@ -90,7 +90,7 @@ class Context:
         self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
 
     POLICY_FLAGS = {"ffma_channel": 1, "split_small": 2, "lane_solve": 4, "block_uplink": 8,
-                    "rows_cta": 16, "poison_ws": 32, "tile_moments": 64}
+                    "rows_cta": 16, "poison_ws": 32, "tile_moments": 64, "serial_chunks": 128}
 
     def set_kernel_policy(self, policy: str):
         """Kernel-variant switches for A/B tests: "auto" (production defaults)
@@ -102,7 +102,9 @@ class Context:
         kernel), "rows_cta" (the 8-warp row CTA instead of the block kernel
         for calls with transmit vectors), "poison_ws" (test only: NaN-fill the
         workspace before every chunk), "tile_moments" (the 4x4-tile CTA
-        moments kernel instead of the warp-per-subcarrier one, U = 32)."""
+        moments kernel instead of the warp-per-subcarrier one, U = 32),
+        "serial_chunks" (every workspace chunk on the call's stream instead of
+        alternating two streams)."""
         bits = 0
         if policy != "auto":
             for name in policy.split("+"):

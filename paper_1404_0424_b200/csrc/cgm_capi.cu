@@ -49,6 +49,11 @@ struct cgm_ctx {
   // optional per-kernel event timing (bench roofline): pairs of events per launch
   int profiling = 0;
   cudaEvent_t order_ev = nullptr;  // host pipeline: ordered after the context stream's work
+  // split path: consecutive chunks alternate between two streams (and two
+  // workspace halves), so one chunk's HBM-bound tail kernels overlap the
+  // next chunk's compute-bound head kernels
+  cudaStream_t chunk_st[2] = {nullptr, nullptr};
+  cudaEvent_t fork_ev = nullptr, join_ev[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_log;  // kind, (start, stop)
   size_t ev_next = 0;
@@ -189,6 +194,7 @@ constexpr int kPolBlockUp = 8;      // U = 32 uplink only: the shared-G block ke
 constexpr int kPolRowsCta = 16;     // U = 32 with transmit vectors: the 8-warp row CTA instead of block
 constexpr int kPolPoisonWs = 32;    // test only: fill the workspace with NaN before every chunk
 constexpr int kPolTileMoments = 64; // U = 32, FP32 moments: the 4x4-tile CTA kernel instead of warp rows
+constexpr int kPolSerialChunks = 128;  // split path: every chunk on the call's stream (no two-stream overlap)
 
 // Device workspace of the split path.  A call captured into a CUDA graph
 // bakes in this pointer, so a larger call never frees it: the old buffer
@@ -418,15 +424,27 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   long chunk = static_cast<long>(ctx->chunk_bytes / std::max<size_t>(per_sc, 1));
   chunk = std::max<long>(chunk, static_cast<long>(ctx->sms) * occ1);
   chunk = std::min(chunk, p.n_sc);
-  const int rc = ensure_ws(ctx, static_cast<size_t>(chunk) * W.stride * sizeof(float2));
+  // two or more chunks: alternate two streams and workspace halves (fork from
+  // and join back into the call's stream; captures into a CUDA graph as a
+  // fork/join)
+  const bool dual = p.n_sc > chunk && !(ctx->policy & kPolSerialChunks);
+  const size_t ws_half = static_cast<size_t>(chunk) * W.stride;  // float2 per workspace half
+  const int rc = ensure_ws(ctx, (dual ? 2 : 1) * ws_half * sizeof(float2));
   if (rc) return rc;
-  p.ws = reinterpret_cast<float2*>(ctx->tscratch);
-  for (long c0 = 0; c0 < p.n_sc; c0 += chunk) {
+  const cudaStream_t call_st = st;
+  if (dual) {
+    CGM_CUDA(ctx, cudaEventRecord(ctx->fork_ev, call_st));
+    for (int k = 0; k < 2; ++k) CGM_CUDA(ctx, cudaStreamWaitEvent(ctx->chunk_st[k], ctx->fork_ev, 0));
+  }
+  int ci = 0;
+  for (long c0 = 0; c0 < p.n_sc; c0 += chunk, ++ci) {
     const long n = std::min(chunk, p.n_sc - c0);
+    st = dual ? ctx->chunk_st[ci & 1] : call_st;
+    p.ws = reinterpret_cast<float2*>(ctx->tscratch) + (dual ? (ci & 1) * ws_half : 0);
     // poisoned workspace: a kernel reading workspace it did not write first
     // turns its outputs into NaN (tests compare against an unpoisoned run)
     if (ctx->policy & kPolPoisonWs)
-      CGM_CUDA(ctx, cudaMemsetAsync(ctx->tscratch, 0xFF, static_cast<size_t>(n) * W.stride * 8, st));
+      CGM_CUDA(ctx, cudaMemsetAsync(p.ws, 0xFF, static_cast<size_t>(n) * W.stride * 8, st));
     cgm::KernelParams q = p;
     q.sc_base = c0;
     q.n_sc = n;
@@ -455,6 +473,12 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       if (r) return r;
     }
     if (km && p.fx && (r = moments())) return r;
+  }
+  if (dual) {
+    for (int k = 0; k < 2; ++k) {
+      CGM_CUDA(ctx, cudaEventRecord(ctx->join_ev[k], ctx->chunk_st[k]));
+      CGM_CUDA(ctx, cudaStreamWaitEvent(call_st, ctx->join_ev[k], 0));
+    }
   }
   return CGM_OK;
 }
@@ -822,6 +846,11 @@ int cgm_ctx_create(int device, cgm_ctx** out) {
   }
   for (int i = 0; i < 3 && e == cudaSuccess; ++i)
     e = cudaStreamCreateWithFlags(&ctx->pipe[i], cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaStreamCreateWithFlags(&ctx->chunk_st[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
   if (const char* hc = std::getenv("CGMIMO_HOST_CHUNKS")) ctx->host_chunks = std::max(0, std::atoi(hc));
   if (const char* cm = std::getenv("CGMIMO_CHUNK_MB")) ctx->chunk_bytes = static_cast<size_t>(std::max(1, std::atoi(cm))) << 20;
   if (e == cudaSuccess) {
@@ -846,6 +875,11 @@ int cgm_ctx_destroy(cgm_ctx* ctx) {
   }
   for (int i = 0; i < 3; ++i)
     if (ctx->pipe[i]) cudaStreamDestroy(ctx->pipe[i]);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->chunk_st[i]) cudaStreamDestroy(ctx->chunk_st[i]);
+    if (ctx->join_ev[i]) cudaEventDestroy(ctx->join_ev[i]);
+  }
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   if (ctx->tscratch) cudaFree(ctx->tscratch);
   for (void* r : ctx->retired) cudaFree(r);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
@@ -908,6 +942,7 @@ int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, lon
 int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy) {
   if (!ctx || policy < 0 ||
       policy > (kPolFfmaChannel | kPolSplitSmall | kPolLaneSolve | kPolBlockUp | kPolRowsCta | kPolTileMoments |
+                kPolSerialChunks |
                 kPolPoisonWs))
     return fail(ctx, CGM_EINVAL, "unknown kernel policy %d", policy);
   ctx->policy = policy;

@@ -374,3 +374,50 @@ def test_partial_output_requests_match_full(gpu_ctx, name):
         assert set(part) == set(want)
         for k in want:
             assert torch.equal(part[k], full[k]), (name, want, k)
+
+
+@pytest.mark.parametrize("name", ["cfg5", "cfg4a_K4", "cfg2"])
+def test_multi_chunk_two_stream_path_bitwise(name):
+    """A small workspace budget (CGMIMO_CHUNK_MB, read at context creation)
+    splits the call into several chunks that alternate two streams and two
+    workspace halves; the results equal the one-chunk call and the serial
+    chunk order bit for bit (every subcarrier's computation is independent of
+    the chunking)."""
+    import os
+
+    from paper_1404_0424_b200 import Context
+
+    cfg = get_config(name).scaled(700)
+    old = os.environ.get("CGMIMO_CHUNK_MB")
+    os.environ["CGMIMO_CHUNK_MB"] = "12"
+    try:
+        small = Context(0)
+    finally:
+        if old is None:
+            del os.environ["CGMIMO_CHUNK_MB"]
+        else:
+            os.environ["CGMIMO_CHUNK_MB"] = old
+    big = Context(0)
+    rs = cfg.rsqrt()
+    rs = None if rs is None else torch.tensor(rs)
+    H, Y = big.generate_uplink(cfg.B, cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits, cfg.n0,
+                               rsqrt=rs)
+    T = big.generate_symbols(cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits)
+
+    def run(ctx):
+        if cfg.kind == "both":
+            return ctx.detect_precode_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                                         cfg.tracker, T, cfg.rho_d, cfg.K)
+        return ctx.detect_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K, cfg.tracker)
+
+    want = run(big)
+    l0 = small.kernel_launches
+    got = run(small)
+    torch.cuda.synchronize()
+    assert small.kernel_launches - l0 >= 4, "expected several chunks"
+    small.set_kernel_policy("serial_chunks")
+    ser = run(small)
+    torch.cuda.synchronize()
+    for k in want:
+        assert torch.equal(got[k], want[k]), (name, k)
+        assert torch.equal(ser[k], want[k]), (name, k)
