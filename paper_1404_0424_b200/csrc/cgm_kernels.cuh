@@ -181,7 +181,12 @@ __device__ __forceinline__ void cheb_coef_warp(const float* hist, int K, double 
       l1 = l0;
       l0 = m == 0 ? a : 0.0;  // L_1 = alpha_1 I
     } else {
-      const double c1 = a * (1.0 + b_m1) / a_m1, c2 = a * b_m2 / a_m2;
+      // ratios of the CG's FP32 step lengths, in FP32: an FP64 division is a
+      // long dependent sequence on this recursion's critical path
+      const double c1 = static_cast<double>(__fdividef(static_cast<float>(a * (1.0 + b_m1)),
+                                                       static_cast<float>(a_m1)));
+      const double c2 = static_cast<double>(__fdividef(static_cast<float>(a * b_m2),
+                                                       static_cast<float>(a_m2)));
       const double d1 = l0 - l1;
       const double t = mulA(d1);
       const double nx = l0 + c1 * d1 - a * t - c2 * (l1 - l2);
