@@ -239,10 +239,14 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT, UP == 32 ? 4 : 2) moments_kern
       for (int it = 0; it <= 6; ++it) {
         if (tid < 2 * UP) {
           const int i = tid % UP, h = tid / UP;
-          float2 y = make_float2(0.f, 0.f);
-#pragma unroll 8
-          for (int j = h * (UP / 2); j < (h + 1) * (UP / 2); ++j) cfma_conj(y, Gs[j * LD + i], xs[j]);
-          yp[h * UP + i] = y;
+          float2 y4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                          make_float2(0.f, 0.f)};  // four independent chains
+#pragma unroll
+          for (int j = h * (UP / 2); j < (h + 1) * (UP / 2); j += 4) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cfma_conj(y4[q], Gs[(j + q) * LD + i], xs[j + q]);
+          }
+          yp[h * UP + i] = cadd(cadd(y4[0], y4[1]), cadd(y4[2], y4[3]));
         }
         __syncthreads();
         float nrm = 0.f, ray = 0.f;
