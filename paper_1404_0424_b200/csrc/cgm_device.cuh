@@ -218,15 +218,31 @@ __device__ __forceinline__ void tile4x4_pipe(float2 (&acc)[4][4], const float2* 
   const float4* xp = reinterpret_cast<const float4*>(X + k0 * ldx + i0);
   const float4* zp = reinterpret_cast<const float4*>(Z + k0 * ldz + j0);
   const int xs = ldx / 2, zs = ldz / 2;  // float4 strides
+  // packed FP32x2 accumulators: conj(x) y = y * x.x + swap(y) * (x.y, -x.y),
+  // the same two roundings per component in the same order as cfma_conj
+  // (bitwise-equal results) at half the FMA-pipe instructions
+  unsigned long long pk[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) pk[r][c] = f2pack(acc[r][c].x, acc[r][c].y);
   auto fma_row = [&](const float4& xa, const float4& xb, const float4& za, const float4& zb) {
     const float2 x[4] = {make_float2(xa.x, xa.y), make_float2(xa.z, xa.w),
                          make_float2(xb.x, xb.y), make_float2(xb.z, xb.w)};
-    const float2 y[4] = {make_float2(za.x, za.y), make_float2(za.z, za.w),
-                         make_float2(zb.x, zb.y), make_float2(zb.z, zb.w)};
+    const unsigned long long y[4] = {f2pack(za.x, za.y), f2pack(za.z, za.w), f2pack(zb.x, zb.y),
+                                     f2pack(zb.z, zb.w)};
+    unsigned long long ys[4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int c = 0; c < 4; ++c) ys[c] = f2swap_hl(y[c]);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) cfma_conj(acc[r][c], x[r], y[c]);
+    for (int r = 0; r < 4; ++r) {
+      const unsigned long long ax = f2pack(x[r].x, x[r].x), ay = f2pack(x[r].y, -x[r].y);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        ffma2(pk[r][c], y[c], ax);
+        ffma2(pk[r][c], ys[c], ay);
+      }
+    }
   };
   int k = k0;
   // two rows per trip: both rows' operands are in flight before the FMAs
@@ -239,6 +255,10 @@ __device__ __forceinline__ void tile4x4_pipe(float2 (&acc)[4][4], const float2* 
     fma_row(xa1, xb1, za1, zb1);
   }
   if (k < k1) fma_row(xp[0], xp[1], zp[0], zp[1]);
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = f2unpack(pk[r][c]);
 }
 
 // acc[r][c] += sum_k conj(X[k*ldx + i0 + r]) * Z[k*ldz + j0 + c], r, c < 2.
