@@ -244,8 +244,12 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   const int Kmax = std::max(p.K, p.Kt);
   p.exact = EXACT ? 1 : 0;
   // one vector per subcarrier: the CG runs before the moments kernel, which
-  // then does the per-vector extraction itself (moments_kernel<..., FX>)
-  p.fx = (EXACT && p.S == 1 && p.St == 0) ? 1 : 0;
+  // then does the per-vector extraction itself (moments_kernel<..., FX>) --
+  // except for U = 32 with K <= 6, where the warp-per-subcarrier row-moment
+  // kernel (FP32 moment table) and the pairs kernel's extraction are faster
+  // (cfg4a K = 4: 2.66 -> see DESIGN s12)
+  const bool rows_moments = UP == 32 && p.K <= cgm::kLaneK && !(ctx->policy & kPolTileMoments);
+  p.fx = (EXACT && p.S == 1 && p.St == 0 && !rows_moments) ? 1 : 0;
   // ------------------------------------------------------------------ K1
   cgm::K1Split sp;
   sp.plan(UP, p.B, p.S);
