@@ -606,6 +606,14 @@ def ours_arm(args, rank, world, local_rank):
             "config": {**workload_config(cfg_all, {"n": n_frames, "bytes": n_frames * frame_bytes},
                                          world=world),
                        "cuda_graphs": graph_note,
+                       "numerics": ("complex64 / FP32 throughout; the U = 32 Gram and matched "
+                                    "filter on tcgen05 tensor cores as a bf16 x 3 split (six "
+                                    "products, two TMEM accumulators, FP32-level accuracy) -- not "
+                                    "north_star's 3xTF32: kind::tf32 with MN-major operands "
+                                    "returned zeros on this B200, and fp16 x 2 missed the "
+                                    "contract on cfg5 (DESIGN s4, s12); exact-tracker moment "
+                                    "table FP32 up to K = 6, FP64 beyond; contract "
+                                    "|d| <= 1e-4 + 1e-3 |ref| against the FP64 reference"),
                        **({} if strong else {"frames_per_step": fps,
                                              "vectors_per_step_per_gpu": cfg.vectors})},
             "llr_gbit_s": value * cfg.U * cfg.qam_bits / 1e9 if cfg.kind != "downlink" else None,
