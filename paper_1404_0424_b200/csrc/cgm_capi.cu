@@ -24,6 +24,7 @@
 #include "cgm_moments.cuh"
 #include "cgm_precode_small.cuh"
 #include "cgm_uplink_small.cuh"
+#include "cgm_tc64.cuh"
 #include "cgm_rows32.cuh"
 #include "cgm_tc.cuh"
 
@@ -293,6 +294,24 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
           k1 = cgm::channel_tc_kernel<8, 0>;
           nt1 = 32 * 10;
         }
+      }
+    }
+  }
+  if constexpr (UP == 64) {
+    // U = 64 natural layout: the M = 128 tensor-core kernel (cgm_tc64.cuh)
+    const uintptr_t al = reinterpret_cast<uintptr_t>(p.H) | reinterpret_cast<uintptr_t>(p.Y);
+    const int tc_tma = (!p.hd_layout && p.U == UP && (al & 15u) == 0) ? 1 : 0;
+    if (cgm::tc64::supported(p.U, p.B, p.S, tc_tma) && !(ctx->policy & kPolFfmaChannel)) {
+      cgm::tc64::Smem T;
+      int nstg = 3;
+      T.plan(p.S, nstg);
+      if (T.total > ctx->max_smem) T.plan(p.S, nstg = 2);
+      if (T.total <= ctx->max_smem) {
+        use_tc = true;
+        p.k1_pair = nstg;
+        smem1 = T.total;
+        k1 = cgm::channel_tc64_kernel;
+        nt1 = cgm::tc64::NT;
       }
     }
   }

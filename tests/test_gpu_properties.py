@@ -156,12 +156,11 @@ def test_kernel_launch_accounting(gpu_ctx):
     assert gpu_ctx.kernel_launches - mid >= 1  # the hot path ran native kernels
 
 
-@pytest.mark.parametrize("name", ["cfg2", "cfg4a_K8", "cfg5"])
+@pytest.mark.parametrize("name", ["cfg2", "cfg4a_K8", "cfg5", "cfg4b_K2", "cfg4b_K8"])
 def test_tensor_core_channel_matches_ffma_channel(gpu_ctx, checker, name):
-    """The tcgen05 channel kernel (bf16 x3 split, cgm_tc.cuh) and the FP32
-    FFMA channel kernel agree to FP32 rounding, and both match the oracle on
-    a subsample (U = 32, B a multiple of 64: the shapes the tensor-core path
-    takes)."""
+    """The tcgen05 channel kernels (bf16 x3 split: cgm_tc.cuh for U = 32,
+    cgm_tc64.cuh for U = 64) and the FP32 FFMA channel kernel agree to FP32
+    rounding, and the default matches the oracle on a subsample."""
     cfg = get_config(name).scaled(600)
     H, Y = gen(gpu_ctx, cfg)
     tc = run(gpu_ctx, cfg, H, Y)
@@ -276,6 +275,9 @@ def test_fused_small_precoder_matches_split_and_oracle(gpu_ctx, checker, U, B, S
     (33, 13, 5, 4, "exact", 4),    # fused U <= 16 kernel, odd B (no bulk copies)
     (48, 3, 7, 2, "exact", 2),     # several systems per warp group, QPSK
     (50, 16, 4, 8, "approx", 6),
+    (96, 64, 3, 4, "exact", 4),    # U = 64 tensor-core channel: 32-antenna k-blocks, odd S
+    (160, 64, 7, 3, "approx", 6),
+    (64, 64, 32, 2, "approx", 2),  # the largest S of the U = 64 tensor-core path (N = 192)
 ])
 def test_ragged_shapes_match_oracle(gpu_ctx, checker, B, U, S, K, tracker, bits):
     """Ragged U (between the kernels' row widths), odd B and S, several
