@@ -118,7 +118,9 @@ def read_traffic(cfg_name: str):
     return v if isinstance(v, dict) else None
 
 
-CPU_MIN_SECONDS = 10.0  # a stated subsample of >= 10 s of CPU work
+# a stated subsample of >= 10 s of CPU work (the CPU tests of the
+# JSON contract shorten it through BENCH_CPU_MIN_SECONDS)
+CPU_MIN_SECONDS = float(os.environ.get("BENCH_CPU_MIN_SECONDS", "10.0"))
 
 
 def cpu_reference(cfg_name: str) -> dict:
