@@ -46,6 +46,7 @@ struct cgm_ctx {
   long launches = 0;
   int policy = 0;  // kernel-variant switches (kPol*), 0 = production defaults
   int host_chunks = 0;  // CGMIMO_HOST_CHUNKS, read once at context creation
+  size_t host_set_bytes = 384ull << 20;  // host pipeline: device bytes per buffer set (CGMIMO_HOST_SET_MB)
   size_t chunk_bytes = 1024ull << 20;  // split-path chunk budget (CGMIMO_CHUNK_MB)
   // optional per-kernel event timing (bench roofline): pairs of events per launch
   int profiling = 0;
@@ -724,7 +725,7 @@ int run_job(cgm_ctx* ctx, const Job& j, unsigned flags) {
   constexpr int NB = cgm_ctx::kHostSets;
   const Sizes z = sizes_of(j);
   const size_t per_sc = z.total() + 16 * 12;
-  const size_t budget = 192ull << 20;  // per buffer set
+  const size_t budget = ctx->host_set_bytes;  // per buffer set (CGMIMO_HOST_SET_MB)
   long chunk = static_cast<long>(std::max<size_t>(1, budget / std::max<size_t>(per_sc, 1)));
   chunk = std::min(chunk, j.n_sc);
   // up to 8 chunks of at least ~8 MB each: small batches are bound by the
@@ -875,6 +876,8 @@ int cgm_ctx_create(int device, cgm_ctx** out) {
   }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
   if (const char* hc = std::getenv("CGMIMO_HOST_CHUNKS")) ctx->host_chunks = std::max(0, std::atoi(hc));
+  if (const char* hs = std::getenv("CGMIMO_HOST_SET_MB"))
+    ctx->host_set_bytes = static_cast<size_t>(std::max(8, std::atoi(hs))) << 20;
   if (const char* cm = std::getenv("CGMIMO_CHUNK_MB")) ctx->chunk_bytes = static_cast<size_t>(std::max(1, std::atoi(cm))) << 20;
   if (e == cudaSuccess) {
     const cgm::AxisTables t = make_axis_tables();
