@@ -423,3 +423,33 @@ def test_multi_chunk_two_stream_path_bitwise(name):
     for k in want:
         assert torch.equal(got[k], want[k]), (name, k)
         assert torch.equal(ser[k], want[k]), (name, k)
+
+
+def test_cfg5_path_degenerate_inputs_match_oracle(gpu_ctx, checker):
+    """The headline detect + precode path (block CG, moment extraction, TMA
+    precoder) on degenerate inputs, against the reference: a subcarrier whose
+    transmit vectors are all zero and one zero vector elsewhere (zero_input:
+    status 2, gain 0, q = s = 0; precode.cpp:22-36), a subcarrier with zero
+    observations (x_hat = 0, frozen CG), and ordinary neighbours."""
+    cfg = get_config("cfg5").scaled(40)
+    H, Y = gen(gpu_ctx, cfg)
+    T = gpu_ctx.generate_symbols(cfg.U, cfg.n_sc, cfg.S, cfg.seed, cfg.qam_bits)
+    T[3] = 0
+    T[5, 2] = 0
+    Y[4] = 0
+    got = gpu_ctx.detect_precode_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                                    cfg.tracker, T, cfg.rho_d, cfg.K)
+    torch.cuda.synchronize()
+    assert int(got["pstatus"][3].min()) == 2 and int(got["pstatus"][5, 2]) == 2
+    assert float(got["gain"][3].abs().max()) == 0.0 and float(got["s"][3].abs().max()) == 0.0
+    assert float(got["xhat"][4].abs().max()) == 0.0
+    h = H.cpu().numpy()
+    want = checker.detect(h, Y.cpu().numpy(), cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, cfg.K,
+                          cfg.tracker, threads=8)
+    check_detect({k: got[k].cpu().numpy() for k in ("xhat", "mu", "rho", "llr", "status")}, want,
+                 "cfg5 degenerate uplink")
+    wantd = checker.precode(np.conj(np.transpose(h, (0, 2, 1))), T.cpu().numpy(), cfg.rho_d,
+                            cfg.K, threads=8)
+    check_precode({"q": got["q"].cpu().numpy(), "s": got["s"].cpu().numpy(),
+                   "gain": got["gain"].cpu().numpy(), "status": got["pstatus"].cpu().numpy()},
+                  wantd, "cfg5 degenerate downlink")
