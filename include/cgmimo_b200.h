@@ -90,6 +90,11 @@ int cgm_ctx_kernel_times_ex(cgm_ctx* ctx, double* channel_ms, double* basis_ms, 
  * (CG, extraction, LLRs), ms[3] the separate precoder kernel (q = H_d^H v,
  * gain, s; cgm_ctx_kernel_times_ex counts it in solve_ms). */
 int cgm_ctx_kernel_times_kinds(cgm_ctx* ctx, double ms[4], long* launches);
+/* The same launches as a timeline: for launch i (up to cap), its kind (1
+ * channel, 2 solve, 3 moments, 4 precoder) and start / end in ms relative to
+ * the first recorded launch's start; *n = launches recorded (may exceed cap). */
+int cgm_ctx_kernel_timeline(cgm_ctx* ctx, int* kinds, double* start_ms, double* end_ms, long cap,
+                            long* n);
 const char* cgm_last_error(const cgm_ctx* ctx);
 /* kernels this context has launched since creation (the bench's gpu_launches) */
 long cgm_kernel_launches(const cgm_ctx* ctx);

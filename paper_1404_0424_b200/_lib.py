@@ -35,6 +35,8 @@ SIGNATURES = {
     "cgm_ctx_set_profiling": (_int, [_vp, _int]),
     "cgm_ctx_kernel_times": (_int, [_vp, C.POINTER(_dbl), C.POINTER(_dbl), C.POINTER(_long)]),
     "cgm_ctx_kernel_times_kinds": (_int, [_vp, C.POINTER(_dbl), C.POINTER(_long)]),
+    "cgm_ctx_kernel_timeline": (_int, [_vp, C.POINTER(_int), C.POINTER(_dbl), C.POINTER(_dbl),
+                                       _long, C.POINTER(_long)]),
     "cgm_ctx_kernel_times_ex": (_int, [_vp, C.POINTER(_dbl), C.POINTER(_dbl), C.POINTER(_dbl),
                                        C.POINTER(_long)]),
     "cgm_last_error": (C.c_char_p, [_vp]),

@@ -130,6 +130,18 @@ class Context:
         self._check(self.lib.cgm_ctx_kernel_times_kinds(self.h, ms, C.byref(n)))
         return dict(zip(("channel", "moments", "solve", "precoder"), list(ms))), n.value
 
+    def kernel_timeline(self, cap: int = 4096):
+        """[(kind, start_ms, end_ms)] of the launches recorded since profiling
+        was enabled (kind: "channel" / "solve" / "moments" / "precoder"),
+        relative to the first one's start."""
+        k = (C.c_int * cap)()
+        a = (C.c_double * cap)()
+        b = (C.c_double * cap)()
+        n = C.c_long()
+        self._check(self.lib.cgm_ctx_kernel_timeline(self.h, k, a, b, cap, C.byref(n)))
+        names = {1: "channel", 2: "solve", 3: "moments", 4: "precoder"}
+        return [(names.get(k[i], str(k[i])), a[i], b[i]) for i in range(min(n.value, cap))]
+
     def kernel_times(self):
         """(channel_ms, solve_ms, launches) summed since profiling was enabled."""
         a, b, n = C.c_double(), C.c_double(), C.c_long()

@@ -958,6 +958,27 @@ int cgm_ctx_kernel_times_kinds(cgm_ctx* ctx, double ms[4], long* launches) {
   return CGM_OK;
 }
 
+int cgm_ctx_kernel_timeline(cgm_ctx* ctx, int* kinds, double* start_ms, double* end_ms, long cap,
+                            long* n) {
+  if (!ctx || !n || cap < 0 || (cap > 0 && (!kinds || !start_ms || !end_ms))) return CGM_EINVAL;
+  *n = static_cast<long>(ctx->ev_log.size());
+  if (ctx->ev_log.empty()) return CGM_OK;
+  const cudaEvent_t t0 = ctx->ev_log.front().second.first;
+  long i = 0;
+  for (auto& rec : ctx->ev_log) {
+    if (i >= cap) break;
+    CGM_CUDA(ctx, cudaEventSynchronize(rec.second.second));
+    float a = 0.f, b = 0.f;
+    CGM_CUDA(ctx, cudaEventElapsedTime(&a, t0, rec.second.first));
+    CGM_CUDA(ctx, cudaEventElapsedTime(&b, t0, rec.second.second));
+    kinds[i] = rec.first;
+    start_ms[i] = a;
+    end_ms[i] = b;
+    ++i;
+  }
+  return CGM_OK;
+}
+
 int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, long* launches) {
   double basis = 0.0;
   const int rc = cgm_ctx_kernel_times_ex(ctx, channel_ms, &basis, solve_ms, launches);
