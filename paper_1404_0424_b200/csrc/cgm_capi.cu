@@ -447,6 +447,10 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
                         static_cast<size_t>(p.B) * p.S * 8;
   long chunk = static_cast<long>(ctx->chunk_bytes / std::max<size_t>(per_sc, 1));
   chunk = std::max<long>(chunk, static_cast<long>(ctx->sms) * occ1);
+  // a call that fits one chunk but is large (a GPU's shard of cfg5 at 8 GPUs)
+  // still splits in two, so the two chunk streams overlap its kernels
+  if (!(ctx->policy & kPolSerialChunks) && p.n_sc <= chunk && p.n_sc >= 32L * ctx->sms)
+    chunk = (p.n_sc + 1) / 2;
   chunk = std::min(chunk, p.n_sc);
   // two or more chunks: alternate two streams and workspace halves (fork from
   // and join back into the call's stream; captures into a CUDA graph as a
