@@ -198,7 +198,8 @@ def sharded_gather_pass(args, ctx, cfg_all, cfg, frame, rank, world, local_rank,
                                                detect_precode_outputs)
 
     uid = [Comm.unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
+    if dist.is_initialized():
+        dist.broadcast_object_list(uid, src=0)
     comm_ctx = Context(local_rank)
     comm = Comm(comm_ctx, world, rank, uid[0])
     spec = detect_precode_outputs(cfg_all)
@@ -240,9 +241,10 @@ def sharded_gather_pass(args, ctx, cfg_all, cfg, frame, rank, world, local_rank,
     to_root = (cfg_all.n_sc - (hi - lo if rank == 0 else 0)) * per_sc
     if rank != 0:
         to_root = 0
-    t = torch.tensor([float(to_root)], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    to_root = float(t.item())
+    if dist.is_initialized():
+        t = torch.tensor([float(to_root)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        to_root = float(t.item())
     comm.close()
     gather_floor_ms = to_root / (NVLINK_GBS * 1e9) * 1e3
     return {"what": ("chunked sharded job: LLRs, precoded vectors q and s, gains and status bytes "
@@ -460,7 +462,7 @@ def ours_arm(args, rank, world, local_rank):
 
     # ---------------------------------------------------- gather (N > 1 only)
     gather = None
-    if world > 1 and strong and cfg.kind == "both":
+    if (world > 1 or args.force_gather) and strong and cfg.kind == "both":
         gather = sharded_gather_pass(args, ctx, cfg_all, cfg, frames[0], rank, world, local_rank,
                                      barrier, max_over_ranks)
     elif world > 1 and "llr" in out:
@@ -644,6 +646,8 @@ def main():
                          "(default: ~1 GB of H + Y per step)")
     ap.add_argument("--gather-chunks", type=int, default=4,
                     help="N > 1, cfg5: chunks per rank of the overlapped output gather")
+    ap.add_argument("--force-gather", action="store_true",
+                    help="run the chunked gather pass even at one rank (exercises cgm_gatherv)")
     ap.add_argument("--no-graphs", action="store_true",
                     help="time direct C-ABI calls instead of CUDA-graph replays of them")
     args = ap.parse_args()
@@ -652,7 +656,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and args.impl == "ours":
+    dist_on = args.impl == "ours" and (world > 1 or "RANK" in os.environ)
+    if dist_on:
         import torch
         import torch.distributed as dist
 
@@ -664,7 +669,7 @@ def main():
         else:
             ours_arm(args, rank, world, local_rank)
     finally:
-        if world > 1 and args.impl == "ours":
+        if dist_on:
             import torch.distributed as dist
 
             dist.destroy_process_group()
