@@ -203,21 +203,32 @@ __device__ __forceinline__ void cheb_coef_warp(const float* hist, int K, double 
   }
 }
 
+// Power iteration for lambda_max(A), A = G + reg I: x_0 = 1, x_{t+1} = A x_t
+// / tr(A) (tr(A) >= lambda_max, so the iterates neither overflow nor, in six
+// steps of at most a factor U, underflow), lambda = the Rayleigh quotient
+// x_6^H A x_6 / x_6^H x_6; one warp reduction for the trace and one for the
+// quotient, none inside the chain.  Interval [reg, 1.1 lambda] -> (c, d).
 template <int UP, int LDG = UP>
 __device__ __forceinline__ float2 cheb_interval(const float2* Gs, float reg, float2* xs, int lane) {
   constexpr int RU = UP < 32 ? 1 : UP / 32;
   float2 xr[RU];
+  float tr = 0.f;
 #pragma unroll
   for (int m = 0; m < RU; ++m) {
     const int i = lane + 32 * m;
     xr[m] = make_float2(i < UP ? 1.f : 0.f, 0.f);
-    if (i < UP) xs[i] = xr[m];
+    if (i < UP) {
+      xs[i] = xr[m];
+      tr += Gs[i * LDG + i].x + reg;
+    }
   }
+  tr = group_sum<32>(tr);
+  const float itr = tr > 0.f ? 1.f / tr : 1.f;
   __syncwarp();
   float lam = reg;
   for (int it = 0; it <= 6; ++it) {
     float2 y[RU];
-    float nrm = 0.f, ray = 0.f;
+    float nx = 0.f, ray = 0.f;
 #pragma unroll
     for (int m = 0; m < RU; ++m) {
       const int i = lane + 32 * m;
@@ -228,18 +239,20 @@ __device__ __forceinline__ float2 cheb_interval(const float2* Gs, float reg, flo
         y[m].x = fmaf(reg, xr[m].x, y[m].x);
         y[m].y = fmaf(reg, xr[m].y, y[m].y);
       }
-      nrm += cnorm(y[m]);
+      nx += cnorm(xr[m]);
       ray += xr[m].x * y[m].x + xr[m].y * y[m].y;
     }
-    nrm = group_sum<32>(nrm);
-    ray = group_sum<32>(ray);
-    if (it > 0) lam = ray;  // Rayleigh quotient x^H A x, ||x|| = 1
-    const float inv = nrm > 0.f ? rsqrtf(nrm) : 0.f;
+    if (it == 6) {
+      nx = group_sum<32>(nx);
+      ray = group_sum<32>(ray);
+      if (nx > 0.f) lam = ray / nx;
+      break;
+    }
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < RU; ++m) {
       const int i = lane + 32 * m;
-      xr[m] = cscale(inv, y[m]);
+      xr[m] = cscale(itr, y[m]);
       if (i < UP) xs[i] = xr[m];
     }
     __syncwarp();

@@ -232,6 +232,18 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT, UP == 32 ? 4 : 2) moments_kern
       float2* yp = xs + UP;
       float* rd = reinterpret_cast<float*>(yp + 2 * UP);  // [warps][2]
       const float reg = p.rho_inv_u;
+      // iterates scaled by 1 / tr(A) (>= lambda_max) instead of normalised:
+      // one CTA reduction for the trace, one for the final Rayleigh quotient
+      float itr;
+      {
+        float t = tid < UP ? Gs[tid * LD + tid].x + reg : 0.f;
+        t = group_sum<32>(t);
+        if (lane == 0 && warp < UP / 32) rd[warp * 2] = t;
+        __syncthreads();
+        t = 0.f;
+        for (int w = 0; w < UP / 32; ++w) t += rd[w * 2];  // fixed order
+        itr = t > 0.f ? 1.f / t : 1.f;
+      }
       float2 xr = make_float2(tid < UP ? 1.f : 0.f, 0.f);
       if (tid < UP) xs[tid] = xr;
       __syncthreads();
@@ -249,32 +261,32 @@ __global__ void __launch_bounds__(MomGeo<UP>::NT, UP == 32 ? 4 : 2) moments_kern
           yp[h * UP + i] = cadd(cadd(y4[0], y4[1]), cadd(y4[2], y4[3]));
         }
         __syncthreads();
-        float nrm = 0.f, ray = 0.f;
         float2 y = make_float2(0.f, 0.f);
         if (tid < UP) {
           y = cadd(yp[tid], yp[UP + tid]);
           y.x = fmaf(reg, xr.x, y.x);
           y.y = fmaf(reg, xr.y, y.y);
-          nrm = cnorm(y);
-          ray = xr.x * y.x + xr.y * y.y;
         }
-        nrm = group_sum<32>(nrm);
-        ray = group_sum<32>(ray);
-        if (lane == 0 && warp < UP / 32) {
-          rd[warp * 2] = nrm;
-          rd[warp * 2 + 1] = ray;
+        if (it == 6) {
+          float nx = tid < UP ? cnorm(xr) : 0.f, ray = tid < UP ? xr.x * y.x + xr.y * y.y : 0.f;
+          nx = group_sum<32>(nx);
+          ray = group_sum<32>(ray);
+          if (lane == 0 && warp < UP / 32) {
+            rd[warp * 2] = nx;
+            rd[warp * 2 + 1] = ray;
+          }
+          __syncthreads();
+          nx = 0.f;
+          ray = 0.f;
+          for (int w = 0; w < UP / 32; ++w) {  // fixed order
+            nx += rd[w * 2];
+            ray += rd[w * 2 + 1];
+          }
+          if (nx > 0.f) lam = ray / nx;
+          break;
         }
-        __syncthreads();
-        nrm = 0.f;
-        ray = 0.f;
-        for (int w = 0; w < UP / 32; ++w) {  // fixed order
-          nrm += rd[w * 2];
-          ray += rd[w * 2 + 1];
-        }
-        if (it > 0) lam = ray;
-        const float inv = nrm > 0.f ? rsqrtf(nrm) : 0.f;
         if (tid < UP) {
-          xr = cscale(inv, y);
+          xr = cscale(itr, y);
           xs[tid] = xr;
         }
         __syncthreads();
@@ -595,8 +607,24 @@ __global__ void __launch_bounds__(32 * kMrW, 3) moments_rows32_kernel(const Kern
     for (int c = 0; c < UP / 2; ++c) g[c] = src[c];
   }
   // power iteration on A = G + reg I (cheb_interval: x_0 = 1, 7 products,
-  // Rayleigh quotient from the second on)
+  // the Rayleigh quotient of x_6).  The iterates are scaled by 1 / tr(A)
+  // (>= lambda_max, so no overflow; >= lambda_max / 32 per step, so no
+  // underflow in 6 steps) instead of normalised, so only the last step
+  // reduces over the warp: the per-step butterfly and rsqrt leave the chain.
   const float reg = p.rho_inv_u;
+  float itr;
+  {
+    float dg = 0.f;
+#pragma unroll
+    for (int c = 0; c < UP / 2; ++c) {
+      if (2 * c == i) dg = f2unpack(g[c].x).x;
+      if (2 * c + 1 == i) dg = f2unpack(g[c].y).x;
+    }
+    float t = dg + reg;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    itr = t > 0.f ? 1.f / t : 1.f;
+  }
   float2 xr = make_float2(1.f, 0.f);
   xs[i] = xr;
   __syncwarp();
@@ -617,23 +645,21 @@ __global__ void __launch_bounds__(32 * kMrW, 3) moments_rows32_kernel(const Kern
     float2 y = make_float2((A0.x - B0.y) + (A1.x - B1.y), (A0.y + B0.x) + (A1.y + B1.x));
     y.x = fmaf(reg, xr.x, y.x);
     y.y = fmaf(reg, xr.y, y.y);
-    // ||y||^2 and x^H A x over the warp in one butterfly: lanes 0-15 carry
-    // the first sum, 16-31 the second after the xor-16 exchange
-    float nrm, ray;
-    {
-      const float v0 = cnorm(y), v1 = xr.x * y.x + xr.y * y.y;
+    if (it == 6) {
+      // ||x||^2 and Re x^H A x over the warp in one butterfly: lanes 0-15
+      // carry the first sum, 16-31 the second after the xor-16 exchange
+      const float v0 = cnorm(xr), v1 = xr.x * y.x + xr.y * y.y;
       const bool up = i & 16;
       float k = up ? v1 : v0;
       k += __shfl_xor_sync(0xffffffffu, up ? v0 : v1, 16);
 #pragma unroll
       for (int o = 8; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
-      nrm = __shfl_sync(0xffffffffu, k, 0);
-      ray = __shfl_sync(0xffffffffu, k, 16);
+      const float nx = __shfl_sync(0xffffffffu, k, 0), ray = __shfl_sync(0xffffffffu, k, 16);
+      if (nx > 0.f) lam = ray / nx;
+      break;
     }
-    if (it > 0) lam = ray;
-    const float inv = nrm > 0.f ? rsqrtf(nrm) : 0.f;
     __syncwarp();
-    xr = cscale(inv, y);
+    xr = cscale(itr, y);
     xs[i] = xr;
     __syncwarp();
   }
