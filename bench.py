@@ -459,6 +459,15 @@ def ours_arm(args, rank, world, local_rank):
     barrier()
     e2e_vectors = cfg_all.vectors if strong else world * e2e_sc * cfg.S
     e2e_value = e2e_vectors * args.steps / e2e_s
+    # the e2e ceiling: this box's pinned copy bandwidth with H2D and D2H at
+    # once (the host pipeline overlaps both), measured here
+    duplex = pcie_duplex_gbs(dev)
+    e2e_roof = {"bound": "pcie", "unit": "GB/s",
+                "achieved_h2d": h2d * args.steps / e2e_s / 1e9,
+                "achieved_d2h": d2h * args.steps / e2e_s / 1e9,
+                "peak_duplex_each": duplex,
+                "frac": h2d * args.steps / e2e_s / 1e9 / duplex if duplex else None,
+                "note": "peak = pinned 256 MB H2D and D2H copies on two streams at once, measured in this run"}
 
     # ---------------------------------------------------- gather (N > 1 only)
     gather = None
@@ -622,7 +631,8 @@ def ours_arm(args, rank, world, local_rank):
                                              "vectors_per_step_per_gpu": cfg.vectors})},
             "llr_gbit_s": value * cfg.U * cfg.qam_bits / 1e9 if cfg.kind != "downlink" else None,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "vectors_per_call_per_gpu": e2e_sc * cfg.S},
+                    "d2h_bytes_per_step": d2h, "vectors_per_call_per_gpu": e2e_sc * cfg.S,
+                    "roofline": e2e_roof},
             "gpu_launches": launches,
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -631,6 +641,35 @@ def ours_arm(args, rank, world, local_rank):
         if gather:
             line["gather"] = gather
         print(json.dumps(line), flush=True)
+
+
+def pcie_duplex_gbs(dev, nbytes=256 << 20, reps=4):
+    """Pinned H2D and D2H copies of nbytes at once on two streams -> GB/s per
+    direction (the slower of the two)."""
+    import torch
+    h_in = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best = None
+    for it in range(reps + 1):
+        torch.cuda.synchronize(dev)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        with torch.cuda.stream(s1):
+            e[0].record()
+            d_a.copy_(h_in, non_blocking=True)
+            e[1].record()
+        with torch.cuda.stream(s2):
+            e[2].record()
+            h_out.copy_(d_b, non_blocking=True)
+            e[3].record()
+        torch.cuda.synchronize(dev)
+        ms = max(e[0].elapsed_time(e[1]), e[2].elapsed_time(e[3]))
+        if it > 0:
+            best = ms if best is None else min(best, ms)
+    del h_in, h_out, d_a, d_b
+    return nbytes / (best * 1e-3) / 1e9
 
 
 def main():
