@@ -540,7 +540,7 @@ def ours_arm(args, rank, world, local_rank):
     pb = cfg.precoder_bytes_per_vector() * cfg.vectors if sep else 0.0
     k_sv = kernel_roof("solve (CG + SINR extraction + LLR" + ("" if sep else " [+ precoder]") + ")",
                        cfg.solve_kernel_flops_per_vector() * cfg.vectors - pf,
-                       cfg.solve_bytes_per_vector() * cfg.vectors - pb, sv_s, traffic.get("solve"))
+                       cfg.solve_bytes_per_vector(sep) * cfg.vectors, sv_s, traffic.get("solve"))
     k_pq = (kernel_roof("precoder (q = H_d^H v, gain, s; H re-read)", pf, pb, pq_s,
                         traffic.get("precoder")) if sep else None)
     bs_s = bs_ms / args.steps / 1e3

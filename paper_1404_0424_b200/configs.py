@@ -146,8 +146,13 @@ class Config:
             return 0.0
         return 8 * self.B * self.U / self.S + 8 * self.U + 16 * self.B + 5
 
-    def solve_bytes_per_vector(self) -> float:
-        """Outputs written by the solve kernel (+ t read, H re-read by the precoder)."""
+    def solve_bytes_per_vector(self, precoder_separate: bool = False) -> float:
+        """Bytes of the solve kernel: the path's bytes minus the channel
+        kernel's; with the precoder as its own kernel (detect + precode
+        calls) only the uplink outputs and the transmit vector read."""
+        if precoder_separate and self.kind == "both":
+            U = self.U
+            return 8 * U + 4 * U + 4 * U + 4 * U * self.qam_bits + 8 * U
         return self.bytes_per_vector() - self.channel_bytes_per_vector()
 
     def scaled(self, n_sc: int) -> "Config":
