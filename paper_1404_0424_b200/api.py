@@ -90,7 +90,8 @@ class Context:
         self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
 
     POLICY_FLAGS = {"ffma_channel": 1, "split_small": 2, "lane_solve": 4, "block_uplink": 8,
-                    "rows_cta": 16, "poison_ws": 32, "tile_moments": 64, "serial_chunks": 128}
+                    "rows_cta": 16, "poison_ws": 32, "tile_moments": 64, "serial_chunks": 128,
+                    "untiled_cg": 256}
 
     def set_kernel_policy(self, policy: str):
         """Kernel-variant switches for A/B tests: "auto" (production defaults)
@@ -104,7 +105,9 @@ class Context:
         workspace before every chunk), "tile_moments" (the 4x4-tile CTA
         moments kernel instead of the warp-per-subcarrier one, U = 32),
         "serial_chunks" (every workspace chunk on the call's stream instead of
-        alternating two streams)."""
+        alternating two streams), "untiled_cg" (the lane-per-row 8-warp block
+        CG kernel instead of the register-tiled one for the exact tracker with
+        transmit vectors, cfg5)."""
         bits = 0
         if policy != "auto":
             for name in policy.split("+"):

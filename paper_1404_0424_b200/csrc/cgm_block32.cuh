@@ -183,6 +183,242 @@ __device__ __forceinline__ void block32_cg_exact(const KernelParams& p, const fl
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-tiled exact CG (cfg5 default): a warp runs 8 systems, lane L owns
+// user rows 2 (L & 15), + 1 of the 4 systems (L >> 4) * 4 .. + 3 of its
+// group.  Per column pair (j, j + 1) a lane issues 2 LDS.128 of G (its two
+// rows, a 16-lane broadcast pair: 4 wavefronts per warp) and 4 broadcast
+// LDS.128 of p (1 wavefront each: the two halves' rows sit 16 banks apart
+// with the kPStr row stride) for 32 FFMA2 -- twice the math per shared-memory
+// wavefront of the lane-per-row form, which was balanced between the two.
+// The inner products reduce over 16 lanes (sum4_16_owned: 5 shuffles for the
+// 4 systems of a half, lane L ends with system (L >> 2) & 3 of its half, the
+// system's 4 owner lanes), the owners apply the freeze / breakdown rules and
+// form alpha / beta, one shuffle per system hands them out.
+constexpr int kTSpw = 8;   // systems per warp (tiled)
+constexpr int kTWarps = 4;  // warps per CTA (tiled)
+constexpr int kPStr = 34;   // float2 row stride of the broadcast p rows
+
+__device__ __forceinline__ float sum4_16_owned(const float (&v)[4]) {
+  const int lane = threadIdx.x & 31;
+  const bool b3 = lane & 8, b2 = lane & 4;
+  float k0 = b3 ? v[2] : v[0], k1 = b3 ? v[3] : v[1];
+  const float s0 = b3 ? v[0] : v[2], s1 = b3 ? v[1] : v[3];
+  k0 += __shfl_xor_sync(0xffffffffu, s0, 8);
+  k1 += __shfl_xor_sync(0xffffffffu, s1, 8);
+  float k = b2 ? k1 : k0;
+  k += __shfl_xor_sync(0xffffffffu, b2 ? k0 : k1, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+  return k;  // system ((L >> 3) & 1) * 2 + ((L >> 2) & 1) = (L >> 2) & 3 of half L >> 4
+}
+
+struct Block32TSmem {
+  int bar, buf, bufb, tb, ps, hist, msh, msh_doubles, sys_st, total;
+  __host__ __device__ static int align(int x) { return (x + 127) & ~127; }
+  __host__ __device__ void plan(int S, int St, int K, int span) {
+    const int nsys = S + St;
+    int o = 0;
+    bar = o; o = align(o + 16);
+    tb = align(span);
+    bufb = align(tb + St * 32 * 8);
+    buf = o; o = align(o + 2 * bufb);
+    ps = o; o = align(o + (nsys + kTSpw - 1) / kTSpw * kTSpw * kPStr * 8);  // p rows, then v_K (uplink)
+    hist = o; o = align(o + S * K * 2 * 4);
+    msh_doubles = kTWarps * kMomScratch > S * kLaneScratch ? kTWarps * kMomScratch : S * kLaneScratch;
+    msh = o; o = align(o + msh_doubles * 8);
+    sys_st = o; o = align(o + nsys);
+    total = o;
+  }
+};
+
+__device__ __forceinline__ void block32t_cg_exact(const KernelParams& p, const float2* mfsrc,
+                                                  const float2* Ts, int base, const float2* Gs,
+                                                  float2* Ps, float* hist, uint8_t* sys_st,
+                                                  float2* zout) {
+  constexpr int UP = 32, NS = 4;
+  const int S = p.S, St = p.St;
+  const int nsys = S + St;
+  const int Kmax = p.K > p.Kt ? p.K : p.Kt;
+  const int lane = threadIdx.x & 31;
+  const int h = lane >> 4, u0 = 2 * (lane & 15);
+  float reg[NS];
+  float2 v[2][NS], r[2][NS], pp[2][NS];
+  float nrm[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int sy = base + 4 * h + s;
+    const bool live = sy < nsys, down = sy >= S;
+    reg[s] = down ? p.rho_inv_d : p.rho_inv_u;
+    float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live)
+      b = *reinterpret_cast<const float4*>(down ? Ts + (sy - S) * UP + u0 : mfsrc + sy * UP + u0);
+    v[0][s] = v[1][s] = make_float2(0.f, 0.f);
+    r[0][s] = pp[0][s] = make_float2(b.x, b.y);
+    r[1][s] = pp[1][s] = make_float2(b.z, b.w);
+    *reinterpret_cast<float4*>(Ps + (4 * h + s) * kPStr + u0) = b;
+    nrm[s] = cnorm(r[0][s]) + cnorm(r[1][s]);
+  }
+  // this lane's system (owner of its scalar work): (L >> 2) & 3 of half h
+  const int my = (lane >> 2) & 3, sy_own = base + 4 * h + my;
+  const bool live_own = sy_own < nsys, down_own = sy_own >= S;
+  const int iters_own = live_own ? (down_own ? p.Kt : p.K) : 0;
+  float rn = sum4_16_owned(nrm);
+  const float rn0 = rn;
+  bool broke = false;
+  const float2* Pg = Ps + 4 * h * kPStr;  // this half's four p rows
+  __syncwarp();
+  for (int k = 1; k <= Kmax; ++k) {
+    // e = (G + reg I) p: G[u][j] = conj(G[j][u]) (packed (re, -im) x p.x, p.y)
+    unsigned long long a[2][NS], b[2][NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) a[0][s] = a[1][s] = b[0][s] = b[1][s] = 0ull;
+#pragma unroll 2
+    for (int j = 0; j < UP; j += 2) {
+      const float4 g0 = *reinterpret_cast<const float4*>(Gs + j * UP + u0);
+      const float4 g1 = *reinterpret_cast<const float4*>(Gs + (j + 1) * UP + u0);
+      const unsigned long long g00 = f2pack(g0.x, -g0.y), g01 = f2pack(g0.z, -g0.w);
+      const unsigned long long g10 = f2pack(g1.x, -g1.y), g11 = f2pack(g1.z, -g1.w);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const ulonglong2 pj = *reinterpret_cast<const ulonglong2*>(Pg + s * kPStr + j);
+        const unsigned long long x0 = f2dup_lo(pj.x), y0 = f2dup_hi(pj.x);
+        const unsigned long long x1 = f2dup_lo(pj.y), y1 = f2dup_hi(pj.y);
+        ffma2(a[0][s], g00, x0);
+        ffma2(b[0][s], g00, y0);
+        ffma2(a[1][s], g01, x0);
+        ffma2(b[1][s], g01, y0);
+        ffma2(a[0][s], g10, x1);
+        ffma2(b[0][s], g10, y1);
+        ffma2(a[1][s], g11, x1);
+        ffma2(b[1][s], g11, y1);
+      }
+    }
+    float2 e[2][NS];
+    float part[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      part[s] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float2 A = f2unpack(a[q][s]), B = f2unpack(b[q][s]);
+        e[q][s].x = fmaf(reg[s], pp[q][s].x, A.x - B.y);
+        e[q][s].y = fmaf(reg[s], pp[q][s].y, A.y + B.x);
+        part[s] += pp[q][s].x * e[q][s].x + pp[q][s].y * e[q][s].y;  // Re p^H e
+      }
+    }
+    const float curv = sum4_16_owned(part);
+    // owner lanes: solvers.cpp:21-27 freeze, :55-57 breakdown
+    const bool step = k <= iters_own;
+    const bool frozen = !(rn > 1e-28f * rn0);
+    const bool go = step && !frozen && !broke;
+    if (go && curv < 1e-30f) broke = true;
+    const bool upd = go && !broke;
+    const float alpha = upd ? __fdividef(rn, curv) : 1.f;
+    const float a_eff = upd ? alpha : 0.f;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const float as = __shfl_sync(0xffffffffu, a_eff, (lane & 16) + 4 * s);
+      part[s] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        v[q][s].x = fmaf(as, pp[q][s].x, v[q][s].x);
+        v[q][s].y = fmaf(as, pp[q][s].y, v[q][s].y);
+        r[q][s].x = fmaf(-as, e[q][s].x, r[q][s].x);
+        r[q][s].y = fmaf(-as, e[q][s].y, r[q][s].y);
+        part[s] += cnorm(r[q][s]);
+      }
+    }
+    const float rnx = sum4_16_owned(part);
+    const float beta = upd ? rnx * __fdividef(1.f, rn) : 0.f;
+    if (upd) rn = rnx;
+    if (step && !down_own && (lane & 3) == 0) {  // the exact tracker's history
+      hist[(sy_own * Kmax + (k - 1)) * 2 + 0] = alpha;
+      hist[(sy_own * Kmax + (k - 1)) * 2 + 1] = beta;
+    }
+    __syncwarp();  // every lane's matvec reads of Ps are done
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const float bs = __shfl_sync(0xffffffffu, beta, (lane & 16) + 4 * s);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        pp[q][s].x = fmaf(bs, pp[q][s].x, r[q][s].x);
+        pp[q][s].y = fmaf(bs, pp[q][s].y, r[q][s].y);
+      }
+      *reinterpret_cast<float4*>(Ps + (4 * h + s) * kPStr + u0) =
+          make_float4(pp[0][s].x, pp[0][s].y, pp[1][s].x, pp[1][s].y);
+    }
+    __syncwarp();
+  }
+  // ------------------------------------------------ per-system epilogue
+  if (live_own && (lane & 3) == 0) {
+    if (down_own) zout[St * UP + (sy_own - S)] = make_float2(broke ? 1.f : 0.f, 0.f);
+    else sys_st[sy_own] = broke ? 1 : 0;
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int sy = base + 4 * h + s;
+    if (sy >= nsys) continue;
+    const float4 vv = make_float4(v[0][s].x, v[0][s].y, v[1][s].x, v[1][s].y);
+    if (sy >= S) *reinterpret_cast<float4*>(zout + (sy - S) * UP + u0) = vv;  // for precode_q_kernel
+    else *reinterpret_cast<float4*>(Ps + (4 * h + s) * kPStr + u0) = vv;     // v_K over its own p row
+  }
+}
+
+// Persistent tiled-CG kernel (exact tracker, U = 32): 4 warps, 4 CTAs per SM;
+// the workspace span / transmit-vector double buffer of block32_kernel.
+__global__ void __launch_bounds__(32 * kTWarps, 4) block32t_kernel(const KernelParams p) {
+  constexpr int UP = 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int S = p.S, St = p.St, U = p.U;
+  const int nsys = S + St;
+  const int Kmax = p.K > p.Kt ? p.K : p.Kt;
+  WsOffsets W;
+  W.plan(UP, S, p.K, true, p.fx, p.zs);
+  const uint32_t span = static_cast<uint32_t>(W.z) * 8u, tbytes = static_cast<uint32_t>(St * U) * 8u;
+  Block32TSmem L;
+  L.plan(S, St, Kmax, static_cast<int>(span));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  float2* Ps = reinterpret_cast<float2*>(smem + L.ps);
+  float* hist = reinterpret_cast<float*>(smem + L.hist);
+  uint8_t* sys_st = reinterpret_cast<uint8_t*>(smem + L.sys_st);
+  const int nt = blockDim.x, nw = nt >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const long n_local = p.n_sc > blockIdx.x ? (p.n_sc - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto bufp = [&](long i) { return smem + L.buf + (i & 1) * L.bufb; };
+  auto issue = [&](long i) {
+    const long lsc = blockIdx.x + i * gridDim.x;
+    unsigned char* dst = bufp(i);
+    fence_proxy_async();  // generic reads of this buffer (two subcarriers ago) before the async write
+    mbar_expect_tx(bar + (i & 1), span + tbytes);
+    bulk_g2s(dst, p.ws + lsc * W.stride, span, bar + (i & 1));
+    if (St > 0) bulk_g2s(dst + L.tb, p.T + (p.sc_base + lsc) * St * U, tbytes, bar + (i & 1));
+  };
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  __syncthreads();
+  if (tid == 0 && n_local > 0) issue(0);
+  for (long i = 0; i < n_local; ++i) {
+    if (tid == 0 && i + 1 < n_local) issue(i + 1);
+    mbar_wait(bar + (i & 1), static_cast<uint32_t>((i >> 1) & 1));
+    const long lsc = blockIdx.x + i * gridDim.x;
+    const long sc = p.sc_base + lsc;
+    const float2* wsb = reinterpret_cast<const float2*>(bufp(i));  // smem copy of the ws span
+    const float2* Ts = reinterpret_cast<const float2*>(bufp(i) + L.tb);
+    float2* zout = p.ws + lsc * W.stride + W.z;
+    for (int base = warp * kTSpw; base < nsys; base += nw * kTSpw)
+      block32t_cg_exact(p, wsb + W.mf, Ts, base, wsb + W.g, Ps + base * kPStr, hist, sys_st, zout);
+    if (S > 0) {
+      __syncthreads();
+      moments_tail<UP>(p, wsb, W, sc, Kmax, hist, Ps, sys_st, nt,
+                       reinterpret_cast<double*>(smem + L.msh), kPStr, L.msh_doubles);
+    }
+    __syncthreads();  // buffer i & 1 and the per-subcarrier scratch are free
+  }
+}
+
 template <bool EXACT>
 __device__ __forceinline__ void block32_cg(const KernelParams& p, long sc, const float2* mfsrc,
                                            const float2* Ts, int base, const float2* Gs,

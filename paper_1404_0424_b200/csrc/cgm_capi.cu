@@ -197,6 +197,7 @@ constexpr int kPolRowsCta = 16;     // U = 32 with transmit vectors: the 8-warp 
 constexpr int kPolPoisonWs = 32;    // test only: fill the workspace with NaN before every chunk
 constexpr int kPolTileMoments = 64; // U = 32, FP32 moments: the 4x4-tile CTA kernel instead of warp rows
 constexpr int kPolSerialChunks = 128;  // split path: every chunk on the call's stream (no two-stream overlap)
+constexpr int kPolUntiledCg = 256;     // cfg5 block CG: lane-per-row 8-warp kernel instead of the tiled one
 
 // Device workspace of the split path.  A call captured into a CUDA graph
 // bakes in this pointer, so a larger call never frees it: the old buffer
@@ -362,7 +363,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
                 L2.total, ctx->max_smem);
   void (*k2)(cgm::KernelParams) = cgm::solve_kernel<UP, EXACT>;
   int smem2 = L2.total;
-  enum { kLanes, kLanesPf, kPairs, kRowsCta, kBlock } mode = kLanes;
+  enum { kLanes, kLanesPf, kPairs, kRowsCta, kBlock, kBlockT } mode = kLanes;
   int pair_ns = 2;
   if constexpr (UP == 32) {
     // persistent shared-G block kernel (+ precode_q_kernel for transmit
@@ -380,6 +381,15 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
       k2 = cgm::block32_kernel<EXACT>;
       smem2 = BL.total;
       p.zs = p.St;  // the transmit vectors' v_K go through the workspace
+      if constexpr (EXACT) {
+        cgm::Block32TSmem BT;
+        BT.plan(p.S, p.St, Kmax, WB.z * 8);
+        if (!(ctx->policy & kPolUntiledCg) && BT.total <= ctx->max_smem) {  // register-tiled CG
+          mode = kBlockT;
+          k2 = cgm::block32t_kernel;
+          smem2 = BT.total;
+        }
+      }
     } else if (!(ctx->policy & kPolLaneSolve)) {
       if (p.St == 0) {
         mode = kPairs;
@@ -418,10 +428,11 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   if (mode == kRowsCta) nw2 = nsys >= 16 ? 8 : 2;
   if (mode == kBlock)  // NS systems per warp
     nw2 = std::min(cgm::kBlkMaxW, (nsys + cgm::kBlkNS - 1) / cgm::kBlkNS);
+  if (mode == kBlockT) nw2 = cgm::kTWarps;
   long g2cap = 1L << 40;
   CUtensorMap tmH{};
   auto pq_kernel = cgm::precode_q_kernel<2>;
-  if (mode == kBlock) {  // persistent
+  if (mode == kBlock || mode == kBlockT) {  // persistent
     int occ2 = 0;
     CGM_PREP(ctx, k2, 32 * nw2, smem2, &occ2);
     g2cap = static_cast<long>(std::max(occ2, 1)) * ctx->sms;
@@ -492,7 +503,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
         k2<<<static_cast<unsigned>(std::min(n, g2cap)), 32 * nw2, smem2, st>>>(q);
     });
     if (r) return r;
-    if (mode == kBlock && p.St > 0) {  // q = H_d^H v, gain, s
+    if ((mode == kBlock || mode == kBlockT) && p.St > 0) {  // q = H_d^H v, gain, s
       cgm::PrecodeQSmem PQ;
       PQ.plan(p.B, p.St);
       r = timed(ctx, st, 4, [&] {
@@ -993,7 +1004,7 @@ int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, lon
 int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy) {
   if (!ctx || policy < 0 ||
       policy > (kPolFfmaChannel | kPolSplitSmall | kPolLaneSolve | kPolBlockUp | kPolRowsCta | kPolTileMoments |
-                kPolSerialChunks |
+                kPolSerialChunks | kPolUntiledCg |
                 kPolPoisonWs))
     return fail(ctx, CGM_EINVAL, "unknown kernel policy %d", policy);
   ctx->policy = policy;

@@ -1008,7 +1008,7 @@ __device__ __forceinline__ void moments_tail_lanes(const KernelParams& p, const 
                                                    const WsOffsets& W, long sc, int Kmax,
                                                    const float* hist, const float2* Vs,
                                                    const uint8_t* sys_st, double* msh, int nthr,
-                                                   int bar_id) {
+                                                   int bar_id, int vstride = UP) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = nthr >> 5;
   const int S = p.S, U = p.U, K = p.K;
   const float2 cdv = ws[W.cd];
@@ -1034,7 +1034,7 @@ __device__ __forceinline__ void moments_tail_lanes(const KernelParams& p, const 
       float mu, rho;
       moments_row(sh, c, K, mom, UP, i, p.es, p.n0, mu, rho, kLaneK);
       const long o = (sc * S + s) * static_cast<long>(U) + i;
-      const float2 xh = ok ? Vs[s * UP + i] : make_float2(0.f, 0.f);
+      const float2 xh = ok ? Vs[s * vstride + i] : make_float2(0.f, 0.f);
       if (!ok) mu = rho = 0.f;
       if (p.xhat) p.xhat[o] = xh;
       if (p.mu) p.mu[o] = mu;
@@ -1054,13 +1054,14 @@ template <int UP>
 __device__ __forceinline__ void moments_tail(const KernelParams& p, const float2* ws,
                                              const WsOffsets& W, long sc, int Kmax,
                                              const float* hist, const float2* Vs,
-                                             const uint8_t* sys_st, int nt, double* msh) {
+                                             const uint8_t* sys_st, int nt, double* msh,
+                                             int vstride = UP, int msh_doubles = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = nt >> 5;
   const int S = p.S, U = p.U, K = p.K;
   const float2 cdv = ws[W.cd];
   const double* mom = reinterpret_cast<const double*>(ws + W.t);
-  if (K <= kLaneK && S * kLaneScratch <= nw * kMomScratch) {
-    moments_tail_lanes<UP>(p, ws, W, sc, Kmax, hist, Vs, sys_st, msh, nt, 0);
+  if (K <= kLaneK && S * kLaneScratch <= (msh_doubles > 0 ? msh_doubles : nw * kMomScratch)) {
+    moments_tail_lanes<UP>(p, ws, W, sc, Kmax, hist, Vs, sys_st, msh, nt, 0, vstride);
     return;
   }
   double* sh = msh + warp * kMomScratch;
@@ -1071,7 +1072,7 @@ __device__ __forceinline__ void moments_tail(const KernelParams& p, const float2
       float mu, rho;
       moments_row(sh, c, K, mom, UP, i, p.es, p.n0, mu, rho);
       const long o = (sc * S + s) * static_cast<long>(U) + i;
-      const float2 xh = ok ? Vs[s * UP + i] : make_float2(0.f, 0.f);
+      const float2 xh = ok ? Vs[s * vstride + i] : make_float2(0.f, 0.f);
       if (!ok) mu = rho = 0.f;
       if (p.xhat) p.xhat[o] = xh;
       if (p.mu) p.mu[o] = mu;

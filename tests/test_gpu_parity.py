@@ -82,3 +82,34 @@ def test_fused_parity_cfg5(policy_ctx, checker):
     check_detect({k: got[k] for k in ("xhat", "mu", "rho", "llr", "status")}, want_u, "cfg5 uplink")
     check_precode({"q": got["q"], "s": got["s"], "gain": got["gain"], "status": got["pstatus"]},
                   want_d, "cfg5 downlink")
+
+
+@pytest.mark.parametrize("S,St,K,Kt,B", [(16, 16, 4, 2, 256), (5, 3, 3, 4, 128), (13, 7, 4, 4, 256),
+                                         (2, 9, 2, 5, 192), (16, 1, 6, 1, 256)])
+@pytest.mark.parametrize("policy", ["auto", "untiled_cg"])
+def test_detect_precode_ragged_systems(gpu_ctx, checker, S, St, K, Kt, B, policy):
+    """The cfg5 path (block CG + moment extraction + TMA precoder) with system
+    counts that do not fill the CG warps (8 systems per warp tiled, 4
+    untiled), different uplink / downlink iteration counts and B below 256,
+    against the reference."""
+    cfg = get_config("cfg5")
+    n_sc = 37
+    H, Y = gpu_ctx.generate_uplink(B, cfg.U, n_sc, S, cfg.seed, cfg.qam_bits, cfg.n0)
+    T = gpu_ctx.generate_symbols(cfg.U, n_sc, 16, cfg.seed + 1, cfg.qam_bits)[:, :St].contiguous()
+    gpu_ctx.set_kernel_policy(policy)
+    try:
+        out = gpu_ctx.detect_precode_cg(H, Y, cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, K,
+                                        "exact", T, cfg.rho_d, Kt)
+        torch.cuda.synchronize()
+    finally:
+        gpu_ctx.set_kernel_policy("auto")
+    got = {k: to_np(v) for k, v in out.items()}
+    Hn = to_np(H)
+    want_u = checker.detect(Hn, to_np(Y), cfg.rho_u, cfg.n0, cfg.es, cfg.qam_bits, K, "exact",
+                            threads=8)
+    Hd = np.ascontiguousarray(np.conj(np.transpose(Hn, (0, 2, 1))))
+    want_d = checker.precode(Hd, to_np(T), cfg.rho_d, Kt, threads=8)
+    tag = f"S{S} St{St} K{K} Kt{Kt} B{B} {policy}"
+    check_detect({k: got[k] for k in ("xhat", "mu", "rho", "llr", "status")}, want_u, tag)
+    check_precode({"q": got["q"], "s": got["s"], "gain": got["gain"], "status": got["pstatus"]},
+                  want_d, tag)

@@ -203,6 +203,7 @@ def test_precode_uplink_layout_equals_downlink_layout(gpu_ctx, U, B, K):
     ("cfg5", "lane_solve"),        # default: 8-warp row CTA with the precoder tail
     ("cfg5", "ffma_channel"),
     ("cfg5", "tile_moments"),      # default: warp-per-subcarrier moments kernel
+    ("cfg5", "untiled_cg"),        # default: register-tiled block CG (8 systems per warp)
     ("cfg1", "split_small"),       # default: fused U <= 16 detector, one warp per subcarrier
 ])
 def test_kernel_variants_agree(gpu_ctx, checker, name, policy):
