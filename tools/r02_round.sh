@@ -16,6 +16,6 @@ done
 timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu > $O/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_cfg5.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu > $O/ncu_launch.log 2>&1
-bash tools/prof_cfg5.sh $O/prof "channel_tc moments_rows32 block32_kernel precode_q_kernel"
+bash tools/prof_cfg5.sh $O/prof "channel_tc moments_rows32 block32t_kernel precode_q_kernel"
 rm -f $O/prof/*.ncu-rep
 ls -la $O
