@@ -50,7 +50,7 @@ def build(verbose: bool = False) -> str:
         objs.append(o)
         if _newer(o, [s] + hdeps + [__file__]):
             jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v",
-                         "-Xcompiler", "-fPIC", *inc, "-c", s, "-o", o])
+                         "-Xcompiler", "-fPIC", *os.environ.get("CGM_NVCC_EXTRA", "").split(), *inc, "-c", s, "-o", o])
     with ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:  # translation units in parallel
         for out in ex.map(_run, jobs):
             log += out

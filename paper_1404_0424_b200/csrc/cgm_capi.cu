@@ -560,7 +560,8 @@ template <int UP>
 int launch_precode_small(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   cgm::PrecodeSmallSmem L;
   L.plan(UP, p.B, p.St);
-  auto k = cgm::precode_small_kernel<UP>;
+  // q of an antenna pass in registers: 4 chunks of 32 antennas up to B = 128, else 16
+  auto k = p.B <= 128 ? cgm::precode_small_kernel<UP, 4> : cgm::precode_small_kernel<UP, 16>;
   int occ = 0;
   CGM_PREP(ctx, k, cgm::PrecodeSmallGeo<UP>::NT, L.total, &occ);
   const long grid = std::max<long>(1, std::min<long>(p.n_sc, static_cast<long>(std::max(occ, 1)) * ctx->sms));

@@ -237,16 +237,28 @@ def test_kernel_variants_agree(gpu_ctx, checker, name, policy):
     check_detect(got, want, name + " default")
 
 
-@pytest.mark.parametrize("U,B,S,K", [(16, 128, 1, 3), (8, 64, 3, 4), (5, 30, 2, 2), (13, 96, 4, 5)])
-def test_fused_small_precoder_matches_split_and_oracle(gpu_ctx, checker, U, B, S, K):
-    """The fused U <= 16 precoder (cgm_precode_small.cuh: one HBM read of H_d)
-    agrees with the channel + solve pair to FP32 rounding and with the
-    oracle, ragged U and B included (B = 30: no TMA, plain copies)."""
+@pytest.mark.parametrize("U,B,S,K,misalign", [
+    (16, 128, 1, 3, False), (8, 64, 3, 4, False), (5, 30, 2, 2, False), (13, 96, 4, 5, False),
+    (12, 200, 2, 3, False),  # B > 128: four 64-antenna chunks (the last one short), q held 16 per lane
+    (16, 512, 1, 2, False),  # the largest B of the fused kernel
+    (16, 128, 2, 3, True),   # H_d 8 bytes off 16-byte alignment: plain copies instead of cp.async
+    (7, 70, 3, 4, True),
+])
+def test_fused_small_precoder_matches_split_and_oracle(gpu_ctx, checker, U, B, S, K, misalign):
+    """The fused U <= 16 precoder (cgm_precode_small.cuh: H_d streamed in
+    64-antenna chunks, one HBM read) agrees with the channel + solve pair to
+    FP32 rounding and with the oracle: ragged U and B, short last chunks,
+    several transmit vectors (one streamed q pass each), misaligned H_d."""
     g = torch.Generator().manual_seed(100 + U)
     n_sc = 300
     Hd = torch.complex(torch.randn(n_sc, U, B, generator=g), torch.randn(n_sc, U, B, generator=g))
     T = torch.complex(torch.randn(n_sc, S, U, generator=g), torch.randn(n_sc, S, U, generator=g))
     Hd, T = (Hd / 2 ** 0.5).cuda(), (T / 2 ** 0.5).cuda()
+    if misalign:
+        flat = torch.empty(Hd.numel() + 1, dtype=Hd.dtype, device=Hd.device)
+        flat[1:] = Hd.reshape(-1)
+        Hd = flat[1:].view(n_sc, U, B)
+        assert Hd.data_ptr() % 16 == 8
     T[7] = 0  # zero transmit vectors: zero_input status, gain 0
     l0 = gpu_ctx.kernel_launches
     a = gpu_ctx.precode_cg(Hd, T, 0.625, K)
