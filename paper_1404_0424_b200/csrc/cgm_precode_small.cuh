@@ -173,12 +173,12 @@ __global__ void __launch_bounds__(32, MQ <= 4 ? 15 : 10) precode_small_kernel(co
   const int fq0 = (item_part * NPF) / KP, fnq = ((item_part + 1) * NPF) / KP - fq0;
   // the rotated start spreads a quarter-warp's LDS.128 over the eight 16-byte
   // bank groups; for U = 16 and 64-antenna chunks a searched table makes
-  // every x / y load of a full chunk conflict-free (tools/ps_rotation.py:
-  // 86 wavefronts per chunk instead of 160 with tile mod range)
+  // the x / y loads of a full chunk nearly conflict-free (tools/ps_rotation.py:
+  // 96 wavefronts per chunk, 88 = none, instead of 178 with tile mod range)
   int fst = fnq > 0 ? item_tile % fnq : 0;
   if constexpr (UP == 16 && CB == 64) {
-    constexpr unsigned char kRot[32] = {9, 1, 1, 6, 6, 3, 6, 6, 5, 5, 3, 0, 0, 2, 1, 2,
-                                        0, 1, 1, 0, 7, 1, 10, 0, 1, 3, 3, 1, 1, 2, 0, 0};
+    constexpr unsigned char kRot[32] = {2, 2, 2, 1, 0, 0, 1, 1, 0, 0, 7, 1, 1, 1, 1, 0,
+                                        10, 5, 5, 10, 5, 5, 5, 10, 0, 0, 6, 1, 0, 5, 0, 0};
     fst = kRot[lane];
   }
 
@@ -216,11 +216,7 @@ __global__ void __launch_bounds__(32, MQ <= 4 ? 15 : 10) precode_small_kernel(co
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
               x[r] = *reinterpret_cast<const ulonglong2*>(hu + r * LDH + b);
-              y[r] = x[r];
-            }
-            if (rb != cb) {  // diagonal tiles: the same rows
-#pragma unroll
-              for (int r = 0; r < 4; ++r) y[r] = *reinterpret_cast<const ulonglong2*>(hv + r * LDH + b);
+              y[r] = *reinterpret_cast<const ulonglong2*>(hv + r * LDH + b);
             }
 #pragma unroll
             for (int r = 0; r < 4; ++r)

@@ -32,7 +32,7 @@ def cost(rot):
                 groups = {}
                 for lane in range(ph * 8, ph * 8 + 8):
                     L = lanes[lane]
-                    if L is None or it >= L[3] or (which == 1 and L[0] == L[1]):
+                    if L is None or it >= L[3]:
                         continue
                     q = L[2] + (rot[lane] + it) % L[3]
                     addr = 4 * (L[0] if which == 0 else L[1]) * LD16 + q
@@ -42,14 +42,19 @@ def cost(rot):
 
 
 base = [(L[4] % L[3]) if L else 0 for L in lanes]
-best, bc = base[:], cost(base)
-print("tile mod range:", bc)
-random.seed(1)
-for _ in range(20000):
-    c = best[:]
-    l = random.randrange(30)
-    c[l] = random.randrange(lanes[l][3])
+print("tile mod range:", cost(base))
+best, bc = None, 10 ** 9
+for seed in range(12):  # hill climbing with restarts
+    random.seed(seed)
+    c = [random.randrange(L[3]) if L else 0 for L in lanes]
     cc = cost(c)
-    if cc <= bc:
+    for _ in range(15000):
+        d = c[:]
+        l = random.randrange(30)
+        d[l] = random.randrange(lanes[l][3])
+        dc = cost(d)
+        if dc <= cc:
+            c, cc = d, dc
+    if cc < bc:
         best, bc = c, cc
-print("searched:", bc, best)
+print("searched:", bc, best, "(88 = one wavefront per phase)")
