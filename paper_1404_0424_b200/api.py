@@ -91,7 +91,7 @@ class Context:
 
     POLICY_FLAGS = {"ffma_channel": 1, "split_small": 2, "lane_solve": 4, "block_uplink": 8,
                     "rows_cta": 16, "poison_ws": 32, "tile_moments": 64, "serial_chunks": 128,
-                    "untiled_cg": 256}
+                    "untiled_cg": 256, "pairs_cg": 512}
 
     def set_kernel_policy(self, policy: str):
         """Kernel-variant switches for A/B tests: "auto" (production defaults)
@@ -107,7 +107,9 @@ class Context:
         "serial_chunks" (every workspace chunk on the call's stream instead of
         alternating two streams), "untiled_cg" (the lane-per-row 8-warp block
         CG kernel instead of the register-tiled one for the exact tracker with
-        transmit vectors, cfg5)."""
+        transmit vectors, cfg5), "pairs_cg" (the warp-per-pair-of-systems
+        kernel with the Gram row in registers instead of the register-tiled
+        block CG for approximate-tracker uplink calls, cfg2)."""
         bits = 0
         if policy != "auto":
             for name in policy.split("+"):

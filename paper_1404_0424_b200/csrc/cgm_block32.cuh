@@ -419,6 +419,225 @@ __global__ void __launch_bounds__(32 * kTWarps, 4) block32t_kernel(const KernelP
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-tiled CG with the approximate tracker (uplink only: cfg2).  Same
+// lane layout as block32t_cg_exact -- a warp runs 8 systems, lane L owns user
+// rows 2 (L & 15), + 1 of the 4 systems of its half -- with Eq. (11)'s
+// diagonal recursion (detect.cpp:409-427) per (row, system) in registers.
+// The system's owner lanes apply the freeze / breakdown rules and form
+// alpha, beta and the recursion's two per-system scalars c1 = alpha_k
+// (1 + beta_{k-1}) / alpha_{k-1}, c2 = alpha_k beta_{k-2} / alpha_{k-2}
+// (detect.cpp:350-358); four shuffles per system hand them out.  alpha
+// travels negated when the system does not update (alpha = 1 by the
+// reference's rule, but v and r stay put), so no fifth value is needed.
+struct Block32ASmem {
+  int bar, buf, bufb, ps, total;
+  __host__ __device__ static int align(int x) { return (x + 127) & ~127; }
+  __host__ __device__ void plan(int S, int span) {
+    int o = 0;
+    bar = o; o = align(o + 16);
+    bufb = align(span);
+    buf = o; o = align(o + 2 * bufb);
+    ps = o; o = align(o + (S + kTSpw - 1) / kTSpw * kTSpw * kPStr * 8);
+    total = o;
+  }
+};
+
+__device__ __forceinline__ void block32a_cg(const KernelParams& p, long sc, const float2* mfsrc,
+                                            int base, const float2* Gs, float2* Ps) {
+  constexpr int UP = 32, NS = 4;
+  const int S = p.S, U = p.U, K = p.K;
+  const int lane = threadIdx.x & 31;
+  const int h = lane >> 4, u0 = 2 * (lane & 15);
+  const float reg = p.rho_inv_u;
+  const float gd[2] = {Gs[u0 * UP + u0].x, Gs[(u0 + 1) * UP + u0 + 1].x};
+  float2 v[2][NS], r[2][NS], pp[2][NS];
+  float f0[2][NS], f1[2][NS], f2[2][NS];
+  float nrm[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int sy = base + 4 * h + s;
+    float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (sy < S) b = *reinterpret_cast<const float4*>(mfsrc + sy * UP + u0);
+    v[0][s] = v[1][s] = make_float2(0.f, 0.f);
+    r[0][s] = pp[0][s] = make_float2(b.x, b.y);
+    r[1][s] = pp[1][s] = make_float2(b.z, b.w);
+    *reinterpret_cast<float4*>(Ps + (4 * h + s) * kPStr + u0) = b;
+    nrm[s] = cnorm(r[0][s]) + cnorm(r[1][s]);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) f0[q][s] = f1[q][s] = f2[q][s] = 0.f;
+  }
+  // this lane's system (owner of its scalar work): (L >> 2) & 3 of half h
+  const int my = (lane >> 2) & 3, sy_own = base + 4 * h + my;
+  const bool live_own = sy_own < S;
+  float rn = sum4_16_owned(nrm);
+  const float rn0 = rn;
+  bool broke = false;
+  float ia1 = 1.f, ia2 = 1.f, bm1 = 0.f, bm2 = 0.f;  // 1 / alpha and beta of the last two iterations
+  const float2* Pg = Ps + 4 * h * kPStr;  // this half's four p rows
+  __syncwarp();
+  for (int k = 1; k <= K; ++k) {
+    unsigned long long a[2][NS], b[2][NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) a[0][s] = a[1][s] = b[0][s] = b[1][s] = 0ull;
+#pragma unroll 2
+    for (int j = 0; j < UP; j += 2) {
+      const float4 g0 = *reinterpret_cast<const float4*>(Gs + j * UP + u0);
+      const float4 g1 = *reinterpret_cast<const float4*>(Gs + (j + 1) * UP + u0);
+      const unsigned long long g00 = f2pack(g0.x, -g0.y), g01 = f2pack(g0.z, -g0.w);
+      const unsigned long long g10 = f2pack(g1.x, -g1.y), g11 = f2pack(g1.z, -g1.w);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const ulonglong2 pj = *reinterpret_cast<const ulonglong2*>(Pg + s * kPStr + j);
+        const unsigned long long x0 = f2dup_lo(pj.x), y0 = f2dup_hi(pj.x);
+        const unsigned long long x1 = f2dup_lo(pj.y), y1 = f2dup_hi(pj.y);
+        ffma2(a[0][s], g00, x0);
+        ffma2(b[0][s], g00, y0);
+        ffma2(a[1][s], g01, x0);
+        ffma2(b[1][s], g01, y0);
+        ffma2(a[0][s], g10, x1);
+        ffma2(b[0][s], g10, y1);
+        ffma2(a[1][s], g11, x1);
+        ffma2(b[1][s], g11, y1);
+      }
+    }
+    float2 e[2][NS];
+    float part[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      part[s] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float2 A = f2unpack(a[q][s]), B = f2unpack(b[q][s]);
+        e[q][s].x = fmaf(reg, pp[q][s].x, A.x - B.y);
+        e[q][s].y = fmaf(reg, pp[q][s].y, A.y + B.x);
+        part[s] += pp[q][s].x * e[q][s].x + pp[q][s].y * e[q][s].y;  // Re p^H e
+      }
+    }
+    const float curv = sum4_16_owned(part);
+    // owner lanes: solvers.cpp:21-27 freeze, :55-57 breakdown
+    const bool frozen = !(rn > 1e-28f * rn0);
+    const bool go = live_own && !frozen && !broke;
+    if (go && curv < 1e-30f) broke = true;
+    const bool upd = go && !broke;
+    const float irn = __fdividef(1.f, rn);
+    const float alpha = upd ? rn * __fdividef(1.f, curv) : 1.f;
+    const float c1 = alpha * (1.f + bm1) * ia1, c2 = alpha * bm2 * ia2;
+    const float a_sgn = upd ? alpha : -alpha;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const float as = __shfl_sync(0xffffffffu, a_sgn, (lane & 16) + 4 * s);
+      const float ae = as > 0.f ? as : 0.f;
+      part[s] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        v[q][s].x = fmaf(ae, pp[q][s].x, v[q][s].x);
+        v[q][s].y = fmaf(ae, pp[q][s].y, v[q][s].y);
+        r[q][s].x = fmaf(-ae, e[q][s].x, r[q][s].x);
+        r[q][s].y = fmaf(-ae, e[q][s].y, r[q][s].y);
+        part[s] += cnorm(r[q][s]);
+      }
+      // Eq. (11) on the diagonal (detect.cpp:409-427); k = 1: L_1 = alpha_1
+      const float al = fabsf(as);
+      const float c1s = __shfl_sync(0xffffffffu, c1, (lane & 16) + 4 * s);
+      const float c2s = __shfl_sync(0xffffffffu, c2, (lane & 16) + 4 * s);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float nk = f0[q][s] + (c1s - al * (gd[q] + reg)) * (f0[q][s] - f1[q][s]) -
+                         c2s * (f1[q][s] - f2[q][s]);
+        f2[q][s] = f1[q][s];
+        f1[q][s] = f0[q][s];
+        f0[q][s] = k == 1 ? al : nk;
+      }
+    }
+    const float rnx = sum4_16_owned(part);
+    const float beta = upd ? rnx * irn : 0.f;
+    ia2 = ia1;
+    ia1 = upd ? curv * irn : 1.f;
+    bm2 = bm1;
+    bm1 = beta;
+    if (upd) rn = rnx;
+    __syncwarp();  // every lane's matvec reads of Ps are done
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const float bs = __shfl_sync(0xffffffffu, beta, (lane & 16) + 4 * s);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        pp[q][s].x = fmaf(bs, pp[q][s].x, r[q][s].x);
+        pp[q][s].y = fmaf(bs, pp[q][s].y, r[q][s].y);
+      }
+      *reinterpret_cast<float4*>(Ps + (4 * h + s) * kPStr + u0) =
+          make_float4(pp[0][s].x, pp[0][s].y, pp[1][s].x, pp[1][s].y);
+    }
+    __syncwarp();
+  }
+  // ------------- outputs: mu = Ltilde G_ii, rho = G_ii / N0 (detect.cpp:435-441)
+  const float rho_row[2] = {gd[0] / p.n0, gd[1] / p.n0};  // the same for every vector of the subcarrier
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int sy = base + 4 * h + s;
+    const bool ok = __shfl_sync(0xffffffffu, broke ? 0 : 1, (lane & 16) + 4 * s) != 0;
+    if (sy >= S) continue;
+    if (p.status && (lane & 15) == 0) p.status[sc * S + sy] = ok ? 0 : 1;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int u = u0 + q;
+      if (u >= U) continue;
+      const long o = (sc * S + sy) * static_cast<long>(U) + u;
+      const float2 xh = ok ? v[q][s] : make_float2(0.f, 0.f);
+      const float mu_u = ok ? f0[q][s] * gd[q] : 0.f;
+      const float rho_u = ok ? rho_row[q] : 0.f;
+      if (p.xhat) p.xhat[o] = xh;
+      if (p.mu) p.mu[o] = mu_u;
+      if (p.rho) p.rho[o] = rho_u;
+      if (p.llr) store_llrs_fast(xh, mu_u, rho_u, p.bits, p.llr + o * p.bits);
+    }
+  }
+}
+
+// Persistent tiled-CG kernel, approximate tracker, uplink only (U = 32):
+// ceil(S / 8) warps per CTA (cfg2: 2), the workspace span (G, matched
+// filters) double-buffered by cp.async.bulk as in block32t_kernel.  Held to
+// 168 registers (no spills; at 128 the tracker state spilled and the kernel
+// lost to the pairs kernel).
+__global__ void __launch_bounds__(32 * kTWarps, 3) block32a_kernel(const KernelParams p) {
+  constexpr int UP = 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int S = p.S;
+  WsOffsets W;
+  W.plan(UP, S, p.K, false, false, 0);
+  const uint32_t span = static_cast<uint32_t>(W.z) * 8u;
+  Block32ASmem L;
+  L.plan(S, static_cast<int>(span));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
+  float2* Ps = reinterpret_cast<float2*>(smem + L.ps);
+  const int nw = blockDim.x >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const long n_local = p.n_sc > blockIdx.x ? (p.n_sc - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto bufp = [&](long i) { return smem + L.buf + (i & 1) * L.bufb; };
+  auto issue = [&](long i) {
+    const long lsc = blockIdx.x + i * gridDim.x;
+    fence_proxy_async();  // generic reads of this buffer (two subcarriers ago) before the async write
+    mbar_expect_tx(bar + (i & 1), span);
+    bulk_g2s(bufp(i), p.ws + lsc * W.stride, span, bar + (i & 1));
+  };
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+  }
+  __syncthreads();
+  if (tid == 0 && n_local > 0) issue(0);
+  for (long i = 0; i < n_local; ++i) {
+    if (tid == 0 && i + 1 < n_local) issue(i + 1);
+    mbar_wait(bar + (i & 1), static_cast<uint32_t>((i >> 1) & 1));
+    const long sc = p.sc_base + blockIdx.x + i * gridDim.x;
+    const float2* wsb = reinterpret_cast<const float2*>(bufp(i));
+    for (int base = warp * kTSpw; base < S; base += nw * kTSpw)
+      block32a_cg(p, sc, wsb + W.mf, base, wsb + W.g, Ps + base * kPStr);
+    __syncthreads();  // buffer i & 1 is free
+  }
+}
+
 template <bool EXACT>
 __device__ __forceinline__ void block32_cg(const KernelParams& p, long sc, const float2* mfsrc,
                                            const float2* Ts, int base, const float2* Gs,

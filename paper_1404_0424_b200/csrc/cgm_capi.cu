@@ -198,6 +198,7 @@ constexpr int kPolPoisonWs = 32;    // test only: fill the workspace with NaN be
 constexpr int kPolTileMoments = 64; // U = 32, FP32 moments: the 4x4-tile CTA kernel instead of warp rows
 constexpr int kPolSerialChunks = 128;  // split path: every chunk on the call's stream (no two-stream overlap)
 constexpr int kPolUntiledCg = 256;     // cfg5 block CG: lane-per-row 8-warp kernel instead of the tiled one
+constexpr int kPolPairsCg = 512;       // cfg2 (approximate, uplink only): warp-per-pair kernel instead of the tiled block CG
 
 // Device workspace of the split path.  A call captured into a CUDA graph
 // bakes in this pointer, so a larger call never frees it: the old buffer
@@ -363,7 +364,7 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
                 L2.total, ctx->max_smem);
   void (*k2)(cgm::KernelParams) = cgm::solve_kernel<UP, EXACT>;
   int smem2 = L2.total;
-  enum { kLanes, kLanesPf, kPairs, kRowsCta, kBlock, kBlockT } mode = kLanes;
+  enum { kLanes, kLanesPf, kPairs, kRowsCta, kBlock, kBlockT, kBlockA } mode = kLanes;
   int pair_ns = 2;
   if constexpr (UP == 32) {
     // persistent shared-G block kernel (+ precode_q_kernel for transmit
@@ -391,7 +392,16 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
         }
       }
     } else if (!(ctx->policy & kPolLaneSolve)) {
-      if (p.St == 0) {
+      cgm::Block32ASmem BA;
+      BA.plan(p.S, WB.z * 8);
+      if (!EXACT && p.St == 0 && p.S >= 2 && p.U == 32 && !(ctx->policy & kPolPairsCg) &&
+          BA.total <= ctx->max_smem) {
+        // approximate tracker, several vectors per subcarrier (cfg2): the
+        // register-tiled block CG, ceil(S / 8) warps per CTA
+        mode = kBlockA;
+        k2 = cgm::block32a_kernel;
+        smem2 = BA.total;
+      } else if (p.St == 0) {
         mode = kPairs;
         pair_ns = p.S == 1 ? 1 : 2;
         k2 = pair_ns == 1 ? cgm::solve_rows32_pairs_kernel<EXACT, 1>
@@ -429,10 +439,11 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
   if (mode == kBlock)  // NS systems per warp
     nw2 = std::min(cgm::kBlkMaxW, (nsys + cgm::kBlkNS - 1) / cgm::kBlkNS);
   if (mode == kBlockT) nw2 = cgm::kTWarps;
+  if (mode == kBlockA) nw2 = std::min(cgm::kTWarps, (nsys + cgm::kTSpw - 1) / cgm::kTSpw);
   long g2cap = 1L << 40;
   CUtensorMap tmH{};
   auto pq_kernel = cgm::precode_q_kernel<2>;
-  if (mode == kBlock || mode == kBlockT) {  // persistent
+  if (mode == kBlock || mode == kBlockT || mode == kBlockA) {  // persistent
     int occ2 = 0;
     CGM_PREP(ctx, k2, 32 * nw2, smem2, &occ2);
     g2cap = static_cast<long>(std::max(occ2, 1)) * ctx->sms;
@@ -1005,7 +1016,7 @@ int cgm_ctx_kernel_times(cgm_ctx* ctx, double* channel_ms, double* solve_ms, lon
 int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy) {
   if (!ctx || policy < 0 ||
       policy > (kPolFfmaChannel | kPolSplitSmall | kPolLaneSolve | kPolBlockUp | kPolRowsCta | kPolTileMoments |
-                kPolSerialChunks | kPolUntiledCg |
+                kPolSerialChunks | kPolUntiledCg | kPolPairsCg |
                 kPolPoisonWs))
     return fail(ctx, CGM_EINVAL, "unknown kernel policy %d", policy);
   ctx->policy = policy;

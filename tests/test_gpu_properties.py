@@ -196,7 +196,8 @@ def test_precode_uplink_layout_equals_downlink_layout(gpu_ctx, U, B, K):
 
 
 @pytest.mark.parametrize("name,policy", [
-    ("cfg2", "lane_solve"),        # default: Gram-row-in-registers pairs kernel
+    ("cfg2", "lane_solve"),        # default: register-tiled block CG, approximate tracker
+    ("cfg2", "pairs_cg"),          # the warp-per-pair kernel (Gram row in registers, single-reduction CG)
     ("cfg4a_K2", "lane_solve"),    # default: exact pairs kernel, one system per warp (S = 1)
     ("cfg4a_K8", "lane_solve"),
     ("cfg4a_K8", "ffma_channel"),  # default: tcgen05 channel kernel
