@@ -292,6 +292,9 @@ def test_fused_small_precoder_matches_split_and_oracle(gpu_ctx, checker, U, B, S
     (96, 64, 3, 4, "exact", 4),    # U = 64 tensor-core channel: 32-antenna k-blocks, odd S
     (160, 64, 7, 3, "approx", 6),
     (64, 64, 32, 2, "approx", 2),  # the largest S of the U = 64 tensor-core path (N = 192)
+    (64, 32, 2, 3, "approx", 4),   # tiled approximate block CG (block32a): one warp, 2 of 8 system slots
+    (64, 32, 9, 4, "approx", 6),   # two warps, the second with one system
+    (64, 32, 37, 3, "approx", 4),  # more than 32 vectors: the CTA's warps take a second round
 ])
 def test_ragged_shapes_match_oracle(gpu_ctx, checker, B, U, S, K, tracker, bits):
     """Ragged U (between the kernels' row widths), odd B and S, several
