@@ -73,8 +73,11 @@ int cgm_synchronize(cgm_ctx* ctx);
  * 4 = lane-per-row solve kernel instead of the U = 32 row kernels,
  * 8 = shared-G block kernel for uplink-only U = 32, 16 = 8-warp row CTA
  * instead of the block kernel, 64 = 4x4-tile moments kernel instead of the
- * warp-per-subcarrier one (32: test only, NaN-poisoned workspace).
- * Every variant is parity-tested against the default. */
+ * warp-per-subcarrier one, 128 = every workspace chunk on the call's
+ * stream, 256 = lane-per-row block CG instead of the register-tiled one
+ * (exact tracker with transmit vectors), 512 = warp-per-pair kernel instead
+ * of the register-tiled approximate block CG (32: test only, NaN-poisoned
+ * workspace).  Every variant is parity-tested against the default. */
 int cgm_ctx_set_kernel_policy(cgm_ctx* ctx, int policy);
 /* Per-kernel device timing: while on, every channel/solve launch pair is
  * bracketed by CUDA events on the launch stream; cgm_ctx_kernel_times
