@@ -285,8 +285,9 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
         smem1 = T.total;
         // split / epilogue warps, measured (tools/microbench/tc_bench.cu,
         // bench.py): approximate 16 unified (cfg2 37.9 vs 39.4 us for 8 + 8
-        // specialised); exact 8 unified for few vectors per subcarrier, 8 + 8
-        // specialised from S = 8 on
+        // specialised); exact 16 unified for few vectors per subcarrier
+        // (cfg4a, 65,536 subcarriers: 0.86 ms against 0.925 for 8 unified and
+        // 0.96 for 8 + 8), 8 + 8 specialised from S = 8 on
         if (!EXACT) {
           k1 = cgm::channel_tc_kernel<16, 0>;
           nt1 = 32 * 18;
@@ -294,8 +295,8 @@ int launch_split(cgm_ctx* ctx, cgm::KernelParams p, cudaStream_t st) {
           k1 = cgm::channel_tc_kernel<8, 8>;
           nt1 = 32 * 18;
         } else {
-          k1 = cgm::channel_tc_kernel<8, 0>;
-          nt1 = 32 * 10;
+          k1 = cgm::channel_tc_kernel<16, 0>;
+          nt1 = 32 * 18;
         }
       }
     }
