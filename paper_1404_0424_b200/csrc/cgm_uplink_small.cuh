@@ -42,9 +42,11 @@ struct UpSmallSmem {
     bar = o; o = align(o + 8);
     hs = o; o = align(o + B * U * 8);
     ys = o; o = align(o + B * S * 8);
-    part = o; o = align(o + ntile * 16 * kp * 8);
+    // the Gram partials are dead once G is summed, before the Chebyshev
+    // basis is formed: the two share one region (more warps per SM)
+    const int part_b = ntile * 16 * kp * 8, tb_b = exact ? K * UP * UP * 8 : 0;
+    part = o; tb = o; o = align(o + (part_b > tb_b ? part_b : tb_b));
     gs = o; o = align(o + UP * UP * 8);
-    tb = o; o = align(o + (exact ? K * UP * UP * 8 : 0));
     xs = o; o = align(o + UP * 8);
     ps = o; o = align(o + 32 * 8);
     mfs = o; o = align(o + S * UP * 8);
