@@ -210,6 +210,45 @@ __device__ __forceinline__ void cheb_coef_warp(const float* hist, int K, double 
 // quotient, none inside the chain.  Interval [reg, 1.1 lambda] -> (c, d).
 template <int UP, int LDG = UP>
 __device__ __forceinline__ float2 cheb_interval(const float2* Gs, float reg, float2* xs, int lane) {
+  float lam = reg;
+  if constexpr (UP < 32) {
+    // U <= 16: the 32 / UP lane groups each take UP / (32 / UP) columns of
+    // the matvec for row i = lane mod UP and the partial sums are combined by
+    // xor shuffles (every group ends with the same bits), instead of UP lanes
+    // walking all UP columns while the rest of the warp idles
+    constexpr int GPW = 32 / UP, NC = UP / GPW;
+    const int part = lane / UP, i = lane - part * UP;
+    float2 xr = make_float2(1.f, 0.f);
+    if (part == 0) xs[i] = xr;
+    const float tr = group_sum<UP>(Gs[i * LDG + i].x + reg);
+    const float itr = tr > 0.f ? 1.f / tr : 1.f;
+    __syncwarp();
+    for (int it = 0; it <= 6; ++it) {
+      float2 y = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int jj = 0; jj < NC; ++jj) {
+        const int j = part * NC + jj;
+        cfma_conj(y, Gs[j * LDG + i], xs[j]);  // (A x)_i = sum_j conj(G[j][i]) x_j
+      }
+#pragma unroll
+      for (int o = UP; o < 32; o <<= 1) {
+        y.x += __shfl_xor_sync(0xffffffffu, y.x, o);
+        y.y += __shfl_xor_sync(0xffffffffu, y.y, o);
+      }
+      y.x = fmaf(reg, xr.x, y.x);
+      y.y = fmaf(reg, xr.y, y.y);
+      if (it == 6) {
+        const float nx = group_sum<UP>(cnorm(xr));
+        const float ray = group_sum<UP>(xr.x * y.x + xr.y * y.y);
+        if (nx > 0.f) lam = ray / nx;
+        break;
+      }
+      __syncwarp();
+      xr = cscale(itr, y);
+      if (part == 0) xs[i] = xr;
+      __syncwarp();
+    }
+  } else {
   constexpr int RU = UP < 32 ? 1 : UP / 32;
   float2 xr[RU];
   float tr = 0.f;
@@ -225,7 +264,6 @@ __device__ __forceinline__ float2 cheb_interval(const float2* Gs, float reg, flo
   tr = group_sum<32>(tr);
   const float itr = tr > 0.f ? 1.f / tr : 1.f;
   __syncwarp();
-  float lam = reg;
   for (int it = 0; it <= 6; ++it) {
     float2 y[RU];
     float nx = 0.f, ray = 0.f;
@@ -256,6 +294,7 @@ __device__ __forceinline__ float2 cheb_interval(const float2* Gs, float reg, flo
       if (i < UP) xs[i] = xr[m];
     }
     __syncwarp();
+  }
   }
   const float lo = reg;
   const float hi = fmaxf(1.1f * lam, 1.0001f * lo);
