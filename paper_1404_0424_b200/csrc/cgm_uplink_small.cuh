@@ -44,7 +44,8 @@ struct UpSmallSmem {
     ys = o; o = align(o + B * S * 8);
     // the Gram partials are dead once G is summed, before the Chebyshev
     // basis is formed: the two share one region (more warps per SM)
-    const int part_b = ntile * 16 * kp * 8, tb_b = exact ? K * UP * UP * 8 : 0;
+    // (+ the matched-filter partials of the one-vector case: UP users x kp parts)
+    const int part_b = (ntile * 16 + UP) * kp * 8, tb_b = exact ? K * UP * UP * 8 : 0;
     part = o; tb = o; o = align(o + (part_b > tb_b ? part_b : tb_b));
     gs = o; o = align(o + UP * UP * 8);
     xs = o; o = align(o + UP * 8);
@@ -120,6 +121,10 @@ __global__ void __launch_bounds__(32) uplink_small_kernel(const KernelParams p) 
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) a[r][c] = bb[r][c] = 0ull;
+      // one vector per subcarrier: the matched filter of the tile's row users
+      // rides on the same loads, conj(x) y = x.x (y.x, y.y) + x.y (y.y, -y.x)
+      // (the diagonal tiles' lanes keep it; the separate pass below is skipped)
+      unsigned long long mfa[4] = {0ull, 0ull, 0ull, 0ull};
       for (int b = b0; b < b1; ++b) {
         unsigned long long x[4], y[4];
 #pragma unroll
@@ -137,6 +142,20 @@ __global__ void __launch_bounds__(32) uplink_small_kernel(const KernelParams p) 
             ffma2(a[r][c], y[c], f2dup_lo(x[r]));
             ffma2(bb[r][c], y[c], f2dup_hi(x[r]));
           }
+        if (S == 1) {
+          const float2 yb = Ys[b];
+          const unsigned long long y1 = f2pack(yb.x, yb.y), y2 = f2pack(yb.y, -yb.x);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            ffma2(mfa[r], y1, f2dup_lo(x[r]));
+            ffma2(mfa[r], y2, f2dup_hi(x[r]));
+          }
+        }
+      }
+      if (S == 1 && rb == cb) {
+        float2* Pm = P + UG::NTILE * 16 * KP;  // [user][part]
+#pragma unroll
+        for (int r = 0; r < 4; ++r) Pm[(rb * 4 + r) * KP + item_part] = f2unpack(mfa[r]);
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r)
@@ -163,7 +182,15 @@ __global__ void __launch_bounds__(32) uplink_small_kernel(const KernelParams p) 
       }
     }
     // --------------------------------------------- 2. matched filters H^H y
-    {
+    if (S == 1) {  // fixed-order sums of the Gram loop's partials
+      if (lane < UP) {
+        const float2* pm = P + UG::NTILE * 16 * KP + lane * KP;
+        float2 m = pm[0];
+#pragma unroll
+        for (int k = 1; k < KP; ++k) m = cadd(m, pm[k]);
+        MFs[lane] = m;
+      }
+    } else {
       // (vector, user) pairs x antenna parts: 4 parts when the pairs fit in 8
       // lanes, 2 in 16, else 1; the parts are summed by xor shuffles
       const int nq = S * UP;
