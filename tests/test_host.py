@@ -88,3 +88,29 @@ def test_output_buffers_are_validated():
                            torch.zeros(1))
     with pytest.raises(ValueError):  # unknown name
         api._check_outputs({"nu": np.zeros((2, 3, 4), np.float32)}, shapes, False, like)
+
+
+def test_precoder_rotation_table_matches_its_bank_model():
+    """The start rotations compiled into precode_small_kernel (U = 16,
+    64-antenna chunks) are valid for their lanes' pair ranges and keep the
+    Gram loads' modelled wavefront count within 10 % of conflict-free, well
+    below the unsearched start (tools/ps_rotation.py holds the model)."""
+    import importlib.util
+    import os
+    import re
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("ps_rotation", os.path.join(root, "tools", "ps_rotation.py"))
+    psr = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(psr)
+    src = open(os.path.join(root, "paper_1404_0424_b200", "csrc", "cgm_precode_small.cuh")).read()
+    m = re.search(r"kRot\[32\] = \{([^}]*)\}", src)
+    assert m, "rotation table not found"
+    rot = [int(x) for x in m.group(1).replace("\n", " ").split(",")]
+    assert len(rot) == 32
+    for lane, L in enumerate(psr.lanes):
+        if L is not None:
+            assert 0 <= rot[lane] < L[3], (lane, rot[lane], L[3])
+    ideal = 88  # 11 steps x 4 quarter-warp phases x (x, y loads), one wavefront each
+    assert psr.cost(rot) <= 1.1 * ideal
+    assert psr.cost(psr.baseline()) > 1.5 * psr.cost(rot)

@@ -41,20 +41,26 @@ def cost(rot):
     return tot
 
 
-base = [(L[4] % L[3]) if L else 0 for L in lanes]
-print("tile mod range:", cost(base))
-best, bc = None, 10 ** 9
-for seed in range(12):  # hill climbing with restarts
-    random.seed(seed)
-    c = [random.randrange(L[3]) if L else 0 for L in lanes]
-    cc = cost(c)
-    for _ in range(15000):
-        d = c[:]
-        l = random.randrange(30)
-        d[l] = random.randrange(lanes[l][3])
-        dc = cost(d)
-        if dc <= cc:
-            c, cc = d, dc
-    if cc < bc:
-        best, bc = c, cc
-print("searched:", bc, best, "(88 = one wavefront per phase)")
+def baseline():
+    """The unsearched start: tile index mod range length."""
+    return [(L[4] % L[3]) if L else 0 for L in lanes]
+
+
+if __name__ == "__main__":
+    base = baseline()
+    print("tile mod range:", cost(base))
+    best, bc = None, 10 ** 9
+    for seed in range(12):  # hill climbing with restarts
+        random.seed(seed)
+        c = [random.randrange(L[3]) if L else 0 for L in lanes]
+        cc = cost(c)
+        for _ in range(15000):
+            d = c[:]
+            l = random.randrange(30)
+            d[l] = random.randrange(lanes[l][3])
+            dc = cost(d)
+            if dc <= cc:
+                c, cc = d, dc
+        if cc < bc:
+            best, bc = c, cc
+    print("searched:", bc, best, "(88 = one wavefront per phase)")
