@@ -28,7 +28,10 @@ template <int UP>
 struct UpSmallGeo {
   static constexpr int NB = UP / 4;
   static constexpr int NTILE = NB * (NB + 1) / 2;
-  static constexpr int KP = 32 / NTILE;  // antenna ranges per tile (10 / 3)
+  static constexpr int KP = 32 / NTILE;  // antenna parts per tile (10 / 3)
+  // Gram / matched-filter partials [part][tile entry | user], odd row stride:
+  // the lanes of the fixed-order sums read consecutive words
+  static constexpr int PSTR = (NTILE * 16 + UP) | 1;
   static constexpr int GL = UP;          // lanes per CG system
   static constexpr int GPW = 32 / GL;
 };
@@ -45,8 +48,16 @@ struct UpSmallSmem {
     // the Gram partials are dead once G is summed, before the Chebyshev
     // basis is formed: the two share one region (more warps per SM)
     // (+ the matched-filter partials of the one-vector case: UP users x kp parts)
-    const int part_b = (ntile * 16 + UP) * kp * 8, tb_b = exact ? K * UP * UP * 8 : 0;
-    part = o; tb = o; o = align(o + (part_b > tb_b ? part_b : tb_b));
+    const int part_b = ((ntile * 16 + UP) | 1) * kp * 8, tb_b = exact ? K * UP * UP * 8 : 0;
+    const int pt_b = part_b > tb_b ? part_b : tb_b;
+    // one vector per subcarrier: the matched filter rides on the Gram loop, so
+    // H is dead too once the loop ends -- the partials and the basis then sit
+    // on top of the H staging buffer (cfg1: 14.1 -> 10.3 KB per warp)
+    if (S == 1 && pt_b <= B * U * 8) {
+      part = hs; tb = hs;
+    } else {
+      part = o; tb = o; o = align(o + pt_b);
+    }
     gs = o; o = align(o + UP * UP * 8);
     xs = o; o = align(o + UP * 8);
     ps = o; o = align(o + 32 * 8);
@@ -59,10 +70,16 @@ struct UpSmallSmem {
   }
 };
 
+// U <= 8 with one vector per subcarrier needs ~10 KB of shared memory per warp
+// (cfg1): registers bound the warps per SM, 104 gives 19 instead of 16
+#ifndef CGM_US_MAXR8
+#define CGM_US_MAXR8 104
+#endif
+
 template <int UP, bool EXACT>
-__global__ void __launch_bounds__(32) uplink_small_kernel(const KernelParams p) {
+__global__ void __maxnreg__(UP == 8 ? CGM_US_MAXR8 : 128) uplink_small_kernel(const KernelParams p) {
   using UG = UpSmallGeo<UP>;
-  constexpr int GL = UG::GL, GPW = UG::GPW, KP = UG::KP;
+  constexpr int GL = UG::GL, GPW = UG::GPW, KP = UG::KP, PSTR = UG::PSTR;
   extern __shared__ __align__(128) unsigned char smem[];
   const int B = p.B, U = p.U, S = p.S, K = p.K;
   UpSmallSmem L;
@@ -91,7 +108,20 @@ __global__ void __launch_bounds__(32) uplink_small_kernel(const KernelParams p) 
   int rb = 0;
   while ((rb + 1) * (rb + 2) / 2 <= item_tile) ++rb;
   const int cb = item_tile - rb * (rb + 1) / 2;
-  const int b0 = (item_part * B) / KP, b1 = ((item_part + 1) * B) / KP;
+  // part p takes antennas p, p + KP, ...: at every step the parts read KP
+  // consecutive rows of H, and each rotates its 4 users by rot -- for U = 8
+  // (64-byte rows: two row phases x four rotations) and U = 16 (one phase)
+  // the half-warp's 8-byte loads then fall in distinct banks, where
+  // contiguous antenna ranges with the same user order were 3- to 4-way
+  // conflicts on every load of the loop.  The accumulators hold the rotated
+  // order; the partials are stored un-rotated.
+  const int rot = UP == 8 ? (item_part >> 1) & 3 : item_part & 3;
+  int xo[4], yo[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    xo[r] = rb * 4 + ((r + rot) & 3);
+    yo[r] = cb * 4 + ((r + rot) & 3);
+  }
 
   uint32_t phase = 0;
   for (long sc = blockIdx.x; sc < p.n_sc; sc += gridDim.x) {
@@ -113,23 +143,23 @@ __global__ void __launch_bounds__(32) uplink_small_kernel(const KernelParams p) 
       __syncwarp();
     }
     // ----------------------------------------------- 1. Gram partials (FFMA2)
+    // acc[r][c] = sum_b conj(H[b][u]) H[b][v], u = 4rb + r, v = 4cb + c:
+    // a += (y.x, y.y) * x.x, b += (y.x, y.y) * x.y; conj(x) y = (a.x + b.y, a.y - b.x)
+    unsigned long long a[4][4], bb[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) a[r][c] = bb[r][c] = 0ull;
+    // one vector per subcarrier: the matched filter of the tile's row users
+    // rides on the same loads, conj(x) y = x.x (y.x, y.y) + x.y (y.y, -y.x)
+    // (the diagonal tiles' lanes keep it; the separate pass below is skipped)
+    unsigned long long mfa[4] = {0ull, 0ull, 0ull, 0ull};
     if (gram_busy) {
-      // acc[r][c] = sum_b conj(H[b][u]) H[b][v], u = 4rb + r, v = 4cb + c:
-      // a += (y.x, y.y) * x.x, b += (y.x, y.y) * x.y; conj(x) y = (a.x + b.y, a.y - b.x)
-      unsigned long long a[4][4], bb[4][4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) a[r][c] = bb[r][c] = 0ull;
-      // one vector per subcarrier: the matched filter of the tile's row users
-      // rides on the same loads, conj(x) y = x.x (y.x, y.y) + x.y (y.y, -y.x)
-      // (the diagonal tiles' lanes keep it; the separate pass below is skipped)
-      unsigned long long mfa[4] = {0ull, 0ull, 0ull, 0ull};
-      for (int b = b0; b < b1; ++b) {
+      for (int b = item_part; b < B; b += KP) {
         unsigned long long x[4], y[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const int u = rb * 4 + r, v = cb * 4 + r;
+          const int u = xo[r], v = yo[r];
           const float2 xu = u < U ? Hs[b * U + u] : make_float2(0.f, 0.f);
           const float2 yv = v < U ? Hs[b * U + v] : make_float2(0.f, 0.f);
           x[r] = f2pack(xu.x, xu.y);
@@ -152,17 +182,21 @@ __global__ void __launch_bounds__(32) uplink_small_kernel(const KernelParams p) 
           }
         }
       }
+    }
+    __syncwarp();  // every lane's reads of H are done (the partials may overlay it)
+    if (gram_busy) {
       if (S == 1 && rb == cb) {
-        float2* Pm = P + UG::NTILE * 16 * KP;  // [user][part]
+        float2* Pm = P + item_part * PSTR + UG::NTILE * 16;  // [part][user]
 #pragma unroll
-        for (int r = 0; r < 4; ++r) Pm[(rb * 4 + r) * KP + item_part] = f2unpack(mfa[r]);
+        for (int r = 0; r < 4; ++r) Pm[xo[r]] = f2unpack(mfa[r]);
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const float2 A2 = f2unpack(a[r][c]), B2 = f2unpack(bb[r][c]);
-          P[((item_tile * 16) + r * 4 + c) * KP + item_part] = make_float2(A2.x + B2.y, A2.y - B2.x);
+          P[item_part * PSTR + (item_tile * 16) + (xo[r] & 3) * 4 + (yo[c] & 3)] =
+              make_float2(A2.x + B2.y, A2.y - B2.x);
         }
     }
     __syncwarp();
@@ -170,10 +204,10 @@ __global__ void __launch_bounds__(32) uplink_small_kernel(const KernelParams p) 
       const int u = e / UP, v = e - u * UP;
       if (v > u) continue;
       const int t = (u / 4) * (u / 4 + 1) / 2 + v / 4;
-      const float2* pp = P + (t * 16 + (u % 4) * 4 + (v % 4)) * KP;
+      const float2* pp = P + (t * 16 + (u % 4) * 4 + (v % 4));
       float2 g = pp[0];
 #pragma unroll
-      for (int k = 1; k < KP; ++k) g = cadd(g, pp[k]);
+      for (int k = 1; k < KP; ++k) g = cadd(g, pp[k * PSTR]);
       if (u == v) {
         Gs[u * UP + u] = make_float2(g.x, 0.f);
       } else {
@@ -184,10 +218,10 @@ __global__ void __launch_bounds__(32) uplink_small_kernel(const KernelParams p) 
     // --------------------------------------------- 2. matched filters H^H y
     if (S == 1) {  // fixed-order sums of the Gram loop's partials
       if (lane < UP) {
-        const float2* pm = P + UG::NTILE * 16 * KP + lane * KP;
+        const float2* pm = P + UG::NTILE * 16 + lane;
         float2 m = pm[0];
 #pragma unroll
-        for (int k = 1; k < KP; ++k) m = cadd(m, pm[k]);
+        for (int k = 1; k < KP; ++k) m = cadd(m, pm[k * PSTR]);
         MFs[lane] = m;
       }
     } else {
@@ -355,12 +389,17 @@ __global__ void __launch_bounds__(32) uplink_small_kernel(const KernelParams p) 
         cheb_coef_warp(hist + s * K * 2, K, cc, dd, p.rho_inv_u, cl, cl + (K + 2));
       }
       __syncwarp();
-      for (int e = lane; e < S * UP; e += 32) {  // (vector, row) per lane
-        const int s = e / UP, i = e - s * UP;
+      // one vector per subcarrier: the 32 / UP lane groups split the columns
+      // of row i = lane mod UP (xor-shuffle sums, every group ends with the
+      // same bits); otherwise a (vector, row) per lane walks all UP columns
+      const int xparts = S == 1 ? GPW : 1, xnc = UP / xparts;
+      for (int e = lane; e < S * UP * xparts; e += 32) {
+        const int xpart = S == 1 ? e / UP : 0;
+        const int s = S == 1 ? 0 : e / UP, i = e - (S == 1 ? xpart : s) * UP;
         const float* cl = coef + s * 2 * (K + 2);
         const float* cbq = cl + (K + 2);
         float ib2 = 0.f, ibl = 0.f, mu_i = 0.f;
-        for (int j = 0; j < UP; ++j) {
+        for (int j = xpart * xnc; j < (xpart + 1) * xnc; ++j) {
           float2 Bv = make_float2(i == j ? cbq[0] : 0.f, 0.f);
           float2 Lv = make_float2(i == j ? cl[0] : 0.f, 0.f);
           for (int m = 1; m <= K; ++m) {
@@ -371,6 +410,15 @@ __global__ void __launch_bounds__(32) uplink_small_kernel(const KernelParams p) 
           if (j == i) mu_i = Bv.x;
           else ib2 += cnorm(Bv);
           ibl += Bv.x * Lv.x + Bv.y * Lv.y;  // Re(B_ij conj(L_ij))
+        }
+        if (S == 1) {  // all 32 lanes are here (UP * GPW = 32)
+#pragma unroll
+          for (int o = UP; o < 32; o <<= 1) {
+            ib2 += __shfl_xor_sync(0xffffffffu, ib2, o);
+            ibl += __shfl_xor_sync(0xffffffffu, ibl, o);
+            mu_i += __shfl_xor_sync(0xffffffffu, mu_i, o);
+          }
+          if (xpart != 0) continue;
         }
         if (i >= U) continue;
         const float nu2 = ib2 * p.es + ibl * p.n0;
@@ -386,6 +434,9 @@ __global__ void __launch_bounds__(32) uplink_small_kernel(const KernelParams p) 
         if (p.status && i == 0) p.status[sc * S + s] = ok ? 0 : 1;
       }
     }
+    // generic-proxy writes over the staging buffer (overlaid partials / basis)
+    // are ordered before the next subcarrier's bulk copy into it
+    if (tma) fence_proxy_async();
     __syncwarp();  // shared buffers reused by the next subcarrier
   }
 }
