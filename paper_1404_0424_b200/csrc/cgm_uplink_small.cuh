@@ -71,9 +71,10 @@ struct UpSmallSmem {
 };
 
 // U <= 8 with one vector per subcarrier needs ~10 KB of shared memory per warp
-// (cfg1): registers bound the warps per SM, 104 gives 19 instead of 16
+// (cfg1): registers bound the warps per SM -- 120 (17 warps) holds the Gram
+// accumulators without spills; 104 (19 warps) spills in the loop and is 40 % slower
 #ifndef CGM_US_MAXR8
-#define CGM_US_MAXR8 104
+#define CGM_US_MAXR8 120
 #endif
 
 template <int UP, bool EXACT>
@@ -109,19 +110,17 @@ __global__ void __maxnreg__(UP == 8 ? CGM_US_MAXR8 : 128) uplink_small_kernel(co
   while ((rb + 1) * (rb + 2) / 2 <= item_tile) ++rb;
   const int cb = item_tile - rb * (rb + 1) / 2;
   // part p takes antennas p, p + KP, ...: at every step the parts read KP
-  // consecutive rows of H, and each rotates its 4 users by rot -- for U = 8
-  // (64-byte rows: two row phases x four rotations) and U = 16 (one phase)
-  // the half-warp's 8-byte loads then fall in distinct banks, where
-  // contiguous antenna ranges with the same user order were 3- to 4-way
-  // conflicts on every load of the loop.  The accumulators hold the rotated
-  // order; the partials are stored un-rotated.
-  const int rot = UP == 8 ? (item_part >> 1) & 3 : item_part & 3;
-  int xo[4], yo[4];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    xo[r] = rb * 4 + ((r + rot) & 3);
-    yo[r] = cb * 4 + ((r + rot) & 3);
-  }
+  // consecutive rows of H, and each takes its 4 users in the order
+  // (0 1 2 3) or (2 3 0 1) (rot2) -- for U = 8 (64-byte rows: two row phases
+  // x two orders) and U = 16 (one phase) the 16-byte loads of a quarter
+  // warp then fall in distinct banks, where contiguous antenna ranges with
+  // the same user order were 3- to 4-way conflicts on every load of the
+  // loop.  The accumulators hold the rotated order; the partials are stored
+  // un-rotated.
+  // (calls with U < UP keep the plain order: their row stride is not the
+  // one the rotation is made for)
+  const int rot2 = p.U != UP ? 0 : UP == 8 ? (item_part >> 1) & 1 : item_part & 1;
+  const int unrot = rot2 * 10;  // (r, c) -> (r ^ 2, c ^ 2) on the index 4 r + c
 
   uint32_t phase = 0;
   for (long sc = blockIdx.x; sc < p.n_sc; sc += gridDim.x) {
@@ -154,33 +153,56 @@ __global__ void __maxnreg__(UP == 8 ? CGM_US_MAXR8 : 128) uplink_small_kernel(co
     // rides on the same loads, conj(x) y = x.x (y.x, y.y) + x.y (y.y, -y.x)
     // (the diagonal tiles' lanes keep it; the separate pass below is skipped)
     unsigned long long mfa[4] = {0ull, 0ull, 0ull, 0ull};
-    if (gram_busy) {
+    // one antenna row into the accumulators
+    auto gram_mac = [&](const unsigned long long (&x)[4], const unsigned long long (&y)[4],
+                        const float2 yb) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          ffma2(a[r][c], y[c], f2dup_lo(x[r]));
+          ffma2(bb[r][c], y[c], f2dup_hi(x[r]));
+        }
+      if (S == 1) {
+        const unsigned long long y1 = f2pack(yb.x, yb.y), y2 = f2pack(yb.y, -yb.x);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          ffma2(mfa[r], y1, f2dup_lo(x[r]));
+          ffma2(mfa[r], y2, f2dup_hi(x[r]));
+        }
+      }
+    };
+    if (gram_busy && U == UP) {
+      // full user count: constant row stride, the users in pairs by 16-byte
+      // loads at [lane pointer + immediate], no bounds selects
+      constexpr int RS = KP * UP / 2;  // ulonglong2 per step
+      const ulonglong2* hx0 = reinterpret_cast<const ulonglong2*>(Hs + item_part * UP + rb * 4) + rot2;
+      const ulonglong2* hx1 = hx0 + 1 - 2 * rot2;
+      const ulonglong2* hy0 = reinterpret_cast<const ulonglong2*>(Hs + item_part * UP + cb * 4) + rot2;
+      const ulonglong2* hy1 = hy0 + 1 - 2 * rot2;
+      const float2* yp = Ys + item_part * S;
+      const int nst = (B - item_part + KP - 1) / KP;
+#pragma unroll 1
+      for (int t = 0; t < nst; ++t) {
+        const ulonglong2 X0 = *hx0, X1 = *hx1, Y0 = *hy0, Y1 = *hy1;
+        const unsigned long long x[4] = {X0.x, X0.y, X1.x, X1.y};
+        const unsigned long long y[4] = {Y0.x, Y0.y, Y1.x, Y1.y};
+        gram_mac(x, y, S == 1 ? *yp : make_float2(0.f, 0.f));
+        hx0 += RS; hx1 += RS; hy0 += RS; hy1 += RS;
+        yp += KP * S;
+      }
+    } else if (gram_busy) {
       for (int b = item_part; b < B; b += KP) {
         unsigned long long x[4], y[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const int u = xo[r], v = yo[r];
+          const int u = rb * 4 + r, v = cb * 4 + r;
           const float2 xu = u < U ? Hs[b * U + u] : make_float2(0.f, 0.f);
           const float2 yv = v < U ? Hs[b * U + v] : make_float2(0.f, 0.f);
           x[r] = f2pack(xu.x, xu.y);
           y[r] = f2pack(yv.x, yv.y);
         }
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            ffma2(a[r][c], y[c], f2dup_lo(x[r]));
-            ffma2(bb[r][c], y[c], f2dup_hi(x[r]));
-          }
-        if (S == 1) {
-          const float2 yb = Ys[b];
-          const unsigned long long y1 = f2pack(yb.x, yb.y), y2 = f2pack(yb.y, -yb.x);
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            ffma2(mfa[r], y1, f2dup_lo(x[r]));
-            ffma2(mfa[r], y2, f2dup_hi(x[r]));
-          }
-        }
+        gram_mac(x, y, S == 1 ? Ys[b] : make_float2(0.f, 0.f));
       }
     }
     __syncwarp();  // every lane's reads of H are done (the partials may overlay it)
@@ -188,14 +210,14 @@ __global__ void __maxnreg__(UP == 8 ? CGM_US_MAXR8 : 128) uplink_small_kernel(co
       if (S == 1 && rb == cb) {
         float2* Pm = P + item_part * PSTR + UG::NTILE * 16;  // [part][user]
 #pragma unroll
-        for (int r = 0; r < 4; ++r) Pm[xo[r]] = f2unpack(mfa[r]);
+        for (int r = 0; r < 4; ++r) Pm[rb * 4 + (r ^ (2 * rot2))] = f2unpack(mfa[r]);
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const float2 A2 = f2unpack(a[r][c]), B2 = f2unpack(bb[r][c]);
-          P[item_part * PSTR + (item_tile * 16) + (xo[r] & 3) * 4 + (yo[c] & 3)] =
+          P[item_part * PSTR + (item_tile * 16) + ((r * 4 + c) ^ unrot)] =
               make_float2(A2.x + B2.y, A2.y - B2.x);
         }
     }
