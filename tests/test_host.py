@@ -114,3 +114,26 @@ def test_precoder_rotation_table_matches_its_bank_model():
     ideal = 88  # 11 steps x 4 quarter-warp phases x (x, y loads), one wavefront each
     assert psr.cost(rot) <= 1.1 * ideal
     assert psr.cost(psr.baseline()) > 1.5 * psr.cost(rot)
+
+
+def test_uplink_small_gram_loads_are_conflict_free_in_the_bank_model():
+    """uplink_small_kernel's full-U Gram loop (cfg1, U = 8; also U = 16):
+    strided antenna parts with the pair order rot2 the kernel compiles in give
+    one wavefront per quarter-warp LDS.128, where the unrotated order needs up
+    to two (tools/us_rotation.py holds the model; rot2 read from the source)."""
+    import importlib.util
+    import os
+    import re
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("us_rotation", os.path.join(root, "tools", "us_rotation.py"))
+    usr = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(usr)
+    src = open(os.path.join(root, "paper_1404_0424_b200", "csrc", "cgm_uplink_small.cuh")).read()
+    # the model's rot2_of must be the kernel's expression
+    assert re.search(r"rot2 = p\.U != UP \? 0 : UP == 8 \? \(item_part >> 1\) & 1 : item_part & 1;", src)
+    for UP in (8, 16):
+        worst, mean = usr.wavefronts(UP)
+        assert worst == 1 and mean == 1.0, (UP, worst, mean)
+        worst0, mean0 = usr.wavefronts(UP, rotate=False)
+        assert worst0 == 2 and mean0 > 1.2, (UP, worst0, mean0)
