@@ -71,10 +71,16 @@ struct UpSmallSmem {
 };
 
 // U <= 8 with one vector per subcarrier needs ~10 KB of shared memory per warp
-// (cfg1): registers bound the warps per SM -- 120 (17 warps) holds the Gram
-// accumulators without spills; 104 (19 warps) spills in the loop and is 40 % slower
+// (cfg1), so registers bound the warps per SM.  Measured on 64 frames of cfg1:
+// 128 registers (16 warps per SM) 0.305 ms, 120 (still 16 warps: warp
+// allocation granularity) 0.322 ms, 104 (19 warps, spills in the Gram loop)
+// 0.461 ms; the Gram loop unrolled by 2 at 128 registers 0.312 ms.
+#ifndef CGM_US_UNR
+#define CGM_US_UNR 1
+#endif
+constexpr int kUsUnroll = CGM_US_UNR;
 #ifndef CGM_US_MAXR8
-#define CGM_US_MAXR8 120
+#define CGM_US_MAXR8 128
 #endif
 
 template <int UP, bool EXACT>
@@ -182,7 +188,7 @@ __global__ void __maxnreg__(UP == 8 ? CGM_US_MAXR8 : 128) uplink_small_kernel(co
       const ulonglong2* hy1 = hy0 + 1 - 2 * rot2;
       const float2* yp = Ys + item_part * S;
       const int nst = (B - item_part + KP - 1) / KP;
-#pragma unroll 1
+#pragma unroll(kUsUnroll)
       for (int t = 0; t < nst; ++t) {
         const ulonglong2 X0 = *hx0, X1 = *hx1, Y0 = *hy0, Y1 = *hy1;
         const unsigned long long x[4] = {X0.x, X0.y, X1.x, X1.y};
