@@ -65,7 +65,7 @@ struct PrecodeSmallSmem {
 // MQ = chunks per antenna pass held in registers (B <= 32 MQ): 4 for B <= 128
 // (16 warps per SM), 16 up to B = 512.
 template <int UP, int MQ>
-__global__ void __launch_bounds__(32, MQ <= 4 ? 15 : 10) precode_small_kernel(const KernelParams p) {
+__global__ void __launch_bounds__(32, MQ <= 4 ? 11 : 10) precode_small_kernel(const KernelParams p) {
   using PG = PrecodeSmallGeo<UP>;
   constexpr int GL = PG::GL, GPW = PG::GPW, KP = PG::KP, CB = PG::CB;
   constexpr int LDH = PrecodeSmallSmem::LDH, LDP = PrecodeSmallSmem::LDP;
