@@ -207,6 +207,10 @@ __host__ __device__ inline bool supported(int U, int B, int S, int use_tma) {
 // split.  NSP == 0 (unified): warps [0, NEP) split subcarrier i, then run
 // the epilogue of subcarrier i-1 while the tensor core works on i.  Then
 // the TMA producer warp and the MMA warp.  k1_pair carries the staging depth.
+// 18 warps = 5 on two of the SM's four sub-partitions, each with a 16 K
+// register file: 96 registers per thread is the most a CTA of this size can
+// have (__maxnreg__(112) compiles without the specialised instantiation's
+// 72 / 120 bytes of spills but cannot launch).
 template <int NEP, int NSP, int RING = 2>
 __global__ void __launch_bounds__(32 * (NEP + NSP + 2), 3 - RING) channel_tc_kernel(const KernelParams p) {
   using namespace tc;
