@@ -64,8 +64,11 @@ struct PrecodeSmallSmem {
 
 // MQ = chunks per antenna pass held in registers (B <= 32 MQ): 4 for B <= 128
 // (16 warps per SM), 16 up to B = 512.
+// Launch bound = the warps per SM that shared memory allows: 11 for U = 16
+// (19.2 KB per warp; a bound of 15 capped the kernel at 128 registers with
+// spills, 11 gives 167 and none at the same occupancy), 15 for U <= 8.
 template <int UP, int MQ>
-__global__ void __launch_bounds__(32, MQ <= 4 ? 11 : 10) precode_small_kernel(const KernelParams p) {
+__global__ void __launch_bounds__(32, MQ > 4 ? 10 : UP == 16 ? 11 : 15) precode_small_kernel(const KernelParams p) {
   using PG = PrecodeSmallGeo<UP>;
   constexpr int GL = PG::GL, GPW = PG::GPW, KP = PG::KP, CB = PG::CB;
   constexpr int LDH = PrecodeSmallSmem::LDH, LDP = PrecodeSmallSmem::LDP;
