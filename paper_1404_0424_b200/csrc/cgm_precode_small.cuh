@@ -118,6 +118,15 @@ __global__ void __launch_bounds__(32, MQ > 4 ? 10 : UP == 16 ? 11 : 15) precode_
       if (2 * cp_p < nb) {
         uint32_t dst = row0 + (nj & 1u) * HB;
         const float2* src = nj_row + c0;
+        if (RPI == 1 && B == 128 && U == UP) {
+          // cfg3's shape: constant row strides, every copy is
+          // [pointer + immediate] (no per-row address arithmetic)
+#pragma unroll
+          for (int u = 0; u < UP; ++u)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + u * (LDH * 8)),
+                         "l"(src + u * 128)
+                         : "memory");
+        } else
 #pragma unroll 4
         for (int u = cp_r; u < U; u += RPI) {
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
